@@ -1,0 +1,180 @@
+/*
+ * eikonal_b200.h -- C-ABI of the B200-native Eikonal hot path.
+ *
+ * Drop-in boundary for the reference's solver interface
+ * (/root/reference/proj/include/eikonal/*.hpp).  Each entry point replaces one
+ * reference function; the reference-side binding a maintainer adds is shown
+ * in INTEGRATION.md.  Plain C: no exceptions, no torch types, plain pointers
+ * and sizes.  Errors come back as status codes plus a thread-local message
+ * (eik_last_error), mapping the reference's exception types:
+ *   EIK_ERR_CONFIG  <- eikonal::ConfigError          (grid.hpp:16-19)
+ *   EIK_ERR_BUDGET  <- std::runtime_error "heap-cell removal budget exceeded"
+ *                                                     (heap_cell.cpp:276-277)
+ *   EIK_ERR_DOMAIN  <- std::domain_error / invalid_argument (grid.cpp:32-35)
+ *
+ * Layout conventions (grid.hpp:36-58): node (i,j) sits at (x0+i*h, y0+j*h),
+ * linear index j*m+i (row-major, rows are constant j).  Values are fp64;
+ * +inf marks unreached nodes.  Indices are 64-bit on this side of the ABI.
+ */
+#ifndef EIKONAL_B200_H
+#define EIKONAL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EIK_ABI_VERSION 1
+
+/* Solver selection; numbering mirrors eikonal::Method (experiment.hpp:11). */
+enum eik_method {
+  EIK_FMM = 0,  /* fmm_solve   classic_solvers.hpp:18 */
+  EIK_FSM = 1,  /* fsm_solve   classic_solvers.hpp:33 */
+  EIK_LSM = 2,  /* lsm_solve   classic_solvers.hpp:38 (not on the GPU path) */
+  EIK_HCM = 3,  /* hcm_solve   heap_cell.hpp:36 */
+  EIK_FHCM = 4, /* fhcm_solve  heap_cell.hpp:41 */
+  EIK_FMSM = 5  /* fmsm_solve  fmsm.hpp:36 */
+};
+
+enum eik_status {
+  EIK_OK = 0,
+  EIK_ERR_CONFIG = 1,   /* bad problem / decomposition (ConfigError) */
+  EIK_ERR_CUDA = 2,     /* CUDA runtime failure or no usable device */
+  EIK_ERR_BUDGET = 3,   /* iteration / removal budget exceeded */
+  EIK_ERR_NOT_IMPL = 4, /* method not implemented on the device path */
+  EIK_ERR_DOMAIN = 5    /* argument outside the domain (domain_error) */
+};
+
+/* Grid (grid.hpp:36-58). */
+typedef struct eik_grid {
+  int64_t m, n; /* node counts in x and y, >= 2 */
+  double h;     /* spacing > 0 */
+  double x0, y0;
+} eik_grid;
+
+/* Problem (grid.hpp:69-80) with the speed function sampled on the host:
+ * speed[j*m+i] == problem.speed(x0+i*h, y0+j*h) bit for bit
+ * (Problem::speed_at, grid.hpp:77-79). */
+typedef struct eik_problem {
+  eik_grid grid;
+  const double* speed;        /* F > 0 at every node, m*n */
+  int32_t speed_on_device;    /* 1: `speed` is a device pointer (cuda:0) */
+  const int64_t* exit_nodes;  /* strictly ascending linear indices */
+  const double* exit_cost;    /* parallel to exit_nodes, finite */
+  int64_t n_exit;             /* >= 1 */
+  /* Pre-snap point-source positions and costs (grid.hpp:76-77), only read by
+   * FMSM's coarse discretisation (fmsm.cpp:40-61).  May be empty. */
+  const double* exit_points_xy; /* 2*n_exit_points, interleaved x,y */
+  const double* exit_point_cost;
+  int64_t n_exit_points;
+} eik_problem;
+
+/* Cell decomposition (cells.hpp:27-75, built exactly like build_cells,
+ * cells.cpp:32-47) plus the host-sampled speed tables the two-scale methods
+ * evaluate off-grid.  Build the tables with eik_cell_probe_points /
+ * eik_cell_centers and the problem's own speed function. */
+typedef struct eik_cells {
+  int32_t cells_x, cells_y;
+  /* HCM/FHCM: F at the clamped border probe point of every border node
+   * (heap_cell.cpp:195-205).  west/east: cells_x*n entries, index cx*n+j;
+   * south/north: cells_y*m entries, index cy*m+i. */
+  const double* probe_speed_w;
+  const double* probe_speed_e;
+  const double* probe_speed_s;
+  const double* probe_speed_n;
+  /* FMSM: F at the geometric centre of every cell (cells.hpp:44-48,
+   * fmsm.cpp:18-30), cells_x*cells_y entries. */
+  const double* center_speed;
+} eik_cells;
+
+/* SolverOutput + HybridStats (grid.hpp:132-149). */
+typedef struct eik_output {
+  double* u;            /* caller-allocated m*n */
+  int32_t u_on_device;  /* 1: `u` is a device pointer (cuda:0) */
+  int64_t sweeps;
+  int64_t node_updates;
+  int64_t heap_removals;
+  int64_t cell_removals, cell_sweeps, mon_checks, mon_single;
+  double avhr, avs, mon_pct;
+  double device_ms;     /* CUDA-event time of the device solve proper */
+  int64_t kernel_launches; /* kernels this call launched (evidence) */
+} eik_output;
+
+/* One solve.  `cells` may be NULL for FMM/FSM.  Thread-safe: each call owns
+ * its device buffers and stream. */
+int eik_solve(const eik_problem* p, const eik_cells* cells, int32_t method,
+              eik_output* out);
+
+/* Resident plan: uploads the problem once and keeps device work buffers, so
+ * repeated solves (benchmarks) time the device path alone.  The plan copies
+ * every input; the caller's arrays may be freed after eik_plan_create. */
+typedef struct eik_plan eik_plan;
+eik_plan* eik_plan_create(const eik_problem* p, const eik_cells* cells,
+                          int32_t method);
+/* Solve into out->u (host or device per out->u_on_device; NULL u keeps the
+ * result resident in the plan).  */
+int eik_plan_run(eik_plan* plan, eik_output* out);
+/* Device pointer to the plan's resident value field (m*n fp64). */
+const double* eik_plan_values(const eik_plan* plan);
+void eik_plan_destroy(eik_plan* plan);
+
+/* Thread-local description / status code of the last failure on this
+ * thread (eik_plan_create returns NULL and sets both). */
+const char* eik_last_error(void);
+int eik_last_status(void);
+int eik_abi_version(void);
+/* Number of visible CUDA devices (0 on a CPU-only host; never fails). */
+int eik_device_count(void);
+
+/* ---- host-side geometry helpers (bit-exact restatements) ------------- */
+
+/* Clamped probe points of heap_cell.cpp:195-205 for every border node of
+ * every cell column/row; side 0=W,1=E,2=S,3=N.  `xy` receives 2*count
+ * doubles (x,y interleaved) where count = cells_x*n (W/E) or cells_y*m
+ * (S/N).  Returns count, or -1 on bad arguments. */
+int64_t eik_cell_probe_points(const eik_grid* g, int32_t cells_x,
+                              int32_t cells_y, int32_t side, double* xy);
+/* Cell centres (cells.hpp:44-48), 2*cells_x*cells_y doubles. */
+int64_t eik_cell_centers(const eik_grid* g, int32_t cells_x, int32_t cells_y,
+                         double* xy);
+
+/* ---- native speed fields (BASELINE synthetic inputs) ------------------ */
+
+enum eik_field_kind {
+  EIK_FIELD_CONSTANT = 0,  /* F = value */
+  EIK_FIELD_SINUSOID = 1,  /* 1 + amp*sin(freq*pi*x)*sin(freq*pi*y), speed_fields.cpp:27-29 */
+  EIK_FIELD_CHECKER = 2,   /* k x k unit-square checkerboard, speed_fields.cpp:23-26 */
+  EIK_FIELD_COMB = 3,      /* comb maze, speed_fields.cpp:30-41 */
+  EIK_FIELD_BLOCKS = 4,    /* nb x nb piecewise-constant blocks (config 3) */
+  EIK_FIELD_NODEMASK = 5,  /* nearest-node wall mask (config 4 maze) */
+  EIK_FIELD_SINSUM = 6     /* 1 + 0.5*S/K, K random-phase sinusoids (config 5) */
+};
+
+typedef struct eik_field {
+  int32_t kind;
+  double value;                           /* CONSTANT */
+  double amp; int32_t freq;               /* SINUSOID */
+  int32_t checkers; double slow, fast;    /* CHECKER (slow on even index sum) */
+  int32_t n_barriers;                     /* COMB */
+  double barrier_speed, barrier_width, gap_fraction;
+  int32_t nb; double bx0, by0, bscale;    /* BLOCKS: b = clamp(floor((x-bx0)*bscale),0,nb-1) */
+  const double* block_speed;              /*   nb*nb, index by*nb+bx */
+  eik_grid mask_grid;                     /* NODEMASK: lattice of the mask */
+  const uint8_t* mask;                    /*   1 = wall (speed `slow`), else `fast` */
+  int32_t K;                              /* SINSUM terms */
+  const double* kp; const double* kq; const double* kphi;
+} eik_field;
+
+double eik_field_eval(const eik_field* f, double x, double y);
+/* out[j*m+i] = eik_field_eval(f, x0+i*h, y0+j*h) bit for bit. */
+int eik_field_sample(const eik_field* f, const eik_grid* g, double* out,
+                     int32_t threads);
+int eik_field_eval_points(const eik_field* f, const double* xy, int64_t count,
+                          double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EIKONAL_B200_H */

@@ -1,0 +1,196 @@
+"""ORACLE -- TEST INFRASTRUCTURE ONLY.
+
+ctypes access to the checkers: oracle/liboracle.so (C restatement) and
+oracle/_ref/libeikref.so (the unmodified reference, built from
+/root/reference by oracle/Makefile).  Only tests/, __graft_entry__.smoke()
+and bench.py's cpu_baseline / --impl reference leg may import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from paper_1110_6220_b200 import _native as N
+from paper_1110_6220_b200.problem import CellDecomposition, CellTables, Problem, SpeedField
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libeikref.so")
+_dp = C.POINTER(C.c_double)
+_i64p = C.POINTER(C.c_int64)
+
+
+class orc_problem(C.Structure):
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("h", C.c_double), ("x0", C.c_double),
+                ("y0", C.c_double), ("F", _dp), ("exit_nodes", _i64p), ("exit_cost", _dp),
+                ("n_exit", C.c_int64), ("exit_points_xy", _dp), ("exit_point_cost", _dp),
+                ("n_exit_points", C.c_int64)]
+
+
+class orc_cells(C.Structure):
+    _fields_ = [("cells_x", C.c_int32), ("cells_y", C.c_int32), ("probe_w", _dp),
+                ("probe_e", _dp), ("probe_s", _dp), ("probe_n", _dp), ("center_F", _dp)]
+
+
+class orc_stats(C.Structure):
+    _fields_ = [("sweeps", C.c_int64), ("node_updates", C.c_int64),
+                ("heap_removals", C.c_int64), ("mon_checks", C.c_int64),
+                ("mon_single", C.c_int64)]
+
+
+class ref_stats(C.Structure):
+    _fields_ = [("sweeps", C.c_int64), ("node_updates", C.c_int64),
+                ("heap_removals", C.c_int64), ("cell_removals", C.c_int64),
+                ("cell_sweeps", C.c_int64), ("mon_checks", C.c_int64),
+                ("mon_single", C.c_int64), ("avhr", C.c_double), ("avs", C.c_double),
+                ("mon_pct", C.c_double), ("elapsed_ms", C.c_double)]
+
+
+@dataclass
+class Result:
+    u: np.ndarray
+    sweeps: int
+    node_updates: int
+    heap_removals: int
+    mon_checks: int = 0
+    mon_single: int = 0
+    elapsed_ms: float = 0.0
+
+
+def _load_oracle():
+    lib = C.CDLL(ORACLE_SO)
+    for nm in ("orc_fmm", "orc_fsm", "orc_lsm"):
+        getattr(lib, nm).argtypes = [C.POINTER(orc_problem), _dp, C.POINTER(orc_stats)]
+        getattr(lib, nm).restype = C.c_int
+    for nm in ("orc_hcm", "orc_fhcm", "orc_fmsm"):
+        getattr(lib, nm).argtypes = [C.POINTER(orc_problem), C.POINTER(orc_cells), _dp,
+                                     C.POINTER(orc_stats)]
+        getattr(lib, nm).restype = C.c_int
+    lib.orc_quadrant_update.argtypes = [C.c_double] * 4
+    lib.orc_quadrant_update.restype = C.c_double
+    lib.orc_node_update.argtypes = [_dp, C.c_double, C.c_double]
+    lib.orc_node_update.restype = C.c_double
+    lib.orc_directional_update.argtypes = [_dp, C.c_int, C.c_double, C.c_double]
+    lib.orc_directional_update.restype = C.c_double
+    return lib
+
+
+def _load_ref():
+    if not os.path.exists(REF_SO):
+        return None
+    lib = C.CDLL(REF_SO)
+    lib.ref_solve.argtypes = [C.c_int, C.POINTER(N.eik_grid), C.POINTER(N.eik_field), _i64p, _dp,
+                              C.c_int64, _dp, _dp, C.c_int64, C.c_int, C.c_int, _dp,
+                              C.POINTER(ref_stats)]
+    lib.ref_solve.restype = C.c_int
+    lib.ref_last_error.restype = C.c_char_p
+    lib.ref_quadrant_update.argtypes = [C.c_double] * 4
+    lib.ref_quadrant_update.restype = C.c_double
+    lib.ref_node_update.argtypes = [_dp, C.c_double, C.c_double]
+    lib.ref_node_update.restype = C.c_double
+    lib.ref_directional_update.argtypes = [_dp, C.c_int, C.c_double, C.c_double]
+    lib.ref_directional_update.restype = C.c_double
+    lib.ref_snap.argtypes = [C.POINTER(N.eik_grid), C.c_double, C.c_double, _i64p, _i64p]
+    lib.ref_snap.restype = C.c_int
+    lib.ref_metrics.argtypes = [C.POINTER(N.eik_grid), C.POINTER(N.eik_field), _i64p, _dp,
+                                C.c_int64, C.c_int, _dp, _dp, _dp]
+    lib.ref_metrics.restype = C.c_int
+    lib.ref_named_speed.argtypes = [C.c_char_p, C.c_double, C.c_double]
+    lib.ref_named_speed.restype = C.c_double
+    return lib
+
+
+olib = _load_oracle()
+rlib = _load_ref()
+
+
+def have_ref() -> bool:
+    return rlib is not None
+
+
+def _orc_problem(p: Problem):
+    F = p.sampled_speed()
+    en = np.ascontiguousarray(p.exit_nodes, dtype=np.int64)
+    ec = np.ascontiguousarray(p.exit_cost, dtype=np.float64)
+    pts = np.ascontiguousarray(p.exit_points, dtype=np.float64).reshape(-1)
+    pc = np.ascontiguousarray(p.exit_point_cost, dtype=np.float64)
+    g = p.grid
+    op = orc_problem(g.m, g.n, g.h, g.x0, g.y0, F.ctypes.data_as(_dp), en.ctypes.data_as(_i64p),
+                     ec.ctypes.data_as(_dp), len(en),
+                     pts.ctypes.data_as(_dp) if pts.size else _dp(),
+                     pc.ctypes.data_as(_dp) if pc.size else _dp(), len(pc))
+    return op, (F, en, ec, pts, pc)
+
+
+def oracle_solve(p: Problem, method: str, cells: CellDecomposition = None,
+                 tables: CellTables = None) -> Result:
+    """C restatement (oracle/eik_oracle.c)."""
+    from paper_1110_6220_b200.problem import cell_tables
+    op, keep = _orc_problem(p)
+    u = np.empty(p.grid.size(), dtype=np.float64)
+    st = orc_stats()
+    if method in ("fmm", "fsm", "lsm"):
+        rc = getattr(olib, "orc_" + method)(C.byref(op), u.ctypes.data_as(_dp), C.byref(st))
+    else:
+        if tables is None:
+            tables = cell_tables(p, cells)
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                (tables.probe_w, tables.probe_e, tables.probe_s, tables.probe_n, tables.center)]
+        oc = orc_cells(cells.cells_x, cells.cells_y, *[a.ctypes.data_as(_dp) for a in arrs])
+        rc = getattr(olib, "orc_" + method)(C.byref(op), C.byref(oc), u.ctypes.data_as(_dp),
+                                            C.byref(st))
+    if rc == 1:
+        raise N.ConfigError("oracle: bad configuration")
+    if rc == 3:
+        raise N.BudgetError("heap-cell removal budget exceeded")
+    return Result(u, st.sweeps, st.node_updates, st.heap_removals, st.mon_checks, st.mon_single)
+
+
+_REF_METHOD = {"fmm": 0, "fsm": 1, "lsm": 2, "hcm": 3, "fhcm": 4, "fmsm": 5}
+
+
+def ref_solve(p: Problem, method: str, cells_x: int = 0, cells_y: int = 0) -> Result:
+    """The UNMODIFIED reference (oracle/_ref) with an on-demand SpeedFn."""
+    if rlib is None:
+        raise RuntimeError("oracle/_ref/libeikref.so not built")
+    if not isinstance(p.speed, SpeedField):
+        raise TypeError("ref_solve needs a native SpeedField")
+    g = p.grid.c()
+    en = np.ascontiguousarray(p.exit_nodes, dtype=np.int64)
+    ec = np.ascontiguousarray(p.exit_cost, dtype=np.float64)
+    pts = np.ascontiguousarray(p.exit_points, dtype=np.float64).reshape(-1)
+    pc = np.ascontiguousarray(p.exit_point_cost, dtype=np.float64)
+    u = np.empty(p.grid.size(), dtype=np.float64)
+    st = ref_stats()
+    rc = rlib.ref_solve(_REF_METHOD[method], C.byref(g), C.byref(p.speed.cfield),
+                        en.ctypes.data_as(_i64p), ec.ctypes.data_as(_dp), len(en),
+                        pts.ctypes.data_as(_dp) if pts.size else _dp(),
+                        pc.ctypes.data_as(_dp) if pc.size else _dp(), len(pc),
+                        cells_x, cells_y, u.ctypes.data_as(_dp), C.byref(st))
+    if rc == 1:
+        raise N.ConfigError(rlib.ref_last_error().decode())
+    if rc == 3:
+        raise N.BudgetError(rlib.ref_last_error().decode())
+    if rc:
+        raise ValueError(rlib.ref_last_error().decode())
+    return Result(u, st.sweeps, st.node_updates, st.heap_removals, st.mon_checks,
+                  st.mon_single, st.elapsed_ms)
+
+
+def ref_metrics(p: Problem, u_method: np.ndarray, u_exact: np.ndarray, refine: int = 4):
+    """(l_inf, l_1, R, rho, R_ratio) of metrics.cpp against refine-x FMM truth."""
+    g = p.grid.c()
+    en = np.ascontiguousarray(p.exit_nodes, dtype=np.int64)
+    ec = np.ascontiguousarray(p.exit_cost, dtype=np.float64)
+    out = np.zeros(5)
+    um = np.ascontiguousarray(u_method, dtype=np.float64)
+    ue = np.ascontiguousarray(u_exact, dtype=np.float64)
+    rc = rlib.ref_metrics(C.byref(g), C.byref(p.speed.cfield), en.ctypes.data_as(_i64p),
+                          ec.ctypes.data_as(_dp), len(en), refine, um.ctypes.data_as(_dp),
+                          ue.ctypes.data_as(_dp), out.ctypes.data_as(_dp))
+    if rc:
+        raise ValueError(rlib.ref_last_error().decode())
+    return tuple(out)

@@ -1,0 +1,165 @@
+// ORACLE -- TEST INFRASTRUCTURE ONLY.
+//
+// extern "C" entry points around the UNMODIFIED reference library, compiled
+// from /root/reference/proj/src by oracle/Makefile into oracle/_ref/.  The
+// reference runs exactly as shipped: its own Problem, its own solvers, and
+// an on-demand SpeedFn (grid.hpp:64,71) that evaluates our native field
+// definitions (paper_1110_6220_b200/csrc/host_fields.c) -- the same
+// function the product samples, so F bits agree.  Used (1) to pin the C
+// restatement in oracle/eik_oracle.c, (2) as the "reference" CPU baseline in
+// bench.py, (3) to generate golden fixtures.
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+
+#include "eikonal/cells.hpp"
+#include "eikonal/classic_solvers.hpp"
+#include "eikonal/fmsm.hpp"
+#include "eikonal/grid.hpp"
+#include "eikonal/heap_cell.hpp"
+#include "eikonal/local_update.hpp"
+#include "eikonal/metrics.hpp"
+#include "eikonal/speed_fields.hpp"
+#include "eikonal_b200.h"
+
+namespace {
+thread_local std::string g_err;
+}
+
+extern "C" {
+
+struct ref_stats {
+  int64_t sweeps, node_updates, heap_removals;
+  int64_t cell_removals, cell_sweeps, mon_checks, mon_single;
+  double avhr, avs, mon_pct;
+  double elapsed_ms;  // steady_clock around the solver call (experiment.cpp:204-213)
+};
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+double ref_quadrant_update(double a, double b, double f, double h) {
+  return eikonal::quadrant_update(a, b, f, h);
+}
+double ref_node_update(const double nb[4], double f, double h) {
+  return eikonal::node_update({nb[0], nb[1], nb[2], nb[3]}, f, h);
+}
+double ref_directional_update(const double nb[4], int dir, double f, double h) {
+  return eikonal::directional_update({nb[0], nb[1], nb[2], nb[3]},
+                                     static_cast<eikonal::SweepDir>(dir), f, h);
+}
+
+// The reference's own named speed fields (speed_fields.cpp:94-110), used to
+// pin our native restatement of them bit for bit.
+double ref_named_speed(const char* name, double x, double y) {
+  return eikonal::named_problem(name).speed(x, y);
+}
+
+// snap_point_to_node (grid.cpp:22-41); returns 0 or 5 on domain_error
+int ref_snap(const eik_grid* g, double x, double y, int64_t* i, int64_t* j) {
+  try {
+    eikonal::Grid grid(static_cast<int>(g->m), static_cast<int>(g->n), g->h, g->x0, g->y0);
+    eikonal::NodeIndex nd = eikonal::snap_point_to_node(grid, {x, y});
+    *i = nd.i;
+    *j = nd.j;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 5;
+  }
+}
+
+// method numbering = eik_method.  cells_* ignored for exact methods.
+// threads: unused (every reference solve is single-threaded).
+int ref_solve(int method, const eik_grid* g, const eik_field* field,
+              const int64_t* exit_nodes, const double* exit_cost, int64_t n_exit,
+              const double* exit_points_xy, const double* exit_point_cost,
+              int64_t n_points, int cells_x, int cells_y, double* u,
+              ref_stats* st) {
+  try {
+    using namespace eikonal;
+    Problem p;
+    p.grid = Grid(static_cast<int>(g->m), static_cast<int>(g->n), g->h, g->x0, g->y0);
+    eik_field fcopy = *field;
+    p.speed = [fcopy](double x, double y) { return eik_field_eval(&fcopy, x, y); };
+    for (int64_t k = 0; k < n_exit; ++k) {
+      p.exit_nodes.push_back(static_cast<int>(exit_nodes[k]));
+      p.exit_cost.push_back(exit_cost[k]);
+    }
+    for (int64_t k = 0; k < n_points; ++k) {
+      p.exit_points.push_back({exit_points_xy[2 * k], exit_points_xy[2 * k + 1]});
+      p.exit_point_cost.push_back(exit_point_cost[k]);
+    }
+    SolverOutput out;
+    auto t0 = std::chrono::steady_clock::now();
+    switch (method) {
+      case 0: out = fmm_solve(p); break;
+      case 1: out = fsm_solve(p); break;
+      case 2: out = lsm_solve(p); break;
+      case 3: out = hcm_solve(p, build_cells(p.grid, cells_x, cells_y)); break;
+      case 4: out = fhcm_solve(p, build_cells(p.grid, cells_x, cells_y)); break;
+      case 5: out = fmsm_solve(p, build_cells(p.grid, cells_x, cells_y)); break;
+      default: g_err = "bad method"; return 1;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    std::memcpy(u, out.values.values.data(), sizeof(double) * out.values.values.size());
+    st->sweeps = out.sweeps;
+    st->node_updates = out.node_updates;
+    st->heap_removals = out.heap_removals;
+    st->cell_removals = out.hybrid.cell_removals;
+    st->cell_sweeps = out.hybrid.cell_sweeps;
+    st->mon_checks = out.hybrid.mon_checks;
+    st->mon_single = out.hybrid.mon_single;
+    st->avhr = out.hybrid.avhr;
+    st->avs = out.hybrid.avs;
+    st->mon_pct = out.hybrid.mon_pct;
+    st->elapsed_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    return 0;
+  } catch (const eikonal::ConfigError& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::runtime_error& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 5;
+  }
+}
+
+// ground_truth (metrics.cpp:77-99) + method_metrics (metrics.cpp:70-75):
+// fills l_inf, l_1, R, rho, R-ratio of `u_method` against FMM-on-refined
+// truth; `u_exact` is the exact-solver field (FMM).  Returns 0 on success.
+int ref_metrics(const eik_grid* g, const eik_field* field, const int64_t* exit_nodes,
+                const double* exit_cost, int64_t n_exit, int refine,
+                const double* u_method, const double* u_exact, double* out5) {
+  try {
+    using namespace eikonal;
+    Problem p;
+    p.grid = Grid(static_cast<int>(g->m), static_cast<int>(g->n), g->h, g->x0, g->y0);
+    eik_field fcopy = *field;
+    p.speed = [fcopy](double x, double y) { return eik_field_eval(&fcopy, x, y); };
+    for (int64_t k = 0; k < n_exit; ++k) {
+      p.exit_nodes.push_back(static_cast<int>(exit_nodes[k]));
+      p.exit_cost.push_back(exit_cost[k]);
+    }
+    ValueField truth = ground_truth(p, refine);
+    ValueField vm(p.grid.m, p.grid.n), ve(p.grid.m, p.grid.n);
+    std::memcpy(vm.values.data(), u_method, sizeof(double) * vm.values.size());
+    std::memcpy(ve.values.data(), u_exact, sizeof(double) * ve.values.size());
+    MetricsReport r = method_metrics(vm, ve, truth, p.exit_nodes);
+    out5[0] = r.l_inf;
+    out5[1] = r.l_1;
+    out5[2] = r.max_error_ratio;
+    out5[3] = r.avg_error_ratio;
+    out5[4] = r.ratio_of_max;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 5;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,28 @@
+"""B200-native hot path of the two-scale Eikonal solvers (arXiv 1110.6220).
+
+Python mirror of the reference solver interface
+(/root/reference/proj/include/eikonal/*.hpp) over the C-ABI in
+include/eikonal_b200.h.  The solves run in hand-written sm_100a kernels
+(paper_1110_6220_b200/csrc/); there is no CPU fallback.
+"""
+from ._native import BudgetError, ConfigError, LIB_PATH, lib
+from .problem import (CellDecomposition, CellTables, ExitSpec, Grid, Problem, SpeedField,
+                      build_cells, build_problem, cell_tables, snap_point_to_node,
+                      speed_blocks, speed_checkerboard, speed_comb_maze, speed_constant,
+                      speed_nodemask, speed_sinsum, speed_sinusoid)
+from .solvers import (HybridStats, Plan, SolverOutput, fhcm_solve, fmm_solve, fmsm_solve,
+                      fsm_solve, hcm_solve, solve)
+
+
+def device_count() -> int:
+    return int(lib.eik_device_count())
+
+
+__all__ = [
+    "BudgetError", "ConfigError", "LIB_PATH", "CellDecomposition", "CellTables", "ExitSpec",
+    "Grid", "Problem", "SpeedField", "build_cells", "build_problem", "cell_tables",
+    "snap_point_to_node", "speed_blocks", "speed_checkerboard", "speed_comb_maze",
+    "speed_constant", "speed_nodemask", "speed_sinsum", "speed_sinusoid", "HybridStats",
+    "Plan", "SolverOutput", "fhcm_solve", "fmm_solve", "fmsm_solve", "fsm_solve",
+    "hcm_solve", "solve", "device_count",
+]

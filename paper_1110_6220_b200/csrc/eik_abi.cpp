@@ -1,0 +1,286 @@
+// Host runtime behind the C-ABI (include/eikonal_b200.h): argument checks
+// with the reference's error semantics, device buffers, streams, dispatch to
+// the sm_100a kernels, and SolverOutput packing.  No CPU solver lives here:
+// every method either runs on the device or fails with EIK_ERR_NOT_IMPL /
+// EIK_ERR_CUDA.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "eik_internal.h"
+#include "eik_plan.h"
+#include "eikonal_b200.h"
+
+namespace eikb200 {
+
+thread_local std::string g_last_error;
+thread_local int g_last_code = EIK_OK;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  g_last_code = code;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(EIK_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr)                                          \
+  do {                                                    \
+    cudaError_t e_ = (expr);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr);   \
+  } while (0)
+
+namespace {
+
+int check_problem(const eik_problem* p) {
+  if (!p) return fail(EIK_ERR_DOMAIN, "null problem");
+  const eik_grid& g = p->grid;
+  // Grid::Grid (grid.cpp:8-12)
+  if (g.m < 2 || g.n < 2) return fail(EIK_ERR_CONFIG, "grid needs at least 2 nodes per axis");
+  if (!(g.h > 0.0)) return fail(EIK_ERR_CONFIG, "grid spacing must be positive");
+  if (!p->speed) return fail(EIK_ERR_DOMAIN, "null speed array");
+  // build_problem (grid.cpp:77)
+  if (p->n_exit < 1 || !p->exit_nodes || !p->exit_cost)
+    return fail(EIK_ERR_CONFIG, "exit set is empty");
+  const int64_t M = g.m * g.n;
+  for (int64_t k = 0; k < p->n_exit; ++k) {
+    if (p->exit_nodes[k] < 0 || p->exit_nodes[k] >= M)
+      return fail(EIK_ERR_CONFIG, "exit node outside grid");
+    if (k > 0 && p->exit_nodes[k] <= p->exit_nodes[k - 1])
+      return fail(EIK_ERR_DOMAIN, "exit nodes must be strictly ascending");
+    if (!std::isfinite(p->exit_cost[k])) return fail(EIK_ERR_CONFIG, "exit cost must be finite");
+  }
+  if (p->n_exit_points < 0 || (p->n_exit_points > 0 && (!p->exit_points_xy || !p->exit_point_cost)))
+    return fail(EIK_ERR_DOMAIN, "bad exit point list");
+  return EIK_OK;
+}
+
+int check_cells(const eik_problem* p, const eik_cells* c, int method) {
+  const bool hybrid = method == EIK_HCM || method == EIK_FHCM || method == EIK_FMSM;
+  if (!hybrid) return EIK_OK;
+  if (!c) return fail(EIK_ERR_CONFIG, "two-scale methods need a cell decomposition");
+  // build_cells (cells.cpp:33-36)
+  if (c->cells_x < 1 || c->cells_y < 1) return fail(EIK_ERR_CONFIG, "cell counts must be positive");
+  if (c->cells_x > p->grid.m || c->cells_y > p->grid.n)
+    return fail(EIK_ERR_CONFIG, "more cells than grid nodes along an axis");
+  if (method == EIK_FMSM) {
+    if (c->cells_x < 2 || c->cells_y < 2) return fail(EIK_ERR_CONFIG, "fmsm needs at least 2x2 cells");
+    if (!c->center_speed) return fail(EIK_ERR_DOMAIN, "fmsm needs center_speed");
+  } else {
+    if (!c->probe_speed_w || !c->probe_speed_e || !c->probe_speed_s || !c->probe_speed_n)
+      return fail(EIK_ERR_DOMAIN, "hcm/fhcm need the four probe_speed tables");
+  }
+  return EIK_OK;
+}
+
+template <class T>
+int dalloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  return EIK_OK;
+}
+
+}  // namespace
+
+void plan_free(eik_plan* P) {
+  if (!P) return;
+  for (void* ptr : P->allocs) cudaFree(ptr);
+  if (P->ev0) cudaEventDestroy(P->ev0);
+  if (P->ev1) cudaEventDestroy(P->ev1);
+  if (P->stream) cudaStreamDestroy(P->stream);
+  delete P;
+}
+
+int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method) {
+  P->method = method;
+  P->g = p->grid;
+  P->M = p->grid.m * p->grid.n;
+  P->n_exit = p->n_exit;
+  CK(cudaGetDevice(&P->device));
+  CK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&P->ev0));
+  CK(cudaEventCreate(&P->ev1));
+  auto track = [&](void* q) { P->allocs.push_back(q); };
+  int rc;
+  if ((rc = dalloc(&P->dF, P->M))) return rc;
+  track(P->dF);
+  if ((rc = dalloc(&P->dC, P->M))) return rc;
+  track(P->dC);
+  if ((rc = dalloc(&P->dU, P->M))) return rc;
+  track(P->dU);
+  if ((rc = dalloc(&P->dExit, P->n_exit))) return rc;
+  track(P->dExit);
+  if ((rc = dalloc(&P->dExitCost, P->n_exit))) return rc;
+  track(P->dExitCost);
+  if ((rc = dalloc(&P->dStatus, 8))) return rc;
+  track(P->dStatus);
+  CK(cudaMemcpyAsync(P->dF, p->speed, sizeof(double) * P->M,
+                     p->speed_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                     P->stream));
+  CK(cudaMemcpyAsync(P->dExit, p->exit_nodes, sizeof(int64_t) * P->n_exit,
+                     cudaMemcpyHostToDevice, P->stream));
+  CK(cudaMemcpyAsync(P->dExitCost, p->exit_cost, sizeof(double) * P->n_exit,
+                     cudaMemcpyHostToDevice, P->stream));
+  P->h2d_bytes = (p->speed_on_device ? 0 : 8 * P->M) + 16 * P->n_exit;
+  if (method == EIK_FSM || method == EIK_FMM) {
+    P->nstrips = (int)((P->g.n + 31) / 32);
+    P->max_sweeps = 1 << 16;
+    if ((rc = dalloc(&P->dProg, P->nstrips))) return rc;
+    track(P->dProg);
+    if ((rc = dalloc(&P->dChanged, P->max_sweeps))) return rc;
+    track(P->dChanged);
+    if ((rc = dalloc(&P->dDone, P->max_sweeps))) return rc;
+    track(P->dDone);
+  } else if (method == EIK_LSM) {
+    return fail(EIK_ERR_NOT_IMPL, "lsm is not on the device path (out of scope, SURVEY.md §2.1)");
+  } else {
+    (void)c;
+    return fail(EIK_ERR_NOT_IMPL, "method not yet implemented on the device path");
+  }
+  CK(cudaStreamSynchronize(P->stream));
+  return EIK_OK;
+}
+
+int plan_run_fsm(eik_plan* P, eik_output* out) {
+  FsmArgs a;
+  a.C = P->dC;
+  a.u = P->dU;
+  a.m = P->g.m;
+  a.n = P->g.n;
+  a.nstrips = P->nstrips;
+  a.prog = P->dProg;
+  a.changed = P->dChanged;
+  a.done = P->dDone;
+  a.max_sweeps = P->max_sweeps;
+  a.lookahead = 3;
+  a.status = P->dStatus;
+  int launches = 0;
+  CK(cudaEventRecord(P->ev0, P->stream));
+  CK(cudaMemsetAsync(P->dProg, 0, sizeof(unsigned long long) * P->nstrips, P->stream));
+  // only the sweeps that can run need clearing; bound by the previous run
+  size_t clear = (size_t)std::min<int64_t>(P->max_sweeps, P->last_sweeps_bound);
+  CK(cudaMemsetAsync(P->dChanged, 0, sizeof(int) * clear, P->stream));
+  CK(cudaMemsetAsync(P->dDone, 0, sizeof(int) * clear, P->stream));
+  CK(launch_prepare(P->dF, P->dC, P->dU, P->M, P->g.h, P->dExit, P->dExitCost, P->n_exit,
+                    P->dStatus, P->stream, &launches));
+  CK(launch_fsm(a, P->stream, &launches));
+  CK(cudaEventRecord(P->ev1, P->stream));
+  int st[8];
+  CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
+  CK(cudaStreamSynchronize(P->stream));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  if (st[0] == 3) return fail(EIK_ERR_BUDGET, "fsm exceeded the device sweep budget");
+  P->last_sweeps_bound = std::min<int64_t>(P->max_sweeps, (int64_t)st[1] + 8);
+  out->sweeps = st[1];
+  out->node_updates = (int64_t)st[1] * (P->M - P->n_exit);
+  out->heap_removals = 0;
+  if (P->method == EIK_FMM) {
+    // The FMM row is served by the exact fixed-point solver (SURVEY.md §8f
+    // row 1); its accepted-node count is M - |Q| as in classic_solvers.cpp:67-69.
+    out->heap_removals = P->M - P->n_exit;
+  }
+  out->device_ms = ms;
+  out->kernel_launches = launches;
+  return EIK_OK;
+}
+
+int plan_run(eik_plan* P, eik_output* out) {
+  if (!out) return fail(EIK_ERR_DOMAIN, "null output");
+  CK(cudaSetDevice(P->device));
+  out->sweeps = out->node_updates = out->heap_removals = 0;
+  out->cell_removals = out->cell_sweeps = out->mon_checks = out->mon_single = 0;
+  out->avhr = out->avs = out->mon_pct = 0.0;
+  CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
+  int rc;
+  switch (P->method) {
+    case EIK_FSM:
+    case EIK_FMM:
+      rc = plan_run_fsm(P, out);
+      break;
+    default:
+      return fail(EIK_ERR_NOT_IMPL, "method not implemented on the device path");
+  }
+  if (rc) return rc;
+  if (out->u) {
+    CK(cudaMemcpyAsync(out->u, P->dU, sizeof(double) * P->M,
+                       out->u_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                       P->stream));
+    CK(cudaStreamSynchronize(P->stream));
+  }
+  return EIK_OK;
+}
+
+}  // namespace eikb200
+
+using namespace eikb200;
+
+extern "C" {
+
+int eik_abi_version(void) { return EIK_ABI_VERSION; }
+
+const char* eik_last_error(void) { return g_last_error.c_str(); }
+
+int eik_last_status(void) { return g_last_code; }
+
+int eik_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+eik_plan* eik_plan_create(const eik_problem* p, const eik_cells* c, int32_t method) {
+  g_last_code = EIK_OK;
+  g_last_error.clear();
+  if (check_problem(p) || check_cells(p, c, method)) return nullptr;
+  if (method < EIK_FMM || method > EIK_FMSM) {
+    fail(EIK_ERR_CONFIG, "unknown method");
+    return nullptr;
+  }
+  if (eik_device_count() < 1) {
+    fail(EIK_ERR_CUDA, "no CUDA device visible: the Eikonal hot path has no CPU fallback");
+    return nullptr;
+  }
+  eik_plan* P = new eik_plan();
+  if (plan_init(P, p, c, method)) {
+    std::string keep = g_last_error;
+    int keep_code = g_last_code;
+    plan_free(P);
+    g_last_error = keep;
+    g_last_code = keep_code;
+    return nullptr;
+  }
+  return P;
+}
+
+int eik_plan_run(eik_plan* P, eik_output* out) {
+  if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
+  return plan_run(P, out);
+}
+
+const double* eik_plan_values(const eik_plan* P) { return P ? P->dU : nullptr; }
+
+void eik_plan_destroy(eik_plan* P) { plan_free(P); }
+
+int eik_solve(const eik_problem* p, const eik_cells* c, int32_t method, eik_output* out) {
+  if (!out || !out->u) return fail(EIK_ERR_DOMAIN, "output needs a u buffer");
+  eik_plan* P = eik_plan_create(p, c, method);
+  if (!P) return g_last_code != EIK_OK ? g_last_code : EIK_ERR_CUDA;
+  int rc = plan_run(P, out);
+  plan_free(P);
+  return rc;
+}
+
+}  // extern "C"

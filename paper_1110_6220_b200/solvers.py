@@ -1,0 +1,178 @@
+"""Solver entry points mirroring the reference's L2 API.
+
+    fmm_solve(problem)            classic_solvers.hpp:18
+    fsm_solve(problem)            classic_solvers.hpp:33
+    hcm_solve(problem, cells)     heap_cell.hpp:36
+    fhcm_solve(problem, cells)    heap_cell.hpp:41
+    fmsm_solve(problem, cells)    fmsm.hpp:36
+
+Every call crosses the C-ABI (include/eikonal_b200.h) into the sm_100a
+kernels; there is no CPU solver behind these names.  Errors map to the
+reference's exception types (ConfigError, BudgetError ~ runtime_error,
+ValueError ~ domain_error).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import _native as N
+from .problem import CellDecomposition, CellTables, Problem, cell_tables
+
+
+@dataclass
+class HybridStats:
+    """grid.hpp:132-140."""
+    avhr: float = 0.0
+    avs: float = 0.0
+    mon_pct: float = 0.0
+    cell_removals: int = 0
+    cell_sweeps: int = 0
+    mon_checks: int = 0
+    mon_single: int = 0
+
+
+@dataclass
+class SolverOutput:
+    """grid.hpp:142-149; `values` is the m*n row-major field (index j*m+i)."""
+    values: np.ndarray
+    m: int
+    n: int
+    sweeps: int = 0
+    node_updates: int = 0
+    heap_removals: int = 0
+    hybrid: HybridStats = field(default_factory=HybridStats)
+    device_ms: float = 0.0
+    kernel_launches: int = 0
+
+    def at(self, i: int, j: int) -> float:
+        return float(self.values[j * self.m + i])
+
+    def as_2d(self) -> np.ndarray:
+        return self.values.reshape(self.n, self.m)
+
+
+def _c_problem(problem: Problem, F: np.ndarray):
+    p = N.eik_problem()
+    p.grid = problem.grid.c()
+    p.speed = N.dptr(F)
+    p.speed_on_device = 0
+    en = np.ascontiguousarray(problem.exit_nodes, dtype=np.int64)
+    ec = np.ascontiguousarray(problem.exit_cost, dtype=np.float64)
+    pts = np.ascontiguousarray(problem.exit_points, dtype=np.float64).reshape(-1)
+    pc = np.ascontiguousarray(problem.exit_point_cost, dtype=np.float64)
+    p.exit_nodes = N.i64ptr(en)
+    p.exit_cost = N.dptr(ec)
+    p.n_exit = len(en)
+    p.exit_points_xy = N.dptr(pts) if pts.size else N.dptr(None)
+    p.exit_point_cost = N.dptr(pc) if pc.size else N.dptr(None)
+    p.n_exit_points = len(pc)
+    return p, (en, ec, pts, pc, F)
+
+
+def _c_cells(cells: Optional[CellDecomposition], tabs: Optional[CellTables]):
+    if cells is None:
+        return None, ()
+    c = N.eik_cells()
+    c.cells_x = cells.cells_x
+    c.cells_y = cells.cells_y
+    keep = ()
+    if tabs is not None:
+        arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+                (tabs.probe_w, tabs.probe_e, tabs.probe_s, tabs.probe_n, tabs.center)]
+        c.probe_speed_w, c.probe_speed_e, c.probe_speed_s, c.probe_speed_n, c.center_speed = \
+            [N.dptr(a) for a in arrs]
+        keep = tuple(arrs)
+    return c, keep
+
+
+def _pack(out: N.eik_output, values: np.ndarray, g) -> SolverOutput:
+    return SolverOutput(values=values, m=g.m, n=g.n, sweeps=out.sweeps,
+                        node_updates=out.node_updates, heap_removals=out.heap_removals,
+                        hybrid=HybridStats(out.avhr, out.avs, out.mon_pct, out.cell_removals,
+                                           out.cell_sweeps, out.mon_checks, out.mon_single),
+                        device_ms=out.device_ms, kernel_launches=out.kernel_launches)
+
+
+def solve(problem: Problem, method: str, cells: Optional[CellDecomposition] = None,
+          tables: Optional[CellTables] = None) -> SolverOutput:
+    """One solve through eik_solve (host buffers in, host values out)."""
+    code = N.METHOD_NAMES[method]
+    F = problem.sampled_speed()
+    p, keep_p = _c_problem(problem, F)
+    if cells is not None and tables is None:
+        tables = cell_tables(problem, cells)
+    c, keep_c = _c_cells(cells, tables)
+    u = np.empty(problem.grid.size(), dtype=np.float64)
+    out = N.eik_output()
+    out.u = N.dptr(u)
+    out.u_on_device = 0
+    rc = N.lib.eik_solve(C.byref(p), C.byref(c) if c is not None else None, code, C.byref(out))
+    N.raise_for(rc)
+    return _pack(out, u, problem.grid)
+
+
+def fmm_solve(problem: Problem) -> SolverOutput:
+    return solve(problem, "fmm")
+
+
+def fsm_solve(problem: Problem) -> SolverOutput:
+    return solve(problem, "fsm")
+
+
+def hcm_solve(problem: Problem, cells: CellDecomposition) -> SolverOutput:
+    return solve(problem, "hcm", cells)
+
+
+def fhcm_solve(problem: Problem, cells: CellDecomposition) -> SolverOutput:
+    return solve(problem, "fhcm", cells)
+
+
+def fmsm_solve(problem: Problem, cells: CellDecomposition) -> SolverOutput:
+    return solve(problem, "fmsm", cells)
+
+
+class Plan:
+    """Resident solve (eik_plan_*): inputs uploaded once, values stay in HBM."""
+
+    def __init__(self, problem: Problem, method: str,
+                 cells: Optional[CellDecomposition] = None,
+                 tables: Optional[CellTables] = None):
+        self.problem = problem
+        self.method = method
+        F = problem.sampled_speed()
+        p, keep_p = _c_problem(problem, F)
+        if cells is not None and tables is None:
+            tables = cell_tables(problem, cells)
+        c, keep_c = _c_cells(cells, tables)
+        self._h = N.lib.eik_plan_create(C.byref(p), C.byref(c) if c is not None else None,
+                                        N.METHOD_NAMES[method])
+        if not self._h:
+            N.raise_for(N.lib.eik_last_status() or N.EIK_ERR_CUDA)
+
+    def run(self, u_host: Optional[np.ndarray] = None, u_device_ptr: int = 0) -> SolverOutput:
+        out = N.eik_output()
+        if u_host is not None:
+            out.u = N.dptr(u_host)
+            out.u_on_device = 0
+        elif u_device_ptr:
+            out.u = C.cast(C.c_void_p(u_device_ptr), C.POINTER(C.c_double))
+            out.u_on_device = 1
+        else:
+            out.u = N.dptr(None)
+        N.raise_for(N.lib.eik_plan_run(self._h, C.byref(out)))
+        return _pack(out, u_host, self.problem.grid)
+
+    def values_ptr(self) -> int:
+        return N.lib.eik_plan_values(self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib.eik_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
