@@ -115,8 +115,11 @@ eik_plan* eik_plan_create(const eik_problem* p, const eik_cells* cells,
 /* Solve into out->u (host or device per out->u_on_device; NULL u keeps the
  * result resident in the plan).  */
 int eik_plan_run(eik_plan* plan, eik_output* out);
-/* Device pointer to the plan's resident value field (m*n fp64). */
+/* Device pointer to the plan's resident value field: node (i,j) is at
+ * values[j*pitch + i] with pitch = eik_plan_pitch(plan) (the device layout is
+ * row-padded for the sweep kernels). */
 const double* eik_plan_values(const eik_plan* plan);
+int64_t eik_plan_pitch(const eik_plan* plan);
 void eik_plan_destroy(eik_plan* plan);
 
 /* Thread-local description / status code of the last failure on this

@@ -73,6 +73,7 @@ EXPORTS = {
     "eik_plan_create": (C.c_void_p, [C.POINTER(eik_problem), C.POINTER(eik_cells), C.c_int32]),
     "eik_plan_run": (C.c_int, [C.c_void_p, C.POINTER(eik_output)]),
     "eik_plan_values": (C.c_void_p, [C.c_void_p]),
+    "eik_plan_pitch": (C.c_int64, [C.c_void_p]),
     "eik_plan_destroy": (None, [C.c_void_p]),
     "eik_last_error": (C.c_char_p, []),
     "eik_last_status": (C.c_int, []),

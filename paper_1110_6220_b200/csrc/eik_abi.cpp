@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -112,9 +113,11 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method)
   int rc;
   if ((rc = dalloc(&P->dF, P->M))) return rc;
   track(P->dF);
-  if ((rc = dalloc(&P->dC, P->M))) return rc;
+  P->pitch = P->g.m + 2 * kPad;
+  const size_t padded = (size_t)(P->g.n + 1) * P->pitch;
+  if ((rc = dalloc(&P->dC, padded))) return rc;
   track(P->dC);
-  if ((rc = dalloc(&P->dU, P->M))) return rc;
+  if ((rc = dalloc(&P->dU, padded))) return rc;
   track(P->dU);
   if ((rc = dalloc(&P->dExit, P->n_exit))) return rc;
   track(P->dExit);
@@ -135,6 +138,8 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method)
     P->max_sweeps = 1 << 16;
     if ((rc = dalloc(&P->dProg, P->nstrips))) return rc;
     track(P->dProg);
+    if ((rc = dalloc(&P->dMbox, (size_t)2 * P->nstrips * P->pitch))) return rc;
+    track(P->dMbox);
     if ((rc = dalloc(&P->dChanged, P->max_sweeps))) return rc;
     track(P->dChanged);
     if ((rc = dalloc(&P->dDone, P->max_sweeps))) return rc;
@@ -155,22 +160,37 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   a.u = P->dU;
   a.m = P->g.m;
   a.n = P->g.n;
+  a.P = P->pitch;
+  a.pad = kPad;
   a.nstrips = P->nstrips;
   a.prog = P->dProg;
+  a.mbox = P->dMbox;
   a.changed = P->dChanged;
   a.done = P->dDone;
   a.max_sweeps = P->max_sweeps;
   a.lookahead = 3;
   a.status = P->dStatus;
+  a.trace = nullptr;
+  if (std::getenv("EIK_TRACE_FSM")) {
+    if (!P->dTrace) {
+      int rc = dalloc(&P->dTrace, (size_t)kTraceSweeps * P->nstrips * 3);
+      if (rc) return rc;
+      P->allocs.push_back(P->dTrace);
+    }
+    CK(cudaMemsetAsync(P->dTrace, 0, sizeof(unsigned long long) * kTraceSweeps * P->nstrips * 3,
+                       P->stream));
+    a.trace = P->dTrace;
+  }
   int launches = 0;
   CK(cudaEventRecord(P->ev0, P->stream));
   CK(cudaMemsetAsync(P->dProg, 0, sizeof(unsigned long long) * P->nstrips, P->stream));
+  CK(cudaMemsetAsync(P->dMbox, 0xFF, sizeof(double) * 2 * P->nstrips * P->pitch, P->stream));
   // only the sweeps that can run need clearing; bound by the previous run
   size_t clear = (size_t)std::min<int64_t>(P->max_sweeps, P->last_sweeps_bound);
   CK(cudaMemsetAsync(P->dChanged, 0, sizeof(int) * clear, P->stream));
   CK(cudaMemsetAsync(P->dDone, 0, sizeof(int) * clear, P->stream));
-  CK(launch_prepare(P->dF, P->dC, P->dU, P->M, P->g.h, P->dExit, P->dExitCost, P->n_exit,
-                    P->dStatus, P->stream, &launches));
+  CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
+                    P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
   CK(launch_fsm(a, P->stream, &launches));
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];
@@ -180,6 +200,7 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
   if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
   if (st[0] == 3) return fail(EIK_ERR_BUDGET, "fsm exceeded the device sweep budget");
+  if (st[0] == 4) return fail(EIK_ERR_CUDA, "fsm wavefront watchdog fired (scheduling bug)");
   P->last_sweeps_bound = std::min<int64_t>(P->max_sweeps, (int64_t)st[1] + 8);
   out->sweeps = st[1];
   out->node_updates = (int64_t)st[1] * (P->M - P->n_exit);
@@ -191,6 +212,20 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   }
   out->device_ms = ms;
   out->kernel_launches = launches;
+  if (a.trace) {
+    std::vector<unsigned long long> tr((size_t)kTraceSweeps * P->nstrips * 3);
+    CK(cudaMemcpy(tr.data(), a.trace, sizeof(unsigned long long) * tr.size(),
+                  cudaMemcpyDeviceToHost));
+    const char* path = std::getenv("EIK_TRACE_FSM");
+    if (FILE* f = std::fopen(path, "w")) {
+      for (int k = 0; k < kTraceSweeps; ++k)
+        for (int b = 0; b < P->nstrips; ++b) {
+          const unsigned long long* t = &tr[((size_t)k * P->nstrips + b) * 3];
+          if (t[0]) std::fprintf(f, "%d %d %llu %llu %llu\n", k, b, t[0], t[1], t[2]);
+        }
+      std::fclose(f);
+    }
+  }
   return EIK_OK;
 }
 
@@ -212,9 +247,11 @@ int plan_run(eik_plan* P, eik_output* out) {
   }
   if (rc) return rc;
   if (out->u) {
-    CK(cudaMemcpyAsync(out->u, P->dU, sizeof(double) * P->M,
-                       out->u_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
-                       P->stream));
+    // padded device layout -> caller's dense row-major m*n field
+    CK(cudaMemcpy2DAsync(out->u, sizeof(double) * P->g.m, P->dU + kPad,
+                         sizeof(double) * P->pitch, sizeof(double) * P->g.m, P->g.n,
+                         out->u_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
+                         P->stream));
     CK(cudaStreamSynchronize(P->stream));
   }
   return EIK_OK;
@@ -270,7 +307,9 @@ int eik_plan_run(eik_plan* P, eik_output* out) {
   return plan_run(P, out);
 }
 
-const double* eik_plan_values(const eik_plan* P) { return P ? P->dU : nullptr; }
+const double* eik_plan_values(const eik_plan* P) { return P ? P->dU + kPad : nullptr; }
+
+int64_t eik_plan_pitch(const eik_plan* P) { return P ? P->pitch : 0; }
 
 void eik_plan_destroy(eik_plan* P) { plan_free(P); }
 

@@ -6,22 +6,34 @@
 
 namespace eikb200 {
 
+// Device layout of every plan (chosen for the kernels, not the caller):
+// value field u and cost C = h/F are stored with a row pitch P = m + 2*kPad
+// and n+1 rows; grid node (i,j) lives at j*P + kPad + i.  Padding columns and
+// the dummy row n hold u = +inf, C = -1 (the exit/no-update marker), so the
+// sweep kernels never test bounds.
+constexpr int64_t kPad = 64;
+
 struct FsmArgs {
-  const double* C;          // h/F per node, -1 for exits
-  double* u;                // value field
-  int64_t m, n;
+  const double* C;          // padded h/F, -1 for exits and padding
+  double* u;                // padded value field
+  int64_t m, n, P, pad;
   int nstrips;              // ceil(n / 32)
-  unsigned long long* prog; // [nstrips] progress of each strip's last row
+  unsigned long long* prog; // [nstrips] sweeps completed by each strip
+  double* mbox;             // [2][nstrips] rows of pitch P: edge-row mailboxes
   int* changed;             // [max_sweeps] change flag per sweep
   int* done;                // [max_sweeps] strips finished per sweep
   int max_sweeps;
   int lookahead;            // D: stop decision for sweep k uses sweep k-D
   int* status;              // [0] error, [1] sweeps
+  unsigned long long* trace; // optional [kTraceSweeps][nstrips][3] globaltimer
+                             // (start, body start, end) per strip-sweep
 };
+constexpr int kTraceSweeps = 16;
 
-cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t M, double h,
-                           const int64_t* exits, const double* cost, int64_t n_exit,
-                           int* status, cudaStream_t s, int* launches);
+cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int64_t n,
+                           int64_t P, int64_t pad, double h, const int64_t* exits,
+                           const double* cost, int64_t n_exit, int* status, cudaStream_t s,
+                           int* launches);
 cudaError_t launch_fsm(const FsmArgs& a, cudaStream_t s, int* launches);
 
 }  // namespace eikb200

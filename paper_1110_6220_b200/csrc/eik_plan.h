@@ -24,11 +24,14 @@ struct eik_plan {
   double* dExitCost = nullptr;
   int* dStatus = nullptr;
   int64_t h2d_bytes = 0;
+  int64_t pitch = 0;       // padded row pitch of dC / dU (m + 2*kPad)
   // FSM wavefront state
   int nstrips = 0;
   int max_sweeps = 0;
   int64_t last_sweeps_bound = 1 << 16;
   unsigned long long* dProg = nullptr;
+  double* dMbox = nullptr;
+  unsigned long long* dTrace = nullptr;
   int* dChanged = nullptr;
   int* dDone = nullptr;
 };
