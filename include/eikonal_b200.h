@@ -98,6 +98,7 @@ typedef struct eik_output {
   int64_t cell_removals, cell_sweeps, mon_checks, mon_single;
   double avhr, avs, mon_pct;
   double device_ms;     /* CUDA-event time of the device solve proper */
+  double host_ms;       /* host part of the solve (FMSM Part I), else 0 */
   int64_t kernel_launches; /* kernels this call launched (evidence) */
 } eik_output;
 

@@ -50,7 +50,7 @@ class eik_output(C.Structure):
                 ("heap_removals", C.c_int64), ("cell_removals", C.c_int64),
                 ("cell_sweeps", C.c_int64), ("mon_checks", C.c_int64),
                 ("mon_single", C.c_int64), ("avhr", C.c_double), ("avs", C.c_double),
-                ("mon_pct", C.c_double), ("device_ms", C.c_double),
+                ("mon_pct", C.c_double), ("device_ms", C.c_double), ("host_ms", C.c_double),
                 ("kernel_launches", C.c_int64)]
 
 

@@ -32,12 +32,6 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(EIK_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-#define CK(expr)                                          \
-  do {                                                    \
-    cudaError_t e_ = (expr);                              \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #expr);   \
-  } while (0)
-
 namespace {
 
 int check_problem(const eik_problem* p) {
@@ -78,14 +72,6 @@ int check_cells(const eik_problem* p, const eik_cells* c, int method) {
     if (!c->probe_speed_w || !c->probe_speed_e || !c->probe_speed_s || !c->probe_speed_n)
       return fail(EIK_ERR_DOMAIN, "hcm/fhcm need the four probe_speed tables");
   }
-  return EIK_OK;
-}
-
-template <class T>
-int dalloc(T** p, size_t count) {
-  if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
   return EIK_OK;
 }
 
@@ -147,8 +133,7 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method)
   } else if (method == EIK_LSM) {
     return fail(EIK_ERR_NOT_IMPL, "lsm is not on the device path (out of scope, SURVEY.md §2.1)");
   } else {
-    (void)c;
-    return fail(EIK_ERR_NOT_IMPL, "method not yet implemented on the device path");
+    if ((rc = plan_init_cells(P, p, c))) return rc;
   }
   CK(cudaStreamSynchronize(P->stream));
   return EIK_OK;
@@ -235,12 +220,16 @@ int plan_run(eik_plan* P, eik_output* out) {
   out->sweeps = out->node_updates = out->heap_removals = 0;
   out->cell_removals = out->cell_sweeps = out->mon_checks = out->mon_single = 0;
   out->avhr = out->avs = out->mon_pct = 0.0;
+  out->host_ms = 0.0;
   CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
   int rc;
   switch (P->method) {
     case EIK_FSM:
     case EIK_FMM:
       rc = plan_run_fsm(P, out);
+      break;
+    case EIK_FMSM:
+      rc = plan_run_fmsm(P, out);
       break;
     default:
       return fail(EIK_ERR_NOT_IMPL, "method not implemented on the device path");

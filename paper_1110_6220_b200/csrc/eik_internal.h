@@ -30,6 +30,34 @@ struct FsmArgs {
 };
 constexpr int kTraceSweeps = 16;
 
+// Cell decomposition as seen by the device (build_cells, cells.cpp:32-47):
+// cell (cx,cy) spans columns [cx*base_x, cx==cells_x-1 ? m : (cx+1)*base_x).
+struct CellGeom {
+  int64_t m, n, P, pad;
+  int cells_x, cells_y;
+  int64_t base_x, base_y;
+  int max_w, max_h;         // largest cell (the last row/column of cells)
+  int pu, pc;               // even smem pitches of the u tile (w+2) and C tile (w)
+  int64_t tile_doubles;     // per-warp smem: (max_h+2)*pu + max_h*pc
+};
+
+struct FmsmArgs {
+  CellGeom g;
+  const double* C;          // padded h/F
+  double* u;                // padded values
+  const int32_t* order;     // cells in coarse order
+  const int32_t* rank;
+  const uint8_t* flags;     // bit d: sweep direction d chosen; bit 4: Q-cell
+  int* done;                // [J] cell finished
+  int* next;                // claim counter
+  unsigned long long* counters;  // [0] sweeps, [1] node updates
+  int* status;
+  int J;
+  int max_cell_sweeps;
+};
+
+cudaError_t launch_fmsm(const FmsmArgs& a, int warps_per_cta, cudaStream_t s, int* launches);
+
 cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int64_t n,
                            int64_t P, int64_t pad, double h, const int64_t* exits,
                            const double* cost, int64_t n_exit, int* status, cudaStream_t s,

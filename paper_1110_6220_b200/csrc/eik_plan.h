@@ -1,11 +1,14 @@
-// Resident solve plan: device buffers and stream owned by one eik_plan.
+// Resident solve plan: device buffers, host copies of the inputs and the
+// stream owned by one eik_plan, plus the host runtime's shared helpers.
 #pragma once
 
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 #include <vector>
 
+#include "eik_internal.h"
 #include "eikonal_b200.h"
 
 struct eik_plan {
@@ -18,8 +21,8 @@ struct eik_plan {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<void*> allocs;
   double* dF = nullptr;   // speed (resident input)
-  double* dC = nullptr;   // h/F, -1 at exits
-  double* dU = nullptr;   // value field
+  double* dC = nullptr;   // padded h/F, -1 at exits and padding
+  double* dU = nullptr;   // padded value field
   int64_t* dExit = nullptr;
   double* dExitCost = nullptr;
   int* dStatus = nullptr;
@@ -34,4 +37,42 @@ struct eik_plan {
   unsigned long long* dTrace = nullptr;
   int* dChanged = nullptr;
   int* dDone = nullptr;
+  // two-scale methods: host copies of the inputs (the plan owns them)
+  int32_t cells_x = 0, cells_y = 0;
+  std::vector<int64_t> exit_nodes;
+  std::vector<double> exit_cost, exit_points_xy, exit_point_cost;
+  std::vector<double> center_speed;
+  std::vector<double> probe[4];
+  eikb200::CellGeom cg{};
+  int warps_per_cta = 0;
+  int32_t* dOrder = nullptr;
+  int32_t* dRank = nullptr;
+  uint8_t* dFlags = nullptr;
+  int* dCellDone = nullptr;
+  int* dNext = nullptr;
+  unsigned long long* dCounters = nullptr;
 };
+
+namespace eikb200 {
+
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t e, const char* where);
+
+#define CK(expr)                                          \
+  do {                                                    \
+    cudaError_t e_ = (expr);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr);   \
+  } while (0)
+
+template <class T>
+int dalloc(T** p, size_t count) {
+  if (count == 0) count = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  return EIK_OK;
+}
+
+int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c);
+int plan_run_fmsm(eik_plan* P, eik_output* out);
+
+}  // namespace eikb200

@@ -1,0 +1,217 @@
+// Kernel (2): in-cell sweeps for the two-scale methods, and the FMSM fine
+// pass as a device-side dataflow schedule.
+//
+// In-cell sweep (replaces the `full_sweep` lambda, /root/reference/proj/src/
+// fmsm.cpp:176-195): a warp stages one cell plus its one-node cross halo and
+// its costs C = h/F in shared memory, then sweeps the cell as an
+// anti-diagonal wavefront in the requested direction -- lane L owns sweep
+// rows L, L+32, ...; the nodes of one anti-diagonal are independent and
+// every node reads its two upwind neighbours from the previous diagonal, so
+// the result is bit-identical to the reference's row-by-row loop.
+//
+// FMSM Part II (fmsm.cpp:164-226): cells are claimed in the coarse order
+// (host Part I, eik_coarse.cpp); a claimed cell waits only for its
+// earlier-ranked neighbour cells.  Cells that run at the same time are never
+// adjacent and a cell reads nothing but its own nodes and its cross halo, so
+// any schedule respecting those edges reproduces the sequential pass bit for
+// bit -- with far less waiting than level-synchronous batches.
+#include "eik_internal.h"
+#include "k_common.cuh"
+
+namespace eikb200 {
+
+namespace {
+
+enum { SW = 0, NW = 1, NE = 2, SE = 3 };  // SweepDir (local_update.hpp:23)
+
+struct Tile {
+  double* U;        // (h+2) x pu, node (x,y) at (y+1)*pu + x+1
+  double* Ct;       // h x pc costs, -1 at exits
+  int pu, pc, w, h;
+};
+
+// One in-cell sweep.  MODE 0: node_update (local_update.hpp:48-51);
+// MODE 1: directional_update (local_update.hpp:55-64).  Returns the warp-wide
+// "some value decreased" flag.
+template <int MODE>
+__device__ bool tile_sweep(const Tile& T, int dir, int lane) {
+  const bool iasc = (dir == SW || dir == NW);
+  const bool jasc = (dir == SW || dir == SE);
+  bool changed = false;
+  const int nsteps = T.w + T.h - 1;
+  for (int s = 0; s < nsteps; ++s) {
+    for (int b = lane; b < T.h; b += 32) {
+      const int a = s - b;
+      if (a >= 0 && a < T.w) {
+        const int x = iasc ? a : T.w - 1 - a;
+        const int y = jasc ? b : T.h - 1 - b;
+        const double c = T.Ct[y * T.pc + x];
+        if (c > 0.0) {
+          double* p = T.U + (y + 1) * T.pu + (x + 1);
+          const double cur = *p;
+          double cand;
+          if (MODE == 0) {
+            cand = node_update4(p[1], p[-1], p[T.pu], p[-T.pu], c);
+          } else {
+            const double hx = (dir == NE || dir == SE) ? p[1] : p[-1];      // E or W
+            const double vy = (dir == NE || dir == NW) ? p[T.pu] : p[-T.pu];  // N or S
+            cand = quad_update(hx, vy, c);
+          }
+          if (cand < cur) {
+            *p = cand;
+            changed = true;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  return __any_sync(kFull, changed);
+}
+
+__device__ __forceinline__ void cell_rect(const CellGeom& g, int cell, int64_t& ib, int64_t& ie,
+                                          int64_t& jb, int64_t& je) {
+  const int cx = cell % g.cells_x, cy = cell / g.cells_x;
+  ib = (int64_t)cx * g.base_x;
+  ie = (cx == g.cells_x - 1) ? g.m : ib + g.base_x;  // remainder to the last cell
+  jb = (int64_t)cy * g.base_y;
+  je = (cy == g.cells_y - 1) ? g.n : jb + g.base_y;
+}
+
+__device__ __forceinline__ int cell_neighbor(const CellGeom& g, int cell, int side) {
+  const int cx = cell % g.cells_x, cy = cell / g.cells_x;
+  switch (side) {  // cells.hpp:51-61 (W, E, S, N)
+    case 0: return cx > 0 ? cell - 1 : -1;
+    case 1: return cx + 1 < g.cells_x ? cell + 1 : -1;
+    case 2: return cy > 0 ? cell - g.cells_x : -1;
+    default: return cy + 1 < g.cells_y ? cell + g.cells_x : -1;
+  }
+}
+
+// Stage a cell and its cross halo (no corners) into the warp's tile; returns
+// the number of exit nodes in the cell.
+__device__ int stage_in(const CellGeom& g, const double* __restrict__ C, const double* u,
+                        int64_t ib, int64_t jb, Tile& T, int lane) {
+  const int W2 = T.w + 2;
+  const int tot = (T.h + 2) * W2;
+  for (int k = lane; k < tot; k += 32) {
+    const int y = k / W2 - 1, x = k % W2 - 1;
+    const bool corner = (x < 0 || x >= T.w) && (y < 0 || y >= T.h);
+    if (corner) continue;
+    const int64_t gj = jb + y;
+    double v = kInf;
+    if (gj >= 0 && gj < g.n) v = __ldcg(u + gj * g.P + g.pad + ib + x);  // padding = +inf
+    T.U[(y + 1) * T.pu + (x + 1)] = v;
+  }
+  int exits = 0;
+  for (int k = lane; k < T.w * T.h; k += 32) {
+    const int y = k / T.w, x = k % T.w;
+    const double c = __ldg(C + (jb + y) * g.P + g.pad + ib + x);
+    T.Ct[y * T.pc + x] = c;
+    exits += (c < 0.0);
+  }
+  __syncwarp();
+  for (int o = 16; o > 0; o >>= 1) exits += __shfl_xor_sync(kFull, exits, o);
+  return exits;
+}
+
+__device__ void stage_out(const CellGeom& g, double* u, int64_t ib, int64_t jb, const Tile& T,
+                          int lane) {
+  for (int k = lane; k < T.w * T.h; k += 32) {
+    const int y = k / T.w, x = k % T.w;
+    u[(jb + y) * g.P + g.pad + ib + x] = T.U[(y + 1) * T.pu + (x + 1)];
+  }
+}
+
+__global__ void fmsm_dataflow_kernel(FmsmArgs a) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  Tile T;
+  T.pu = a.g.pu;
+  T.pc = a.g.pc;
+  T.U = smem + (size_t)wib * a.g.tile_doubles;
+  T.Ct = T.U + (size_t)(a.g.max_h + 2) * a.g.pu;
+  long long my_sweeps = 0, my_updates = 0;
+
+  for (;;) {
+    int p = 0;
+    if (lane == 0) p = atomicAdd(a.next, 1);
+    p = __shfl_sync(kFull, p, 0);
+    if (p >= a.J) break;
+    const int cell = a.order[p];
+    int64_t ib, ie, jb, je;
+    cell_rect(a.g, cell, ib, ie, jb, je);
+    T.w = (int)(ie - ib);
+    T.h = (int)(je - jb);
+    // wait for the earlier-ranked neighbour cells (one lane per side)
+    int ok = 1;
+    if (lane < 4) {
+      const int nb = cell_neighbor(a.g, cell, lane);
+      if (nb >= 0 && a.rank[nb] < p) ok = wait_ge_s32(a.done + nb, 1, a.status);
+    }
+    if (__any_sync(kFull, !ok)) return;
+    const int exits = stage_in(a.g, a.C, a.u, ib, jb, T, lane);
+    const int flags = a.flags[cell];
+    int nsw = 0;
+    if (flags & 16) {
+      // Q-cell: FSM to convergence with the halo frozen (fmsm.cpp:200-210)
+      bool changed = true;
+      while (changed) {
+        changed = tile_sweep<0>(T, nsw & 3, lane);
+        ++nsw;
+        if (nsw > a.max_cell_sweeps) {
+          if (lane == 0) atomicExch(a.status, 3);
+          return;
+        }
+      }
+    } else {
+      // one directional sweep per chosen direction, in NE, NW, SE, SW order
+      const int order[4] = {NE, NW, SE, SW};
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (flags & (1 << order[k])) {
+          tile_sweep<1>(T, order[k], lane);
+          ++nsw;
+        }
+    }
+    stage_out(a.g, a.u, ib, jb, T, lane);
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release_s32(a.done + cell, 1);
+    my_sweeps += nsw;
+    my_updates += (long long)nsw * (T.w * T.h - exits);
+  }
+  if (lane == 0) {
+    atomicAdd(a.counters + 0, (unsigned long long)my_sweeps);
+    atomicAdd(a.counters + 1, (unsigned long long)my_updates);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_fmsm(const FmsmArgs& args, int warps_per_cta, cudaStream_t s, int* launches) {
+  const size_t smem = (size_t)warps_per_cta * args.g.tile_doubles * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(fmsm_dataflow_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fmsm_dataflow_kernel,
+                                                    32 * warps_per_cta, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int ctas = per_sm * sms;
+  const int need = (args.J + warps_per_cta - 1) / warps_per_cta;
+  if (ctas > need) ctas = need;
+  FmsmArgs a = args;
+  void* params[] = {&a};
+  // workers spin on each other's cells: all CTAs must be co-resident
+  e = cudaLaunchCooperativeKernel((const void*)fmsm_dataflow_kernel, dim3(ctas),
+                                  dim3(32 * warps_per_cta), params, smem, s);
+  *launches += 1;
+  return e;
+}
+
+}  // namespace eikb200

@@ -46,6 +46,7 @@ class SolverOutput:
     heap_removals: int = 0
     hybrid: HybridStats = field(default_factory=HybridStats)
     device_ms: float = 0.0
+    host_ms: float = 0.0
     kernel_launches: int = 0
 
     def at(self, i: int, j: int) -> float:
@@ -94,7 +95,8 @@ def _pack(out: N.eik_output, values: np.ndarray, g) -> SolverOutput:
                         node_updates=out.node_updates, heap_removals=out.heap_removals,
                         hybrid=HybridStats(out.avhr, out.avs, out.mon_pct, out.cell_removals,
                                            out.cell_sweeps, out.mon_checks, out.mon_single),
-                        device_ms=out.device_ms, kernel_launches=out.kernel_launches)
+                        device_ms=out.device_ms, host_ms=out.host_ms,
+                        kernel_launches=out.kernel_launches)
 
 
 def solve(problem: Problem, method: str, cells: Optional[CellDecomposition] = None,

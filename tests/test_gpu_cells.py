@@ -1,0 +1,119 @@
+"""GPU parity for the two-scale methods (kernels 2 and 3).
+
+FMSM must be bitwise-identical to the reference with identical counters
+(SURVEY.md finding 4: the DAG-respecting schedule reproduces the one-pass
+order exactly).  Golden values come from the unmodified reference
+(tests/golden/make_golden.py); random cases use the oracle, which is pinned
+to the reference by tests/test_oracle.py.
+"""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1110_6220_b200 as E
+from paper_1110_6220_b200 import configs
+from oracle import oracle as O
+from tests.golden.make_golden import SMALL_CASES
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def sha(u):
+    return hashlib.sha256(np.ascontiguousarray(u, dtype=np.float64).tobytes()).hexdigest()
+
+
+def bitwise(a, b):
+    return np.array_equal(np.asarray(a).view(np.int64), np.asarray(b).view(np.int64))
+
+
+def _big():
+    with open(os.path.join(GOLD, "big.json")) as f:
+        return json.load(f)
+
+
+def _small():
+    with open(os.path.join(GOLD, "small.json")) as f:
+        return np.load(os.path.join(GOLD, "small.npz")), json.load(f)
+
+
+@pytest.mark.parametrize("cid,make,cells", SMALL_CASES, ids=[c[0] for c in SMALL_CASES])
+def test_fmsm_small_golden_fields(cid, make, cells):
+    arrays, meta = _small()
+    p = make()
+    for c in cells:
+        key = f"{cid}/fmsm/{c}"
+        out = E.fmsm_solve(p, E.build_cells(p.grid, c, c))
+        assert bitwise(out.values, arrays[key]), key
+        m = meta[key]
+        assert (out.sweeps, out.node_updates, out.heap_removals) == \
+            (m["sweeps"], m["node_updates"], m["heap_removals"]), key
+
+
+def test_fmsm_c1_bitwise():
+    big = _big()["c1/fmsm/16"]
+    p = configs.config1().problem
+    out = E.fmsm_solve(p, E.build_cells(p.grid, 16, 16))
+    assert sha(out.values) == big["sha256"]
+    assert (out.sweeps, out.node_updates, out.heap_removals) == \
+        (big["sweeps"], big["node_updates"], big["heap_removals"])
+
+
+@pytest.mark.parametrize("cs", [8, 16, 32, 64])
+def test_fmsm_c2_bitwise_full_size(cs):
+    big = _big()[f"c2/fmsm/{cs}"]
+    p = configs.config2().problem
+    out = E.fmsm_solve(p, E.build_cells(p.grid, big["cells"], big["cells"]))
+    assert sha(out.values) == big["sha256"]
+    assert (out.sweeps, out.node_updates, out.heap_removals) == \
+        (big["sweeps"], big["node_updates"], big["heap_removals"])
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fmsm_random_against_oracle(seed):
+    rng = np.random.default_rng(100 + seed)
+    m, n = int(rng.integers(12, 160)), int(rng.integers(12, 160))
+    g = E.Grid(m, n, float(rng.uniform(0.002, 0.05)), -0.1, 0.3)
+    F = rng.uniform(0.1, 3.0, size=(n, m))
+    sp = lambda x, y, F=F, g=g: F[np.rint((y - g.y0) / g.h).astype(int),  # noqa: E731
+                                  np.rint((x - g.x0) / g.h).astype(int)]
+    if seed % 3 == 0:
+        ex = E.ExitSpec.point_source((g.x(int(rng.integers(0, m))) + 0.3 * g.h,
+                                      g.y(int(rng.integers(0, n))) - 0.2 * g.h))
+    elif seed % 3 == 1:
+        k = int(rng.integers(2, 9))
+        ex = E.ExitSpec.node_set([(int(rng.integers(0, m)), int(rng.integers(0, n)))
+                                  for _ in range(k)], list(rng.uniform(0, 0.2, size=k)))
+    else:
+        ex = E.ExitSpec.full_boundary()
+    p = E.build_problem(g, sp, ex)
+    for cx, cy in [(2, 2), (int(rng.integers(2, 9)), int(rng.integers(2, 9))),
+                   (max(2, m // 8), max(2, n // 8))]:
+        cells = E.build_cells(g, cx, cy)
+        a = E.fmsm_solve(p, cells)
+        b = O.oracle_solve(p, "fmsm", cells)
+        assert bitwise(a.values, b.u), (cx, cy)
+        assert (a.sweeps, a.node_updates, a.heap_removals) == \
+            (b.sweeps, b.node_updates, b.heap_removals), (cx, cy)
+
+
+def test_fmsm_rejects_degenerate_decompositions():
+    # test_fmsm.cpp:99-103
+    p = E.build_problem(E.Grid.unit_square(16), E.speed_constant(), E.ExitSpec.point_source((0.5, 0.5)))
+    with pytest.raises(E.ConfigError):
+        E.fmsm_solve(p, E.build_cells(p.grid, 1, 1))
+    with pytest.raises(E.ConfigError):
+        E.fmsm_solve(p, E.build_cells(p.grid, 1, 4))
+
+
+def test_fmsm_exact_for_constant_speed():
+    # test_fmsm.cpp:128-136: FMSM within 1e-13 of FMM for constant speed
+    p = E.build_problem(E.Grid.unit_square(56), E.speed_constant(), E.ExitSpec.point_source((0.5, 0.5)))
+    exact = O.oracle_solve(p, "fmm").u
+    for c in (4, 7, 8):
+        out = E.fmsm_solve(p, E.build_cells(p.grid, c, c))
+        rel = np.abs(out.values - exact) / np.maximum(np.abs(exact), 1e-300)
+        assert float(rel.max()) < 1e-13
