@@ -231,6 +231,10 @@ int plan_run(eik_plan* P, eik_output* out) {
     case EIK_FMSM:
       rc = plan_run_fmsm(P, out);
       break;
+    case EIK_HCM:
+    case EIK_FHCM:
+      rc = plan_run_heapcell(P, out);
+      break;
     default:
       return fail(EIK_ERR_NOT_IMPL, "method not implemented on the device path");
   }

@@ -58,6 +58,32 @@ struct FmsmArgs {
 
 cudaError_t launch_fmsm(const FmsmArgs& a, int warps_per_cta, cudaStream_t s, int* launches);
 
+struct HcArgs {
+  CellGeom g;
+  const double* C;          // padded h/F
+  double* u;                // padded values
+  const double* probe[4];   // F at border probe points: W/E [cells_x*n], S/N [cells_y*m]
+  double h, hc_x, hc_y;
+  double* cell_value;       // [J] heap keys (cell values)
+  uint8_t* flags;           // [J] raised sweep directions
+  uint8_t* first_done;      // [J]
+  double* hkey;             // heap storage
+  int* hpos;
+  int* harr;
+  const int* init_cells;    // Q-cells in ascending id order with their initial values
+  const double* init_values;
+  int n_init;
+  unsigned long long* counters;  // removals, sweeps, node updates, mon checks, mon single
+  int* status;
+  int J;
+  int fast;                 // 0 = HCM, 1 = FHCM
+  long long budget;         // removal budget 100*J+16 (heap_cell.cpp:270)
+  int max_len;              // longest cell side
+};
+
+size_t heapcell_smem_bytes(const CellGeom& g, int max_len);
+cudaError_t launch_heapcell(const HcArgs& a, cudaStream_t s, int* launches);
+
 cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int64_t n,
                            int64_t P, int64_t pad, double h, const int64_t* exits,
                            const double* cost, int64_t n_exit, int* status, cudaStream_t s,

@@ -51,6 +51,17 @@ struct eik_plan {
   int* dCellDone = nullptr;
   int* dNext = nullptr;
   unsigned long long* dCounters = nullptr;
+  // heap-cell state
+  double* dProbe[4] = {nullptr, nullptr, nullptr, nullptr};
+  double* dCellValue = nullptr;
+  uint8_t* dHcFlags = nullptr;
+  uint8_t* dFirstDone = nullptr;
+  double* dHKey = nullptr;
+  int* dHPos = nullptr;
+  int* dHArr = nullptr;
+  int* dInitCells = nullptr;
+  double* dInitValues = nullptr;
+  int max_len = 0;
 };
 
 namespace eikb200 {
@@ -74,5 +85,6 @@ int dalloc(T** p, size_t count) {
 
 int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c);
 int plan_run_fmsm(eik_plan* P, eik_output* out);
+int plan_run_heapcell(eik_plan* P, eik_output* out);
 
 }  // namespace eikb200

@@ -74,6 +74,37 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
   P->warps_per_cta = (int)std::max<size_t>(1, std::min<size_t>(8, kTileBudget / tile_bytes));
 
   int rc;
+  if (P->method == EIK_HCM || P->method == EIK_FHCM) {
+    P->max_len = std::max(g.max_w, g.max_h);
+    const size_t smem = heapcell_smem_bytes(g, P->max_len);
+    if (smem > 227 * 1024)
+      return fail(EIK_ERR_NOT_IMPL, "cell too large for the shared-memory tile (max ~110x110 nodes)");
+    for (int s = 0; s < 4; ++s) {
+      if ((rc = dalloc(&P->dProbe[s], P->probe[s].size()))) return rc;
+      P->allocs.push_back(P->dProbe[s]);
+      CK(cudaMemcpyAsync(P->dProbe[s], P->probe[s].data(), sizeof(double) * P->probe[s].size(),
+                         cudaMemcpyHostToDevice, P->stream));
+    }
+    if ((rc = dalloc(&P->dCellValue, J))) return rc;
+    P->allocs.push_back(P->dCellValue);
+    if ((rc = dalloc(&P->dHcFlags, J))) return rc;
+    P->allocs.push_back(P->dHcFlags);
+    if ((rc = dalloc(&P->dFirstDone, J))) return rc;
+    P->allocs.push_back(P->dFirstDone);
+    if ((rc = dalloc(&P->dHKey, J))) return rc;
+    P->allocs.push_back(P->dHKey);
+    if ((rc = dalloc(&P->dHPos, J))) return rc;
+    P->allocs.push_back(P->dHPos);
+    if ((rc = dalloc(&P->dHArr, J))) return rc;
+    P->allocs.push_back(P->dHArr);
+    if ((rc = dalloc(&P->dInitCells, J))) return rc;
+    P->allocs.push_back(P->dInitCells);
+    if ((rc = dalloc(&P->dInitValues, J))) return rc;
+    P->allocs.push_back(P->dInitValues);
+    if ((rc = dalloc(&P->dCounters, 8))) return rc;
+    P->allocs.push_back(P->dCounters);
+    return EIK_OK;
+  }
   if ((rc = dalloc(&P->dOrder, J))) return rc;
   P->allocs.push_back(P->dOrder);
   if ((rc = dalloc(&P->dRank, J))) return rc;
@@ -171,6 +202,104 @@ int plan_run_fmsm(eik_plan* P, eik_output* out) {
   out->avs = (double)out->sweeps / (double)J;
   out->device_ms = ms;
   out->host_ms = host_ms;
+  out->kernel_launches = launches;
+  return EIK_OK;
+}
+
+int plan_run_heapcell(eik_plan* P, eik_output* out) {
+  const int64_t J = (int64_t)P->cells_x * P->cells_y;
+  // Cells intersecting the exit set start on the list with value = max exit
+  // cost inside the cell (heap_cell.cpp:255-268); O(|Q|) host work.
+  std::vector<int64_t> ib, ie, jb, je;
+  split_axis(P->g.m, P->cells_x, ib, ie);
+  split_axis(P->g.n, P->cells_y, jb, je);
+  std::vector<std::pair<int, double>> init;
+  {
+    std::vector<double> cv;
+    std::vector<int> touched;
+    std::vector<char> seen;
+    const int64_t m = P->g.m;
+    for (size_t k = 0; k < P->exit_nodes.size(); ++k) {
+      const int64_t i = P->exit_nodes[k] % m, j = P->exit_nodes[k] / m;
+      const int64_t a = std::upper_bound(ie.begin(), ie.end(), i) - ie.begin();
+      const int64_t b = std::upper_bound(je.begin(), je.end(), j) - je.begin();
+      const int cell = (int)(b * P->cells_x + a);
+      const double q = P->exit_cost[k];
+      bool found = false;
+      for (auto& pr : init)
+        if (pr.first == cell) {
+          pr.second = std::max(pr.second, q);
+          found = true;
+          break;
+        }
+      if (!found) init.push_back({cell, q});
+    }
+    std::sort(init.begin(), init.end(),
+              [](const std::pair<int, double>& x, const std::pair<int, double>& y) {
+                return x.first < y.first;
+              });
+  }
+  std::vector<int> icells(init.size());
+  std::vector<double> ivals(init.size());
+  for (size_t k = 0; k < init.size(); ++k) {
+    icells[k] = init[k].first;
+    ivals[k] = init[k].second;
+  }
+  int launches = 0;
+  CK(cudaEventRecord(P->ev0, P->stream));
+  CK(cudaMemcpyAsync(P->dInitCells, icells.data(), sizeof(int) * icells.size(),
+                     cudaMemcpyHostToDevice, P->stream));
+  CK(cudaMemcpyAsync(P->dInitValues, ivals.data(), sizeof(double) * ivals.size(),
+                     cudaMemcpyHostToDevice, P->stream));
+  CK(cudaMemsetAsync(P->dCounters, 0, sizeof(unsigned long long) * 8, P->stream));
+  CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
+                    P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
+  HcArgs a;
+  a.g = P->cg;
+  a.C = P->dC;
+  a.u = P->dU;
+  for (int s = 0; s < 4; ++s) a.probe[s] = P->dProbe[s];
+  a.h = P->g.h;
+  a.hc_x = (double)(P->g.m / P->cells_x) * P->g.h;  // cells.cpp:44-45
+  a.hc_y = (double)(P->g.n / P->cells_y) * P->g.h;
+  a.cell_value = P->dCellValue;
+  a.flags = P->dHcFlags;
+  a.first_done = P->dFirstDone;
+  a.hkey = P->dHKey;
+  a.hpos = P->dHPos;
+  a.harr = P->dHArr;
+  a.init_cells = P->dInitCells;
+  a.init_values = P->dInitValues;
+  a.n_init = (int)icells.size();
+  a.counters = P->dCounters;
+  a.status = P->dStatus;
+  a.J = (int)J;
+  a.fast = P->method == EIK_FHCM ? 1 : 0;
+  a.budget = 100LL * J + 16;
+  a.max_len = P->max_len;
+  CK(launch_heapcell(a, P->stream, &launches));
+  CK(cudaEventRecord(P->ev1, P->stream));
+  int st[8];
+  unsigned long long cnt[5];
+  CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
+  CK(cudaMemcpyAsync(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost, P->stream));
+  CK(cudaStreamSynchronize(P->stream));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  if (st[0] == 3) return fail(EIK_ERR_BUDGET, "heap-cell removal budget exceeded");
+  // SolverOutput / HybridStats (heap_cell.cpp:314-322)
+  out->heap_removals = (int64_t)cnt[0];
+  out->sweeps = (int64_t)cnt[1];
+  out->node_updates = (int64_t)cnt[2];
+  out->mon_checks = (int64_t)cnt[3];
+  out->mon_single = (int64_t)cnt[4];
+  out->cell_removals = out->heap_removals;
+  out->cell_sweeps = out->sweeps;
+  out->avhr = (double)out->heap_removals / (double)J;
+  out->avs = (double)out->sweeps / (double)J;
+  out->mon_pct = out->mon_checks == 0 ? 0.0 : 100.0 * out->mon_single / (double)out->mon_checks;
+  out->device_ms = ms;
   out->kernel_launches = launches;
   return EIK_OK;
 }

@@ -117,3 +117,93 @@ def test_fmsm_exact_for_constant_speed():
         out = E.fmsm_solve(p, E.build_cells(p.grid, c, c))
         rel = np.abs(out.values - exact) / np.maximum(np.abs(exact), 1e-300)
         assert float(rel.max()) < 1e-13
+
+
+# ---- heap-cell methods (exact device replay of heap_cell.cpp) ---------------
+
+@pytest.mark.parametrize("cid,make,cells", SMALL_CASES, ids=[c[0] for c in SMALL_CASES])
+def test_hcm_fhcm_small_golden_fields(cid, make, cells):
+    arrays, meta = _small()
+    p = make()
+    for c in cells:
+        for method in ("hcm", "fhcm"):
+            key = f"{cid}/{method}/{c}"
+            out = E.solve(p, method, E.build_cells(p.grid, c, c))
+            assert bitwise(out.values, arrays[key]), key
+            m = meta[key]
+            assert (out.sweeps, out.node_updates, out.heap_removals, out.hybrid.mon_checks,
+                    out.hybrid.mon_single) == (m["sweeps"], m["node_updates"], m["heap_removals"],
+                                               m["mon_checks"], m["mon_single"]), key
+
+
+@pytest.mark.parametrize("method", ["hcm", "fhcm"])
+@pytest.mark.parametrize("cs", [8, 16, 32, 64])
+def test_heapcell_c2_bitwise_full_size(method, cs):
+    big = _big()[f"c2/{method}/{cs}"]
+    p = configs.config2().problem
+    out = E.solve(p, method, E.build_cells(p.grid, big["cells"], big["cells"]))
+    assert sha(out.values) == big["sha256"]
+    assert (out.sweeps, out.node_updates, out.heap_removals, out.hybrid.mon_checks,
+            out.hybrid.mon_single) == (big["sweeps"], big["node_updates"], big["heap_removals"],
+                                       big["mon_checks"], big["mon_single"])
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_heapcell_random_against_oracle(seed):
+    rng = np.random.default_rng(300 + seed)
+    m, n = int(rng.integers(10, 120)), int(rng.integers(10, 120))
+    g = E.Grid(m, n, float(rng.uniform(0.002, 0.05)), 0.2, -0.4)
+    F = rng.uniform(0.05, 3.0, size=(n, m))
+    sp = lambda x, y, F=F, g=g: F[np.clip(np.rint((y - g.y0) / g.h).astype(int), 0, g.n - 1),  # noqa: E731
+                                  np.clip(np.rint((x - g.x0) / g.h).astype(int), 0, g.m - 1)]
+    k = int(rng.integers(1, 6))
+    ex = E.ExitSpec.node_set([(int(rng.integers(0, m)), int(rng.integers(0, n))) for _ in range(k)],
+                             list(rng.uniform(0, 0.1, size=k)))
+    p = E.build_problem(g, sp, ex)
+    for cx, cy in [(1, 1), (2, 3), (int(rng.integers(2, 10)), int(rng.integers(2, 10)))]:
+        cells = E.build_cells(g, cx, cy)
+        for method in ("hcm", "fhcm"):
+            a = E.solve(p, method, cells)
+            b = O.oracle_solve(p, method, cells)
+            assert bitwise(a.values, b.u), (method, cx, cy)
+            assert (a.sweeps, a.node_updates, a.heap_removals, a.hybrid.mon_checks,
+                    a.hybrid.mon_single) == (b.sweeps, b.node_updates, b.heap_removals,
+                                             b.mon_checks, b.mon_single), (method, cx, cy)
+
+
+def test_hcm_single_cell_is_lsm():
+    # test_heap_cell.cpp:80-90: one cell -> HCM == LSM bit for bit, incl. counters
+    p = E.build_problem(E.Grid.unit_square(33), E.speed_checkerboard(11),
+                        E.ExitSpec.point_source((0.5, 0.5)))
+    out = E.hcm_solve(p, E.build_cells(p.grid, 1, 1))
+    lsm = O.oracle_solve(p, "lsm")
+    assert out.heap_removals == 1 and out.hybrid.avhr == 1.0
+    assert (out.sweeps, out.node_updates) == (lsm.sweeps, lsm.node_updates)
+    assert bitwise(out.values, lsm.u)
+
+
+def test_fhcm_exact_for_constant_speed():
+    # test_heap_cell.cpp:142-151
+    p = E.build_problem(E.Grid.unit_square(56), E.speed_constant(), E.ExitSpec.point_source((0.5, 0.5)))
+    exact = O.oracle_solve(p, "fmm").u
+    for c in (4, 8):
+        out = E.fhcm_solve(p, E.build_cells(p.grid, c, c))
+        rel = np.abs(out.values - exact) / np.maximum(np.abs(exact), 1e-300)
+        assert float(rel.max()) < 1e-13
+        assert out.hybrid.mon_pct == 100.0 and out.hybrid.avhr == 1.0
+
+
+def test_heapcell_all_exit_and_first_removal():
+    # test_heap_cell.cpp:153-185
+    ex = E.ExitSpec.node_set([(i, j) for j in range(8) for i in range(8)])
+    p = E.build_problem(E.Grid.unit_square(8), E.speed_constant(), ex)
+    out = E.hcm_solve(p, E.build_cells(p.grid, 2, 2))
+    assert out.node_updates == 0 and np.all(out.values == 0.0)
+    ex = E.ExitSpec.node_set([(i, j) for j in range(4) for i in range(4)])
+    p = E.build_problem(E.Grid.unit_square(8), E.speed_constant(), ex)
+    exact = O.oracle_solve(p, "fmm").u
+    for method in ("hcm", "fhcm"):
+        out = E.solve(p, method, E.build_cells(p.grid, 2, 2))
+        assert np.all(np.isfinite(out.values))
+    out = E.hcm_solve(p, E.build_cells(p.grid, 2, 2))
+    assert float(np.max(np.abs(out.values - exact) / np.maximum(exact, 1e-300))) < 1e-12
