@@ -1,0 +1,331 @@
+"""Benchmark: converged fine-grid points/s on BASELINE config 2 (2049^2,
+F = 1 + 0.5 sin(20 pi x) sin(20 pi y), centre source), the full method matrix
+of BASELINE.json: fmm, fsm, and fmsm / hcm / fhcm at 8, 16, 32, 64-point cells.
+
+One step = one solve of every method-config in the matrix.  `value` is the
+whole-job throughput (sum of grid points converged / sum of solve times) with
+the speed field already resident in HBM; `e2e` is the same metric through the
+public API with pinned host buffers (H2D of F and tables, D2H of u inside the
+timed region).  Prints one JSON line (rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CELL_SIZES = [8, 16, 32, 64]
+METHODS = ["fmm", "fsm", "fmsm", "hcm", "fhcm"]
+
+
+def matrix(cfg):
+    rows = [("fmm", 0), ("fsm", 0)]
+    for cs in CELL_SIZES:
+        for meth in ("fmsm", "hcm", "fhcm"):
+            rows.append((meth, cs))
+    return rows
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                         text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def run_reference(args):
+    """Reference arm: the unmodified reference (oracle/_ref, built from
+    /root/reference) on the host cores, one method-config per thread (the
+    reference's own --jobs model, experiment.cpp:284-310)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import oracle as O
+    from paper_1110_6220_b200 import configs
+    if not O.have_ref():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libeikref.so not built"}))
+        return
+    cfg = configs.config2()
+    p = cfg.problem
+    M = p.grid.size()
+    rows = matrix(cfg)
+    cores = os.cpu_count() or 1
+
+    def one(row):
+        meth, cs = row
+        cx = p.grid.m // cs if cs else 0
+        return O.ref_solve(p, meth, cx, cx).elapsed_ms
+
+    times = []
+    per = {}
+    for step in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        with ThreadPoolExecutor(max_workers=min(cores, len(rows))) as ex:
+            ms = list(ex.map(one, rows))
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+            for r, t in zip(rows, ms):
+                per.setdefault(f"{r[0]}" + (f"/{r[1]}" if r[1] else ""), []).append(t)
+    step_s = statistics.mean(times)
+    value = len(rows) * M / step_s
+    out = {
+        "impl": "reference", "metric": "converged fine-grid points/s", "value": value,
+        "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config 2)",
+        "config": {"workload": "c2_sinusoid_2049_method_matrix", "grid": 2049,
+                   "methods": METHODS, "cell_sizes": CELL_SIZES},
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": min(cores, len(rows)),
+                         "kind": "reference",
+                         "sample": f"the full {len(rows)}-solve C2 matrix per step, one solve per "
+                                   f"thread (reference solves are single-threaded)"},
+        "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "per_solve_ms": {k: statistics.mean(v) for k, v in per.items()},
+    }
+    print(json.dumps(out))
+
+
+def cpu_baseline_single_core():
+    """Single-core reference timing on a bounded sample: one solve of every
+    method-config of the matrix except FSM, plus FSM (13 s) -- ~20 s."""
+    from oracle import oracle as O
+    from paper_1110_6220_b200 import configs
+    if not O.have_ref():
+        return None
+    p = configs.config2().problem
+    rows = matrix(None)
+    tot = 0.0
+    for meth, cs in rows:
+        cx = p.grid.m // cs if cs else 0
+        tot += O.ref_solve(p, meth, cx, cx).elapsed_ms
+    return {"value": len(rows) * p.grid.size() / (tot / 1e3), "unit": "points/s", "cores": 1,
+            "kind": "reference",
+            "sample": f"one pass of the {len(rows)}-solve C2 matrix on 1 core "
+                      f"({tot / 1e3:.1f} s, solver call only as experiment.cpp:204-213)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    rank, world, local = dist_env()
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    import paper_1110_6220_b200 as E
+    from paper_1110_6220_b200 import configs
+
+    # Weak scaling: every rank solves its own replica of the C2 matrix (the
+    # method matrix does not shard; SURVEY.md §8e -- row strips are for C5).
+    cfg = configs.config2()
+    p = cfg.problem
+    g = p.grid
+    M = g.size()
+    rows = matrix(cfg)
+    plans = {}
+    tables = {}
+    for meth, cs in rows:
+        cells = E.build_cells(g, g.m // cs, g.m // cs) if cs else None
+        if cells is not None and cs not in tables:
+            tables[cs] = E.cell_tables(p, cells)
+        plans[(meth, cs)] = (E.Plan(p, meth, cells, tables.get(cs)), cells)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def flush_l2():
+        flush.zero_()
+        torch.cuda.synchronize()
+
+    def step(timed):
+        tot_ms, launches, per = 0.0, 0, {}
+        for (meth, cs), (plan, _) in plans.items():
+            flush_l2()  # inputs < L2 (126 MB): flush between timed solves
+            o = plan.run()
+            t = o.device_ms + o.host_ms
+            tot_ms += t
+            launches += o.kernel_launches
+            per[f"{meth}" + (f"/{cs}" if cs else "")] = (t, o)
+        return tot_ms, launches, per
+
+    for _ in range(args.warmup):
+        step(False)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    step_ms, launches, per_all = [], 0, {}
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            ms, L, per = step(True)
+            step_ms.append(ms)
+            launches += L
+            for k, (t, o) in per.items():
+                per_all.setdefault(k, []).append((t, o))
+    torch.cuda.synchronize()
+    mean_ms = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([mean_ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        mean_ms = float(t.item())
+    value = world * len(rows) * M / (mean_ms / 1e3)
+
+    # per-method table with the reference's counters beside ours
+    with open(os.path.join(ROOT, "tests", "golden", "big.json")) as f:
+        gold = json.load(f)
+    methods = {}
+    hbm, peak_kind = peaks()
+    best = None
+    for k, lst in per_all.items():
+        t = statistics.mean(x[0] for x in lst)
+        o = lst[-1][1]
+        meth = k.split("/")[0]
+        cs = int(k.split("/")[1]) if "/" in k else 0
+        ref = gold.get(f"c2/{k}", {})
+        if meth in ("fsm", "fmm"):
+            nbytes = 24.0 * M * o.sweeps  # 24 B per node per sweep
+        else:
+            nbytes = (24.0 * cs * cs + 32.0 * cs) * (o.heap_removals if meth != "fmsm"
+                                                      else (g.m // cs) ** 2)
+        ach = nbytes / (t / 1e3) / 1e9
+        methods[k] = {"ms": round(t, 3), "points_per_s": M / (t / 1e3), "sweeps": o.sweeps,
+                      "ref_sweeps": ref.get("sweeps"), "heap_removals": o.heap_removals,
+                      "ref_heap_removals": ref.get("heap_removals"),
+                      "node_updates": o.node_updates, "ref_node_updates": ref.get("node_updates"),
+                      "host_ms": round(o.host_ms, 3), "algorithmic_GBps": round(ach, 2),
+                      "ref_cpu_ms": ref.get("ms")}
+        if best is None or t > best[1]:
+            best = (k, t, nbytes, ach)
+    dom_k, dom_t, dom_bytes, dom_ach = best
+    roofline = {"bound": "hbm", "kernel": dom_k, "achieved": round(dom_ach, 2), "peak": hbm,
+                "unit": "GB/s", "frac": dom_ach / hbm, "traffic": None, "peak_kind": peak_kind,
+                "note": "latency-bound fp64 dependency chains; algorithmic bytes per SURVEY §8(d)"}
+
+    # e2e: public API, pinned host buffers, H2D + solve + D2H inside the timed region
+    pinned_F = torch.empty(M, dtype=torch.float64, pin_memory=True).numpy()
+    pinned_F[:] = p.sampled_speed()
+    pinned_u = torch.empty(M, dtype=torch.float64, pin_memory=True).numpy()
+    p_pin = E.Problem(g, p.speed, p.exit_nodes, p.exit_cost, p.exit_points, p.exit_point_cost,
+                      _F=pinned_F)
+    e2e_s, h2d, d2h = 0.0, 0, 0
+    for meth, cs in rows:
+        cells = E.build_cells(g, g.m // cs, g.m // cs) if cs else None
+        flush_l2()
+        t0 = time.perf_counter()
+        E.solve(p_pin, meth, cells, tables.get(cs), out=pinned_u)
+        e2e_s += time.perf_counter() - t0
+        h2d += 8 * M + 16 * len(p.exit_nodes)
+        if cs:
+            tb = tables[cs]
+            h2d += 8 * sum(len(a) for a in (tb.probe_w, tb.probe_e, tb.probe_s, tb.probe_n, tb.center))
+        d2h += 8 * M
+
+    cpu = None if args.no_cpu_baseline or rank != 0 else cpu_baseline_single_core()
+    if rank == 0:
+        out = {
+            "metric": "converged fine-grid points/s", "value": value, "unit": "points/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, BASELINE config 2)",
+            "config": {"workload": "c2_sinusoid_2049_method_matrix", "grid": 2049,
+                       "methods": METHODS, "cell_sizes": CELL_SIZES,
+                       "parallelism": f"replicas x{world}",
+                       "l2": "256 MB flush before every solve (inputs < L2)"},
+            "e2e": {"value": world * len(rows) * M / e2e_s, "unit": "points/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches,
+            "clocks": clk.summary(), "methods": methods,
+        }
+        print(json.dumps(out))
+    for plan, _ in plans.values():
+        plan.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -100,6 +100,9 @@ typedef struct eik_output {
   double device_ms;     /* CUDA-event time of the device solve proper */
   double host_ms;       /* host part of the solve (FMSM Part I), else 0 */
   int64_t kernel_launches; /* kernels this call launched (evidence) */
+  /* HCM/FHCM speculative replay: pops whose worker result was valid at
+   * commit, pops that waited on a worker, pops processed by the committer */
+  int64_t spec_hits, spec_waits, spec_self;
 } eik_output;
 
 /* One solve.  `cells` may be NULL for FMM/FSM.  Thread-safe: each call owns

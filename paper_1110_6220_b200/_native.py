@@ -51,7 +51,8 @@ class eik_output(C.Structure):
                 ("cell_sweeps", C.c_int64), ("mon_checks", C.c_int64),
                 ("mon_single", C.c_int64), ("avhr", C.c_double), ("avs", C.c_double),
                 ("mon_pct", C.c_double), ("device_ms", C.c_double), ("host_ms", C.c_double),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("spec_hits", C.c_int64),
+                ("spec_waits", C.c_int64), ("spec_self", C.c_int64)]
 
 
 class eik_field(C.Structure):

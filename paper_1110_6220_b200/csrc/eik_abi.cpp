@@ -221,6 +221,7 @@ int plan_run(eik_plan* P, eik_output* out) {
   out->cell_removals = out->cell_sweeps = out->mon_checks = out->mon_single = 0;
   out->avhr = out->avs = out->mon_pct = 0.0;
   out->host_ms = 0.0;
+  out->spec_hits = out->spec_waits = out->spec_self = 0;
   CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
   int rc;
   switch (P->method) {

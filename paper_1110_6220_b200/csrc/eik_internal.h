@@ -58,8 +58,27 @@ struct FmsmArgs {
 
 cudaError_t launch_fmsm(const FmsmArgs& a, int warps_per_cta, cudaStream_t s, int* launches);
 
+// Result of processing one cell (sweeps + the four border scans), produced by
+// a worker speculatively and applied by the committer.
+struct SpecRec {
+  double cand[4];
+  int sweeps, updates;
+  uint8_t add[4], fl[4], monc[4], mons[4];
+};
+
 struct HcArgs {
   CellGeom g;
+  double* slots;            // [2][J][max_h*max_w] per-cell value slots
+  int64_t cellsz;           // max_h * max_w
+  uint8_t* cur;             // [J] committed slot of each cell
+  int* version;             // [J] commits in {c} u N(c)
+  int* spec_ver;            // [J] version the spare slot / record was computed for
+  int* busy;                // [J] a warp is computing the spare slot
+  SpecRec* rec;             // [J]
+  int* done_flag;
+  int* hsize_pub;           // heap size, published for the workers
+  int window;               // workers speculate heap positions [0, window)
+  int64_t tile_doubles;     // per-warp smem
   const double* C;          // padded h/F
   double* u;                // padded values
   const double* probe[4];   // F at border probe points: W/E [cells_x*n], S/N [cells_y*m]
@@ -82,7 +101,8 @@ struct HcArgs {
 };
 
 size_t heapcell_smem_bytes(const CellGeom& g, int max_len);
-cudaError_t launch_heapcell(const HcArgs& a, cudaStream_t s, int* launches);
+cudaError_t launch_heapcell(const HcArgs& a, int warps_per_cta, int max_ctas, cudaStream_t s,
+                            int* launches);
 
 cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int64_t n,
                            int64_t P, int64_t pad, double h, const int64_t* exits,

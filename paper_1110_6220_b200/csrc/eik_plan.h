@@ -62,6 +62,15 @@ struct eik_plan {
   int* dInitCells = nullptr;
   double* dInitValues = nullptr;
   int max_len = 0;
+  double* dSlots = nullptr;
+  uint8_t* dCur = nullptr;
+  int* dVersion = nullptr;
+  int* dSpecVer = nullptr;
+  int* dBusy = nullptr;
+  eikb200::SpecRec* dRec = nullptr;
+  int* dHcMisc = nullptr;   // [0] done flag, [1] published heap size
+  int hc_warps_per_cta = 1;
+  int hc_max_ctas = 1;
 };
 
 namespace eikb200 {

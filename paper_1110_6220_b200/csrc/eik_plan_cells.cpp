@@ -2,6 +2,8 @@
 // host (as in the reference), uploads, and the device dataflow launch.
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -67,7 +69,9 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
   g.max_h = (int)(P->g.n - (c->cells_y - 1) * g.base_y);
   g.pu = even_up(g.max_w + 2);
   g.pc = even_up(g.max_w);
-  g.tile_doubles = (int64_t)(g.max_h + 2) * g.pu + (int64_t)g.max_h * g.pc;
+  g.tile_doubles = 2 * (int64_t)(g.max_h + 2) * g.pu;  // values + costs, both with halo
+  if (g.max_h > 32 * 4)
+    return fail(EIK_ERR_NOT_IMPL, "cells taller than 128 nodes are not supported by the warp engine");
   const size_t tile_bytes = (size_t)g.tile_doubles * sizeof(double);
   if (tile_bytes > kTileMax)
     return fail(EIK_ERR_NOT_IMPL, "cell too large for the shared-memory tile (max ~150x150 nodes)");
@@ -101,8 +105,30 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     P->allocs.push_back(P->dInitCells);
     if ((rc = dalloc(&P->dInitValues, J))) return rc;
     P->allocs.push_back(P->dInitValues);
-    if ((rc = dalloc(&P->dCounters, 8))) return rc;
+    if ((rc = dalloc(&P->dCounters, 16))) return rc;
     P->allocs.push_back(P->dCounters);
+    const size_t cellsz = (size_t)g.max_w * g.max_h;
+    if ((rc = dalloc(&P->dSlots, 2 * (size_t)J * cellsz))) return rc;
+    P->allocs.push_back(P->dSlots);
+    if ((rc = dalloc(&P->dCur, J))) return rc;
+    P->allocs.push_back(P->dCur);
+    if ((rc = dalloc(&P->dVersion, J))) return rc;
+    P->allocs.push_back(P->dVersion);
+    if ((rc = dalloc(&P->dSpecVer, J))) return rc;
+    P->allocs.push_back(P->dSpecVer);
+    if ((rc = dalloc(&P->dBusy, J))) return rc;
+    P->allocs.push_back(P->dBusy);
+    if ((rc = dalloc(&P->dRec, J))) return rc;
+    P->allocs.push_back(P->dRec);
+    if ((rc = dalloc(&P->dHcMisc, 4))) return rc;
+    P->allocs.push_back(P->dHcMisc);
+    // per-warp tile: values + costs with halo, 4 border snapshots, lock bytes
+    const size_t tile = (smem + sizeof(double) - 1) / sizeof(double);
+    P->cg.tile_doubles = (int64_t)tile;
+    P->hc_warps_per_cta = (int)std::max<size_t>(1, std::min<size_t>(8, kTileBudget / (tile * 8)));
+    // EIK_HC_WORKERS=0 runs the committer alone (serial exact replay)
+    P->hc_max_ctas = 1 << 20;
+    if (const char* w = std::getenv("EIK_HC_CTAS")) P->hc_max_ctas = std::max(1, std::atoi(w));
     return EIK_OK;
   }
   if ((rc = dalloc(&P->dOrder, J))) return rc;
@@ -251,7 +277,7 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
                      cudaMemcpyHostToDevice, P->stream));
   CK(cudaMemcpyAsync(P->dInitValues, ivals.data(), sizeof(double) * ivals.size(),
                      cudaMemcpyHostToDevice, P->stream));
-  CK(cudaMemsetAsync(P->dCounters, 0, sizeof(unsigned long long) * 8, P->stream));
+  CK(cudaMemsetAsync(P->dCounters, 0, sizeof(unsigned long long) * 16, P->stream));
   CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
                     P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
   HcArgs a;
@@ -277,10 +303,22 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
   a.fast = P->method == EIK_FHCM ? 1 : 0;
   a.budget = 100LL * J + 16;
   a.max_len = P->max_len;
-  CK(launch_heapcell(a, P->stream, &launches));
+  a.slots = P->dSlots;
+  a.cellsz = (int64_t)P->cg.max_w * P->cg.max_h;
+  a.cur = P->dCur;
+  a.version = P->dVersion;
+  a.spec_ver = P->dSpecVer;
+  a.busy = P->dBusy;
+  a.rec = P->dRec;
+  a.done_flag = P->dHcMisc;
+  a.hsize_pub = P->dHcMisc + 1;
+  a.window = 4096;
+  a.tile_doubles = P->cg.tile_doubles;
+  CK(cudaMemsetAsync(P->dHcMisc, 0, sizeof(int) * 4, P->stream));
+  CK(launch_heapcell(a, P->hc_warps_per_cta, P->hc_max_ctas, P->stream, &launches));
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];
-  unsigned long long cnt[5];
+  unsigned long long cnt[16];
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaMemcpyAsync(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaStreamSynchronize(P->stream));
@@ -288,6 +326,15 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
   if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
   if (st[0] == 3) return fail(EIK_ERR_BUDGET, "heap-cell removal budget exceeded");
+  if (st[0] == 4) return fail(EIK_ERR_CUDA, "heap-cell committer watchdog fired");
+  if (std::getenv("EIK_HC_PROFILE"))
+    std::fprintf(stderr,
+                 "heapcell committer cycles: pop %llu obtain %llu self %llu commit %llu | self: "
+                 "stage %llu sweeps %llu scans %llu\n",
+                 cnt[8], cnt[9], cnt[10], cnt[11], cnt[12], cnt[13], cnt[14]);
+  out->spec_self = (int64_t)cnt[5];
+  out->spec_hits = (int64_t)cnt[6];
+  out->spec_waits = (int64_t)cnt[7];
   // SolverOutput / HybridStats (heap_cell.cpp:314-322)
   out->heap_removals = (int64_t)cnt[0];
   out->sweeps = (int64_t)cnt[1];

@@ -3,11 +3,8 @@
 //
 // In-cell sweep (replaces the `full_sweep` lambda, /root/reference/proj/src/
 // fmsm.cpp:176-195): a warp stages one cell plus its one-node cross halo and
-// its costs C = h/F in shared memory, then sweeps the cell as an
-// anti-diagonal wavefront in the requested direction -- lane L owns sweep
-// rows L, L+32, ...; the nodes of one anti-diagonal are independent and
-// every node reads its two upwind neighbours from the previous diagonal, so
-// the result is bit-identical to the reference's row-by-row loop.
+// its costs C = h/F in shared memory and sweeps it with the register-pipeline
+// wavefront of k_cellsweep.cuh, bit-identical to the reference's row loop.
 //
 // FMSM Part II (fmsm.cpp:164-226): cells are claimed in the coarse order
 // (host Part I, eik_coarse.cpp); a claimed cell waits only for its
@@ -16,58 +13,12 @@
 // any schedule respecting those edges reproduces the sequential pass bit for
 // bit -- with far less waiting than level-synchronous batches.
 #include "eik_internal.h"
+#include "k_cellsweep.cuh"
 #include "k_common.cuh"
 
 namespace eikb200 {
 
 namespace {
-
-enum { SW = 0, NW = 1, NE = 2, SE = 3 };  // SweepDir (local_update.hpp:23)
-
-struct Tile {
-  double* U;        // (h+2) x pu, node (x,y) at (y+1)*pu + x+1
-  double* Ct;       // h x pc costs, -1 at exits
-  int pu, pc, w, h;
-};
-
-// One in-cell sweep.  MODE 0: node_update (local_update.hpp:48-51);
-// MODE 1: directional_update (local_update.hpp:55-64).  Returns the warp-wide
-// "some value decreased" flag.
-template <int MODE>
-__device__ bool tile_sweep(const Tile& T, int dir, int lane) {
-  const bool iasc = (dir == SW || dir == NW);
-  const bool jasc = (dir == SW || dir == SE);
-  bool changed = false;
-  const int nsteps = T.w + T.h - 1;
-  for (int s = 0; s < nsteps; ++s) {
-    for (int b = lane; b < T.h; b += 32) {
-      const int a = s - b;
-      if (a >= 0 && a < T.w) {
-        const int x = iasc ? a : T.w - 1 - a;
-        const int y = jasc ? b : T.h - 1 - b;
-        const double c = T.Ct[y * T.pc + x];
-        if (c > 0.0) {
-          double* p = T.U + (y + 1) * T.pu + (x + 1);
-          const double cur = *p;
-          double cand;
-          if (MODE == 0) {
-            cand = node_update4(p[1], p[-1], p[T.pu], p[-T.pu], c);
-          } else {
-            const double hx = (dir == NE || dir == SE) ? p[1] : p[-1];      // E or W
-            const double vy = (dir == NE || dir == NW) ? p[T.pu] : p[-T.pu];  // N or S
-            cand = quad_update(hx, vy, c);
-          }
-          if (cand < cur) {
-            *p = cand;
-            changed = true;
-          }
-        }
-      }
-    }
-    __syncwarp();
-  }
-  return __any_sync(kFull, changed);
-}
 
 __device__ __forceinline__ void cell_rect(const CellGeom& g, int cell, int64_t& ib, int64_t& ie,
                                           int64_t& jb, int64_t& je) {
@@ -88,34 +39,34 @@ __device__ __forceinline__ int cell_neighbor(const CellGeom& g, int cell, int si
   }
 }
 
-// Stage a cell and its cross halo (no corners) into the warp's tile; returns
-// the number of exit nodes in the cell.
+// Stage a cell, its cross halo (no corners) and the costs of both into the
+// warp's tile; returns the number of exit nodes in the cell.
 __device__ int stage_in(const CellGeom& g, const double* __restrict__ C, const double* u,
-                        int64_t ib, int64_t jb, Tile& T, int lane) {
+                        int64_t ib, int64_t jb, CellTile& T, int lane) {
   const int W2 = T.w + 2;
   const int tot = (T.h + 2) * W2;
+  int exits = 0;
   for (int k = lane; k < tot; k += 32) {
     const int y = k / W2 - 1, x = k % W2 - 1;
     const bool corner = (x < 0 || x >= T.w) && (y < 0 || y >= T.h);
     if (corner) continue;
     const int64_t gj = jb + y;
-    double v = kInf;
-    if (gj >= 0 && gj < g.n) v = __ldcg(u + gj * g.P + g.pad + ib + x);  // padding = +inf
+    double v = kInf, c = -1.0;
+    if (gj >= 0 && gj < g.n) {
+      const int64_t o = gj * g.P + g.pad + ib + x;  // padding columns: +inf / -1
+      v = __ldcg(u + o);
+      c = __ldg(C + o);
+    }
     T.U[(y + 1) * T.pu + (x + 1)] = v;
-  }
-  int exits = 0;
-  for (int k = lane; k < T.w * T.h; k += 32) {
-    const int y = k / T.w, x = k % T.w;
-    const double c = __ldg(C + (jb + y) * g.P + g.pad + ib + x);
-    T.Ct[y * T.pc + x] = c;
-    exits += (c < 0.0);
+    T.Ct[(y + 1) * T.pu + (x + 1)] = c;
+    if (x >= 0 && x < T.w && y >= 0 && y < T.h) exits += (c < 0.0);
   }
   __syncwarp();
   for (int o = 16; o > 0; o >>= 1) exits += __shfl_xor_sync(kFull, exits, o);
   return exits;
 }
 
-__device__ void stage_out(const CellGeom& g, double* u, int64_t ib, int64_t jb, const Tile& T,
+__device__ void stage_out(const CellGeom& g, double* u, int64_t ib, int64_t jb, const CellTile& T,
                           int lane) {
   for (int k = lane; k < T.w * T.h; k += 32) {
     const int y = k / T.w, x = k % T.w;
@@ -127,11 +78,11 @@ __global__ void fmsm_dataflow_kernel(FmsmArgs a) {
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  Tile T;
+  CellTile T;
   T.pu = a.g.pu;
-  T.pc = a.g.pc;
   T.U = smem + (size_t)wib * a.g.tile_doubles;
   T.Ct = T.U + (size_t)(a.g.max_h + 2) * a.g.pu;
+  T.lock = nullptr;
   long long my_sweeps = 0, my_updates = 0;
 
   for (;;) {
@@ -154,11 +105,12 @@ __global__ void fmsm_dataflow_kernel(FmsmArgs a) {
     const int exits = stage_in(a.g, a.C, a.u, ib, jb, T, lane);
     const int flags = a.flags[cell];
     int nsw = 0;
+    long long unused = 0;
     if (flags & 16) {
       // Q-cell: FSM to convergence with the halo frozen (fmsm.cpp:200-210)
       bool changed = true;
       while (changed) {
-        changed = tile_sweep<0>(T, nsw & 3, lane);
+        changed = cell_sweep<0>(T, nsw & 3, lane, unused);
         ++nsw;
         if (nsw > a.max_cell_sweeps) {
           if (lane == 0) atomicExch(a.status, 3);
@@ -167,11 +119,11 @@ __global__ void fmsm_dataflow_kernel(FmsmArgs a) {
       }
     } else {
       // one directional sweep per chosen direction, in NE, NW, SE, SW order
-      const int order[4] = {NE, NW, SE, SW};
+      const int order[4] = {kNE, kNW, kSE, kSW};
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         if (flags & (1 << order[k])) {
-          tile_sweep<1>(T, order[k], lane);
+          cell_sweep<1>(T, order[k], lane, unused);
           ++nsw;
         }
     }

@@ -1,0 +1,185 @@
+// In-cell sweep engine shared by FMSM (k_cells.cu) and HCM/FHCM
+// (k_heapcell.cu): one warp sweeps one cell held in shared memory.
+//
+// Register pipeline.  Lane t owns sweep rows t, t+32, ... ("slots") and at
+// step s processes column s-t-32r of slot r -- every node of one
+// anti-diagonal at once, each after its two upwind neighbours, exactly the
+// dependency order of the reference's row loop, so values and counters are
+// bit-identical.  On the critical path sit only a shuffle (the new value of
+// the upwind row) and the fp64 update; the old values, costs and lock bytes of
+// the next step are prefetched from shared memory while the current step
+// computes.  Lock propagation (heap_cell.cpp:113-122) into the next row goes
+// through a ballot, into the lane's own next column through a register, and
+// into already-processed neighbours (next sweep) through the lock bytes.
+#pragma once
+
+#include "k_common.cuh"
+
+namespace eikb200 {
+
+enum { kSW = 0, kNW = 1, kNE = 2, kSE = 3 };  // SweepDir (local_update.hpp:23)
+constexpr int kMaxSlots = 4;                   // cells up to 128 rows
+
+struct CellTile {
+  double* U;        // (h+2) x pu values with cross halo, node (x,y) at (y+1)*pu + x+1
+  double* Ct;       // (h+2) x pu costs with halo; < 0 marks exits (and off-grid halo)
+  uint8_t* lock;    // h x w lock bytes (1 = unlocked), locked sweeps only
+  int pu, w, h;
+};
+
+// MODE 0: node_update over all non-exit nodes (FSM inside a cell,
+//         fmsm.cpp:200-210); MODE 1: directional_update with the two upwind
+//         neighbours (fmsm.cpp:211-221); MODE 2: locking sweep
+//         (heap_cell.cpp:98-126).
+// Returns the warp-wide "some value decreased" flag and adds this lane's
+// processed nodes to `updates` (MODE 2 counts unlocked nodes only).
+template <int MODE, int NS>
+__device__ bool cell_sweep_ns(const CellTile& T, int dir, int lane, long long& updates_out) {
+  int updates = 0;
+  const bool iasc = (dir == kSW || dir == kNW);
+  const bool jasc = (dir == kSW || dir == kSE);
+  const int dx = iasc ? 1 : -1;           // next column in sweep order
+  const int dyp = jasc ? T.pu : -T.pu;    // next row in sweep order (value pitch)
+  const int dyl = jasc ? T.w : -T.w;      // next row in sweep order (lock pitch)
+  const int w = T.w, h = T.h;
+  const int x0 = iasc ? 0 : w - 1;        // column of sweep step a = 0
+
+  int vbase[NS];             // value offset of (a = 0) for this lane's row
+  int lbase[NS];             // lock offset of (a = 0)
+  bool rvalid[NS];
+  double res_prev[NS];       // own new value at the previous column (W)
+  double c_prev[NS];         // own cost at the previous column
+  bool unW[NS];              // W neighbour unlocked us for this sweep
+  unsigned nmask[NS];        // ballot of "unlock my N neighbour" at the last step
+  double cur[NS], eo[NS], no[NS], cc[NS], hs[NS], ce[NS], cn[NS], cs[NS];
+  uint8_t lk[NS];
+
+#pragma unroll
+  for (int r = 0; r < NS; ++r) {
+    const int b = lane + 32 * r;
+    rvalid[r] = b < h;
+    const int y = jasc ? b : h - 1 - b;
+    vbase[r] = rvalid[r] ? (y + 1) * T.pu + (x0 + 1) : 0;
+    lbase[r] = rvalid[r] ? y * w + x0 : 0;
+    res_prev[r] = rvalid[r] ? T.U[vbase[r] - dx] : kInf;  // frozen halo column
+    c_prev[r] = -1.0;
+    unW[r] = false;
+    nmask[r] = 0u;
+  }
+
+  auto load_step = [&](int s) {
+#pragma unroll
+    for (int r = 0; r < NS; ++r) {
+      const int a = s - lane - 32 * r;
+      const bool act = rvalid[r] && a >= 0 && a < w;
+      const int o = act ? vbase[r] + dx * a : T.pu + 1;  // a safe in-tile offset
+      cur[r] = act ? T.U[o] : kInf;
+      eo[r] = act ? T.U[o + dx] : kInf;   // old E (halo at the last column)
+      no[r] = act ? T.U[o + dyp] : kInf;  // old N (halo on the last row)
+      hs[r] = act ? T.U[o - dyp] : kInf;  // S -- only used when it is the halo
+      cc[r] = act ? T.Ct[o] : -1.0;
+      if (MODE == 2) {
+        ce[r] = (act && a + 1 < w) ? T.Ct[o + dx] : -1.0;
+        cn[r] = act ? T.Ct[o + dyp] : -1.0;
+        cs[r] = act ? T.Ct[o - dyp] : -1.0;
+        lk[r] = act ? T.lock[lbase[r] + dx * a] : (uint8_t)0;
+      }
+    }
+  };
+
+  bool changed = false;
+  const int last = (h - 1) + (w - 1);
+  load_step(0);
+  for (int s = 0; s <= last; ++s) {
+    double c_cur[NS], c_e[NS], c_n[NS], c_cc[NS], c_hs[NS], c_ce[NS], c_cn[NS], c_cs[NS];
+    uint8_t c_lk[NS];
+#pragma unroll
+    for (int r = 0; r < NS; ++r) {
+      c_cur[r] = cur[r];
+      c_e[r] = eo[r];
+      c_n[r] = no[r];
+      c_cc[r] = cc[r];
+      c_hs[r] = hs[r];
+      c_ce[r] = ce[r];
+      c_cn[r] = cn[r];
+      c_cs[r] = cs[r];
+      c_lk[r] = lk[r];
+    }
+    if (s < last) load_step(s + 1);  // prefetch while this step computes
+    // previous-step results of every slot: slot r's lane 0 reads slot r-1's
+    // lane 31, which this step's iteration r-1 is about to overwrite
+    double rp_old[NS];
+    unsigned nm_old[NS];
+#pragma unroll
+    for (int r = 0; r < NS; ++r) {
+      rp_old[r] = res_prev[r];
+      nm_old[r] = nmask[r];
+    }
+#pragma unroll
+    for (int r = 0; r < NS; ++r) {
+      const int b = lane + 32 * r;
+      const int a = s - b;
+      const bool act = rvalid[r] && a >= 0 && a < w;
+      // new value of the upwind row: lane-1 of this slot, lane 31 of the
+      // previous slot for lane 0, the frozen halo for sweep row 0
+      const double send = (lane == 31 && r > 0) ? rp_old[r > 0 ? r - 1 : 0] : rp_old[r];
+      double sv = __shfl_sync(kFull, send, (lane + 31) & 31);
+      unsigned sbit = 0u;
+      if (MODE == 2) {
+        if (lane == 0) sbit = (r > 0) ? (nm_old[r > 0 ? r - 1 : 0] >> 31) & 1u : 0u;
+        else sbit = (nm_old[r] >> (lane - 1)) & 1u;
+      }
+      if (b == 0) {
+        sv = c_hs[r];
+        sbit = 0u;
+      }
+      const double wv = res_prev[r];
+      double res = c_cur[r];
+      bool un_n = false, proc = false;
+      // Branchy on purpose: a slot/step whose lanes are all inactive or locked
+      // skips the fp64 chain (measured faster than predicating it away).
+      if (act && c_cc[r] >= 0.0) {
+        proc = (MODE != 2) || c_lk[r] || unW[r] || sbit;
+        if (proc) {
+          const double cand = (MODE == 1) ? quad_update(wv, sv, c_cc[r])
+                                          : node_update4(c_e[r], wv, c_n[r], sv, c_cc[r]);
+          ++updates;
+          if (cand < res) {
+            res = cand;
+            changed = true;
+            T.U[vbase[r] + dx * a] = res;
+            if (MODE == 2) {
+              uint8_t* lp = T.lock + lbase[r] + dx * a;
+              // already-processed W and S neighbours: unlocked for the next sweep
+              if (a > 0 && c_prev[r] >= 0.0 && wv > cand) lp[-dx] = 1;
+              if (b > 0 && c_cs[r] >= 0.0 && sv > cand) lp[-dyl] = 1;
+              un_n = (b + 1 < h) && c_cn[r] >= 0.0 && c_n[r] > cand;
+            }
+          }
+          // relock on processing (heap_cell.cpp:110-111)
+          if (MODE == 2) T.lock[lbase[r] + dx * a] = 0;
+        }
+      }
+      if (MODE == 2) {
+        const bool dec = proc && res < c_cur[r];
+        unW[r] = dec && (a + 1 < w) && c_ce[r] >= 0.0 && c_e[r] > res;
+        nmask[r] = __ballot_sync(kFull, un_n);
+      }
+      c_prev[r] = act ? c_cc[r] : -1.0;
+      if (act) res_prev[r] = res;
+    }
+    __syncwarp();
+  }
+  updates_out += updates;
+  return __any_sync(kFull, changed);
+}
+
+template <int MODE>
+__device__ bool cell_sweep(const CellTile& T, int dir, int lane, long long& updates) {
+  if (T.h <= 32) return cell_sweep_ns<MODE, 1>(T, dir, lane, updates);
+  if (T.h <= 64) return cell_sweep_ns<MODE, 2>(T, dir, lane, updates);
+  if (T.h <= 96) return cell_sweep_ns<MODE, 3>(T, dir, lane, updates);
+  return cell_sweep_ns<MODE, 4>(T, dir, lane, updates);
+}
+
+}  // namespace eikb200

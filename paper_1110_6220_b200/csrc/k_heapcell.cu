@@ -11,7 +11,10 @@
 // every value and counter, is the reference's.  FHCM's output depends on that
 // exact order (SURVEY.md finding 6), which is why the replay is exact rather
 // than band-parallel.
+#include <algorithm>
+
 #include "eik_internal.h"
+#include "k_cellsweep.cuh"
 #include "k_common.cuh"
 
 namespace eikb200 {
@@ -108,41 +111,6 @@ __device__ void reset_locks(const HTile& T, bool west_in, bool east_in, bool sou
     T.lock[k] = un ? 1 : 0;
   }
   __syncwarp();
-}
-
-// locked_sweep (heap_cell.cpp:98-126) in anti-diagonal order
-__device__ bool locked_sweep(const HTile& T, int dir, int lane, long long& updates) {
-  const bool iasc = (dir == SW || dir == NW);
-  const bool jasc = (dir == SW || dir == SE);
-  bool changed = false;
-  const int nsteps = T.w + T.h - 1;
-  for (int s = 0; s < nsteps; ++s) {
-    for (int b = lane; b < T.h; b += 32) {
-      const int a = s - b;
-      if (a >= 0 && a < T.w) {
-        const int x = iasc ? a : T.w - 1 - a;
-        const int y = jasc ? b : T.h - 1 - b;
-        uint8_t* lk = T.lock + y * T.w + x;
-        if (*lk) {
-          *lk = 0;
-          ++updates;
-          double* p = &T.u(x, y);
-          const double cand = node_update4(p[1], p[-1], p[T.pu], p[-T.pu], T.c(x, y));
-          if (cand < *p) {
-            *p = cand;
-            changed = true;
-            // unlock in-cell neighbours that this value can still improve
-            if (x + 1 < T.w && T.c(x + 1, y) >= 0.0 && p[1] > cand) lk[1] = 1;
-            if (x > 0 && T.c(x - 1, y) >= 0.0 && p[-1] > cand) lk[-1] = 1;
-            if (y + 1 < T.h && T.c(x, y + 1) >= 0.0 && p[T.pu] > cand) lk[T.w] = 1;
-            if (y > 0 && T.c(x, y - 1) >= 0.0 && p[-T.pu] > cand) lk[-T.w] = 1;
-          }
-        }
-      }
-    }
-    __syncwarp();
-  }
-  return __any_sync(kFull, changed);
 }
 
 struct Scan {
@@ -242,150 +210,403 @@ __device__ __forceinline__ void hc_cell_rect(const CellGeom& g, int cell, int64_
   je = (cy == g.cells_y - 1) ? g.n : jb + g.base_y;
 }
 
-__global__ void __launch_bounds__(32, 1) heapcell_serial_kernel(HcArgs a) {
+// ---- speculative exact replay ---------------------------------------------
+//
+// A cell's processing (sweeps + border scans) reads only its own nodes, the
+// cross halo from its 4 neighbour cells, flags[c] and first_done[c].  All of
+// that changes only when the cell itself or a neighbour is committed, so
+// version[c] = number of commits in {c} u N(c) identifies the inputs.  Worker
+// warps process cells near the top of the heap into the cell's spare slot and
+// tag the result with the version they read; the committer (block 0, warp 0)
+// pops cells in the reference's exact order and commits a result only if its
+// tag equals the cell's current version, else processes the cell itself.
+// Committed values live in one of two per-cell slots (cur[c]), so a commit is
+// a slot flip plus the precomputed scans -- no data copy on the serial path.
+
+__device__ __forceinline__ double* slot_ptr(const HcArgs& a, int s, int cell) {
+  return a.slots + ((size_t)s * a.J + cell) * a.cellsz;
+}
+
+// Process `cell` at the state the caller read version `v` for: stage from
+// the committed slots, sweep, scan, write the spare slot and the record.
+__device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell, int lane,
+                             long long* prof = nullptr) {
+  const long long p0 = prof ? clock64() : 0;
+  const CellGeom& g = a.g;
+  int64_t ib, ie, jb, je;
+  hc_cell_rect(g, cell, ib, ie, jb, je);
+  T.w = (int)(ie - ib);
+  T.h = (int)(je - jb);
+  const int cx = cell % g.cells_x, cy = cell / g.cells_x;
+  const int mw = g.max_w;
+  const int s_cur = __ldcg(a.cur + cell);
+  const double* own = slot_ptr(a, s_cur, cell);
+  // own values and costs (with cross halo costs from the global C array)
+  for (int k = lane; k < T.w * T.h; k += 32) {
+    const int y = k / T.w, x = k % T.w;
+    T.u(x, y) = __ldcg(own + y * mw + x);
+  }
+  const int W2 = T.w + 2;
+  for (int k = lane; k < (T.h + 2) * W2; k += 32) {
+    const int y = k / W2 - 1, x = k % W2 - 1;
+    if ((x < 0 || x >= T.w) && (y < 0 || y >= T.h)) continue;
+    const int64_t gj = jb + y;
+    double c = -1.0;
+    if (gj >= 0 && gj < g.n) c = __ldg(a.C + gj * g.P + g.pad + ib + x);
+    T.Ct[(y + 1) * T.pu + (x + 1)] = c;
+  }
+  // cross halo values from the neighbours' committed slots (+inf off-grid)
+  const bool has_nb[4] = {cx > 0, cx + 1 < g.cells_x, cy > 0, cy + 1 < g.cells_y};
+  for (int t = lane; t < T.h; t += 32) {
+    double wv = kInf, ev = kInf;
+    if (has_nb[0]) {
+      const int nb = cell - 1;
+      wv = __ldcg(slot_ptr(a, __ldcg(a.cur + nb), nb) + t * mw + (int)(g.base_x - 1));
+    } else if (ib > 0) {
+      wv = kInf;
+    }
+    if (has_nb[1]) {
+      const int nb = cell + 1;
+      ev = __ldcg(slot_ptr(a, __ldcg(a.cur + nb), nb) + t * mw + 0);
+    }
+    T.u(-1, t) = wv;
+    T.u(T.w, t) = ev;
+  }
+  for (int t = lane; t < T.w; t += 32) {
+    double sv = kInf, nv = kInf;
+    if (has_nb[2]) {
+      const int nb = cell - g.cells_x;
+      sv = __ldcg(slot_ptr(a, __ldcg(a.cur + nb), nb) + (int)(g.base_y - 1) * mw + t);
+    }
+    if (has_nb[3]) {
+      const int nb = cell + g.cells_x;
+      nv = __ldcg(slot_ptr(a, __ldcg(a.cur + nb), nb) + t);
+    }
+    T.u(t, -1) = sv;
+    T.u(t, T.h) = nv;
+  }
+  __syncwarp();
+  // border snapshots (heap_cell.cpp:279-282)
+  for (int t = lane; t < T.h; t += 32) {
+    before[0 * a.max_len + t] = T.u(0, t);
+    before[1 * a.max_len + t] = T.u(T.w - 1, t);
+  }
+  for (int t = lane; t < T.w; t += 32) {
+    before[2 * a.max_len + t] = T.u(t, 0);
+    before[3 * a.max_len + t] = T.u(t, T.h - 1);
+  }
+  const long long p1 = prof ? clock64() : 0;
+  const unsigned my_flags = __ldcg(a.flags + cell);
+  const bool first_removal = __ldcg(a.first_done + cell) == 0;
+  reset_locks(T, ib > 0, ie < g.m, jb > 0, je < g.n, lane);
+  const CellTile ct{T.U, T.Ct, T.lock, T.pu, T.w, T.h};
+  long long nsw = 0, upd = 0;
+  if (a.fast) {
+    for (int k = 0; k < 4; ++k) {  // process_flagged_once (heap_cell.cpp:150-160)
+      if (!(my_flags & (1u << kFlagOrder[k]))) continue;
+      cell_sweep<2>(ct, kFlagOrder[k], lane, upd);
+      ++nsw;
+    }
+  } else {  // process_to_convergence (heap_cell.cpp:130-147)
+    int perm[4], at = 0;
+    for (int k = 0; k < 4; ++k)
+      if (my_flags & (1u << kFlagOrder[k])) perm[at++] = kFlagOrder[k];
+    for (int k = 0; k < 4; ++k)
+      if (!(my_flags & (1u << kRotation[k]))) perm[at++] = kRotation[k];
+    bool changed = true;
+    while (changed) {
+      const int dir = nsw < 4 ? perm[nsw] : kRotation[nsw % 4];
+      changed = cell_sweep<2>(ct, dir, lane, upd);
+      ++nsw;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) upd += __shfl_xor_sync(kFull, upd, o);
+  const long long p2 = prof ? clock64() : 0;
+  // processed values into the spare slot
+  double* spare = slot_ptr(a, s_cur ^ 1, cell);
+  for (int k = lane; k < T.w * T.h; k += 32) {
+    const int y = k / T.w, x = k % T.w;
+    spare[y * mw + x] = T.u(x, y);
+  }
+  SpecRec* rec = a.rec + cell;
+  for (int side = 0; side < 4; ++side) {
+    Scan sc;
+    if (has_nb[side]) {
+      sc = scan_side(a, T, side, before + side * a.max_len, first_removal, ib, jb, cx, cy, lane);
+    } else {
+      sc.add = false;
+      sc.fl = 0;
+      sc.cand = kInf;
+      sc.mon_checked = sc.mon_single = false;
+    }
+    if (lane == 0) {
+      rec->cand[side] = sc.cand;
+      rec->add[side] = sc.add;
+      rec->fl[side] = (uint8_t)sc.fl;
+      rec->monc[side] = sc.mon_checked;
+      rec->mons[side] = sc.mon_single;
+    }
+  }
+  if (lane == 0) {
+    rec->sweeps = (int)nsw;
+    rec->updates = (int)upd;
+  }
+  if (prof) {
+    const long long p3 = clock64();
+    prof[0] += p1 - p0;  // staging
+    prof[1] += p2 - p1;  // locks + sweeps
+    prof[2] += p3 - p2;  // spare slot + scans + record
+  }
+}
+
+__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__global__ void heapcell_spec_kernel(HcArgs a) {
   extern __shared__ double smem[];
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
   const CellGeom& g = a.g;
   HTile T;
   T.pu = g.pu;
-  T.U = smem;
+  T.U = smem + (size_t)wib * a.tile_doubles;
   T.Ct = T.U + (size_t)(g.max_h + 2) * g.pu;
   double* before = T.Ct + (size_t)(g.max_h + 2) * g.pu;  // [4][max_len]
   T.lock = reinterpret_cast<uint8_t*>(before + 4 * a.max_len);
+  // The committer runs alone in CTA 0: every gpu-scope acquire issued on an
+  // SM invalidates that SM's L1 (CCTL.IVALL), and the committer's heap lives
+  // in L1.  Workers poll with relaxed loads and acquire once per speculation.
+  const bool committer = (blockIdx.x == 0 && wib == 0);
+  if (blockIdx.x == 0 && wib != 0) return;
 
+  if (!committer) {
+    // ---- worker: speculate cells near the top of the heap ----------------
+    const int wpc = blockDim.x >> 5;
+    const int wid = (blockIdx.x - 1) * wpc + wib;
+    const int nworkers = (gridDim.x - 1) * wpc;
+    for (;;) {
+      if (ld_relaxed_s32(a.done_flag)) return;
+      int hs = ld_relaxed_s32(a.hsize_pub);
+      if (hs > a.window) hs = a.window;
+      bool worked = false;
+      for (int pidx = wid; pidx < hs; pidx += nworkers) {
+        int cell = -1, v = 0;
+        if (lane == 0) {
+          cell = ld_relaxed_s32(a.harr + pidx);
+          if (cell >= 0 && cell < a.J) {
+            v = ld_relaxed_s32(a.version + cell);
+            if (ld_relaxed_s32(a.spec_ver + cell) == v || atomicCAS(a.busy + cell, 0, 1) != 0) {
+              cell = -1;
+            } else {
+              v = ld_acquire_s32(a.version + cell);
+              if (ld_relaxed_s32(a.spec_ver + cell) == v) {
+                st_release_s32(a.busy + cell, 0);
+                cell = -1;
+              }
+            }
+          } else {
+            cell = -1;
+          }
+        }
+        cell = __shfl_sync(kFull, cell, 0);
+        v = __shfl_sync(kFull, v, 0);
+        if (cell < 0) continue;
+        process_cell(a, T, before, cell, lane);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) {
+          st_release_s32(a.spec_ver + cell, v);
+          st_release_s32(a.busy + cell, 0);
+        }
+        worked = true;
+        break;
+      }
+      if (!worked) __nanosleep(200);
+    }
+  }
+
+  // ---- committer: the reference's heap loop in exact order ------------------
   DevHeap H{a.hkey, a.hpos, a.harr, 0};
   if (lane == 0) {
-    // cells intersecting the exit set start on the list (heap_cell.cpp:255-268)
-    for (int k = 0; k < a.n_init; ++k) {
+    for (int k = 0; k < a.n_init; ++k) {  // heap_cell.cpp:255-268
       const int cell = a.init_cells[k];
       a.cell_value[cell] = a.init_values[k];
       H.insert(cell, a.init_values[k]);
       if (a.fast) a.flags[cell] = 0xF;
     }
+    __threadfence();
+    st_release_s32(a.hsize_pub, H.size);
   }
   long long removals = 0, sweeps = 0, updates = 0, mon_checks = 0, mon_single = 0;
+  long long self_processed = 0, fast_hits = 0, waits = 0;
+  long long cyc_pop = 0, cyc_obtain = 0, cyc_self = 0, cyc_commit = 0;
+  long long prof[3] = {0, 0, 0};
   for (;;) {
     int cell = -1;
-    if (lane == 0 && H.size > 0) cell = H.pop();
+    long long t0 = clock64();
+    if (lane == 0 && H.size > 0) {
+      cell = H.pop();
+      *(volatile int*)a.hsize_pub = H.size;
+    }
     cell = __shfl_sync(kFull, cell, 0);
+    long long t1 = clock64();
+    cyc_pop += t1 - t0;
     if (cell < 0) break;
     ++removals;
     if (removals > a.budget) {  // heap_cell.cpp:276-277
       if (lane == 0) atomicExch(a.status, 3);
       break;
     }
-    int64_t ib, ie, jb, je;
-    hc_cell_rect(g, cell, ib, ie, jb, je);
-    T.w = (int)(ie - ib);
-    T.h = (int)(je - jb);
-    const int cx = cell % g.cells_x, cy = cell / g.cells_x;
-    // stage the cell with its cross halo (values and costs)
-    const int W2 = T.w + 2;
-    for (int k = lane; k < (T.h + 2) * W2; k += 32) {
-      const int y = k / W2 - 1, x = k % W2 - 1;
-      if ((x < 0 || x >= T.w) && (y < 0 || y >= T.h)) continue;
-      const int64_t gj = jb + y;
-      double v = kInf, c = -1.0;
-      if (gj >= 0 && gj < g.n) {
-        const int64_t o = gj * g.P + g.pad + ib + x;
-        v = a.u[o];
-        c = a.C[o];
-      }
-      T.U[(y + 1) * T.pu + (x + 1)] = v;
-      T.Ct[(y + 1) * T.pu + (x + 1)] = c;
-    }
-    __syncwarp();
-    const bool has_nb[4] = {cx > 0, cx + 1 < g.cells_x, cy > 0, cy + 1 < g.cells_y};
-    // border snapshots (heap_cell.cpp:279-282)
-    for (int t = lane; t < T.h; t += 32) {
-      before[0 * a.max_len + t] = T.u(0, t);
-      before[1 * a.max_len + t] = T.u(T.w - 1, t);
-    }
-    for (int t = lane; t < T.w; t += 32) {
-      before[2 * a.max_len + t] = T.u(t, 0);
-      before[3 * a.max_len + t] = T.u(t, T.h - 1);
-    }
-    unsigned my_flags = 0;
-    bool first_removal = false;
+    // obtain a result tagged with the current version.  Polls are relaxed
+    // (no L1 flush); the record is then read through an address that depends
+    // on the observed tag, so it cannot be read before the tag was seen.
+    int v = 0, mode = 0, dep = 0;  // mode 0: valid speculation, 1: process here
     if (lane == 0) {
-      my_flags = a.flags[cell];
-      a.flags[cell] = 0;
-      first_removal = !a.first_done[cell];
-      a.first_done[cell] = 1;
-    }
-    my_flags = __shfl_sync(kFull, my_flags, 0);
-    first_removal = __shfl_sync(kFull, (int)first_removal, 0) != 0;
-    reset_locks(T, ib > 0, ie < g.m, jb > 0, je < g.n, lane);
-    long long nsw = 0, upd = 0;
-    if (a.fast) {
-      // process_flagged_once (heap_cell.cpp:150-160)
-      for (int k = 0; k < 4; ++k) {
-        if (!(my_flags & (1u << kFlagOrder[k]))) continue;
-        locked_sweep(T, kFlagOrder[k], lane, upd);
-        ++nsw;
-      }
-    } else {
-      // process_to_convergence (heap_cell.cpp:130-147)
-      int perm[4], at = 0;
-      for (int k = 0; k < 4; ++k)
-        if (my_flags & (1u << kFlagOrder[k])) perm[at++] = kFlagOrder[k];
-      for (int k = 0; k < 4; ++k)
-        if (!(my_flags & (1u << kRotation[k]))) perm[at++] = kRotation[k];
-      bool changed = true;
-      while (changed) {
-        const int dir = nsw < 4 ? perm[nsw] : kRotation[nsw % 4];
-        changed = locked_sweep(T, dir, lane, upd);
-        ++nsw;
-      }
-    }
-    sweeps += nsw;
-    for (int o = 16; o > 0; o >>= 1) upd += __shfl_xor_sync(kFull, upd, o);
-    updates += upd;
-    // write the cell back
-    for (int k = lane; k < T.w * T.h; k += 32) {
-      const int y = k / T.w, x = k % T.w;
-      a.u[(jb + y) * g.P + g.pad + ib + x] = T.u(x, y);
-    }
-    // border scans and heap updates, sides W, E, S, N (heap_cell.cpp:288-311)
-    for (int side = 0; side < 4; ++side) {
-      if (!has_nb[side]) continue;
-      const Scan sc = scan_side(a, T, side, before + side * a.max_len, first_removal, ib, jb, cx,
-                                cy, lane);
-      if (lane == 0) {
-        const int nb = side == WEST ? cell - 1 : side == EAST ? cell + 1
-                     : side == SOUTH ? cell - g.cells_x : cell + g.cells_x;
-        if (sc.cand < a.cell_value[nb]) {
-          a.cell_value[nb] = sc.cand;
-          if (H.contains(nb)) H.decrease(nb, sc.cand);
+      v = a.version[cell];
+      long long spins = 0;
+      bool waited = false;
+      for (;;) {
+        const int sv = ld_relaxed_s32(a.spec_ver + cell);
+        if (sv == v) {
+          asm volatile("mov.b32 %0, %1;" : "=r"(dep) : "r"(sv));
+          dep -= v;  // == 0, but the compiler cannot know
+          break;
         }
-        if (sc.add) {
-          a.flags[nb] |= (uint8_t)sc.fl;
-          if (sc.mon_checked) {
+        if (atomicCAS(a.busy + cell, 0, 1) == 0) {
+          const int sv2 = ld_relaxed_s32(a.spec_ver + cell);
+          if (sv2 == v) {
+            st_release_s32(a.busy + cell, 0);
+            asm volatile("mov.b32 %0, %1;" : "=r"(dep) : "r"(sv2));
+            dep -= v;
+          } else {
+            mode = 1;
+          }
+          break;
+        }
+        waited = true;
+        if (++spins > kSpinCap) {
+          atomicExch(a.status, kStatusWatchdog);
+          mode = 2;
+          break;
+        }
+      }
+      if (mode == 0) ++fast_hits;
+      if (waited) ++waits;
+    }
+    mode = __shfl_sync(kFull, mode, 0);
+    long long t2 = clock64();
+    cyc_obtain += t2 - t1;
+    if (mode == 2) break;
+    if (mode == 1) {
+      process_cell(a, T, before, cell, lane, prof);
+      __syncwarp();
+      if (lane == 0) {
+        st_release_s32(a.spec_ver + cell, a.version[cell]);
+        st_release_s32(a.busy + cell, 0);
+      }
+      ++self_processed;
+    }
+    long long t3 = clock64();
+    cyc_self += t3 - t2;
+    // commit (lane 0): slot flip, flags, first_done, scans, versions
+    if (lane == 0) {
+      const SpecRec* rec = a.rec + cell + dep;
+      a.cur[cell] ^= 1;
+      a.flags[cell] = 0;
+      a.first_done[cell] = 1;
+      sweeps += __ldcg(&rec->sweeps);
+      updates += __ldcg(&rec->updates);
+      const int cxi = cell % g.cells_x, cyi = cell / g.cells_x;
+      int nbs[4] = {cxi > 0 ? cell - 1 : -1, cxi + 1 < g.cells_x ? cell + 1 : -1,
+                    cyi > 0 ? cell - g.cells_x : -1, cyi + 1 < g.cells_y ? cell + g.cells_x : -1};
+      for (int side = 0; side < 4; ++side) {  // heap_cell.cpp:288-311
+        const int nb = nbs[side];
+        if (nb < 0) continue;
+        const double cand = __ldcg(&rec->cand[side]);
+        if (cand < a.cell_value[nb]) {
+          a.cell_value[nb] = cand;
+          if (H.contains(nb)) H.decrease(nb, cand);
+        }
+        if (__ldcg(&rec->add[side])) {
+          a.flags[nb] |= __ldcg(&rec->fl[side]);
+          if (__ldcg(&rec->monc[side])) {
             ++mon_checks;
-            if (sc.mon_single) ++mon_single;
+            if (__ldcg(&rec->mons[side])) ++mon_single;
           }
           if (!H.contains(nb)) H.insert(nb, a.cell_value[nb]);
         }
       }
+      // one release orders the flag / slot-flip writes before the version
+      // bumps (st.release = MEMBAR, no L1 flush); the rest follow it
+      st_release_s32(a.version + cell, a.version[cell] + 1);
+      for (int side = 0; side < 4; ++side)
+        if (nbs[side] >= 0) *(volatile int*)(a.version + nbs[side]) = a.version[nbs[side]] + 1;
+      *(volatile int*)a.hsize_pub = H.size;
     }
     __syncwarp();
+    cyc_commit += clock64() - t3;
   }
   if (lane == 0) {
+    a.counters[8] = cyc_pop;
+    a.counters[9] = cyc_obtain;
+    a.counters[10] = cyc_self;
+    a.counters[11] = cyc_commit;
+    a.counters[12] = prof[0];
+    a.counters[13] = prof[1];
+    a.counters[14] = prof[2];
     a.counters[0] = removals;
     a.counters[1] = sweeps;
     a.counters[2] = updates;
     a.counters[3] = mon_checks;
     a.counters[4] = mon_single;
+    a.counters[5] = self_processed;
+    a.counters[6] = fast_hits;
+    a.counters[7] = waits;
+    __threadfence();
+    st_release_s32(a.done_flag, 1);
   }
 }
 
-__global__ void heapcell_init_kernel(double* cell_value, uint8_t* flags, uint8_t* first_done,
-                                     int* hpos, int J) {
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < J; k += gridDim.x * blockDim.x) {
-    cell_value[k] = kInf;
-    flags[k] = 0;
-    first_done[k] = 0;
-    hpos[k] = -1;
+__global__ void heapcell_init_kernel(HcArgs a) {
+  const int64_t cellsz = a.cellsz;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < (int64_t)a.J * cellsz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int cell = (int)(k / cellsz);
+    const int r = (int)(k - (int64_t)cell * cellsz);
+    const int y = r / a.g.max_w, x = r % a.g.max_w;
+    int64_t ib, ie, jb, je;
+    hc_cell_rect(a.g, cell, ib, ie, jb, je);
+    double v = kInf;
+    if (x < ie - ib && y < je - jb) v = a.u[(jb + y) * a.g.P + a.g.pad + ib + x];
+    a.slots[k] = v;  // slot 0 <- the prepared field
+    if (r == 0) {
+      a.cur[cell] = 0;
+      a.version[cell] = 0;
+      a.spec_ver[cell] = -1;
+      a.busy[cell] = 0;
+      a.cell_value[cell] = kInf;
+      a.flags[cell] = 0;
+      a.first_done[cell] = 0;
+      a.hpos[cell] = -1;
+      a.harr[cell] = -1;
+    }
+  }
+}
+
+__global__ void heapcell_gather_kernel(HcArgs a) {
+  const int64_t cellsz = a.cellsz;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < (int64_t)a.J * cellsz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int cell = (int)(k / cellsz);
+    const int r = (int)(k - (int64_t)cell * cellsz);
+    const int y = r / a.g.max_w, x = r % a.g.max_w;
+    int64_t ib, ie, jb, je;
+    hc_cell_rect(a.g, cell, ib, ie, jb, je);
+    if (x < ie - ib && y < je - jb)
+      a.u[(jb + y) * a.g.P + a.g.pad + ib + x] = slot_ptr(a, a.cur[cell], cell)[r];
   }
 }
 
@@ -393,20 +614,34 @@ __global__ void heapcell_init_kernel(double* cell_value, uint8_t* flags, uint8_t
 
 size_t heapcell_smem_bytes(const CellGeom& g, int max_len) {
   return sizeof(double) * (2 * (size_t)(g.max_h + 2) * g.pu + 4 * (size_t)max_len) +
-         (size_t)g.max_w * g.max_h;
+         (((size_t)g.max_w * g.max_h + 7) & ~(size_t)7);
 }
 
-cudaError_t launch_heapcell(const HcArgs& args, cudaStream_t s, int* launches) {
-  int blocks = (args.J + 255) / 256;
-  if (blocks > 1184) blocks = 1184;
-  heapcell_init_kernel<<<blocks, 256, 0, s>>>(args.cell_value, args.flags, args.first_done,
-                                              args.hpos, args.J);
-  const size_t smem = heapcell_smem_bytes(args.g, args.max_len);
-  cudaError_t e = cudaFuncSetAttribute(heapcell_serial_kernel,
+cudaError_t launch_heapcell(const HcArgs& args, int warps_per_cta, int max_ctas, cudaStream_t s,
+                            int* launches) {
+  const int64_t total = (int64_t)args.J * args.cellsz;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+  heapcell_init_kernel<<<blocks, 256, 0, s>>>(args);
+  const size_t smem = (size_t)warps_per_cta * args.tile_doubles * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(heapcell_spec_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  heapcell_serial_kernel<<<1, 32, smem, s>>>(args);
-  *launches += 2;
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heapcell_spec_kernel,
+                                                    32 * warps_per_cta, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int ctas = std::min(per_sm * sms, max_ctas);
+  if (ctas < 1) ctas = 1;
+  HcArgs a = args;
+  void* params[] = {&a};
+  e = cudaLaunchCooperativeKernel((const void*)heapcell_spec_kernel, dim3(ctas),
+                                  dim3(32 * warps_per_cta), params, smem, s);
+  if (e != cudaSuccess) return e;
+  heapcell_gather_kernel<<<blocks, 256, 0, s>>>(args);
+  *launches += 3;
   return cudaGetLastError();
 }
 

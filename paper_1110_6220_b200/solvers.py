@@ -48,6 +48,7 @@ class SolverOutput:
     device_ms: float = 0.0
     host_ms: float = 0.0
     kernel_launches: int = 0
+    spec: tuple = (0, 0, 0)  # heap-cell replay: (hits, waits, self-processed)
 
     def at(self, i: int, j: int) -> float:
         return float(self.values[j * self.m + i])
@@ -96,25 +97,27 @@ def _pack(out: N.eik_output, values: np.ndarray, g) -> SolverOutput:
                         hybrid=HybridStats(out.avhr, out.avs, out.mon_pct, out.cell_removals,
                                            out.cell_sweeps, out.mon_checks, out.mon_single),
                         device_ms=out.device_ms, host_ms=out.host_ms,
-                        kernel_launches=out.kernel_launches)
+                        kernel_launches=out.kernel_launches,
+                        spec=(out.spec_hits, out.spec_waits, out.spec_self))
 
 
 def solve(problem: Problem, method: str, cells: Optional[CellDecomposition] = None,
-          tables: Optional[CellTables] = None) -> SolverOutput:
-    """One solve through eik_solve (host buffers in, host values out)."""
+          tables: Optional[CellTables] = None, out: Optional[np.ndarray] = None) -> SolverOutput:
+    """One solve through eik_solve (host buffers in, host values out).
+    `out` may be a caller-owned (e.g. pinned) float64 buffer of m*n values."""
     code = N.METHOD_NAMES[method]
     F = problem.sampled_speed()
     p, keep_p = _c_problem(problem, F)
     if cells is not None and tables is None:
         tables = cell_tables(problem, cells)
     c, keep_c = _c_cells(cells, tables)
-    u = np.empty(problem.grid.size(), dtype=np.float64)
-    out = N.eik_output()
-    out.u = N.dptr(u)
-    out.u_on_device = 0
-    rc = N.lib.eik_solve(C.byref(p), C.byref(c) if c is not None else None, code, C.byref(out))
+    u = out if out is not None else np.empty(problem.grid.size(), dtype=np.float64)
+    res = N.eik_output()
+    res.u = N.dptr(u)
+    res.u_on_device = 0
+    rc = N.lib.eik_solve(C.byref(p), C.byref(c) if c is not None else None, code, C.byref(res))
     N.raise_for(rc)
-    return _pack(out, u, problem.grid)
+    return _pack(res, u, problem.grid)
 
 
 def fmm_solve(problem: Problem) -> SolverOutput:

@@ -38,5 +38,5 @@ for cname in a.configs.split(","):
             best = min(ts)
             print(f"{cname} {method:5s} cs={cs} M={M} sweeps={o.sweeps} pops={o.heap_removals} "
                   f"dev_ms={best:.3f} (all {['%.3f' % t for t in ts]}) wall_ms={wall:.2f} "
-                  f"Gpts/s={M / best / 1e6:.3f} launches={o.kernel_launches}", flush=True)
+                  f"Gpts/s={M / best / 1e6:.3f} launches={o.kernel_launches} spec(hit,wait,self)={o.spec}", flush=True)
             plan.close()
