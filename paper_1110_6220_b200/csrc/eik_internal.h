@@ -70,25 +70,22 @@ struct HcArgs {
   CellGeom g;
   double* slots;            // [2][J][max_h*max_w] per-cell value slots
   int64_t cellsz;           // max_h * max_w
-  uint8_t* cur;             // [J] committed slot of each cell
-  int* version;             // [J] commits in {c} u N(c)
-  int* spec_ver;            // [J] version the spare slot / record was computed for
+  unsigned* state;          // [J] flags | first_done<<4 | slot<<5 | version<<8
+  unsigned* spec_ver;       // [J] version the spare slot / record was computed for
   int* busy;                // [J] a warp is computing the spare slot
   SpecRec* rec;             // [J]
   int* done_flag;
   int* hsize_pub;           // heap size, published for the workers
   int window;               // workers speculate heap positions [0, window)
   int64_t tile_doubles;     // per-warp smem
+  int heap_in_smem;         // committer heap + cell values in its shared memory
   const double* C;          // padded h/F
   double* u;                // padded values
   const double* probe[4];   // F at border probe points: W/E [cells_x*n], S/N [cells_y*m]
   double h, hc_x, hc_y;
-  double* cell_value;       // [J] heap keys (cell values)
-  uint8_t* flags;           // [J] raised sweep directions
-  uint8_t* first_done;      // [J]
-  double* hkey;             // heap storage
-  int* hpos;
-  int* harr;
+  double* hkey;             // [J] cell values = heap keys (global-heap mode)
+  int* hpos;                // [J] (global-heap mode)
+  int* harr;                // [J] heap array; published prefix in smem mode
   const int* init_cells;    // Q-cells in ascending id order with their initial values
   const double* init_values;
   int n_init;
@@ -101,6 +98,7 @@ struct HcArgs {
 };
 
 size_t heapcell_smem_bytes(const CellGeom& g, int max_len);
+size_t heapcell_committer_heap_bytes(int J);
 cudaError_t launch_heapcell(const HcArgs& a, int warps_per_cta, int max_ctas, cudaStream_t s,
                             int* launches);
 

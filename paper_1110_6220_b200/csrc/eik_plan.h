@@ -53,9 +53,8 @@ struct eik_plan {
   unsigned long long* dCounters = nullptr;
   // heap-cell state
   double* dProbe[4] = {nullptr, nullptr, nullptr, nullptr};
-  double* dCellValue = nullptr;
-  uint8_t* dHcFlags = nullptr;
-  uint8_t* dFirstDone = nullptr;
+  unsigned* dState = nullptr;   // packed per-cell state words
+  int hc_heap_in_smem = 0;
   double* dHKey = nullptr;
   int* dHPos = nullptr;
   int* dHArr = nullptr;
@@ -63,9 +62,7 @@ struct eik_plan {
   double* dInitValues = nullptr;
   int max_len = 0;
   double* dSlots = nullptr;
-  uint8_t* dCur = nullptr;
-  int* dVersion = nullptr;
-  int* dSpecVer = nullptr;
+  unsigned* dSpecVer = nullptr;
   int* dBusy = nullptr;
   eikb200::SpecRec* dRec = nullptr;
   int* dHcMisc = nullptr;   // [0] done flag, [1] published heap size

@@ -89,12 +89,8 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
       CK(cudaMemcpyAsync(P->dProbe[s], P->probe[s].data(), sizeof(double) * P->probe[s].size(),
                          cudaMemcpyHostToDevice, P->stream));
     }
-    if ((rc = dalloc(&P->dCellValue, J))) return rc;
-    P->allocs.push_back(P->dCellValue);
-    if ((rc = dalloc(&P->dHcFlags, J))) return rc;
-    P->allocs.push_back(P->dHcFlags);
-    if ((rc = dalloc(&P->dFirstDone, J))) return rc;
-    P->allocs.push_back(P->dFirstDone);
+    if ((rc = dalloc(&P->dState, J))) return rc;
+    P->allocs.push_back(P->dState);
     if ((rc = dalloc(&P->dHKey, J))) return rc;
     P->allocs.push_back(P->dHKey);
     if ((rc = dalloc(&P->dHPos, J))) return rc;
@@ -110,10 +106,6 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     const size_t cellsz = (size_t)g.max_w * g.max_h;
     if ((rc = dalloc(&P->dSlots, 2 * (size_t)J * cellsz))) return rc;
     P->allocs.push_back(P->dSlots);
-    if ((rc = dalloc(&P->dCur, J))) return rc;
-    P->allocs.push_back(P->dCur);
-    if ((rc = dalloc(&P->dVersion, J))) return rc;
-    P->allocs.push_back(P->dVersion);
     if ((rc = dalloc(&P->dSpecVer, J))) return rc;
     P->allocs.push_back(P->dSpecVer);
     if ((rc = dalloc(&P->dBusy, J))) return rc;
@@ -126,7 +118,12 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     const size_t tile = (smem + sizeof(double) - 1) / sizeof(double);
     P->cg.tile_doubles = (int64_t)tile;
     P->hc_warps_per_cta = (int)std::max<size_t>(1, std::min<size_t>(8, kTileBudget / (tile * 8)));
-    // EIK_HC_WORKERS=0 runs the committer alone (serial exact replay)
+    // the committer's heap + cell values go to its shared memory when they
+    // fit next to its tile (uint16 heap indices)
+    P->hc_heap_in_smem =
+        J < 65535 && tile * 8 + heapcell_committer_heap_bytes((int)J) <= 220 * 1024 ? 1 : 0;
+    if (std::getenv("EIK_HC_GLOBAL_HEAP")) P->hc_heap_in_smem = 0;
+    // EIK_HC_CTAS=1 runs the committer alone (serial exact replay)
     P->hc_max_ctas = 1 << 20;
     if (const char* w = std::getenv("EIK_HC_CTAS")) P->hc_max_ctas = std::max(1, std::atoi(w));
     return EIK_OK;
@@ -288,9 +285,8 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
   a.h = P->g.h;
   a.hc_x = (double)(P->g.m / P->cells_x) * P->g.h;  // cells.cpp:44-45
   a.hc_y = (double)(P->g.n / P->cells_y) * P->g.h;
-  a.cell_value = P->dCellValue;
-  a.flags = P->dHcFlags;
-  a.first_done = P->dFirstDone;
+  a.state = P->dState;
+  a.heap_in_smem = P->hc_heap_in_smem;
   a.hkey = P->dHKey;
   a.hpos = P->dHPos;
   a.harr = P->dHArr;
@@ -305,8 +301,6 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
   a.max_len = P->max_len;
   a.slots = P->dSlots;
   a.cellsz = (int64_t)P->cg.max_w * P->cg.max_h;
-  a.cur = P->dCur;
-  a.version = P->dVersion;
   a.spec_ver = P->dSpecVer;
   a.busy = P->dBusy;
   a.rec = P->dRec;

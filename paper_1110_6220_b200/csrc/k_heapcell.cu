@@ -1,16 +1,26 @@
 // Kernel (3): the heap-cell methods HCM / FHCM (/root/reference/proj/src/
-// heap_cell.cpp:13-336) as a device-resident exact replay.
+// heap_cell.cpp:13-336) as a device-resident speculative exact replay.
 //
-// One warp runs the reference's loop: lane 0 owns an indexed binary min-heap
-// of cells keyed by (cell value, cell id) (indexed_min_heap.hpp, ties to the
-// smaller id), the whole warp processes the popped cell in shared memory --
-// border snapshot, reset_locks, locking sweeps in anti-diagonal wavefront
-// order (bit-identical to the row-by-row loop including every counter,
-// SURVEY.md finding 7), the four border scans with warp reductions -- and
-// lane 0 applies the scans to the heap.  The pop sequence, and therefore
-// every value and counter, is the reference's.  FHCM's output depends on that
-// exact order (SURVEY.md finding 6), which is why the replay is exact rather
-// than band-parallel.
+// The reference pops cells from a (value, id) min-heap one at a time; FHCM's
+// output depends on that exact order (SURVEY.md finding 6), so the order is
+// replayed exactly.  A cell's processing (border snapshot, reset_locks,
+// locking sweeps, the four border scans) reads only its own nodes, the cross
+// halo from its 4 neighbour cells, its flags and its first-removal bit.  All
+// of that changes only when the cell itself or a neighbour is committed, so
+// version[c] = number of commits in {c} u N(c) identifies the inputs:
+//
+//   * worker warps process cells near the top of the heap into the cell's
+//     spare value slot and tag the result record with the version they read;
+//   * the committer (CTA 0, warp 0) pops cells in the reference's order and
+//     commits a result only if its tag equals the cell's current version --
+//     a slot flip plus the precomputed scans -- and otherwise processes the
+//     cell itself.
+//
+// Per-cell flags, first-removal bit, committed slot and version share one
+// 32-bit state word, so a commit is a few plain stores and a worker reads a
+// consistent snapshot with one load.  The committer's heap and cell values
+// live in its shared memory when they fit (uint16 indices), else in global.
+// Every value and counter equals the reference's (tests/test_gpu_cells.py).
 #include <algorithm>
 
 #include "eik_internal.h"
@@ -26,28 +36,69 @@ enum { WEST = 0, EAST = 1, SOUTH = 2, NORTH = 3 };
 __device__ const int kFlagOrder[4] = {NE, NW, SE, SW};  // heap_cell.cpp:13-14
 __device__ const int kRotation[4] = {SW, NW, NE, SE};   // heap_cell.cpp:15-16
 
-// ---- indexed min-heap (single thread) -------------------------------------
-struct DevHeap {
+// ---- per-cell state word -----------------------------------------------------
+// bits 0-3 raised sweep flags, bit 4 first removal done, bit 5 committed slot,
+// bits 8-31 version (commits in {c} u N(c), mod 2^24)
+__device__ __forceinline__ unsigned st_flags(unsigned s) { return s & 15u; }
+__device__ __forceinline__ bool st_first_done(unsigned s) { return (s >> 4) & 1u; }
+__device__ __forceinline__ int st_cur(unsigned s) { return (int)((s >> 5) & 1u); }
+__device__ __forceinline__ unsigned st_ver(unsigned s) { return s >> 8; }
+constexpr unsigned kVerOne = 1u << 8;
+
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ---- indexed min-heap over cells keyed by (cell value, id) ------------------
+// indexed_min_heap.hpp:11-106, ties to the smaller id.  key[] is the cell
+// value array itself (the reference keeps them equal for queued cells).
+// `pub` mirrors heap positions < window to global memory for the workers.
+template <class IdxT>
+struct Heap {
   double* key;
-  int* pos;
-  int* arr;
+  IdxT* pos;
+  IdxT* arr;
+  int* pub;
+  int window;
   int size;
+  IdxT absent;
   __device__ bool less(int a, int b) const {
     const double ka = key[a], kb = key[b];
     if (ka != kb) return ka < kb;
     return a < b;
+  }
+  __device__ void put(int p, int id) {
+    arr[p] = (IdxT)id;
+    pos[id] = (IdxT)p;
+    if (pub && p < window) *(volatile int*)(pub + p) = id;
   }
   __device__ void up(int p) {
     const int id = arr[p];
     while (p > 0) {
       const int par = (p - 1) >> 1;
       if (!less(id, arr[par])) break;
-      arr[p] = arr[par];
-      pos[arr[p]] = p;
+      put(p, arr[par]);
       p = par;
     }
-    arr[p] = id;
-    pos[id] = p;
+    put(p, id);
   }
   __device__ void down(int p) {
     const int id = arr[p];
@@ -56,31 +107,23 @@ struct DevHeap {
       if (c >= size) break;
       if (c + 1 < size && less(arr[c + 1], arr[c])) ++c;
       if (!less(arr[c], id)) break;
-      arr[p] = arr[c];
-      pos[arr[p]] = p;
+      put(p, arr[c]);
       p = c;
     }
-    arr[p] = id;
-    pos[id] = p;
+    put(p, id);
   }
-  __device__ bool contains(int id) const { return pos[id] >= 0; }
-  __device__ void insert(int id, double k) {
-    key[id] = k;
-    pos[id] = size;
-    arr[size++] = id;
-    up(pos[id]);
-  }
-  __device__ void decrease(int id, double k) {
-    key[id] = k;
-    up(pos[id]);
+  __device__ bool contains(int id) const { return pos[id] != absent; }
+  __device__ void insert(int id) {  // key[id] already holds the cell value
+    put(size, id);
+    ++size;
+    up(size - 1);
   }
   __device__ int pop() {
     const int top = arr[0];
     const int last = arr[--size];
-    pos[top] = -1;
+    pos[top] = absent;
     if (size > 0) {
-      arr[0] = last;
-      pos[last] = 0;
+      put(0, last);
       down(0);
     }
     return top;
@@ -175,8 +218,8 @@ __device__ Scan scan_side(const HcArgs& a, const HTile& T, int side, const doubl
   r.cand = kInf;
   if (vmax < kInf) {  // isfinite(vmax): vmax > -inf always holds here
     double fprobe;
-    if (vertical) fprobe = a.probe[side][(int64_t)cx * a.g.n + (jb + arg)];
-    else fprobe = a.probe[side][(int64_t)cy * a.g.m + (ib + arg)];
+    if (vertical) fprobe = __ldg(a.probe[side] + (int64_t)cx * a.g.n + (jb + arg));
+    else fprobe = __ldg(a.probe[side] + (int64_t)cy * a.g.m + (ib + arg));
     const double hc = vertical ? a.hc_x : a.hc_y;
     r.cand = vmax + 0.5 * (a.h + hc) / fprobe;  // cell_value_candidate (cells.hpp:109-112)
   }
@@ -210,27 +253,14 @@ __device__ __forceinline__ void hc_cell_rect(const CellGeom& g, int cell, int64_
   je = (cy == g.cells_y - 1) ? g.n : jb + g.base_y;
 }
 
-// ---- speculative exact replay ---------------------------------------------
-//
-// A cell's processing (sweeps + border scans) reads only its own nodes, the
-// cross halo from its 4 neighbour cells, flags[c] and first_done[c].  All of
-// that changes only when the cell itself or a neighbour is committed, so
-// version[c] = number of commits in {c} u N(c) identifies the inputs.  Worker
-// warps process cells near the top of the heap into the cell's spare slot and
-// tag the result with the version they read; the committer (block 0, warp 0)
-// pops cells in the reference's exact order and commits a result only if its
-// tag equals the cell's current version, else processes the cell itself.
-// Committed values live in one of two per-cell slots (cur[c]), so a commit is
-// a slot flip plus the precomputed scans -- no data copy on the serial path.
-
 __device__ __forceinline__ double* slot_ptr(const HcArgs& a, int s, int cell) {
   return a.slots + ((size_t)s * a.J + cell) * a.cellsz;
 }
 
-// Process `cell` at the state the caller read version `v` for: stage from
+// Process `cell` against the committed state whose word is `st`: stage from
 // the committed slots, sweep, scan, write the spare slot and the record.
-__device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell, int lane,
-                             long long* prof = nullptr) {
+__device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell, unsigned st,
+                             int lane, long long* prof = nullptr) {
   const long long p0 = prof ? clock64() : 0;
   const CellGeom& g = a.g;
   int64_t ib, ie, jb, je;
@@ -239,9 +269,13 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
   T.h = (int)(je - jb);
   const int cx = cell % g.cells_x, cy = cell / g.cells_x;
   const int mw = g.max_w;
-  const int s_cur = __ldcg(a.cur + cell);
-  const double* own = slot_ptr(a, s_cur, cell);
-  // own values and costs (with cross halo costs from the global C array)
+  const bool has_nb[4] = {cx > 0, cx + 1 < g.cells_x, cy > 0, cy + 1 < g.cells_y};
+  const int nbs[4] = {cell - 1, cell + 1, cell - g.cells_x, cell + g.cells_x};
+  int ncur[4];
+#pragma unroll
+  for (int d = 0; d < 4; ++d) ncur[d] = has_nb[d] ? st_cur(ld_relaxed_u32(a.state + nbs[d])) : 0;
+  const double* own = slot_ptr(a, st_cur(st), cell);
+  // own values; costs of the cell and its cross halo from the global C array
   for (int k = lane; k < T.w * T.h; k += 32) {
     const int y = k / T.w, x = k % T.w;
     T.u(x, y) = __ldcg(own + y * mw + x);
@@ -256,34 +290,15 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
     T.Ct[(y + 1) * T.pu + (x + 1)] = c;
   }
   // cross halo values from the neighbours' committed slots (+inf off-grid)
-  const bool has_nb[4] = {cx > 0, cx + 1 < g.cells_x, cy > 0, cy + 1 < g.cells_y};
   for (int t = lane; t < T.h; t += 32) {
-    double wv = kInf, ev = kInf;
-    if (has_nb[0]) {
-      const int nb = cell - 1;
-      wv = __ldcg(slot_ptr(a, __ldcg(a.cur + nb), nb) + t * mw + (int)(g.base_x - 1));
-    } else if (ib > 0) {
-      wv = kInf;
-    }
-    if (has_nb[1]) {
-      const int nb = cell + 1;
-      ev = __ldcg(slot_ptr(a, __ldcg(a.cur + nb), nb) + t * mw + 0);
-    }
-    T.u(-1, t) = wv;
-    T.u(T.w, t) = ev;
+    T.u(-1, t) = has_nb[0] ? __ldcg(slot_ptr(a, ncur[0], nbs[0]) + t * mw + (int)(g.base_x - 1))
+                           : kInf;
+    T.u(T.w, t) = has_nb[1] ? __ldcg(slot_ptr(a, ncur[1], nbs[1]) + t * mw) : kInf;
   }
   for (int t = lane; t < T.w; t += 32) {
-    double sv = kInf, nv = kInf;
-    if (has_nb[2]) {
-      const int nb = cell - g.cells_x;
-      sv = __ldcg(slot_ptr(a, __ldcg(a.cur + nb), nb) + (int)(g.base_y - 1) * mw + t);
-    }
-    if (has_nb[3]) {
-      const int nb = cell + g.cells_x;
-      nv = __ldcg(slot_ptr(a, __ldcg(a.cur + nb), nb) + t);
-    }
-    T.u(t, -1) = sv;
-    T.u(t, T.h) = nv;
+    T.u(t, -1) = has_nb[2] ? __ldcg(slot_ptr(a, ncur[2], nbs[2]) + (int)(g.base_y - 1) * mw + t)
+                           : kInf;
+    T.u(t, T.h) = has_nb[3] ? __ldcg(slot_ptr(a, ncur[3], nbs[3]) + t) : kInf;
   }
   __syncwarp();
   // border snapshots (heap_cell.cpp:279-282)
@@ -296,8 +311,8 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
     before[3 * a.max_len + t] = T.u(t, T.h - 1);
   }
   const long long p1 = prof ? clock64() : 0;
-  const unsigned my_flags = __ldcg(a.flags + cell);
-  const bool first_removal = __ldcg(a.first_done + cell) == 0;
+  const unsigned my_flags = st_flags(st);
+  const bool first_removal = !st_first_done(st);
   reset_locks(T, ib > 0, ie < g.m, jb > 0, je < g.n, lane);
   const CellTile ct{T.U, T.Ct, T.lock, T.pu, T.w, T.h};
   long long nsw = 0, upd = 0;
@@ -323,7 +338,7 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
   for (int o = 16; o > 0; o >>= 1) upd += __shfl_xor_sync(kFull, upd, o);
   const long long p2 = prof ? clock64() : 0;
   // processed values into the spare slot
-  double* spare = slot_ptr(a, s_cur ^ 1, cell);
+  double* spare = slot_ptr(a, st_cur(st) ^ 1, cell);
   for (int k = lane; k < T.w * T.h; k += 32) {
     const int y = k / T.w, x = k % T.w;
     spare[y * mw + x] = T.u(x, y);
@@ -359,86 +374,18 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
   }
 }
 
-__device__ __forceinline__ int ld_relaxed_s32(const int* p) {
-  int v;
-  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__global__ void heapcell_spec_kernel(HcArgs a) {
-  extern __shared__ double smem[];
-  const int lane = threadIdx.x & 31;
-  const int wib = threadIdx.x >> 5;
+// ---- the committer: the reference's heap loop in exact order ----------------
+template <class IdxT>
+__device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* before, int lane) {
   const CellGeom& g = a.g;
-  HTile T;
-  T.pu = g.pu;
-  T.U = smem + (size_t)wib * a.tile_doubles;
-  T.Ct = T.U + (size_t)(g.max_h + 2) * g.pu;
-  double* before = T.Ct + (size_t)(g.max_h + 2) * g.pu;  // [4][max_len]
-  T.lock = reinterpret_cast<uint8_t*>(before + 4 * a.max_len);
-  // The committer runs alone in CTA 0: every gpu-scope acquire issued on an
-  // SM invalidates that SM's L1 (CCTL.IVALL), and the committer's heap lives
-  // in L1.  Workers poll with relaxed loads and acquire once per speculation.
-  const bool committer = (blockIdx.x == 0 && wib == 0);
-  if (blockIdx.x == 0 && wib != 0) return;
-
-  if (!committer) {
-    // ---- worker: speculate cells near the top of the heap ----------------
-    const int wpc = blockDim.x >> 5;
-    const int wid = (blockIdx.x - 1) * wpc + wib;
-    const int nworkers = (gridDim.x - 1) * wpc;
-    for (;;) {
-      if (ld_relaxed_s32(a.done_flag)) return;
-      int hs = ld_relaxed_s32(a.hsize_pub);
-      if (hs > a.window) hs = a.window;
-      bool worked = false;
-      for (int pidx = wid; pidx < hs; pidx += nworkers) {
-        int cell = -1, v = 0;
-        if (lane == 0) {
-          cell = ld_relaxed_s32(a.harr + pidx);
-          if (cell >= 0 && cell < a.J) {
-            v = ld_relaxed_s32(a.version + cell);
-            if (ld_relaxed_s32(a.spec_ver + cell) == v || atomicCAS(a.busy + cell, 0, 1) != 0) {
-              cell = -1;
-            } else {
-              v = ld_acquire_s32(a.version + cell);
-              if (ld_relaxed_s32(a.spec_ver + cell) == v) {
-                st_release_s32(a.busy + cell, 0);
-                cell = -1;
-              }
-            }
-          } else {
-            cell = -1;
-          }
-        }
-        cell = __shfl_sync(kFull, cell, 0);
-        v = __shfl_sync(kFull, v, 0);
-        if (cell < 0) continue;
-        process_cell(a, T, before, cell, lane);
-        __threadfence();
-        __syncwarp();
-        if (lane == 0) {
-          st_release_s32(a.spec_ver + cell, v);
-          st_release_s32(a.busy + cell, 0);
-        }
-        worked = true;
-        break;
-      }
-      if (!worked) __nanosleep(200);
-    }
-  }
-
-  // ---- committer: the reference's heap loop in exact order ------------------
-  DevHeap H{a.hkey, a.hpos, a.harr, 0};
   if (lane == 0) {
     for (int k = 0; k < a.n_init; ++k) {  // heap_cell.cpp:255-268
       const int cell = a.init_cells[k];
-      a.cell_value[cell] = a.init_values[k];
-      H.insert(cell, a.init_values[k]);
-      if (a.fast) a.flags[cell] = 0xF;
+      H.key[cell] = a.init_values[k];
+      H.insert(cell);
+      if (a.fast) st_relaxed_u32(a.state + cell, 0xFu);  // Q-cells start with all flags
     }
-    __threadfence();
-    st_release_s32(a.hsize_pub, H.size);
+    *(volatile int*)a.hsize_pub = H.size;
   }
   long long removals = 0, sweeps = 0, updates = 0, mon_checks = 0, mon_single = 0;
   long long self_processed = 0, fast_hits = 0, waits = 0;
@@ -460,27 +407,34 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
       if (lane == 0) atomicExch(a.status, 3);
       break;
     }
-    // obtain a result tagged with the current version.  Polls are relaxed
-    // (no L1 flush); the record is then read through an address that depends
-    // on the observed tag, so it cannot be read before the tag was seen.
-    int v = 0, mode = 0, dep = 0;  // mode 0: valid speculation, 1: process here
+    const int cxi = cell % g.cells_x, cyi = cell / g.cells_x;
+    const int nbs[4] = {cxi > 0 ? cell - 1 : -1, cxi + 1 < g.cells_x ? cell + 1 : -1,
+                        cyi > 0 ? cell - g.cells_x : -1, cyi + 1 < g.cells_y ? cell + g.cells_x : -1};
+    // obtain a result tagged with the current version.  Polls are relaxed (an
+    // acquire would flush this SM's L1); the record is then read through an
+    // address that depends on the observed tag, so it cannot be read early.
+    int mode = 0, dep = 0;  // mode 0: valid speculation, 1: process here
+    unsigned st = 0;
     if (lane == 0) {
-      v = a.version[cell];
+      st = ld_relaxed_u32(a.state + cell);
+      const unsigned v = st_ver(st);
       long long spins = 0;
       bool waited = false;
       for (;;) {
-        const int sv = ld_relaxed_s32(a.spec_ver + cell);
+        const unsigned sv = ld_relaxed_u32(a.spec_ver + cell);
         if (sv == v) {
-          asm volatile("mov.b32 %0, %1;" : "=r"(dep) : "r"(sv));
-          dep -= v;  // == 0, but the compiler cannot know
+          unsigned d;
+          asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(sv));
+          dep = (int)(d - v);  // == 0, but the compiler cannot know
           break;
         }
         if (atomicCAS(a.busy + cell, 0, 1) == 0) {
-          const int sv2 = ld_relaxed_s32(a.spec_ver + cell);
+          const unsigned sv2 = ld_relaxed_u32(a.spec_ver + cell);
           if (sv2 == v) {
             st_release_s32(a.busy + cell, 0);
-            asm volatile("mov.b32 %0, %1;" : "=r"(dep) : "r"(sv2));
-            dep -= v;
+            unsigned d;
+            asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(sv2));
+            dep = (int)(d - v);
           } else {
             mode = 1;
           }
@@ -497,66 +451,57 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
       if (waited) ++waits;
     }
     mode = __shfl_sync(kFull, mode, 0);
+    st = __shfl_sync(kFull, st, 0);
     long long t2 = clock64();
     cyc_obtain += t2 - t1;
     if (mode == 2) break;
     if (mode == 1) {
-      process_cell(a, T, before, cell, lane, prof);
+      process_cell(a, T, before, cell, st, lane, prof);
       __syncwarp();
       if (lane == 0) {
-        st_release_s32(a.spec_ver + cell, a.version[cell]);
+        st_release_u32(a.spec_ver + cell, st_ver(st));
         st_release_s32(a.busy + cell, 0);
       }
       ++self_processed;
     }
     long long t3 = clock64();
     cyc_self += t3 - t2;
-    // commit (lane 0): slot flip, flags, first_done, scans, versions
+    // commit (lane 0): slot flip, flags, first removal, scans, versions
     if (lane == 0) {
+      unsigned nst[4];
+#pragma unroll
+      for (int d = 0; d < 4; ++d) nst[d] = nbs[d] >= 0 ? ld_relaxed_u32(a.state + nbs[d]) : 0u;
       const SpecRec* rec = a.rec + cell + dep;
-      a.cur[cell] ^= 1;
-      a.flags[cell] = 0;
-      a.first_done[cell] = 1;
       sweeps += __ldcg(&rec->sweeps);
       updates += __ldcg(&rec->updates);
-      const int cxi = cell % g.cells_x, cyi = cell / g.cells_x;
-      int nbs[4] = {cxi > 0 ? cell - 1 : -1, cxi + 1 < g.cells_x ? cell + 1 : -1,
-                    cyi > 0 ? cell - g.cells_x : -1, cyi + 1 < g.cells_y ? cell + g.cells_x : -1};
+      // popped cell: flags cleared, first removal done, slot flipped, +1 version
+      const unsigned ncell = ((st & ~15u) | 16u | (st & 32u)) ^ 32u;
+      st_relaxed_u32(a.state + cell, ncell + kVerOne);
       for (int side = 0; side < 4; ++side) {  // heap_cell.cpp:288-311
         const int nb = nbs[side];
         if (nb < 0) continue;
         const double cand = __ldcg(&rec->cand[side]);
-        if (cand < a.cell_value[nb]) {
-          a.cell_value[nb] = cand;
-          if (H.contains(nb)) H.decrease(nb, cand);
+        if (cand < H.key[nb]) {
+          H.key[nb] = cand;
+          if (H.contains(nb)) H.up(H.pos[nb]);
         }
+        unsigned s2 = nst[side] + kVerOne;
         if (__ldcg(&rec->add[side])) {
-          a.flags[nb] |= __ldcg(&rec->fl[side]);
+          s2 |= __ldcg(&rec->fl[side]);
           if (__ldcg(&rec->monc[side])) {
             ++mon_checks;
             if (__ldcg(&rec->mons[side])) ++mon_single;
           }
-          if (!H.contains(nb)) H.insert(nb, a.cell_value[nb]);
+          if (!H.contains(nb)) H.insert(nb);
         }
+        st_relaxed_u32(a.state + nb, s2);
       }
-      // one release orders the flag / slot-flip writes before the version
-      // bumps (st.release = MEMBAR, no L1 flush); the rest follow it
-      st_release_s32(a.version + cell, a.version[cell] + 1);
-      for (int side = 0; side < 4; ++side)
-        if (nbs[side] >= 0) *(volatile int*)(a.version + nbs[side]) = a.version[nbs[side]] + 1;
       *(volatile int*)a.hsize_pub = H.size;
     }
     __syncwarp();
     cyc_commit += clock64() - t3;
   }
   if (lane == 0) {
-    a.counters[8] = cyc_pop;
-    a.counters[9] = cyc_obtain;
-    a.counters[10] = cyc_self;
-    a.counters[11] = cyc_commit;
-    a.counters[12] = prof[0];
-    a.counters[13] = prof[1];
-    a.counters[14] = prof[2];
     a.counters[0] = removals;
     a.counters[1] = sweeps;
     a.counters[2] = updates;
@@ -565,8 +510,98 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
     a.counters[5] = self_processed;
     a.counters[6] = fast_hits;
     a.counters[7] = waits;
+    a.counters[8] = cyc_pop;
+    a.counters[9] = cyc_obtain;
+    a.counters[10] = cyc_self;
+    a.counters[11] = cyc_commit;
+    a.counters[12] = prof[0];
+    a.counters[13] = prof[1];
+    a.counters[14] = prof[2];
     __threadfence();
     st_release_s32(a.done_flag, 1);
+  }
+}
+
+__global__ void heapcell_spec_kernel(HcArgs a) {
+  extern __shared__ double smem[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const CellGeom& g = a.g;
+  HTile T;
+  T.pu = g.pu;
+  T.U = smem + (size_t)wib * a.tile_doubles;
+  T.Ct = T.U + (size_t)(g.max_h + 2) * g.pu;
+  double* before = T.Ct + (size_t)(g.max_h + 2) * g.pu;  // [4][max_len]
+  T.lock = reinterpret_cast<uint8_t*>(before + 4 * a.max_len);
+
+  // The committer runs alone in CTA 0: every gpu-scope acquire issued on an
+  // SM invalidates that SM's L1 (CCTL.IVALL).  Workers poll with relaxed
+  // loads and acquire once per speculation.
+  if (blockIdx.x == 0) {
+    if (wib != 0) return;
+    if (a.heap_in_smem) {
+      // [tile][key: J doubles][pos: J u16][arr: J u16]
+      double* key = smem + a.tile_doubles;
+      uint16_t* pos = reinterpret_cast<uint16_t*>(key + a.J);
+      uint16_t* arr = pos + a.J;
+      for (int k = lane; k < a.J; k += 32) {
+        key[k] = kInf;
+        pos[k] = 0xFFFFu;
+      }
+      __syncwarp();
+      Heap<uint16_t> H{key, pos, arr, a.harr, a.window, 0, (uint16_t)0xFFFFu};
+      committer(a, H, T, before, lane);
+    } else {
+      Heap<int> H{a.hkey, a.hpos, a.harr, nullptr, 0, 0, -1};
+      committer(a, H, T, before, lane);
+    }
+    return;
+  }
+
+  // ---- worker: speculate cells near the top of the heap ----------------------
+  const int wpc = blockDim.x >> 5;
+  const int wid = (blockIdx.x - 1) * wpc + wib;
+  const int nworkers = (gridDim.x - 1) * wpc;
+  for (;;) {
+    if (ld_relaxed_s32(a.done_flag)) return;
+    int hs = ld_relaxed_s32(a.hsize_pub);
+    if (hs > a.window) hs = a.window;
+    bool worked = false;
+    for (int pidx = wid; pidx < hs; pidx += nworkers) {
+      int cell = -1;
+      unsigned st = 0;
+      if (lane == 0) {
+        cell = ld_relaxed_s32(a.harr + pidx);
+        if (cell >= 0 && cell < a.J) {
+          st = ld_relaxed_u32(a.state + cell);
+          if (ld_relaxed_u32(a.spec_ver + cell) == st_ver(st) ||
+              atomicCAS(a.busy + cell, 0, 1) != 0) {
+            cell = -1;
+          } else {
+            st = ld_acquire_u32(a.state + cell);
+            if (ld_relaxed_u32(a.spec_ver + cell) == st_ver(st)) {
+              st_release_s32(a.busy + cell, 0);
+              cell = -1;
+            }
+          }
+        } else {
+          cell = -1;
+        }
+      }
+      cell = __shfl_sync(kFull, cell, 0);
+      st = __shfl_sync(kFull, st, 0);
+      if (cell < 0) continue;
+      process_cell(a, T, before, cell, st, lane);
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        st_release_u32(a.spec_ver + cell, st_ver(st));
+        st_release_s32(a.busy + cell, 0);
+      }
+      worked = true;
+      break;
+    }
+    if (!worked) __nanosleep(200);
   }
 }
 
@@ -583,13 +618,10 @@ __global__ void heapcell_init_kernel(HcArgs a) {
     if (x < ie - ib && y < je - jb) v = a.u[(jb + y) * a.g.P + a.g.pad + ib + x];
     a.slots[k] = v;  // slot 0 <- the prepared field
     if (r == 0) {
-      a.cur[cell] = 0;
-      a.version[cell] = 0;
-      a.spec_ver[cell] = -1;
+      a.state[cell] = 0u;
+      a.spec_ver[cell] = 0xFFFFFFFFu;
       a.busy[cell] = 0;
-      a.cell_value[cell] = kInf;
-      a.flags[cell] = 0;
-      a.first_done[cell] = 0;
+      a.hkey[cell] = kInf;
       a.hpos[cell] = -1;
       a.harr[cell] = -1;
     }
@@ -606,7 +638,7 @@ __global__ void heapcell_gather_kernel(HcArgs a) {
     int64_t ib, ie, jb, je;
     hc_cell_rect(a.g, cell, ib, ie, jb, je);
     if (x < ie - ib && y < je - jb)
-      a.u[(jb + y) * a.g.P + a.g.pad + ib + x] = slot_ptr(a, a.cur[cell], cell)[r];
+      a.u[(jb + y) * a.g.P + a.g.pad + ib + x] = slot_ptr(a, st_cur(a.state[cell]), cell)[r];
   }
 }
 
@@ -617,12 +649,16 @@ size_t heapcell_smem_bytes(const CellGeom& g, int max_len) {
          (((size_t)g.max_w * g.max_h + 7) & ~(size_t)7);
 }
 
+size_t heapcell_committer_heap_bytes(int J) { return (size_t)J * (sizeof(double) + 4); }
+
 cudaError_t launch_heapcell(const HcArgs& args, int warps_per_cta, int max_ctas, cudaStream_t s,
                             int* launches) {
   const int64_t total = (int64_t)args.J * args.cellsz;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   heapcell_init_kernel<<<blocks, 256, 0, s>>>(args);
-  const size_t smem = (size_t)warps_per_cta * args.tile_doubles * sizeof(double);
+  size_t smem = (size_t)warps_per_cta * args.tile_doubles * sizeof(double);
+  if (args.heap_in_smem)
+    smem = std::max(smem, args.tile_doubles * sizeof(double) + heapcell_committer_heap_bytes(args.J));
   cudaError_t e = cudaFuncSetAttribute(heapcell_spec_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
