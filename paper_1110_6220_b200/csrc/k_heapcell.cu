@@ -50,6 +50,13 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// same load without the compiler barrier, for staging (lets independent
+// loads be issued together)
+__device__ __forceinline__ unsigned ld_relaxed_u32_nb(const unsigned* p) {
+  unsigned v;
+  asm("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -88,7 +95,9 @@ struct Heap {
   __device__ void put(int p, int id) {
     arr[p] = (IdxT)id;
     pos[id] = (IdxT)p;
-    if (pub && p < window) *(volatile int*)(pub + p) = id;
+    // plain store: the published prefix is only a hint for the workers (a
+    // strong store per sift level cost ~150 cycles each on the serial path)
+    if (pub && p < window) pub[p] = id;
   }
   __device__ void up(int p) {
     const int id = arr[p];
@@ -174,7 +183,7 @@ __device__ void mono_sides(int from_side, int out[2]) {  // cells.cpp:49-60
 
 // scan_cell_boundary (heap_cell.cpp:173-239) as warp reductions
 __device__ Scan scan_side(const HcArgs& a, const HTile& T, int side, const double* before,
-                          bool first_removal, int64_t ib, int64_t jb, int cx, int cy, int lane) {
+                          const double* pstrip, bool first_removal, int lane) {
   const bool vertical = (side == WEST || side == EAST);
   const int len = vertical ? T.h : T.w;
   double vmax = -kInf;
@@ -217,9 +226,7 @@ __device__ Scan scan_side(const HcArgs& a, const HTile& T, int side, const doubl
   dec_viol = __any_sync(kFull, dec_viol);
   r.cand = kInf;
   if (vmax < kInf) {  // isfinite(vmax): vmax > -inf always holds here
-    double fprobe;
-    if (vertical) fprobe = __ldg(a.probe[side] + (int64_t)cx * a.g.n + (jb + arg));
-    else fprobe = __ldg(a.probe[side] + (int64_t)cy * a.g.m + (ib + arg));
+    const double fprobe = pstrip[arg];  // preloaded probe strip of this side
     const double hc = vertical ? a.hc_x : a.hc_y;
     r.cand = vmax + 0.5 * (a.h + hc) / fprobe;  // cell_value_candidate (cells.hpp:109-112)
   }
@@ -273,21 +280,32 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
   const int nbs[4] = {cell - 1, cell + 1, cell - g.cells_x, cell + g.cells_x};
   int ncur[4];
 #pragma unroll
-  for (int d = 0; d < 4; ++d) ncur[d] = has_nb[d] ? st_cur(ld_relaxed_u32(a.state + nbs[d])) : 0;
+  for (int d = 0; d < 4; ++d) ncur[d] = has_nb[d] ? st_cur(ld_relaxed_u32_nb(a.state + nbs[d])) : 0;
   const double* own = slot_ptr(a, st_cur(st), cell);
-  // own values; costs of the cell and its cross halo from the global C array
-  for (int k = lane; k < T.w * T.h; k += 32) {
-    const int y = k / T.w, x = k % T.w;
-    T.u(x, y) = __ldcg(own + y * mw + x);
-  }
+  // own values and costs of the cell and its cross halo (one pass, so the
+  // independent loads of an iteration batch are in flight together)
   const int W2 = T.w + 2;
+#pragma unroll 4
   for (int k = lane; k < (T.h + 2) * W2; k += 32) {
     const int y = k / W2 - 1, x = k % W2 - 1;
-    if ((x < 0 || x >= T.w) && (y < 0 || y >= T.h)) continue;
+    const bool inside = x >= 0 && x < T.w && y >= 0 && y < T.h;
+    if (!inside && (x < 0 || x >= T.w) && (y < 0 || y >= T.h)) continue;
     const int64_t gj = jb + y;
     double c = -1.0;
     if (gj >= 0 && gj < g.n) c = __ldg(a.C + gj * g.P + g.pad + ib + x);
+    if (inside) T.u(x, y) = __ldcg(own + y * mw + x);
     T.Ct[(y + 1) * T.pu + (x + 1)] = c;
+  }
+  // the four border probe strips (F at the clamped probe points,
+  // heap_cell.cpp:195-205), used by the scans after the sweeps
+  double* pstrip = before + 4 * a.max_len;
+  for (int t = lane; t < T.h; t += 32) {
+    pstrip[0 * a.max_len + t] = has_nb[0] ? __ldg(a.probe[0] + (int64_t)cx * g.n + jb + t) : 1.0;
+    pstrip[1 * a.max_len + t] = has_nb[1] ? __ldg(a.probe[1] + (int64_t)cx * g.n + jb + t) : 1.0;
+  }
+  for (int t = lane; t < T.w; t += 32) {
+    pstrip[2 * a.max_len + t] = has_nb[2] ? __ldg(a.probe[2] + (int64_t)cy * g.m + ib + t) : 1.0;
+    pstrip[3 * a.max_len + t] = has_nb[3] ? __ldg(a.probe[3] + (int64_t)cy * g.m + ib + t) : 1.0;
   }
   // cross halo values from the neighbours' committed slots (+inf off-grid)
   for (int t = lane; t < T.h; t += 32) {
@@ -347,7 +365,8 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
   for (int side = 0; side < 4; ++side) {
     Scan sc;
     if (has_nb[side]) {
-      sc = scan_side(a, T, side, before + side * a.max_len, first_removal, ib, jb, cx, cy, lane);
+      sc = scan_side(a, T, side, before + side * a.max_len, pstrip + side * a.max_len,
+                     first_removal, lane);
     } else {
       sc.add = false;
       sc.fl = 0;
@@ -385,7 +404,7 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
       H.insert(cell);
       if (a.fast) st_relaxed_u32(a.state + cell, 0xFu);  // Q-cells start with all flags
     }
-    *(volatile int*)a.hsize_pub = H.size;
+    *a.hsize_pub = H.size;
   }
   long long removals = 0, sweeps = 0, updates = 0, mon_checks = 0, mon_single = 0;
   long long self_processed = 0, fast_hits = 0, waits = 0;
@@ -396,7 +415,7 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
     long long t0 = clock64();
     if (lane == 0 && H.size > 0) {
       cell = H.pop();
-      *(volatile int*)a.hsize_pub = H.size;
+      *a.hsize_pub = H.size;
     }
     cell = __shfl_sync(kFull, cell, 0);
     long long t1 = clock64();
@@ -468,35 +487,49 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
     cyc_self += t3 - t2;
     // commit (lane 0): slot flip, flags, first removal, scans, versions
     if (lane == 0) {
+      // every load of the commit is issued before the first heap operation
+      // (one L2 round trip instead of one per side)
       unsigned nst[4];
 #pragma unroll
-      for (int d = 0; d < 4; ++d) nst[d] = nbs[d] >= 0 ? ld_relaxed_u32(a.state + nbs[d]) : 0u;
+      for (int d = 0; d < 4; ++d) nst[d] = nbs[d] >= 0 ? ld_relaxed_u32_nb(a.state + nbs[d]) : 0u;
       const SpecRec* rec = a.rec + cell + dep;
-      sweeps += __ldcg(&rec->sweeps);
-      updates += __ldcg(&rec->updates);
+      double cand[4];
+      unsigned word[4];  // add | fl | monc | mons, one byte each
+#pragma unroll
+      for (int d = 0; d < 4; ++d) cand[d] = __ldcg(&rec->cand[d]);
+      const int rsweeps = __ldcg(&rec->sweeps), rupdates = __ldcg(&rec->updates);
+      const unsigned add4 = __ldcg(reinterpret_cast<const unsigned*>(rec->add));
+      const unsigned fl4 = __ldcg(reinterpret_cast<const unsigned*>(rec->fl));
+      const unsigned mc4 = __ldcg(reinterpret_cast<const unsigned*>(rec->monc));
+      const unsigned ms4 = __ldcg(reinterpret_cast<const unsigned*>(rec->mons));
+#pragma unroll
+      for (int d = 0; d < 4; ++d)
+        word[d] = ((add4 >> (8 * d)) & 0xFFu) | (((fl4 >> (8 * d)) & 0xFFu) << 8) |
+                  (((mc4 >> (8 * d)) & 0xFFu) << 16) | (((ms4 >> (8 * d)) & 0xFFu) << 24);
+      sweeps += rsweeps;
+      updates += rupdates;
       // popped cell: flags cleared, first removal done, slot flipped, +1 version
       const unsigned ncell = ((st & ~15u) | 16u | (st & 32u)) ^ 32u;
       st_relaxed_u32(a.state + cell, ncell + kVerOne);
       for (int side = 0; side < 4; ++side) {  // heap_cell.cpp:288-311
         const int nb = nbs[side];
         if (nb < 0) continue;
-        const double cand = __ldcg(&rec->cand[side]);
-        if (cand < H.key[nb]) {
-          H.key[nb] = cand;
+        if (cand[side] < H.key[nb]) {
+          H.key[nb] = cand[side];
           if (H.contains(nb)) H.up(H.pos[nb]);
         }
         unsigned s2 = nst[side] + kVerOne;
-        if (__ldcg(&rec->add[side])) {
-          s2 |= __ldcg(&rec->fl[side]);
-          if (__ldcg(&rec->monc[side])) {
+        if (word[side] & 0xFFu) {
+          s2 |= (word[side] >> 8) & 0xFFu;
+          if ((word[side] >> 16) & 0xFFu) {
             ++mon_checks;
-            if (__ldcg(&rec->mons[side])) ++mon_single;
+            if (word[side] >> 24) ++mon_single;
           }
           if (!H.contains(nb)) H.insert(nb);
         }
         st_relaxed_u32(a.state + nb, s2);
       }
-      *(volatile int*)a.hsize_pub = H.size;
+      *a.hsize_pub = H.size;
     }
     __syncwarp();
     cyc_commit += clock64() - t3;
@@ -532,7 +565,7 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
   T.U = smem + (size_t)wib * a.tile_doubles;
   T.Ct = T.U + (size_t)(g.max_h + 2) * g.pu;
   double* before = T.Ct + (size_t)(g.max_h + 2) * g.pu;  // [4][max_len]
-  T.lock = reinterpret_cast<uint8_t*>(before + 4 * a.max_len);
+  T.lock = reinterpret_cast<uint8_t*>(before + 8 * a.max_len);  // [4] snapshots + [4] probes
 
   // The committer runs alone in CTA 0: every gpu-scope acquire issued on an
   // SM invalidates that SM's L1 (CCTL.IVALL).  Workers poll with relaxed
@@ -645,7 +678,7 @@ __global__ void heapcell_gather_kernel(HcArgs a) {
 }  // namespace
 
 size_t heapcell_smem_bytes(const CellGeom& g, int max_len) {
-  return sizeof(double) * (2 * (size_t)(g.max_h + 2) * g.pu + 4 * (size_t)max_len) +
+  return sizeof(double) * (2 * (size_t)(g.max_h + 2) * g.pu + 8 * (size_t)max_len) +
          (((size_t)g.max_w * g.max_h + 7) & ~(size_t)7);
 }
 

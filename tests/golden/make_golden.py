@@ -142,12 +142,42 @@ def big():
         json.dump(out, f, indent=1, sort_keys=True)
 
 
+C34_CELLS = {"c3": [16, 32, 64, 24, 48], "c4": [16, 32]}
+
+
+def c34():
+    """BASELINE configs 3 (4097^2 8x8 checkerboard; cell sizes aligned with
+    the 512-node blocks and misaligned) and 4 (4097^2 seeded maze, corner
+    source): sha256 + counters of the reference for every method."""
+    out = {}
+    for name, make in (("c3", configs.config3), ("c4", configs.config4)):
+        p = make().problem
+        for method in ("fsm", "fmm"):
+            t = time.time()
+            r = O.ref_solve(p, method)
+            out[f"{name}/{method}"] = dict(sha256=sha(r.u), ms=r.elapsed_ms, **counters(r))
+            print(name, method, round(time.time() - t, 1), flush=True)
+        for cs in C34_CELLS[name]:
+            cx = p.grid.m // cs
+            for method in ("fmsm", "hcm", "fhcm"):
+                r = O.ref_solve(p, method, cx, cx)
+                out[f"{name}/{method}/{cs}"] = dict(sha256=sha(r.u), cells=cx, ms=r.elapsed_ms,
+                                                    **counters(r))
+                print(name, method, cs, round(r.elapsed_ms), flush=True)
+    with open(os.path.join(HERE, "c34.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
+    ap.add_argument("--c34", action="store_true")
     a = ap.parse_args()
     if not O.have_ref():
         sys.exit("oracle/_ref/libeikref.so missing: run make -C oracle here")
+    if a.c34:
+        c34()
+        sys.exit(0)
     with open(os.path.join(HERE, "kat.json"), "w") as f:
         json.dump(kat(), f, indent=1)
     small()
