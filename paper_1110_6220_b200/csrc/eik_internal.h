@@ -64,16 +64,26 @@ struct SpecRec {
   double cand[4];
   int sweeps, updates;
   uint8_t add[4], fl[4], monc[4], mons[4];
+  unsigned inst;            // instance number (written last)
+  unsigned tag;             // version of the cell the result is valid at
+  unsigned dmask;           // chained: sides whose pending results it assumes
+  unsigned dinst[4];        // ... and their instance numbers
+  unsigned nseq;            // instances written so far (busy holder only)
 };
 
 struct HcArgs {
   CellGeom g;
-  double* slots;            // [2][J][max_h*max_w] per-cell value slots
+  double* slots;            // [3][J][max_h*max_w] per-cell value slots
   int64_t cellsz;           // max_h * max_w
-  unsigned* state;          // [J] flags | first_done<<4 | slot<<5 | version<<8
-  unsigned* spec_ver;       // [J] version the spare slot / record was computed for
-  int* busy;                // [J] a warp is computing the spare slot
-  SpecRec* rec;             // [J]
+  unsigned long long* state;  // [J] packed state word (k_heapcell.cu)
+  unsigned* spec_ver;       // [2][J] tag of the plain / chained speculation
+  int* busy;                // [2][J] a warp is computing that speculation
+  SpecRec* rec;             // [2][J]
+  double* ckey;             // [J] heap key published for the workers (inf = not queued)
+  unsigned* ctag;           // [J] instance number of the last committed result
+  int chain;                // make chained speculations
+  int* wdbg;                // optional debug: [workers][4] phase, cell, kind, time
+  int* owner;               // optional debug: [2][J] last claiming worker
   int* done_flag;
   int* hsize_pub;           // heap size, published for the workers
   int window;               // workers speculate heap positions [0, window)

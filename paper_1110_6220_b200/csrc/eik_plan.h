@@ -53,7 +53,10 @@ struct eik_plan {
   unsigned long long* dCounters = nullptr;
   // heap-cell state
   double* dProbe[4] = {nullptr, nullptr, nullptr, nullptr};
-  unsigned* dState = nullptr;   // packed per-cell state words
+  unsigned long long* dState = nullptr;   // packed per-cell state words
+  double* dCKey = nullptr;                // published heap keys
+  unsigned* dCTag = nullptr;              // last committed instance per cell
+  int hc_chain = 1;
   int hc_heap_in_smem = 0;
   double* dHKey = nullptr;
   int* dHPos = nullptr;

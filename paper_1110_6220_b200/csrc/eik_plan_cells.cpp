@@ -93,6 +93,10 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     P->allocs.push_back(P->dState);
     if ((rc = dalloc(&P->dHKey, J))) return rc;
     P->allocs.push_back(P->dHKey);
+    if ((rc = dalloc(&P->dCKey, J))) return rc;
+    P->allocs.push_back(P->dCKey);
+    if ((rc = dalloc(&P->dCTag, J))) return rc;
+    P->allocs.push_back(P->dCTag);
     if ((rc = dalloc(&P->dHPos, J))) return rc;
     P->allocs.push_back(P->dHPos);
     if ((rc = dalloc(&P->dHArr, J))) return rc;
@@ -101,16 +105,16 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     P->allocs.push_back(P->dInitCells);
     if ((rc = dalloc(&P->dInitValues, J))) return rc;
     P->allocs.push_back(P->dInitValues);
-    if ((rc = dalloc(&P->dCounters, 16))) return rc;
+    if ((rc = dalloc(&P->dCounters, 48))) return rc;
     P->allocs.push_back(P->dCounters);
     const size_t cellsz = (size_t)g.max_w * g.max_h;
-    if ((rc = dalloc(&P->dSlots, 2 * (size_t)J * cellsz))) return rc;
+    if ((rc = dalloc(&P->dSlots, 3 * (size_t)J * cellsz))) return rc;
     P->allocs.push_back(P->dSlots);
-    if ((rc = dalloc(&P->dSpecVer, J))) return rc;
+    if ((rc = dalloc(&P->dSpecVer, 2 * J))) return rc;
     P->allocs.push_back(P->dSpecVer);
-    if ((rc = dalloc(&P->dBusy, J))) return rc;
+    if ((rc = dalloc(&P->dBusy, 2 * J))) return rc;
     P->allocs.push_back(P->dBusy);
-    if ((rc = dalloc(&P->dRec, J))) return rc;
+    if ((rc = dalloc(&P->dRec, 2 * J))) return rc;
     P->allocs.push_back(P->dRec);
     if ((rc = dalloc(&P->dHcMisc, 4))) return rc;
     P->allocs.push_back(P->dHcMisc);
@@ -123,6 +127,9 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     P->hc_heap_in_smem =
         J < 65535 && tile * 8 + heapcell_committer_heap_bytes((int)J) <= 220 * 1024 ? 1 : 0;
     if (std::getenv("EIK_HC_GLOBAL_HEAP")) P->hc_heap_in_smem = 0;
+    // EIK_HC_CHAIN: 0 plain speculations only, 1 chain on the neighbour
+    // expected next (default), 2 on every neighbour expected first
+    if (const char* c = std::getenv("EIK_HC_CHAIN")) P->hc_chain = std::atoi(c);
     // EIK_HC_CTAS=1 runs the committer alone (serial exact replay)
     P->hc_max_ctas = 1 << 20;
     if (const char* w = std::getenv("EIK_HC_CTAS")) P->hc_max_ctas = std::max(1, std::atoi(w));
@@ -274,7 +281,7 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
                      cudaMemcpyHostToDevice, P->stream));
   CK(cudaMemcpyAsync(P->dInitValues, ivals.data(), sizeof(double) * ivals.size(),
                      cudaMemcpyHostToDevice, P->stream));
-  CK(cudaMemsetAsync(P->dCounters, 0, sizeof(unsigned long long) * 16, P->stream));
+  CK(cudaMemsetAsync(P->dCounters, 0, sizeof(unsigned long long) * 48, P->stream));
   CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
                     P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
   HcArgs a;
@@ -304,6 +311,24 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
   a.spec_ver = P->dSpecVer;
   a.busy = P->dBusy;
   a.rec = P->dRec;
+  a.ckey = P->dCKey;
+  a.wdbg = nullptr;
+  a.owner = nullptr;
+  if (std::getenv("EIK_HC_DEBUG")) {
+    static int* dbg = nullptr;
+    static int* own = nullptr;
+    if (!dbg) {
+      cudaMalloc(&dbg, sizeof(int) * 4 * 148 * 64);
+      cudaMemset(dbg, 0, sizeof(int) * 4 * 148 * 64);
+      cudaMalloc(&own, sizeof(int) * 2 * (size_t)(1 << 20));
+    }
+    cudaMemsetAsync(dbg, 0, sizeof(int) * 4 * 148 * 64, P->stream);
+    cudaMemsetAsync(own, 0xFF, sizeof(int) * 2 * (size_t)J, P->stream);
+    a.wdbg = dbg;
+    a.owner = own;
+  }
+  a.ctag = P->dCTag;
+  a.chain = P->hc_chain;
   a.done_flag = P->dHcMisc;
   a.hsize_pub = P->dHcMisc + 1;
   a.window = 4096;
@@ -312,7 +337,7 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
   CK(launch_heapcell(a, P->hc_warps_per_cta, P->hc_max_ctas, P->stream, &launches));
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];
-  unsigned long long cnt[16];
+  unsigned long long cnt[48];
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaMemcpyAsync(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaStreamSynchronize(P->stream));
@@ -320,12 +345,27 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
   if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
   if (st[0] == 3) return fail(EIK_ERR_BUDGET, "heap-cell removal budget exceeded");
-  if (st[0] == 4) return fail(EIK_ERR_CUDA, "heap-cell committer watchdog fired");
+  if (st[0] == 4 || st[0] == 5) {
+    std::fprintf(stderr,
+                 "heapcell stuck: status %d cell %llu busy %llu/%llu state %llx spec %llx/%llx "
+                 "after %llu pops; bad-slot state %llx | owner %llx phase %llu cell %llu kind %llu "
+                 "age %llu kcycles worker %lld\n",
+                 st[0], cnt[24], cnt[25], cnt[26], cnt[27], cnt[28], cnt[29], cnt[30], cnt[31],
+                 (long long)cnt[32], cnt[33], cnt[34], cnt[35], cnt[36], (long long)cnt[37]);
+    return fail(EIK_ERR_CUDA, st[0] == 4 ? "heap-cell committer watchdog fired"
+                                         : "heap-cell slot index out of range");
+  }
   if (std::getenv("EIK_HC_PROFILE"))
     std::fprintf(stderr,
                  "heapcell committer cycles: pop %llu obtain %llu self %llu commit %llu | self: "
-                 "stage %llu sweeps %llu scans %llu\n",
-                 cnt[8], cnt[9], cnt[10], cnt[11], cnt[12], cnt[13], cnt[14]);
+                 "stage %llu sweeps %llu scans %llu | hits %llu (chained %llu) self %llu\n",
+                 cnt[8], cnt[9], cnt[10], cnt[11], cnt[12], cnt[13], cnt[14], cnt[6], cnt[15],
+                 cnt[5]);
+  if (std::getenv("EIK_HC_PROFILE"))
+    std::fprintf(stderr,
+                 "heapcell misses: unchained %llu pending %llu stale %llu wrong-inst %llu "
+                 "other-side %llu | last=self %llu prev-pop-adjacent %llu plain-stale-by-1 %llu\n",
+                 cnt[16], cnt[17], cnt[18], cnt[19], cnt[20], cnt[21], cnt[22], cnt[23]);
   out->spec_self = (int64_t)cnt[5];
   out->spec_hits = (int64_t)cnt[6];
   out->spec_waits = (int64_t)cnt[7];

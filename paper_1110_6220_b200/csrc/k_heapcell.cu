@@ -9,18 +9,27 @@
 // of that changes only when the cell itself or a neighbour is committed, so
 // version[c] = number of commits in {c} u N(c) identifies the inputs:
 //
-//   * worker warps process cells near the top of the heap into the cell's
-//     spare value slot and tag the result record with the version they read;
+//   * worker warps process cells near the top of the heap into a spare value
+//     slot and tag the result record with the version they read (a "plain"
+//     speculation);
+//   * a worker may also process a cell x on top of the pending, not yet
+//     committed results of a set A of neighbours expected to be committed
+//     before x (a "chained" speculation).  Every result carries a unique
+//     instance number and the committer records the last committed instance
+//     of each cell; the chained result is valid iff x's version advanced by
+//     exactly |A| and each y in A last committed the very instance x read.
+//     Neighbours of x are not adjacent to each other, so their commits
+//     commute and the test is exact;
 //   * the committer (CTA 0, warp 0) pops cells in the reference's order and
-//     commits a result only if its tag equals the cell's current version --
-//     a slot flip plus the precomputed scans -- and otherwise processes the
-//     cell itself.
+//     commits a valid result -- a slot flip plus the precomputed scans -- and
+//     otherwise processes the cell itself.
 //
-// Per-cell flags, first-removal bit, committed slot and version share one
-// 32-bit state word, so a commit is a few plain stores and a worker reads a
-// consistent snapshot with one load.  The committer's heap and cell values
-// live in its shared memory when they fit (uint16 indices), else in global.
-// Every value and counter equals the reference's (tests/test_gpu_cells.py).
+// Each cell has three value slots: the committed one and one per speculation
+// kind.  The slot of kind K changes role only when a result of kind K is
+// committed, so a writer whose result went stale only ever writes into a slot
+// no valid result lives in.  The committer's heap and cell values live in its
+// shared memory when they fit (uint16 indices), else in global.  Every value
+// and counter equals the reference's (tests/test_gpu_cells.py).
 #include <algorithm>
 
 #include "eik_internal.h"
@@ -36,26 +45,54 @@ enum { WEST = 0, EAST = 1, SOUTH = 2, NORTH = 3 };
 __device__ const int kFlagOrder[4] = {NE, NW, SE, SW};  // heap_cell.cpp:13-14
 __device__ const int kRotation[4] = {SW, NW, NE, SE};   // heap_cell.cpp:15-16
 
+using u64 = unsigned long long;
+
 // ---- per-cell state word -----------------------------------------------------
-// bits 0-3 raised sweep flags, bit 4 first removal done, bit 5 committed slot,
-// bits 8-31 version (commits in {c} u N(c), mod 2^24)
-__device__ __forceinline__ unsigned st_flags(unsigned s) { return s & 15u; }
-__device__ __forceinline__ bool st_first_done(unsigned s) { return (s >> 4) & 1u; }
-__device__ __forceinline__ int st_cur(unsigned s) { return (int)((s >> 5) & 1u); }
-__device__ __forceinline__ unsigned st_ver(unsigned s) { return s >> 8; }
+// low 32 bits: 0-3 raised sweep flags, 4 first removal done, 5-6 committed
+//   slot, 8-31 version (commits in {c} u N(c), mod 2^24)
+// high 32 bits: 0-1 slot of the plain speculation (the chained one uses the
+//   third)
+__device__ __forceinline__ unsigned st_flags(u64 s) { return (unsigned)s & 15u; }
+__device__ __forceinline__ bool st_first_done(u64 s) { return (s >> 4) & 1u; }
+__device__ __forceinline__ int st_cur(u64 s) { return (int)((s >> 5) & 3u); }
+__device__ __forceinline__ unsigned st_ver(u64 s) { return (unsigned)s >> 8; }
+__device__ __forceinline__ int st_pslot(u64 s) { return (int)((s >> 32) & 3u); }
+__device__ __forceinline__ int kind_slot(u64 s, int kind) {
+  return kind == 0 ? st_pslot(s) : 3 - st_cur(s) - st_pslot(s);
+}
 constexpr unsigned kVerOne = 1u << 8;
+constexpr unsigned kSpecNone = 0xFFFFFFFFu;
+constexpr unsigned kTagMask = 0xFFFFFFu;
 
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// same load without the compiler barrier, for staging (lets independent
-// loads be issued together)
+// same loads without the compiler memory barrier, so independent loads are
+// issued together (still volatile: never hoisted out of a polling loop)
 __device__ __forceinline__ unsigned ld_relaxed_u32_nb(const unsigned* p) {
   unsigned v;
-  asm("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
+}
+__device__ __forceinline__ u64 ld_relaxed_u64(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ u64 ld_relaxed_u64_nb(const u64* p) {
+  u64 v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ u64 ld_acquire_u64(const u64* p) {
+  u64 v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(u64* p, u64 v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
   asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -72,6 +109,9 @@ __device__ __forceinline__ int ld_relaxed_s32(const int* p) {
   int v;
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
+}
+__device__ __forceinline__ bool tag_is(unsigned sv, unsigned v) {
+  return sv != kSpecNone && (sv & kTagMask) == v;
 }
 
 // ---- indexed min-heap over cells keyed by (cell value, id) ------------------
@@ -263,11 +303,19 @@ __device__ __forceinline__ void hc_cell_rect(const CellGeom& g, int cell, int64_
 __device__ __forceinline__ double* slot_ptr(const HcArgs& a, int s, int cell) {
   return a.slots + ((size_t)s * a.J + cell) * a.cellsz;
 }
+__device__ __forceinline__ SpecRec* rec_ptr(const HcArgs& a, int kind, int cell) {
+  return a.rec + (size_t)kind * a.J + cell;
+}
 
-// Process `cell` against the committed state whose word is `st`: stage from
-// the committed slots, sweep, scan, write the spare slot and the record.
-__device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell, unsigned st,
-                             int lane, long long* prof = nullptr) {
+// Process `cell` against the state word `st` into the slot of speculation
+// `kind`: stage own values from the committed slot and the halo from the
+// neighbours' committed slots -- except the sides in `omask`, whose values
+// come from slot oslot[side] (the pending results a chained speculation
+// builds on, whose scans add `cflags` to the cell's flags) -- then sweep,
+// scan and write the record (all fields but the instance number and tags).
+__device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell, int kind, u64 st,
+                             unsigned omask, const int oslot[4], unsigned cflags, int lane,
+                             long long* prof = nullptr) {
   const long long p0 = prof ? clock64() : 0;
   const CellGeom& g = a.g;
   int64_t ib, ie, jb, je;
@@ -280,7 +328,18 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
   const int nbs[4] = {cell - 1, cell + 1, cell - g.cells_x, cell + g.cells_x};
   int ncur[4];
 #pragma unroll
-  for (int d = 0; d < 4; ++d) ncur[d] = has_nb[d] ? st_cur(ld_relaxed_u32_nb(a.state + nbs[d])) : 0;
+  for (int d = 0; d < 4; ++d)
+    ncur[d] = !has_nb[d]          ? 0
+              : (omask >> d) & 1u ? oslot[d]
+                                  : st_cur(ld_relaxed_u64_nb(a.state + nbs[d]));
+  if (lane == 0) {
+    bool bad = kind_slot(st, kind) > 2 || st_cur(st) > 2 || kind_slot(st, kind) == st_cur(st);
+    for (int d = 0; d < 4; ++d) bad = bad || ((omask >> d) & 1u && (unsigned)oslot[d] > 2u);
+    if (bad) {
+      atomicExch(a.status, 5);
+      a.counters[31] = st;
+    }
+  }
   const double* own = slot_ptr(a, st_cur(st), cell);
   // own values and costs of the cell and its cross halo (one pass, so the
   // independent loads of an iteration batch are in flight together)
@@ -307,7 +366,7 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
     pstrip[2 * a.max_len + t] = has_nb[2] ? __ldg(a.probe[2] + (int64_t)cy * g.m + ib + t) : 1.0;
     pstrip[3 * a.max_len + t] = has_nb[3] ? __ldg(a.probe[3] + (int64_t)cy * g.m + ib + t) : 1.0;
   }
-  // cross halo values from the neighbours' committed slots (+inf off-grid)
+  // cross halo values from the neighbours' slots (+inf off-grid)
   for (int t = lane; t < T.h; t += 32) {
     T.u(-1, t) = has_nb[0] ? __ldcg(slot_ptr(a, ncur[0], nbs[0]) + t * mw + (int)(g.base_x - 1))
                            : kInf;
@@ -329,7 +388,7 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
     before[3 * a.max_len + t] = T.u(t, T.h - 1);
   }
   const long long p1 = prof ? clock64() : 0;
-  const unsigned my_flags = st_flags(st);
+  const unsigned my_flags = st_flags(st) | cflags;
   const bool first_removal = !st_first_done(st);
   reset_locks(T, ib > 0, ie < g.m, jb > 0, je < g.n, lane);
   const CellTile ct{T.U, T.Ct, T.lock, T.pu, T.w, T.h};
@@ -355,13 +414,13 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
   }
   for (int o = 16; o > 0; o >>= 1) upd += __shfl_xor_sync(kFull, upd, o);
   const long long p2 = prof ? clock64() : 0;
-  // processed values into the spare slot
-  double* spare = slot_ptr(a, st_cur(st) ^ 1, cell);
+  // processed values into the slot of this speculation kind
+  double* spare = slot_ptr(a, kind_slot(st, kind), cell);
   for (int k = lane; k < T.w * T.h; k += 32) {
     const int y = k / T.w, x = k % T.w;
     spare[y * mw + x] = T.u(x, y);
   }
-  SpecRec* rec = a.rec + cell;
+  SpecRec* rec = rec_ptr(a, kind, cell);
   for (int side = 0; side < 4; ++side) {
     Scan sc;
     if (has_nb[side]) {
@@ -393,6 +452,33 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
   }
 }
 
+// Publish the result process_cell just wrote (all lanes call; lane 0 writes):
+// tag, assumed instances and instance number, then the speculation word, then
+// free the cell.  A chained result assuming |A| commits is valid at version
+// (read version + |A|).
+__device__ void publish(const HcArgs& a, int cell, int kind, u64 st, unsigned dmask,
+                        const unsigned dinst[4], int lane) {
+  SpecRec* rec = rec_ptr(a, kind, cell);
+  const unsigned tag = (st_ver(st) + (unsigned)__popc(dmask)) & kTagMask;
+  unsigned inst = 0;
+  if (lane == 0) {
+    const unsigned n = __ldcg(&rec->nseq) + 1u;  // only the busy holder writes it
+    rec->nseq = n;
+    inst = ((n << 1) | (unsigned)kind) & kTagMask;
+    rec->tag = tag;
+    rec->dmask = dmask;
+    for (int d = 0; d < 4; ++d) rec->dinst[d] = dinst[d];
+  }
+  __threadfence();  // values, record, tag before the instance number
+  __syncwarp();
+  if (lane == 0) {
+    st_relaxed_u32(&rec->inst, inst);
+    st_release_u32(a.spec_ver + (size_t)kind * a.J + cell, tag);
+    if (a.wdbg) a.owner[(size_t)kind * a.J + cell] = 0x60000 | kind;
+    st_release_s32(a.busy + (size_t)kind * a.J + cell, 0);
+  }
+}
+
 // ---- the committer: the reference's heap loop in exact order ----------------
 template <class IdxT>
 __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* before, int lane) {
@@ -402,20 +488,26 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
       const int cell = a.init_cells[k];
       H.key[cell] = a.init_values[k];
       H.insert(cell);
-      if (a.fast) st_relaxed_u32(a.state + cell, 0xFu);  // Q-cells start with all flags
+      a.ckey[cell] = a.init_values[k];
+      if (a.fast) st_relaxed_u64(a.state + cell, (1ull << 32) | 0xFull);  // Q-cells: all flags
     }
     *a.hsize_pub = H.size;
   }
   long long removals = 0, sweeps = 0, updates = 0, mon_checks = 0, mon_single = 0;
-  long long self_processed = 0, fast_hits = 0, waits = 0;
+  long long self_processed = 0, fast_hits = 0, waits = 0, chain_hits = 0;
   long long cyc_pop = 0, cyc_obtain = 0, cyc_self = 0, cyc_commit = 0;
   long long prof[3] = {0, 0, 0};
+  long long miss_cls[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int prev_cell = -1;
+  const unsigned* spec_p = a.spec_ver;
+  const unsigned* spec_c = a.spec_ver + a.J;
   for (;;) {
     int cell = -1;
     long long t0 = clock64();
     if (lane == 0 && H.size > 0) {
       cell = H.pop();
       *a.hsize_pub = H.size;
+      a.ckey[cell] = kInf;
     }
     cell = __shfl_sync(kFull, cell, 0);
     long long t1 = clock64();
@@ -429,39 +521,106 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
     const int cxi = cell % g.cells_x, cyi = cell / g.cells_x;
     const int nbs[4] = {cxi > 0 ? cell - 1 : -1, cxi + 1 < g.cells_x ? cell + 1 : -1,
                         cyi > 0 ? cell - g.cells_x : -1, cyi + 1 < g.cells_y ? cell + g.cells_x : -1};
-    // obtain a result tagged with the current version.  Polls are relaxed (an
-    // acquire would flush this SM's L1); the record is then read through an
-    // address that depends on the observed tag, so it cannot be read early.
-    int mode = 0, dep = 0;  // mode 0: valid speculation, 1: process here
-    unsigned st = 0;
+    // obtain a valid result: the plain speculation if its tag is the current
+    // version, else the chained one if its tag is the current version and
+    // every neighbour it assumed last committed the instance it read, else
+    // process the cell here.  Polls are relaxed (an acquire would flush
+    // this SM's L1); the record is then read through an address that depends
+    // on the observed tag, so it cannot be read early.
+    int mode = 0, kind = 0, dep = 0;  // mode 0: valid speculation, 1: process here
+    u64 st = 0;
     if (lane == 0) {
-      st = ld_relaxed_u32(a.state + cell);
+      st = ld_relaxed_u64(a.state + cell);
       const unsigned v = st_ver(st);
+      unsigned ctn[4];  // only this warp writes ctag
+#pragma unroll
+      for (int d = 0; d < 4; ++d) ctn[d] = nbs[d] >= 0 ? __ldcg(a.ctag + nbs[d]) : kSpecNone;
       long long spins = 0;
       bool waited = false;
       for (;;) {
-        const unsigned sv = ld_relaxed_u32(a.spec_ver + cell);
-        if (sv == v) {
+        const unsigned svp = ld_relaxed_u32_nb(spec_p + cell);
+        const unsigned svc = ld_relaxed_u32_nb(spec_c + cell);
+        if (tag_is(svp, v)) {
           unsigned d;
-          asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(sv));
-          dep = (int)(d - v);  // == 0, but the compiler cannot know
+          asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(svp));
+          dep = (int)((d & kTagMask) - v);  // == 0, but the compiler cannot know
+          kind = 0;
           break;
         }
+        if (tag_is(svc, v)) {
+          unsigned d;
+          asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(svc));
+          const int dd = (int)((d & kTagMask) - v);
+          const SpecRec* r1 = rec_ptr(a, 1, cell + dd);
+          const unsigned dm = __ldcg(&r1->dmask);
+          bool ok = true;
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if ((dm >> k) & 1u) ok = ok && __ldcg(&r1->dinst[k]) == ctn[k];
+          if (ok) {
+            dep = dd;
+            kind = 1;
+            ++chain_hits;
+            break;
+          }
+        }
         if (atomicCAS(a.busy + cell, 0, 1) == 0) {
-          const unsigned sv2 = ld_relaxed_u32(a.spec_ver + cell);
-          if (sv2 == v) {
+          if (a.wdbg) a.owner[cell] = 0x30000;
+          const unsigned sv2 = ld_relaxed_u32(spec_p + cell);
+          if (tag_is(sv2, v)) {
+            if (a.wdbg) a.owner[cell] = 0x40000;
             st_release_s32(a.busy + cell, 0);
             unsigned d;
             asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(sv2));
-            dep = (int)(d - v);
+            dep = (int)((d & kTagMask) - v);
+            kind = 0;
           } else {
             mode = 1;
+            if (a.wdbg) a.owner[cell] = 0x50000;
+            // classify the miss (profiling counters 16..23)
+            const unsigned svc2 = ld_relaxed_u32(spec_c + cell);
+            int cls;
+            if (svc2 == kSpecNone) {
+              cls = 0;  // never chained
+            } else {
+              const unsigned diff = ((svc2 & kTagMask) - v) & kTagMask;
+              if (diff >= 1 && diff <= 4) cls = 1;  // assumed commits not all done
+              else if (diff != 0) cls = 2;          // stale: more commits than assumed
+              else cls = 3;                         // a commit it did not assume
+            }
+            ++miss_cls[cls];
+            if (prev_cell >= 0 && (prev_cell == nbs[0] || prev_cell == nbs[1] ||
+                                   prev_cell == nbs[2] || prev_cell == nbs[3]))
+              ++miss_cls[6];  // the previous pop was a neighbour
+            if (((ld_relaxed_u32(spec_p + cell) & kTagMask) + 1u) == v) ++miss_cls[7];
           }
           break;
         }
         waited = true;
         if (++spins > kSpinCap) {
           atomicExch(a.status, kStatusWatchdog);
+          // diagnostics for the host (EIK_HC_PROFILE)
+          a.counters[24] = (unsigned long long)cell;
+          a.counters[25] = (unsigned long long)(unsigned)ld_relaxed_s32(a.busy + cell);
+          a.counters[26] = (unsigned long long)(unsigned)ld_relaxed_s32(a.busy + a.J + cell);
+          a.counters[27] = ld_relaxed_u64(a.state + cell);
+          a.counters[28] = ld_relaxed_u32(spec_p + cell);
+          a.counters[29] = ld_relaxed_u32(spec_c + cell);
+          a.counters[30] = (unsigned long long)removals;
+          if (a.wdbg) {
+            const int ow0 = a.owner[cell];
+            a.counters[32] = (unsigned long long)ow0;
+            int ow = -1;
+            for (int w = 0; w < 148 * 16; ++w)
+              if (a.wdbg[4 * w + 1] == cell && a.wdbg[4 * w + 0] >= 10) ow = w;
+            a.counters[37] = (unsigned long long)(long long)ow;
+            if (ow >= 0) {
+              a.counters[33] = (unsigned)a.wdbg[4 * ow + 0];
+              a.counters[34] = (unsigned)a.wdbg[4 * ow + 1];
+              a.counters[35] = (unsigned)a.wdbg[4 * ow + 2];
+              a.counters[36] = (unsigned long long)((clock64() >> 10) - a.wdbg[4 * ow + 3]);
+            }
+          }
           mode = 2;
           break;
         }
@@ -475,12 +634,11 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
     cyc_obtain += t2 - t1;
     if (mode == 2) break;
     if (mode == 1) {
-      process_cell(a, T, before, cell, st, lane, prof);
-      __syncwarp();
-      if (lane == 0) {
-        st_release_u32(a.spec_ver + cell, st_ver(st));
-        st_release_s32(a.busy + cell, 0);
-      }
+      const int none[4] = {0, 0, 0, 0};
+      const unsigned noinst[4] = {0, 0, 0, 0};
+      process_cell(a, T, before, cell, 0, st, 0u, none, 0u, lane, prof);
+      publish(a, cell, 0, st, 0u, noinst, lane);
+      kind = 0;
       ++self_processed;
     }
     long long t3 = clock64();
@@ -489,10 +647,10 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
     if (lane == 0) {
       // every load of the commit is issued before the first heap operation
       // (one L2 round trip instead of one per side)
-      unsigned nst[4];
+      u64 nst[4];
 #pragma unroll
-      for (int d = 0; d < 4; ++d) nst[d] = nbs[d] >= 0 ? ld_relaxed_u32_nb(a.state + nbs[d]) : 0u;
-      const SpecRec* rec = a.rec + cell + dep;
+      for (int d = 0; d < 4; ++d) nst[d] = nbs[d] >= 0 ? ld_relaxed_u64_nb(a.state + nbs[d]) : 0ull;
+      const SpecRec* rec = rec_ptr(a, kind, cell + dep);
       double cand[4];
       unsigned word[4];  // add | fl | monc | mons, one byte each
 #pragma unroll
@@ -502,37 +660,55 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
       const unsigned fl4 = __ldcg(reinterpret_cast<const unsigned*>(rec->fl));
       const unsigned mc4 = __ldcg(reinterpret_cast<const unsigned*>(rec->monc));
       const unsigned ms4 = __ldcg(reinterpret_cast<const unsigned*>(rec->mons));
+      const unsigned inst = __ldcg(&rec->inst);
 #pragma unroll
       for (int d = 0; d < 4; ++d)
         word[d] = ((add4 >> (8 * d)) & 0xFFu) | (((fl4 >> (8 * d)) & 0xFFu) << 8) |
                   (((mc4 >> (8 * d)) & 0xFFu) << 16) | (((ms4 >> (8 * d)) & 0xFFu) << 24);
       sweeps += rsweeps;
       updates += rupdates;
-      // popped cell: flags cleared, first removal done, slot flipped, +1 version
-      const unsigned ncell = ((st & ~15u) | 16u | (st & 32u)) ^ 32u;
-      st_relaxed_u32(a.state + cell, ncell + kVerOne);
+      // popped cell: flags cleared, first removal done, the committed kind's
+      // slot becomes current and the old current slot takes its role, +1
+      // version, last commit = itself
+      {
+        const int cur = st_cur(st), ps = st_pslot(st), qs = 3 - cur - ps;
+        const int ncur = kind ? qs : ps, nps = kind ? ps : cur;
+        const unsigned lo = (((unsigned)st & ~(15u | (3u << 5))) | 16u | ((unsigned)ncur << 5)) +
+                            kVerOne;
+        st_relaxed_u64(a.state + cell, (u64)lo | ((u64)nps << 32));
+        a.ctag[cell] = inst;
+      }
       for (int side = 0; side < 4; ++side) {  // heap_cell.cpp:288-311
         const int nb = nbs[side];
         if (nb < 0) continue;
+        bool moved = false;
         if (cand[side] < H.key[nb]) {
           H.key[nb] = cand[side];
-          if (H.contains(nb)) H.up(H.pos[nb]);
+          if (H.contains(nb)) {
+            H.up(H.pos[nb]);
+            moved = true;
+          }
         }
-        unsigned s2 = nst[side] + kVerOne;
+        unsigned lo = (unsigned)nst[side] + kVerOne;
         if (word[side] & 0xFFu) {
-          s2 |= (word[side] >> 8) & 0xFFu;
+          lo |= (word[side] >> 8) & 0xFFu;
           if ((word[side] >> 16) & 0xFFu) {
             ++mon_checks;
             if (word[side] >> 24) ++mon_single;
           }
-          if (!H.contains(nb)) H.insert(nb);
+          if (!H.contains(nb)) {
+            H.insert(nb);
+            moved = true;
+          }
         }
-        st_relaxed_u32(a.state + nb, s2);
+        if (moved) a.ckey[nb] = H.key[nb];
+        st_relaxed_u64(a.state + nb, (u64)lo | (nst[side] & (3ull << 32)));
       }
       *a.hsize_pub = H.size;
     }
     __syncwarp();
     cyc_commit += clock64() - t3;
+    prev_cell = cell;
   }
   if (lane == 0) {
     a.counters[0] = removals;
@@ -550,9 +726,204 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
     a.counters[12] = prof[0];
     a.counters[13] = prof[1];
     a.counters[14] = prof[2];
+    a.counters[15] = chain_hits;
+    for (int k = 0; k < 8; ++k) a.counters[16 + k] = miss_cls[k];
     __threadfence();
     st_release_s32(a.done_flag, 1);
   }
+}
+
+__device__ __forceinline__ void cell_nbs(const CellGeom& g, int cell, int nbs[4]) {
+  const int cx = cell % g.cells_x, cy = cell / g.cells_x;
+  nbs[0] = cx > 0 ? cell - 1 : -1;
+  nbs[1] = cx + 1 < g.cells_x ? cell + 1 : -1;
+  nbs[2] = cy > 0 ? cell - g.cells_x : -1;
+  nbs[3] = cy + 1 < g.cells_y ? cell + g.cells_x : -1;
+}
+
+// A chained speculation of x assuming the set A (|A| = n) is dead -- it can
+// never become valid -- once more than n commits happened in {x} u N(x) since
+// it was read, or a commit that is not one of A's.  k commits happened; c of
+// them are A's (their last committed instance is the one assumed).  Reading
+// x's version before the ctags keeps the test conservative, and both
+// conditions only get more true as commits happen.  Exact when the caller
+// holds x's chained busy flag (the record is then stable).
+__device__ bool chain_dead(const HcArgs& a, int x, unsigned svc, u64 st, const int nbx[4]) {
+  if (svc == kSpecNone) return true;
+  const SpecRec* r = rec_ptr(a, 1, x);
+  const unsigned dm = __ldcg(&r->dmask);
+  const unsigned n = (unsigned)__popc(dm);
+  const unsigned k = (st_ver(st) - (((svc & kTagMask) - n) & kTagMask)) & kTagMask;
+  if (k > n) return true;
+  unsigned c = 0;
+#pragma unroll
+  for (int d = 0; d < 4; ++d)
+    if ((dm >> d) & 1u) c += __ldcg(a.ctag + nbx[d]) == __ldcg(&r->dinst[d]) ? 1u : 0u;
+  return k > c;
+}
+
+// The result of y a neighbour's chained speculation builds on: y's chained
+// result while it is not dead (valid, or waiting for commits of y's own
+// neighbours expected first), else y's plain result if valid; -1 if none.
+__device__ int pick_kind(const HcArgs& a, int y, u64 sty) {
+  int nby[4];
+  cell_nbs(a.g, y, nby);
+  const unsigned svc = ld_relaxed_u32(a.spec_ver + a.J + y);
+  if (svc != kSpecNone && !chain_dead(a, y, svc, sty, nby)) return 1;
+  if (tag_is(ld_relaxed_u32(a.spec_ver + y), st_ver(sty))) return 0;
+  return -1;
+}
+
+struct Job {
+  int cell, kind;
+  u64 st;
+  unsigned omask, cflags;
+  int oslot[4];
+  unsigned dinst[4];
+};
+
+// Claim a chained speculation of x on the current results of its neighbours
+// on the sides in amask.  For each y: the instance number of y's result is
+// read first (acquire), y's state and the record's tag after it.  A tag at
+// most 4 ahead of y's version means that instance was not committed when y's
+// state was read -- after x's state was read -- so its values are still in
+// y's slot of that kind.  A result replaced meanwhile can never be committed,
+// so neither can this speculation.
+__device__ bool claim_chain(const HcArgs& a, int x, const int nbx[4], unsigned amask, Job& j) {
+  if (atomicCAS(a.busy + (size_t)a.J + x, 0, 1) != 0) return false;
+  const u64 st = ld_acquire_u64(a.state + x);
+  bool ok = chain_dead(a, x, ld_relaxed_u32(a.spec_ver + a.J + x), st, nbx);
+  j.cflags = 0;
+  for (int d = 0; d < 4 && ok; ++d) {
+    j.oslot[d] = 0;
+    j.dinst[d] = 0;
+    if (!((amask >> d) & 1u)) continue;
+    const int y = nbx[d];
+    const int yk = pick_kind(a, y, ld_relaxed_u64(a.state + y));
+    if (yk < 0) {
+      ok = false;
+      break;
+    }
+    const SpecRec* ry = rec_ptr(a, yk, y);
+    const unsigned inst = ld_acquire_u32(&ry->inst);
+    const u64 sty = ld_relaxed_u64(a.state + y);
+    const unsigned ahead = (__ldcg(&ry->tag) - st_ver(sty)) & kTagMask;
+    if (inst == kSpecNone || ahead > 4) {
+      ok = false;
+      break;
+    }
+    const int xside_of_y = d ^ 1;
+    if (__ldcg(&ry->add[xside_of_y])) j.cflags |= __ldcg(&ry->fl[xside_of_y]);
+    j.oslot[d] = kind_slot(sty, yk);
+    j.dinst[d] = inst;
+  }
+  if (!ok) {
+    st_release_s32(a.busy + (size_t)a.J + x, 0);
+    return false;
+  }
+  j.cell = x;
+  j.kind = 1;
+  j.st = st;
+  j.omask = amask;
+  return true;
+}
+
+__device__ __forceinline__ bool key_before(double ka, int a_id, double kb, int b_id) {
+  return ka < kb || (ka == kb && a_id < b_id);
+}
+
+// Worker lane 0: choose and claim a job around heap position pidx.  For the
+// queued cell c there:
+//   1. a chained speculation of c on its neighbours queued above it (they
+//      will be committed first unless keys change), if its chained result is
+//      dead; else a plain speculation if the plain result is stale;
+//   2. chained speculations of c's neighbours that c's commit will queue or
+//      move up (the front's next cells), on c and on their other neighbours
+//      queued above them.
+__device__ bool pick_job(const HcArgs& a, int pidx, Job& j, int wid) {
+  const int cell = ld_relaxed_s32(a.harr + pidx);
+  if (cell < 0 || cell >= a.J) return false;
+  int nbs[4];
+  cell_nbs(a.g, cell, nbs);
+  u64 st = ld_relaxed_u64_nb(a.state + cell);
+  const unsigned svp = ld_relaxed_u32_nb(a.spec_ver + cell);
+  const unsigned svc = ld_relaxed_u32_nb(a.spec_ver + a.J + cell);
+  double kc = kInf, knb[4] = {kInf, kInf, kInf, kInf};
+  unsigned amask = 0;
+  if (a.chain) {
+    kc = __ldcg(a.ckey + cell);
+#pragma unroll
+    for (int d = 0; d < 4; ++d) knb[d] = nbs[d] >= 0 ? __ldcg(a.ckey + nbs[d]) : kInf;
+    double kb = kc;
+    int yb = cell;
+#pragma unroll
+    for (int d = 0; d < 4; ++d)
+      if (nbs[d] >= 0 && knb[d] < kInf && key_before(knb[d], nbs[d], kc, cell)) {
+        amask |= 1u << d;
+        if (key_before(knb[d], nbs[d], kb, yb)) {
+          kb = knb[d];
+          yb = nbs[d];
+        }
+      }
+    // chain mode 1: only the neighbour expected next; 2: all expected first
+    if (a.chain == 1 && amask)
+      for (int d = 0; d < 4; ++d)
+        if (nbs[d] == yb) amask = 1u << d;
+  }
+  // 1. the queued cell itself
+  if (amask && chain_dead(a, cell, svc, st, nbs) && claim_chain(a, cell, nbs, amask, j))
+    return true;
+  if (!tag_is(svp, st_ver(st)) && atomicCAS(a.busy + cell, 0, 1) == 0) {
+    if (a.wdbg) {
+      a.owner[cell] = 0x10000;
+      a.wdbg[4 * wid + 0] = 10;
+      a.wdbg[4 * wid + 1] = cell;
+      a.wdbg[4 * wid + 3] = (int)(clock64() >> 10);
+    }
+    st = ld_acquire_u64(a.state + cell);
+    if (a.wdbg) a.wdbg[4 * wid + 0] = 11;
+    if (!tag_is(ld_relaxed_u32(a.spec_ver + cell), st_ver(st))) {
+      j.cell = cell;
+      j.kind = 0;
+      j.st = st;
+      j.omask = 0;
+      j.cflags = 0;
+      for (int d = 0; d < 4; ++d) j.oslot[d] = 0, j.dinst[d] = 0;
+      if (a.wdbg) a.wdbg[4 * wid + 0] = 12;
+      return true;
+    }
+    if (a.wdbg) a.owner[cell] = 0x20000;
+    st_release_s32(a.busy + cell, 0);
+  }
+  if (!a.chain) return false;
+  // 2. neighbours that the commit of this cell's result queues or moves up
+  const int ck = pick_kind(a, cell, st);
+  if (ck < 0) return false;
+  const SpecRec* rc = rec_ptr(a, ck, cell);
+  for (int d = 0; d < 4; ++d) {
+    const int x = nbs[d];
+    if (x < 0) continue;
+    const double cand = __ldcg(&rc->cand[d]);
+    if (!__ldcg(&rc->add[d]) && !(cand < knb[d])) continue;
+    const double kx = cand < knb[d] ? cand : knb[d];  // x's key after this commit
+    int nbx[4];
+    cell_nbs(a.g, x, nbx);
+    unsigned am = 0;
+    for (int e = 0; e < 4; ++e) {
+      const int y = nbx[e];
+      if (y < 0) continue;
+      if (y == cell) {
+        am |= 1u << e;
+        continue;
+      }
+      const double ky = a.chain == 2 ? __ldcg(a.ckey + y) : kInf;
+      if (ky < kInf && key_before(ky, y, kx, x)) am |= 1u << e;
+    }
+    if (!chain_dead(a, x, ld_relaxed_u32(a.spec_ver + a.J + x), ld_relaxed_u64(a.state + x), nbx))
+      continue;
+    if (claim_chain(a, x, nbx, am, j)) return true;
+  }
+  return false;
 }
 
 __global__ void heapcell_spec_kernel(HcArgs a) {
@@ -596,41 +967,46 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
   const int wid = (blockIdx.x - 1) * wpc + wib;
   const int nworkers = (gridDim.x - 1) * wpc;
   for (;;) {
-    if (ld_relaxed_s32(a.done_flag)) return;
-    int hs = ld_relaxed_s32(a.hsize_pub);
+    // lane 0 reads the shared words and broadcasts them: lanes reading them
+    // independently could see different values, run different trip counts
+    // and meet at mismatched warp collectives (a deadlock)
+    int done = 0, hs = 0;
+    if (lane == 0) {
+      done = ld_relaxed_s32(a.done_flag);
+      hs = ld_relaxed_s32(a.hsize_pub);
+    }
+    if (__shfl_sync(kFull, done, 0)) return;
+    hs = __shfl_sync(kFull, hs, 0);
     if (hs > a.window) hs = a.window;
     bool worked = false;
     for (int pidx = wid; pidx < hs; pidx += nworkers) {
-      int cell = -1;
-      unsigned st = 0;
-      if (lane == 0) {
-        cell = ld_relaxed_s32(a.harr + pidx);
-        if (cell >= 0 && cell < a.J) {
-          st = ld_relaxed_u32(a.state + cell);
-          if (ld_relaxed_u32(a.spec_ver + cell) == st_ver(st) ||
-              atomicCAS(a.busy + cell, 0, 1) != 0) {
-            cell = -1;
-          } else {
-            st = ld_acquire_u32(a.state + cell);
-            if (ld_relaxed_u32(a.spec_ver + cell) == st_ver(st)) {
-              st_release_s32(a.busy + cell, 0);
-              cell = -1;
-            }
-          }
-        } else {
-          cell = -1;
-        }
+      Job j;
+      int got = 0;
+      if (lane == 0) got = pick_job(a, pidx, j, wid) ? 1 : 0;
+      if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 2] = 100 + got;
+      if (!__shfl_sync(kFull, got, 0)) continue;
+      if (lane == 0 && a.wdbg) {
+        a.wdbg[4 * wid + 0] = 1;
+        a.wdbg[4 * wid + 1] = j.cell;
+        a.wdbg[4 * wid + 2] = j.kind;
+        a.wdbg[4 * wid + 3] = (int)(clock64() >> 10);
+        a.owner[(size_t)j.kind * a.J + j.cell] = 0x70000 | wid;
       }
-      cell = __shfl_sync(kFull, cell, 0);
-      st = __shfl_sync(kFull, st, 0);
-      if (cell < 0) continue;
-      process_cell(a, T, before, cell, st, lane);
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) {
-        st_release_u32(a.spec_ver + cell, st_ver(st));
-        st_release_s32(a.busy + cell, 0);
+      j.cell = __shfl_sync(kFull, j.cell, 0);
+      j.kind = __shfl_sync(kFull, j.kind, 0);
+      j.st = __shfl_sync(kFull, j.st, 0);
+      j.omask = __shfl_sync(kFull, j.omask, 0);
+      j.cflags = __shfl_sync(kFull, j.cflags, 0);
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        j.oslot[d] = __shfl_sync(kFull, j.oslot[d], 0);
+        j.dinst[d] = __shfl_sync(kFull, j.dinst[d], 0);
       }
+      if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 13;
+      process_cell(a, T, before, j.cell, j.kind, j.st, j.omask, j.oslot, j.cflags, lane);
+      if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 2;
+      publish(a, j.cell, j.kind, j.st, j.omask, j.dinst, lane);
+      if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 3;
       worked = true;
       break;
     }
@@ -651,9 +1027,18 @@ __global__ void heapcell_init_kernel(HcArgs a) {
     if (x < ie - ib && y < je - jb) v = a.u[(jb + y) * a.g.P + a.g.pad + ib + x];
     a.slots[k] = v;  // slot 0 <- the prepared field
     if (r == 0) {
-      a.state[cell] = 0u;
-      a.spec_ver[cell] = 0xFFFFFFFFu;
-      a.busy[cell] = 0;
+      a.state[cell] = 1ull << 32;  // committed slot 0, plain slot 1, chained slot 2
+      for (int kind = 0; kind < 2; ++kind) {
+        a.spec_ver[(size_t)kind * a.J + cell] = kSpecNone;
+        a.busy[(size_t)kind * a.J + cell] = 0;
+        SpecRec* rec = rec_ptr(a, kind, cell);
+        rec->inst = kSpecNone;
+        rec->nseq = 0;
+        rec->tag = kSpecNone;
+        rec->dmask = 0;
+      }
+      a.ckey[cell] = kInf;
+      a.ctag[cell] = kSpecNone;
       a.hkey[cell] = kInf;
       a.hpos[cell] = -1;
       a.harr[cell] = -1;
