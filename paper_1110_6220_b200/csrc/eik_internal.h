@@ -74,7 +74,8 @@ struct SpecRec {
 struct HcArgs {
   CellGeom g;
   double* slots;            // [3][J][max_h*max_w] per-cell value slots
-  int64_t cellsz;           // max_h * max_w
+  int64_t cellsz;           // max_h * spw
+  int spw;                  // slot row pitch: max_w rounded up to even
   unsigned long long* state;  // [J] packed state word (k_heapcell.cu)
   unsigned* spec_ver;       // [2][J] tag of the plain / chained speculation
   int* busy;                // [2][J] a warp is computing that speculation
@@ -82,20 +83,23 @@ struct HcArgs {
   double* ckey;             // [J] heap key published for the workers (inf = not queued)
   unsigned* ctag;           // [J] instance number of the last committed result
   int chain;                // make chained speculations
+  int idle_ns;              // worker back-off when it found nothing to do
   int* wdbg;                // optional debug: [workers][4] phase, cell, kind, time
   int* owner;               // optional debug: [2][J] last claiming worker
   int* done_flag;
   int* hsize_pub;           // heap size, published for the workers
   int window;               // workers speculate heap positions [0, window)
   int64_t tile_doubles;     // per-warp smem
-  int heap_in_smem;         // committer heap + cell values in its shared memory
+  int heap_cap;             // >0: committer heap entries in shared memory, capacity;
+                            // 0: entries in global memory (hkey + harr)
   const double* C;          // padded h/F
   double* u;                // padded values
   const double* probe[4];   // F at border probe points: W/E [cells_x*n], S/N [cells_y*m]
   double h, hc_x, hc_y;
-  double* hkey;             // [J] cell values = heap keys (global-heap mode)
-  int* hpos;                // [J] (global-heap mode)
-  int* harr;                // [J] heap array; published prefix in smem mode
+  double* cval;             // [J] cell values (heap_cell.cpp cell_value)
+  double* hkey;             // [J] heap entry keys (global-entry mode)
+  int* hpos;                // [J] heap position of every cell, -1 if not queued
+  int* harr;                // [J] heap entry ids: published prefix / global entries
   const int* init_cells;    // Q-cells in ascending id order with their initial values
   const double* init_values;
   int n_init;
@@ -108,7 +112,7 @@ struct HcArgs {
 };
 
 size_t heapcell_smem_bytes(const CellGeom& g, int max_len);
-size_t heapcell_committer_heap_bytes(int J);
+size_t heapcell_committer_heap_bytes(int cap);
 cudaError_t launch_heapcell(const HcArgs& a, int warps_per_cta, int max_ctas, cudaStream_t s,
                             int* launches);
 

@@ -57,7 +57,8 @@ struct eik_plan {
   double* dCKey = nullptr;                // published heap keys
   unsigned* dCTag = nullptr;              // last committed instance per cell
   int hc_chain = 1;
-  int hc_heap_in_smem = 0;
+  int hc_heap_cap = 0;                    // committer heap capacity in smem (0 = global)
+  double* dCVal = nullptr;                // cell values
   double* dHKey = nullptr;
   int* dHPos = nullptr;
   int* dHArr = nullptr;

@@ -68,6 +68,8 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
   g.max_w = (int)(P->g.m - (c->cells_x - 1) * g.base_x);
   g.max_h = (int)(P->g.n - (c->cells_y - 1) * g.base_y);
   g.pu = even_up(g.max_w + 2);
+  // heap-cell tiles put node x at column x+2 (16-byte aligned value pairs)
+  if (P->method == EIK_HCM || P->method == EIK_FHCM) g.pu = even_up(g.max_w + 3);
   g.pc = even_up(g.max_w);
   g.tile_doubles = 2 * (int64_t)(g.max_h + 2) * g.pu;  // values + costs, both with halo
   if (g.max_h > 32 * 4)
@@ -97,6 +99,8 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     P->allocs.push_back(P->dCKey);
     if ((rc = dalloc(&P->dCTag, J))) return rc;
     P->allocs.push_back(P->dCTag);
+    if ((rc = dalloc(&P->dCVal, J))) return rc;
+    P->allocs.push_back(P->dCVal);
     if ((rc = dalloc(&P->dHPos, J))) return rc;
     P->allocs.push_back(P->dHPos);
     if ((rc = dalloc(&P->dHArr, J))) return rc;
@@ -107,7 +111,7 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     P->allocs.push_back(P->dInitValues);
     if ((rc = dalloc(&P->dCounters, 48))) return rc;
     P->allocs.push_back(P->dCounters);
-    const size_t cellsz = (size_t)g.max_w * g.max_h;
+    const size_t cellsz = (size_t)even_up(g.max_w) * g.max_h;  // even slot pitch
     if ((rc = dalloc(&P->dSlots, 3 * (size_t)J * cellsz))) return rc;
     P->allocs.push_back(P->dSlots);
     if ((rc = dalloc(&P->dSpecVer, 2 * J))) return rc;
@@ -119,14 +123,21 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     if ((rc = dalloc(&P->dHcMisc, 4))) return rc;
     P->allocs.push_back(P->dHcMisc);
     // per-warp tile: values + costs with halo, 4 border snapshots, lock bytes
-    const size_t tile = (smem + sizeof(double) - 1) / sizeof(double);
+    const size_t tile = ((smem + sizeof(double) - 1) / sizeof(double) + 1) & ~(size_t)1;
     P->cg.tile_doubles = (int64_t)tile;
     P->hc_warps_per_cta = (int)std::max<size_t>(1, std::min<size_t>(8, kTileBudget / (tile * 8)));
     // the committer's heap + cell values go to its shared memory when they
     // fit next to its tile (uint16 heap indices)
-    P->hc_heap_in_smem =
-        J < 65535 && tile * 8 + heapcell_committer_heap_bytes((int)J) <= 220 * 1024 ? 1 : 0;
-    if (std::getenv("EIK_HC_GLOBAL_HEAP")) P->hc_heap_in_smem = 0;
+    {
+      const size_t room = 220 * 1024 > tile * 8 ? 220 * 1024 - tile * 8 : 0;
+      const size_t cap = std::min<size_t>((size_t)J, room / heapcell_committer_heap_bytes(1));
+      P->hc_heap_cap = cap >= 64 ? (int)cap : 0;
+    }
+    if (std::getenv("EIK_HC_GLOBAL_HEAP")) P->hc_heap_cap = 0;
+    // EIK_HC_HEAP_CAP=n caps the shared-memory heap (exercises the overflow
+    // fallback in tests)
+    if (const char* c = std::getenv("EIK_HC_HEAP_CAP"))
+      P->hc_heap_cap = std::min(P->hc_heap_cap, std::max(1, std::atoi(c)));
     // EIK_HC_CHAIN: 0 plain speculations only, 1 chain on the neighbour
     // expected next (default), 2 on every neighbour expected first
     if (const char* c = std::getenv("EIK_HC_CHAIN")) P->hc_chain = std::atoi(c);
@@ -276,6 +287,7 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
     ivals[k] = init[k].second;
   }
   int launches = 0;
+retry:  // after a committer heap overflow, with the heap in global memory
   CK(cudaEventRecord(P->ev0, P->stream));
   CK(cudaMemcpyAsync(P->dInitCells, icells.data(), sizeof(int) * icells.size(),
                      cudaMemcpyHostToDevice, P->stream));
@@ -293,7 +305,8 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
   a.hc_x = (double)(P->g.m / P->cells_x) * P->g.h;  // cells.cpp:44-45
   a.hc_y = (double)(P->g.n / P->cells_y) * P->g.h;
   a.state = P->dState;
-  a.heap_in_smem = P->hc_heap_in_smem;
+  a.heap_cap = P->hc_heap_cap;
+  a.cval = P->dCVal;
   a.hkey = P->dHKey;
   a.hpos = P->dHPos;
   a.harr = P->dHArr;
@@ -307,7 +320,8 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
   a.budget = 100LL * J + 16;
   a.max_len = P->max_len;
   a.slots = P->dSlots;
-  a.cellsz = (int64_t)P->cg.max_w * P->cg.max_h;
+  a.spw = even_up(P->cg.max_w);
+  a.cellsz = (int64_t)a.spw * P->cg.max_h;
   a.spec_ver = P->dSpecVer;
   a.busy = P->dBusy;
   a.rec = P->dRec;
@@ -329,6 +343,8 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
   }
   a.ctag = P->dCTag;
   a.chain = P->hc_chain;
+  a.idle_ns = 200;
+  if (const char* c = std::getenv("EIK_HC_IDLE_NS")) a.idle_ns = std::atoi(c);
   a.done_flag = P->dHcMisc;
   a.hsize_pub = P->dHcMisc + 1;
   a.window = 4096;
@@ -341,6 +357,11 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaMemcpyAsync(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaStreamSynchronize(P->stream));
+  if (st[0] == 6 && P->hc_heap_cap > 0) {
+    P->hc_heap_cap = 0;
+    CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
+    goto retry;
+  }
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
   if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
@@ -358,9 +379,10 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
   if (std::getenv("EIK_HC_PROFILE"))
     std::fprintf(stderr,
                  "heapcell committer cycles: pop %llu obtain %llu self %llu commit %llu | self: "
-                 "stage %llu sweeps %llu scans %llu | hits %llu (chained %llu) self %llu\n",
+                 "stage %llu sweeps %llu scans %llu | hits %llu (chained %llu) self %llu | "
+                 "heap max %llu cap %d | stage: states %llu chunk0 %llu\n",
                  cnt[8], cnt[9], cnt[10], cnt[11], cnt[12], cnt[13], cnt[14], cnt[6], cnt[15],
-                 cnt[5]);
+                 cnt[5], cnt[38], P->hc_heap_cap, cnt[39], cnt[40]);
   if (std::getenv("EIK_HC_PROFILE"))
     std::fprintf(stderr,
                  "heapcell misses: unchained %llu pending %llu stale %llu wrong-inst %llu "

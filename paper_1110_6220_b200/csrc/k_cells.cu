@@ -80,6 +80,7 @@ __global__ void fmsm_dataflow_kernel(FmsmArgs a) {
   const int wib = threadIdx.x >> 5;
   CellTile T;
   T.pu = a.g.pu;
+  T.ox = 1;
   T.U = smem + (size_t)wib * a.g.tile_doubles;
   T.Ct = T.U + (size_t)(a.g.max_h + 2) * a.g.pu;
   T.lock = nullptr;

@@ -21,10 +21,11 @@ enum { kSW = 0, kNW = 1, kNE = 2, kSE = 3 };  // SweepDir (local_update.hpp:23)
 constexpr int kMaxSlots = 4;                   // cells up to 128 rows
 
 struct CellTile {
-  double* U;        // (h+2) x pu values with cross halo, node (x,y) at (y+1)*pu + x+1
+  double* U;        // (h+2) x pu values with cross halo, node (x,y) at (y+1)*pu + x+ox
   double* Ct;       // (h+2) x pu costs with halo; < 0 marks exits (and off-grid halo)
   uint8_t* lock;    // h x w lock bytes (1 = unlocked), locked sweeps only
   int pu, w, h;
+  int ox;           // column of node x = 0 in a tile row (the west halo is ox-1)
 };
 
 // MODE 0: node_update over all non-exit nodes (FSM inside a cell,
@@ -59,7 +60,7 @@ __device__ bool cell_sweep_ns(const CellTile& T, int dir, int lane, long long& u
     const int b = lane + 32 * r;
     rvalid[r] = b < h;
     const int y = jasc ? b : h - 1 - b;
-    vbase[r] = rvalid[r] ? (y + 1) * T.pu + (x0 + 1) : 0;
+    vbase[r] = rvalid[r] ? (y + 1) * T.pu + (x0 + T.ox) : 0;
     lbase[r] = rvalid[r] ? y * w + x0 : 0;
     res_prev[r] = rvalid[r] ? T.U[vbase[r] - dx] : kInf;  // frozen halo column
     c_prev[r] = -1.0;
@@ -72,7 +73,7 @@ __device__ bool cell_sweep_ns(const CellTile& T, int dir, int lane, long long& u
     for (int r = 0; r < NS; ++r) {
       const int a = s - lane - 32 * r;
       const bool act = rvalid[r] && a >= 0 && a < w;
-      const int o = act ? vbase[r] + dx * a : T.pu + 1;  // a safe in-tile offset
+      const int o = act ? vbase[r] + dx * a : T.pu + T.ox;  // a safe in-tile offset
       cur[r] = act ? T.U[o] : kInf;
       eo[r] = act ? T.U[o + dx] : kInf;   // old E (halo at the last column)
       no[r] = act ? T.U[o + dyp] : kInf;  // old N (halo on the last row)
@@ -174,8 +175,103 @@ __device__ bool cell_sweep_ns(const CellTile& T, int dir, int lane, long long& u
   return __any_sync(kFull, changed);
 }
 
+// Locking sweep (MODE 2) for cells of at most 32 rows, one node per lane per
+// step: the dataflow of cell_sweep_ns<2, 1> restated for the common small
+// cells with branch-free operand loads (clamped in-tile addresses, selected
+// afterwards) and the fp64 update skipped warp-uniformly when no lane holds
+// an unlocked node (most steps of a locked sweep).  Stores are predicated.
+__device__ __forceinline__ bool cell_sweep_lock32(const CellTile& T, int dir, int lane,
+                                                  long long& updates_out) {
+  const bool iasc = (dir == kSW || dir == kNW);
+  const bool jasc = (dir == kSW || dir == kSE);
+  const int w = T.w, h = T.h, pu = T.pu;
+  const int dx = iasc ? 1 : -1;
+  const int dyp = jasc ? pu : -pu;
+  const int dyl = jasc ? w : -w;
+  const int x0 = iasc ? 0 : w - 1;
+  const int b = lane;
+  const bool rv = b < h;
+  const int y = jasc ? b : h - 1 - b;
+  const int ox = T.ox;
+  const int vb = rv ? (y + 1) * pu + (x0 + ox) : pu + ox;  // value offset of a = 0
+  const int lb = rv ? y * w + x0 : 0;                    // lock offset of a = 0
+  double* __restrict__ U = T.U;
+  const double* __restrict__ C = T.Ct;
+  uint8_t* __restrict__ L = T.lock;
+  double wv = rv ? U[vb - dx] : kInf;  // W: frozen halo column, then own new values
+  double cw = -1.0;                    // W cost (< 0: halo or exit, never unlocked)
+  bool unW = false;                    // the W neighbour unlocked this node
+  unsigned nm = 0u;                    // last step's ballot of "unlock my N"
+  int updates = 0;
+  bool changed = false;
+  double q_cur, q_cc, q_e, q_ce, q_n, q_cn, q_cs, q_hs;
+  int q_lk;
+  auto load = [&](int s) {
+    const int a = s - b;
+    const bool act = rv && a >= 0 && a < w;
+    const int o = act ? vb + dx * a : pu + ox;  // (0,0): every neighbour is in the tile
+    q_cur = U[o];
+    q_cc = C[o];
+    q_e = U[o + dx];
+    q_ce = C[o + dx];
+    q_n = U[o + dyp];
+    q_cn = C[o + dyp];
+    q_cs = C[o - dyp];
+    q_hs = U[o - dyp];
+    q_lk = L[act ? lb + dx * a : 0];
+  };
+  load(0);
+  const int last = (h - 1) + (w - 1);
+  for (int s = 0; s <= last; ++s) {
+    const double cur = q_cur, cc = q_cc, e = q_e, ce = q_ce, n = q_n, cn = q_cn, cs = q_cs,
+                 hs = q_hs;
+    const int lk = q_lk;
+    if (s < last) load(s + 1);  // prefetch while this step computes
+    const int a = s - b;
+    const bool act = rv && a >= 0 && a < w;
+    // the S neighbour's new value and N-unlock: lane-1 at the previous step
+    double sv = __shfl_up_sync(kFull, wv, 1);
+    unsigned sbit = (nm >> ((lane + 31) & 31)) & 1u;
+    if (b == 0) {
+      sv = hs;
+      sbit = 0u;
+    }
+    const bool proc = act && cc >= 0.0 && (lk != 0 || unW || sbit != 0u);
+    bool un_n = false, nunW = false;
+    double res = cur;
+    if (__any_sync(kFull, proc)) {
+      const int o = act ? vb + dx * a : pu + ox;
+      const int lo = act ? lb + dx * a : 0;
+      const double cand = node_update4(e, wv, n, sv, cc);
+      const bool dec = proc && cand < cur;
+      if (dec) {
+        res = cand;
+        changed = true;
+        U[o] = cand;
+        // already-processed W and S neighbours: unlocked for the next sweep
+        if (a > 0 && cw >= 0.0 && wv > cand) L[lo - dx] = 1;
+        if (b > 0 && cs >= 0.0 && sv > cand) L[lo - dyl] = 1;
+        un_n = (b + 1 < h) && cn >= 0.0 && n > cand;
+        nunW = (a + 1 < w) && ce >= 0.0 && e > cand;
+      }
+      if (proc) {  // relock on processing (heap_cell.cpp:110-111)
+        L[lo] = 0;
+        ++updates;
+      }
+    }
+    unW = nunW;
+    nm = __ballot_sync(kFull, un_n);
+    if (act) wv = res;
+    cw = act ? cc : -1.0;
+    __syncwarp();
+  }
+  updates_out += updates;
+  return __any_sync(kFull, changed);
+}
+
 template <int MODE>
 __device__ bool cell_sweep(const CellTile& T, int dir, int lane, long long& updates) {
+  if (MODE == 2 && T.h <= 32) return cell_sweep_lock32(T, dir, lane, updates);
   if (T.h <= 32) return cell_sweep_ns<MODE, 1>(T, dir, lane, updates);
   if (T.h <= 64) return cell_sweep_ns<MODE, 2>(T, dir, lane, updates);
   if (T.h <= 96) return cell_sweep_ns<MODE, 3>(T, dir, lane, updates);

@@ -115,78 +115,108 @@ __device__ __forceinline__ bool tag_is(unsigned sv, unsigned v) {
 }
 
 // ---- indexed min-heap over cells keyed by (cell value, id) ------------------
-// indexed_min_heap.hpp:11-106, ties to the smaller id.  key[] is the cell
-// value array itself (the reference keeps them equal for queued cells).
-// `pub` mirrors heap positions < window to global memory for the workers.
-template <class IdxT>
+// indexed_min_heap.hpp:11-106, ties to the smaller id.  Entries (key, id) live
+// in the committer's shared memory (or global memory when the heap could
+// outgrow it); the heap position of every cell is mirrored to global memory
+// (pos[]), since it is needed only for the popped cell's 4 neighbours, whose
+// positions are prefetched with the rest of the commit and tracked through
+// the sifts (trk/tps).  `pub` mirrors heap positions < window for the
+// workers.
 struct Heap {
-  double* key;
-  IdxT* pos;
-  IdxT* arr;
+  double* hk;
+  int* hid;
+  int* pos;
   int* pub;
   int window;
   int size;
-  IdxT absent;
-  __device__ bool less(int a, int b) const {
-    const double ka = key[a], kb = key[b];
-    if (ka != kb) return ka < kb;
-    return a < b;
+  int cap;
+  bool overflow;
+  int trk[4], tps[4];
+  __device__ static bool less(double ka, int ia, double kb, int ib) {
+    return ka < kb || (ka == kb && ia < ib);
   }
-  __device__ void put(int p, int id) {
-    arr[p] = (IdxT)id;
-    pos[id] = (IdxT)p;
-    // plain store: the published prefix is only a hint for the workers (a
-    // strong store per sift level cost ~150 cycles each on the serial path)
+  __device__ void put(int p, double k, int id) {
+    hk[p] = k;
+    hid[p] = id;
+    pos[id] = p;
+    // plain stores: the published prefix is only a hint for the workers
     if (pub && p < window) pub[p] = id;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (trk[t] == id) tps[t] = p;
   }
-  __device__ void up(int p) {
-    const int id = arr[p];
+  __device__ void up(int p, double k, int id) {
     while (p > 0) {
       const int par = (p - 1) >> 1;
-      if (!less(id, arr[par])) break;
-      put(p, arr[par]);
+      const double kp = hk[par];
+      const int ip = hid[par];
+      if (!less(k, id, kp, ip)) break;
+      put(p, kp, ip);
       p = par;
     }
-    put(p, id);
+    put(p, k, id);
   }
-  __device__ void down(int p) {
-    const int id = arr[p];
+  __device__ void down(int p, double k, int id) {
     for (;;) {
       int c = 2 * p + 1;
       if (c >= size) break;
-      if (c + 1 < size && less(arr[c + 1], arr[c])) ++c;
-      if (!less(arr[c], id)) break;
-      put(p, arr[c]);
+      double kc = hk[c];
+      int ic = hid[c];
+      if (c + 1 < size) {
+        const double k2 = hk[c + 1];
+        const int i2 = hid[c + 1];
+        if (less(k2, i2, kc, ic)) {
+          ++c;
+          kc = k2;
+          ic = i2;
+        }
+      }
+      if (!less(kc, ic, k, id)) break;
+      put(p, kc, ic);
       p = c;
     }
-    put(p, id);
+    put(p, k, id);
   }
-  __device__ bool contains(int id) const { return pos[id] != absent; }
-  __device__ void insert(int id) {  // key[id] already holds the cell value
-    put(size, id);
-    ++size;
-    up(size - 1);
-  }
-  __device__ int pop() {
-    const int top = arr[0];
-    const int last = arr[--size];
-    pos[top] = absent;
-    if (size > 0) {
-      put(0, last);
-      down(0);
+  __device__ void insert(int id, double k) {
+    if (size >= cap) {
+      overflow = true;
+      return;
     }
+    ++size;
+    up(size - 1, k, id);
+  }
+  __device__ void decrease(int p, double k) { up(p, k, hid[p]); }
+  __device__ int pop() {
+    const int top = hid[0];
+    pos[top] = -1;
+    --size;
+    if (size > 0) down(0, hk[size], hid[size]);
     return top;
   }
 };
 
+// Node (x, y) of the cell sits at row y+1, column x+2 of the tile, so even
+// columns of the interior are 16-byte aligned (async 16-byte copies of value
+// pairs); the west halo is column 1.
 struct HTile {
   double* U;      // (h+2) x pu values with cross halo
   double* Ct;     // (h+2) x pu costs with halo (-1 = exit / off-grid)
   uint8_t* lock;  // h x w, 1 = unlocked
   int pu, w, h;
-  __device__ double& u(int x, int y) const { return U[(y + 1) * pu + (x + 1)]; }
-  __device__ double c(int x, int y) const { return Ct[(y + 1) * pu + (x + 1)]; }
+  __device__ int ci(int x, int y) const { return (y + 1) * pu + (x + 2); }
+  __device__ double& u(int x, int y) const { return U[ci(x, y)]; }
+  __device__ double c(int x, int y) const { return Ct[ci(x, y)]; }
 };
+
+__device__ __forceinline__ void cp_async16_cg(void* sdst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async8_ca(void* sdst, const void* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // reset_locks (heap_cell.cpp:65-94)
 __device__ void reset_locks(const HTile& T, bool west_in, bool east_in, bool south_in,
@@ -323,59 +353,88 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
   T.w = (int)(ie - ib);
   T.h = (int)(je - jb);
   const int cx = cell % g.cells_x, cy = cell / g.cells_x;
-  const int mw = g.max_w;
+  const int mw = a.spw;  // slot row pitch (even)
   const bool has_nb[4] = {cx > 0, cx + 1 < g.cells_x, cy > 0, cy + 1 < g.cells_y};
   const int nbs[4] = {cell - 1, cell + 1, cell - g.cells_x, cell + g.cells_x};
-  int ncur[4];
+  // Staging with every load in flight at once: the cell's own values as
+  // 16-byte async copies that bypass L1 (other SMs write the slots), its costs
+  // with the cost halo as 8-byte async copies (read-only data), and -- once
+  // the neighbours' state words locate their committed slots -- the value
+  // halo and the probe strips through registers.
+  u64 nstw[4];
 #pragma unroll
   for (int d = 0; d < 4; ++d)
-    ncur[d] = !has_nb[d]          ? 0
-              : (omask >> d) & 1u ? oslot[d]
-                                  : st_cur(ld_relaxed_u64_nb(a.state + nbs[d]));
-  if (lane == 0) {
-    bool bad = kind_slot(st, kind) > 2 || st_cur(st) > 2 || kind_slot(st, kind) == st_cur(st);
-    for (int d = 0; d < 4; ++d) bad = bad || ((omask >> d) & 1u && (unsigned)oslot[d] > 2u);
-    if (bad) {
-      atomicExch(a.status, 5);
-      a.counters[31] = st;
+    nstw[d] = (has_nb[d] && !((omask >> d) & 1u)) ? ld_relaxed_u64_nb(a.state + nbs[d]) : 0ull;
+  const double* own = slot_ptr(a, st_cur(st), cell);
+  double* pstrip = before + 4 * a.max_len;
+  {
+    const int pr = (T.w + 1) >> 1;  // value pairs per row (an odd width copies
+                                    // one pad value into the east halo column,
+                                    // overwritten below after the wait)
+    if (pr <= 32) {
+      const int rstep = 32 / pr, px = lane % pr, ry = lane / pr;
+      if (ry < rstep)
+        for (int y = ry; y < T.h; y += rstep)
+          cp_async16_cg(&T.U[T.ci(2 * px, y)], own + y * mw + 2 * px);
+    } else {
+      for (int p2 = lane; p2 < pr; p2 += 32)
+        for (int y = 0; y < T.h; ++y) cp_async16_cg(&T.U[T.ci(2 * p2, y)], own + y * mw + 2 * p2);
+    }
+    for (int xb = 0; xb < T.w + 2; xb += 32) {
+      const int x = xb + lane - 1;  // tile column -1 .. w
+      if (x > T.w) continue;
+      const bool xin = x >= 0 && x < T.w;
+      const double* cb = a.C + (jb - 1) * g.P + g.pad + ib + x;  // row y = -1
+      for (int y = xin ? -1 : 0; y <= (xin ? T.h : T.h - 1); ++y) {
+        const int64_t gj = jb + y;
+        double* dst = &T.Ct[T.ci(x, y)];
+        if (gj >= 0 && gj < g.n) cp_async8_ca(dst, cb + (int64_t)(y + 1) * g.P);
+        else *dst = -1.0;
+      }
     }
   }
-  const double* own = slot_ptr(a, st_cur(st), cell);
-  // own values and costs of the cell and its cross halo (one pass, so the
-  // independent loads of an iteration batch are in flight together)
-  const int W2 = T.w + 2;
-#pragma unroll 4
-  for (int k = lane; k < (T.h + 2) * W2; k += 32) {
-    const int y = k / W2 - 1, x = k % W2 - 1;
-    const bool inside = x >= 0 && x < T.w && y >= 0 && y < T.h;
-    if (!inside && (x < 0 || x >= T.w) && (y < 0 || y >= T.h)) continue;
-    const int64_t gj = jb + y;
-    double c = -1.0;
-    if (gj >= 0 && gj < g.n) c = __ldg(a.C + gj * g.P + g.pad + ib + x);
-    if (inside) T.u(x, y) = __ldcg(own + y * mw + x);
-    T.Ct[(y + 1) * T.pu + (x + 1)] = c;
-  }
-  // the four border probe strips (F at the clamped probe points,
-  // heap_cell.cpp:195-205), used by the scans after the sweeps
-  double* pstrip = before + 4 * a.max_len;
-  for (int t = lane; t < T.h; t += 32) {
-    pstrip[0 * a.max_len + t] = has_nb[0] ? __ldg(a.probe[0] + (int64_t)cx * g.n + jb + t) : 1.0;
-    pstrip[1 * a.max_len + t] = has_nb[1] ? __ldg(a.probe[1] + (int64_t)cx * g.n + jb + t) : 1.0;
-  }
-  for (int t = lane; t < T.w; t += 32) {
-    pstrip[2 * a.max_len + t] = has_nb[2] ? __ldg(a.probe[2] + (int64_t)cy * g.m + ib + t) : 1.0;
-    pstrip[3 * a.max_len + t] = has_nb[3] ? __ldg(a.probe[3] + (int64_t)cy * g.m + ib + t) : 1.0;
-  }
-  // cross halo values from the neighbours' slots (+inf off-grid)
-  for (int t = lane; t < T.h; t += 32) {
-    T.u(-1, t) = has_nb[0] ? __ldcg(slot_ptr(a, ncur[0], nbs[0]) + t * mw + (int)(g.base_x - 1))
-                           : kInf;
-    T.u(T.w, t) = has_nb[1] ? __ldcg(slot_ptr(a, ncur[1], nbs[1]) + t * mw) : kInf;
-  }
-  for (int t = lane; t < T.w; t += 32) {
-    T.u(t, -1) = has_nb[2] ? __ldcg(slot_ptr(a, ncur[2], nbs[2]) + (int)(g.base_y - 1) * mw + t)
-                           : kInf;
-    T.u(t, T.h) = has_nb[3] ? __ldcg(slot_ptr(a, ncur[3], nbs[3]) + t) : kInf;
+  {
+    int ncur[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d)
+      ncur[d] = !has_nb[d] ? 0 : (omask >> d) & 1u ? oslot[d] : st_cur(nstw[d]);
+    const double* sw = slot_ptr(a, ncur[0], nbs[0]) + (int)(g.base_x - 1);
+    const double* se = slot_ptr(a, ncur[1], nbs[1]);
+    const double* ss = slot_ptr(a, ncur[2], nbs[2]) + (int)(g.base_y - 1) * mw;
+    const double* sn = slot_ptr(a, ncur[3], nbs[3]);
+    // cross halo values from the neighbours' slots (+inf off-grid) and the
+    // four border probe strips (F at the clamped probe points,
+    // heap_cell.cpp:195-205), used by the scans after the sweeps
+    bool first = true;
+    for (int t = lane; t < a.max_len; t += 32) {
+      const bool tv = t < T.h, th = t < T.w;
+      const double hw = has_nb[0] && tv ? __ldcg(sw + t * mw) : kInf;
+      const double he = has_nb[1] && tv ? __ldcg(se + t * mw) : kInf;
+      const double hs = has_nb[2] && th ? __ldcg(ss + t) : kInf;
+      const double hn = has_nb[3] && th ? __ldcg(sn + t) : kInf;
+      const double p0v = has_nb[0] && tv ? __ldg(a.probe[0] + (int64_t)cx * g.n + jb + t) : 1.0;
+      const double p1v = has_nb[1] && tv ? __ldg(a.probe[1] + (int64_t)cx * g.n + jb + t) : 1.0;
+      const double p2v = has_nb[2] && th ? __ldg(a.probe[2] + (int64_t)cy * g.m + ib + t) : 1.0;
+      const double p3v = has_nb[3] && th ? __ldg(a.probe[3] + (int64_t)cy * g.m + ib + t) : 1.0;
+      if (first) {
+        cp_async_wait_all();  // the east halo column may hold a copied pad value
+        first = false;
+      }
+      if (tv) {
+        T.u(-1, t) = hw;
+        T.u(T.w, t) = he;
+        pstrip[0 * a.max_len + t] = p0v;
+        pstrip[1 * a.max_len + t] = p1v;
+      }
+      if (th) {
+        T.u(t, -1) = hs;
+        T.u(t, T.h) = hn;
+        pstrip[2 * a.max_len + t] = p2v;
+        pstrip[3 * a.max_len + t] = p3v;
+      }
+    }
+    if (first) cp_async_wait_all();
+    if (prof) prof[3] += clock64() - p0;
   }
   __syncwarp();
   // border snapshots (heap_cell.cpp:279-282)
@@ -391,7 +450,7 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
   const unsigned my_flags = st_flags(st) | cflags;
   const bool first_removal = !st_first_done(st);
   reset_locks(T, ib > 0, ie < g.m, jb > 0, je < g.n, lane);
-  const CellTile ct{T.U, T.Ct, T.lock, T.pu, T.w, T.h};
+  const CellTile ct{T.U, T.Ct, T.lock, T.pu, T.w, T.h, 2};
   long long nsw = 0, upd = 0;
   if (a.fast) {
     for (int k = 0; k < 4; ++k) {  // process_flagged_once (heap_cell.cpp:150-160)
@@ -480,14 +539,13 @@ __device__ void publish(const HcArgs& a, int cell, int kind, u64 st, unsigned dm
 }
 
 // ---- the committer: the reference's heap loop in exact order ----------------
-template <class IdxT>
-__device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* before, int lane) {
+__device__ void committer(const HcArgs& a, Heap& H, HTile& T, double* before, int lane) {
   const CellGeom& g = a.g;
   if (lane == 0) {
     for (int k = 0; k < a.n_init; ++k) {  // heap_cell.cpp:255-268
       const int cell = a.init_cells[k];
-      H.key[cell] = a.init_values[k];
-      H.insert(cell);
+      a.cval[cell] = a.init_values[k];
+      H.insert(cell, a.init_values[k]);
       a.ckey[cell] = a.init_values[k];
       if (a.fast) st_relaxed_u64(a.state + cell, (1ull << 32) | 0xFull);  // Q-cells: all flags
     }
@@ -496,15 +554,16 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
   long long removals = 0, sweeps = 0, updates = 0, mon_checks = 0, mon_single = 0;
   long long self_processed = 0, fast_hits = 0, waits = 0, chain_hits = 0;
   long long cyc_pop = 0, cyc_obtain = 0, cyc_self = 0, cyc_commit = 0;
-  long long prof[3] = {0, 0, 0};
+  long long prof[5] = {0, 0, 0, 0, 0};
   long long miss_cls[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int max_size = H.size;
   int prev_cell = -1;
   const unsigned* spec_p = a.spec_ver;
   const unsigned* spec_c = a.spec_ver + a.J;
   for (;;) {
     int cell = -1;
     long long t0 = clock64();
-    if (lane == 0 && H.size > 0) {
+    if (lane == 0 && H.size > 0 && !H.overflow) {
       cell = H.pop();
       *a.hsize_pub = H.size;
       a.ckey[cell] = kInf;
@@ -529,7 +588,18 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
     // on the observed tag, so it cannot be read early.
     int mode = 0, kind = 0, dep = 0;  // mode 0: valid speculation, 1: process here
     u64 st = 0;
+    // the commit's loads that do not depend on the speculation (only this
+    // warp writes these words) go out with the first poll
+    u64 nst[4];
+    double cv[4];
     if (lane == 0) {
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        nst[d] = nbs[d] >= 0 ? ld_relaxed_u64_nb(a.state + nbs[d]) : 0ull;
+        cv[d] = nbs[d] >= 0 ? __ldcg(a.cval + nbs[d]) : kInf;
+        H.trk[d] = nbs[d];
+        H.tps[d] = nbs[d] >= 0 ? __ldcg(a.hpos + nbs[d]) : -1;
+      }
       st = ld_relaxed_u64(a.state + cell);
       const unsigned v = st_ver(st);
       unsigned ctn[4];  // only this warp writes ctag
@@ -647,9 +717,6 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
     if (lane == 0) {
       // every load of the commit is issued before the first heap operation
       // (one L2 round trip instead of one per side)
-      u64 nst[4];
-#pragma unroll
-      for (int d = 0; d < 4; ++d) nst[d] = nbs[d] >= 0 ? ld_relaxed_u64_nb(a.state + nbs[d]) : 0ull;
       const SpecRec* rec = rec_ptr(a, kind, cell + dep);
       double cand[4];
       unsigned word[4];  // add | fl | monc | mons, one byte each
@@ -682,10 +749,11 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
         const int nb = nbs[side];
         if (nb < 0) continue;
         bool moved = false;
-        if (cand[side] < H.key[nb]) {
-          H.key[nb] = cand[side];
-          if (H.contains(nb)) {
-            H.up(H.pos[nb]);
+        if (cand[side] < cv[side]) {
+          cv[side] = cand[side];
+          a.cval[nb] = cand[side];
+          if (H.tps[side] >= 0) {
+            H.decrease(H.tps[side], cand[side]);
             moved = true;
           }
         }
@@ -696,15 +764,17 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
             ++mon_checks;
             if (word[side] >> 24) ++mon_single;
           }
-          if (!H.contains(nb)) {
-            H.insert(nb);
+          if (H.tps[side] < 0) {
+            H.insert(nb, cv[side]);
             moved = true;
           }
         }
-        if (moved) a.ckey[nb] = H.key[nb];
+        if (moved) a.ckey[nb] = cv[side];
         st_relaxed_u64(a.state + nb, (u64)lo | (nst[side] & (3ull << 32)));
       }
       *a.hsize_pub = H.size;
+      for (int d = 0; d < 4; ++d) H.trk[d] = -1;
+      if (H.size > max_size) max_size = H.size;
     }
     __syncwarp();
     cyc_commit += clock64() - t3;
@@ -726,8 +796,12 @@ __device__ void committer(const HcArgs& a, Heap<IdxT>& H, HTile& T, double* befo
     a.counters[12] = prof[0];
     a.counters[13] = prof[1];
     a.counters[14] = prof[2];
+    a.counters[39] = prof[3];
+    a.counters[40] = prof[4];
     a.counters[15] = chain_hits;
     for (int k = 0; k < 8; ++k) a.counters[16 + k] = miss_cls[k];
+    a.counters[38] = (unsigned long long)max_size;
+    if (H.overflow) atomicExch(a.status, 6);
     __threadfence();
     st_release_s32(a.done_flag, 1);
   }
@@ -927,7 +1001,7 @@ __device__ bool pick_job(const HcArgs& a, int pidx, Job& j, int wid) {
 }
 
 __global__ void heapcell_spec_kernel(HcArgs a) {
-  extern __shared__ double smem[];
+  extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const CellGeom& g = a.g;
@@ -943,22 +1017,24 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
   // loads and acquire once per speculation.
   if (blockIdx.x == 0) {
     if (wib != 0) return;
-    if (a.heap_in_smem) {
-      // [tile][key: J doubles][pos: J u16][arr: J u16]
-      double* key = smem + a.tile_doubles;
-      uint16_t* pos = reinterpret_cast<uint16_t*>(key + a.J);
-      uint16_t* arr = pos + a.J;
-      for (int k = lane; k < a.J; k += 32) {
-        key[k] = kInf;
-        pos[k] = 0xFFFFu;
-      }
-      __syncwarp();
-      Heap<uint16_t> H{key, pos, arr, a.harr, a.window, 0, (uint16_t)0xFFFFu};
-      committer(a, H, T, before, lane);
-    } else {
-      Heap<int> H{a.hkey, a.hpos, a.harr, nullptr, 0, 0, -1};
-      committer(a, H, T, before, lane);
+    Heap H;
+    if (a.heap_cap > 0) {  // [tile][keys: cap doubles][ids: cap ints]
+      H.hk = smem + a.tile_doubles;
+      H.hid = reinterpret_cast<int*>(H.hk + a.heap_cap);
+      H.pub = a.harr;
+      H.cap = a.heap_cap;
+    } else {  // global entries; the id array is the published array itself
+      H.hk = a.hkey;
+      H.hid = a.harr;
+      H.pub = nullptr;
+      H.cap = a.J;
     }
+    H.pos = a.hpos;
+    H.window = a.window;
+    H.size = 0;
+    H.overflow = false;
+    for (int d = 0; d < 4; ++d) H.trk[d] = -1, H.tps[d] = -1;
+    committer(a, H, T, before, lane);
     return;
   }
 
@@ -1010,7 +1086,7 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
       worked = true;
       break;
     }
-    if (!worked) __nanosleep(200);
+    if (!worked) __nanosleep(a.idle_ns);
   }
 }
 
@@ -1020,7 +1096,7 @@ __global__ void heapcell_init_kernel(HcArgs a) {
        k += (int64_t)gridDim.x * blockDim.x) {
     const int cell = (int)(k / cellsz);
     const int r = (int)(k - (int64_t)cell * cellsz);
-    const int y = r / a.g.max_w, x = r % a.g.max_w;
+    const int y = r / a.spw, x = r % a.spw;
     int64_t ib, ie, jb, je;
     hc_cell_rect(a.g, cell, ib, ie, jb, je);
     double v = kInf;
@@ -1039,6 +1115,7 @@ __global__ void heapcell_init_kernel(HcArgs a) {
       }
       a.ckey[cell] = kInf;
       a.ctag[cell] = kSpecNone;
+      a.cval[cell] = kInf;
       a.hkey[cell] = kInf;
       a.hpos[cell] = -1;
       a.harr[cell] = -1;
@@ -1052,7 +1129,7 @@ __global__ void heapcell_gather_kernel(HcArgs a) {
        k += (int64_t)gridDim.x * blockDim.x) {
     const int cell = (int)(k / cellsz);
     const int r = (int)(k - (int64_t)cell * cellsz);
-    const int y = r / a.g.max_w, x = r % a.g.max_w;
+    const int y = r / a.spw, x = r % a.spw;
     int64_t ib, ie, jb, je;
     hc_cell_rect(a.g, cell, ib, ie, jb, je);
     if (x < ie - ib && y < je - jb)
@@ -1067,7 +1144,7 @@ size_t heapcell_smem_bytes(const CellGeom& g, int max_len) {
          (((size_t)g.max_w * g.max_h + 7) & ~(size_t)7);
 }
 
-size_t heapcell_committer_heap_bytes(int J) { return (size_t)J * (sizeof(double) + 4); }
+size_t heapcell_committer_heap_bytes(int cap) { return (size_t)cap * (sizeof(double) + 4); }
 
 cudaError_t launch_heapcell(const HcArgs& args, int warps_per_cta, int max_ctas, cudaStream_t s,
                             int* launches) {
@@ -1075,8 +1152,9 @@ cudaError_t launch_heapcell(const HcArgs& args, int warps_per_cta, int max_ctas,
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   heapcell_init_kernel<<<blocks, 256, 0, s>>>(args);
   size_t smem = (size_t)warps_per_cta * args.tile_doubles * sizeof(double);
-  if (args.heap_in_smem)
-    smem = std::max(smem, args.tile_doubles * sizeof(double) + heapcell_committer_heap_bytes(args.J));
+  if (args.heap_cap > 0)
+    smem = std::max(smem, args.tile_doubles * sizeof(double) +
+                              heapcell_committer_heap_bytes(args.heap_cap));
   cudaError_t e = cudaFuncSetAttribute(heapcell_spec_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -16,6 +16,7 @@ __global__ void bench(int w, int h, int reps, long long* out, double* sink) {
   const int pu = (w + 3) & ~1;
   CellTile T;
   T.pu = pu;
+  T.ox = 1;
   T.U = sm;
   T.Ct = sm + (h + 2) * pu;
   T.lock = reinterpret_cast<uint8_t*>(T.Ct + (h + 2) * pu);
@@ -32,8 +33,9 @@ __global__ void bench(int w, int h, int reps, long long* out, double* sink) {
   long long upd = 0;
   long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
-    cell_sweep<MODE>(T, r & 3, lane, upd);
-    if (MODE == 2)
+    if (MODE == 3) cell_sweep_ns<2, 1>(T, r & 3, lane, upd);  // the generic locked engine
+    else cell_sweep<MODE>(T, r & 3, lane, upd);
+    if (MODE >= 2)
       for (int k = lane; k < w * h; k += 32) T.lock[k] = 1;
     __syncwarp();
   }
@@ -54,19 +56,23 @@ int main() {
     const int w = sz[0], h = sz[1], reps = 200;
     const int pu = (w + 3) & ~1;
     const size_t smem = 2 * (h + 2) * pu * 8 + w * h + 16;
-    long long cyc[3];
+    long long cyc[4];
     cudaFuncSetAttribute(bench<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(bench<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(bench<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     bench<0><<<1, 32, smem>>>(w, h, reps, d_out, d_sink);
     cudaMemcpy(&cyc[0], d_out, 8, cudaMemcpyDeviceToHost);
     bench<1><<<1, 32, smem>>>(w, h, reps, d_out, d_sink);
     cudaMemcpy(&cyc[1], d_out, 8, cudaMemcpyDeviceToHost);
     bench<2><<<1, 32, smem>>>(w, h, reps, d_out, d_sink);
     cudaMemcpy(&cyc[2], d_out, 8, cudaMemcpyDeviceToHost);
+    bench<3><<<1, 32, smem>>>(w, h, reps, d_out, d_sink);
+    cudaMemcpy(&cyc[3], d_out, 8, cudaMemcpyDeviceToHost);
     const double steps = (double)reps * (w + h - 1);
-    printf("cell %dx%d: cycles/step full %.0f directional %.0f locked %.0f  (%s)\n", w, h,
-           cyc[0] / steps, cyc[1] / steps, cyc[2] / steps, cudaGetErrorString(cudaGetLastError()));
+    printf("cell %dx%d: cycles/step full %.0f directional %.0f locked %.0f (generic %.0f)  (%s)\n",
+           w, h, cyc[0] / steps, cyc[1] / steps, cyc[2] / steps, cyc[3] / steps,
+           cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }

@@ -207,3 +207,26 @@ def test_heapcell_all_exit_and_first_removal():
         assert np.all(np.isfinite(out.values))
     out = E.hcm_solve(p, E.build_cells(p.grid, 2, 2))
     assert float(np.max(np.abs(out.values - exact) / np.maximum(exact, 1e-300))) < 1e-12
+
+
+@pytest.mark.parametrize("env", [{"EIK_HC_HEAP_CAP": "64"}, {"EIK_HC_GLOBAL_HEAP": "1"},
+                                 {"EIK_HC_CHAIN": "0"}, {"EIK_HC_CHAIN": "2"},
+                                 {"EIK_HC_CTAS": "1"}],
+                         ids=["heap-overflow-fallback", "global-heap", "no-chain", "chain-all",
+                              "committer-only"])
+def test_heapcell_engine_variants_bitwise(env, monkeypatch):
+    """Every scheduling variant of the heap-cell kernel -- a committer heap that
+    overflows shared memory and falls back to global memory, the global heap,
+    plain-only / all-neighbour chained speculation, the committer alone -- must
+    give the reference's bits and counters (C2 at 16x16-node cells)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    p = configs.config2(257).problem
+    cells = E.build_cells(p.grid, 16, 16)
+    for method in ("hcm", "fhcm"):
+        a = E.solve(p, method, cells)
+        b = O.oracle_solve(p, method, cells)
+        assert bitwise(a.values, b.u), (method, env)
+        assert (a.sweeps, a.node_updates, a.heap_removals, a.hybrid.mon_checks,
+                a.hybrid.mon_single) == (b.sweeps, b.node_updates, b.heap_removals,
+                                         b.mon_checks, b.mon_single), (method, env)
