@@ -126,6 +126,27 @@ const double* eik_plan_values(const eik_plan* plan);
 int64_t eik_plan_pitch(const eik_plan* plan);
 void eik_plan_destroy(eik_plan* plan);
 
+/* Sweep-level control of an EIK_FSM / EIK_FMM plan -- the building blocks of
+ * strip-Jacobi FSM across GPUs (SURVEY.md section 8(e)
+ * option A).  They replace no single reference function: a rank owns a row
+ * strip of fsm_solve's grid (classic_solvers.cpp:128-158) plus one frozen
+ * ghost row on each side, given as exit nodes whose values are overwritten
+ * after every exchange.
+ *   eik_plan_prepare  u <- +inf, exits <- their cost, C <- h/F (the start of
+ *                     fsm_solve, classic_solvers.cpp:130-137).
+ *   eik_plan_sweep    exactly `count` Gauss-Seidel sweeps on the current
+ *                     values, local sweep k in direction (first_sweep+k) mod 4
+ *                     (sweep_direction, classic_solvers.cpp:94-96);
+ *                     changed[k] = 1 iff sweep k lowered some value.
+ *   eik_plan_get_rows / eik_plan_set_rows  copy rows [row0, row0+nrows) of
+ *                     the value field out of / into the plan (dense m-wide
+ *                     rows; host or device buffer). */
+int eik_plan_prepare(eik_plan* plan);
+int eik_plan_sweep(eik_plan* plan, int64_t first_sweep, int32_t count, int32_t* changed);
+int eik_plan_get_rows(eik_plan* plan, int64_t row0, int64_t nrows, double* dst, int32_t on_device);
+int eik_plan_set_rows(eik_plan* plan, int64_t row0, int64_t nrows, const double* src,
+                      int32_t on_device);
+
 /* Thread-local description / status code of the last failure on this
  * thread (eik_plan_create returns NULL and sets both). */
 const char* eik_last_error(void);

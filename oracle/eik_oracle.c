@@ -238,6 +238,29 @@ int orc_fsm(const orc_problem* p, double* v, orc_stats* st) {
   return 0;
 }
 
+/* One sweep of the loop body above (classic_solvers.cpp:140-155) in direction
+ * dir over v; nodes with frozen[idx] != 0 are skipped (exits, and the ghost
+ * rows of a strip in the strip-Jacobi emulation).  Returns 1 if a value
+ * decreased. */
+int orc_fsm_sweep(int64_t m, int64_t n, double h, const double* F, const char* frozen, double* v,
+                  int dir) {
+  int changed = 0;
+  double nb[4];
+  axis io = i_order(dir & 3, 0, m), jo = j_order(dir & 3, 0, n);
+  for (int64_t i = io.begin; i != io.end; i += io.step)
+    for (int64_t j = jo.begin; j != jo.end; j += jo.step) {
+      int64_t idx = j * m + i;
+      if (frozen[idx]) continue;
+      gather(v, m, n, i, j, nb);
+      double cand = orc_node_update(nb, F[idx], h);
+      if (cand < v[idx]) {
+        v[idx] = cand;
+        changed = 1;
+      }
+    }
+  return changed;
+}
+
 /* ---- LSM: classic_solvers.cpp:160-212 ---------------------------------- */
 
 int orc_lsm(const orc_problem* p, double* v, orc_stats* st) {

@@ -56,6 +56,9 @@ double orc_directional_update(const double nb[4], int dir, double f, double h);
  * (ConfigError), 3 when the heap-cell removal budget is exceeded. */
 int orc_fmm(const orc_problem* p, double* u, orc_stats* st);
 int orc_fsm(const orc_problem* p, double* u, orc_stats* st);
+/* one FSM sweep in direction dir; frozen nodes are not updated; 1 if changed */
+int orc_fsm_sweep(int64_t m, int64_t n, double h, const double* F, const char* frozen, double* u,
+                  int dir);
 int orc_lsm(const orc_problem* p, double* u, orc_stats* st);
 int orc_hcm(const orc_problem* p, const orc_cells* c, double* u, orc_stats* st);
 int orc_fhcm(const orc_problem* p, const orc_cells* c, double* u, orc_stats* st);

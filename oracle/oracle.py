@@ -75,6 +75,8 @@ def _load_oracle():
     lib.orc_node_update.restype = C.c_double
     lib.orc_directional_update.argtypes = [_dp, C.c_int, C.c_double, C.c_double]
     lib.orc_directional_update.restype = C.c_double
+    lib.orc_fsm_sweep.argtypes = [C.c_int64, C.c_int64, C.c_double, _dp, C.c_void_p, _dp, C.c_int]
+    lib.orc_fsm_sweep.restype = C.c_int
     return lib
 
 
@@ -147,6 +149,15 @@ def oracle_solve(p: Problem, method: str, cells: CellDecomposition = None,
     if rc == 3:
         raise N.BudgetError("heap-cell removal budget exceeded")
     return Result(u, st.sweeps, st.node_updates, st.heap_removals, st.mon_checks, st.mon_single)
+
+
+def oracle_fsm_sweep(m: int, n: int, h: float, F: np.ndarray, frozen: np.ndarray, u: np.ndarray,
+                     direction: int) -> bool:
+    """One FSM sweep in place (classic_solvers.cpp:140-155); frozen nodes are
+    skipped.  Test infrastructure for the strip-Jacobi emulation."""
+    assert F.dtype == np.float64 and u.dtype == np.float64 and frozen.dtype == np.uint8
+    return bool(olib.orc_fsm_sweep(m, n, h, F.ctypes.data_as(_dp), frozen.ctypes.data,
+                                   u.ctypes.data_as(_dp), direction))
 
 
 _REF_METHOD = {"fmm": 0, "fsm": 1, "lsm": 2, "hcm": 3, "fhcm": 4, "fmsm": 5}

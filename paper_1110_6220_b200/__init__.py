@@ -12,6 +12,7 @@ from .problem import (CellDecomposition, CellTables, ExitSpec, Grid, Problem, Sp
                       speed_nodemask, speed_sinsum, speed_sinusoid)
 from .solvers import (HybridStats, Plan, SolverOutput, fhcm_solve, fmm_solve, fmsm_solve,
                       fsm_solve, hcm_solve, solve)
+from .distributed import StripSolve, fsm_solve_strips, strip_bounds
 
 
 def device_count() -> int:
@@ -24,5 +25,5 @@ __all__ = [
     "snap_point_to_node", "speed_blocks", "speed_checkerboard", "speed_comb_maze",
     "speed_constant", "speed_nodemask", "speed_sinsum", "speed_sinusoid", "HybridStats",
     "Plan", "SolverOutput", "fhcm_solve", "fmm_solve", "fmsm_solve", "fsm_solve",
-    "hcm_solve", "solve", "device_count",
+    "hcm_solve", "solve", "device_count", "StripSolve", "fsm_solve_strips", "strip_bounds",
 ]

@@ -154,6 +154,8 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   a.done = P->dDone;
   a.max_sweeps = P->max_sweeps;
   a.lookahead = 3;
+  a.first_sweep = 0;
+  a.fixed = 0;
   a.status = P->dStatus;
   a.trace = nullptr;
   if (std::getenv("EIK_TRACE_FSM")) {
@@ -251,6 +253,84 @@ int plan_run(eik_plan* P, eik_output* out) {
   return EIK_OK;
 }
 
+// ---- sweep-level control of FSM plans (strip-Jacobi FSM across GPUs) ----
+int plan_prepare(eik_plan* P) {
+  if (P->method != EIK_FSM && P->method != EIK_FMM)
+    return fail(EIK_ERR_CONFIG, "sweep-level control needs an fsm/fmm plan");
+  CK(cudaSetDevice(P->device));
+  CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
+  int launches = 0;
+  CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
+                    P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
+  int st[8];
+  CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
+  CK(cudaStreamSynchronize(P->stream));
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  return EIK_OK;
+}
+
+int plan_sweep(eik_plan* P, int64_t first_sweep, int count, int* changed) {
+  if (P->method != EIK_FSM && P->method != EIK_FMM)
+    return fail(EIK_ERR_CONFIG, "sweep-level control needs an fsm/fmm plan");
+  if (count < 1 || count > P->max_sweeps || first_sweep < 0)
+    return fail(EIK_ERR_CONFIG, "sweep count out of range");
+  CK(cudaSetDevice(P->device));
+  FsmArgs a;
+  a.C = P->dC;
+  a.u = P->dU;
+  a.m = P->g.m;
+  a.n = P->g.n;
+  a.P = P->pitch;
+  a.pad = kPad;
+  a.nstrips = P->nstrips;
+  a.prog = P->dProg;
+  a.mbox = P->dMbox;
+  a.changed = P->dChanged;
+  a.done = P->dDone;
+  a.max_sweeps = count;
+  a.lookahead = 3;
+  a.first_sweep = (int)(first_sweep & 3);
+  a.fixed = 1;
+  a.status = P->dStatus;
+  a.trace = nullptr;
+  int launches = 0;
+  CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
+  CK(cudaMemsetAsync(P->dProg, 0, sizeof(unsigned long long) * P->nstrips, P->stream));
+  CK(cudaMemsetAsync(P->dMbox, 0xFF, sizeof(double) * 2 * P->nstrips * P->pitch, P->stream));
+  CK(cudaMemsetAsync(P->dChanged, 0, sizeof(int) * count, P->stream));
+  CK(cudaMemsetAsync(P->dDone, 0, sizeof(int) * count, P->stream));
+  CK(launch_fsm(a, P->stream, &launches));
+  int st[8];
+  std::vector<int> ch((size_t)count);
+  CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
+  CK(cudaMemcpyAsync(ch.data(), P->dChanged, sizeof(int) * count, cudaMemcpyDeviceToHost,
+                     P->stream));
+  CK(cudaStreamSynchronize(P->stream));
+  if (st[0] == 4) return fail(EIK_ERR_CUDA, "fsm wavefront watchdog fired (scheduling bug)");
+  if (changed)
+    for (int k = 0; k < count; ++k) changed[k] = ch[k] != 0;
+  return EIK_OK;
+}
+
+int plan_rows(eik_plan* P, int64_t row0, int64_t nrows, double* host_or_dev, int on_device,
+              bool to_plan) {
+  if (row0 < 0 || nrows < 0 || row0 + nrows > P->g.n)
+    return fail(EIK_ERR_CONFIG, "row range outside the grid");
+  if (nrows == 0) return EIK_OK;
+  if (!host_or_dev) return fail(EIK_ERR_DOMAIN, "null row buffer");
+  CK(cudaSetDevice(P->device));
+  double* dev = P->dU + row0 * P->pitch + kPad;
+  const size_t w = sizeof(double) * P->g.m, dp = sizeof(double) * P->pitch;
+  if (to_plan)
+    CK(cudaMemcpy2DAsync(dev, dp, host_or_dev, w, w, nrows,
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P->stream));
+  else
+    CK(cudaMemcpy2DAsync(host_or_dev, w, dev, dp, w, nrows,
+                         on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, P->stream));
+  CK(cudaStreamSynchronize(P->stream));
+  return EIK_OK;
+}
+
 }  // namespace eikb200
 
 using namespace eikb200;
@@ -306,6 +386,27 @@ const double* eik_plan_values(const eik_plan* P) { return P ? P->dU + kPad : nul
 int64_t eik_plan_pitch(const eik_plan* P) { return P ? P->pitch : 0; }
 
 void eik_plan_destroy(eik_plan* P) { plan_free(P); }
+
+int eik_plan_prepare(eik_plan* P) {
+  if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
+  return plan_prepare(P);
+}
+
+int eik_plan_sweep(eik_plan* P, int64_t first_sweep, int32_t count, int32_t* changed) {
+  if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
+  return plan_sweep(P, first_sweep, count, changed);
+}
+
+int eik_plan_get_rows(eik_plan* P, int64_t row0, int64_t nrows, double* dst, int32_t on_device) {
+  if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
+  return plan_rows(P, row0, nrows, dst, on_device, false);
+}
+
+int eik_plan_set_rows(eik_plan* P, int64_t row0, int64_t nrows, const double* src,
+                      int32_t on_device) {
+  if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
+  return plan_rows(P, row0, nrows, const_cast<double*>(src), on_device, true);
+}
 
 int eik_solve(const eik_problem* p, const eik_cells* c, int32_t method, eik_output* out) {
   if (!out || !out->u) return fail(EIK_ERR_DOMAIN, "output needs a u buffer");

@@ -24,6 +24,8 @@ struct FsmArgs {
   int* done;                // [max_sweeps] strips finished per sweep
   int max_sweeps;
   int lookahead;            // D: stop decision for sweep k uses sweep k-D
+  int first_sweep;          // direction of local sweep k is (first_sweep + k) mod 4
+  int fixed;                // run exactly max_sweeps sweeps (no stop decision)
   int* status;              // [0] error, [1] sweeps
   unsigned long long* trace; // optional [kTraceSweeps][nstrips][3] globaltimer
                              // (start, body start, end) per strip-sweep

@@ -162,7 +162,7 @@ fsm_wavefront_kernel(FsmArgs a) {
 
   for (int k = 0;; ++k) {
     // ---- stop decision: identical in every strip --------------------------
-    if (k >= a.lookahead) {
+    if (!a.fixed && k >= a.lookahead) {
       const int kk = k - a.lookahead;
       int chg = 1, ok = 1;
       if (lane == 0) {
@@ -177,10 +177,14 @@ fsm_wavefront_kernel(FsmArgs a) {
       }
     }
     if (k >= a.max_sweeps) {
-      if (lane == 0) atomicExch(&a.status[0], 3);
+      if (a.fixed) {
+        if (b == 0 && lane == 0) a.status[1] = k;
+      } else if (lane == 0) {
+        atomicExch(&a.status[0], 3);
+      }
       break;
     }
-    const int dir = k & 3;  // sweep_direction (classic_solvers.cpp:94-96)
+    const int dir = (a.first_sweep + k) & 3;  // sweep_direction (classic_solvers.cpp:94-96)
     const bool iasc = (dir == 0 || dir == 1);
     const bool jasc = (dir == 0 || dir == 3);
     const int64_t base = (int64_t)b * 32;

@@ -1,0 +1,177 @@
+"""Strip-Jacobi FSM across ranks (paper_1110_6220_b200/distributed.py,
+SURVEY.md section 8(e) option A).
+
+CPU (gloo, world size 2, the oracle's sweep plugged in as the strip sweeper):
+the distributed run must equal a serial emulation of the same rounds bit for
+bit, with the same round count, and the reference's fixed point within 1e-10.
+GPU: one strip is fsm_solve bit for bit (identical sweeps); two ranks on one
+device (gloo exchange, no kernel waits on another rank) equal the emulation.
+"""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+
+import paper_1110_6220_b200 as E
+from paper_1110_6220_b200.distributed import strip_bounds, strip_problem
+from oracle import oracle as O
+
+
+def _problem(m=61, n=57, kind="sin"):
+    g = E.Grid(m, n, 1.0 / (m - 1), 0.0, 0.0)
+    sp = E.speed_sinusoid(0.5, 3) if kind == "sin" else E.speed_checkerboard(5)
+    ex = E.ExitSpec.node_set([(5, 7), (m - 9, n - 4), (m // 2, n // 2)], [0.0, 0.02, 0.01])
+    return E.build_problem(g, sp, ex)
+
+
+class OracleStripSweeper:
+    """The strip on the CPU through the oracle's sweep (test infrastructure):
+    mirrors eik_plan_prepare (u = +inf, exits = cost) and eik_plan_sweep."""
+
+    def __init__(self, local):
+        g = local.grid
+        self.m, self.nl, self.h = g.m, g.n, g.h
+        self.F = np.ascontiguousarray(local.sampled_speed(), dtype=np.float64)
+        self.frozen = np.zeros(g.m * g.n, dtype=np.uint8)
+        self.frozen[local.exit_nodes] = 1
+        self.u = np.full(g.m * g.n, np.inf)
+        self.u[local.exit_nodes] = local.exit_cost
+
+    def sweep(self, k):
+        return O.oracle_fsm_sweep(self.m, self.nl, self.h, self.F, self.frozen, self.u, k & 3)
+
+    def get_rows(self, r, nrows, out):
+        out[:] = self.u[r * self.m:(r + nrows) * self.m]
+
+    def set_rows(self, r, nrows, src):
+        self.u[r * self.m:(r + nrows) * self.m] = np.asarray(src)
+
+
+def emulate(problem, world, factory=OracleStripSweeper):
+    """The same rounds in one process: every strip sweeps, then edges swap."""
+    m, n = problem.grid.m, problem.grid.n
+    strips = [strip_bounds(n, world, r) for r in range(world)]
+    sws = [factory(strip_problem(problem, a, b)) for a, b in strips]
+    for s in sws:
+        s.set_rows(0, 1, np.full(m, np.inf))
+        s.set_rows(s.nl - 1, 1, np.full(m, np.inf))
+    k = 0
+    while True:
+        changed = [s.sweep(k) for s in sws]
+        k += 1
+        lo = [np.empty(m) for _ in sws]
+        hi = [np.empty(m) for _ in sws]
+        for r, s in enumerate(sws):
+            s.get_rows(1, 1, lo[r])
+            s.get_rows(s.nl - 2, 1, hi[r])
+        for r, s in enumerate(sws):
+            if r > 0:
+                s.set_rows(0, 1, hi[r - 1])
+            if r < world - 1:
+                s.set_rows(s.nl - 1, 1, lo[r + 1])
+        if not any(changed):
+            break
+    u = np.empty(m * n)
+    for (a, b), s in zip(strips, sws):
+        s.get_rows(1, b - a, u[a * m:b * m])
+    return u, k
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, outdir, use_device, kind):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        p = _problem(kind=kind)
+        fac = None if use_device else OracleStripSweeper
+        r = E.fsm_solve_strips(p, sweeper_factory=fac)
+        np.save(os.path.join(outdir, f"u{rank}.npy"), r.values)
+        np.save(os.path.join(outdir, f"k{rank}.npy"), np.array([r.sweeps, r.node_updates]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_world(world, use_device, kind="sin"):
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, _free_port(), d, use_device, kind), nprocs=world, join=True)
+        us = [np.load(os.path.join(d, f"u{r}.npy")) for r in range(world)]
+        ks = [np.load(os.path.join(d, f"k{r}.npy")) for r in range(world)]
+    return us, ks
+
+
+def test_strip_bounds_cover_rows():
+    for n, world in [(10, 1), (10, 3), (2049, 8), (57, 2)]:
+        b = [strip_bounds(n, world, r) for r in range(world)]
+        assert b[0][0] == 0 and b[-1][1] == n
+        assert all(b[r][1] == b[r + 1][0] and b[r][1] > b[r][0] for r in range(world - 1))
+    with pytest.raises(E.ConfigError):
+        strip_bounds(3, 4, 0)
+
+
+def test_strip_problem_maps_rows_and_exits():
+    p = _problem()
+    m = p.grid.m
+    loc = strip_problem(p, 20, 40)
+    assert (loc.grid.m, loc.grid.n) == (m, 22)
+    F = p.sampled_speed().reshape(p.grid.n, m)
+    assert np.array_equal(loc.sampled_speed().reshape(22, m)[1:-1], F[20:40])
+    own = [(e % m, e // m) for e in p.exit_nodes if 20 <= e // m < 40]
+    lex = set(int(e) for e in loc.exit_nodes)
+    assert all((j - 19) * m + i in lex for i, j in own)
+    assert all(i in lex and (21 * m + i) in lex for i in range(m))  # ghost rows frozen
+    assert np.all(np.diff(loc.exit_nodes) > 0)
+
+
+def test_single_strip_is_fsm_bitwise():
+    p = _problem()
+    u, k = emulate(p, 1)
+    ref = O.oracle_solve(p, "fsm")
+    assert np.array_equal(u, ref.u) and k == ref.sweeps
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_emulated_strips_reach_the_fixed_point(world):
+    p = _problem(kind="chk")
+    u, k = emulate(p, world)
+    ref = O.oracle_solve(p, "fsm")
+    assert float(np.max(np.abs(u - ref.u))) <= 1e-10
+    assert k >= ref.sweeps
+
+
+def test_gloo_world2_equals_emulation():
+    p = _problem()
+    us, ks = _run_world(2, use_device=False)
+    u, k = emulate(p, 2)
+    for r in range(2):
+        assert np.array_equal(us[r], u)
+        assert ks[r][0] == k
+        assert ks[r][1] == k * (p.grid.size() - len(p.exit_nodes))
+    assert float(np.max(np.abs(u - O.oracle_solve(p, "fsm").u))) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_device_single_strip_is_fsm_bitwise():
+    p = _problem()
+    r = E.fsm_solve_strips(p)
+    ref = O.oracle_solve(p, "fsm")
+    assert np.array_equal(r.values, ref.u)
+    assert r.sweeps == ref.sweeps and r.node_updates == ref.node_updates
+
+
+@pytest.mark.gpu
+def test_device_strips_two_ranks_equal_emulation():
+    p = _problem(kind="chk")
+    us, ks = _run_world(2, use_device=True, kind="chk")
+    u, k = emulate(p, 2)
+    for r in range(2):
+        assert np.array_equal(us[r], u) and ks[r][0] == k
