@@ -380,9 +380,9 @@ retry:  // after a committer heap overflow, with the heap in global memory
     std::fprintf(stderr,
                  "heapcell committer cycles: pop %llu obtain %llu self %llu commit %llu | self: "
                  "stage %llu sweeps %llu scans %llu | hits %llu (chained %llu) self %llu | "
-                 "heap max %llu cap %d | stage: states %llu chunk0 %llu\n",
+                 "heap max %llu cap %d | stage: %llu reset_locks %llu steps %llu\n",
                  cnt[8], cnt[9], cnt[10], cnt[11], cnt[12], cnt[13], cnt[14], cnt[6], cnt[15],
-                 cnt[5], cnt[38], P->hc_heap_cap, cnt[39], cnt[40]);
+                 cnt[5], cnt[38], P->hc_heap_cap, cnt[39], cnt[40], cnt[41]);
   if (std::getenv("EIK_HC_PROFILE"))
     std::fprintf(stderr,
                  "heapcell misses: unchained %llu pending %llu stale %llu wrong-inst %llu "

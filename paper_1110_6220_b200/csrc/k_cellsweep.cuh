@@ -263,8 +263,12 @@ __device__ __forceinline__ bool cell_sweep_lock32(const CellTile& T, int dir, in
     nm = __ballot_sync(kFull, un_n);
     if (act) wv = res;
     cw = act ? cc : -1.0;
-    __syncwarp();
+    // no per-step barrier: within a sweep no lane reads shared memory another
+    // lane wrote at an earlier step (operands come from later diagonals, and
+    // unlocks target already-processed nodes for the next sweep); the
+    // full-mask vote and ballot keep the lanes converged step by step
   }
+  __syncwarp();  // the next sweep / the scans read this sweep's stores
   updates_out += updates;
   return __any_sync(kFull, changed);
 }

@@ -218,19 +218,29 @@ __device__ __forceinline__ void cp_async8_ca(void* sdst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-// reset_locks (heap_cell.cpp:65-94)
+// reset_locks (heap_cell.cpp:65-94).  Lanes take (row offset, column) pairs
+// with one division per call, and every node's five cost loads are issued
+// together (the neighbour reads stay inside the tile: halo rows/columns).
 __device__ void reset_locks(const HTile& T, bool west_in, bool east_in, bool south_in,
                             bool north_in, int lane) {
-  for (int k = lane; k < T.w * T.h; k += 32) {
-    const int y = k / T.w, x = k % T.w;
-    bool un = false;
-    if (T.c(x, y) >= 0.0) {
-      un = (west_in && x == 0) || (east_in && x == T.w - 1) || (south_in && y == 0) ||
-           (north_in && y == T.h - 1);
-      un = un || (x + 1 < T.w && T.c(x + 1, y) < 0.0) || (x > 0 && T.c(x - 1, y) < 0.0) ||
-           (y + 1 < T.h && T.c(x, y + 1) < 0.0) || (y > 0 && T.c(x, y - 1) < 0.0);
+  const int w = T.w, h = T.h, pu = T.pu;
+  const int rows = w <= 32 ? 32 / w : 1;  // rows per pass
+  const int x0 = w <= 32 ? lane % w : lane, y0 = w <= 32 ? lane / w : 0;
+  const int xstep = w <= 32 ? w : 32;
+  if (y0 < rows) {
+    for (int x = x0; x < w; x += xstep) {
+      const bool bw = west_in && x == 0, be = east_in && x == w - 1;
+      const bool inE = x + 1 < w, inW = x > 0;
+#pragma unroll 4
+      for (int y = y0; y < h; y += rows) {
+        const double* c = &T.Ct[T.ci(x, y)];
+        const double cc = c[0], ce = c[1], cw = c[-1], cn = c[pu], cs = c[-pu];
+        const bool edge = bw || be || (south_in && y == 0) || (north_in && y == h - 1);
+        const bool exit_nb = (inE && ce < 0.0) | (inW && cw < 0.0) | (y + 1 < h && cn < 0.0) |
+                             (y > 0 && cs < 0.0);
+        T.lock[y * w + x] = (cc >= 0.0 && (edge || exit_nb)) ? 1 : 0;
+      }
     }
-    T.lock[k] = un ? 1 : 0;
   }
   __syncwarp();
 }
@@ -450,6 +460,7 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
   const unsigned my_flags = st_flags(st) | cflags;
   const bool first_removal = !st_first_done(st);
   reset_locks(T, ib > 0, ie < g.m, jb > 0, je < g.n, lane);
+  const long long p1b = prof ? clock64() : 0;
   const CellTile ct{T.U, T.Ct, T.lock, T.pu, T.w, T.h, 2};
   long long nsw = 0, upd = 0;
   if (a.fast) {
@@ -504,6 +515,8 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
     rec->updates = (int)upd;
   }
   if (prof) {
+    prof[4] += p1b - p1;                        // reset_locks
+    prof[5] += nsw * (long long)(T.w + T.h - 1);  // wavefront steps
     const long long p3 = clock64();
     prof[0] += p1 - p0;  // staging
     prof[1] += p2 - p1;  // locks + sweeps
@@ -554,7 +567,7 @@ __device__ void committer(const HcArgs& a, Heap& H, HTile& T, double* before, in
   long long removals = 0, sweeps = 0, updates = 0, mon_checks = 0, mon_single = 0;
   long long self_processed = 0, fast_hits = 0, waits = 0, chain_hits = 0;
   long long cyc_pop = 0, cyc_obtain = 0, cyc_self = 0, cyc_commit = 0;
-  long long prof[5] = {0, 0, 0, 0, 0};
+  long long prof[6] = {0, 0, 0, 0, 0, 0};
   long long miss_cls[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int max_size = H.size;
   int prev_cell = -1;
@@ -798,6 +811,7 @@ __device__ void committer(const HcArgs& a, Heap& H, HTile& T, double* before, in
     a.counters[14] = prof[2];
     a.counters[39] = prof[3];
     a.counters[40] = prof[4];
+    a.counters[41] = prof[5];
     a.counters[15] = chain_hits;
     for (int k = 0; k < 8; ++k) a.counters[16 + k] = miss_cls[k];
     a.counters[38] = (unsigned long long)max_size;
