@@ -245,13 +245,6 @@ __device__ void reset_locks(const HTile& T, bool west_in, bool east_in, bool sou
   __syncwarp();
 }
 
-struct Scan {
-  bool add;
-  unsigned fl;
-  double cand;
-  bool mon_checked, mon_single;
-};
-
 __device__ void mono_sides(int from_side, int out[2]) {  // cells.cpp:49-60
   switch (from_side) {
     case WEST: out[0] = NW; out[1] = SW; break;
@@ -261,38 +254,49 @@ __device__ void mono_sides(int from_side, int out[2]) {  // cells.cpp:49-60
   }
 }
 
-// scan_cell_boundary (heap_cell.cpp:173-239) as warp reductions
-__device__ Scan scan_side(const HcArgs& a, const HTile& T, int side, const double* before,
-                          const double* pstrip, bool first_removal, int lane) {
-  const bool vertical = (side == WEST || side == EAST);
+// scan_cell_boundary (heap_cell.cpp:173-239) for the four sides at once:
+// lanes 8s..8s+7 scan side s, so the
+// reductions (first strict maximum, should_add, monotonicity) stay inside an
+// 8-lane group and the four candidate divisions run in parallel; lane 8s
+// writes side s of the record.
+__device__ void scan_all(const HcArgs& a, const HTile& T, const double* before,
+                         const double* pstrip, bool first_removal, unsigned nbmask, SpecRec* rec,
+                         int lane) {
+  const int side = lane >> 3, q = lane & 7;
+  const bool vertical = side == WEST || side == EAST;
   const int len = vertical ? T.h : T.w;
+  const double* bf = before + side * a.max_len;
+  const bool has = (nbmask >> side) & 1u;
   double vmax = -kInf;
   int arg = 0x7fffffff;
   bool add = false, inc_viol = false, dec_viol = false;
-  for (int t = lane; t < len; t += 32) {
-    int x, y, ax, ay;
-    switch (side) {
-      case WEST: x = 0; y = t; ax = -1; ay = t; break;
-      case EAST: x = T.w - 1; y = t; ax = T.w; ay = t; break;
-      case SOUTH: x = t; y = 0; ax = t; ay = -1; break;
-      default: x = t; y = T.h - 1; ax = t; ay = T.h; break;
-    }
-    const double vi = T.u(x, y);
-    if (vi > vmax) {  // first strict maximum along the strip
-      vmax = vi;
-      arg = t;
-    }
-    const bool across_exit = T.c(ax, ay) < 0.0;
-    const bool changed = vi < before[t];
-    if (!across_exit && vi < T.u(ax, ay) && (changed || (first_removal && T.c(x, y) < 0.0)))
-      add = true;
-    if (t > 0) {
-      const double prev = vertical ? T.u(x, y - 1) : T.u(x - 1, y);
-      if (vi < prev) inc_viol = true;
-      if (vi > prev) dec_viol = true;
+  if (has) {
+    for (int t = q; t < len; t += 8) {
+      int x, y, ax, ay;
+      switch (side) {
+        case WEST: x = 0; y = t; ax = -1; ay = t; break;
+        case EAST: x = T.w - 1; y = t; ax = T.w; ay = t; break;
+        case SOUTH: x = t; y = 0; ax = t; ay = -1; break;
+        default: x = t; y = T.h - 1; ax = t; ay = T.h; break;
+      }
+      const double vi = T.u(x, y);
+      if (vi > vmax) {  // first strict maximum along the strip
+        vmax = vi;
+        arg = t;
+      }
+      const bool across_exit = T.c(ax, ay) < 0.0;
+      const bool changed = vi < bf[t];
+      if (!across_exit && vi < T.u(ax, ay) && (changed || (first_removal && T.c(x, y) < 0.0)))
+        add = true;
+      if (t > 0) {
+        const double prev = vertical ? T.u(x, y - 1) : T.u(x - 1, y);
+        if (vi < prev) inc_viol = true;
+        if (vi > prev) dec_viol = true;
+      }
     }
   }
-  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
     const double ov = __shfl_xor_sync(kFull, vmax, o);
     const int oa = __shfl_xor_sync(kFull, arg, o);
     if (ov > vmax || (ov == vmax && oa < arg)) {
@@ -300,35 +304,44 @@ __device__ Scan scan_side(const HcArgs& a, const HTile& T, int side, const doubl
       arg = oa;
     }
   }
-  Scan r;
-  r.add = __any_sync(kFull, add);
-  inc_viol = __any_sync(kFull, inc_viol);
-  dec_viol = __any_sync(kFull, dec_viol);
-  r.cand = kInf;
-  if (vmax < kInf) {  // isfinite(vmax): vmax > -inf always holds here
-    const double fprobe = pstrip[arg];  // preloaded probe strip of this side
-    const double hc = vertical ? a.hc_x : a.hc_y;
-    r.cand = vmax + 0.5 * (a.h + hc) / fprobe;  // cell_value_candidate (cells.hpp:109-112)
-  }
-  r.fl = 0;
-  r.mon_checked = r.mon_single = false;
-  if (r.add) {
-    int both[2];
-    mono_sides(side ^ 1, both);  // the neighbour is entered through the opposite side
-    if (a.fast) {
-      // sequences run north-to-south (vertical borders reversed) or west-to-east
-      const bool nondec = vertical ? !dec_viol : !inc_viol;
-      const bool noninc = vertical ? !inc_viol : !dec_viol;
-      if (nondec && !noninc) r.fl = 1u << both[0];
-      else if (noninc && !nondec) r.fl = 1u << both[1];
-      else r.fl = (1u << both[0]) | (1u << both[1]);
-      r.mon_checked = true;
-      r.mon_single = (nondec != noninc);
-    } else {
-      r.fl = (1u << both[0]) | (1u << both[1]);
+  const unsigned gm = 0xFFu << (8 * side);
+  add = (__ballot_sync(kFull, add) & gm) != 0u;
+  inc_viol = (__ballot_sync(kFull, inc_viol) & gm) != 0u;
+  dec_viol = (__ballot_sync(kFull, dec_viol) & gm) != 0u;
+  if (q != 0) return;
+  double cand = kInf;
+  unsigned fl = 0;
+  bool mon_checked = false, mon_single = false;
+  if (has) {
+    if (vmax < kInf) {  // isfinite(vmax): vmax > -inf always holds here
+      const double fprobe = pstrip[side * a.max_len + arg];
+      const double hc = vertical ? a.hc_x : a.hc_y;
+      cand = vmax + 0.5 * (a.h + hc) / fprobe;  // cell_value_candidate (cells.hpp:109-112)
     }
+    if (add) {
+      int both[2];
+      mono_sides(side ^ 1, both);  // the neighbour is entered through the opposite side
+      if (a.fast) {
+        // sequences run north-to-south (vertical borders reversed) or west-to-east
+        const bool nondec = vertical ? !dec_viol : !inc_viol;
+        const bool noninc = vertical ? !inc_viol : !dec_viol;
+        if (nondec && !noninc) fl = 1u << both[0];
+        else if (noninc && !nondec) fl = 1u << both[1];
+        else fl = (1u << both[0]) | (1u << both[1]);
+        mon_checked = true;
+        mon_single = (nondec != noninc);
+      } else {
+        fl = (1u << both[0]) | (1u << both[1]);
+      }
+    }
+  } else {
+    add = false;
   }
-  return r;
+  rec->cand[side] = cand;
+  rec->add[side] = add;
+  rec->fl[side] = (uint8_t)fl;
+  rec->monc[side] = mon_checked;
+  rec->mons[side] = mon_single;
 }
 
 __device__ __forceinline__ void hc_cell_rect(const CellGeom& g, int cell, int64_t& ib, int64_t& ie,
@@ -491,25 +504,10 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
     spare[y * mw + x] = T.u(x, y);
   }
   SpecRec* rec = rec_ptr(a, kind, cell);
-  for (int side = 0; side < 4; ++side) {
-    Scan sc;
-    if (has_nb[side]) {
-      sc = scan_side(a, T, side, before + side * a.max_len, pstrip + side * a.max_len,
-                     first_removal, lane);
-    } else {
-      sc.add = false;
-      sc.fl = 0;
-      sc.cand = kInf;
-      sc.mon_checked = sc.mon_single = false;
-    }
-    if (lane == 0) {
-      rec->cand[side] = sc.cand;
-      rec->add[side] = sc.add;
-      rec->fl[side] = (uint8_t)sc.fl;
-      rec->monc[side] = sc.mon_checked;
-      rec->mons[side] = sc.mon_single;
-    }
-  }
+  scan_all(a, T, before, pstrip, first_removal,
+           (has_nb[0] ? 1u : 0u) | (has_nb[1] ? 2u : 0u) | (has_nb[2] ? 4u : 0u) |
+               (has_nb[3] ? 8u : 0u),
+           rec, lane);
   if (lane == 0) {
     rec->sweeps = (int)nsw;
     rec->updates = (int)upd;
