@@ -180,6 +180,7 @@ __device__ bool cell_sweep_ns(const CellTile& T, int dir, int lane, long long& u
 // cells with branch-free operand loads (clamped in-tile addresses, selected
 // afterwards) and the fp64 update skipped warp-uniformly when no lane holds
 // an unlocked node (most steps of a locked sweep).  Stores are predicated.
+template <bool SKIP>
 __device__ __forceinline__ bool cell_sweep_lock32(const CellTile& T, int dir, int lane,
                                                   long long& updates_out) {
   const bool iasc = (dir == kSW || dir == kNW);
@@ -210,6 +211,7 @@ __device__ __forceinline__ bool cell_sweep_lock32(const CellTile& T, int dir, in
     const int a = s - b;
     const bool act = rv && a >= 0 && a < w;
     const int o = act ? vb + dx * a : pu + ox;  // (0,0): every neighbour is in the tile
+    // (the prefetch after the last step reads this harmless node)
     q_cur = U[o];
     q_cc = C[o];
     q_e = U[o + dx];
@@ -226,7 +228,7 @@ __device__ __forceinline__ bool cell_sweep_lock32(const CellTile& T, int dir, in
     const double cur = q_cur, cc = q_cc, e = q_e, ce = q_ce, n = q_n, cn = q_cn, cs = q_cs,
                  hs = q_hs;
     const int lk = q_lk;
-    if (s < last) load(s + 1);  // prefetch while this step computes
+    load(s + 1);  // prefetch while this step computes
     const int a = s - b;
     const bool act = rv && a >= 0 && a < w;
     // the S neighbour's new value and N-unlock: lane-1 at the previous step
@@ -239,21 +241,25 @@ __device__ __forceinline__ bool cell_sweep_lock32(const CellTile& T, int dir, in
     const bool proc = act && cc >= 0.0 && (lk != 0 || unW || sbit != 0u);
     bool un_n = false, nunW = false;
     double res = cur;
-    if (__any_sync(kFull, proc)) {
+    // SKIP: jump over the fp64 chain when no lane holds an unlocked node (a
+    // vote on the critical path); otherwise compute it for every lane and
+    // predicate the stores, leaving only value -> shuffle -> update ->
+    // select between consecutive steps.
+    if (!SKIP || __any_sync(kFull, proc)) {
       const int o = act ? vb + dx * a : pu + ox;
       const int lo = act ? lb + dx * a : 0;
       const double cand = node_update4(e, wv, n, sv, cc);
       const bool dec = proc && cand < cur;
+      res = dec ? cand : cur;
       if (dec) {
-        res = cand;
         changed = true;
         U[o] = cand;
         // already-processed W and S neighbours: unlocked for the next sweep
         if (a > 0 && cw >= 0.0 && wv > cand) L[lo - dx] = 1;
         if (b > 0 && cs >= 0.0 && sv > cand) L[lo - dyl] = 1;
-        un_n = (b + 1 < h) && cn >= 0.0 && n > cand;
-        nunW = (a + 1 < w) && ce >= 0.0 && e > cand;
       }
+      un_n = dec && (b + 1 < h) && cn >= 0.0 && n > cand;
+      nunW = dec && (a + 1 < w) && ce >= 0.0 && e > cand;
       if (proc) {  // relock on processing (heap_cell.cpp:110-111)
         L[lo] = 0;
         ++updates;
@@ -273,9 +279,14 @@ __device__ __forceinline__ bool cell_sweep_lock32(const CellTile& T, int dir, in
   return __any_sync(kFull, changed);
 }
 
+// skip (MODE 2, <= 32 rows): jump over steps in which no node is unlocked --
+// worth it for sweeps that are mostly locked (HCM's convergence sweeps).
 template <int MODE>
-__device__ bool cell_sweep(const CellTile& T, int dir, int lane, long long& updates) {
-  if (MODE == 2 && T.h <= 32) return cell_sweep_lock32(T, dir, lane, updates);
+__device__ bool cell_sweep(const CellTile& T, int dir, int lane, long long& updates,
+                           bool skip = false) {
+  if (MODE == 2 && T.h <= 32)
+    return skip ? cell_sweep_lock32<true>(T, dir, lane, updates)
+                : cell_sweep_lock32<false>(T, dir, lane, updates);
   if (T.h <= 32) return cell_sweep_ns<MODE, 1>(T, dir, lane, updates);
   if (T.h <= 64) return cell_sweep_ns<MODE, 2>(T, dir, lane, updates);
   if (T.h <= 96) return cell_sweep_ns<MODE, 3>(T, dir, lane, updates);

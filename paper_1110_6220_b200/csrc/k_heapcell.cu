@@ -491,7 +491,7 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
     bool changed = true;
     while (changed) {
       const int dir = nsw < 4 ? perm[nsw] : kRotation[nsw % 4];
-      changed = cell_sweep<2>(ct, dir, lane, upd);
+      changed = cell_sweep<2>(ct, dir, lane, upd, /*skip=*/true);
       ++nsw;
     }
   }

@@ -34,6 +34,7 @@ __global__ void bench(int w, int h, int reps, long long* out, double* sink) {
   long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
     if (MODE == 3) cell_sweep_ns<2, 1>(T, r & 3, lane, upd);  // the generic locked engine
+    else if (MODE == 4) cell_sweep_lock32<true>(T, r & 3, lane, upd);  // with the vote skip
     else cell_sweep<MODE>(T, r & 3, lane, upd);
     if (MODE >= 2)
       for (int k = lane; k < w * h; k += 32) T.lock[k] = 1;
@@ -56,11 +57,12 @@ int main() {
     const int w = sz[0], h = sz[1], reps = 200;
     const int pu = (w + 3) & ~1;
     const size_t smem = 2 * (h + 2) * pu * 8 + w * h + 16;
-    long long cyc[4];
+    long long cyc[5];
     cudaFuncSetAttribute(bench<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(bench<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(bench<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaFuncSetAttribute(bench<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(bench<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     bench<0><<<1, 32, smem>>>(w, h, reps, d_out, d_sink);
     cudaMemcpy(&cyc[0], d_out, 8, cudaMemcpyDeviceToHost);
     bench<1><<<1, 32, smem>>>(w, h, reps, d_out, d_sink);
@@ -69,9 +71,12 @@ int main() {
     cudaMemcpy(&cyc[2], d_out, 8, cudaMemcpyDeviceToHost);
     bench<3><<<1, 32, smem>>>(w, h, reps, d_out, d_sink);
     cudaMemcpy(&cyc[3], d_out, 8, cudaMemcpyDeviceToHost);
+    bench<4><<<1, 32, smem>>>(w, h, reps, d_out, d_sink);
+    cudaMemcpy(&cyc[4], d_out, 8, cudaMemcpyDeviceToHost);
     const double steps = (double)reps * (w + h - 1);
-    printf("cell %dx%d: cycles/step full %.0f directional %.0f locked %.0f (generic %.0f)  (%s)\n",
-           w, h, cyc[0] / steps, cyc[1] / steps, cyc[2] / steps, cyc[3] / steps,
+    printf("cell %dx%d: cycles/step full %.0f directional %.0f locked %.0f (vote-skip %.0f, generic "
+           "%.0f)  (%s)\n",
+           w, h, cyc[0] / steps, cyc[1] / steps, cyc[2] / steps, cyc[4] / steps, cyc[3] / steps,
            cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
