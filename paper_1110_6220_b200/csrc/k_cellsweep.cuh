@@ -175,118 +175,156 @@ __device__ bool cell_sweep_ns(const CellTile& T, int dir, int lane, long long& u
   return __any_sync(kFull, changed);
 }
 
-// Locking sweep (MODE 2) for cells of at most 32 rows, one node per lane per
-// step: the dataflow of cell_sweep_ns<2, 1> restated for the common small
-// cells with branch-free operand loads (clamped in-tile addresses, selected
-// afterwards) and the fp64 update skipped warp-uniformly when no lane holds
-// an unlocked node (most steps of a locked sweep).  Stores are predicated.
-template <bool SKIP>
-__device__ __forceinline__ bool cell_sweep_lock32(const CellTile& T, int dir, int lane,
-                                                  long long& updates_out) {
+// Locking sweep (MODE 2), NS rows per lane (row lane + 32r in slot r): the
+// dataflow of cell_sweep_ns<2, NS> restated with branch-free operand loads
+// (clamped in-tile addresses) and predicated stores.  SKIP jumps over the
+// fp64 chain when no lane holds an unlocked node (a vote on the critical
+// path, worth it for mostly-locked sweeps); otherwise only value -> shuffle
+// -> update -> select lies between consecutive steps.  Within a sweep no lane
+// reads shared memory another lane wrote at an earlier step (operands come
+// from later diagonals; unlocks target already-processed nodes for the next
+// sweep), and the full-mask shuffles/ballots keep the lanes converged, so
+// there is no per-step barrier.
+template <bool SKIP, int NS>
+__device__ __forceinline__ bool cell_sweep_lock(const CellTile& T, int dir, int lane,
+                                                long long& updates_out) {
   const bool iasc = (dir == kSW || dir == kNW);
   const bool jasc = (dir == kSW || dir == kSE);
-  const int w = T.w, h = T.h, pu = T.pu;
+  const int w = T.w, h = T.h, pu = T.pu, ox = T.ox;
   const int dx = iasc ? 1 : -1;
   const int dyp = jasc ? pu : -pu;
   const int dyl = jasc ? w : -w;
   const int x0 = iasc ? 0 : w - 1;
-  const int b = lane;
-  const bool rv = b < h;
-  const int y = jasc ? b : h - 1 - b;
-  const int ox = T.ox;
-  const int vb = rv ? (y + 1) * pu + (x0 + ox) : pu + ox;  // value offset of a = 0
-  const int lb = rv ? y * w + x0 : 0;                    // lock offset of a = 0
   double* __restrict__ U = T.U;
   const double* __restrict__ C = T.Ct;
   uint8_t* __restrict__ L = T.lock;
-  double wv = rv ? U[vb - dx] : kInf;  // W: frozen halo column, then own new values
-  double cw = -1.0;                    // W cost (< 0: halo or exit, never unlocked)
-  bool unW = false;                    // the W neighbour unlocked this node
-  unsigned nm = 0u;                    // last step's ballot of "unlock my N"
+  int vb[NS], lb[NS];
+  bool rv[NS], unW[NS];
+  double wv[NS], cw[NS];
+  unsigned nm[NS];
+#pragma unroll
+  for (int r = 0; r < NS; ++r) {
+    const int b = lane + 32 * r;
+    rv[r] = b < h;
+    const int y = jasc ? b : h - 1 - b;
+    vb[r] = rv[r] ? (y + 1) * pu + (x0 + ox) : pu + ox;  // value offset of a = 0
+    lb[r] = rv[r] ? y * w + x0 : 0;                      // lock offset of a = 0
+    wv[r] = rv[r] ? U[vb[r] - dx] : kInf;  // W: frozen halo column, then own new values
+    cw[r] = -1.0;                          // W cost (< 0: halo or exit, never unlocked)
+    unW[r] = false;                        // the W neighbour unlocked this node
+    nm[r] = 0u;                            // last step's ballot of "unlock my N"
+  }
   int updates = 0;
   bool changed = false;
-  double q_cur, q_cc, q_e, q_ce, q_n, q_cn, q_cs, q_hs;
-  int q_lk;
+  double q_cur[NS], q_cc[NS], q_e[NS], q_ce[NS], q_n[NS], q_cn[NS], q_cs[NS], q_hs[NS];
+  int q_lk[NS];
   auto load = [&](int s) {
-    const int a = s - b;
-    const bool act = rv && a >= 0 && a < w;
-    const int o = act ? vb + dx * a : pu + ox;  // (0,0): every neighbour is in the tile
-    // (the prefetch after the last step reads this harmless node)
-    q_cur = U[o];
-    q_cc = C[o];
-    q_e = U[o + dx];
-    q_ce = C[o + dx];
-    q_n = U[o + dyp];
-    q_cn = C[o + dyp];
-    q_cs = C[o - dyp];
-    q_hs = U[o - dyp];
-    q_lk = L[act ? lb + dx * a : 0];
+#pragma unroll
+    for (int r = 0; r < NS; ++r) {
+      const int a = s - lane - 32 * r;
+      const bool act = rv[r] && a >= 0 && a < w;
+      // (0,0) when inactive: every neighbour read stays in the tile
+      const int o = act ? vb[r] + dx * a : pu + ox;
+      q_cur[r] = U[o];
+      q_cc[r] = C[o];
+      q_e[r] = U[o + dx];
+      q_ce[r] = C[o + dx];
+      q_n[r] = U[o + dyp];
+      q_cn[r] = C[o + dyp];
+      q_cs[r] = C[o - dyp];
+      q_hs[r] = U[o - dyp];
+      q_lk[r] = L[act ? lb[r] + dx * a : 0];
+    }
   };
   load(0);
   const int last = (h - 1) + (w - 1);
   for (int s = 0; s <= last; ++s) {
-    const double cur = q_cur, cc = q_cc, e = q_e, ce = q_ce, n = q_n, cn = q_cn, cs = q_cs,
-                 hs = q_hs;
-    const int lk = q_lk;
-    load(s + 1);  // prefetch while this step computes
-    const int a = s - b;
-    const bool act = rv && a >= 0 && a < w;
-    // the S neighbour's new value and N-unlock: lane-1 at the previous step
-    double sv = __shfl_up_sync(kFull, wv, 1);
-    unsigned sbit = (nm >> ((lane + 31) & 31)) & 1u;
-    if (b == 0) {
-      sv = hs;
-      sbit = 0u;
+    double cur[NS], cc[NS], e[NS], ce[NS], n[NS], cn[NS], cs[NS], hs[NS];
+    int lk[NS];
+#pragma unroll
+    for (int r = 0; r < NS; ++r) {
+      cur[r] = q_cur[r];
+      cc[r] = q_cc[r];
+      e[r] = q_e[r];
+      ce[r] = q_ce[r];
+      n[r] = q_n[r];
+      cn[r] = q_cn[r];
+      cs[r] = q_cs[r];
+      hs[r] = q_hs[r];
+      lk[r] = q_lk[r];
     }
-    const bool proc = act && cc >= 0.0 && (lk != 0 || unW || sbit != 0u);
-    bool un_n = false, nunW = false;
-    double res = cur;
-    // SKIP: jump over the fp64 chain when no lane holds an unlocked node (a
-    // vote on the critical path); otherwise compute it for every lane and
-    // predicate the stores, leaving only value -> shuffle -> update ->
-    // select between consecutive steps.
-    if (!SKIP || __any_sync(kFull, proc)) {
-      const int o = act ? vb + dx * a : pu + ox;
-      const int lo = act ? lb + dx * a : 0;
-      const double cand = node_update4(e, wv, n, sv, cc);
-      const bool dec = proc && cand < cur;
-      res = dec ? cand : cur;
-      if (dec) {
-        changed = true;
-        U[o] = cand;
-        // already-processed W and S neighbours: unlocked for the next sweep
-        if (a > 0 && cw >= 0.0 && wv > cand) L[lo - dx] = 1;
-        if (b > 0 && cs >= 0.0 && sv > cand) L[lo - dyl] = 1;
-      }
-      un_n = dec && (b + 1 < h) && cn >= 0.0 && n > cand;
-      nunW = dec && (a + 1 < w) && ce >= 0.0 && e > cand;
-      if (proc) {  // relock on processing (heap_cell.cpp:110-111)
-        L[lo] = 0;
-        ++updates;
-      }
+    load(s + 1);  // prefetch while this step computes (past the end: harmless)
+    // previous-step values: slot r's lane 0 takes slot r-1's lane 31
+    double wv_old[NS];
+    unsigned nm_old[NS];
+#pragma unroll
+    for (int r = 0; r < NS; ++r) {
+      wv_old[r] = wv[r];
+      nm_old[r] = nm[r];
     }
-    unW = nunW;
-    nm = __ballot_sync(kFull, un_n);
-    if (act) wv = res;
-    cw = act ? cc : -1.0;
-    // no per-step barrier: within a sweep no lane reads shared memory another
-    // lane wrote at an earlier step (operands come from later diagonals, and
-    // unlocks target already-processed nodes for the next sweep); the
-    // full-mask vote and ballot keep the lanes converged step by step
+#pragma unroll
+    for (int r = 0; r < NS; ++r) {
+      const int b = lane + 32 * r;
+      const int a = s - b;
+      const bool act = rv[r] && a >= 0 && a < w;
+      const double send = (lane == 31 && r > 0) ? wv_old[r > 0 ? r - 1 : 0] : wv_old[r];
+      double sv = __shfl_sync(kFull, send, (lane + 31) & 31);
+      unsigned sbit = lane == 0 ? (r > 0 ? (nm_old[r > 0 ? r - 1 : 0] >> 31) & 1u : 0u)
+                                : (nm_old[r] >> (lane - 1)) & 1u;
+      if (b == 0) {
+        sv = hs[r];
+        sbit = 0u;
+      }
+      const bool proc = act && cc[r] >= 0.0 && (lk[r] != 0 || unW[r] || sbit != 0u);
+      bool un_n = false, nunW = false;
+      double res = cur[r];
+      if (!SKIP || __any_sync(kFull, proc)) {
+        const int o = act ? vb[r] + dx * a : pu + ox;
+        const int lo = act ? lb[r] + dx * a : 0;
+        const double cand = node_update4(e[r], wv[r], n[r], sv, cc[r]);
+        const bool dec = proc && cand < cur[r];
+        res = dec ? cand : cur[r];
+        if (dec) {
+          changed = true;
+          U[o] = cand;
+          // already-processed W and S neighbours: unlocked for the next sweep
+          if (a > 0 && cw[r] >= 0.0 && wv[r] > cand) L[lo - dx] = 1;
+          if (b > 0 && cs[r] >= 0.0 && sv > cand) L[lo - dyl] = 1;
+        }
+        un_n = dec && (b + 1 < h) && cn[r] >= 0.0 && n[r] > cand;
+        nunW = dec && (a + 1 < w) && ce[r] >= 0.0 && e[r] > cand;
+        if (proc) {  // relock on processing (heap_cell.cpp:110-111)
+          L[lo] = 0;
+          ++updates;
+        }
+      }
+      unW[r] = nunW;
+      nm[r] = __ballot_sync(kFull, un_n);
+      if (act) wv[r] = res;
+      cw[r] = act ? cc[r] : -1.0;
+    }
   }
   __syncwarp();  // the next sweep / the scans read this sweep's stores
   updates_out += updates;
   return __any_sync(kFull, changed);
 }
 
-// skip (MODE 2, <= 32 rows): jump over steps in which no node is unlocked --
-// worth it for sweeps that are mostly locked (HCM's convergence sweeps).
+// skip (MODE 2): jump over steps in which no node is unlocked -- worth it for
+// sweeps that are mostly locked (HCM's convergence sweeps).
 template <int MODE>
 __device__ bool cell_sweep(const CellTile& T, int dir, int lane, long long& updates,
                            bool skip = false) {
-  if (MODE == 2 && T.h <= 32)
-    return skip ? cell_sweep_lock32<true>(T, dir, lane, updates)
-                : cell_sweep_lock32<false>(T, dir, lane, updates);
+  if (MODE == 2) {
+    if (T.h <= 32)
+      return skip ? cell_sweep_lock<true, 1>(T, dir, lane, updates)
+                  : cell_sweep_lock<false, 1>(T, dir, lane, updates);
+    if (T.h <= 64)
+      return skip ? cell_sweep_lock<true, 2>(T, dir, lane, updates)
+                  : cell_sweep_lock<false, 2>(T, dir, lane, updates);
+    if (T.h <= 96)
+      return skip ? cell_sweep_lock<true, 3>(T, dir, lane, updates)
+                  : cell_sweep_lock<false, 3>(T, dir, lane, updates);
+  }
   if (T.h <= 32) return cell_sweep_ns<MODE, 1>(T, dir, lane, updates);
   if (T.h <= 64) return cell_sweep_ns<MODE, 2>(T, dir, lane, updates);
   if (T.h <= 96) return cell_sweep_ns<MODE, 3>(T, dir, lane, updates);

@@ -34,7 +34,7 @@ __global__ void bench(int w, int h, int reps, long long* out, double* sink) {
   long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
     if (MODE == 3) cell_sweep_ns<2, 1>(T, r & 3, lane, upd);  // the generic locked engine
-    else if (MODE == 4) cell_sweep_lock32<true>(T, r & 3, lane, upd);  // with the vote skip
+    else if (MODE == 4) cell_sweep_lock<true, 1>(T, r & 3, lane, upd);  // with the vote skip
     else cell_sweep<MODE>(T, r & 3, lane, upd);
     if (MODE >= 2)
       for (int k = lane; k < w * h; k += 32) T.lock[k] = 1;
