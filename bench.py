@@ -281,8 +281,17 @@ def main():
         if best is None or t > best[1]:
             best = (k, t, nbytes, ach)
     dom_k, dom_t, dom_bytes, dom_ach = best
+    # DRAM bytes of the dominant launch from a committed `ncu --set full`
+    # capture (profiles/r01_traffic.json), when it profiled this same solve
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
+            traffic = json.load(f).get(dom_k, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
     roofline = {"bound": "hbm", "kernel": dom_k, "achieved": round(dom_ach, 2), "peak": hbm,
-                "unit": "GB/s", "frac": dom_ach / hbm, "traffic": None, "peak_kind": peak_kind,
+                "unit": "GB/s", "frac": dom_ach / hbm, "traffic": traffic,
+                "algorithmic_bytes": dom_bytes, "peak_kind": peak_kind,
                 "note": "latency-bound fp64 dependency chains; algorithmic bytes per SURVEY §8(d)"}
 
     # e2e: public API, pinned host buffers, H2D + solve + D2H inside the timed region
