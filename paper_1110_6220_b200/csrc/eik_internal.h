@@ -89,19 +89,20 @@ struct HcArgs {
   int* wdbg;                // optional debug: [workers][4] phase, cell, kind, time
   int* owner;               // optional debug: [2][J] last claiming worker
   int* done_flag;
-  int* hsize_pub;           // heap size, published for the workers
-  int window;               // workers speculate heap positions [0, window)
+  int* hsize_pub;           // [0] queue size, [31..62] per-bucket counts (workers)
   int64_t tile_doubles;     // per-warp smem
-  int heap_cap;             // >0: committer heap entries in shared memory, capacity;
-                            // 0: entries in global memory (hkey + harr)
+  int heap_cap;             // >0: committer queue buckets in shared memory, capacity
+                            // per bucket; 0: buckets in global memory (hkey + harr)
+  int heap_capb_global;     // bucket capacity of the global layout (ceil(J/32))
+  int pub_capb;             // bucket stride of the published id mirror (harr)
   const double* C;          // padded h/F
   double* u;                // padded values
   const double* probe[4];   // F at border probe points: W/E [cells_x*n], S/N [cells_y*m]
   double h, hc_x, hc_y;
   double* cval;             // [J] cell values (heap_cell.cpp cell_value)
-  double* hkey;             // [J] heap entry keys (global-entry mode)
-  int* hpos;                // [J] heap position of every cell, -1 if not queued
-  int* harr;                // [J] heap entry ids: published prefix / global entries
+  double* hkey;             // [32][capb] queue keys (global-bucket mode)
+  int* hpos;                // [J] queue position of every cell (bucket << 24 | slot), -1
+  int* harr;                // [32][capb] queue ids: mirror for the workers / global buckets
   const int* init_cells;    // Q-cells in ascending id order with their initial values
   const double* init_values;
   int n_init;

@@ -57,7 +57,8 @@ struct eik_plan {
   double* dCKey = nullptr;                // published heap keys
   unsigned* dCTag = nullptr;              // last committed instance per cell
   int hc_chain = 1;
-  int hc_heap_cap = 0;                    // committer heap capacity in smem (0 = global)
+  int hc_heap_cap = 0;                    // committer queue bucket capacity in smem (0 = global)
+  int hc_capb_global = 0;                 // bucket capacity in global memory
   double* dCVal = nullptr;                // cell values
   double* dHKey = nullptr;
   int* dHPos = nullptr;

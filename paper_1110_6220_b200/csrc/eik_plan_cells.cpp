@@ -93,7 +93,9 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     }
     if ((rc = dalloc(&P->dState, J))) return rc;
     P->allocs.push_back(P->dState);
-    if ((rc = dalloc(&P->dHKey, J))) return rc;
+    const int64_t capb_g = (J + 31) / 32;  // a bucket holds every id = b mod 32
+    P->hc_capb_global = (int)capb_g;
+    if ((rc = dalloc(&P->dHKey, 32 * capb_g))) return rc;
     P->allocs.push_back(P->dHKey);
     if ((rc = dalloc(&P->dCKey, J))) return rc;
     P->allocs.push_back(P->dCKey);
@@ -103,7 +105,7 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     P->allocs.push_back(P->dCVal);
     if ((rc = dalloc(&P->dHPos, J))) return rc;
     P->allocs.push_back(P->dHPos);
-    if ((rc = dalloc(&P->dHArr, J))) return rc;
+    if ((rc = dalloc(&P->dHArr, 32 * capb_g))) return rc;
     P->allocs.push_back(P->dHArr);
     if ((rc = dalloc(&P->dInitCells, J))) return rc;
     P->allocs.push_back(P->dInitCells);
@@ -120,7 +122,7 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     P->allocs.push_back(P->dBusy);
     if ((rc = dalloc(&P->dRec, 2 * J))) return rc;
     P->allocs.push_back(P->dRec);
-    if ((rc = dalloc(&P->dHcMisc, 4))) return rc;
+    if ((rc = dalloc(&P->dHcMisc, 64))) return rc;
     P->allocs.push_back(P->dHcMisc);
     // per-warp tile: values + costs with halo, 4 border snapshots, lock bytes
     const size_t tile = ((smem + sizeof(double) - 1) / sizeof(double) + 1) & ~(size_t)1;
@@ -129,9 +131,12 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     // the committer's heap + cell values go to its shared memory when they
     // fit next to its tile (uint16 heap indices)
     {
+      // committer queue buckets in shared memory next to its tile; a bucket
+      // that fills up raises a status and the run repeats with global buckets
       const size_t room = 220 * 1024 > tile * 8 ? 220 * 1024 - tile * 8 : 0;
-      const size_t cap = std::min<size_t>((size_t)J, room / heapcell_committer_heap_bytes(1));
-      P->hc_heap_cap = cap >= 64 ? (int)cap : 0;
+      size_t capb = std::min<size_t>((size_t)capb_g, room / (32 * 12));
+      while (capb > 0 && heapcell_committer_heap_bytes((int)capb) > room) --capb;
+      P->hc_heap_cap = capb >= 8 ? (int)capb : 0;
     }
     if (std::getenv("EIK_HC_GLOBAL_HEAP")) P->hc_heap_cap = 0;
     // EIK_HC_HEAP_CAP=n caps the shared-memory heap (exercises the overflow
@@ -347,9 +352,10 @@ retry:  // after a committer heap overflow, with the heap in global memory
   if (const char* c = std::getenv("EIK_HC_IDLE_NS")) a.idle_ns = std::atoi(c);
   a.done_flag = P->dHcMisc;
   a.hsize_pub = P->dHcMisc + 1;
-  a.window = 4096;
+  a.heap_capb_global = P->hc_capb_global;
+  a.pub_capb = P->hc_heap_cap > 0 ? P->hc_heap_cap : P->hc_capb_global;
   a.tile_doubles = P->cg.tile_doubles;
-  CK(cudaMemsetAsync(P->dHcMisc, 0, sizeof(int) * 4, P->stream));
+  CK(cudaMemsetAsync(P->dHcMisc, 0, sizeof(int) * 64, P->stream));
   CK(launch_heapcell(a, P->hc_warps_per_cta, P->hc_max_ctas, P->stream, &launches));
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];

@@ -114,83 +114,129 @@ __device__ __forceinline__ bool tag_is(unsigned sv, unsigned v) {
   return sv != kSpecNone && (sv & kTagMask) == v;
 }
 
-// ---- indexed min-heap over cells keyed by (cell value, id) ------------------
-// indexed_min_heap.hpp:11-106, ties to the smaller id.  Entries (key, id) live
-// in the committer's shared memory (or global memory when the heap could
-// outgrow it); the heap position of every cell is mirrored to global memory
-// (pos[]), since it is needed only for the popped cell's 4 neighbours, whose
-// positions are prefetched with the rest of the commit and tracked through
-// the sifts (trk/tps).  `pub` mirrors heap positions < window for the
-// workers.
-struct Heap {
-  double* hk;
-  int* hid;
-  int* pos;
-  int* pub;
-  int window;
+// ---- the committer's priority queue over cells keyed by (cell value, id) ---
+// The reference pops the minimum (value, id) of an indexed binary heap
+// (indexed_min_heap.hpp:11-106, ties to the smaller id); the pop order depends
+// only on the keys, not on the heap's shape, so any exact min-structure
+// replays it.  Here: 32 buckets (cell id mod 32) of unordered entries with
+// each bucket's minimum cached.  pop = one warp argmin over the 32 cached
+// minima + a warp rescan of the winning bucket; insert and decrease-key are
+// O(1).  Entries live in the committer's shared memory (or global memory
+// when a bucket could overflow it); every cell's position is mirrored to
+// global memory (pos[], needed only for the popped cell's 4 neighbours,
+// prefetched with the rest of the commit and tracked through moves).  The
+// bucket arrays and counts are mirrored to global memory for the workers.
+struct BucketPQ {
+  double* bk;     // [32][capb] keys
+  int* bi;        // [32][capb] ids
+  int* cnt;       // [32] entries per bucket
+  double* mk;     // [32] cached bucket minima (+inf when empty)
+  int* mi;        //      their ids (INT_MAX when empty)
+  int* msl;       //      their slots
+  int capb;
+  int* pos;       // global [J]: bucket << 24 | slot, -1 = not queued
+  int* pub;       // global [32][capb] id mirror (null: bi is global already)
+  int* pubcnt;    // global [32] count mirror
   int size;
-  int cap;
   bool overflow;
-  int trk[4], tps[4];
+  int trk[4], tps[4];  // tracked cells (the popped cell's neighbours) and positions
   __device__ static bool less(double ka, int ia, double kb, int ib) {
     return ka < kb || (ka == kb && ia < ib);
   }
-  __device__ void put(int p, double k, int id) {
-    hk[p] = k;
-    hid[p] = id;
-    pos[id] = p;
-    // plain stores: the published prefix is only a hint for the workers
-    if (pub && p < window) pub[p] = id;
+  __device__ void track(int id, int enc) {
 #pragma unroll
     for (int t = 0; t < 4; ++t)
-      if (trk[t] == id) tps[t] = p;
+      if (trk[t] == id) tps[t] = enc;
   }
-  __device__ void up(int p, double k, int id) {
-    while (p > 0) {
-      const int par = (p - 1) >> 1;
-      const double kp = hk[par];
-      const int ip = hid[par];
-      if (!less(k, id, kp, ip)) break;
-      put(p, kp, ip);
-      p = par;
-    }
-    put(p, k, id);
+  __device__ void set(int l, int s, double k, int id) {  // lane 0
+    bk[l * capb + s] = k;
+    bi[l * capb + s] = id;
+    pos[id] = (l << 24) | s;
+    if (pub) pub[l * capb + s] = id;
+    track(id, (l << 24) | s);
   }
-  __device__ void down(int p, double k, int id) {
-    for (;;) {
-      int c = 2 * p + 1;
-      if (c >= size) break;
-      double kc = hk[c];
-      int ic = hid[c];
-      if (c + 1 < size) {
-        const double k2 = hk[c + 1];
-        const int i2 = hid[c + 1];
-        if (less(k2, i2, kc, ic)) {
-          ++c;
-          kc = k2;
-          ic = i2;
-        }
-      }
-      if (!less(kc, ic, k, id)) break;
-      put(p, kc, ic);
-      p = c;
-    }
-    put(p, k, id);
-  }
-  __device__ void insert(int id, double k) {
-    if (size >= cap) {
+  __device__ void insert(int id, double k) {  // lane 0
+    const int l = id & 31, s = cnt[l];
+    if (s >= capb) {
       overflow = true;
       return;
     }
+    set(l, s, k, id);
+    cnt[l] = s + 1;
+    pubcnt[l] = s + 1;
+    if (less(k, id, mk[l], mi[l])) {
+      mk[l] = k;
+      mi[l] = id;
+      msl[l] = s;
+    }
     ++size;
-    up(size - 1, k, id);
   }
-  __device__ void decrease(int p, double k) { up(p, k, hid[p]); }
-  __device__ int pop() {
-    const int top = hid[0];
-    pos[top] = -1;
-    --size;
-    if (size > 0) down(0, hk[size], hid[size]);
+  __device__ void decrease(int enc, double k) {  // lane 0; keys only decrease
+    const int l = enc >> 24, s = enc & 0xFFFFFF;
+    const int id = bi[l * capb + s];
+    bk[l * capb + s] = k;
+    if (less(k, id, mk[l], mi[l])) {
+      mk[l] = k;
+      mi[l] = id;
+      msl[l] = s;
+    }
+  }
+  // all lanes; returns the popped id (or -1 when empty) on every lane
+  __device__ int pop(int lane) {
+    double kl = mk[lane];
+    int il = mi[lane], wl = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ko = __shfl_xor_sync(kFull, kl, o);
+      const int io = __shfl_xor_sync(kFull, il, o);
+      const int wo = __shfl_xor_sync(kFull, wl, o);
+      if (less(ko, io, kl, il)) {
+        kl = ko;
+        il = io;
+        wl = wo;
+      }
+    }
+    if (!(kl < kInf) && il == 0x7fffffff) return -1;  // every bucket empty
+    const int w = wl, top = il;
+    if (lane == 0) {
+      const int s = msl[w], last = cnt[w] - 1;
+      if (s != last) set(w, s, bk[w * capb + last], bi[w * capb + last]);
+      cnt[w] = last;
+      pubcnt[w] = last;
+      pos[top] = -1;
+      --size;
+    }
+    __syncwarp();
+    // rescan bucket w
+    const int n = cnt[w];
+    double kb = kInf;
+    int ib = 0x7fffffff, sb = 0;
+    for (int s = lane; s < n; s += 32) {
+      const double k = bk[w * capb + s];
+      const int id = bi[w * capb + s];
+      if (less(k, id, kb, ib)) {
+        kb = k;
+        ib = id;
+        sb = s;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ko = __shfl_xor_sync(kFull, kb, o);
+      const int io = __shfl_xor_sync(kFull, ib, o);
+      const int so = __shfl_xor_sync(kFull, sb, o);
+      if (less(ko, io, kb, ib)) {
+        kb = ko;
+        ib = io;
+        sb = so;
+      }
+    }
+    if (lane == 0) {
+      mk[w] = kb;
+      mi[w] = ib;
+      msl[w] = sb;
+    }
+    __syncwarp();
     return top;
   }
 };
@@ -550,7 +596,7 @@ __device__ void publish(const HcArgs& a, int cell, int kind, u64 st, unsigned dm
 }
 
 // ---- the committer: the reference's heap loop in exact order ----------------
-__device__ void committer(const HcArgs& a, Heap& H, HTile& T, double* before, int lane) {
+__device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before, int lane) {
   const CellGeom& g = a.g;
   if (lane == 0) {
     for (int k = 0; k < a.n_init; ++k) {  // heap_cell.cpp:255-268
@@ -562,6 +608,7 @@ __device__ void committer(const HcArgs& a, Heap& H, HTile& T, double* before, in
     }
     *a.hsize_pub = H.size;
   }
+  __syncwarp();
   long long removals = 0, sweeps = 0, updates = 0, mon_checks = 0, mon_single = 0;
   long long self_processed = 0, fast_hits = 0, waits = 0, chain_hits = 0;
   long long cyc_pop = 0, cyc_obtain = 0, cyc_self = 0, cyc_commit = 0;
@@ -572,14 +619,13 @@ __device__ void committer(const HcArgs& a, Heap& H, HTile& T, double* before, in
   const unsigned* spec_p = a.spec_ver;
   const unsigned* spec_c = a.spec_ver + a.J;
   for (;;) {
-    int cell = -1;
     long long t0 = clock64();
-    if (lane == 0 && H.size > 0 && !H.overflow) {
-      cell = H.pop();
+    const bool over = __shfl_sync(kFull, H.overflow ? 1 : 0, 0) != 0;
+    const int cell = over ? -1 : H.pop(lane);
+    if (lane == 0 && cell >= 0) {
       *a.hsize_pub = H.size;
       a.ckey[cell] = kInf;
     }
-    cell = __shfl_sync(kFull, cell, 0);
     long long t1 = clock64();
     cyc_pop += t1 - t0;
     if (cell < 0) break;
@@ -1029,23 +1075,37 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
   // loads and acquire once per speculation.
   if (blockIdx.x == 0) {
     if (wib != 0) return;
-    Heap H;
-    if (a.heap_cap > 0) {  // [tile][keys: cap doubles][ids: cap ints]
-      H.hk = smem + a.tile_doubles;
-      H.hid = reinterpret_cast<int*>(H.hk + a.heap_cap);
+    BucketPQ H;
+    // [tile][keys: 32 capb doubles][ids: 32 capb ints] in smem when heap_cap
+    // > 0, else in global memory; [minima: 32 doubles][ids][slots][counts]
+    double* qbase = smem + a.tile_doubles;
+    if (a.heap_cap > 0) {
+      H.capb = a.heap_cap;
+      H.bk = qbase;
+      H.bi = reinterpret_cast<int*>(H.bk + 32 * H.capb);
       H.pub = a.harr;
-      H.cap = a.heap_cap;
-    } else {  // global entries; the id array is the published array itself
-      H.hk = a.hkey;
-      H.hid = a.harr;
+      qbase = reinterpret_cast<double*>(H.bi + 32 * H.capb);
+    } else {
+      H.capb = a.heap_capb_global;
+      H.bk = a.hkey;
+      H.bi = a.harr;
       H.pub = nullptr;
-      H.cap = a.J;
     }
+    H.mk = qbase;
+    H.mi = reinterpret_cast<int*>(H.mk + 32);
+    H.msl = H.mi + 32;
+    H.cnt = H.msl + 32;
+    H.mk[lane] = kInf;
+    H.mi[lane] = 0x7fffffff;
+    H.msl[lane] = 0;
+    H.cnt[lane] = 0;
     H.pos = a.hpos;
-    H.window = a.window;
+    H.pubcnt = a.hsize_pub + 31;  // [32] bucket counts after the total
+    H.pubcnt[lane] = 0;
     H.size = 0;
     H.overflow = false;
     for (int d = 0; d < 4; ++d) H.trk[d] = -1, H.tps[d] = -1;
+    __syncwarp();
     committer(a, H, T, before, lane);
     return;
   }
@@ -1058,16 +1118,20 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
     // lane 0 reads the shared words and broadcasts them: lanes reading them
     // independently could see different values, run different trip counts
     // and meet at mismatched warp collectives (a deadlock)
-    int done = 0, hs = 0;
-    if (lane == 0) {
-      done = ld_relaxed_s32(a.done_flag);
-      hs = ld_relaxed_s32(a.hsize_pub);
-    }
+    int done = 0;
+    if (lane == 0) done = ld_relaxed_s32(a.done_flag);
     if (__shfl_sync(kFull, done, 0)) return;
-    hs = __shfl_sync(kFull, hs, 0);
-    if (hs > a.window) hs = a.window;
+    // queued cells: bucket b's entries [b*pub_capb, b*pub_capb + count_b) of
+    // the mirror; workers spread over the buckets, then over their slots
     bool worked = false;
-    for (int pidx = wid; pidx < hs; pidx += nworkers) {
+    const bool wide = nworkers >= 32;
+    for (int bkt = wide ? (wid & 31) : wid; bkt < 32 && !worked; bkt += wide ? 32 : nworkers) {
+      int nb = 0;
+      if (lane == 0) nb = ld_relaxed_s32(a.hsize_pub + 31 + bkt);
+      nb = __shfl_sync(kFull, nb, 0);
+      const int sstep = wide ? (nworkers >> 5) : 1;
+    for (int sl = wide ? (wid >> 5) : 0; sl < nb; sl += sstep) {
+      const int pidx = bkt * a.pub_capb + sl;
       Job j;
       int got = 0;
       if (lane == 0) got = pick_job(a, pidx, j, wid) ? 1 : 0;
@@ -1097,6 +1161,7 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
       if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 3;
       worked = true;
       break;
+    }
     }
     if (!worked) __nanosleep(a.idle_ns);
   }
@@ -1128,9 +1193,7 @@ __global__ void heapcell_init_kernel(HcArgs a) {
       a.ckey[cell] = kInf;
       a.ctag[cell] = kSpecNone;
       a.cval[cell] = kInf;
-      a.hkey[cell] = kInf;
       a.hpos[cell] = -1;
-      a.harr[cell] = -1;
     }
   }
 }
@@ -1156,7 +1219,10 @@ size_t heapcell_smem_bytes(const CellGeom& g, int max_len) {
          (((size_t)g.max_w * g.max_h + 7) & ~(size_t)7);
 }
 
-size_t heapcell_committer_heap_bytes(int cap) { return (size_t)cap * (sizeof(double) + 4); }
+size_t heapcell_committer_heap_bytes(int capb) {
+  // 32 buckets of capb (key, id) entries + per-bucket minimum, id, slot, count
+  return (size_t)32 * capb * (sizeof(double) + 4) + 32 * (sizeof(double) + 12);
+}
 
 cudaError_t launch_heapcell(const HcArgs& args, int warps_per_cta, int max_ctas, cudaStream_t s,
                             int* launches) {
@@ -1164,9 +1230,8 @@ cudaError_t launch_heapcell(const HcArgs& args, int warps_per_cta, int max_ctas,
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   heapcell_init_kernel<<<blocks, 256, 0, s>>>(args);
   size_t smem = (size_t)warps_per_cta * args.tile_doubles * sizeof(double);
-  if (args.heap_cap > 0)
-    smem = std::max(smem, args.tile_doubles * sizeof(double) +
-                              heapcell_committer_heap_bytes(args.heap_cap));
+  smem = std::max(smem, args.tile_doubles * sizeof(double) +
+                           heapcell_committer_heap_bytes(args.heap_cap > 0 ? args.heap_cap : 0));
   cudaError_t e = cudaFuncSetAttribute(heapcell_spec_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -209,7 +209,7 @@ def test_heapcell_all_exit_and_first_removal():
     assert float(np.max(np.abs(out.values - exact) / np.maximum(exact, 1e-300))) < 1e-12
 
 
-@pytest.mark.parametrize("env", [{"EIK_HC_HEAP_CAP": "64"}, {"EIK_HC_GLOBAL_HEAP": "1"},
+@pytest.mark.parametrize("env", [{"EIK_HC_HEAP_CAP": "2"}, {"EIK_HC_GLOBAL_HEAP": "1"},
                                  {"EIK_HC_CHAIN": "0"}, {"EIK_HC_CHAIN": "2"},
                                  {"EIK_HC_CTAS": "1"}],
                          ids=["heap-overflow-fallback", "global-heap", "no-chain", "chain-all",
