@@ -86,6 +86,8 @@ double eik_field_eval(const eik_field* f, double x, double y) {
 int eik_field_eval_points(const eik_field* f, const double* xy, int64_t count,
                           double* out) {
   if (!f || (!xy && count) || (!out && count) || count < 0) return EIK_ERR_DOMAIN;
+  /* independent points: any thread count gives the same bits */
+#pragma omp parallel for schedule(static) if (count > 65536)
   for (int64_t k = 0; k < count; ++k) out[k] = eik_field_eval(f, xy[2 * k], xy[2 * k + 1]);
   return EIK_OK;
 }
@@ -183,6 +185,7 @@ int64_t eik_cell_probe_points(const eik_grid* g, int32_t cells_x,
   const double hc = vertical ? (double)(m / cells_x) * g->h : (double)(n / cells_y) * g->h;
   const double step = 0.5 * (g->h + hc); /* heap_cell.cpp:199 */
   const double xmax = gx(g, m - 1), ymax = gy(g, n - 1);
+#pragma omp parallel for schedule(static) if ((int64_t)ncell * len > 65536)
   for (int32_t c = 0; c < ncell; ++c) {
     for (int64_t t = 0; t < len; ++t) {
       int64_t i, j;

@@ -174,6 +174,13 @@ class Plan:
     def values_ptr(self) -> int:
         return N.lib.eik_plan_values(self._h)
 
+    def sweep(self, first_sweep: int, count: int = 1):
+        """FSM/FMM plans: exactly `count` more sweeps on the current values
+        (eik_plan_sweep); per-sweep "changed" flags."""
+        ch = (C.c_int32 * count)()
+        N.raise_for(N.lib.eik_plan_sweep(self._h, first_sweep, count, ch))
+        return [bool(x) for x in ch]
+
     def close(self):
         if getattr(self, "_h", None):
             N.lib.eik_plan_destroy(self._h)

@@ -11,6 +11,8 @@ built):  python tests/golden/make_golden.py [--big]
   big.json      BASELINE configs: sha256 of the reference's u bytes and its
                 counters (C1 257^2, C2 2049^2 all methods/cell sizes, and the
                 acceptance sweep counts of acceptance.cpp:133-146).
+  c34.json      (--c34) configs 3 and 4 at 4097^2.
+  c5.json       (--c5) config 5's field family at 2049^2.
 """
 from __future__ import annotations
 
@@ -168,15 +170,40 @@ def c34():
         json.dump(out, f, indent=1, sort_keys=True)
 
 
+def c5():
+    """BASELINE config 5's field family (16 random-phase sinusoids, 64 random
+    node sources) at 2049^2, where the reference runs here: sha256 + counters
+    of FSM and FHCM at 16/32-node cells (c5.json)."""
+    out = {}
+    p = configs.config5(2049).problem
+    t = time.time()
+    r = O.ref_solve(p, "fsm")
+    out["c5_2049/fsm"] = dict(sha256=sha(r.u), ms=r.elapsed_ms, **counters(r))
+    print("fsm", round(time.time() - t, 1), flush=True)
+    for cs in (16, 32):
+        cx = p.grid.m // cs
+        for method in ("fhcm", "hcm", "fmsm"):
+            r = O.ref_solve(p, method, cx, cx)
+            out[f"c5_2049/{method}/{cs}"] = dict(sha256=sha(r.u), cells=cx, ms=r.elapsed_ms,
+                                                 **counters(r))
+            print(method, cs, round(r.elapsed_ms), flush=True)
+    with open(os.path.join(HERE, "c5.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--c34", action="store_true")
+    ap.add_argument("--c5", action="store_true")
     a = ap.parse_args()
     if not O.have_ref():
         sys.exit("oracle/_ref/libeikref.so missing: run make -C oracle here")
     if a.c34:
         c34()
+        sys.exit(0)
+    if a.c5:
+        c5()
         sys.exit(0)
     with open(os.path.join(HERE, "kat.json"), "w") as f:
         json.dump(kat(), f, indent=1)
