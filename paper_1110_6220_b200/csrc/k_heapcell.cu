@@ -51,12 +51,15 @@ using u64 = unsigned long long;
 // low 32 bits: 0-3 raised sweep flags, 4 first removal done, 5-6 committed
 //   slot, 8-31 version (commits in {c} u N(c), mod 2^24)
 // high 32 bits: 0-1 slot of the plain speculation (the chained one uses the
-//   third)
+//   third), 2-9 the committed slot of the neighbour on side d at bits 2+2d
+//   (kept current by the committer, which rewrites this word whenever that
+//   neighbour commits; the halo is then located without reading its state)
 __device__ __forceinline__ unsigned st_flags(u64 s) { return (unsigned)s & 15u; }
 __device__ __forceinline__ bool st_first_done(u64 s) { return (s >> 4) & 1u; }
 __device__ __forceinline__ int st_cur(u64 s) { return (int)((s >> 5) & 3u); }
 __device__ __forceinline__ unsigned st_ver(u64 s) { return (unsigned)s >> 8; }
 __device__ __forceinline__ int st_pslot(u64 s) { return (int)((s >> 32) & 3u); }
+__device__ __forceinline__ int st_nbcur(u64 s, int d) { return (int)((s >> (34 + 2 * d)) & 3u); }
 __device__ __forceinline__ int kind_slot(u64 s, int kind) {
   return kind == 0 ? st_pslot(s) : 3 - st_cur(s) - st_pslot(s);
 }
@@ -430,10 +433,6 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
   // with the cost halo as 8-byte async copies (read-only data), and -- once
   // the neighbours' state words locate their committed slots -- the value
   // halo and the probe strips through registers.
-  u64 nstw[4];
-#pragma unroll
-  for (int d = 0; d < 4; ++d)
-    nstw[d] = (has_nb[d] && !((omask >> d) & 1u)) ? ld_relaxed_u64_nb(a.state + nbs[d]) : 0ull;
   const double* own = slot_ptr(a, st_cur(st), cell);
   double* pstrip = before + 4 * a.max_len;
   {
@@ -466,7 +465,7 @@ __device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell
     int ncur[4];
 #pragma unroll
     for (int d = 0; d < 4; ++d)
-      ncur[d] = !has_nb[d] ? 0 : (omask >> d) & 1u ? oslot[d] : st_cur(nstw[d]);
+      ncur[d] = !has_nb[d] ? 0 : (omask >> d) & 1u ? oslot[d] : st_nbcur(st, d);
     const double* sw = slot_ptr(a, ncur[0], nbs[0]) + (int)(g.base_x - 1);
     const double* se = slot_ptr(a, ncur[1], nbs[1]);
     const double* ss = slot_ptr(a, ncur[2], nbs[2]) + (int)(g.base_y - 1) * mw;
@@ -793,13 +792,15 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       updates += rupdates;
       // popped cell: flags cleared, first removal done, the committed kind's
       // slot becomes current and the old current slot takes its role, +1
-      // version, last commit = itself
+      // version; its neighbours learn its new slot
+      int ncur_pop = 0;
       {
         const int cur = st_cur(st), ps = st_pslot(st), qs = 3 - cur - ps;
         const int ncur = kind ? qs : ps, nps = kind ? ps : cur;
         const unsigned lo = (((unsigned)st & ~(15u | (3u << 5))) | 16u | ((unsigned)ncur << 5)) +
                             kVerOne;
-        st_relaxed_u64(a.state + cell, (u64)lo | ((u64)nps << 32));
+        st_relaxed_u64(a.state + cell, (u64)lo | (st & (0xFFull << 34)) | ((u64)nps << 32));
+        ncur_pop = ncur;
         a.ctag[cell] = inst;
       }
       for (int side = 0; side < 4; ++side) {  // heap_cell.cpp:288-311
@@ -827,7 +828,10 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
           }
         }
         if (moved) a.ckey[nb] = cv[side];
-        st_relaxed_u64(a.state + nb, (u64)lo | (nst[side] & (3ull << 32)));
+        // the popped cell sits on side (side ^ 1) of its neighbour
+        const int sh = 34 + 2 * (side ^ 1);
+        st_relaxed_u64(a.state + nb, (u64)lo | (nst[side] & ~((3ull << sh) | 0xFFFFFFFFull)) |
+                                         ((u64)ncur_pop << sh));
       }
       *a.hsize_pub = H.size;
       for (int d = 0; d < 4; ++d) H.trk[d] = -1;
