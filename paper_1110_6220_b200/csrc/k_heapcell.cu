@@ -184,8 +184,10 @@ struct BucketPQ {
       msl[l] = s;
     }
   }
-  // all lanes; returns the popped id (or -1 when empty) on every lane
-  __device__ int pop(int lane) {
+  // all lanes; removes the minimum and returns it (or -1 when empty) on
+  // every lane, with its bucket in w.  The bucket's cached minimum is stale
+  // until rescan(w): the committer overlaps that with its next loads.
+  __device__ int pop_min(int lane, int& w_out) {
     double kl = mk[lane];
     int il = mi[lane], wl = lane;
 #pragma unroll
@@ -201,6 +203,7 @@ struct BucketPQ {
     }
     if (!(kl < kInf) && il == 0x7fffffff) return -1;  // every bucket empty
     const int w = wl, top = il;
+    w_out = w;
     if (lane == 0) {
       const int s = msl[w], last = cnt[w] - 1;
       if (s != last) set(w, s, bk[w * capb + last], bi[w * capb + last]);
@@ -210,7 +213,10 @@ struct BucketPQ {
       --size;
     }
     __syncwarp();
-    // rescan bucket w
+    return top;
+  }
+  // all lanes: recompute bucket w's cached minimum
+  __device__ void rescan(int lane, int w) {
     const int n = cnt[w];
     double kb = kInf;
     int ib = 0x7fffffff, sb = 0;
@@ -240,7 +246,6 @@ struct BucketPQ {
       msl[w] = sb;
     }
     __syncwarp();
-    return top;
   }
 };
 
@@ -620,7 +625,8 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
   for (;;) {
     long long t0 = clock64();
     const bool over = __shfl_sync(kFull, H.overflow ? 1 : 0, 0) != 0;
-    const int cell = over ? -1 : H.pop(lane);
+    int wpop = 0;
+    const int cell = over ? -1 : H.pop_min(lane, wpop);
     if (lane == 0 && cell >= 0) {
       *a.hsize_pub = H.size;
       a.ckey[cell] = kInf;
@@ -648,6 +654,8 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     // warp writes these words) go out with the first poll
     u64 nst[4];
     double cv[4];
+    unsigned ctn[4];  // only this warp writes ctag
+    unsigned svp0 = 0, svc0 = 0;
     if (lane == 0) {
 #pragma unroll
       for (int d = 0; d < 4; ++d) {
@@ -655,17 +663,22 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
         cv[d] = nbs[d] >= 0 ? __ldcg(a.cval + nbs[d]) : kInf;
         H.trk[d] = nbs[d];
         H.tps[d] = nbs[d] >= 0 ? __ldcg(a.hpos + nbs[d]) : -1;
+        ctn[d] = nbs[d] >= 0 ? __ldcg(a.ctag + nbs[d]) : kSpecNone;
       }
-      st = ld_relaxed_u64(a.state + cell);
+      st = ld_relaxed_u64_nb(a.state + cell);
+      svp0 = ld_relaxed_u32_nb(spec_p + cell);
+      svc0 = ld_relaxed_u32_nb(spec_c + cell);
+    }
+    H.rescan(lane, wpop);  // while those loads are in flight
+    if (lane == 0) {
       const unsigned v = st_ver(st);
-      unsigned ctn[4];  // only this warp writes ctag
-#pragma unroll
-      for (int d = 0; d < 4; ++d) ctn[d] = nbs[d] >= 0 ? __ldcg(a.ctag + nbs[d]) : kSpecNone;
       long long spins = 0;
       bool waited = false;
+      bool first = true;
       for (;;) {
-        const unsigned svp = ld_relaxed_u32_nb(spec_p + cell);
-        const unsigned svc = ld_relaxed_u32_nb(spec_c + cell);
+        const unsigned svp = first ? svp0 : ld_relaxed_u32_nb(spec_p + cell);
+        const unsigned svc = first ? svc0 : ld_relaxed_u32_nb(spec_c + cell);
+        first = false;
         if (tag_is(svp, v)) {
           unsigned d;
           asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(svp));
