@@ -93,7 +93,15 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     }
     if ((rc = dalloc(&P->dState, J))) return rc;
     P->allocs.push_back(P->dState);
-    const int64_t capb_g = (J + 31) / 32;  // a bucket holds every id = b mod 32
+    // committer queue bucket of cell (x, y): (x + 2y) mod 32 (k_heapcell.cu);
+    // the global layout holds every cell of the fullest bucket
+    int64_t capb_g = 1;
+    {
+      std::vector<int64_t> per(32, 0);
+      for (int64_t y = 0; y < c->cells_y; ++y)
+        for (int64_t x = 0; x < c->cells_x; ++x) ++per[(x + 2 * y) & 31];
+      for (int64_t v : per) capb_g = std::max(capb_g, v);
+    }
     P->hc_capb_global = (int)capb_g;
     if ((rc = dalloc(&P->dHKey, 32 * capb_g))) return rc;
     P->allocs.push_back(P->dHKey);
@@ -363,6 +371,8 @@ retry:  // after a committer heap overflow, with the heap in global memory
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaMemcpyAsync(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaStreamSynchronize(P->stream));
+  if (st[0] == 6 && P->hc_heap_cap == 0)
+    return fail(EIK_ERR_CUDA, "heap-cell queue bucket overflow in global memory (sizing bug)");
   if (st[0] == 6 && P->hc_heap_cap > 0) {
     P->hc_heap_cap = 0;
     CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
@@ -386,9 +396,9 @@ retry:  // after a committer heap overflow, with the heap in global memory
     std::fprintf(stderr,
                  "heapcell committer cycles: pop %llu obtain %llu self %llu commit %llu | self: "
                  "stage %llu sweeps %llu scans %llu | hits %llu (chained %llu) self %llu | "
-                 "heap max %llu cap %d | stage: %llu reset_locks %llu steps %llu\n",
+                 "heap max %llu cap %d | stage: %llu reset_locks %llu steps %llu | commit: record %llu\n",
                  cnt[8], cnt[9], cnt[10], cnt[11], cnt[12], cnt[13], cnt[14], cnt[6], cnt[15],
-                 cnt[5], cnt[38], P->hc_heap_cap, cnt[39], cnt[40], cnt[41]);
+                 cnt[5], cnt[38], P->hc_heap_cap, cnt[39], cnt[40], cnt[41], cnt[42]);
   if (std::getenv("EIK_HC_PROFILE"))
     std::fprintf(stderr,
                  "heapcell misses: unchained %llu pending %llu stale %llu wrong-inst %llu "

@@ -121,8 +121,10 @@ __device__ __forceinline__ bool tag_is(unsigned sv, unsigned v) {
 // The reference pops the minimum (value, id) of an indexed binary heap
 // (indexed_min_heap.hpp:11-106, ties to the smaller id); the pop order depends
 // only on the keys, not on the heap's shape, so any exact min-structure
-// replays it.  Here: 32 buckets (cell id mod 32) of unordered entries with
-// each bucket's minimum cached.  pop = one warp argmin over the 32 cached
+// replays it.  Here: 32 buckets of unordered entries with each bucket's
+// minimum cached; cell (x, y) goes to bucket (x + 2y) mod 32, so the W/E/S/N
+// neighbours of any cell sit in four distinct buckets (b-1, b+1, b-2, b+2)
+// and a commit updates them from four lanes at once.  pop = one warp argmin over the 32 cached
 // minima + a warp rescan of the winning bucket; insert and decrease-key are
 // O(1).  Entries live in the committer's shared memory (or global memory
 // when a bucket could overflow it); every cell's position is mirrored to
@@ -137,6 +139,7 @@ struct BucketPQ {
   int* mi;        //      their ids (INT_MAX when empty)
   int* msl;       //      their slots
   int capb;
+  int cells_x;
   int* pos;       // global [J]: bucket << 24 | slot, -1 = not queued
   int* pub;       // global [32][capb] id mirror (null: bi is global already)
   int* pubcnt;    // global [32] count mirror
@@ -158,12 +161,14 @@ struct BucketPQ {
     if (pub) pub[l * capb + s] = id;
     track(id, (l << 24) | s);
   }
-  __device__ void insert(int id, double k) {  // lane 0
-    const int l = id & 31, s = cnt[l];
-    if (s >= capb) {
-      overflow = true;
-      return;
-    }
+  __device__ int bucket_of(int id) const {
+    const int y = id / cells_x;
+    return (id - y * cells_x + 2 * y) & 31;
+  }
+  // one lane per bucket at a time; false when the bucket is full
+  __device__ bool insert(int id, double k) {
+    const int l = bucket_of(id), s = cnt[l];
+    if (s >= capb) return false;
     set(l, s, k, id);
     cnt[l] = s + 1;
     pubcnt[l] = s + 1;
@@ -172,9 +177,9 @@ struct BucketPQ {
       mi[l] = id;
       msl[l] = s;
     }
-    ++size;
+    return true;
   }
-  __device__ void decrease(int enc, double k) {  // lane 0; keys only decrease
+  __device__ void decrease(int enc, double k) {  // one lane per bucket; keys only decrease
     const int l = enc >> 24, s = enc & 0xFFFFFF;
     const int id = bi[l * capb + s];
     bk[l * capb + s] = k;
@@ -606,7 +611,8 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     for (int k = 0; k < a.n_init; ++k) {  // heap_cell.cpp:255-268
       const int cell = a.init_cells[k];
       a.cval[cell] = a.init_values[k];
-      H.insert(cell, a.init_values[k]);
+      if (H.insert(cell, a.init_values[k])) ++H.size;
+      else H.overflow = true;
       a.ckey[cell] = a.init_values[k];
       if (a.fast) st_relaxed_u64(a.state + cell, (1ull << 32) | 0xFull);  // Q-cells: all flags
     }
@@ -615,7 +621,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
   __syncwarp();
   long long removals = 0, sweeps = 0, updates = 0, mon_checks = 0, mon_single = 0;
   long long self_processed = 0, fast_hits = 0, waits = 0, chain_hits = 0;
-  long long cyc_pop = 0, cyc_obtain = 0, cyc_self = 0, cyc_commit = 0;
+  long long cyc_pop = 0, cyc_obtain = 0, cyc_self = 0, cyc_commit = 0, cyc_rec = 0;
   long long prof[6] = {0, 0, 0, 0, 0, 0};
   long long miss_cls[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int max_size = H.size;
@@ -652,24 +658,29 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     u64 st = 0;
     // the commit's loads that do not depend on the speculation (only this
     // warp writes these words) go out with the first poll
-    u64 nst[4];
-    double cv[4];
-    unsigned ctn[4];  // only this warp writes ctag
+    // lanes 0-3 load side `lane`: the neighbour's state, cell value, queue
+    // position and committed instance (only this warp writes those words)
+    u64 my_nst = 0ull;
+    double my_cv = kInf;
+    int my_pos = -1;
+    unsigned my_ctag = kSpecNone;
     unsigned svp0 = 0, svc0 = 0;
+    if (lane < 4 && nbs[lane < 4 ? lane : 0] >= 0) {
+      const int nb = nbs[lane];
+      my_nst = ld_relaxed_u64_nb(a.state + nb);
+      my_cv = __ldcg(a.cval + nb);
+      my_pos = __ldcg(a.hpos + nb);
+      my_ctag = __ldcg(a.ctag + nb);
+    }
     if (lane == 0) {
-#pragma unroll
-      for (int d = 0; d < 4; ++d) {
-        nst[d] = nbs[d] >= 0 ? ld_relaxed_u64_nb(a.state + nbs[d]) : 0ull;
-        cv[d] = nbs[d] >= 0 ? __ldcg(a.cval + nbs[d]) : kInf;
-        H.trk[d] = nbs[d];
-        H.tps[d] = nbs[d] >= 0 ? __ldcg(a.hpos + nbs[d]) : -1;
-        ctn[d] = nbs[d] >= 0 ? __ldcg(a.ctag + nbs[d]) : kSpecNone;
-      }
       st = ld_relaxed_u64_nb(a.state + cell);
       svp0 = ld_relaxed_u32_nb(spec_p + cell);
       svc0 = ld_relaxed_u32_nb(spec_c + cell);
     }
     H.rescan(lane, wpop);  // while those loads are in flight
+    unsigned ctn[4];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) ctn[d] = __shfl_sync(kFull, my_ctag, d);
     if (lane == 0) {
       const unsigned v = st_ver(st);
       long long spins = 0;
@@ -769,6 +780,8 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     }
     mode = __shfl_sync(kFull, mode, 0);
     st = __shfl_sync(kFull, st, 0);
+    kind = __shfl_sync(kFull, kind, 0);
+    dep = __shfl_sync(kFull, dep, 0);
     long long t2 = clock64();
     cyc_obtain += t2 - t1;
     if (mode == 2) break;
@@ -782,77 +795,87 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     }
     long long t3 = clock64();
     cyc_self += t3 - t2;
-    // commit (lane 0): slot flip, flags, first removal, scans, versions
-    if (lane == 0) {
-      // every load of the commit is issued before the first heap operation
-      // (one L2 round trip instead of one per side)
+    // commit: the popped cell on lane 0, its four neighbours on lanes 0-3 at
+    // once (their queue buckets differ); every load before the first update
+    {
       const SpecRec* rec = rec_ptr(a, kind, cell + dep);
-      double cand[4];
-      unsigned word[4];  // add | fl | monc | mons, one byte each
-#pragma unroll
-      for (int d = 0; d < 4; ++d) cand[d] = __ldcg(&rec->cand[d]);
-      const int rsweeps = __ldcg(&rec->sweeps), rupdates = __ldcg(&rec->updates);
-      const unsigned add4 = __ldcg(reinterpret_cast<const unsigned*>(rec->add));
-      const unsigned fl4 = __ldcg(reinterpret_cast<const unsigned*>(rec->fl));
-      const unsigned mc4 = __ldcg(reinterpret_cast<const unsigned*>(rec->monc));
-      const unsigned ms4 = __ldcg(reinterpret_cast<const unsigned*>(rec->mons));
-      const unsigned inst = __ldcg(&rec->inst);
-#pragma unroll
-      for (int d = 0; d < 4; ++d)
-        word[d] = ((add4 >> (8 * d)) & 0xFFu) | (((fl4 >> (8 * d)) & 0xFFu) << 8) |
-                  (((mc4 >> (8 * d)) & 0xFFu) << 16) | (((ms4 >> (8 * d)) & 0xFFu) << 24);
-      sweeps += rsweeps;
-      updates += rupdates;
-      // popped cell: flags cleared, first removal done, the committed kind's
-      // slot becomes current and the old current slot takes its role, +1
-      // version; its neighbours learn its new slot
-      int ncur_pop = 0;
-      {
-        const int cur = st_cur(st), ps = st_pslot(st), qs = 3 - cur - ps;
-        const int ncur = kind ? qs : ps, nps = kind ? ps : cur;
-        const unsigned lo = (((unsigned)st & ~(15u | (3u << 5))) | 16u | ((unsigned)ncur << 5)) +
-                            kVerOne;
-        st_relaxed_u64(a.state + cell, (u64)lo | (st & (0xFFull << 34)) | ((u64)nps << 32));
-        ncur_pop = ncur;
-        a.ctag[cell] = inst;
-      }
-      for (int side = 0; side < 4; ++side) {  // heap_cell.cpp:288-311
-        const int nb = nbs[side];
-        if (nb < 0) continue;
-        bool moved = false;
-        if (cand[side] < cv[side]) {
-          cv[side] = cand[side];
-          a.cval[nb] = cand[side];
-          if (H.tps[side] >= 0) {
-            H.decrease(H.tps[side], cand[side]);
-            moved = true;
-          }
+      const int cur = st_cur(st), ps = st_pslot(st), qs = 3 - cur - ps;
+      const int ncur = kind ? qs : ps, nps = kind ? ps : cur;
+      int ins = 0;
+      bool ovf = false;
+      if (lane < 4) {
+        const int d = lane, nb = nbs[d];
+        const double cand = __ldcg(&rec->cand[d]);
+        const unsigned add = __ldcg(&rec->add[d]), fl = __ldcg(&rec->fl[d]);
+        const unsigned mc = __ldcg(&rec->monc[d]), ms = __ldcg(&rec->mons[d]);
+        int rsweeps = 0, rupdates = 0;
+        unsigned inst = 0;
+        if (d == 0) {
+          rsweeps = __ldcg(&rec->sweeps);
+          rupdates = __ldcg(&rec->updates);
+          inst = __ldcg(&rec->inst);
         }
-        unsigned lo = (unsigned)nst[side] + kVerOne;
-        if (word[side] & 0xFFu) {
-          lo |= (word[side] >> 8) & 0xFFu;
-          if ((word[side] >> 16) & 0xFFu) {
-            ++mon_checks;
-            if (word[side] >> 24) ++mon_single;
-          }
-          if (H.tps[side] < 0) {
-            H.insert(nb, cv[side]);
-            moved = true;
-          }
+        if (d == 0) {
+          sweeps += rsweeps;
+          updates += rupdates;
+          cyc_rec += clock64() - t3;  // the record has arrived
+          // popped cell: flags cleared, first removal done, the committed
+          // kind's slot becomes current and the old current slot takes its
+          // role, +1 version
+          const unsigned lo =
+              (((unsigned)st & ~(15u | (3u << 5))) | 16u | ((unsigned)ncur << 5)) + kVerOne;
+          st_relaxed_u64(a.state + cell, (u64)lo | (st & (0xFFull << 34)) | ((u64)nps << 32));
+          a.ctag[cell] = inst;
         }
-        if (moved) a.ckey[nb] = cv[side];
-        // the popped cell sits on side (side ^ 1) of its neighbour
-        const int sh = 34 + 2 * (side ^ 1);
-        st_relaxed_u64(a.state + nb, (u64)lo | (nst[side] & ~((3ull << sh) | 0xFFFFFFFFull)) |
-                                         ((u64)ncur_pop << sh));
+        if (nb >= 0) {  // heap_cell.cpp:288-311
+          bool moved = false;
+          double cvd = my_cv;
+          if (cand < cvd) {
+            cvd = cand;
+            a.cval[nb] = cand;
+            if (my_pos >= 0) {
+              H.decrease(my_pos, cand);
+              moved = true;
+            }
+          }
+          unsigned lo = (unsigned)my_nst + kVerOne;
+          if (add) {
+            lo |= fl;
+            if (mc) {
+              ++mon_checks;
+              if (ms) ++mon_single;
+            }
+            if (my_pos < 0) {
+              if (H.insert(nb, cvd)) ++ins;
+              else ovf = true;
+              moved = true;
+            }
+          }
+          if (moved) a.ckey[nb] = cvd;
+          // the popped cell sits on side (d ^ 1) of its neighbour, which
+          // learns its new slot
+          const int sh = 34 + 2 * (d ^ 1);
+          st_relaxed_u64(a.state + nb, (u64)lo | (my_nst & ~((3ull << sh) | 0xFFFFFFFFull)) |
+                                           ((u64)ncur << sh));
+        }
       }
-      *a.hsize_pub = H.size;
-      for (int d = 0; d < 4; ++d) H.trk[d] = -1;
-      if (H.size > max_size) max_size = H.size;
+      ins += __shfl_xor_sync(kFull, ins, 1);
+      ins += __shfl_xor_sync(kFull, ins, 2);
+      const bool any_ovf = __any_sync(kFull, ovf);
+      if (lane == 0) {
+        H.size += ins;
+        if (any_ovf) H.overflow = true;
+        *a.hsize_pub = H.size;
+        if (H.size > max_size) max_size = H.size;
+      }
     }
     __syncwarp();
     cyc_commit += clock64() - t3;
     prev_cell = cell;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mon_checks += __shfl_xor_sync(kFull, mon_checks, o);
+    mon_single += __shfl_xor_sync(kFull, mon_single, o);
   }
   if (lane == 0) {
     a.counters[0] = removals;
@@ -873,6 +896,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     a.counters[39] = prof[3];
     a.counters[40] = prof[4];
     a.counters[41] = prof[5];
+    a.counters[42] = cyc_rec;
     a.counters[15] = chain_hits;
     for (int k = 0; k < 8; ++k) a.counters[16 + k] = miss_cls[k];
     a.counters[38] = (unsigned long long)max_size;
@@ -1117,6 +1141,7 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
     H.msl[lane] = 0;
     H.cnt[lane] = 0;
     H.pos = a.hpos;
+    H.cells_x = a.g.cells_x;
     H.pubcnt = a.hsize_pub + 31;  // [32] bucket counts after the total
     H.pubcnt[lane] = 0;
     H.size = 0;
