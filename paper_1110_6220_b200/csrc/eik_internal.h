@@ -89,7 +89,7 @@ struct HcArgs {
   int* wdbg;                // optional debug: [workers][4] phase, cell, kind, time
   int* owner;               // optional debug: [2][J] last claiming worker
   int* done_flag;
-  int* hsize_pub;           // [0] queue size, [31..62] per-bucket counts (workers)
+  int* hsize_pub;           // per-bucket queue counts for the workers, bucket b at [32 b]
   int64_t tile_doubles;     // per-warp smem
   int heap_cap;             // >0: committer queue buckets in shared memory, capacity
                             // per bucket; 0: buckets in global memory (hkey + harr)

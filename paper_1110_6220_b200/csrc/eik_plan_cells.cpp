@@ -130,7 +130,9 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     P->allocs.push_back(P->dBusy);
     if ((rc = dalloc(&P->dRec, 2 * J))) return rc;
     P->allocs.push_back(P->dRec);
-    if ((rc = dalloc(&P->dHcMisc, 64))) return rc;
+    // [0] done flag (its own line), then the 32 published bucket counts, one
+    // 128-byte line each (all workers poll them)
+    if ((rc = dalloc(&P->dHcMisc, 32 + 32 * 32))) return rc;
     P->allocs.push_back(P->dHcMisc);
     // per-warp tile: values + costs with halo, 4 border snapshots, lock bytes
     const size_t tile = ((smem + sizeof(double) - 1) / sizeof(double) + 1) & ~(size_t)1;
@@ -359,11 +361,11 @@ retry:  // after a committer heap overflow, with the heap in global memory
   a.idle_ns = 200;
   if (const char* c = std::getenv("EIK_HC_IDLE_NS")) a.idle_ns = std::atoi(c);
   a.done_flag = P->dHcMisc;
-  a.hsize_pub = P->dHcMisc + 1;
+  a.hsize_pub = P->dHcMisc + 32;
   a.heap_capb_global = P->hc_capb_global;
   a.pub_capb = P->hc_heap_cap > 0 ? P->hc_heap_cap : P->hc_capb_global;
   a.tile_doubles = P->cg.tile_doubles;
-  CK(cudaMemsetAsync(P->dHcMisc, 0, sizeof(int) * 64, P->stream));
+  CK(cudaMemsetAsync(P->dHcMisc, 0, sizeof(int) * (32 + 32 * 32), P->stream));
   CK(launch_heapcell(a, P->hc_warps_per_cta, P->hc_max_ctas, P->stream, &launches));
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];
@@ -396,9 +398,11 @@ retry:  // after a committer heap overflow, with the heap in global memory
     std::fprintf(stderr,
                  "heapcell committer cycles: pop %llu obtain %llu self %llu commit %llu | self: "
                  "stage %llu sweeps %llu scans %llu | hits %llu (chained %llu) self %llu | "
-                 "heap max %llu cap %d | stage: %llu reset_locks %llu steps %llu | commit: record %llu\n",
+                 "heap max %llu cap %d | stage: %llu reset_locks %llu steps %llu | commit: record %llu | "
+                 "obtain: rescan %llu first-rt %llu\n",
                  cnt[8], cnt[9], cnt[10], cnt[11], cnt[12], cnt[13], cnt[14], cnt[6], cnt[15],
-                 cnt[5], cnt[38], P->hc_heap_cap, cnt[39], cnt[40], cnt[41], cnt[42]);
+                 cnt[5], cnt[38], P->hc_heap_cap, cnt[39], cnt[40], cnt[41], cnt[42], cnt[43],
+                 cnt[44]);
   if (std::getenv("EIK_HC_PROFILE"))
     std::fprintf(stderr,
                  "heapcell misses: unchained %llu pending %llu stale %llu wrong-inst %llu "

@@ -142,7 +142,7 @@ struct BucketPQ {
   int cells_x;
   int* pos;       // global [J]: bucket << 24 | slot, -1 = not queued
   int* pub;       // global [32][capb] id mirror (null: bi is global already)
-  int* pubcnt;    // global [32] count mirror
+  int* pubcnt;    // global count mirror, bucket l at pubcnt[32 * l] (one line each)
   int size;
   bool overflow;
   int trk[4], tps[4];  // tracked cells (the popped cell's neighbours) and positions
@@ -171,7 +171,7 @@ struct BucketPQ {
     if (s >= capb) return false;
     set(l, s, k, id);
     cnt[l] = s + 1;
-    pubcnt[l] = s + 1;
+    pubcnt[32 * l] = s + 1;
     if (less(k, id, mk[l], mi[l])) {
       mk[l] = k;
       mi[l] = id;
@@ -213,7 +213,7 @@ struct BucketPQ {
       const int s = msl[w], last = cnt[w] - 1;
       if (s != last) set(w, s, bk[w * capb + last], bi[w * capb + last]);
       cnt[w] = last;
-      pubcnt[w] = last;
+      pubcnt[32 * w] = last;
       pos[top] = -1;
       --size;
     }
@@ -616,12 +616,12 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       a.ckey[cell] = a.init_values[k];
       if (a.fast) st_relaxed_u64(a.state + cell, (1ull << 32) | 0xFull);  // Q-cells: all flags
     }
-    *a.hsize_pub = H.size;
   }
   __syncwarp();
   long long removals = 0, sweeps = 0, updates = 0, mon_checks = 0, mon_single = 0;
   long long self_processed = 0, fast_hits = 0, waits = 0, chain_hits = 0;
   long long cyc_pop = 0, cyc_obtain = 0, cyc_self = 0, cyc_commit = 0, cyc_rec = 0;
+  long long cyc_rescan = 0, cyc_rt1 = 0;
   long long prof[6] = {0, 0, 0, 0, 0, 0};
   long long miss_cls[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int max_size = H.size;
@@ -634,8 +634,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     int wpop = 0;
     const int cell = over ? -1 : H.pop_min(lane, wpop);
     if (lane == 0 && cell >= 0) {
-      *a.hsize_pub = H.size;
-      a.ckey[cell] = kInf;
+        a.ckey[cell] = kInf;
     }
     long long t1 = clock64();
     cyc_pop += t1 - t0;
@@ -678,6 +677,8 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       svc0 = ld_relaxed_u32_nb(spec_c + cell);
     }
     H.rescan(lane, wpop);  // while those loads are in flight
+    const long long t1a = clock64();
+    cyc_rescan += t1a - t1;
     unsigned ctn[4];
 #pragma unroll
     for (int d = 0; d < 4; ++d) ctn[d] = __shfl_sync(kFull, my_ctag, d);
@@ -686,6 +687,8 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       long long spins = 0;
       bool waited = false;
       bool first = true;
+      const unsigned vchk = v;  // first use of the loaded state word
+      cyc_rt1 += (vchk == 0xFFFFFFFFu ? 1 : 0) + clock64() - t1a;
       for (;;) {
         const unsigned svp = first ? svp0 : ld_relaxed_u32_nb(spec_p + cell);
         const unsigned svc = first ? svc0 : ld_relaxed_u32_nb(spec_c + cell);
@@ -865,8 +868,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       if (lane == 0) {
         H.size += ins;
         if (any_ovf) H.overflow = true;
-        *a.hsize_pub = H.size;
-        if (H.size > max_size) max_size = H.size;
+            if (H.size > max_size) max_size = H.size;
       }
     }
     __syncwarp();
@@ -897,6 +899,8 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     a.counters[40] = prof[4];
     a.counters[41] = prof[5];
     a.counters[42] = cyc_rec;
+    a.counters[43] = cyc_rescan;
+    a.counters[44] = cyc_rt1;
     a.counters[15] = chain_hits;
     for (int k = 0; k < 8; ++k) a.counters[16 + k] = miss_cls[k];
     a.counters[38] = (unsigned long long)max_size;
@@ -1142,8 +1146,8 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
     H.cnt[lane] = 0;
     H.pos = a.hpos;
     H.cells_x = a.g.cells_x;
-    H.pubcnt = a.hsize_pub + 31;  // [32] bucket counts after the total
-    H.pubcnt[lane] = 0;
+    H.pubcnt = a.hsize_pub;  // bucket counts, one 128-byte line each
+    H.pubcnt[32 * lane] = 0;
     H.size = 0;
     H.overflow = false;
     for (int d = 0; d < 4; ++d) H.trk[d] = -1, H.tps[d] = -1;
@@ -1156,12 +1160,13 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
   const int wpc = blockDim.x >> 5;
   const int wid = (blockIdx.x - 1) * wpc + wib;
   const int nworkers = (gridDim.x - 1) * wpc;
+  unsigned polls = 0;
   for (;;) {
     // lane 0 reads the shared words and broadcasts them: lanes reading them
     // independently could see different values, run different trip counts
     // and meet at mismatched warp collectives (a deadlock)
     int done = 0;
-    if (lane == 0) done = ld_relaxed_s32(a.done_flag);
+    if (lane == 0 && (++polls & 7) == 0) done = ld_relaxed_s32(a.done_flag);  // 1 poll in 8
     if (__shfl_sync(kFull, done, 0)) return;
     // queued cells: bucket b's entries [b*pub_capb, b*pub_capb + count_b) of
     // the mirror; workers spread over the buckets, then over their slots
@@ -1169,7 +1174,7 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
     const bool wide = nworkers >= 32;
     for (int bkt = wide ? (wid & 31) : wid; bkt < 32 && !worked; bkt += wide ? 32 : nworkers) {
       int nb = 0;
-      if (lane == 0) nb = ld_relaxed_s32(a.hsize_pub + 31 + bkt);
+      if (lane == 0) nb = ld_relaxed_s32(a.hsize_pub + 32 * bkt);
       nb = __shfl_sync(kFull, nb, 0);
       const int sstep = wide ? (nworkers >> 5) : 1;
     for (int sl = wide ? (wid >> 5) : 0; sl < nb; sl += sstep) {
