@@ -86,6 +86,7 @@ struct HcArgs {
   unsigned* ctag;           // [J] instance number of the last committed result
   int chain;                // make chained speculations
   int idle_ns;              // worker back-off when it found nothing to do
+  int prof;                 // run the instrumented kernel (EIK_HC_PROFILE)
   int* wdbg;                // optional debug: [workers][4] phase, cell, kind, time
   int* owner;               // optional debug: [2][J] last claiming worker
   int* done_flag;

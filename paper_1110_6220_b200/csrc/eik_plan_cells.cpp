@@ -359,6 +359,7 @@ retry:  // after a committer heap overflow, with the heap in global memory
   a.ctag = P->dCTag;
   a.chain = P->hc_chain;
   a.idle_ns = 200;
+  a.prof = std::getenv("EIK_HC_PROFILE") ? 1 : 0;
   if (const char* c = std::getenv("EIK_HC_IDLE_NS")) a.idle_ns = std::atoi(c);
   a.done_flag = P->dHcMisc;
   a.hsize_pub = P->dHcMisc + 32;

@@ -425,7 +425,7 @@ __device__ __forceinline__ SpecRec* rec_ptr(const HcArgs& a, int kind, int cell)
 // come from slot oslot[side] (the pending results a chained speculation
 // builds on, whose scans add `cflags` to the cell's flags) -- then sweep,
 // scan and write the record (all fields but the instance number and tags).
-__device__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell, int kind, u64 st,
+__device__ __forceinline__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell, int kind, u64 st,
                              unsigned omask, const int oslot[4], unsigned cflags, int lane,
                              long long* prof = nullptr) {
   const long long p0 = prof ? clock64() : 0;
@@ -605,6 +605,10 @@ __device__ void publish(const HcArgs& a, int cell, int kind, u64 st, unsigned dm
 }
 
 // ---- the committer: the reference's heap loop in exact order ----------------
+// PROF: the cycle / miss-class instrumentation (EIK_HC_PROFILE); compiled out
+// of the production instantiation, where those ~25 live counters would cost
+// registers the hot path needs.
+template <bool PROF>
 __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before, int lane) {
   const CellGeom& g = a.g;
   if (lane == 0) {
@@ -629,15 +633,15 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
   const unsigned* spec_p = a.spec_ver;
   const unsigned* spec_c = a.spec_ver + a.J;
   for (;;) {
-    long long t0 = clock64();
+    long long t0 = PROF ? clock64() : 0;
     const bool over = __shfl_sync(kFull, H.overflow ? 1 : 0, 0) != 0;
     int wpop = 0;
     const int cell = over ? -1 : H.pop_min(lane, wpop);
     if (lane == 0 && cell >= 0) {
         a.ckey[cell] = kInf;
     }
-    long long t1 = clock64();
-    cyc_pop += t1 - t0;
+    long long t1 = PROF ? clock64() : 0;
+    if (PROF) cyc_pop += t1 - t0;
     if (cell < 0) break;
     ++removals;
     if (removals > a.budget) {  // heap_cell.cpp:276-277
@@ -677,8 +681,8 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       svc0 = ld_relaxed_u32_nb(spec_c + cell);
     }
     H.rescan(lane, wpop);  // while those loads are in flight
-    const long long t1a = clock64();
-    cyc_rescan += t1a - t1;
+    const long long t1a = PROF ? clock64() : 0;
+    if (PROF) cyc_rescan += t1a - t1;
     unsigned ctn[4];
 #pragma unroll
     for (int d = 0; d < 4; ++d) ctn[d] = __shfl_sync(kFull, my_ctag, d);
@@ -688,7 +692,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       bool waited = false;
       bool first = true;
       const unsigned vchk = v;  // first use of the loaded state word
-      cyc_rt1 += (vchk == 0xFFFFFFFFu ? 1 : 0) + clock64() - t1a;
+      if (PROF) cyc_rt1 += (vchk == 0xFFFFFFFFu ? 1 : 0) + clock64() - t1a;
       for (;;) {
         const unsigned svp = first ? svp0 : ld_relaxed_u32_nb(spec_p + cell);
         const unsigned svc = first ? svc0 : ld_relaxed_u32_nb(spec_c + cell);
@@ -731,6 +735,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
             mode = 1;
             if (a.wdbg) a.owner[cell] = 0x50000;
             // classify the miss (profiling counters 16..23)
+            if (PROF) {
             const unsigned svc2 = ld_relaxed_u32(spec_c + cell);
             int cls;
             if (svc2 == kSpecNone) {
@@ -746,6 +751,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
                                    prev_cell == nbs[2] || prev_cell == nbs[3]))
               ++miss_cls[6];  // the previous pop was a neighbour
             if (((ld_relaxed_u32(spec_p + cell) & kTagMask) + 1u) == v) ++miss_cls[7];
+            }
           }
           break;
         }
@@ -785,19 +791,19 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     st = __shfl_sync(kFull, st, 0);
     kind = __shfl_sync(kFull, kind, 0);
     dep = __shfl_sync(kFull, dep, 0);
-    long long t2 = clock64();
-    cyc_obtain += t2 - t1;
+    long long t2 = PROF ? clock64() : 0;
+    if (PROF) cyc_obtain += t2 - t1;
     if (mode == 2) break;
     if (mode == 1) {
       const int none[4] = {0, 0, 0, 0};
       const unsigned noinst[4] = {0, 0, 0, 0};
-      process_cell(a, T, before, cell, 0, st, 0u, none, 0u, lane, prof);
+      process_cell(a, T, before, cell, 0, st, 0u, none, 0u, lane, PROF ? prof : nullptr);
       publish(a, cell, 0, st, 0u, noinst, lane);
       kind = 0;
       ++self_processed;
     }
-    long long t3 = clock64();
-    cyc_self += t3 - t2;
+    long long t3 = PROF ? clock64() : 0;
+    if (PROF) cyc_self += t3 - t2;
     // commit: the popped cell on lane 0, its four neighbours on lanes 0-3 at
     // once (their queue buckets differ); every load before the first update
     {
@@ -821,7 +827,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
         if (d == 0) {
           sweeps += rsweeps;
           updates += rupdates;
-          cyc_rec += clock64() - t3;  // the record has arrived
+          if (PROF) cyc_rec += clock64() - t3;  // the record has arrived
           // popped cell: flags cleared, first removal done, the committed
           // kind's slot becomes current and the old current slot takes its
           // role, +1 version
@@ -868,12 +874,14 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       if (lane == 0) {
         H.size += ins;
         if (any_ovf) H.overflow = true;
-            if (H.size > max_size) max_size = H.size;
+            if (PROF && H.size > max_size) max_size = H.size;
       }
     }
     __syncwarp();
-    cyc_commit += clock64() - t3;
-    prev_cell = cell;
+    if (PROF) {
+      cyc_commit += clock64() - t3;
+      prev_cell = cell;
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     mon_checks += __shfl_xor_sync(kFull, mon_checks, o);
@@ -888,6 +896,9 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     a.counters[5] = self_processed;
     a.counters[6] = fast_hits;
     a.counters[7] = waits;
+    a.counters[15] = chain_hits;
+  }
+  if (PROF && lane == 0) {
     a.counters[8] = cyc_pop;
     a.counters[9] = cyc_obtain;
     a.counters[10] = cyc_self;
@@ -901,9 +912,10 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     a.counters[42] = cyc_rec;
     a.counters[43] = cyc_rescan;
     a.counters[44] = cyc_rt1;
-    a.counters[15] = chain_hits;
     for (int k = 0; k < 8; ++k) a.counters[16 + k] = miss_cls[k];
     a.counters[38] = (unsigned long long)max_size;
+  }
+  if (lane == 0) {
     if (H.overflow) atomicExch(a.status, 6);
     __threadfence();
     st_release_s32(a.done_flag, 1);
@@ -1103,6 +1115,7 @@ __device__ bool pick_job(const HcArgs& a, int pidx, Job& j, int wid) {
   return false;
 }
 
+template <bool PROF>
 __global__ void heapcell_spec_kernel(HcArgs a) {
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31;
@@ -1152,7 +1165,7 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
     H.overflow = false;
     for (int d = 0; d < 4; ++d) H.trk[d] = -1, H.tps[d] = -1;
     __syncwarp();
-    committer(a, H, T, before, lane);
+    committer<PROF>(a, H, T, before, lane);
     return;
   }
 
@@ -1279,13 +1292,16 @@ cudaError_t launch_heapcell(const HcArgs& args, int warps_per_cta, int max_ctas,
   size_t smem = (size_t)warps_per_cta * args.tile_doubles * sizeof(double);
   smem = std::max(smem, args.tile_doubles * sizeof(double) +
                            heapcell_committer_heap_bytes(args.heap_cap > 0 ? args.heap_cap : 0));
-  cudaError_t e = cudaFuncSetAttribute(heapcell_spec_kernel,
+  // the instrumented instantiation only when EIK_HC_PROFILE asked for it
+  const void* kern = args.prof ? (const void*)heapcell_spec_kernel<true>
+                               : (const void*)heapcell_spec_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heapcell_spec_kernel,
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
                                                     32 * warps_per_cta, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
@@ -1293,7 +1309,7 @@ cudaError_t launch_heapcell(const HcArgs& args, int warps_per_cta, int max_ctas,
   if (ctas < 1) ctas = 1;
   HcArgs a = args;
   void* params[] = {&a};
-  e = cudaLaunchCooperativeKernel((const void*)heapcell_spec_kernel, dim3(ctas),
+  e = cudaLaunchCooperativeKernel(kern, dim3(ctas),
                                   dim3(32 * warps_per_cta), params, smem, s);
   if (e != cudaSuccess) return e;
   heapcell_gather_kernel<<<blocks, 256, 0, s>>>(args);
