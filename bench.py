@@ -201,6 +201,7 @@ def main():
     torch.cuda.set_device(local)
     import paper_1110_6220_b200 as E
     from paper_1110_6220_b200 import configs
+    E.set_device(local)  # the library's own CUDA runtime: select the rank's GPU there too
 
     # Weak scaling: every rank solves its own replica of the C2 matrix (the
     # method matrix does not shard; SURVEY.md §8e -- row strips are for C5).

@@ -154,6 +154,11 @@ int eik_last_status(void);
 int eik_abi_version(void);
 /* Number of visible CUDA devices (0 on a CPU-only host; never fails). */
 int eik_device_count(void);
+/* Select the device later eik_solve / eik_plan_create calls on this thread
+ * use (the library carries its own CUDA runtime, so a host framework's
+ * device selection does not reach it).  One process per GPU calls this with
+ * its local rank. */
+int eik_set_device(int32_t device);
 
 /* ---- host-side geometry helpers (bit-exact restatements) ------------- */
 

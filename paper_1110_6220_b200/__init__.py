@@ -19,11 +19,20 @@ def device_count() -> int:
     return int(lib.eik_device_count())
 
 
+def set_device(device: int) -> None:
+    """Device for this thread's later solves/plans (eik_set_device): the
+    library has its own CUDA runtime, so torch.cuda.set_device does not
+    reach it."""
+    from ._native import raise_for
+    raise_for(lib.eik_set_device(int(device)))
+
+
 __all__ = [
     "BudgetError", "ConfigError", "LIB_PATH", "CellDecomposition", "CellTables", "ExitSpec",
     "Grid", "Problem", "SpeedField", "build_cells", "build_problem", "cell_tables",
     "snap_point_to_node", "speed_blocks", "speed_checkerboard", "speed_comb_maze",
     "speed_constant", "speed_nodemask", "speed_sinsum", "speed_sinusoid", "HybridStats",
     "Plan", "SolverOutput", "fhcm_solve", "fmm_solve", "fmsm_solve", "fsm_solve",
-    "hcm_solve", "solve", "device_count", "StripSolve", "fsm_solve_strips", "strip_bounds",
+    "hcm_solve", "solve", "device_count", "set_device", "StripSolve", "fsm_solve_strips",
+    "strip_bounds",
 ]

@@ -352,6 +352,13 @@ int eik_device_count(void) {
   return n;
 }
 
+int eik_set_device(int32_t device) {
+  int n = eik_device_count();
+  if (device < 0 || device >= n) return fail(EIK_ERR_CONFIG, "no such CUDA device");
+  CK(cudaSetDevice(device));
+  return EIK_OK;
+}
+
 eik_plan* eik_plan_create(const eik_problem* p, const eik_cells* c, int32_t method) {
   g_last_code = EIK_OK;
   g_last_error.clear();

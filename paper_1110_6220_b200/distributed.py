@@ -71,6 +71,12 @@ class DeviceStripSweeper:
 
     def __init__(self, local: Problem):
         from .solvers import Plan
+        try:
+            import torch
+            if torch.cuda.is_available() and torch.cuda.is_initialized():
+                N.raise_for(N.lib.eik_set_device(torch.cuda.current_device()))
+        except ImportError:
+            pass
         self.plan = Plan(local, "fsm")
         self.m, self.nl = local.grid.m, local.grid.n
         N.raise_for(N.lib.eik_plan_prepare(self.plan._h))

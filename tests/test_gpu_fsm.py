@@ -142,3 +142,13 @@ def test_bad_speed_is_rejected():
     p = E.build_problem(g, lambda x, y: np.where(x > 0.5, 0.0, 1.0), E.ExitSpec.point_source((0.5, 0.5)))
     with pytest.raises(ValueError):
         E.fsm_solve(p)
+
+
+def test_set_device_selects_and_rejects():
+    """eik_set_device: the library's own CUDA runtime follows the caller's
+    device choice (one process per GPU); an absent device is a ConfigError."""
+    E.set_device(0)
+    p = E.build_problem(E.Grid.unit_square(33), E.speed_constant(), E.ExitSpec.point_source((0.5, 0.5)))
+    assert E.fsm_solve(p).sweeps >= 2
+    with pytest.raises(E.ConfigError):
+        E.set_device(E.device_count() + 7)
