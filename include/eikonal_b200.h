@@ -159,6 +159,9 @@ int eik_device_count(void);
  * device selection does not reach it).  One process per GPU calls this with
  * its local rank. */
 int eik_set_device(int32_t device);
+/* Free the device buffers the library keeps cached for reuse by later plans
+ * (released plans return their buffers to a per-device cache). */
+void eik_release_cached(void);
 
 /* ---- host-side geometry helpers (bit-exact restatements) ------------- */
 

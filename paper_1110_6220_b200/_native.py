@@ -85,6 +85,7 @@ EXPORTS = {
     "eik_abi_version": (C.c_int, []),
     "eik_device_count": (C.c_int, []),
     "eik_set_device": (C.c_int, [C.c_int32]),
+    "eik_release_cached": (None, []),
     "eik_cell_probe_points": (C.c_int64, [C.POINTER(eik_grid), C.c_int32, C.c_int32,
                                           C.c_int32, _dp]),
     "eik_cell_centers": (C.c_int64, [C.POINTER(eik_grid), C.c_int32, C.c_int32, _dp]),

@@ -10,6 +10,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -77,9 +79,65 @@ int check_cells(const eik_problem* p, const eik_cells* c, int method) {
 
 }  // namespace
 
+// ---- device buffer cache ------------------------------------------------
+namespace {
+std::mutex g_pool_mu;
+std::map<std::pair<int, size_t>, std::vector<void*>> g_pool_free;  // (device, bytes)
+std::map<void*, std::pair<int, size_t>> g_pool_live;
+size_t g_pool_cached = 0;
+constexpr size_t kPoolCap = size_t(32) << 30;  // cached bytes kept at most
+}  // namespace
+
+cudaError_t pool_alloc(void** p, size_t bytes) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    auto it = g_pool_free.find({dev, bytes});
+    if (it != g_pool_free.end() && !it->second.empty()) {
+      *p = it->second.back();
+      it->second.pop_back();
+      g_pool_cached -= bytes;
+      g_pool_live[*p] = {dev, bytes};
+      return cudaSuccess;
+    }
+  }
+  e = cudaMalloc(p, bytes);
+  if (e == cudaErrorMemoryAllocation) {  // give the cache back and retry once
+    eik_release_cached();
+    cudaGetLastError();
+    e = cudaMalloc(p, bytes);
+  }
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  g_pool_live[*p] = {dev, bytes};
+  return cudaSuccess;
+}
+
+void pool_release(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  auto it = g_pool_live.find(p);
+  if (it == g_pool_live.end()) return;
+  const auto key = it->second;
+  g_pool_live.erase(it);
+  if (g_pool_cached + key.second > kPoolCap) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(key.first);
+    cudaFree(p);
+    cudaSetDevice(cur);
+    return;
+  }
+  g_pool_free[key].push_back(p);
+  g_pool_cached += key.second;
+}
+
 void plan_free(eik_plan* P) {
   if (!P) return;
-  for (void* ptr : P->allocs) cudaFree(ptr);
+  if (P->stream) cudaStreamSynchronize(P->stream);  // nothing in flight on reused blocks
+  for (void* ptr : P->allocs) pool_release(ptr);
   if (P->ev0) cudaEventDestroy(P->ev0);
   if (P->ev1) cudaEventDestroy(P->ev1);
   if (P->stream) cudaStreamDestroy(P->stream);
@@ -350,6 +408,19 @@ int eik_device_count(void) {
     return 0;
   }
   return n;
+}
+
+void eik_release_cached(void) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& kv : g_pool_free) {
+    cudaSetDevice(kv.first.first);
+    for (void* q : kv.second) cudaFree(q);
+  }
+  cudaSetDevice(cur);
+  g_pool_free.clear();
+  g_pool_cached = 0;
 }
 
 int eik_set_device(int32_t device) {

@@ -86,10 +86,18 @@ int cuda_fail(cudaError_t e, const char* where);
     if (e_ != cudaSuccess) return cuda_fail(e_, #expr);   \
   } while (0)
 
+// Device buffers come from a per-device cache of released blocks (exact-size
+// reuse): plans of one problem shape are created and destroyed repeatedly
+// through eik_solve, and cudaMalloc/cudaFree (which synchronises the device)
+// would otherwise sit on that path.  Released blocks stay cached up to a cap
+// (eik_release_cached frees them).
+cudaError_t pool_alloc(void** p, size_t bytes);
+void pool_release(void* p);
+
 template <class T>
 int dalloc(T** p, size_t count) {
   if (count == 0) count = 1;
-  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), count * sizeof(T));
+  cudaError_t e = pool_alloc(reinterpret_cast<void**>(p), count * sizeof(T));
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
   return EIK_OK;
 }
