@@ -137,13 +137,13 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     // per-warp tile: values + costs with halo, 4 border snapshots, lock bytes
     const size_t tile = ((smem + sizeof(double) - 1) / sizeof(double) + 1) & ~(size_t)1;
     P->cg.tile_doubles = (int64_t)tile;
-    P->hc_warps_per_cta = (int)std::max<size_t>(1, std::min<size_t>(8, kTileBudget / (tile * 8)));
+    const int fit = (int)std::max<size_t>(1, std::min<size_t>(8, kTileBudget / (tile * 8)));
     // worker warps per SM: 1-8 measured within 2 % of each other on C2, 2 the
     // best (one warp per scheduler pair keeps each speculation's latency
-    // short); EIK_HC_WARPS overrides
-    P->hc_warps_per_cta = std::min(P->hc_warps_per_cta, 2);
+    // short); EIK_HC_WARPS overrides within what shared memory fits
+    P->hc_warps_per_cta = std::min(fit, 2);
     if (const char* w = std::getenv("EIK_HC_WARPS"))
-      P->hc_warps_per_cta = std::max(1, std::min(8, std::atoi(w)));
+      P->hc_warps_per_cta = std::max(1, std::min(fit, std::atoi(w)));
     // the committer's heap + cell values go to its shared memory when they
     // fit next to its tile (uint16 heap indices)
     {
