@@ -154,6 +154,21 @@ int eik_last_status(void);
 int eik_abi_version(void);
 /* Number of visible CUDA devices (0 on a CPU-only host; never fails). */
 int eik_device_count(void);
+/* Error metrics of a method's field against a ground truth
+ * (metrics.cpp:11-69, error_fields + error_ratios): e = |u_exact - u_truth|,
+ * E = |u_method - u_truth|, X+ = non-exit nodes with e > 1e-14.  Fields are
+ * dense m*n (host or device per on_device); exit_nodes is a host array.  Maxima and counts match the
+ * reference exactly; l_1 and avg_error_ratio are deterministic block-ordered
+ * sums (within a few ulps of the reference's sequential sums). */
+typedef struct eik_metrics_out {
+  double l_inf, l_1, max_error_ratio, avg_error_ratio, ratio_of_max;
+  int64_t m_plus;
+  int32_t x_plus_empty;
+} eik_metrics_out;
+int eik_metrics(const double* u_method, const double* u_exact, const double* u_truth, int64_t m,
+                int64_t n, const int64_t* exit_nodes, int64_t n_exit, int32_t on_device,
+                eik_metrics_out* out);
+
 /* Select the device later eik_solve / eik_plan_create calls on this thread
  * use (the library carries its own CUDA runtime, so a host framework's
  * device selection does not reach it).  One process per GPU calls this with

@@ -192,11 +192,12 @@ def ref_solve(p: Problem, method: str, cells_x: int = 0, cells_y: int = 0) -> Re
 
 
 def ref_metrics(p: Problem, u_method: np.ndarray, u_exact: np.ndarray, refine: int = 4):
-    """(l_inf, l_1, R, rho, R_ratio) of metrics.cpp against refine-x FMM truth."""
+    """(l_inf, l_1, R, rho, R_ratio, m_plus, x_plus_empty) of metrics.cpp against
+    refine-x FMM truth."""
     g = p.grid.c()
     en = np.ascontiguousarray(p.exit_nodes, dtype=np.int64)
     ec = np.ascontiguousarray(p.exit_cost, dtype=np.float64)
-    out = np.zeros(5)
+    out = np.zeros(7)
     um = np.ascontiguousarray(u_method, dtype=np.float64)
     ue = np.ascontiguousarray(u_exact, dtype=np.float64)
     rc = rlib.ref_metrics(C.byref(g), C.byref(p.speed.cfield), en.ctypes.data_as(_i64p),

@@ -134,7 +134,7 @@ int ref_solve(int method, const eik_grid* g, const eik_field* field,
 // truth; `u_exact` is the exact-solver field (FMM).  Returns 0 on success.
 int ref_metrics(const eik_grid* g, const eik_field* field, const int64_t* exit_nodes,
                 const double* exit_cost, int64_t n_exit, int refine,
-                const double* u_method, const double* u_exact, double* out5) {
+                const double* u_method, const double* u_exact, double* out5) {  // out5[7]
   try {
     using namespace eikonal;
     Problem p;
@@ -155,6 +155,8 @@ int ref_metrics(const eik_grid* g, const eik_field* field, const int64_t* exit_n
     out5[2] = r.max_error_ratio;
     out5[3] = r.avg_error_ratio;
     out5[4] = r.ratio_of_max;
+    out5[5] = static_cast<double>(r.m_plus);
+    out5[6] = r.x_plus_empty ? 1.0 : 0.0;
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -13,6 +13,7 @@ from .problem import (CellDecomposition, CellTables, ExitSpec, Grid, Problem, Sp
 from .solvers import (HybridStats, Plan, SolverOutput, fhcm_solve, fmm_solve, fmsm_solve,
                       fsm_solve, hcm_solve, solve)
 from .distributed import StripSolve, fsm_solve_strips, strip_bounds
+from .metrics import MetricsReport, ground_truth, method_metrics, refined_problem
 
 
 def device_count() -> int:
@@ -34,5 +35,5 @@ __all__ = [
     "speed_constant", "speed_nodemask", "speed_sinsum", "speed_sinusoid", "HybridStats",
     "Plan", "SolverOutput", "fhcm_solve", "fmm_solve", "fmsm_solve", "fsm_solve",
     "hcm_solve", "solve", "device_count", "set_device", "StripSolve", "fsm_solve_strips",
-    "strip_bounds",
+    "strip_bounds", "MetricsReport", "ground_truth", "method_metrics", "refined_problem",
 ]

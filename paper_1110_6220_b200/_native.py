@@ -67,6 +67,12 @@ class eik_field(C.Structure):
                 ("K", C.c_int32), ("kp", _dp), ("kq", _dp), ("kphi", _dp)]
 
 
+class eik_metrics_out(C.Structure):
+    _fields_ = [("l_inf", C.c_double), ("l_1", C.c_double), ("max_error_ratio", C.c_double),
+                ("avg_error_ratio", C.c_double), ("ratio_of_max", C.c_double),
+                ("m_plus", C.c_int64), ("x_plus_empty", C.c_int32)]
+
+
 EXPORTS = {
     # name: (restype, argtypes)
     "eik_solve": (C.c_int, [C.POINTER(eik_problem), C.POINTER(eik_cells), C.c_int32,
@@ -86,6 +92,8 @@ EXPORTS = {
     "eik_device_count": (C.c_int, []),
     "eik_set_device": (C.c_int, [C.c_int32]),
     "eik_release_cached": (None, []),
+    "eik_metrics": (C.c_int, [_dp, _dp, _dp, C.c_int64, C.c_int64, _i64p, C.c_int64, C.c_int32,
+                              C.POINTER(eik_metrics_out)]),
     "eik_cell_probe_points": (C.c_int64, [C.POINTER(eik_grid), C.c_int32, C.c_int32,
                                           C.c_int32, _dp]),
     "eik_cell_centers": (C.c_int64, [C.POINTER(eik_grid), C.c_int32, C.c_int32, _dp]),

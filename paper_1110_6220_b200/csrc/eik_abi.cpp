@@ -410,6 +410,64 @@ int eik_device_count(void) {
   return n;
 }
 
+int eik_metrics(const double* u_method, const double* u_exact, const double* u_truth, int64_t m,
+                int64_t n, const int64_t* exit_nodes, int64_t n_exit, int32_t on_device,
+                eik_metrics_out* out) {
+  g_last_code = EIK_OK;
+  g_last_error.clear();
+  if (!out || !u_method || !u_exact || !u_truth || m < 1 || n < 1 || n_exit < 0 ||
+      (n_exit > 0 && !exit_nodes))
+    return fail(EIK_ERR_DOMAIN, "eik_metrics: bad arguments");
+  if (eik_device_count() < 1)
+    return fail(EIK_ERR_CUDA, "no CUDA device visible: the Eikonal hot path has no CPU fallback");
+  const int64_t M = m * n;
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  std::vector<void*> tmp;
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(s);
+    for (void* q : tmp) pool_release(q);
+    cudaStreamDestroy(s);
+  };
+  auto dev_copy = [&](const void* src, size_t bytes, void** dst) -> cudaError_t {
+    cudaError_t e = pool_alloc(dst, bytes);
+    if (e != cudaSuccess) return e;
+    tmp.push_back(*dst);
+    return cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, s);
+  };
+  const double *vm = u_method, *ve = u_exact, *vt = u_truth;
+  cudaError_t e = cudaSuccess;
+  if (!on_device) {
+    void *a = nullptr, *b = nullptr, *c = nullptr;
+    if ((e = dev_copy(u_method, 8 * M, &a)) == cudaSuccess &&
+        (e = dev_copy(u_exact, 8 * M, &b)) == cudaSuccess &&
+        (e = dev_copy(u_truth, 8 * M, &c)) == cudaSuccess) {
+      vm = static_cast<const double*>(a);
+      ve = static_cast<const double*>(b);
+      vt = static_cast<const double*>(c);
+    }
+  }
+  void* dex = nullptr;
+  void* mask = nullptr;
+  if (e == cudaSuccess && n_exit > 0) e = dev_copy(exit_nodes, 8 * n_exit, &dex);
+  if (e == cudaSuccess && (e = pool_alloc(&mask, (size_t)M)) == cudaSuccess) tmp.push_back(mask);
+  double res[5];
+  long long cnt[2];
+  if (e == cudaSuccess)
+    e = device_metrics(vm, ve, vt, M, static_cast<const int64_t*>(dex), n_exit,
+                       static_cast<uint8_t*>(mask), s, res, cnt);
+  cleanup();
+  if (e != cudaSuccess) return cuda_fail(e, "eik_metrics");
+  out->l_inf = res[0];
+  out->l_1 = res[1];
+  out->max_error_ratio = res[2];
+  out->avg_error_ratio = res[3];
+  out->ratio_of_max = res[4];
+  out->m_plus = cnt[0];
+  out->x_plus_empty = (int32_t)cnt[1];
+  return EIK_OK;
+}
+
 void eik_release_cached(void) {
   std::lock_guard<std::mutex> lk(g_pool_mu);
   int cur = 0;

@@ -126,4 +126,8 @@ cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int
                            int* launches);
 cudaError_t launch_fsm(const FsmArgs& a, cudaStream_t s, int* launches);
 
+cudaError_t device_metrics(const double* vm, const double* ve, const double* vt, int64_t M,
+                           const int64_t* exits, int64_t n_exit, uint8_t* mask, cudaStream_t s,
+                           double res[5], long long counts[2]);
+
 }  // namespace eikb200

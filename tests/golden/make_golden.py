@@ -13,6 +13,7 @@ built):  python tests/golden/make_golden.py [--big]
                 acceptance sweep counts of acceptance.cpp:133-146).
   c34.json      (--c34) configs 3 and 4 at 4097^2.
   c5.json       (--c5) config 5's field family at 2049^2.
+  metrics.*     (--metrics) metrics.cpp ground truth and reports, small cases.
 """
 from __future__ import annotations
 
@@ -170,6 +171,30 @@ def c34():
         json.dump(out, f, indent=1, sort_keys=True)
 
 
+def metrics():
+    """metrics.cpp on the small cases: the reference's refine-4 ground truth
+    (metrics.npz, its FMM on the refined grid, subsampled) and its
+    method_metrics report for every method against it (metrics.json), with
+    u_method / u_exact taken from small.npz (the reference's own fields)."""
+    fields = np.load(os.path.join(HERE, "small.npz"))
+    arrays, meta = {}, {}
+    for cid, make, cells in SMALL_CASES:
+        p = make()
+        fine = E.refined_problem(p, 4)
+        rt = O.ref_solve(fine, "fmm").u.reshape(fine.grid.n, fine.grid.m)[::4, ::4]
+        arrays[f"{cid}/truth4"] = np.ascontiguousarray(rt).reshape(-1)
+        exact = fields[f"{cid}/fmm"]
+        keys = [f"{cid}/fsm"] + [f"{cid}/{meth}/{c}" for c in cells for meth in ("hcm", "fhcm", "fmsm")]
+        for k in keys:
+            r = O.ref_metrics(p, fields[k], exact, 4)
+            meta[k] = {"l_inf": r[0], "l_1": r[1], "max_error_ratio": r[2],
+                       "avg_error_ratio": r[3], "ratio_of_max": r[4], "m_plus": int(r[5]),
+                       "x_plus_empty": bool(r[6])}
+    np.savez_compressed(os.path.join(HERE, "metrics.npz"), **arrays)
+    with open(os.path.join(HERE, "metrics.json"), "w") as f:
+        json.dump(meta, f, indent=1, sort_keys=True)
+
+
 def c5():
     """BASELINE config 5's field family (16 random-phase sinusoids, 64 random
     node sources) at 2049^2, where the reference runs here: sha256 + counters
@@ -196,6 +221,7 @@ if __name__ == "__main__":
     ap.add_argument("--big", action="store_true")
     ap.add_argument("--c34", action="store_true")
     ap.add_argument("--c5", action="store_true")
+    ap.add_argument("--metrics", action="store_true")
     a = ap.parse_args()
     if not O.have_ref():
         sys.exit("oracle/_ref/libeikref.so missing: run make -C oracle here")
@@ -204,6 +230,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if a.c5:
         c5()
+        sys.exit(0)
+    if a.metrics:
+        metrics()
         sys.exit(0)
     with open(os.path.join(HERE, "kat.json"), "w") as f:
         json.dump(kat(), f, indent=1)
