@@ -94,6 +94,13 @@ def _load_ref():
     lib.ref_node_update.argtypes = [_dp, C.c_double, C.c_double]
     lib.ref_node_update.restype = C.c_double
     lib.ref_directional_update.argtypes = [_dp, C.c_int, C.c_double, C.c_double]
+    lib.ref_dump_field.argtypes = [_dp, C.c_int, C.c_int, C.c_double, C.c_char_p, C.c_int]
+    lib.ref_dump_field.restype = C.c_int
+    lib.ref_csv_line.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int, _dp, _i64p, C.c_char_p,
+                                 C.c_int]
+    lib.ref_csv_line.restype = C.c_int
+    lib.ref_csv_header.argtypes = []
+    lib.ref_csv_header.restype = C.c_char_p
     lib.ref_directional_update.restype = C.c_double
     lib.ref_snap.argtypes = [C.POINTER(N.eik_grid), C.c_double, C.c_double, _i64p, _i64p]
     lib.ref_snap.restype = C.c_int
@@ -158,6 +165,30 @@ def oracle_fsm_sweep(m: int, n: int, h: float, F: np.ndarray, frozen: np.ndarray
     assert F.dtype == np.float64 and u.dtype == np.float64 and frozen.dtype == np.uint8
     return bool(olib.orc_fsm_sweep(m, n, h, F.ctypes.data_as(_dp), frozen.ctypes.data,
                                    u.ctypes.data_as(_dp), direction))
+
+
+def ref_dump_field(u: np.ndarray, m: int, n: int, h: float, path: str, ascii: bool) -> None:
+    """The reference's dump_field (field_io.cpp:20-45)."""
+    uu = np.ascontiguousarray(u, dtype=np.float64)
+    if rlib.ref_dump_field(uu.ctypes.data_as(_dp), m, n, h, path.encode(), 1 if ascii else 0):
+        raise RuntimeError(rlib.ref_last_error().decode())
+
+
+_METHOD_ENUM = {"fmm": 0, "fsm": 1, "lsm": 2, "hcm": 3, "fhcm": 4, "fmsm": 5}  # experiment.hpp:11
+
+
+def ref_csv_line(problem: str, method: str, grid_m: int, cells_x: int, d9, c3) -> str:
+    """The reference's csv_line (experiment.cpp:319-329)."""
+    d = np.ascontiguousarray(d9, dtype=np.float64)
+    c = np.ascontiguousarray(c3, dtype=np.int64)
+    buf = C.create_string_buffer(1024)
+    rlib.ref_csv_line(problem.encode(), _METHOD_ENUM[method], grid_m, cells_x,
+                      d.ctypes.data_as(_dp), c.ctypes.data_as(_i64p), buf, 1024)
+    return buf.value.decode()
+
+
+def ref_csv_header() -> str:
+    return rlib.ref_csv_header().decode()
 
 
 _REF_METHOD = {"fmm": 0, "fsm": 1, "lsm": 2, "hcm": 3, "fhcm": 4, "fmsm": 5}

@@ -16,6 +16,8 @@
 #include <string>
 
 #include "eikonal/cells.hpp"
+#include "eikonal/experiment.hpp"
+#include "eikonal/field_io.hpp"
 #include "eikonal/classic_solvers.hpp"
 #include "eikonal/fmsm.hpp"
 #include "eikonal/grid.hpp"
@@ -162,6 +164,51 @@ int ref_metrics(const eik_grid* g, const eik_field* field, const int64_t* exit_n
     g_err = e.what();
     return 5;
   }
+}
+
+// The reference's own writers, for byte-level comparisons (field_io.cpp,
+// experiment.cpp:314-329).
+int ref_dump_field(const double* u, int m, int n, double h, const char* path, int ascii) {
+  try {
+    using namespace eikonal;
+    ValueField v(m, n);
+    std::memcpy(v.values.data(), u, sizeof(double) * (size_t)m * n);
+    dump_field(v, h, path, ascii ? DumpFormat::Ascii : DumpFormat::Raw);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 5;
+  }
+}
+
+int ref_csv_line(const char* problem, int method, int grid_m, int cells_x, const double* d9,
+                 const long long* c3, char* out, int cap) {
+  using namespace eikonal;
+  ExperimentRow r;
+  r.problem = problem;
+  r.method = static_cast<Method>(method);
+  r.grid_m = grid_m;
+  r.cells_x = cells_x;
+  r.elapsed_ms = d9[0];
+  r.l_inf = d9[1];
+  r.l_1 = d9[2];
+  r.max_ratio = d9[3];
+  r.rho = d9[4];
+  r.ratio_of_max = d9[5];
+  r.avhr = d9[6];
+  r.avs = d9[7];
+  r.mon_pct = d9[8];
+  r.sweeps = c3[0];
+  r.node_updates = c3[1];
+  r.heap_removals = c3[2];
+  std::string line = csv_line(r);
+  std::snprintf(out, (size_t)cap, "%s", line.c_str());
+  return (int)line.size();
+}
+
+const char* ref_csv_header() {
+  static std::string h = eikonal::csv_header();
+  return h.c_str();
 }
 
 }  // extern "C"

@@ -14,6 +14,7 @@ from .solvers import (HybridStats, Plan, SolverOutput, fhcm_solve, fmm_solve, fm
                       fsm_solve, hcm_solve, solve)
 from .distributed import StripSolve, fsm_solve_strips, strip_bounds
 from .metrics import MetricsReport, ground_truth, method_metrics, refined_problem
+from . import experiment_io
 
 
 def device_count() -> int:
@@ -36,4 +37,5 @@ __all__ = [
     "Plan", "SolverOutput", "fhcm_solve", "fmm_solve", "fmsm_solve", "fsm_solve",
     "hcm_solve", "solve", "device_count", "set_device", "StripSolve", "fsm_solve_strips",
     "strip_bounds", "MetricsReport", "ground_truth", "method_metrics", "refined_problem",
+    "experiment_io",
 ]
