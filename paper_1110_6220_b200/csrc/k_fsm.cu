@@ -132,7 +132,7 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       const double res = upd ? cand : cur;
       if (upd) pu[S * t] = cand;
       changed |= upd;
-      if (out_glob) po[S * t] = res;
+      if (out_glob) __stcg(po + S * t, res);  // straight to L2: the next strip polls it
       res_prev = res;
     }
     pu += S * kU;
