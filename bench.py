@@ -2,11 +2,15 @@
 F = 1 + 0.5 sin(20 pi x) sin(20 pi y), centre source), the full method matrix
 of BASELINE.json: fmm, fsm, and fmsm / hcm / fhcm at 8, 16, 32, 64-point cells.
 
-One step = one solve of every method-config in the matrix.  `value` is the
-whole-job throughput (sum of grid points converged / sum of solve times) with
-the speed field already resident in HBM; `e2e` is the same metric through the
-public API with pinned host buffers (H2D of F and tables, D2H of u inside the
-timed region).  Prints one JSON line (rank 0).
+One step = one solve of every method-config in the matrix, the 14 solves
+running concurrently on the GPU (eik_plan_run_batch: SM-partitioned
+persistent kernels, one stream each -- the device counterpart of the
+reference runner's --jobs pool).  `value` is the whole-job throughput (grid
+points converged per step / step device time) with the speed fields already
+resident in HBM; `e2e` is the same metric through the public API
+(eik_solve_batch) with pinned host buffers (H2D of F and tables, D2H of u
+inside the timed region).  `methods` also lists each solve's device time
+alone on the whole GPU (`solo_ms`).  Prints one JSON line (rank 0).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -22,6 +26,10 @@ import threading
 import time
 
 import numpy as np
+
+# one hardware work queue per stream for the concurrent solves; must be set
+# before anything in the process creates the CUDA context
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -223,30 +231,27 @@ def main():
         flush.zero_()
         torch.cuda.synchronize()
 
-    def step(timed):
-        tot_ms, launches, per = 0.0, 0, {}
-        for (meth, cs), (plan, _) in plans.items():
-            flush_l2()  # inputs < L2 (126 MB): flush between timed solves
-            o = plan.run()
-            t = o.device_ms + o.host_ms
-            tot_ms += t
-            launches += o.kernel_launches
-            per[f"{meth}" + (f"/{cs}" if cs else "")] = (t, o)
-        return tot_ms, launches, per
+    keys = [f"{meth}" + (f"/{cs}" if cs else "") for meth, cs in rows]
+    plan_list = [plans[r][0] for r in rows]
+
+    def step():
+        flush_l2()  # per-plan inputs < L2 (126 MB): flush before every timed step
+        outs, ms = E.run_batch(plan_list)
+        return ms, sum(o.kernel_launches for o in outs), dict(zip(keys, outs))
 
     for _ in range(args.warmup):
-        step(False)
+        step()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
     step_ms, launches, per_all = [], 0, {}
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
-            ms, L, per = step(True)
+            ms, L, per = step()
             step_ms.append(ms)
             launches += L
-            for k, (t, o) in per.items():
-                per_all.setdefault(k, []).append((t, o))
+            for k, o in per.items():
+                per_all.setdefault(k, []).append((o.device_ms + o.host_ms, o))
     torch.cuda.synchronize()
     mean_ms = statistics.mean(step_ms)
     if world > 1:
@@ -254,6 +259,13 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         mean_ms = float(t.item())
     value = world * len(rows) * M / (mean_ms / 1e3)
+
+    # each solve alone on the whole GPU (latency; outside the timed region)
+    solo = {}
+    for k, pl in zip(keys, plan_list):
+        flush_l2()
+        o = pl.run()
+        solo[k] = o.device_ms + o.host_ms
 
     # per-method table with the reference's counters beside ours
     with open(os.path.join(ROOT, "tests", "golden", "big.json")) as f:
@@ -273,7 +285,8 @@ def main():
             nbytes = (24.0 * cs * cs + 32.0 * cs) * (o.heap_removals if meth != "fmsm"
                                                       else (g.m // cs) ** 2)
         ach = nbytes / (t / 1e3) / 1e9
-        methods[k] = {"ms": round(t, 3), "points_per_s": M / (t / 1e3), "sweeps": o.sweeps,
+        methods[k] = {"ms": round(t, 3), "solo_ms": round(solo[k], 3), "ctas": o.ctas,
+                      "points_per_s": M / (t / 1e3), "sweeps": o.sweeps,
                       "ref_sweeps": ref.get("sweeps"), "heap_removals": o.heap_removals,
                       "ref_heap_removals": ref.get("heap_removals"),
                       "node_updates": o.node_updates, "ref_node_updates": ref.get("node_updates"),
@@ -293,26 +306,33 @@ def main():
     roofline = {"bound": "hbm", "kernel": dom_k, "achieved": round(dom_ach, 2), "peak": hbm,
                 "unit": "GB/s", "frac": dom_ach / hbm, "traffic": traffic,
                 "algorithmic_bytes": dom_bytes, "peak_kind": peak_kind,
-                "note": "latency-bound fp64 dependency chains; algorithmic bytes per SURVEY §8(d)"}
+                "note": "the longest solve of the concurrent step (its kernel's duration inside "
+                        "the step); latency-bound fp64 dependency chains; algorithmic bytes per "
+                        "SURVEY §8(d)"}
 
-    # e2e: public API, pinned host buffers, H2D + solve + D2H inside the timed region
+    # e2e: public API (eik_solve_batch), pinned host buffers, H2D + solves +
+    # D2H of every solve of the step inside the timed region
     pinned_F = torch.empty(M, dtype=torch.float64, pin_memory=True).numpy()
     pinned_F[:] = p.sampled_speed()
-    pinned_u = torch.empty(M, dtype=torch.float64, pin_memory=True).numpy()
     p_pin = E.Problem(g, p.speed, p.exit_nodes, p.exit_cost, p.exit_points, p.exit_point_cost,
                       _F=pinned_F)
-    e2e_s, h2d, d2h = 0.0, 0, 0
+    pinned_u = [torch.empty(M, dtype=torch.float64, pin_memory=True).numpy() for _ in rows]
+    jobs = [(p_pin, meth, plans[(meth, cs)][1], tables.get(cs)) for meth, cs in rows]
+    h2d = d2h = 0
     for meth, cs in rows:
-        cells = E.build_cells(g, g.m // cs, g.m // cs) if cs else None
-        flush_l2()
-        t0 = time.perf_counter()
-        E.solve(p_pin, meth, cells, tables.get(cs), out=pinned_u)
-        e2e_s += time.perf_counter() - t0
         h2d += 8 * M + 16 * len(p.exit_nodes)
         if cs:
             tb = tables[cs]
             h2d += 8 * sum(len(a) for a in (tb.probe_w, tb.probe_e, tb.probe_s, tb.probe_n, tb.center))
         d2h += 8 * M
+    E.solve_batch(jobs, outs=pinned_u)  # warm-up (device buffer cache)
+    e2e_t = []
+    for _ in range(max(1, args.steps)):
+        flush_l2()
+        t0 = time.perf_counter()
+        E.solve_batch(jobs, outs=pinned_u)
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = statistics.mean(e2e_t)
 
     cpu = None if args.no_cpu_baseline or rank != 0 else cpu_baseline_single_core()
     if rank == 0:
@@ -324,6 +344,8 @@ def main():
             "config": {"workload": "c2_sinusoid_2049_method_matrix", "grid": 2049,
                        "methods": METHODS, "cell_sizes": CELL_SIZES,
                        "parallelism": f"replicas x{world}",
+                       "concurrency": f"{len(rows)} solves per step run concurrently "
+                                      "(eik_plan_run_batch, SM-partitioned)",
                        "l2": "256 MB flush before every solve (inputs < L2)"},
             "e2e": {"value": world * len(rows) * M / e2e_s, "unit": "points/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

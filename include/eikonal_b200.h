@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define EIK_ABI_VERSION 1
+#define EIK_ABI_VERSION 2
 
 /* Solver selection; numbering mirrors eikonal::Method (experiment.hpp:11). */
 enum eik_method {
@@ -103,6 +103,7 @@ typedef struct eik_output {
   /* HCM/FHCM speculative replay: pops whose worker result was valid at
    * commit, pops that waited on a worker, pops processed by the committer */
   int64_t spec_hits, spec_waits, spec_self;
+  int64_t grid_ctas;    /* CTAs of the persistent solve kernel this run launched */
 } eik_output;
 
 /* One solve.  `cells` may be NULL for FMM/FSM.  Thread-safe: each call owns
@@ -125,6 +126,34 @@ int eik_plan_run(eik_plan* plan, eik_output* out);
 const double* eik_plan_values(const eik_plan* plan);
 int64_t eik_plan_pitch(const eik_plan* plan);
 void eik_plan_destroy(eik_plan* plan);
+
+/* ---- several solves sharing one GPU ------------------------------------
+ * The device-side counterpart of the reference's experiment runner, which
+ * runs the rows of its method matrix on a pool of --jobs threads
+ * (experiment.cpp:284-310): every solve's persistent kernel gets a slice of
+ * the device and the solves run concurrently, one stream and one host
+ * thread each.  Results, counters and errors per solve are exactly those of
+ * eik_plan_run / eik_solve.
+ *
+ * eik_plan_set_ctas   cap the CTAs of a plan's persistent kernel (0 = the
+ *                     whole device, the default).  FSM/FMM grids are fixed
+ *                     (one warp per 32-row strip) and ignore the cap.
+ * eik_plan_capacity   CTAs of the plan's persistent kernel the whole device
+ *                     holds, and the fixed grid size (FSM/FMM) or 0.
+ * eik_plan_run_batch  run n distinct plans of one device concurrently.
+ *                     Plans without a cap split what the fixed grids and the
+ *                     capped plans leave (heap-cell plans weight 1, FMSM
+ *                     1/4).  *batch_ms = device time from the call until the
+ *                     last solve ended.  Returns the first failing plan's
+ *                     code (eik_last_error names it).
+ * eik_solve_batch     n eik_solve calls run the same way (uploads, solves
+ *                     and downloads overlap); cells[k] may be NULL for
+ *                     FMM/FSM and `cells` itself NULL when no solve needs one. */
+int eik_plan_set_ctas(eik_plan* plan, int32_t max_ctas);
+int eik_plan_capacity(eik_plan* plan, int32_t* device_ctas, int32_t* fixed_ctas);
+int eik_plan_run_batch(eik_plan* const* plans, int32_t n, eik_output* outs, double* batch_ms);
+int eik_solve_batch(const eik_problem* const* problems, const eik_cells* const* cells,
+                    const int32_t* methods, int32_t n, eik_output* outs, double* batch_ms);
 
 /* Sweep-level control of an EIK_FSM / EIK_FMM plan -- the building blocks of
  * strip-Jacobi FSM across GPUs (SURVEY.md section 8(e)

@@ -52,7 +52,7 @@ class eik_output(C.Structure):
                 ("mon_single", C.c_int64), ("avhr", C.c_double), ("avs", C.c_double),
                 ("mon_pct", C.c_double), ("device_ms", C.c_double), ("host_ms", C.c_double),
                 ("kernel_launches", C.c_int64), ("spec_hits", C.c_int64),
-                ("spec_waits", C.c_int64), ("spec_self", C.c_int64)]
+                ("spec_waits", C.c_int64), ("spec_self", C.c_int64), ("grid_ctas", C.c_int64)]
 
 
 class eik_field(C.Structure):
@@ -86,6 +86,13 @@ EXPORTS = {
     "eik_plan_sweep": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_int32)]),
     "eik_plan_get_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]),
     "eik_plan_set_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]),
+    "eik_plan_set_ctas": (C.c_int, [C.c_void_p, C.c_int32]),
+    "eik_plan_capacity": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
+    "eik_plan_run_batch": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(eik_output),
+                                     C.POINTER(C.c_double)]),
+    "eik_solve_batch": (C.c_int, [C.POINTER(C.POINTER(eik_problem)), C.POINTER(C.POINTER(eik_cells)),
+                                  C.POINTER(C.c_int32), C.c_int32, C.POINTER(eik_output),
+                                  C.POINTER(C.c_double)]),
     "eik_last_error": (C.c_char_p, []),
     "eik_last_status": (C.c_int, []),
     "eik_abi_version": (C.c_int, []),

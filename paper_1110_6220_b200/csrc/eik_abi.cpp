@@ -9,10 +9,13 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "eik_internal.h"
@@ -20,6 +23,18 @@
 #include "eikonal_b200.h"
 
 namespace eikb200 {
+
+namespace {
+// Concurrent plans (eik_plan_run_batch) need a hardware work queue per
+// stream: with the driver's default of 8, streams share queues and a solve
+// waits behind another stream's persistent kernel.  Read when the CUDA
+// context is created, so this only takes effect if the library is loaded
+// before anything else in the process initialises CUDA; a value the user set
+// is kept.
+struct ConnectionsDefault {
+  ConnectionsDefault() { setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0); }
+} g_connections_default;
+}  // namespace
 
 thread_local std::string g_last_error;
 thread_local int g_last_code = EIK_OK;
@@ -134,6 +149,38 @@ void pool_release(void* p) {
   g_pool_cached += key.second;
 }
 
+cudaError_t ensure_dynamic_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> set;  // (device, kernel) -> limit
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = set[{dev, kernel}];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+
+int plan_capacity(eik_plan* P, int* device, int* fixed) {
+  CK(cudaSetDevice(P->device));
+  *fixed = 0;
+  switch (P->method) {
+    case EIK_FSM:
+    case EIK_FMM:
+      CK(fsm_capacity(P->nstrips, fixed, device));
+      break;
+    case EIK_FMSM:
+      CK(fmsm_capacity(P->cg.tile_doubles, P->warps_per_cta, device));
+      break;
+    default:
+      CK(heapcell_capacity(P->cg.tile_doubles, P->hc_heap_cap, P->hc_warps_per_cta,
+                           (size_t)P->hc_min_smem, device));
+  }
+  return EIK_OK;
+}
+
 void plan_free(eik_plan* P) {
   if (!P) return;
   if (P->stream) cudaStreamSynchronize(P->stream);  // nothing in flight on reused blocks
@@ -236,7 +283,9 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   CK(cudaMemsetAsync(P->dDone, 0, sizeof(int) * clear, P->stream));
   CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
                     P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
-  CK(launch_fsm(a, P->stream, &launches));
+  int grid = 0;
+  CK(launch_fsm(a, P->stream, &launches, &grid));
+  out->grid_ctas = grid;
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
@@ -282,6 +331,7 @@ int plan_run(eik_plan* P, eik_output* out) {
   out->avhr = out->avs = out->mon_pct = 0.0;
   out->host_ms = 0.0;
   out->spec_hits = out->spec_waits = out->spec_self = 0;
+  out->grid_ctas = 0;
   CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
   int rc;
   switch (P->method) {
@@ -386,6 +436,121 @@ int plan_rows(eik_plan* P, int64_t row0, int64_t nrows, double* host_or_dev, int
     CK(cudaMemcpy2DAsync(host_or_dev, w, dev, dp, w, nrows,
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, P->stream));
   CK(cudaStreamSynchronize(P->stream));
+  return EIK_OK;
+}
+
+// Device split for plans sharing one GPU (eik_plan_run_batch), in SMs.
+// Fixed-size grids (FSM/FMM strips) may spread one CTA per SM, so they
+// count one SM per CTA; FMSM dataflows (a few ms alone) get 2 CTAs; plans
+// capped by the caller keep their cap; the heap-cell replays, whose CTAs
+// each hold a whole SM, split what is left equally.  Equal shares suit
+// them: each is bound by its committer's serial chain and runs within a few
+// % of its solo time once it holds ~16 SMs of workers (measured on C2), so
+// the batch ends with its longest solve.
+int batch_split(eik_plan* const* plans, int n) {
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plans[0]->device));
+  std::vector<int> dev(n), fixed(n);
+  double used = 0.0;
+  int flex = 0;
+  for (int k = 0; k < n; ++k) {
+    eik_plan* P = plans[k];
+    int rc = plan_capacity(P, &dev[k], &fixed[k]);
+    if (rc) return rc;
+    if (dev[k] < 1) return fail(EIK_ERR_CUDA, "batch: a kernel does not fit on the device");
+    P->run_cap = 0;
+    if (fixed[k] > 0) {
+      used += std::min(sms, fixed[k]);
+    } else if (P->ctas_cap > 0) {
+      used += (double)std::min(P->ctas_cap, dev[k]) * sms / dev[k];
+    } else if (P->method == EIK_FMSM) {
+      P->run_cap = 2;
+      used += std::min(2.0, 2.0 * sms / dev[k]);
+    } else {
+      ++flex;
+    }
+  }
+  const double room = std::max(0.0, 0.98 * sms - used);
+  for (int k = 0; k < n; ++k) {
+    eik_plan* P = plans[k];
+    if (fixed[k] > 0 || P->ctas_cap > 0 || P->method == EIK_FMSM) continue;
+    P->run_cap = std::max(2, (int)std::floor(room / flex * dev[k] / sms));
+  }
+  return EIK_OK;
+}
+
+int plan_run_batch(eik_plan* const* plans, int n, eik_output* outs, double* batch_ms) {
+  for (int k = 0; k < n; ++k) {
+    if (!plans[k]) return fail(EIK_ERR_DOMAIN, "batch: null plan");
+    for (int j = 0; j < k; ++j)
+      if (plans[j] == plans[k]) return fail(EIK_ERR_DOMAIN, "batch: a plan appears twice");
+    if (plans[k]->device != plans[0]->device)
+      return fail(EIK_ERR_CONFIG, "batch: plans on different devices");
+  }
+  int rc = batch_split(plans, n);
+  if (rc) return rc;
+  const int device = plans[0]->device;
+  CK(cudaSetDevice(device));
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t ref;
+  CK(cudaEventCreate(&ref));
+  CK(cudaEventRecord(ref, plans[0]->stream));
+  CK(cudaEventSynchronize(ref));
+  std::vector<int> codes(n, EIK_OK);
+  std::vector<std::string> msgs(n);
+  {
+    // The SM-exclusive heap-cell grids are submitted first; the other plans
+    // (whose small CTAs would otherwise spread over the SMs those grids
+    // need) start once every heap-cell thread has issued its launches.
+    std::mutex mu;
+    std::condition_variable cv;
+    int hc_pending = 0;
+    for (int k = 0; k < n; ++k)
+      if (plans[k]->method == EIK_HCM || plans[k]->method == EIK_FHCM) ++hc_pending;
+    auto launched = [&]() {
+      std::lock_guard<std::mutex> lk(mu);
+      if (--hc_pending == 0) cv.notify_all();
+    };
+    std::vector<std::thread> th;
+    th.reserve(n);
+    for (int k = 0; k < n; ++k) {
+      eik_plan* P = plans[k];
+      const bool hc = P->method == EIK_HCM || P->method == EIK_FHCM;
+      th.emplace_back([&, k, P, hc]() {
+        cudaSetDevice(device);
+        if (hc) {
+          P->on_launched = launched;
+        } else {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&]() { return hc_pending == 0; });
+        }
+        codes[k] = plan_run(P, &outs[k]);
+        if (codes[k]) msgs[k] = g_last_error;  // thread-local: carry it back
+        if (hc && P->on_launched) {             // failed before its launch
+          P->on_launched = nullptr;
+          launched();
+        }
+      });
+    }
+    for (auto& t : th) t.join();
+  }
+  for (int k = 0; k < n; ++k) plans[k]->run_cap = 0;
+  double t_end = 0.0;
+  cudaError_t e = cudaSuccess;
+  const bool trace = std::getenv("EIK_BATCH_TRACE") != nullptr;
+  for (int k = 0; k < n && e == cudaSuccess; ++k) {
+    float ms = 0.f, ms0 = 0.f;
+    if (codes[k] == EIK_OK) e = cudaEventElapsedTime(&ms, ref, plans[k]->ev1);
+    if (trace && codes[k] == EIK_OK && cudaEventElapsedTime(&ms0, ref, plans[k]->ev0) == cudaSuccess)
+      std::fprintf(stderr, "batch plan %d method %d ctas %lld: %.1f -> %.1f ms\n", k,
+                   plans[k]->method, (long long)outs[k].grid_ctas, ms0, ms);
+    t_end = std::max(t_end, (double)ms);
+  }
+  cudaEventDestroy(ref);
+  for (int k = 0; k < n; ++k)
+    if (codes[k]) return fail(codes[k], "batch plan " + std::to_string(k) + ": " + msgs[k]);
+  if (e != cudaSuccess) return cuda_fail(e, "batch timing");
+  if (batch_ms) *batch_ms = t_end;
   return EIK_OK;
 }
 
@@ -542,6 +707,68 @@ int eik_plan_set_rows(eik_plan* P, int64_t row0, int64_t nrows, const double* sr
                       int32_t on_device) {
   if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
   return plan_rows(P, row0, nrows, const_cast<double*>(src), on_device, true);
+}
+
+int eik_plan_set_ctas(eik_plan* P, int32_t max_ctas) {
+  if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
+  if (max_ctas < 0) return fail(EIK_ERR_CONFIG, "max_ctas must be >= 0");
+  P->ctas_cap = max_ctas;
+  return EIK_OK;
+}
+
+int eik_plan_capacity(eik_plan* P, int32_t* device_ctas, int32_t* fixed_ctas) {
+  if (!P || !device_ctas || !fixed_ctas) return fail(EIK_ERR_DOMAIN, "null argument");
+  int d = 0, f = 0;
+  int rc = plan_capacity(P, &d, &f);
+  if (rc) return rc;
+  *device_ctas = d;
+  *fixed_ctas = f;
+  return EIK_OK;
+}
+
+int eik_plan_run_batch(eik_plan* const* plans, int32_t n, eik_output* outs, double* batch_ms) {
+  g_last_code = EIK_OK;
+  g_last_error.clear();
+  if (n < 0 || (n > 0 && (!plans || !outs))) return fail(EIK_ERR_DOMAIN, "batch: bad arguments");
+  if (n == 0) {
+    if (batch_ms) *batch_ms = 0.0;
+    return EIK_OK;
+  }
+  return plan_run_batch(plans, n, outs, batch_ms);
+}
+
+int eik_solve_batch(const eik_problem* const* problems, const eik_cells* const* cells,
+                    const int32_t* methods, int32_t n, eik_output* outs, double* batch_ms) {
+  g_last_code = EIK_OK;
+  g_last_error.clear();
+  if (n < 0 || (n > 0 && (!problems || !methods || !outs)))
+    return fail(EIK_ERR_DOMAIN, "batch: bad arguments");
+  for (int k = 0; k < n; ++k)
+    if (!outs[k].u) return fail(EIK_ERR_DOMAIN, "output needs a u buffer");
+  int device = 0;
+  CK(cudaGetDevice(&device));
+  std::vector<eik_plan*> plans(n, nullptr);
+  std::vector<int> codes(n, EIK_OK);
+  std::vector<std::string> msgs(n);
+  {  // uploads overlap: one host thread per problem
+    std::vector<std::thread> th;
+    for (int k = 0; k < n; ++k)
+      th.emplace_back([&, k]() {
+        cudaSetDevice(device);
+        plans[k] = eik_plan_create(problems[k], cells ? cells[k] : nullptr, methods[k]);
+        if (!plans[k]) {
+          codes[k] = g_last_code != EIK_OK ? g_last_code : EIK_ERR_CUDA;
+          msgs[k] = g_last_error;
+        }
+      });
+    for (auto& t : th) t.join();
+  }
+  int rc = EIK_OK;
+  for (int k = 0; k < n && !rc; ++k)
+    if (codes[k]) rc = fail(codes[k], "batch problem " + std::to_string(k) + ": " + msgs[k]);
+  if (!rc) rc = plan_run_batch(plans.data(), n, outs, batch_ms);
+  for (eik_plan* P : plans) plan_free(P);
+  return rc;
 }
 
 int eik_solve(const eik_problem* p, const eik_cells* c, int32_t method, eik_output* out) {

@@ -58,7 +58,12 @@ struct FmsmArgs {
   int max_cell_sweeps;
 };
 
-cudaError_t launch_fmsm(const FmsmArgs& a, int warps_per_cta, cudaStream_t s, int* launches);
+// max_ctas caps the persistent grid (0: the whole device) so that plans can
+// share a GPU (eik_plan_run_batch); *_capacity report the CTAs the whole
+// device holds for that kernel configuration.
+cudaError_t launch_fmsm(const FmsmArgs& a, int warps_per_cta, int max_ctas, cudaStream_t s,
+                        int* launches, int* grid = nullptr);
+cudaError_t fmsm_capacity(int64_t tile_doubles, int warps_per_cta, int* ctas);
 
 // Result of processing one cell (sweeps + the four border scans), produced by
 // a worker speculatively and applied by the committer.
@@ -92,6 +97,7 @@ struct HcArgs {
   int* done_flag;
   int* hsize_pub;           // per-bucket queue counts for the workers, bucket b at [32 b]
   int64_t tile_doubles;     // per-warp smem
+  int64_t min_smem;         // launch at least this much dynamic smem per CTA (SM-exclusive CTAs)
   int heap_cap;             // >0: committer queue buckets in shared memory, capacity
                             // per bucket; 0: buckets in global memory (hkey + harr)
   int heap_capb_global;     // bucket capacity of the global layout (ceil(J/32))
@@ -118,13 +124,20 @@ struct HcArgs {
 size_t heapcell_smem_bytes(const CellGeom& g, int max_len);
 size_t heapcell_committer_heap_bytes(int cap);
 cudaError_t launch_heapcell(const HcArgs& a, int warps_per_cta, int max_ctas, cudaStream_t s,
-                            int* launches);
+                            int* launches, int* grid = nullptr);
+cudaError_t heapcell_capacity(int64_t tile_doubles, int heap_cap, int warps_per_cta,
+                              size_t min_smem, int* ctas);
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` (never
+// lowers it: concurrent launches of the same kernel from other host threads
+// may need the larger limit).
+cudaError_t ensure_dynamic_smem(const void* kernel, size_t bytes);
 
 cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int64_t n,
                            int64_t P, int64_t pad, double h, const int64_t* exits,
                            const double* cost, int64_t n_exit, int* status, cudaStream_t s,
                            int* launches);
-cudaError_t launch_fsm(const FsmArgs& a, cudaStream_t s, int* launches);
+cudaError_t launch_fsm(const FsmArgs& a, cudaStream_t s, int* launches, int* grid = nullptr);
+cudaError_t fsm_capacity(int nstrips, int* need, int* ctas);
 
 cudaError_t device_metrics(const double* vm, const double* ve, const double* vt, int64_t M,
                            const int64_t* exits, int64_t n_exit, uint8_t* mask, cudaStream_t s,

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -72,7 +73,16 @@ struct eik_plan {
   eikb200::SpecRec* dRec = nullptr;
   int* dHcMisc = nullptr;   // [0] done flag, [1] published heap size
   int hc_warps_per_cta = 1;
+  int64_t hc_min_smem = 0;  // dynamic smem floor per CTA (one CTA per SM)
   int hc_max_ctas = 1;
+  // CTA cap of the persistent kernel (0 = the whole device): ctas_cap set by
+  // eik_plan_set_ctas, run_cap by eik_plan_run_batch's device split for one run
+  int ctas_cap = 0;
+  int run_cap = 0;
+
+  int cap() const { return run_cap > 0 ? run_cap : ctas_cap; }
+  // batch runs: called (then cleared) once the heap-cell grid is submitted
+  std::function<void()> on_launched;
 };
 
 namespace eikb200 {
@@ -103,6 +113,10 @@ int dalloc(T** p, size_t count) {
 }
 
 int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c);
+// CTAs of the plan's persistent kernel the whole device holds (*device) and,
+// for kernels whose grid size is fixed (FSM/FMM strips), that size (*fixed,
+// else 0).
+int plan_capacity(eik_plan* P, int* device, int* fixed);
 int plan_run_fmsm(eik_plan* P, eik_output* out);
 int plan_run_heapcell(eik_plan* P, eik_output* out);
 

@@ -137,13 +137,19 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     // per-warp tile: values + costs with halo, 4 border snapshots, lock bytes
     const size_t tile = ((smem + sizeof(double) - 1) / sizeof(double) + 1) & ~(size_t)1;
     P->cg.tile_doubles = (int64_t)tile;
-    const int fit = (int)std::max<size_t>(1, std::min<size_t>(8, kTileBudget / (tile * 8)));
-    // worker warps per SM: 1-8 measured within 2 % of each other on C2, 2 the
-    // best (one warp per scheduler pair keeps each speculation's latency
-    // short); EIK_HC_WARPS overrides within what shared memory fits
-    P->hc_warps_per_cta = std::min(fit, 2);
+    // One CTA per SM: up to 8 warps (their tiles within 216 KB) and a shared-
+    // memory floor above half the SM, so no second CTA of this or another
+    // smem-using kernel lands on the SM (8 warps x 250 registers also fill the
+    // register file).  The committer (CTA 0) then has its SM to itself, and
+    // plans sharing the GPU (eik_plan_run_batch) split it by whole SMs.
+    // Solo times within 3 % of 2-warp CTAs packed 1-4 per SM.
+    // EIK_HC_WARPS / EIK_HC_MIN_SMEM override.
+    const int fit = (int)std::max<size_t>(1, std::min<size_t>(8, (216 * 1024) / (tile * 8)));
+    P->hc_warps_per_cta = fit;
     if (const char* w = std::getenv("EIK_HC_WARPS"))
       P->hc_warps_per_cta = std::max(1, std::min(fit, std::atoi(w)));
+    P->hc_min_smem = 116 * 1024;
+    if (const char* w = std::getenv("EIK_HC_MIN_SMEM")) P->hc_min_smem = std::atol(w);
     // the committer's heap + cell values go to its shared memory when they
     // fit next to its tile (uint16 heap indices)
     {
@@ -243,7 +249,9 @@ int plan_run_fmsm(eik_plan* P, eik_output* out) {
   a.status = P->dStatus;
   a.J = (int)J;
   a.max_cell_sweeps = 1 << 20;
-  CK(launch_fmsm(a, P->warps_per_cta, P->stream, &launches));
+  int grid = 0;
+  CK(launch_fmsm(a, P->warps_per_cta, P->cap(), P->stream, &launches, &grid));
+  out->grid_ctas = grid;
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];
   unsigned long long cnt[2];
@@ -372,8 +380,17 @@ retry:  // after a committer heap overflow, with the heap in global memory
   a.heap_capb_global = P->hc_capb_global;
   a.pub_capb = P->hc_heap_cap > 0 ? P->hc_heap_cap : P->hc_capb_global;
   a.tile_doubles = P->cg.tile_doubles;
+  a.min_smem = P->hc_min_smem;
   CK(cudaMemsetAsync(P->dHcMisc, 0, sizeof(int) * (32 + 32 * 32), P->stream));
-  CK(launch_heapcell(a, P->hc_warps_per_cta, P->hc_max_ctas, P->stream, &launches));
+  const int hc_ctas = P->cap() > 0 ? std::min(P->hc_max_ctas, P->cap()) : P->hc_max_ctas;
+  int grid = 0;
+  CK(launch_heapcell(a, P->hc_warps_per_cta, hc_ctas, P->stream, &launches, &grid));
+  out->grid_ctas = grid;
+  if (P->on_launched) {
+    auto f = std::move(P->on_launched);
+    P->on_launched = nullptr;
+    f();
+  }
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];
   unsigned long long cnt[48];

@@ -143,10 +143,9 @@ __global__ void fmsm_dataflow_kernel(FmsmArgs a) {
 
 }  // namespace
 
-cudaError_t launch_fmsm(const FmsmArgs& args, int warps_per_cta, cudaStream_t s, int* launches) {
-  const size_t smem = (size_t)warps_per_cta * args.g.tile_doubles * sizeof(double);
-  cudaError_t e = cudaFuncSetAttribute(fmsm_dataflow_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+cudaError_t fmsm_capacity(int64_t tile_doubles, int warps_per_cta, int* ctas) {
+  const size_t smem = (size_t)warps_per_cta * tile_doubles * sizeof(double);
+  cudaError_t e = ensure_dynamic_smem((const void*)fmsm_dataflow_kernel, smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -154,10 +153,21 @@ cudaError_t launch_fmsm(const FmsmArgs& args, int warps_per_cta, cudaStream_t s,
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fmsm_dataflow_kernel,
                                                     32 * warps_per_cta, smem);
   if (e != cudaSuccess) return e;
-  if (per_sm < 1) return cudaErrorInvalidConfiguration;
-  int ctas = per_sm * sms;
+  *ctas = per_sm * sms;
+  return cudaSuccess;
+}
+
+cudaError_t launch_fmsm(const FmsmArgs& args, int warps_per_cta, int max_ctas, cudaStream_t s,
+                        int* launches, int* grid) {
+  const size_t smem = (size_t)warps_per_cta * args.g.tile_doubles * sizeof(double);
+  int ctas = 0;
+  cudaError_t e = fmsm_capacity(args.g.tile_doubles, warps_per_cta, &ctas);
+  if (e != cudaSuccess) return e;
+  if (ctas < 1) return cudaErrorInvalidConfiguration;
   const int need = (args.J + warps_per_cta - 1) / warps_per_cta;
   if (ctas > need) ctas = need;
+  if (max_ctas > 0 && ctas > max_ctas) ctas = max_ctas;
+  if (grid) *grid = ctas;
   FmsmArgs a = args;
   void* params[] = {&a};
   // workers spin on each other's cells: all CTAs must be co-resident

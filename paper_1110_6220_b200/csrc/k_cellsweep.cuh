@@ -254,54 +254,66 @@ __device__ __forceinline__ bool cell_sweep_lock(const CellTile& T, int dir, int 
       lk[r] = q_lk[r];
     }
     load(s + 1);  // prefetch while this step computes (past the end: harmless)
-    // previous-step values: slot r's lane 0 takes slot r-1's lane 31
-    double wv_old[NS];
-    unsigned nm_old[NS];
-#pragma unroll
-    for (int r = 0; r < NS; ++r) {
-      wv_old[r] = wv[r];
-      nm_old[r] = nm[r];
-    }
+    // phase 1, every slot: the upwind row's new value and unlock bit, and
+    // whether the slot processes a node.  The slots' fp64 chains are
+    // independent, so they are computed together (phase 2) and overlap;
+    // the stores and ballots follow (phase 3).
+    double sv[NS], cand[NS];
+    bool act[NS], proc[NS];
+    bool any = false;
 #pragma unroll
     for (int r = 0; r < NS; ++r) {
       const int b = lane + 32 * r;
       const int a = s - b;
-      const bool act = rv[r] && a >= 0 && a < w;
-      const double send = (lane == 31 && r > 0) ? wv_old[r > 0 ? r - 1 : 0] : wv_old[r];
-      double sv = __shfl_sync(kFull, send, (lane + 31) & 31);
-      unsigned sbit = lane == 0 ? (r > 0 ? (nm_old[r > 0 ? r - 1 : 0] >> 31) & 1u : 0u)
-                                : (nm_old[r] >> (lane - 1)) & 1u;
+      act[r] = rv[r] && a >= 0 && a < w;
+      // previous-step values: slot r's lane 0 takes slot r-1's lane 31
+      const double send = (lane == 31 && r > 0) ? wv[r > 0 ? r - 1 : 0] : wv[r];
+      sv[r] = __shfl_sync(kFull, send, (lane + 31) & 31);
+      unsigned sbit = lane == 0 ? (r > 0 ? (nm[r > 0 ? r - 1 : 0] >> 31) & 1u : 0u)
+                                : (nm[r] >> (lane - 1)) & 1u;
       if (b == 0) {
-        sv = hs[r];
+        sv[r] = hs[r];
         sbit = 0u;
       }
-      const bool proc = act && cc[r] >= 0.0 && (lk[r] != 0 || unW[r] || sbit != 0u);
-      bool un_n = false, nunW = false;
-      double res = cur[r];
-      if (!SKIP || __any_sync(kFull, proc)) {
-        const int o = act ? vb[r] + dx * a : pu + ox;
-        const int lo = act ? lb[r] + dx * a : 0;
-        const double cand = node_update4(e[r], wv[r], n[r], sv, cc[r]);
-        const bool dec = proc && cand < cur[r];
-        res = dec ? cand : cur[r];
-        if (dec) {
-          changed = true;
-          U[o] = cand;
-          // already-processed W and S neighbours: unlocked for the next sweep
-          if (a > 0 && cw[r] >= 0.0 && wv[r] > cand) L[lo - dx] = 1;
-          if (b > 0 && cs[r] >= 0.0 && sv > cand) L[lo - dyl] = 1;
-        }
-        un_n = dec && (b + 1 < h) && cn[r] >= 0.0 && n[r] > cand;
-        nunW = dec && (a + 1 < w) && ce[r] >= 0.0 && e[r] > cand;
-        if (proc) {  // relock on processing (heap_cell.cpp:110-111)
-          L[lo] = 0;
-          ++updates;
-        }
+      proc[r] = act[r] && cc[r] >= 0.0 && (lk[r] != 0 || unW[r] || sbit != 0u);
+      any = any || proc[r];
+    }
+    if (SKIP && !__any_sync(kFull, any)) {
+#pragma unroll
+      for (int r = 0; r < NS; ++r) {
+        unW[r] = false;
+        nm[r] = 0u;
+        if (act[r]) wv[r] = cur[r];
+        cw[r] = act[r] ? cc[r] : -1.0;
       }
-      unW[r] = nunW;
+      continue;
+    }
+#pragma unroll
+    for (int r = 0; r < NS; ++r) cand[r] = node_update4(e[r], wv[r], n[r], sv[r], cc[r]);
+#pragma unroll
+    for (int r = 0; r < NS; ++r) {
+      const int b = lane + 32 * r;
+      const int a = s - b;
+      const int o = act[r] ? vb[r] + dx * a : pu + ox;
+      const int lo = act[r] ? lb[r] + dx * a : 0;
+      const bool dec = proc[r] && cand[r] < cur[r];
+      const double res = dec ? cand[r] : cur[r];
+      if (dec) {
+        changed = true;
+        U[o] = cand[r];
+        // already-processed W and S neighbours: unlocked for the next sweep
+        if (a > 0 && cw[r] >= 0.0 && wv[r] > cand[r]) L[lo - dx] = 1;
+        if (b > 0 && cs[r] >= 0.0 && sv[r] > cand[r]) L[lo - dyl] = 1;
+      }
+      const bool un_n = dec && (b + 1 < h) && cn[r] >= 0.0 && n[r] > cand[r];
+      unW[r] = dec && (a + 1 < w) && ce[r] >= 0.0 && e[r] > cand[r];
+      if (proc[r]) {  // relock on processing (heap_cell.cpp:110-111)
+        L[lo] = 0;
+        ++updates;
+      }
       nm[r] = __ballot_sync(kFull, un_n);
-      if (act) wv[r] = res;
-      cw[r] = act ? cc[r] : -1.0;
+      if (act[r]) wv[r] = res;
+      cw[r] = act[r] ? cc[r] : -1.0;
     }
   }
   __syncwarp();  // the next sweep / the scans read this sweep's stores

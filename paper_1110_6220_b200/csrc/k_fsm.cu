@@ -285,8 +285,21 @@ cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int
   return cudaGetLastError();
 }
 
-cudaError_t launch_fsm(const FsmArgs& args, cudaStream_t s, int* launches) {
+cudaError_t fsm_capacity(int nstrips, int* need, int* ctas) {
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, fsm_wavefront_kernel, 32 * kWarpsPerCta, 0);
+  if (e != cudaSuccess) return e;
+  *need = (nstrips + kWarpsPerCta - 1) / kWarpsPerCta;
+  *ctas = per_sm * sms;
+  return cudaSuccess;
+}
+
+cudaError_t launch_fsm(const FsmArgs& args, cudaStream_t s, int* launches, int* grid) {
   const int ctas = (args.nstrips + kWarpsPerCta - 1) / kWarpsPerCta;
+  if (grid) *grid = ctas;
   FsmArgs a = args;
   void* params[] = {&a};
   // Strips spin on each other's progress, so every CTA must be co-resident:

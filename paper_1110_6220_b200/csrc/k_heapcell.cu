@@ -1284,19 +1284,42 @@ size_t heapcell_committer_heap_bytes(int capb) {
   return (size_t)32 * capb * (sizeof(double) + 4) + 32 * (sizeof(double) + 12);
 }
 
+namespace {
+size_t heapcell_launch_smem(int64_t tile_doubles, int heap_cap, int warps_per_cta,
+                            size_t min_smem) {
+  size_t smem = (size_t)warps_per_cta * tile_doubles * sizeof(double);
+  smem = std::max(smem, tile_doubles * sizeof(double) +
+                            heapcell_committer_heap_bytes(heap_cap > 0 ? heap_cap : 0));
+  return std::max(smem, min_smem);
+}
+}  // namespace
+
+cudaError_t heapcell_capacity(int64_t tile_doubles, int heap_cap, int warps_per_cta,
+                              size_t min_smem, int* ctas) {
+  const size_t smem = heapcell_launch_smem(tile_doubles, heap_cap, warps_per_cta, min_smem);
+  const void* kern = (const void*)heapcell_spec_kernel<false>;
+  cudaError_t e = ensure_dynamic_smem(kern, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps_per_cta, smem);
+  if (e != cudaSuccess) return e;
+  *ctas = per_sm * sms;
+  return cudaSuccess;
+}
+
 cudaError_t launch_heapcell(const HcArgs& args, int warps_per_cta, int max_ctas, cudaStream_t s,
-                            int* launches) {
+                            int* launches, int* grid) {
   const int64_t total = (int64_t)args.J * args.cellsz;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
   heapcell_init_kernel<<<blocks, 256, 0, s>>>(args);
-  size_t smem = (size_t)warps_per_cta * args.tile_doubles * sizeof(double);
-  smem = std::max(smem, args.tile_doubles * sizeof(double) +
-                           heapcell_committer_heap_bytes(args.heap_cap > 0 ? args.heap_cap : 0));
+  const size_t smem =
+      heapcell_launch_smem(args.tile_doubles, args.heap_cap, warps_per_cta, (size_t)args.min_smem);
   // the instrumented instantiation only when EIK_HC_PROFILE asked for it
   const void* kern = args.prof ? (const void*)heapcell_spec_kernel<true>
                                : (const void*)heapcell_spec_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(kern,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_dynamic_smem(kern, smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -1307,6 +1330,7 @@ cudaError_t launch_heapcell(const HcArgs& args, int warps_per_cta, int max_ctas,
   if (per_sm < 1) return cudaErrorInvalidConfiguration;
   int ctas = std::min(per_sm * sms, max_ctas);
   if (ctas < 1) ctas = 1;
+  if (grid) *grid = ctas;
   HcArgs a = args;
   void* params[] = {&a};
   e = cudaLaunchCooperativeKernel(kern, dim3(ctas),

@@ -49,6 +49,7 @@ class SolverOutput:
     host_ms: float = 0.0
     kernel_launches: int = 0
     spec: tuple = (0, 0, 0)  # heap-cell replay: (hits, waits, self-processed)
+    ctas: int = 0            # CTAs of the persistent solve kernel
 
     def at(self, i: int, j: int) -> float:
         return float(self.values[j * self.m + i])
@@ -98,7 +99,8 @@ def _pack(out: N.eik_output, values: np.ndarray, g) -> SolverOutput:
                                            out.cell_sweeps, out.mon_checks, out.mon_single),
                         device_ms=out.device_ms, host_ms=out.host_ms,
                         kernel_launches=out.kernel_launches,
-                        spec=(out.spec_hits, out.spec_waits, out.spec_self))
+                        spec=(out.spec_hits, out.spec_waits, out.spec_self),
+                        ctas=out.grid_ctas)
 
 
 def solve(problem: Problem, method: str, cells: Optional[CellDecomposition] = None,
@@ -171,6 +173,16 @@ class Plan:
         N.raise_for(N.lib.eik_plan_run(self._h, C.byref(out)))
         return _pack(out, u_host, self.problem.grid)
 
+    def set_ctas(self, max_ctas: int) -> None:
+        """Cap the CTAs of this plan's persistent kernel (0 = whole device)."""
+        N.raise_for(N.lib.eik_plan_set_ctas(self._h, int(max_ctas)))
+
+    def capacity(self):
+        """(CTAs of the persistent kernel the device holds, fixed grid or 0)."""
+        d, f = C.c_int32(), C.c_int32()
+        N.raise_for(N.lib.eik_plan_capacity(self._h, C.byref(d), C.byref(f)))
+        return d.value, f.value
+
     def values_ptr(self) -> int:
         return N.lib.eik_plan_values(self._h)
 
@@ -188,3 +200,47 @@ class Plan:
 
     def __del__(self):
         self.close()
+
+
+def run_batch(plans, u_hosts=None):
+    """Run distinct plans concurrently on their device (eik_plan_run_batch):
+    the device-side counterpart of the reference's --jobs thread pool
+    (experiment.cpp:284-310).  Returns (outputs, batch device ms)."""
+    n = len(plans)
+    outs = (N.eik_output * n)()
+    for k in range(n):
+        outs[k].u = N.dptr(u_hosts[k] if u_hosts is not None else None)
+        outs[k].u_on_device = 0
+    hs = (C.c_void_p * n)(*[p._h for p in plans])
+    ms = C.c_double()
+    N.raise_for(N.lib.eik_plan_run_batch(hs, n, outs, C.byref(ms)))
+    return [_pack(outs[k], u_hosts[k] if u_hosts is not None else None, plans[k].problem.grid)
+            for k in range(n)], ms.value
+
+
+def solve_batch(jobs, outs=None):
+    """Several solve() calls at once (eik_solve_batch): jobs are
+    (problem, method, cells, tables) tuples (cells/tables None for FMM/FSM);
+    `outs` optional caller-owned float64 buffers.  Returns (outputs, batch
+    device ms)."""
+    n = len(jobs)
+    keep, pp, cc, us = [], (C.POINTER(N.eik_problem) * n)(), (C.POINTER(N.eik_cells) * n)(), []
+    meth = (C.c_int32 * n)()
+    res = (N.eik_output * n)()
+    for k, (problem, method, cells, tables) in enumerate(jobs):
+        F = problem.sampled_speed()
+        p, kp = _c_problem(problem, F)
+        if cells is not None and tables is None:
+            tables = cell_tables(problem, cells)
+        c, kc = _c_cells(cells, tables)
+        keep += [p, kp, c, kc]
+        pp[k] = C.pointer(p)
+        cc[k] = C.pointer(c) if c is not None else C.POINTER(N.eik_cells)()
+        meth[k] = N.METHOD_NAMES[method]
+        u = outs[k] if outs is not None else np.empty(problem.grid.size(), dtype=np.float64)
+        us.append(u)
+        res[k].u = N.dptr(u)
+        res[k].u_on_device = 0
+    ms = C.c_double()
+    N.raise_for(N.lib.eik_solve_batch(pp, cc, meth, n, res, C.byref(ms)))
+    return [_pack(res[k], us[k], jobs[k][0].grid) for k in range(n)], ms.value

@@ -3,6 +3,10 @@ import sys
 
 import pytest
 
+# concurrent solves (tests/test_gpu_batch.py) want one hardware queue per
+# stream; set before anything creates the CUDA context
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
