@@ -74,6 +74,7 @@ struct eik_plan {
   int* dHcMisc = nullptr;   // [0] done flag, [1] published heap size
   int hc_warps_per_cta = 1;
   int64_t hc_min_smem = 0;  // dynamic smem floor per CTA (one CTA per SM)
+  uint64_t hc_cx_magic = 0; // cell id -> row by multiply-shift (0: division)
   int hc_max_ctas = 1;
   // CTA cap of the persistent kernel (0 = the whole device): ctas_cap set by
   // eik_plan_set_ctas, run_cap by eik_plan_run_batch's device split for one run

@@ -149,6 +149,14 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     if (const char* w = std::getenv("EIK_HC_WARPS"))
       P->hc_warps_per_cta = std::max(1, std::min(fit, std::atoi(w)));
     P->hc_min_smem = 116 * 1024;
+    {  // row of a cell id by a multiply and shift, checked for every id
+      const uint64_t d = (uint64_t)P->cells_x;
+      uint64_t magic = ((1ull << 40) + d - 1) / d;
+      if (J > 1 && (uint64_t)(J - 1) > ~0ull / magic) magic = 0;
+      for (int64_t c = 0; magic && c < J; ++c)
+        if ((((uint64_t)c * magic) >> 40) != (uint64_t)c / d) magic = 0;
+      P->hc_cx_magic = magic;
+    }
     if (const char* w = std::getenv("EIK_HC_MIN_SMEM")) P->hc_min_smem = std::atol(w);
     // the committer's heap + cell values go to its shared memory when they
     // fit next to its tile (uint16 heap indices)
@@ -381,6 +389,7 @@ retry:  // after a committer heap overflow, with the heap in global memory
   a.pub_capb = P->hc_heap_cap > 0 ? P->hc_heap_cap : P->hc_capb_global;
   a.tile_doubles = P->cg.tile_doubles;
   a.min_smem = P->hc_min_smem;
+  a.cx_magic = P->hc_cx_magic;
   CK(cudaMemsetAsync(P->dHcMisc, 0, sizeof(int) * (32 + 32 * 32), P->stream));
   const int hc_ctas = P->cap() > 0 ? std::min(P->hc_max_ctas, P->cap()) : P->hc_max_ctas;
   int grid = 0;
@@ -423,10 +432,10 @@ retry:  // after a committer heap overflow, with the heap in global memory
                  "heapcell committer cycles: pop %llu obtain %llu self %llu commit %llu | self: "
                  "stage %llu sweeps %llu scans %llu | hits %llu (chained %llu) self %llu | "
                  "heap max %llu cap %d | stage: %llu reset_locks %llu steps %llu | commit: record %llu | "
-                 "obtain: rescan %llu first-rt %llu\n",
+                 "obtain: rescan %llu first-rt %llu waits %llu (%llu cycles)\n",
                  cnt[8], cnt[9], cnt[10], cnt[11], cnt[12], cnt[13], cnt[14], cnt[6], cnt[15],
                  cnt[5], cnt[38], P->hc_heap_cap, cnt[39], cnt[40], cnt[41], cnt[42], cnt[43],
-                 cnt[44]);
+                 cnt[44], cnt[7], cnt[45]);
   if (std::getenv("EIK_HC_PROFILE"))
     std::fprintf(stderr,
                  "heapcell misses: unchained %llu pending %llu stale %llu wrong-inst %llu "

@@ -131,6 +131,14 @@ __device__ __forceinline__ bool tag_is(unsigned sv, unsigned v) {
 // global memory (pos[], needed only for the popped cell's 4 neighbours,
 // prefetched with the rest of the commit and tracked through moves).  The
 // bucket arrays and counts are mirrored to global memory for the workers.
+// Cell id -> (column, row) without an integer division: q = (id * magic)
+// >> 40, exact for every id < J (the host checks all of them and passes 0
+// when it is not, which falls back to the division).
+__device__ __forceinline__ void cell_xy(int cell, int cells_x, u64 magic, int& cx, int& cy) {
+  cy = magic ? (int)(((u64)(unsigned)cell * magic) >> 40) : cell / cells_x;
+  cx = cell - cy * cells_x;
+}
+
 struct BucketPQ {
   double* bk;     // [32][capb] keys
   int* bi;        // [32][capb] ids
@@ -139,35 +147,24 @@ struct BucketPQ {
   int* mi;        //      their ids (INT_MAX when empty)
   int* msl;       //      their slots
   int capb;
-  int cells_x;
   int* pos;       // global [J]: bucket << 24 | slot, -1 = not queued
   int* pub;       // global [32][capb] id mirror (null: bi is global already)
   int* pubcnt;    // global count mirror, bucket l at pubcnt[32 * l] (one line each)
-  int size;
-  bool overflow;
-  int trk[4], tps[4];  // tracked cells (the popped cell's neighbours) and positions
+  int size;       // entries (instrumented build only)
   __device__ static bool less(double ka, int ia, double kb, int ib) {
     return ka < kb || (ka == kb && ia < ib);
-  }
-  __device__ void track(int id, int enc) {
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (trk[t] == id) tps[t] = enc;
   }
   __device__ void set(int l, int s, double k, int id) {  // lane 0
     bk[l * capb + s] = k;
     bi[l * capb + s] = id;
     pos[id] = (l << 24) | s;
     if (pub) pub[l * capb + s] = id;
-    track(id, (l << 24) | s);
   }
-  __device__ int bucket_of(int id) const {
-    const int y = id / cells_x;
-    return (id - y * cells_x + 2 * y) & 31;
-  }
-  // one lane per bucket at a time; false when the bucket is full
-  __device__ bool insert(int id, double k) {
-    const int l = bucket_of(id), s = cnt[l];
+  // bucket of cell (x, y); its W/E/S/N neighbours sit in b-1, b+1, b-2, b+2
+  __device__ static int bucket_xy(int x, int y) { return (x + 2 * y) & 31; }
+  // one lane per bucket at a time; false when bucket l is full
+  __device__ bool insert(int id, double k, int l) {
+    const int s = cnt[l];
     if (s >= capb) return false;
     set(l, s, k, id);
     cnt[l] = s + 1;
@@ -189,10 +186,10 @@ struct BucketPQ {
       msl[l] = s;
     }
   }
-  // all lanes; removes the minimum and returns it (or -1 when empty) on
-  // every lane, with its bucket in w.  The bucket's cached minimum is stale
-  // until rescan(w): the committer overlaps that with its next loads.
-  __device__ int pop_min(int lane, int& w_out) {
+  // all lanes: the minimum's id (or -1 when empty) and its bucket in w_out;
+  // remove(w) takes it out, rescan(w) renews the bucket's cached minimum --
+  // the committer overlaps both with the loads the popped cell needs
+  __device__ int argmin(int lane, int& w_out) const {
     double kl = mk[lane];
     int il = mi[lane], wl = lane;
 #pragma unroll
@@ -206,19 +203,18 @@ struct BucketPQ {
         wl = wo;
       }
     }
-    if (!(kl < kInf) && il == 0x7fffffff) return -1;  // every bucket empty
-    const int w = wl, top = il;
-    w_out = w;
+    w_out = wl;
+    return (!(kl < kInf) && il == 0x7fffffff) ? -1 : il;  // every bucket empty
+  }
+  __device__ void remove(int lane, int w, int top) {
     if (lane == 0) {
       const int s = msl[w], last = cnt[w] - 1;
       if (s != last) set(w, s, bk[w * capb + last], bi[w * capb + last]);
       cnt[w] = last;
       pubcnt[32 * w] = last;
       pos[top] = -1;
-      --size;
     }
     __syncwarp();
-    return top;
   }
   // all lanes: recompute bucket w's cached minimum
   __device__ void rescan(int lane, int w) {
@@ -403,9 +399,10 @@ __device__ void scan_all(const HcArgs& a, const HTile& T, const double* before,
   rec->mons[side] = mon_single;
 }
 
-__device__ __forceinline__ void hc_cell_rect(const CellGeom& g, int cell, int64_t& ib, int64_t& ie,
-                                             int64_t& jb, int64_t& je) {
-  const int cx = cell % g.cells_x, cy = cell / g.cells_x;
+__device__ __forceinline__ void hc_cell_rect(const CellGeom& g, u64 magic, int cell, int64_t& ib,
+                                             int64_t& ie, int64_t& jb, int64_t& je) {
+  int cx, cy;
+  cell_xy(cell, g.cells_x, magic, cx, cy);
   ib = (int64_t)cx * g.base_x;
   ie = (cx == g.cells_x - 1) ? g.m : ib + g.base_x;
   jb = (int64_t)cy * g.base_y;
@@ -431,10 +428,11 @@ __device__ __forceinline__ void process_cell(const HcArgs& a, HTile& T, double* 
   const long long p0 = prof ? clock64() : 0;
   const CellGeom& g = a.g;
   int64_t ib, ie, jb, je;
-  hc_cell_rect(g, cell, ib, ie, jb, je);
+  hc_cell_rect(g, a.cx_magic, cell, ib, ie, jb, je);
   T.w = (int)(ie - ib);
   T.h = (int)(je - jb);
-  const int cx = cell % g.cells_x, cy = cell / g.cells_x;
+  int cx, cy;
+  cell_xy(cell, g.cells_x, a.cx_magic, cx, cy);
   const int mw = a.spw;  // slot row pitch (even)
   const bool has_nb[4] = {cx > 0, cx + 1 < g.cells_x, cy > 0, cy + 1 < g.cells_y};
   const int nbs[4] = {cell - 1, cell + 1, cell - g.cells_x, cell + g.cells_x};
@@ -611,12 +609,15 @@ __device__ void publish(const HcArgs& a, int cell, int kind, u64 st, unsigned dm
 template <bool PROF>
 __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before, int lane) {
   const CellGeom& g = a.g;
+  bool ovf = false;  // a bucket filled up (per lane; voted once per pop)
   if (lane == 0) {
     for (int k = 0; k < a.n_init; ++k) {  // heap_cell.cpp:255-268
       const int cell = a.init_cells[k];
       a.cval[cell] = a.init_values[k];
-      if (H.insert(cell, a.init_values[k])) ++H.size;
-      else H.overflow = true;
+      int ix, iy;
+      cell_xy(cell, g.cells_x, a.cx_magic, ix, iy);
+      if (H.insert(cell, a.init_values[k], BucketPQ::bucket_xy(ix, iy))) ++H.size;
+      else ovf = true;
       a.ckey[cell] = a.init_values[k];
       if (a.fast) st_relaxed_u64(a.state + cell, (1ull << 32) | 0xFull);  // Q-cells: all flags
     }
@@ -625,21 +626,23 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
   long long removals = 0, sweeps = 0, updates = 0, mon_checks = 0, mon_single = 0;
   long long self_processed = 0, fast_hits = 0, waits = 0, chain_hits = 0;
   long long cyc_pop = 0, cyc_obtain = 0, cyc_self = 0, cyc_commit = 0, cyc_rec = 0;
-  long long cyc_rescan = 0, cyc_rt1 = 0;
+  long long cyc_rescan = 0, cyc_rt1 = 0, cyc_wait = 0;
   long long prof[6] = {0, 0, 0, 0, 0, 0};
   long long miss_cls[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int max_size = H.size;
   int prev_cell = -1;
   const unsigned* spec_p = a.spec_ver;
   const unsigned* spec_c = a.spec_ver + a.J;
+  bool over = false;
   for (;;) {
     long long t0 = PROF ? clock64() : 0;
-    const bool over = __shfl_sync(kFull, H.overflow ? 1 : 0, 0) != 0;
-    int wpop = 0;
-    const int cell = over ? -1 : H.pop_min(lane, wpop);
-    if (lane == 0 && cell >= 0) {
-        a.ckey[cell] = kInf;
+    // a full bucket dropped an entry: stop, the host reruns with global buckets
+    if (__any_sync(kFull, ovf)) {
+      over = true;
+      break;
     }
+    int wpop = 0;
+    const int cell = H.argmin(lane, wpop);
     long long t1 = PROF ? clock64() : 0;
     if (PROF) cyc_pop += t1 - t0;
     if (cell < 0) break;
@@ -648,7 +651,8 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       if (lane == 0) atomicExch(a.status, 3);
       break;
     }
-    const int cxi = cell % g.cells_x, cyi = cell / g.cells_x;
+    int cxi, cyi;
+    cell_xy(cell, g.cells_x, a.cx_magic, cxi, cyi);
     const int nbs[4] = {cxi > 0 ? cell - 1 : -1, cxi + 1 < g.cells_x ? cell + 1 : -1,
                         cyi > 0 ? cell - g.cells_x : -1, cyi + 1 < g.cells_y ? cell + g.cells_x : -1};
     // obtain a valid result: the plain speculation if its tag is the current
@@ -680,7 +684,12 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       svp0 = ld_relaxed_u32_nb(spec_p + cell);
       svc0 = ld_relaxed_u32_nb(spec_c + cell);
     }
-    H.rescan(lane, wpop);  // while those loads are in flight
+    // take the cell out of its bucket and renew that bucket's minimum while
+    // those loads are in flight (the neighbours sit in other buckets, so
+    // neither moves their prefetched positions)
+    H.remove(lane, wpop, cell);
+    if (lane == 0) a.ckey[cell] = kInf;
+    H.rescan(lane, wpop);
     const long long t1a = PROF ? clock64() : 0;
     if (PROF) cyc_rescan += t1a - t1;
     unsigned ctn[4];
@@ -692,7 +701,11 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       bool waited = false;
       bool first = true;
       const unsigned vchk = v;  // first use of the loaded state word
-      if (PROF) cyc_rt1 += (vchk == 0xFFFFFFFFu ? 1 : 0) + clock64() - t1a;
+      long long tw0 = 0;
+      if (PROF) {
+        tw0 = clock64();
+        cyc_rt1 += (vchk == 0xFFFFFFFFu ? 1 : 0) + tw0 - t1a;
+      }
       for (;;) {
         const unsigned svp = first ? svp0 : ld_relaxed_u32_nb(spec_p + cell);
         const unsigned svc = first ? svc0 : ld_relaxed_u32_nb(spec_c + cell);
@@ -786,6 +799,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       }
       if (mode == 0) ++fast_hits;
       if (waited) ++waits;
+      if (PROF && waited) cyc_wait += clock64() - tw0;
     }
     mode = __shfl_sync(kFull, mode, 0);
     st = __shfl_sync(kFull, st, 0);
@@ -811,7 +825,6 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       const int cur = st_cur(st), ps = st_pslot(st), qs = 3 - cur - ps;
       const int ncur = kind ? qs : ps, nps = kind ? ps : cur;
       int ins = 0;
-      bool ovf = false;
       if (lane < 4) {
         const int d = lane, nb = nbs[d];
         const double cand = __ldcg(&rec->cand[d]);
@@ -855,7 +868,9 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
               if (ms) ++mon_single;
             }
             if (my_pos < 0) {
-              if (H.insert(nb, cvd)) ++ins;
+              // the neighbour on side d sits in bucket wpop -1, +1, -2, +2
+              const int l = (wpop + (d < 2 ? 2 * d - 1 : 2 * (2 * d - 5))) & 31;
+              if (H.insert(nb, cvd, l)) ++ins;
               else ovf = true;
               moved = true;
             }
@@ -868,13 +883,13 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
                                            ((u64)ncur << sh));
         }
       }
-      ins += __shfl_xor_sync(kFull, ins, 1);
-      ins += __shfl_xor_sync(kFull, ins, 2);
-      const bool any_ovf = __any_sync(kFull, ovf);
-      if (lane == 0) {
-        H.size += ins;
-        if (any_ovf) H.overflow = true;
-            if (PROF && H.size > max_size) max_size = H.size;
+      if (PROF) {
+        ins += __shfl_xor_sync(kFull, ins, 1);
+        ins += __shfl_xor_sync(kFull, ins, 2);
+        if (lane == 0) {
+          H.size += ins - 1;
+          if (H.size > max_size) max_size = H.size;
+        }
       }
     }
     __syncwarp();
@@ -912,18 +927,21 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     a.counters[42] = cyc_rec;
     a.counters[43] = cyc_rescan;
     a.counters[44] = cyc_rt1;
+    a.counters[45] = cyc_wait;
     for (int k = 0; k < 8; ++k) a.counters[16 + k] = miss_cls[k];
     a.counters[38] = (unsigned long long)max_size;
   }
   if (lane == 0) {
-    if (H.overflow) atomicExch(a.status, 6);
+    if (over) atomicExch(a.status, 6);
     __threadfence();
     st_release_s32(a.done_flag, 1);
   }
 }
 
-__device__ __forceinline__ void cell_nbs(const CellGeom& g, int cell, int nbs[4]) {
-  const int cx = cell % g.cells_x, cy = cell / g.cells_x;
+__device__ __forceinline__ void cell_nbs(const HcArgs& a, int cell, int nbs[4]) {
+  const CellGeom& g = a.g;
+  int cx, cy;
+  cell_xy(cell, g.cells_x, a.cx_magic, cx, cy);
   nbs[0] = cx > 0 ? cell - 1 : -1;
   nbs[1] = cx + 1 < g.cells_x ? cell + 1 : -1;
   nbs[2] = cy > 0 ? cell - g.cells_x : -1;
@@ -956,7 +974,7 @@ __device__ bool chain_dead(const HcArgs& a, int x, unsigned svc, u64 st, const i
 // neighbours expected first), else y's plain result if valid; -1 if none.
 __device__ int pick_kind(const HcArgs& a, int y, u64 sty) {
   int nby[4];
-  cell_nbs(a.g, y, nby);
+  cell_nbs(a, y, nby);
   const unsigned svc = ld_relaxed_u32(a.spec_ver + a.J + y);
   if (svc != kSpecNone && !chain_dead(a, y, svc, sty, nby)) return 1;
   if (tag_is(ld_relaxed_u32(a.spec_ver + y), st_ver(sty))) return 0;
@@ -1033,7 +1051,7 @@ __device__ bool pick_job(const HcArgs& a, int pidx, Job& j, int wid) {
   const int cell = ld_relaxed_s32(a.harr + pidx);
   if (cell < 0 || cell >= a.J) return false;
   int nbs[4];
-  cell_nbs(a.g, cell, nbs);
+  cell_nbs(a, cell, nbs);
   u64 st = ld_relaxed_u64_nb(a.state + cell);
   const unsigned svp = ld_relaxed_u32_nb(a.spec_ver + cell);
   const unsigned svc = ld_relaxed_u32_nb(a.spec_ver + a.J + cell);
@@ -1096,7 +1114,7 @@ __device__ bool pick_job(const HcArgs& a, int pidx, Job& j, int wid) {
     if (!__ldcg(&rc->add[d]) && !(cand < knb[d])) continue;
     const double kx = cand < knb[d] ? cand : knb[d];  // x's key after this commit
     int nbx[4];
-    cell_nbs(a.g, x, nbx);
+    cell_nbs(a, x, nbx);
     unsigned am = 0;
     for (int e = 0; e < 4; ++e) {
       const int y = nbx[e];
@@ -1158,12 +1176,9 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
     H.msl[lane] = 0;
     H.cnt[lane] = 0;
     H.pos = a.hpos;
-    H.cells_x = a.g.cells_x;
     H.pubcnt = a.hsize_pub;  // bucket counts, one 128-byte line each
     H.pubcnt[32 * lane] = 0;
     H.size = 0;
-    H.overflow = false;
-    for (int d = 0; d < 4; ++d) H.trk[d] = -1, H.tps[d] = -1;
     __syncwarp();
     committer<PROF>(a, H, T, before, lane);
     return;
@@ -1235,7 +1250,7 @@ __global__ void heapcell_init_kernel(HcArgs a) {
     const int r = (int)(k - (int64_t)cell * cellsz);
     const int y = r / a.spw, x = r % a.spw;
     int64_t ib, ie, jb, je;
-    hc_cell_rect(a.g, cell, ib, ie, jb, je);
+    hc_cell_rect(a.g, a.cx_magic, cell, ib, ie, jb, je);
     double v = kInf;
     if (x < ie - ib && y < je - jb) v = a.u[(jb + y) * a.g.P + a.g.pad + ib + x];
     a.slots[k] = v;  // slot 0 <- the prepared field
@@ -1266,7 +1281,7 @@ __global__ void heapcell_gather_kernel(HcArgs a) {
     const int r = (int)(k - (int64_t)cell * cellsz);
     const int y = r / a.spw, x = r % a.spw;
     int64_t ib, ie, jb, je;
-    hc_cell_rect(a.g, cell, ib, ie, jb, je);
+    hc_cell_rect(a.g, a.cx_magic, cell, ib, ie, jb, je);
     if (x < ie - ib && y < je - jb)
       a.u[(jb + y) * a.g.P + a.g.pad + ib + x] = slot_ptr(a, st_cur(a.state[cell]), cell)[r];
   }
