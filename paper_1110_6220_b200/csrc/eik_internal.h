@@ -67,12 +67,15 @@ cudaError_t fmsm_capacity(int64_t tile_doubles, int warps_per_cta, int* ctas);
 
 // Result of processing one cell (sweeps + the four border scans), produced by
 // a worker speculatively and applied by the committer.
-struct SpecRec {
+// Laid out for the committer's loads: per side one double and one word, the
+// counters and instance number in one 16-byte vector.
+struct alignas(16) SpecRec {
   double cand[4];
   int sweeps, updates;
-  uint8_t add[4], fl[4], monc[4], mons[4];
   unsigned inst;            // instance number (written last)
   unsigned tag;             // version of the cell the result is valid at
+  unsigned side[4];         // per side: bit 0 add, bits 8-15 sweep flags, bit 16
+                            // monotonicity checked, bit 24 single-direction
   unsigned dmask;           // chained: sides whose pending results it assumes
   unsigned dinst[4];        // ... and their instance numbers
   unsigned nseq;            // instances written so far (busy holder only)

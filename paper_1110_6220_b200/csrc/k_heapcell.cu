@@ -393,10 +393,8 @@ __device__ void scan_all(const HcArgs& a, const HTile& T, const double* before,
     add = false;
   }
   rec->cand[side] = cand;
-  rec->add[side] = add;
-  rec->fl[side] = (uint8_t)fl;
-  rec->monc[side] = mon_checked;
-  rec->mons[side] = mon_single;
+  rec->side[side] = (add ? 1u : 0u) | (fl << 8) | (mon_checked ? 1u << 16 : 0u) |
+                    (mon_single ? 1u << 24 : 0u);
 }
 
 __device__ __forceinline__ void hc_cell_rect(const CellGeom& g, u64 magic, int cell, int64_t& ib,
@@ -679,11 +677,9 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       my_pos = __ldcg(a.hpos + nb);
       my_ctag = __ldcg(a.ctag + nb);
     }
-    if (lane == 0) {
-      st = ld_relaxed_u64_nb(a.state + cell);
-      svp0 = ld_relaxed_u32_nb(spec_p + cell);
-      svc0 = ld_relaxed_u32_nb(spec_c + cell);
-    }
+    st = ld_relaxed_u64_nb(a.state + cell);  // every lane: one warp-wide load each
+    svp0 = ld_relaxed_u32_nb(spec_p + cell);
+    svc0 = ld_relaxed_u32_nb(spec_c + cell);
     // take the cell out of its bucket and renew that bucket's minimum while
     // those loads are in flight (the neighbours sit in other buckets, so
     // neither moves their prefetched positions)
@@ -692,10 +688,9 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     H.rescan(lane, wpop);
     const long long t1a = PROF ? clock64() : 0;
     if (PROF) cyc_rescan += t1a - t1;
-    unsigned ctn[4];
-#pragma unroll
-    for (int d = 0; d < 4; ++d) ctn[d] = __shfl_sync(kFull, my_ctag, d);
-    if (lane == 0) {
+    // every lane validates (the same words, each read by one warp-wide load,
+    // so the lanes agree without a broadcast); lane 0 alone claims
+    {
       const unsigned v = st_ver(st);
       long long spins = 0;
       bool waited = false;
@@ -725,8 +720,10 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
           const unsigned dm = __ldcg(&r1->dmask);
           bool ok = true;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if ((dm >> k) & 1u) ok = ok && __ldcg(&r1->dinst[k]) == ctn[k];
+          for (int k = 0; k < 4; ++k) {
+            const unsigned ctk = __shfl_sync(kFull, my_ctag, k);
+            if ((dm >> k) & 1u) ok = ok && __ldcg(&r1->dinst[k]) == ctk;
+          }
           if (ok) {
             dep = dd;
             kind = 1;
@@ -734,21 +731,27 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
             break;
           }
         }
-        if (atomicCAS(a.busy + cell, 0, 1) == 0) {
-          if (a.wdbg) a.owner[cell] = 0x30000;
-          const unsigned sv2 = ld_relaxed_u32(spec_p + cell);
+        int got = 0;
+        if (lane == 0) got = atomicCAS(a.busy + cell, 0, 1) == 0 ? 1 : 0;
+        if (__shfl_sync(kFull, got, 0)) {
+          if (lane == 0 && a.wdbg) a.owner[cell] = 0x30000;
+          unsigned sv2 = 0;
+          if (lane == 0) sv2 = ld_relaxed_u32(spec_p + cell);
+          sv2 = __shfl_sync(kFull, sv2, 0);
           if (tag_is(sv2, v)) {
-            if (a.wdbg) a.owner[cell] = 0x40000;
-            st_release_s32(a.busy + cell, 0);
+            if (lane == 0) {
+              if (a.wdbg) a.owner[cell] = 0x40000;
+              st_release_s32(a.busy + cell, 0);
+            }
             unsigned d;
             asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(sv2));
             dep = (int)((d & kTagMask) - v);
             kind = 0;
           } else {
             mode = 1;
-            if (a.wdbg) a.owner[cell] = 0x50000;
+            if (lane == 0 && a.wdbg) a.owner[cell] = 0x50000;
             // classify the miss (profiling counters 16..23)
-            if (PROF) {
+            if (PROF && lane == 0) {
             const unsigned svc2 = ld_relaxed_u32(spec_c + cell);
             int cls;
             if (svc2 == kSpecNone) {
@@ -770,6 +773,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
         }
         waited = true;
         if (++spins > kSpinCap) {
+          if (lane == 0) {
           atomicExch(a.status, kStatusWatchdog);
           // diagnostics for the host (EIK_HC_PROFILE)
           a.counters[24] = (unsigned long long)cell;
@@ -793,6 +797,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
               a.counters[36] = (unsigned long long)((clock64() >> 10) - a.wdbg[4 * ow + 3]);
             }
           }
+          }
           mode = 2;
           break;
         }
@@ -801,10 +806,6 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       if (waited) ++waits;
       if (PROF && waited) cyc_wait += clock64() - tw0;
     }
-    mode = __shfl_sync(kFull, mode, 0);
-    st = __shfl_sync(kFull, st, 0);
-    kind = __shfl_sync(kFull, kind, 0);
-    dep = __shfl_sync(kFull, dep, 0);
     long long t2 = PROF ? clock64() : 0;
     if (PROF) cyc_obtain += t2 - t1;
     if (mode == 2) break;
@@ -828,15 +829,17 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       if (lane < 4) {
         const int d = lane, nb = nbs[d];
         const double cand = __ldcg(&rec->cand[d]);
-        const unsigned add = __ldcg(&rec->add[d]), fl = __ldcg(&rec->fl[d]);
-        const unsigned mc = __ldcg(&rec->monc[d]), ms = __ldcg(&rec->mons[d]);
+        const unsigned sw = __ldcg(&rec->side[d]);
         int rsweeps = 0, rupdates = 0;
         unsigned inst = 0;
         if (d == 0) {
-          rsweeps = __ldcg(&rec->sweeps);
-          rupdates = __ldcg(&rec->updates);
-          inst = __ldcg(&rec->inst);
+          const int4 ctr = __ldcg(reinterpret_cast<const int4*>(&rec->sweeps));
+          rsweeps = ctr.x;
+          rupdates = ctr.y;
+          inst = (unsigned)ctr.z;
         }
+        const unsigned add = sw & 1u, fl = (sw >> 8) & 0xFFu;
+        const unsigned mc = (sw >> 16) & 1u, ms = sw >> 24;
         if (d == 0) {
           sweeps += rsweeps;
           updates += rupdates;
@@ -1020,7 +1023,8 @@ __device__ bool claim_chain(const HcArgs& a, int x, const int nbx[4], unsigned a
       break;
     }
     const int xside_of_y = d ^ 1;
-    if (__ldcg(&ry->add[xside_of_y])) j.cflags |= __ldcg(&ry->fl[xside_of_y]);
+    const unsigned sw = __ldcg(&ry->side[xside_of_y]);
+    if (sw & 1u) j.cflags |= (sw >> 8) & 0xFFu;
     j.oslot[d] = kind_slot(sty, yk);
     j.dinst[d] = inst;
   }
@@ -1111,7 +1115,7 @@ __device__ bool pick_job(const HcArgs& a, int pidx, Job& j, int wid) {
     const int x = nbs[d];
     if (x < 0) continue;
     const double cand = __ldcg(&rc->cand[d]);
-    if (!__ldcg(&rc->add[d]) && !(cand < knb[d])) continue;
+    if (!(__ldcg(&rc->side[d]) & 1u) && !(cand < knb[d])) continue;
     const double kx = cand < knb[d] ? cand : knb[d];  // x's key after this commit
     int nbx[4];
     cell_nbs(a, x, nbx);
