@@ -116,6 +116,15 @@ __device__ __forceinline__ int ld_relaxed_s32(const int* p) {
 __device__ __forceinline__ bool tag_is(unsigned sv, unsigned v) {
   return sv != kSpecNone && (sv & kTagMask) == v;
 }
+// named barriers between the committer (warp 0) and its queue helper (warp 1)
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+constexpr int kBarQueueDone = 1;  // helper -> committer: the popped bucket is renewed
+constexpr int kBarQueuePop = 2;   // committer -> helper: a pop to remove (or -1: stop)
 
 // ---- the committer's priority queue over cells keyed by (cell value, id) ---
 // The reference pops the minimum (value, id) of an indexed binary heap
@@ -632,8 +641,18 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
   const unsigned* spec_p = a.spec_ver;
   const unsigned* spec_c = a.spec_ver + a.J;
   bool over = false;
+  // With a second warp in the CTA, the popped cell's bucket removal and the
+  // bucket's new minimum are its job (queue_helper), off this warp's path:
+  // the commit touches only the neighbours' buckets, never the popped one.
+  const bool helper = blockDim.x >= 64;
+  int* mbox = H.cnt + 32;  // [0] popped cell (-1: stop), [1] its bucket
+  bool pending = false;    // the helper is renewing the last pop's bucket
   for (;;) {
     long long t0 = PROF ? clock64() : 0;
+    if (pending) {
+      named_bar_sync(kBarQueueDone, 64);
+      pending = false;
+    }
     // a full bucket dropped an entry: stop, the host reruns with global buckets
     if (__any_sync(kFull, ovf)) {
       over = true;
@@ -648,6 +667,15 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     if (removals > a.budget) {  // heap_cell.cpp:276-277
       if (lane == 0) atomicExch(a.status, 3);
       break;
+    }
+    if (helper) {
+      if (lane == 0) {
+        mbox[0] = cell;
+        mbox[1] = wpop;
+      }
+      __threadfence_block();
+      named_bar_arrive(kBarQueuePop, 64);
+      pending = true;
     }
     int cxi, cyi;
     cell_xy(cell, g.cells_x, a.cx_magic, cxi, cyi);
@@ -683,9 +711,11 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     // take the cell out of its bucket and renew that bucket's minimum while
     // those loads are in flight (the neighbours sit in other buckets, so
     // neither moves their prefetched positions)
-    H.remove(lane, wpop, cell);
-    if (lane == 0) a.ckey[cell] = kInf;
-    H.rescan(lane, wpop);
+    if (!helper) {
+      H.remove(lane, wpop, cell);
+      if (lane == 0) a.ckey[cell] = kInf;
+      H.rescan(lane, wpop);
+    }
     const long long t1a = PROF ? clock64() : 0;
     if (PROF) cyc_rescan += t1a - t1;
     // every lane validates (the same words, each read by one warp-wide load,
@@ -901,6 +931,12 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       prev_cell = cell;
     }
   }
+  if (helper) {  // stop the helper
+    if (pending) named_bar_sync(kBarQueueDone, 64);
+    if (lane == 0) mbox[0] = -1;
+    __threadfence_block();
+    named_bar_arrive(kBarQueuePop, 64);
+  }
   for (int o = 16; o > 0; o >>= 1) {
     mon_checks += __shfl_xor_sync(kFull, mon_checks, o);
     mon_single += __shfl_xor_sync(kFull, mon_single, o);
@@ -938,6 +974,23 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     if (over) atomicExch(a.status, 6);
     __threadfence();
     st_release_s32(a.done_flag, 1);
+  }
+}
+
+// Warp 1 of the committer's CTA: for every pop, take the cell out of its
+// bucket and renew the bucket's cached minimum while the committer validates
+// and commits (which touches only the neighbours' buckets).
+__device__ void queue_helper(const HcArgs& a, BucketPQ& H, int lane) {
+  const int* mbox = H.cnt + 32;
+  for (;;) {
+    named_bar_sync(kBarQueuePop, 64);
+    const int cell = mbox[0], w = mbox[1];
+    if (cell < 0) return;
+    H.remove(lane, w, cell);
+    if (lane == 0) a.ckey[cell] = kInf;
+    H.rescan(lane, w);
+    __threadfence_block();
+    named_bar_arrive(kBarQueueDone, 64);
   }
 }
 
@@ -1154,7 +1207,7 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
   // SM invalidates that SM's L1 (CCTL.IVALL).  Workers poll with relaxed
   // loads and acquire once per speculation.
   if (blockIdx.x == 0) {
-    if (wib != 0) return;
+    if (wib > 1) return;  // warp 0 commits, warp 1 (if any) keeps the queue
     BucketPQ H;
     // [tile][keys: 32 capb doubles][ids: 32 capb ints] in smem when heap_cap
     // > 0, else in global memory; [minima: 32 doubles][ids][slots][counts]
@@ -1175,14 +1228,18 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
     H.mi = reinterpret_cast<int*>(H.mk + 32);
     H.msl = H.mi + 32;
     H.cnt = H.msl + 32;
+    H.pos = a.hpos;
+    H.pubcnt = a.hsize_pub;  // bucket counts, one 128-byte line each
+    H.size = 0;
+    if (wib == 1) {
+      queue_helper(a, H, lane);
+      return;
+    }
     H.mk[lane] = kInf;
     H.mi[lane] = 0x7fffffff;
     H.msl[lane] = 0;
     H.cnt[lane] = 0;
-    H.pos = a.hpos;
-    H.pubcnt = a.hsize_pub;  // bucket counts, one 128-byte line each
     H.pubcnt[32 * lane] = 0;
-    H.size = 0;
     __syncwarp();
     committer<PROF>(a, H, T, before, lane);
     return;
@@ -1299,8 +1356,9 @@ size_t heapcell_smem_bytes(const CellGeom& g, int max_len) {
 }
 
 size_t heapcell_committer_heap_bytes(int capb) {
-  // 32 buckets of capb (key, id) entries + per-bucket minimum, id, slot, count
-  return (size_t)32 * capb * (sizeof(double) + 4) + 32 * (sizeof(double) + 12);
+  // 32 buckets of capb (key, id) entries + per-bucket minimum, id, slot,
+  // count + the committer -> helper mailbox
+  return (size_t)32 * capb * (sizeof(double) + 4) + 32 * (sizeof(double) + 12) + 16;
 }
 
 namespace {
