@@ -101,7 +101,8 @@ struct HcArgs {
   int* hsize_pub;           // per-bucket queue counts for the workers, bucket b at [32 b]
   int64_t tile_doubles;     // per-warp smem
   int64_t min_smem;         // launch at least this much dynamic smem per CTA (SM-exclusive CTAs)
-  unsigned long long cx_magic;  // cell / cells_x == (cell * cx_magic) >> 40 for every cell (0: divide)
+  unsigned long long cx_magic;
+  int skip_from;            // HCM: sweeps from this one on use the vote-skip engine  // cell / cells_x == (cell * cx_magic) >> 40 for every cell (0: divide)
   int heap_cap;             // >0: committer queue buckets in shared memory, capacity
                             // per bucket; 0: buckets in global memory (hkey + harr)
   int heap_capb_global;     // bucket capacity of the global layout (ceil(J/32))

@@ -390,6 +390,11 @@ retry:  // after a committer heap overflow, with the heap in global memory
   a.tile_doubles = P->cg.tile_doubles;
   a.min_smem = P->hc_min_smem;
   a.cx_magic = P->hc_cx_magic;
+  // HCM's first sweep runs mostly unlocked nodes: the branch-free engine wins
+  // there, the vote-skip one on the convergence sweeps (measured 1-3 % at
+  // every cell size; EIK_HC_SKIP_FROM overrides)
+  a.skip_from = 1;
+  if (const char* c = std::getenv("EIK_HC_SKIP_FROM")) a.skip_from = std::atoi(c);
   CK(cudaMemsetAsync(P->dHcMisc, 0, sizeof(int) * (32 + 32 * 32), P->stream));
   const int hc_ctas = P->cap() > 0 ? std::min(P->hc_max_ctas, P->cap()) : P->hc_max_ctas;
   int grid = 0;

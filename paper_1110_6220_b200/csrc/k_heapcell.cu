@@ -551,7 +551,7 @@ __device__ __forceinline__ void process_cell(const HcArgs& a, HTile& T, double* 
     bool changed = true;
     while (changed) {
       const int dir = nsw < 4 ? perm[nsw] : kRotation[nsw % 4];
-      changed = cell_sweep<2>(ct, dir, lane, upd, /*skip=*/true);
+      changed = cell_sweep<2>(ct, dir, lane, upd, /*skip=*/nsw >= a.skip_from);
       ++nsw;
     }
   }
