@@ -211,14 +211,19 @@ def test_heapcell_all_exit_and_first_removal():
 
 @pytest.mark.parametrize("env", [{"EIK_HC_HEAP_CAP": "2"}, {"EIK_HC_GLOBAL_HEAP": "1"},
                                  {"EIK_HC_CHAIN": "0"}, {"EIK_HC_CHAIN": "2"},
-                                 {"EIK_HC_CTAS": "1"}],
+                                 {"EIK_HC_CTAS": "1"}, {"EIK_HC_WARPS": "1"},
+                                 {"EIK_HC_SKIP_FROM": "0"}, {"EIK_HC_SKIP_FROM": "9"},
+                                 {"EIK_HC_MIN_SMEM": "0", "EIK_HC_WARPS": "2"}],
                          ids=["heap-overflow-fallback", "global-heap", "no-chain", "chain-all",
-                              "committer-only"])
+                              "committer-only", "no-queue-helper", "skip-engine-all",
+                              "skip-engine-none", "packed-ctas"])
 def test_heapcell_engine_variants_bitwise(env, monkeypatch):
     """Every scheduling variant of the heap-cell kernel -- a committer heap that
     overflows shared memory and falls back to global memory, the global heap,
-    plain-only / all-neighbour chained speculation, the committer alone -- must
-    give the reference's bits and counters (C2 at 16x16-node cells)."""
+    plain-only / all-neighbour chained speculation, the committer alone, one
+    warp per CTA (no queue helper), either in-cell engine for HCM's sweeps,
+    CTAs packed several per SM -- must give the reference's bits and counters
+    (C2 at 16x16-node cells)."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     p = configs.config2(257).problem
