@@ -440,42 +440,46 @@ int plan_rows(eik_plan* P, int64_t row0, int64_t nrows, double* host_or_dev, int
 }
 
 // Device split for plans sharing one GPU (eik_plan_run_batch), in SMs.
-// Fixed-size grids (FSM/FMM strips) may spread one CTA per SM, so they
-// count one SM per CTA; FMSM dataflows (a few ms alone) get 2 CTAs; plans
-// capped by the caller keep their cap; the heap-cell replays, whose CTAs
-// each hold a whole SM, split what is left equally.  Equal shares suit
-// them: each is bound by its committer's serial chain and runs within a few
-// % of its solo time once it holds ~16 SMs of workers (measured on C2), so
-// the batch ends with its longest solve.
+// The heap-cell grids (one CTA per SM) are submitted first and take almost
+// everything; the fixed FSM/FMM grids are counted packed (their CTAs fill
+// the SMs left over, or wait for a replay to end -- they are short), FMSM
+// dataflows get 2 CTAs, plans capped by the caller keep their cap.  The
+// heap-cell replays split the rest by weight J^(1/4) / sqrt(warps per CTA):
+// a replay is bound by its committer's serial chain once it has enough
+// workers, and more cells (more pops in flight) or fewer warps per SM (large
+// cells) need more SMs to get there (measured on C2: HCM/8 at 13/20/30 SMs
+// 300/288/284 ms, HCM/64 265/234/212 ms, HCM/32 150/144/142 ms).
 int batch_split(eik_plan* const* plans, int n) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plans[0]->device));
   std::vector<int> dev(n), fixed(n);
-  double used = 0.0;
-  int flex = 0;
+  std::vector<double> w(n, 0.0);
+  double used = 0.0, wsum = 0.0;
   for (int k = 0; k < n; ++k) {
     eik_plan* P = plans[k];
     int rc = plan_capacity(P, &dev[k], &fixed[k]);
     if (rc) return rc;
     if (dev[k] < 1) return fail(EIK_ERR_CUDA, "batch: a kernel does not fit on the device");
     P->run_cap = 0;
+    const double per_sm = std::max(1.0, (double)dev[k] / sms);
     if (fixed[k] > 0) {
-      used += std::min(sms, fixed[k]);
+      used += std::ceil(fixed[k] / per_sm);
     } else if (P->ctas_cap > 0) {
-      used += (double)std::min(P->ctas_cap, dev[k]) * sms / dev[k];
+      used += std::ceil(std::min(P->ctas_cap, dev[k]) / per_sm);
     } else if (P->method == EIK_FMSM) {
       P->run_cap = 2;
-      used += std::min(2.0, 2.0 * sms / dev[k]);
+      used += std::ceil(2.0 / per_sm);
     } else {
-      ++flex;
+      const double J = (double)P->cells_x * P->cells_y;
+      w[k] = std::pow(J, 0.25) / std::sqrt((double)std::max(1, P->hc_warps_per_cta));
+      wsum += w[k];
     }
   }
   const double room = std::max(0.0, 0.98 * sms - used);
-  for (int k = 0; k < n; ++k) {
-    eik_plan* P = plans[k];
-    if (fixed[k] > 0 || P->ctas_cap > 0 || P->method == EIK_FMSM) continue;
-    P->run_cap = std::max(2, (int)std::floor(room / flex * dev[k] / sms));
-  }
+  for (int k = 0; k < n; ++k)
+    if (w[k] > 0.0)
+      plans[k]->run_cap =
+          std::max(2, (int)std::floor(room * w[k] / wsum * (double)dev[k] / sms));
   return EIK_OK;
 }
 
