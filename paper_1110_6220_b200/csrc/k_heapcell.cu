@@ -673,8 +673,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
         mbox[0] = cell;
         mbox[1] = wpop;
       }
-      __threadfence_block();
-      named_bar_arrive(kBarQueuePop, 64);
+      named_bar_arrive(kBarQueuePop, 64);  // orders the mailbox stores (BAR drains STS)
       pending = true;
     }
     int cxi, cyi;
@@ -934,7 +933,6 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
   if (helper) {  // stop the helper
     if (pending) named_bar_sync(kBarQueueDone, 64);
     if (lane == 0) mbox[0] = -1;
-    __threadfence_block();
     named_bar_arrive(kBarQueuePop, 64);
   }
   for (int o = 16; o > 0; o >>= 1) {
@@ -989,8 +987,7 @@ __device__ void queue_helper(const HcArgs& a, BucketPQ& H, int lane) {
     H.remove(lane, w, cell);
     if (lane == 0) a.ckey[cell] = kInf;
     H.rescan(lane, w);
-    __threadfence_block();
-    named_bar_arrive(kBarQueueDone, 64);
+    named_bar_arrive(kBarQueueDone, 64);  // the bucket's new minimum is in shared memory
   }
 }
 
