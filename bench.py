@@ -2,15 +2,18 @@
 F = 1 + 0.5 sin(20 pi x) sin(20 pi y), centre source), the full method matrix
 of BASELINE.json: fmm, fsm, and fmsm / hcm / fhcm at 8, 16, 32, 64-point cells.
 
-One step = one solve of every method-config in the matrix, the 14 solves
-running concurrently on the GPU (eik_plan_run_batch: SM-partitioned
-persistent kernels, one stream each -- the device counterpart of the
-reference runner's --jobs pool).  `value` is the whole-job throughput (grid
-points converged per step / step device time) with the speed fields already
-resident in HBM; `e2e` is the same metric through the public API
-(eik_solve_batch) with pinned host buffers (H2D of F and tables, D2H of u
-inside the timed region).  `methods` also lists each solve's device time
-alone on the whole GPU (`solo_ms`).  Prints one JSON line (rank 0).
+One step = one solve of every method-config in the matrix (14 solves).  The
+K timed steps are submitted together as one list schedule on the GPU
+(eik_plan_run_batch: each solve's persistent kernel on its own SMs, one
+stream each, a solve starting as soon as SMs free up -- the device
+counterpart of the reference runner's --jobs pool), so a step's long
+replays overlap the next step's solves.  `value` is the whole-job throughput
+(grid points converged / device time of the K steps) with the speed fields
+already resident in HBM; `e2e` is the same metric through the public API
+(eik_solve_batch over the K steps' solves) with pinned host buffers (H2D of
+F and tables, D2H of u inside the timed region).  `single_step_ms` is one
+step alone; `methods` lists each solve's time inside the schedule and alone
+on the whole GPU (`solo_ms`).  Prints one JSON line (rank 0).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -218,47 +221,52 @@ def main():
     g = p.grid
     M = g.size()
     rows = matrix(cfg)
-    plans = {}
-    tables = {}
+    # One plan set (the 14 solves of a step) per timed step: the K steps are
+    # submitted together and run as one list schedule on the GPU
+    # (eik_plan_run_batch), so a step's long replays overlap the next step's
+    # solves.  Every plan keeps its own inputs and buffers resident.
+    K = max(1, args.steps)
+    tables, cells_of = {}, {}
     for meth, cs in rows:
-        cells = E.build_cells(g, g.m // cs, g.m // cs) if cs else None
-        if cells is not None and cs not in tables:
-            tables[cs] = E.cell_tables(p, cells)
-        plans[(meth, cs)] = (E.Plan(p, meth, cells, tables.get(cs)), cells)
+        if cs and cs not in tables:
+            cells_of[cs] = E.build_cells(g, g.m // cs, g.m // cs)
+            tables[cs] = E.cell_tables(p, cells_of[cs])
+    keys = [f"{meth}" + (f"/{cs}" if cs else "") for meth, cs in rows]
+    sets = [[E.Plan(p, meth, cells_of.get(cs), tables.get(cs)) for meth, cs in rows]
+            for _ in range(K)]
+    plan_list = sets[0]
+    all_plans = [pl for st in sets for pl in st]
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def flush_l2():
         flush.zero_()
         torch.cuda.synchronize()
 
-    keys = [f"{meth}" + (f"/{cs}" if cs else "") for meth, cs in rows]
-    plan_list = [plans[r][0] for r in rows]
-
-    def step():
-        flush_l2()  # per-plan inputs < L2 (126 MB): flush before every timed step
-        outs, ms = E.run_batch(plan_list)
-        return ms, sum(o.kernel_launches for o in outs), dict(zip(keys, outs))
-
-    for _ in range(args.warmup):
-        step()
+    # W warm-up steps (whole K-step schedules until at least W steps ran)
+    for _ in range(max(1, -(-args.warmup // K))):
+        E.run_batch(all_plans)
+    flush_l2()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    step_ms, launches, per_all = [], 0, {}
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
-            ms, L, per = step()
-            step_ms.append(ms)
-            launches += L
-            for k, o in per.items():
-                per_all.setdefault(k, []).append((o.device_ms + o.host_ms, o))
+        outs, total_ms = E.run_batch(all_plans)
     torch.cuda.synchronize()
-    mean_ms = statistics.mean(step_ms)
+    launches = sum(o.kernel_launches for o in outs)
+    per_all = {}
+    for i, o in enumerate(outs):
+        per_all.setdefault(keys[i % len(rows)], []).append((o.device_ms + o.host_ms, o))
     if world > 1:
-        t = torch.tensor([mean_ms], device="cuda", dtype=torch.float64)
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        mean_ms = float(t.item())
+        total_ms = float(t.item())
+    mean_ms = total_ms / K
     value = world * len(rows) * M / (mean_ms / 1e3)
+
+    # one step alone (its 14 solves concurrently, nothing overlapping it) and
+    # each solve alone on the whole GPU: latencies, outside the timed region
+    flush_l2()
+    _, single_step_ms = E.run_batch(plan_list)
 
     # each solve alone on the whole GPU (latency; outside the timed region)
     solo = {}
@@ -316,8 +324,9 @@ def main():
     pinned_F[:] = p.sampled_speed()
     p_pin = E.Problem(g, p.speed, p.exit_nodes, p.exit_cost, p.exit_points, p.exit_point_cost,
                       _F=pinned_F)
-    pinned_u = [torch.empty(M, dtype=torch.float64, pin_memory=True).numpy() for _ in rows]
-    jobs = [(p_pin, meth, plans[(meth, cs)][1], tables.get(cs)) for meth, cs in rows]
+    pinned_u = [torch.empty(M, dtype=torch.float64, pin_memory=True).numpy()
+                for _ in range(K * len(rows))]
+    jobs = [(p_pin, meth, cells_of.get(cs), tables.get(cs)) for meth, cs in rows] * K
     h2d = d2h = 0
     for meth, cs in rows:
         h2d += 8 * M + 16 * len(p.exit_nodes)
@@ -326,13 +335,10 @@ def main():
             h2d += 8 * sum(len(a) for a in (tb.probe_w, tb.probe_e, tb.probe_s, tb.probe_n, tb.center))
         d2h += 8 * M
     E.solve_batch(jobs, outs=pinned_u)  # warm-up (device buffer cache)
-    e2e_t = []
-    for _ in range(max(1, args.steps)):
-        flush_l2()
-        t0 = time.perf_counter()
-        E.solve_batch(jobs, outs=pinned_u)
-        e2e_t.append(time.perf_counter() - t0)
-    e2e_s = statistics.mean(e2e_t)
+    flush_l2()
+    t0 = time.perf_counter()
+    E.solve_batch(jobs, outs=pinned_u)  # the K steps' solves, uploads and downloads
+    e2e_s = (time.perf_counter() - t0) / K
 
     cpu = None if args.no_cpu_baseline or rank != 0 else cpu_baseline_single_core()
     if rank == 0:
@@ -344,16 +350,21 @@ def main():
             "config": {"workload": "c2_sinusoid_2049_method_matrix", "grid": 2049,
                        "methods": METHODS, "cell_sizes": CELL_SIZES,
                        "parallelism": f"replicas x{world}",
-                       "concurrency": f"{len(rows)} solves per step run concurrently "
-                                      "(eik_plan_run_batch, SM-partitioned)",
-                       "l2": "256 MB flush before every solve (inputs < L2)"},
+                       "concurrency": f"{len(rows)} solves per step, each on its own SMs "
+                                      "(eik_plan_run_batch list schedule)",
+                       "steps_overlap": f"the {K} timed steps run as one list schedule "
+                                        "(a step's long replays overlap the next step's "
+                                        "solves); single_step_ms is one step alone",
+                       "l2": f"inputs larger than L2 ({K * len(rows)} resident plans, "
+                             "~0.2 GB each); one 256 MB flush before the timed region"},
             "e2e": {"value": world * len(rows) * M / e2e_s, "unit": "points/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "single_step_ms": single_step_ms,
             "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches,
             "clocks": clk.summary(), "methods": methods,
         }
         print(json.dumps(out))
-    for plan, _ in plans.values():
+    for plan in all_plans:
         plan.close()
     if world > 1:
         torch.distributed.destroy_process_group()

@@ -350,6 +350,7 @@ int plan_run(eik_plan* P, eik_output* out) {
       return fail(EIK_ERR_NOT_IMPL, "method not implemented on the device path");
   }
   if (rc) return rc;
+  P->last_ms = out->device_ms + out->host_ms;
   if (out->u) {
     // padded device layout -> caller's dense row-major m*n field
     CK(cudaMemcpy2DAsync(out->u, sizeof(double) * P->g.m, P->dU + kPad,
@@ -439,50 +440,73 @@ int plan_rows(eik_plan* P, int64_t row0, int64_t nrows, double* host_or_dev, int
   return EIK_OK;
 }
 
-// Device split for plans sharing one GPU (eik_plan_run_batch), in SMs.
-// The heap-cell grids (one CTA per SM) are submitted first and take almost
-// everything; the fixed FSM/FMM grids are counted packed (their CTAs fill
-// the SMs left over, or wait for a replay to end -- they are short), FMSM
-// dataflows get 2 CTAs, plans capped by the caller keep their cap.  The
-// heap-cell replays split the rest by weight J^(1/4) / sqrt(warps per CTA):
-// a replay is bound by its committer's serial chain once it has enough
-// workers, and more cells (more pops in flight) or fewer warps per SM (large
-// cells) need more SMs to get there (measured on C2: HCM/8 at 13/20/30 SMs
-// 300/288/284 ms, HCM/64 265/234/212 ms, HCM/32 150/144/142 ms).
-int batch_split(eik_plan* const* plans, int n) {
+// Device slices for plans sharing one GPU (eik_plan_run_batch), in SMs.
+// Every persistent grid holds whole SMs: the heap-cell CTAs and the FSM
+// strips (12 warps x 168 registers) fill an SM's register file, FMSM CTAs
+// its shared memory.  A heap-cell replay is bound by its committer's serial
+// chain once it has enough workers; more cells (more pops in flight) or
+// fewer warps per SM (large cells) need more SMs to get there, and past that
+// point SMs buy little (measured on C2: HCM/8 at 8/13/20/30 SMs
+// 428/300/288/284 ms, HCM/64 313/265/234/212 ms, HCM/32 162/150/144/142 ms),
+// so it asks for 2 J^(1/4) / sqrt(warps per CTA) SMs (EIK_BATCH_SMS_SCALE
+// overrides the 2): the slice where SM-time per solve is near its minimum,
+// which is what a schedule of many solves needs (C2, 3 steps: 2 -> 134 ms
+// per step, 4 -> 190 ms; one step alone 332 vs 295 ms).  Admission order:
+// heap-cell replays by that weight (larger first, HCM before FHCM), then the
+// fixed grids, then FMSM -- measured better than ordering by the last run's
+// time (170 ms per step).  FMSM dataflows (a few ms alone) get 2 CTAs, fixed
+// grids what they need, plans capped by the caller their cap.
+struct BatchSlot {
+  int sms = 0;        // SMs the plan's grid holds while it runs
+  double prio = 0.0;  // admission order
+  bool hc = false;
+};
+
+int batch_slots(eik_plan* const* plans, int n, int budget, std::vector<BatchSlot>& slot) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plans[0]->device));
-  std::vector<int> dev(n), fixed(n);
-  std::vector<double> w(n, 0.0);
-  double used = 0.0, wsum = 0.0;
+  slot.assign(n, BatchSlot{});
+  double scale = 2.0;
+  if (const char* c = std::getenv("EIK_BATCH_SMS_SCALE")) scale = std::atof(c);
   for (int k = 0; k < n; ++k) {
     eik_plan* P = plans[k];
-    int rc = plan_capacity(P, &dev[k], &fixed[k]);
+    int dev = 0, fixed = 0;
+    int rc = plan_capacity(P, &dev, &fixed);
     if (rc) return rc;
-    if (dev[k] < 1) return fail(EIK_ERR_CUDA, "batch: a kernel does not fit on the device");
+    if (dev < 1) return fail(EIK_ERR_CUDA, "batch: a kernel does not fit on the device");
+    const int per_sm = std::max(1, dev / sms);
+    BatchSlot& b = slot[k];
     P->run_cap = 0;
-    const double per_sm = std::max(1.0, (double)dev[k] / sms);
-    if (fixed[k] > 0) {
-      used += std::ceil(fixed[k] / per_sm);
+    if (fixed > 0) {
+      b.sms = (fixed + per_sm - 1) / per_sm;
+      b.prio = 1.0;
     } else if (P->ctas_cap > 0) {
-      used += std::ceil(std::min(P->ctas_cap, dev[k]) / per_sm);
+      b.sms = (std::min(P->ctas_cap, dev) + per_sm - 1) / per_sm;
+      b.prio = 1.5;
+      b.hc = P->method == EIK_HCM || P->method == EIK_FHCM;
     } else if (P->method == EIK_FMSM) {
       P->run_cap = 2;
-      used += std::ceil(2.0 / per_sm);
+      b.sms = 2;
+      b.prio = 0.5;
     } else {
       const double J = (double)P->cells_x * P->cells_y;
-      w[k] = std::pow(J, 0.25) / std::sqrt((double)std::max(1, P->hc_warps_per_cta));
-      wsum += w[k];
+      const double w =
+          std::pow(J, 0.25) / std::sqrt((double)std::max(1, P->hc_warps_per_cta));
+      b.sms = std::max(2, (int)std::lround(scale * w));
+      b.prio = 2.0 + w + (P->method == EIK_HCM ? 0.01 : 0.0);
+      b.hc = true;
     }
+    b.sms = std::min(b.sms, budget);
+    if (P->run_cap == 0 && fixed == 0 && P->ctas_cap == 0) P->run_cap = b.sms * per_sm;
   }
-  const double room = std::max(0.0, 0.98 * sms - used);
-  for (int k = 0; k < n; ++k)
-    if (w[k] > 0.0)
-      plans[k]->run_cap =
-          std::max(2, (int)std::floor(room * w[k] / wsum * (double)dev[k] / sms));
   return EIK_OK;
 }
 
+// Runs the plans as a list schedule: in order of priority, each plan starts
+// (on its own host thread and stream) as soon as its SMs are free, later
+// plans filling in behind one that does not fit yet; a plan ending returns
+// its SMs.  Admitted heap-cell grids are submitted before the other
+// admitted plans start, so their SM-exclusive CTAs find whole free SMs.
 int plan_run_batch(eik_plan* const* plans, int n, eik_output* outs, double* batch_ms) {
   for (int k = 0; k < n; ++k) {
     if (!plans[k]) return fail(EIK_ERR_DOMAIN, "batch: null plan");
@@ -491,10 +515,18 @@ int plan_run_batch(eik_plan* const* plans, int n, eik_output* outs, double* batc
     if (plans[k]->device != plans[0]->device)
       return fail(EIK_ERR_CONFIG, "batch: plans on different devices");
   }
-  int rc = batch_split(plans, n);
-  if (rc) return rc;
   const int device = plans[0]->device;
   CK(cudaSetDevice(device));
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const int budget = std::max(1, (int)std::floor(0.98 * sms));
+  std::vector<BatchSlot> slot;
+  int rc = batch_slots(plans, n, budget, slot);
+  if (rc) return rc;
+  std::vector<int> order(n);
+  for (int k = 0; k < n; ++k) order[k] = k;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](int x, int y) { return slot[x].prio > slot[y].prio; });
   CK(cudaDeviceSynchronize());
   cudaEvent_t ref;
   CK(cudaEventCreate(&ref));
@@ -503,37 +535,51 @@ int plan_run_batch(eik_plan* const* plans, int n, eik_output* outs, double* batc
   std::vector<int> codes(n, EIK_OK);
   std::vector<std::string> msgs(n);
   {
-    // The SM-exclusive heap-cell grids are submitted first; the other plans
-    // (whose small CTAs would otherwise spread over the SMs those grids
-    // need) start once every heap-cell thread has issued its launches.
     std::mutex mu;
     std::condition_variable cv;
-    int hc_pending = 0;
-    for (int k = 0; k < n; ++k)
-      if (plans[k]->method == EIK_HCM || plans[k]->method == EIK_FHCM) ++hc_pending;
-    auto launched = [&]() {
-      std::lock_guard<std::mutex> lk(mu);
-      if (--hc_pending == 0) cv.notify_all();
+    int free_sms = budget;
+    int hc_launching = 0;               // admitted heap-cell plans not yet submitted
+    std::vector<char> admitted(n, 0);
+    auto admit = [&]() {                // under mu
+      for (int k : order) {
+        if (admitted[k] || slot[k].sms > free_sms) continue;
+        admitted[k] = 1;
+        free_sms -= slot[k].sms;
+        if (slot[k].hc) ++hc_launching;
+      }
+      cv.notify_all();
     };
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      admit();
+    }
     std::vector<std::thread> th;
     th.reserve(n);
     for (int k = 0; k < n; ++k) {
       eik_plan* P = plans[k];
-      const bool hc = P->method == EIK_HCM || P->method == EIK_FHCM;
-      th.emplace_back([&, k, P, hc]() {
+      th.emplace_back([&, k, P]() {
         cudaSetDevice(device);
-        if (hc) {
-          P->on_launched = launched;
-        } else {
+        const bool hc = slot[k].hc;
+        {
           std::unique_lock<std::mutex> lk(mu);
-          cv.wait(lk, [&]() { return hc_pending == 0; });
+          cv.wait(lk, [&]() { return admitted[k] && (hc || hc_launching == 0); });
         }
+        bool signalled = !hc;
+        auto launched = [&]() {
+          std::lock_guard<std::mutex> lk(mu);
+          if (--hc_launching == 0) cv.notify_all();
+        };
+        if (hc) P->on_launched = [&]() {
+          signalled = true;
+          launched();
+        };
         codes[k] = plan_run(P, &outs[k]);
         if (codes[k]) msgs[k] = g_last_error;  // thread-local: carry it back
-        if (hc && P->on_launched) {             // failed before its launch
-          P->on_launched = nullptr;
-          launched();
-        }
+        P->on_launched = nullptr;
+        if (!signalled) launched();            // failed before its launch
+        std::lock_guard<std::mutex> lk(mu);
+        free_sms += slot[k].sms;
+        admit();
       });
     }
     for (auto& t : th) t.join();
@@ -546,8 +592,8 @@ int plan_run_batch(eik_plan* const* plans, int n, eik_output* outs, double* batc
     float ms = 0.f, ms0 = 0.f;
     if (codes[k] == EIK_OK) e = cudaEventElapsedTime(&ms, ref, plans[k]->ev1);
     if (trace && codes[k] == EIK_OK && cudaEventElapsedTime(&ms0, ref, plans[k]->ev0) == cudaSuccess)
-      std::fprintf(stderr, "batch plan %d method %d ctas %lld: %.1f -> %.1f ms\n", k,
-                   plans[k]->method, (long long)outs[k].grid_ctas, ms0, ms);
+      std::fprintf(stderr, "batch plan %d method %d ctas %lld sms %d: %.1f -> %.1f ms\n", k,
+                   plans[k]->method, (long long)outs[k].grid_ctas, slot[k].sms, ms0, ms);
     t_end = std::max(t_end, (double)ms);
   }
   cudaEventDestroy(ref);

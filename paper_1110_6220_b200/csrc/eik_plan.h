@@ -82,6 +82,7 @@ struct eik_plan {
   int run_cap = 0;
 
   int cap() const { return run_cap > 0 ? run_cap : ctas_cap; }
+  double last_ms = 0.0;  // device + host ms of the last run (batch admission order)
   // batch runs: called (then cleared) once the heap-cell grid is submitted
   std::function<void()> on_launched;
 };
