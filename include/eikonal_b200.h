@@ -140,12 +140,14 @@ void eik_plan_destroy(eik_plan* plan);
  *                     (one warp per 32-row strip) and ignore the cap.
  * eik_plan_capacity   CTAs of the plan's persistent kernel the whole device
  *                     holds, and the fixed grid size (FSM/FMM) or 0.
- * eik_plan_run_batch  run n distinct plans of one device concurrently.
- *                     Plans without a cap split what the fixed grids and the
- *                     capped plans leave (heap-cell plans weight 1, FMSM
- *                     1/4).  *batch_ms = device time from the call until the
- *                     last solve ended.  Returns the first failing plan's
- *                     code (eik_last_error names it).
+ * eik_plan_run_batch  run n distinct plans of one device as a list
+ *                     schedule: each plan's persistent kernel gets a slice of
+ *                     whole SMs (heap-cell replays 2 J^(1/4)/sqrt(warps per
+ *                     CTA), FSM/FMM their fixed grid, FMSM 2 CTAs, a capped
+ *                     plan its cap) and starts as soon as the slice is free.
+ *                     *batch_ms = device time from the call until the last
+ *                     solve ended.  Returns the first failing plan's code
+ *                     (eik_last_error names it).
  * eik_solve_batch     n eik_solve calls run the same way (uploads, solves
  *                     and downloads overlap); cells[k] may be NULL for
  *                     FMM/FSM and `cells` itself NULL when no solve needs one. */
