@@ -235,6 +235,13 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method)
     track(P->dChanged);
     if ((rc = dalloc(&P->dDone, P->max_sweeps))) return rc;
     track(P->dDone);
+    // change bits: zeroed once; every sweep rewrites every word of a real row
+    // and nothing ever writes a nonzero bit into the pad rows/words
+    P->chg_cw = (P->g.m + 31) / 32 + kChgWordPad;
+    const size_t nchg = (size_t)2 * (P->g.n + 3) * P->chg_cw;
+    if ((rc = dalloc(&P->dChg, nchg))) return rc;
+    track(P->dChg);
+    CK(cudaMemsetAsync(P->dChg, 0, sizeof(unsigned) * nchg, P->stream));
   } else if (method == EIK_LSM) {
     return fail(EIK_ERR_NOT_IMPL, "lsm is not on the device path (out of scope, SURVEY.md §2.1)");
   } else {
@@ -263,13 +270,16 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   a.fixed = 0;
   a.status = P->dStatus;
   a.trace = nullptr;
+  a.chg = P->dChg;
+  a.cw = P->chg_cw;
+  a.noskip = std::getenv("EIK_FSM_NOSKIP") ? 1 : 0;
   if (std::getenv("EIK_TRACE_FSM")) {
     if (!P->dTrace) {
-      int rc = dalloc(&P->dTrace, (size_t)kTraceSweeps * P->nstrips * 3);
+      int rc = dalloc(&P->dTrace, (size_t)kTraceSweeps * P->nstrips * kTraceWords);
       if (rc) return rc;
       P->allocs.push_back(P->dTrace);
     }
-    CK(cudaMemsetAsync(P->dTrace, 0, sizeof(unsigned long long) * kTraceSweeps * P->nstrips * 3,
+    CK(cudaMemsetAsync(P->dTrace, 0, sizeof(unsigned long long) * kTraceSweeps * P->nstrips * kTraceWords,
                        P->stream));
     a.trace = P->dTrace;
   }
@@ -307,15 +317,17 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   out->device_ms = ms;
   out->kernel_launches = launches;
   if (a.trace) {
-    std::vector<unsigned long long> tr((size_t)kTraceSweeps * P->nstrips * 3);
+    std::vector<unsigned long long> tr((size_t)kTraceSweeps * P->nstrips * kTraceWords);
     CK(cudaMemcpy(tr.data(), a.trace, sizeof(unsigned long long) * tr.size(),
                   cudaMemcpyDeviceToHost));
     const char* path = std::getenv("EIK_TRACE_FSM");
     if (FILE* f = std::fopen(path, "w")) {
       for (int k = 0; k < kTraceSweeps; ++k)
         for (int b = 0; b < P->nstrips; ++b) {
-          const unsigned long long* t = &tr[((size_t)k * P->nstrips + b) * 3];
-          if (t[0]) std::fprintf(f, "%d %d %llu %llu %llu\n", k, b, t[0], t[1], t[2]);
+          const unsigned long long* t = &tr[((size_t)k * P->nstrips + b) * kTraceWords];
+          if (t[0])
+            std::fprintf(f, "%d %d %llu %llu %llu %llu %llu\n", k, b, t[0], t[1], t[2], t[3],
+                         t[4]);
         }
       std::fclose(f);
     }
@@ -402,6 +414,9 @@ int plan_sweep(eik_plan* P, int64_t first_sweep, int count, int* changed) {
   a.fixed = 1;
   a.status = P->dStatus;
   a.trace = nullptr;
+  a.chg = P->dChg;
+  a.cw = P->chg_cw;
+  a.noskip = std::getenv("EIK_FSM_NOSKIP") ? 1 : 0;
   int launches = 0;
   CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
   CK(cudaMemsetAsync(P->dProg, 0, sizeof(unsigned long long) * P->nstrips, P->stream));

@@ -27,10 +27,19 @@ struct FsmArgs {
   int first_sweep;          // direction of local sweep k is (first_sweep + k) mod 4
   int fixed;                // run exactly max_sweeps sweeps (no stop decision)
   int* status;              // [0] error, [1] sweeps
-  unsigned long long* trace; // optional [kTraceSweeps][nstrips][3] globaltimer
-                             // (start, body start, end) per strip-sweep
+  unsigned long long* trace; // optional [kTraceSweeps][nstrips][kTraceWords]: globaltimer
+                             // (start, body start, end), polls, compute steps
+  // Change bits (k_fsm.cu): [2][n+3][cw] u32, bit i of row r in sweep parity
+  // k&1 = node (i,r) decreased in sweep k.  Row r at (r+1)*cw, column word w
+  // at +w+kChgWordOff; the pad rows/words are never written (stay zero).
+  unsigned* chg;
+  int64_t cw;               // words per row: ceil(m/32) + kChgWordPad
+  int noskip;               // evaluate every node (no clean-step skipping)
 };
+constexpr int64_t kChgWordOff = 3;
+constexpr int64_t kChgWordPad = 8;  // pad words per row (kChgWordOff before, the rest after)
 constexpr int kTraceSweeps = 16;
+constexpr int kTraceWords = 5;  // start, body start, end, polls, compute steps
 
 // Cell decomposition as seen by the device (build_cells, cells.cpp:32-47):
 // cell (cx,cy) spans columns [cx*base_x, cx==cells_x-1 ? m : (cx+1)*base_x).

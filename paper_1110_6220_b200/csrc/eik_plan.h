@@ -37,6 +37,8 @@ struct eik_plan {
   double* dMbox = nullptr;
   unsigned long long* dTrace = nullptr;
   int* dChanged = nullptr;
+  unsigned* dChg = nullptr;   // [2][n+3][chg_cw] change bits (k_fsm.cu)
+  int64_t chg_cw = 0;
   int* dDone = nullptr;
   // two-scale methods: host copies of the inputs (the plan owns them)
   int32_t cells_x = 0, cells_y = 0;

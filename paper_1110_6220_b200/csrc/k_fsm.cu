@@ -47,7 +47,7 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const void* p) {
 __device__ __forceinline__ bool is_sent(double v) {
   return (unsigned long long)__double_as_longlong(v) == kSent;
 }
-__device__ __noinline__ double poll_slot(const double* p, int* status) {
+__device__ __forceinline__ double poll_slot(const double* p, int* status) {
   long long spins = 0;
   unsigned long long v;
   while ((v = ld_relaxed_u64(p)) == kSent) {
@@ -59,10 +59,7 @@ __device__ __noinline__ double poll_slot(const double* p, int* status) {
   }
   return __longlong_as_double((long long)v);
 }
-// Measured (profiles/README.md): handing edges between the warps of one CTA
-// through shared-memory rings with per-column spinning is 2-5x slower than
-// these global mailboxes -- the spinning LDS traffic competes with the
-// shuffles for the MIO pipe -- so every strip boundary uses a mailbox.
+
 struct Chan {
   double* gin;            // global mailbox row of the upwind strip (or the dummy row)
   double* gout;           // global mailbox row to the downwind strip (or dummy)
@@ -70,26 +67,85 @@ struct Chan {
   bool in_glob, out_glob; // lane 0 / lane 31 use the mailboxes
 };
 
+// Change bits around one block: the four-neighbour change mask of the kU
+// columns a block visits, from the previous sweep's bits of rows r-1, r, r+1
+// (loaded two blocks ahead; L2 loads, since neighbouring strips on other SMs
+// wrote them).
+struct ChgWin {
+  unsigned u0, u1, c0, c1, d0, d1;
+  int sh;
+};
+__device__ __forceinline__ ChgWin ld_chgwin(const unsigned* rows, int64_t cw, int64_t a) {
+  // bit j of the window = absolute column a + j (a >= -64: floor by shift)
+  const unsigned* p = rows + (a >> 5) + kChgWordOff;
+  ChgWin w;
+  w.u0 = __ldcg(p);
+  w.u1 = __ldcg(p + 1);
+  w.c0 = __ldcg(p + cw);
+  w.c1 = __ldcg(p + cw + 1);
+  w.d0 = __ldcg(p + 2 * cw);
+  w.d1 = __ldcg(p + 2 * cw + 1);
+  w.sh = (int)(a & 31);
+  return w;
+}
+// Node at column c is dirty iff a 4-neighbour changed: W/E from the own row
+// (columns c-1, c+1), S/N from rows r-1, r+1 (column c).  The window starts
+// at column lo-1, so own-row bits j and j+2 and the other rows' bit j+1 are
+// the neighbours of column lo+j.
+template <bool IASC>
+__device__ __forceinline__ unsigned chg_mask(const ChgWin& w) {
+  const unsigned long long xu = (((unsigned long long)w.u1 << 32) | w.u0) >> w.sh;
+  const unsigned long long xc = (((unsigned long long)w.c1 << 32) | w.c0) >> w.sh;
+  const unsigned long long xd = (((unsigned long long)w.d1 << 32) | w.d0) >> w.sh;
+  const unsigned d = (unsigned)(xc | (xc >> 2) | (xu >> 1) | (xd >> 1)) & 0xFFu;
+  // bit t of the result = the block's step t (column lo+t ascending, lo+7-t descending)
+  return IASC ? d : (__brev(d) >> 24);
+}
+
 // One sweep of one warp-strip.  IASC selects the column direction at compile
 // time so every access in the unrolled block is an immediate offset from a
 // per-block pointer; the padded layout (kPad columns of +inf / -1 on both
 // sides, a dummy row for lanes past the last grid row) removes every bounds
 // check from the step.
+//
+// Clean-step skipping (LSM's idea, classic_solvers.cpp:160-212, applied to
+// the exact sweep): a node whose four neighbours did not change since its
+// last evaluation recomputes exactly its old candidate, which cannot be below
+// its value, so skipping it changes nothing.  A step is skipped by the whole
+// warp when no lane's node is dirty: no neighbour changed in the previous
+// sweep (change bits), and neither the upwind column (the lane's previous
+// step) nor the upwind row (lane t-1's previous step, or the upwind strip's
+// edge value, sent with its sign bit set when it changed) changed in this
+// sweep.  Any lane updating at step s makes step s+1 a compute step, so the
+// in-sweep test is one flag per lane.
 template <bool IASC>
 __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t rowp,
-                                            const Chan& ch) {
+                                            const Chan& ch, const unsigned* crd, unsigned* cwr,
+                                            unsigned force, unsigned long long* tr) {
   constexpr int S = IASC ? 1 : -1;
-  const int64_t m = a.m, P = a.P;
+  const int64_t m = a.m, cw = a.cw;
+  const int64_t P = a.P;
   const int64_t q0off = IASC ? 0 : m - 1;  // element q of a row sits at base + S*q
   double* pu = a.u + rowp * P + a.pad + q0off - S * lane;
   const double* pc = a.C + rowp * P + a.pad + q0off - S * lane;
-  const bool in_lane = (lane == 0) && ch.in_glob;
+  const bool in_g = (lane == 0) && ch.in_glob;  // lane 0 reads the upwind mailbox
   const bool dn_lane = (lane == 31);
-  const bool halo_lane = in_lane || dn_lane;
+  const bool halo_lane = in_g || dn_lane;
   double* ph = (lane == 0 ? ch.gin : const_cast<double*>(ch.dnh)) + a.pad + q0off - S * lane;
   double* po = ch.gout + a.pad + q0off - S * lane;
-  const bool out_glob = dn_lane && ch.out_glob;
+  const bool out_g = dn_lane && ch.out_glob;
   const int nblocks = (int)((m + 31 + kU - 1) / kU);
+  const unsigned* crow = crd + rowp * cw;                 // rows rowp-1 .. rowp+1
+  unsigned* wrow = cwr + (rowp + 1) * cw + kChgWordOff;   // own row, word 0
+
+  // lo(b) = lowest absolute column block b visits; the window starts at lo-1
+  auto lo_of = [&](int b) -> int64_t {
+    const int64_t q = (int64_t)b * kU - lane;
+    return IASC ? q : m - 1 - q - (kU - 1);
+  };
+  unsigned pm = force ? force : chg_mask<IASC>(ld_chgwin(crow, cw, lo_of(0) - 1));
+  ChgWin wa = ld_chgwin(crow, cw, lo_of(1) - 1);
+  ChgWin wb = ld_chgwin(crow, cw, lo_of(2) - 1);
 
   double cu[kU + 1], cc[kU], hv[kU];
   double nu[kU + 1], nc[kU], nh[kU];
@@ -101,11 +157,25 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
     hv[t] = halo_lane ? __ldcg(ph + S * t) : kInf;
   }
   double res_prev = kInf;
-  bool changed = false;
+  bool upd_prev = false, changed = false;
   int q0 = -lane;
   const double sent = __longlong_as_double((long long)kSent);
+  // change bits of the word holding the next column to visit
+  int64_t wcur = (IASC ? (int64_t)-lane : m - 1 + lane) >> 5;
+  unsigned acc = 0;
+  unsigned npoll = 0, ncomp = 0;
 
   for (int blk = 0; blk < nblocks; ++blk) {
+    {
+      // land the previous prefetch before issuing the next one: the steps
+      // below then never wait on a scoreboard shared with fresh loads
+      unsigned x = 0;
+#pragma unroll
+      for (int t = 0; t < kU; ++t)
+        x |= (unsigned)__double2hiint(cu[t + 1]) ^ (unsigned)__double2hiint(cc[t]) ^
+             (unsigned)__double2hiint(hv[t]);
+      if (x == 0x7ff7dea1u) atomicAdd(a.status + 7, 1);  // never true
+    }
 #pragma unroll
     for (int t = 1; t <= kU; ++t) nu[t] = pu[S * (kU + t)];
 #pragma unroll
@@ -113,28 +183,83 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       nc[t] = __ldg(pc + S * (kU + t));
       nh[t] = halo_lane ? __ldcg(ph + S * (kU + t)) : kInf;
     }
+    const unsigned pm_next = force ? force : chg_mask<IASC>(wa);
+    wa = wb;
+    wb = ld_chgwin(crow, cw, lo_of(blk + 3) - 1);
+    unsigned um = 0;
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
       const int q = q0 + t;
-      double sv = __shfl_up_sync(kFull, res_prev, 1);
-      double nv = __shfl_down_sync(kFull, cu[t + 1], 1);
       double h = hv[t];
-      if (in_lane && q < m) {
-        if (is_sent(h)) h = poll_slot(ph + S * t, a.status);
+      if (in_g && q < m) {
+        if (is_sent(h)) {
+          h = poll_slot(ph + S * t, a.status);
+          ++npoll;
+          // the upwind strip is close ahead: every later slot loaded so far
+          // predates its write too; reload them once instead of polling
+          // each one a round trip apart
+#pragma unroll
+          for (int t2 = t + 1; t2 < kU; ++t2) hv[t2] = __ldcg(ph + S * t2);
+#pragma unroll
+          for (int t2 = 0; t2 < kU; ++t2) nh[t2] = __ldcg(ph + S * (kU + t2));
+        }
         ph[S * t] = sent;  // re-arm the slot for the next sweep
       }
-      if (lane == 0) sv = h;
-      if (lane == 31) nv = h;
+      // the upwind strip's edge value carries "changed in this sweep" in its sign
+      const bool h_chg = (lane == 0) && q < m && (__double_as_longlong(h) < 0);
+      const bool dirty = ((pm >> t) & 1u) || upd_prev || h_chg;
       const double cur = cu[t];
-      const double c = cc[t];
-      const double cand = node_update4(cu[t + 1], res_prev, nv, sv, c);
-      const bool upd = (c > 0.0) && (cand < cur);  // exits / padding carry c = -1
-      const double res = upd ? cand : cur;
-      if (upd) pu[S * t] = cand;
+      double res = cur;
+      bool upd = false;
+      if (__any_sync(kFull, dirty)) {
+        ++ncomp;
+        double sv = __shfl_up_sync(kFull, res_prev, 1);
+        double nv = __shfl_down_sync(kFull, cu[t + 1], 1);
+        const double hval = fabs(h);
+        if (lane == 0) sv = hval;
+        if (lane == 31) nv = hval;
+        const double c = cc[t];
+        const double cand = node_update4(cu[t + 1], res_prev, nv, sv, c);
+        upd = (c > 0.0) && (cand < cur);  // exits / padding carry c = -1
+        if (upd) {
+          res = cand;
+          pu[S * t] = cand;
+        }
+      }
       changed |= upd;
-      if (out_glob) __stcg(po + S * t, res);  // straight to L2: the next strip polls it
+      um |= (unsigned)upd << t;
+      const double ov = upd ? -res : res;
+      if (out_g) __stcg(po + S * t, ov);  // straight to L2: the next strip polls it
       res_prev = res;
+      upd_prev = upd;
     }
+    // this block's change bits into the row's words (absolute columns lo..lo+7)
+    {
+      const int64_t lo = lo_of(blk);
+      const unsigned ub = IASC ? um : (__brev(um) >> 24);
+      const int64_t wl = lo >> 5;
+      const unsigned long long x = (unsigned long long)ub << (lo & 31);
+      const unsigned lowp = (unsigned)x, highp = (unsigned)(x >> 32);
+      const int64_t wn = (IASC ? lo + kU : lo - 1) >> 5;  // word of the next column
+      if (IASC) {
+        acc |= lowp;
+        if (wn != wl) {
+          __stcg(wrow + wl, acc);
+          acc = highp;
+        }
+      } else if (wcur != wl) {  // straddles: word wl+1 first, then wl
+        __stcg(wrow + wcur, acc | highp);
+        acc = lowp;
+      } else {
+        acc |= lowp;
+        if (wn != wl) {
+          __stcg(wrow + wl, acc);
+          acc = 0;
+        }
+      }
+      wcur = wn;
+    }
+    pm = pm_next;
     pu += S * kU;
     pc += S * kU;
     ph += S * kU;
@@ -148,6 +273,11 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       cc[t] = nc[t];
       hv[t] = nh[t];
     }
+  }
+  __stcg(wrow + wcur, acc);
+  if (tr && lane == 0) {
+    tr[3] = npoll;
+    tr[4] = ncomp;
   }
   return changed;
 }
@@ -195,17 +325,23 @@ fsm_wavefront_kernel(FsmArgs a) {
     const bool has_up = uprow >= 0 && uprow < n;
     const bool has_dn = dnrow >= 0 && dnrow < n;
     const int flow = jasc ? 0 : 1;
-    unsigned long long* tr =
-        (a.trace && k < kTraceSweeps) ? a.trace + ((int64_t)k * a.nstrips + b) * 3 : nullptr;
+    unsigned long long* tr = (a.trace && k < kTraceSweeps)
+                                 ? a.trace + ((int64_t)k * a.nstrips + b) * kTraceWords
+                                 : nullptr;
     if (tr && lane == 0) tr[0] = globaltimer();
 
     // The strip downwind of us in sweep k must have finished sweep k-1: its
     // edge row is our "old" neighbour row, and the hand-off slots it emptied
-    // must be visible before we refill them.  Once per sweep.
+    // must be visible before we refill them.  The strip upwind of us must
+    // have finished sweep k-1 too: its edge row's change bits of sweep k-1
+    // make our first row dirty (when the direction turns it finishes k-1
+    // after us, but before it sends us any value of sweep k).  Once per sweep.
     {
       int ok = 1;
       if (k > 0 && has_dn && lane == 0)
         ok = wait_ge_u64(&a.prog[jasc ? b + 1 : b - 1], (unsigned long long)k, a.status);
+      if (k > 0 && has_up && lane == 0 && ok)
+        ok = wait_ge_u64(&a.prog[jasc ? b - 1 : b + 1], (unsigned long long)k, a.status);
       if (!__shfl_sync(kFull, ok, 0)) return;
     }
     double* dummy = a.u + n * P;  // all +inf
@@ -217,8 +353,16 @@ fsm_wavefront_kernel(FsmArgs a) {
     ch.dnh = has_dn ? a.u + dnrow * P : dummy;
 
     if (tr && lane == 0) tr[1] = globaltimer();
-    const bool changed = iasc ? sweep_strip<true>(a, lane, rowp, ch)
-                              : sweep_strip<false>(a, lane, rowp, ch);
+    // change bits: read sweep k-1's parity, write sweep k's; the first sweep
+    // of a launch evaluates every node (the bits of an earlier launch do not
+    // describe changes made since, e.g. ghost rows set by the host)
+    const int64_t cpar = (n + 3) * a.cw;
+    const unsigned* crd = a.chg + (int64_t)((k + 1) & 1) * cpar;
+    unsigned* cwr = a.chg + (int64_t)(k & 1) * cpar;
+    const unsigned force = (k == 0 || a.noskip) ? 0xFFu : 0u;
+    const bool changed = iasc ? sweep_strip<true>(a, lane, rowp, ch, crd, cwr, force, tr)
+                              : sweep_strip<false>(a, lane, rowp, ch, crd, cwr, force, tr);
+    if (*(volatile int*)a.status == kStatusWatchdog) return;
 
     // sweep complete for this strip: make every lane's writes visible, then
     // publish completion and the change flag (once per sweep).

@@ -27,6 +27,6 @@ for name, p in cases:
         rk = sorted([r for r in rows if r[0] == k], key=lambda r: r[1])
         pick = rk if nstr <= 8 else [rk[0], rk[1], rk[len(rk) // 2], rk[-2], rk[-1]]
         s = "  ".join(f"b{r[1]}:[{(r[2]-t0)/1e3:.1f} w{(r[3]-r[2])/1e3:.1f} "
-                      f"body{(r[4]-r[3])/1e3:.1f}]" for r in pick)
+                      f"body{(r[4]-r[3])/1e3:.1f} p{r[5]} c{r[6]}]" for r in pick)
         print(f" k={k:2d} {s}")
     plan.close()
