@@ -152,6 +152,15 @@ void eik_plan_destroy(eik_plan* plan);
  *                     and downloads overlap); cells[k] may be NULL for
  *                     FMM/FSM and `cells` itself NULL when no solve needs one. */
 int eik_plan_set_ctas(eik_plan* plan, int32_t max_ctas);
+/* eik_plan_set_partitions  strip-Jacobi on one device for an EIK_FSM/EIK_FMM
+ *                     plan: parts of part_rows rows (a multiple of 32; 0 =
+ *                     one exact Gauss-Seidel wavefront, the default) sweep
+ *                     side by side and read each other's edge rows as they
+ *                     were at the end of the previous sweep -- the rounds of
+ *                     the multi-GPU strip decomposition (SURVEY.md 8(e)
+ *                     option A) inside one launch.  Same discrete fixed
+ *                     point; the sweep count is the rounds', not fsm_solve's. */
+int eik_plan_set_partitions(eik_plan* plan, int32_t part_rows);
 int eik_plan_capacity(eik_plan* plan, int32_t* device_ctas, int32_t* fixed_ctas);
 int eik_plan_run_batch(eik_plan* const* plans, int32_t n, eik_output* outs, double* batch_ms);
 int eik_solve_batch(const eik_problem* const* problems, const eik_cells* const* cells,

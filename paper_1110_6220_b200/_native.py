@@ -87,6 +87,7 @@ EXPORTS = {
     "eik_plan_get_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]),
     "eik_plan_set_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]),
     "eik_plan_set_ctas": (C.c_int, [C.c_void_p, C.c_int32]),
+    "eik_plan_set_partitions": (C.c_int, [C.c_void_p, C.c_int32]),
     "eik_plan_capacity": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "eik_plan_run_batch": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(eik_output),
                                      C.POINTER(C.c_double)]),

@@ -25,6 +25,7 @@
 namespace eikb200 {
 
 namespace {
+constexpr double kInfHost = __builtin_huge_val();
 // Concurrent plans (eik_plan_run_batch) need a hardware work queue per
 // stream: with the driver's default of 8, streams share queues and a solve
 // waits behind another stream's persistent kernel.  Read when the CUDA
@@ -273,6 +274,25 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   a.chg = P->dChg;
   a.cw = P->chg_cw;
   a.noskip = std::getenv("EIK_FSM_NOSKIP") ? 1 : 0;
+  a.part_strips = 0;
+  a.snap = nullptr;
+  if (P->part_strips > 0 && P->part_strips < P->nstrips) {
+    const int nb = (P->nstrips - 1) / P->part_strips;
+    const int64_t need = (int64_t)2 * nb * 2 * P->pitch;
+    if (need > P->snap_count) {
+      if (P->dSnap) {
+        pool_release(P->dSnap);
+        P->allocs.erase(std::find(P->allocs.begin(), P->allocs.end(), (void*)P->dSnap));
+        P->dSnap = nullptr;
+      }
+      int rc = dalloc(&P->dSnap, (size_t)need);
+      if (rc) return rc;
+      P->allocs.push_back(P->dSnap);
+      P->snap_count = need;
+    }
+    a.part_strips = P->part_strips;
+    a.snap = P->dSnap;
+  }
   if (std::getenv("EIK_TRACE_FSM")) {
     if (!P->dTrace) {
       int rc = dalloc(&P->dTrace, (size_t)kTraceSweeps * P->nstrips * kTraceWords);
@@ -293,6 +313,8 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   CK(cudaMemsetAsync(P->dDone, 0, sizeof(int) * clear, P->stream));
   CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
                     P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
+  if (a.part_strips > 0)  // part edges read +inf before the first exchange
+    CK(launch_fill(a.snap, P->snap_count, kInfHost, P->stream, &launches));
   int grid = 0;
   CK(launch_fsm(a, P->stream, &launches, &grid));
   out->grid_ctas = grid;
@@ -417,6 +439,8 @@ int plan_sweep(eik_plan* P, int64_t first_sweep, int count, int* changed) {
   a.chg = P->dChg;
   a.cw = P->chg_cw;
   a.noskip = std::getenv("EIK_FSM_NOSKIP") ? 1 : 0;
+  a.part_strips = 0;  // sweep-level control is one Gauss-Seidel wavefront
+  a.snap = nullptr;
   int launches = 0;
   CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
   CK(cudaMemsetAsync(P->dProg, 0, sizeof(unsigned long long) * P->nstrips, P->stream));
@@ -778,6 +802,16 @@ int eik_plan_set_ctas(eik_plan* P, int32_t max_ctas) {
   if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
   if (max_ctas < 0) return fail(EIK_ERR_CONFIG, "max_ctas must be >= 0");
   P->ctas_cap = max_ctas;
+  return EIK_OK;
+}
+
+int eik_plan_set_partitions(eik_plan* P, int32_t part_rows) {
+  if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
+  if (P->method != EIK_FSM && P->method != EIK_FMM)
+    return fail(EIK_ERR_CONFIG, "partitions apply to fsm/fmm plans");
+  if (part_rows < 0 || part_rows % 32 != 0)
+    return fail(EIK_ERR_CONFIG, "part_rows must be a non-negative multiple of 32");
+  P->part_strips = part_rows / 32;
   return EIK_OK;
 }
 

@@ -35,6 +35,13 @@ struct FsmArgs {
   unsigned* chg;
   int64_t cw;               // words per row: ceil(m/32) + kChgWordPad
   int noskip;               // evaluate every node (no clean-step skipping)
+  // Strip-Jacobi partitions (0: one Gauss-Seidel wavefront over all rows):
+  // parts of part_strips strips sweep side by side, reading the neighbouring
+  // part's edge row as it was at the end of the previous sweep from
+  // snap[k&1][boundary][side][P] (side 0: the lower part's top row, side 1:
+  // the upper part's bottom row; padded rows, +inf before the first sweep).
+  int part_strips;
+  double* snap;
 };
 constexpr int64_t kChgWordOff = 3;
 constexpr int64_t kChgWordPad = 8;  // pad words per row (kChgWordOff before, the rest after)
@@ -151,6 +158,7 @@ cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int
                            const double* cost, int64_t n_exit, int* status, cudaStream_t s,
                            int* launches);
 cudaError_t launch_fsm(const FsmArgs& a, cudaStream_t s, int* launches, int* grid = nullptr);
+cudaError_t launch_fill(double* p, int64_t count, double v, cudaStream_t s, int* launches);
 cudaError_t fsm_capacity(int nstrips, int* need, int* ctas);
 
 cudaError_t device_metrics(const double* vm, const double* ve, const double* vt, int64_t M,

@@ -39,6 +39,9 @@ struct eik_plan {
   int* dChanged = nullptr;
   unsigned* dChg = nullptr;   // [2][n+3][chg_cw] change bits (k_fsm.cu)
   int64_t chg_cw = 0;
+  int part_strips = 0;        // strip-Jacobi parts (eik_plan_set_partitions), 0 = exact GS
+  double* dSnap = nullptr;    // [2][boundaries][2] padded rows
+  int64_t snap_count = 0;
   int* dDone = nullptr;
   // two-scale methods: host copies of the inputs (the plan owns them)
   int32_t cells_x = 0, cells_y = 0;

@@ -65,6 +65,9 @@ struct Chan {
   double* gout;           // global mailbox row to the downwind strip (or dummy)
   const double* dnh;      // downwind edge row (old values) in u (or dummy)
   bool in_glob, out_glob; // lane 0 / lane 31 use the mailboxes
+  bool in_snap;           // lane 0 reads the upwind part's snapshot row (gin)
+  double* sw0;            // lane 0 / lane 31 write their row's snapshot (part
+  double* sw31;           // edges of a strip-Jacobi run), or null
 };
 
 // Change bits around one block: the four-neighbour change mask of the kU
@@ -130,7 +133,9 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
   const double* pc = a.C + rowp * P + a.pad + q0off - S * lane;
   const bool in_g = (lane == 0) && ch.in_glob;  // lane 0 reads the upwind mailbox
   const bool dn_lane = (lane == 31);
-  const bool halo_lane = in_g || dn_lane;
+  const bool halo_lane = in_g || dn_lane || ((lane == 0) && ch.in_snap);
+  double* psw = lane == 0 ? ch.sw0 : (lane == 31 ? ch.sw31 : nullptr);
+  if (psw) psw += a.pad + q0off - S * lane;
   double* ph = (lane == 0 ? ch.gin : const_cast<double*>(ch.dnh)) + a.pad + q0off - S * lane;
   double* po = ch.gout + a.pad + q0off - S * lane;
   const bool out_g = dn_lane && ch.out_glob;
@@ -230,6 +235,7 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       um |= (unsigned)upd << t;
       const double ov = upd ? -res : res;
       if (out_g) __stcg(po + S * t, ov);  // straight to L2: the next strip polls it
+      if (psw) __stcg(psw + S * t, res);  // part edge row for the next sweep
       res_prev = res;
       upd_prev = upd;
     }
@@ -264,6 +270,7 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
     pc += S * kU;
     ph += S * kU;
     po += S * kU;
+    if (psw) psw += S * kU;
     q0 += kU;
     cu[0] = cu[kU];
 #pragma unroll
@@ -345,12 +352,30 @@ fsm_wavefront_kernel(FsmArgs a) {
       if (!__shfl_sync(kFull, ok, 0)) return;
     }
     double* dummy = a.u + n * P;  // all +inf
+    // strip-Jacobi partitions: a strip at a part edge reads the neighbouring
+    // part's edge row from the previous sweep's snapshot and writes its own
+    const int ps = a.part_strips;
+    const bool first_of_part = ps > 0 && b > 0 && (b % ps) == 0;
+    const bool last_of_part = ps > 0 && b + 1 < a.nstrips && ((b + 1) % ps) == 0;
+    const bool up_jac = has_up && (jasc ? first_of_part : last_of_part);
+    const bool dn_jac = has_dn && (jasc ? last_of_part : first_of_part);
+    const int nbnd = ps > 0 ? (a.nstrips - 1) / ps : 0;
+    auto snap_row = [&](int par, int bnd, int side) -> double* {
+      return a.snap + ((((int64_t)par * nbnd + bnd) * 2 + side) * P);
+    };
+    const int blo = ps > 0 ? b / ps - 1 : 0, bhi = ps > 0 ? b / ps : 0;  // boundaries below / above
+    const int rd = (k + 1) & 1, wr = k & 1;
     Chan ch;
-    ch.in_glob = has_up;
-    ch.out_glob = has_dn;
-    ch.gin = ch.in_glob ? a.mbox + ((int64_t)flow * a.nstrips + (jasc ? b - 1 : b + 1)) * P : dummy;
+    ch.in_glob = has_up && !up_jac;
+    ch.out_glob = has_dn && !dn_jac;
+    ch.in_snap = up_jac;
+    ch.gin = ch.in_glob ? a.mbox + ((int64_t)flow * a.nstrips + (jasc ? b - 1 : b + 1)) * P
+                        : (up_jac ? (jasc ? snap_row(rd, blo, 0) : snap_row(rd, bhi, 1)) : dummy);
     ch.gout = ch.out_glob ? a.mbox + ((int64_t)flow * a.nstrips + b) * P : dummy;
-    ch.dnh = has_dn ? a.u + dnrow * P : dummy;
+    ch.dnh = dn_jac ? (jasc ? snap_row(rd, bhi, 1) : snap_row(rd, blo, 0))
+                    : (has_dn ? a.u + dnrow * P : dummy);
+    ch.sw0 = up_jac ? (jasc ? snap_row(wr, blo, 1) : snap_row(wr, bhi, 0)) : nullptr;
+    ch.sw31 = dn_jac ? (jasc ? snap_row(wr, bhi, 0) : snap_row(wr, blo, 1)) : nullptr;
 
     if (tr && lane == 0) tr[1] = globaltimer();
     // change bits: read sweep k-1's parity, write sweep k's; the first sweep
@@ -411,7 +436,22 @@ __global__ void mark_exits_kernel(const int64_t* __restrict__ exits,
   }
 }
 
+__global__ void fill_kernel(double* __restrict__ p, int64_t count, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
 }  // namespace
+
+cudaError_t launch_fill(double* p, int64_t count, double v, cudaStream_t s, int* launches) {
+  int64_t blocks = (count + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(p, count, v);
+  *launches += 1;
+  return cudaGetLastError();
+}
 
 cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int64_t n,
                            int64_t P, int64_t pad, double h, const int64_t* exits,

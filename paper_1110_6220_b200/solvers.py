@@ -177,6 +177,12 @@ class Plan:
         """Cap the CTAs of this plan's persistent kernel (0 = whole device)."""
         N.raise_for(N.lib.eik_plan_set_ctas(self._h, int(max_ctas)))
 
+    def set_partitions(self, part_rows: int) -> None:
+        """FSM/FMM plans: strip-Jacobi parts of `part_rows` rows (multiple of
+        32) swept side by side on the device; 0 = one exact Gauss-Seidel
+        wavefront (the default, fsm_solve's order bit for bit)."""
+        N.raise_for(N.lib.eik_plan_set_partitions(self._h, int(part_rows)))
+
     def capacity(self):
         """(CTAs of the persistent kernel the device holds, fixed grid or 0)."""
         d, f = C.c_int32(), C.c_int32()

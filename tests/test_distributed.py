@@ -49,10 +49,12 @@ class OracleStripSweeper:
         self.u[r * self.m:(r + nrows) * self.m] = np.asarray(src)
 
 
-def emulate(problem, world, factory=OracleStripSweeper):
-    """The same rounds in one process: every strip sweeps, then edges swap."""
+def emulate(problem, world, factory=OracleStripSweeper, bounds=None):
+    """The same rounds in one process: every strip sweeps, then edges swap.
+    `bounds` overrides the balanced row split with explicit [r0, r1) strips."""
     m, n = problem.grid.m, problem.grid.n
-    strips = [strip_bounds(n, world, r) for r in range(world)]
+    strips = bounds or [strip_bounds(n, world, r) for r in range(world)]
+    world = len(strips)
     sws = [factory(strip_problem(problem, a, b)) for a, b in strips]
     for s in sws:
         s.set_rows(0, 1, np.full(m, np.inf))
@@ -175,3 +177,28 @@ def test_device_strips_two_ranks_equal_emulation():
     u, k = emulate(p, 2)
     for r in range(2):
         assert np.array_equal(us[r], u) and ks[r][0] == k
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("part_rows,kind", [(32, "chk"), (64, "sin"), (96, "chk")])
+def test_device_partitions_equal_emulation(part_rows, kind):
+    """eik_plan_set_partitions: the strip-Jacobi rounds inside one launch
+    (parts of part_rows rows, edge rows read from the previous sweep) equal
+    the serial emulation of the same rounds bit for bit, sweep count included."""
+    p = _problem(m=61, n=203, kind=kind)
+    n = p.grid.n
+    bounds = [(a, min(a + part_rows, n)) for a in range(0, n, part_rows)]
+    u, k = emulate(p, len(bounds), bounds=bounds)
+    plan = E.Plan(p, "fsm")
+    plan.set_partitions(part_rows)
+    got = np.empty(p.grid.size())
+    o = plan.run(u_host=got)
+    assert np.array_equal(got, u)
+    assert o.sweeps == k
+    plan.set_partitions(0)  # back to the exact wavefront: fsm_solve bit for bit
+    o = plan.run(u_host=got)
+    ref = O.oracle_solve(p, "fsm")
+    assert np.array_equal(got, ref.u) and o.sweeps == ref.sweeps
+    plan.close()
+    with pytest.raises(E.ConfigError):
+        E.Plan(p, "fsm").set_partitions(48)
