@@ -173,6 +173,55 @@ def run_reference(args):
     print(json.dumps(out))
 
 
+def fsm_roof(methods, M, hbm, peak_kind):
+    """Roofline line of the global-sweep kernel (FSM) inside the C2 step."""
+    f = methods.get("fsm")
+    if not f:
+        return None
+    ach = 24.0 * M * f["sweeps"] / (f["solo_ms"] / 1e3) / 1e9
+    return {"bound": "hbm", "kernel": "fsm_wavefront (C2, alone on the GPU)",
+            "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+            "algorithmic_bytes": 24.0 * M * f["sweeps"], "peak_kind": peak_kind,
+            "note": "u + C (67 MB) stay in L2; the fp64 wavefront chain (m + n steps per "
+                    "direction turn) bounds it, not HBM"}
+
+
+def measure_fsm_c5(hbm, peak_kind):
+    """FSM on BASELINE config 5 with the field resident: best of 2 device
+    times, algorithmic bytes 24 B per node per sweep; DRAM
+    traffic per launch from the committed ncu capture of the same solve."""
+    import paper_1110_6220_b200 as E
+    from paper_1110_6220_b200 import configs
+    p5 = configs.config5().problem
+    M5 = p5.grid.m * p5.grid.n
+    plan = E.Plan(p5, "fsm")
+    best = None
+    for _ in range(2):
+        o = plan.run()
+        best = o if best is None or o.device_ms < best.device_ms else best
+    plan.close()
+    del p5
+    traffic = None
+    try:
+        import csv
+        with open(os.path.join(ROOT, "profiles", "r01_fsm_c5_v4_metrics.csv")) as f:
+            rows = [r for r in csv.reader(x for x in f if not x.startswith("=="))]
+        hdr = rows[0]
+        vals = {r[hdr.index("Metric Name")]: float(r[hdr.index("Metric Value")]) for r in rows[1:]}
+        traffic = vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+    except (OSError, ValueError, KeyError, IndexError):
+        pass
+    ms = best.device_ms
+    nbytes = 24.0 * M5 * best.sweeps
+    ach = nbytes / (ms / 1e3) / 1e9
+    return {"workload": "c5_sinsum_32769_64_sources_fsm", "points": M5, "device_ms": round(ms, 3),
+            "sweeps": best.sweeps, "points_per_s": M5 / (ms / 1e3),
+            "roofline": {"bound": "hbm", "kernel": "fsm_wavefront", "achieved": round(ach, 2),
+                         "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
+                         "algorithmic_bytes": nbytes, "peak_kind": peak_kind},
+            "ref_cpu_estimate": "~1-1.3 h on one core (SURVEY 8(d)); not run"}
+
+
 def cpu_baseline_single_core():
     """Single-core reference timing on a bounded sample: one solve of every
     method-config of the matrix except FSM, plus FSM (13 s) -- ~20 s."""
@@ -199,6 +248,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true",
+                    help="skip the config-5 FSM measurement (HBM-scale global sweep)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -340,6 +391,13 @@ def main():
     E.solve_batch(jobs, outs=pinned_u)  # the K steps' solves, uploads and downloads
     e2e_s = (time.perf_counter() - t0) / K
 
+    # the global sweep at BASELINE config 5 (32769^2, 1.07e9 points, u + F ~17 GB):
+    # the one configuration of the path where HBM, not the dependency chain
+    # alone, is in reach; measured after the timed region, rank 0 at N = 1
+    fsm_c5 = None
+    if not args.no_c5 and rank == 0 and world == 1:
+        fsm_c5 = measure_fsm_c5(hbm, peak_kind)
+
     cpu = None if args.no_cpu_baseline or rank != 0 else cpu_baseline_single_core()
     if rank == 0:
         out = {
@@ -360,7 +418,8 @@ def main():
             "e2e": {"value": world * len(rows) * M / e2e_s, "unit": "points/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "single_step_ms": single_step_ms,
-            "roofline": roofline, "cpu_baseline": cpu, "gpu_launches": launches,
+            "roofline": roofline, "roofline_fsm_c2": fsm_roof(methods, M, hbm, peak_kind),
+            "fsm_c5": fsm_c5, "cpu_baseline": cpu, "gpu_launches": launches,
             "clocks": clk.summary(), "methods": methods,
         }
         print(json.dumps(out))
