@@ -25,6 +25,8 @@
 //
 // Counters match the reference: sweeps = first unchanged sweep + 1
 // (classic_solvers.cpp:146-157), node_updates = sweeps * (M - |Q|).
+#include <type_traits>
+
 #include "eik_internal.h"
 #include "k_common.cuh"
 
@@ -192,53 +194,72 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
     wa = wb;
     wb = ld_chgwin(crow, cw, lo_of(blk + 3) - 1);
     unsigned um = 0;
+    // The block's steps.  SLOW: lane 0 found an empty mailbox slot among the
+    // block's prefetched values and polls per step; otherwise the mailbox
+    // costs the steps nothing (no divergent branch on lane 0) and the slots
+    // are re-armed after the block.
+    auto steps = [&](auto slow_tag) {
+      constexpr bool SLOW = decltype(slow_tag)::value;
 #pragma unroll
-    for (int t = 0; t < kU; ++t) {
-      const int q = q0 + t;
-      double h = hv[t];
-      if (in_g && q < m) {
-        if (is_sent(h)) {
-          h = poll_slot(ph + S * t, a.status);
-          ++npoll;
-          // the upwind strip is close ahead: every later slot loaded so far
-          // predates its write too; reload them once instead of polling
-          // each one a round trip apart
+      for (int t = 0; t < kU; ++t) {
+        const int q = q0 + t;
+        double h = hv[t];
+        if (SLOW && in_g && q < m) {
+          if (is_sent(h)) {
+            h = poll_slot(ph + S * t, a.status);
+            ++npoll;
+            // the upwind strip is close ahead: every later slot loaded so far
+            // predates its write too; reload them once instead of polling
+            // each one a round trip apart
 #pragma unroll
-          for (int t2 = t + 1; t2 < kU; ++t2) hv[t2] = __ldcg(ph + S * t2);
+            for (int t2 = t + 1; t2 < kU; ++t2) hv[t2] = __ldcg(ph + S * t2);
 #pragma unroll
-          for (int t2 = 0; t2 < kU; ++t2) nh[t2] = __ldcg(ph + S * (kU + t2));
+            for (int t2 = 0; t2 < kU; ++t2) nh[t2] = __ldcg(ph + S * (kU + t2));
+          }
+          ph[S * t] = sent;  // re-arm the slot for the next sweep
         }
-        ph[S * t] = sent;  // re-arm the slot for the next sweep
-      }
-      // the upwind strip's edge value carries "changed in this sweep" in its sign
-      const bool h_chg = (lane == 0) && q < m && (__double_as_longlong(h) < 0);
-      const bool dirty = ((pm >> t) & 1u) || upd_prev || h_chg;
-      const double cur = cu[t];
-      double res = cur;
-      bool upd = false;
-      if (__any_sync(kFull, dirty)) {
-        ++ncomp;
-        double sv = __shfl_up_sync(kFull, res_prev, 1);
-        double nv = __shfl_down_sync(kFull, cu[t + 1], 1);
-        const double hval = fabs(h);
-        if (lane == 0) sv = hval;
-        if (lane == 31) nv = hval;
-        const double c = cc[t];
-        const double cand = node_update4(cu[t + 1], res_prev, nv, sv, c);
-        upd = (c > 0.0) && (cand < cur);  // exits / padding carry c = -1
-        if (upd) {
-          res = cand;
-          pu[S * t] = cand;
+        // the upwind strip's edge value carries "changed in this sweep" in its sign
+        const bool h_chg = (lane == 0) && q < m && (__double_as_longlong(h) < 0);
+        const bool dirty = ((pm >> t) & 1u) || upd_prev || h_chg;
+        const double cur = cu[t];
+        double res = cur;
+        bool upd = false;
+        if (__any_sync(kFull, dirty)) {
+          ++ncomp;
+          double sv = __shfl_up_sync(kFull, res_prev, 1);
+          double nv = __shfl_down_sync(kFull, cu[t + 1], 1);
+          const double hval = fabs(h);
+          if (lane == 0) sv = hval;
+          if (lane == 31) nv = hval;
+          const double c = cc[t];
+          const double cand = node_update4(cu[t + 1], res_prev, nv, sv, c);
+          upd = (c > 0.0) && (cand < cur);  // exits / padding carry c = -1
+          if (upd) {
+            res = cand;
+            pu[S * t] = cand;
+          }
         }
+        changed |= upd;
+        um |= (unsigned)upd << t;
+        const double ov = upd ? -res : res;
+        if (out_g) __stcg(po + S * t, ov);  // straight to L2: the next strip polls it
+        if (psw) __stcg(psw + S * t, res);  // part edge row for the next sweep
+        res_prev = res;
+        upd_prev = upd;
       }
-      changed |= upd;
-      um |= (unsigned)upd << t;
-      const double ov = upd ? -res : res;
-      if (out_g) __stcg(po + S * t, ov);  // straight to L2: the next strip polls it
-      if (psw) __stcg(psw + S * t, res);  // part edge row for the next sweep
-      res_prev = res;
-      upd_prev = upd;
+      if (!SLOW && in_g) {
+#pragma unroll
+        for (int t = 0; t < kU; ++t)
+          if (q0 + t < m) ph[S * t] = sent;  // re-arm the block's slots
+      }
+    };
+    bool need_poll = false;
+    if (in_g) {
+#pragma unroll
+      for (int t = 0; t < kU; ++t) need_poll |= (q0 + t < m) && is_sent(hv[t]);
     }
+    if (__any_sync(kFull, need_poll)) steps(std::true_type{});
+    else steps(std::false_type{});
     // this block's change bits into the row's words (absolute columns lo..lo+7)
     {
       const int64_t lo = lo_of(blk);
