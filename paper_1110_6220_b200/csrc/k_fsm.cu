@@ -26,6 +26,8 @@
 // Counters match the reference: sweeps = first unchanged sweep + 1
 // (classic_solvers.cpp:146-157), node_updates = sweeps * (M - |Q|).
 #include <type_traits>
+#include <cstdlib>
+#include <algorithm>
 
 #include "eik_internal.h"
 #include "k_common.cuh"
@@ -35,7 +37,8 @@ namespace eikb200 {
 namespace {
 
 constexpr int kU = 8;          // columns per register block (prefetch unit)
-constexpr int kWarpsPerCta = 4;
+constexpr int kWarpsPerCta = 4;  // strips per CTA up to 4 * SMs strips
+constexpr int kMaxWarpsPerCta = 8;
 // Mailbox slots hold a strip's edge-row value for its downwind neighbour; an
 // all-ones NaN marks "empty" (values are never NaN).  The datum is its own
 // flag, so the per-column hand-off needs no fence at all.
@@ -310,11 +313,11 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
   return changed;
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerCta)
+__global__ void __launch_bounds__(32 * kMaxWarpsPerCta)
 fsm_wavefront_kernel(FsmArgs a) {
   const int lane = threadIdx.x & 31;
   const int w = threadIdx.x >> 5;
-  const int b = blockIdx.x * kWarpsPerCta + w;
+  const int b = blockIdx.x * (blockDim.x >> 5) + w;
   if (b >= a.nstrips) return;  // warps past the last grid row do not exist
   const int64_t n = a.n, P = a.P;
 
@@ -490,27 +493,41 @@ cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int
   return cudaGetLastError();
 }
 
+// Strips per CTA: 4, or the same number on every SM when the grid has more
+// strips than 4 per SM (config 5: 1025 strips -> 7 per CTA, one CTA per SM,
+// instead of 1-2 CTAs of 4 per SM whose 8-warp SMs would pace the pipeline).
+static int fsm_wpc(int nstrips) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (const char* e = std::getenv("EIK_FSM_WPC")) return std::max(1, std::min(kMaxWarpsPerCta, std::atoi(e)));
+  if (nstrips <= kWarpsPerCta * sms) return kWarpsPerCta;
+  return std::min(kMaxWarpsPerCta, (nstrips + sms - 1) / sms);
+}
+
 cudaError_t fsm_capacity(int nstrips, int* need, int* ctas) {
   int per_sm = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, fsm_wavefront_kernel, 32 * kWarpsPerCta, 0);
+  const int wpc = fsm_wpc(nstrips);
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fsm_wavefront_kernel,
+                                                                32 * wpc, 0);
   if (e != cudaSuccess) return e;
-  *need = (nstrips + kWarpsPerCta - 1) / kWarpsPerCta;
+  *need = (nstrips + wpc - 1) / wpc;
   *ctas = per_sm * sms;
   return cudaSuccess;
 }
 
 cudaError_t launch_fsm(const FsmArgs& args, cudaStream_t s, int* launches, int* grid) {
-  const int ctas = (args.nstrips + kWarpsPerCta - 1) / kWarpsPerCta;
+  const int wpc = fsm_wpc(args.nstrips);
+  const int ctas = (args.nstrips + wpc - 1) / wpc;
   if (grid) *grid = ctas;
   FsmArgs a = args;
   void* params[] = {&a};
   // Strips spin on each other's progress, so every CTA must be co-resident:
   // a cooperative launch guarantees it (or fails loudly).
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)fsm_wavefront_kernel, dim3(ctas),
-                                              dim3(32 * kWarpsPerCta), params, 0, s);
+                                              dim3(32 * wpc), params, 0, s);
   *launches += 1;
   return e;
 }
