@@ -12,7 +12,12 @@ cases = [("n64", E.build_problem(E.Grid(4096, 64, 1 / 64, 0, 0), E.speed_constan
          ("n256", E.build_problem(E.Grid(4096, 256, 1 / 64, 0, 0), E.speed_constant(),
                                   E.ExitSpec.node_set([(0, 0)]))),
          ("c2", configs.config2().problem)]
+only = sys.argv[2:] if len(sys.argv) > 2 else None
+if only and "c5" in only:
+    cases.append(("c5", configs.config5().problem))
 for name, p in cases:
+    if only and name not in only:
+        continue
     plan = E.Plan(p, "fsm")
     plan.run()
     path = os.path.join(out_dir, f"trace_{name}.txt")
