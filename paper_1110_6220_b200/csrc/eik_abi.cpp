@@ -252,13 +252,13 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method)
   return EIK_OK;
 }
 
-// Line prefetch ahead of the register blocks: only for grids whose u + C
-// do not stay in L2 (EIK_FSM_PF=<blocks>[,l2] overrides).
+// Line prefetch ahead of the register blocks (EIK_FSM_PF=<blocks>[,l2]):
+// off -- on config 5 (u + C 17 GB) it measured 592 ms off vs 622 ms at 4
+// blocks into L1 and 623-624 ms into L2 (profiles/README.md).
 static void fsm_prefetch(const eik_plan* P, FsmArgs& a) {
+  (void)P;
   a.pf_dist = 0;
   a.pf_l2 = 0;
-  const double bytes = 16.0 * (double)(P->g.n + 1) * (double)P->pitch;
-  if (bytes > 96.0e6) a.pf_dist = 4;
   if (const char* e = std::getenv("EIK_FSM_PF")) {
     a.pf_dist = std::atoi(e);
     a.pf_l2 = std::strstr(e, "l2") != nullptr;
