@@ -253,7 +253,6 @@ __device__ __forceinline__ bool cell_sweep_lock(const CellTile& T, int dir, int 
       hs[r] = q_hs[r];
       lk[r] = q_lk[r];
     }
-    load(s + 1);  // prefetch while this step computes (past the end: harmless)
     // phase 1, every slot: the upwind row's new value and unlock bit, and
     // whether the slot processes a node.  The slots' fp64 chains are
     // independent, so they are computed together (phase 2) and overlap;
@@ -278,6 +277,10 @@ __device__ __forceinline__ bool cell_sweep_lock(const CellTile& T, int dir, int 
       proc[r] = act[r] && cc[r] >= 0.0 && (lk[r] != 0 || unW[r] || sbit != 0u);
       any = any || proc[r];
     }
+    // the next step's operands: issued after the shuffles, so the critical
+    // shuffle does not queue behind nine shared loads in the MIO pipe
+    asm volatile("" ::: "memory");
+    load(s + 1);  // prefetch while this step computes (past the end: harmless)
     if (SKIP && !__any_sync(kFull, any)) {
 #pragma unroll
       for (int r = 0; r < NS; ++r) {
