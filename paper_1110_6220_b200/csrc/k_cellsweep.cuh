@@ -106,7 +106,6 @@ __device__ bool cell_sweep_ns(const CellTile& T, int dir, int lane, long long& u
       c_cs[r] = cs[r];
       c_lk[r] = lk[r];
     }
-    if (s < last) load_step(s + 1);  // prefetch while this step computes
     // previous-step results of every slot: slot r's lane 0 reads slot r-1's
     // lane 31, which this step's iteration r-1 is about to overwrite
     double rp_old[NS];
@@ -116,15 +115,24 @@ __device__ bool cell_sweep_ns(const CellTile& T, int dir, int lane, long long& u
       rp_old[r] = res_prev[r];
       nm_old[r] = nmask[r];
     }
+    // new value of the upwind row: lane-1 of this slot, lane 31 of the
+    // previous slot for lane 0 (the frozen halo for sweep row 0, below)
+    double svs[NS];
+#pragma unroll
+    for (int r = 0; r < NS; ++r) {
+      const double send = (lane == 31 && r > 0) ? rp_old[r > 0 ? r - 1 : 0] : rp_old[r];
+      svs[r] = __shfl_sync(kFull, send, (lane + 31) & 31);
+    }
+    // the next step's operands after the shuffles: loads queued ahead of a
+    // shuffle in the MIO pipe would delay it
+    asm volatile("" ::: "memory");
+    if (s < last) load_step(s + 1);  // prefetch while this step computes
 #pragma unroll
     for (int r = 0; r < NS; ++r) {
       const int b = lane + 32 * r;
       const int a = s - b;
       const bool act = rvalid[r] && a >= 0 && a < w;
-      // new value of the upwind row: lane-1 of this slot, lane 31 of the
-      // previous slot for lane 0, the frozen halo for sweep row 0
-      const double send = (lane == 31 && r > 0) ? rp_old[r > 0 ? r - 1 : 0] : rp_old[r];
-      double sv = __shfl_sync(kFull, send, (lane + 31) & 31);
+      double sv = svs[r];
       unsigned sbit = 0u;
       if (MODE == 2) {
         if (lane == 0) sbit = (r > 0) ? (nm_old[r > 0 ? r - 1 : 0] >> 31) & 1u : 0u;
