@@ -252,19 +252,6 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method)
   return EIK_OK;
 }
 
-// Line prefetch ahead of the register blocks (EIK_FSM_PF=<blocks>[,l2]):
-// off -- on config 5 (u + C 17 GB) it measured 592 ms off vs 622 ms at 4
-// blocks into L1 and 623-624 ms into L2 (profiles/README.md).
-static void fsm_prefetch(const eik_plan* P, FsmArgs& a) {
-  (void)P;
-  a.pf_dist = 0;
-  a.pf_l2 = 0;
-  if (const char* e = std::getenv("EIK_FSM_PF")) {
-    a.pf_dist = std::atoi(e);
-    a.pf_l2 = std::strstr(e, "l2") != nullptr;
-  }
-}
-
 int plan_run_fsm(eik_plan* P, eik_output* out) {
   FsmArgs a;
   a.C = P->dC;
@@ -287,7 +274,6 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   a.chg = P->dChg;
   a.cw = P->chg_cw;
   a.noskip = std::getenv("EIK_FSM_NOSKIP") ? 1 : 0;
-  fsm_prefetch(P, a);
   a.part_strips = 0;
   a.snap = nullptr;
   if (P->part_strips > 0 && P->part_strips < P->nstrips) {
@@ -453,7 +439,6 @@ int plan_sweep(eik_plan* P, int64_t first_sweep, int count, int* changed) {
   a.chg = P->dChg;
   a.cw = P->chg_cw;
   a.noskip = std::getenv("EIK_FSM_NOSKIP") ? 1 : 0;
-  fsm_prefetch(P, a);
   a.part_strips = 0;  // sweep-level control is one Gauss-Seidel wavefront
   a.snap = nullptr;
   int launches = 0;

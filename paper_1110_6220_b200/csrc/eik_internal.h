@@ -42,8 +42,6 @@ struct FsmArgs {
   // the upper part's bottom row; padded rows, +inf before the first sweep).
   int part_strips;
   double* snap;
-  int pf_dist;              // prefetch u/C lines this many 8-column blocks ahead (0: off)
-  int pf_l2;                // ... into L2 instead of L1
 };
 constexpr int64_t kChgWordOff = 3;
 constexpr int64_t kChgWordPad = 8;  // pad words per row (kChgWordOff before, the rest after)

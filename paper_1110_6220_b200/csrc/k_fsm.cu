@@ -193,21 +193,6 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       nc[t] = __ldg(pc + S * (kU + t));
       nh[t] = halo_lane ? __ldcg(ph + S * (kU + t)) : kInf;
     }
-    if (a.pf_dist > 0) {
-      // a grid far larger than L2 (config 5): pull the row's u and C lines
-      // pf_dist blocks ahead into L1 (L2 with pf_l2), so the one-block
-      // register prefetch above finds them on chip; clean steps run faster
-      // than one block per DRAM round trip
-      const double* fu = pu + S * (kU * a.pf_dist);
-      const double* fc = pc + S * (kU * a.pf_dist);
-      if (a.pf_l2) {
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(fu));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(fc));
-      } else {
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(fu));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(fc));
-      }
-    }
     const unsigned pm_next = force ? force : chg_mask<IASC>(wa);
     wa = wb;
     wb = ld_chgwin(crow, cw, lo_of(blk + 3) - 1);
