@@ -192,7 +192,8 @@ void plan_free(eik_plan* P) {
   delete P;
 }
 
-int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method) {
+int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
+              bool defer_upload = false) {
   P->method = method;
   P->g = p->grid;
   P->M = p->grid.m * p->grid.n;
@@ -217,9 +218,14 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method)
   track(P->dExitCost);
   if ((rc = dalloc(&P->dStatus, 8))) return rc;
   track(P->dStatus);
-  CK(cudaMemcpyAsync(P->dF, p->speed, sizeof(double) * P->M,
-                     p->speed_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                     P->stream));
+  if (defer_upload) {
+    P->defer_F = p->speed;
+    P->defer_F_dev = p->speed_on_device != 0;
+  } else {
+    CK(cudaMemcpyAsync(P->dF, p->speed, sizeof(double) * P->M,
+                       p->speed_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       P->stream));
+  }
   CK(cudaMemcpyAsync(P->dExit, p->exit_nodes, sizeof(int64_t) * P->n_exit,
                      cudaMemcpyHostToDevice, P->stream));
   CK(cudaMemcpyAsync(P->dExitCost, p->exit_cost, sizeof(double) * P->n_exit,
@@ -367,6 +373,12 @@ int plan_run(eik_plan* P, eik_output* out) {
   out->spec_hits = out->spec_waits = out->spec_self = 0;
   out->grid_ctas = 0;
   CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
+  if (P->defer_F) {  // created by eik_solve_batch: the field goes up now
+    CK(cudaMemcpyAsync(P->dF, P->defer_F, sizeof(double) * P->M,
+                       P->defer_F_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                       P->stream));
+    P->defer_F = nullptr;
+  }
   int rc;
   switch (P->method) {
     case EIK_FSM:
@@ -742,7 +754,15 @@ int eik_set_device(int32_t device) {
   return EIK_OK;
 }
 
+static eik_plan* plan_create(const eik_problem* p, const eik_cells* c, int32_t method,
+                      bool defer_upload);
+
 eik_plan* eik_plan_create(const eik_problem* p, const eik_cells* c, int32_t method) {
+  return plan_create(p, c, method, false);
+}
+
+static eik_plan* plan_create(const eik_problem* p, const eik_cells* c, int32_t method,
+                      bool defer_upload) {
   g_last_code = EIK_OK;
   g_last_error.clear();
   if (check_problem(p) || check_cells(p, c, method)) return nullptr;
@@ -755,7 +775,7 @@ eik_plan* eik_plan_create(const eik_problem* p, const eik_cells* c, int32_t meth
     return nullptr;
   }
   eik_plan* P = new eik_plan();
-  if (plan_init(P, p, c, method)) {
+  if (plan_init(P, p, c, method, defer_upload)) {
     std::string keep = g_last_error;
     int keep_code = g_last_code;
     plan_free(P);
@@ -849,12 +869,13 @@ int eik_solve_batch(const eik_problem* const* problems, const eik_cells* const* 
   std::vector<eik_plan*> plans(n, nullptr);
   std::vector<int> codes(n, EIK_OK);
   std::vector<std::string> msgs(n);
-  {  // uploads overlap: one host thread per problem
+  {  // one host thread per problem; each speed field is uploaded by its
+     // plan's run, in the schedule's order, overlapping earlier solves
     std::vector<std::thread> th;
     for (int k = 0; k < n; ++k)
       th.emplace_back([&, k]() {
         cudaSetDevice(device);
-        plans[k] = eik_plan_create(problems[k], cells ? cells[k] : nullptr, methods[k]);
+        plans[k] = plan_create(problems[k], cells ? cells[k] : nullptr, methods[k], true);
         if (!plans[k]) {
           codes[k] = g_last_code != EIK_OK ? g_last_code : EIK_ERR_CUDA;
           msgs[k] = g_last_error;

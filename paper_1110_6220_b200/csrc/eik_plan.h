@@ -28,6 +28,11 @@ struct eik_plan {
   double* dExitCost = nullptr;
   int* dStatus = nullptr;
   int64_t h2d_bytes = 0;
+  // eik_solve_batch: the speed field is uploaded by the plan's first run, on
+  // its stream, instead of at creation (later plans' uploads overlap earlier
+  // plans' solves)
+  const double* defer_F = nullptr;
+  bool defer_F_dev = false;
   int64_t pitch = 0;       // padded row pitch of dC / dU (m + 2*kPad)
   // FSM wavefront state
   int nstrips = 0;
