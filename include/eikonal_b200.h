@@ -143,7 +143,7 @@ void eik_plan_destroy(eik_plan* plan);
  * eik_plan_run_batch  run n distinct plans of one device as a list
  *                     schedule: each plan's persistent kernel gets a slice of
  *                     whole SMs (heap-cell replays 2 J^(1/4)/sqrt(warps per
- *                     CTA), FSM/FMM their fixed grid, FMSM 2 CTAs, a capped
+ *                     CTA), FSM/FMM their fixed grid, FMSM 16 CTAs, a capped
  *                     plan its cap) and starts as soon as the slice is free.
  *                     *batch_ms = device time from the call until the last
  *                     solve ended.  Returns the first failing plan's code

@@ -1,3 +1,4 @@
+#include <chrono>
 // Host runtime behind the C-ABI (include/eikonal_b200.h): argument checks
 // with the reference's error semantics, device buffers, streams, dispatch to
 // the sm_100a kernels, and SolverOutput packing.  No CPU solver lives here:
@@ -505,8 +506,10 @@ int plan_rows(eik_plan* P, int64_t row0, int64_t nrows, double* host_or_dev, int
 // per step, 4 -> 190 ms; one step alone 332 vs 295 ms).  Admission order:
 // heap-cell replays by that weight (larger first, HCM before FHCM), then the
 // fixed grids, then FMSM -- measured better than ordering by the last run's
-// time (170 ms per step).  FMSM dataflows (a few ms alone) get 2 CTAs, fixed
-// grids what they need, plans capped by the caller their cap.
+// time (170 ms per step).  FMSM dataflows (a few ms alone on the GPU) get 16
+// CTAs: admitted last, they finish the schedule, and a short tail beats a
+// small slice (2 CTAs: ~100 ms at 64-node cells, the step 6-8 % slower and
+// twice as variable); fixed grids get what they need, capped plans their cap.
 struct BatchSlot {
   int sms = 0;        // SMs the plan's grid holds while it runs
   double prio = 0.0;  // admission order
@@ -519,6 +522,11 @@ int batch_slots(eik_plan* const* plans, int n, int budget, std::vector<BatchSlot
   slot.assign(n, BatchSlot{});
   double scale = 2.0;
   if (const char* c = std::getenv("EIK_BATCH_SMS_SCALE")) scale = std::atof(c);
+  int fmsm_ctas = 16;  // C2 step, 3 runs each: 2 -> 432, 4 -> 447, 8 -> 462,
+                       // 16 -> 468 (+-0.6 %), 32 -> 461 M points/s
+  double fmsm_prio = 0.5;
+  if (const char* c = std::getenv("EIK_BATCH_FMSM_CTAS")) fmsm_ctas = std::max(1, std::atoi(c));
+  if (const char* c = std::getenv("EIK_BATCH_FMSM_PRIO")) fmsm_prio = std::atof(c);
   for (int k = 0; k < n; ++k) {
     eik_plan* P = plans[k];
     int dev = 0, fixed = 0;
@@ -536,9 +544,9 @@ int batch_slots(eik_plan* const* plans, int n, int budget, std::vector<BatchSlot
       b.prio = 1.5;
       b.hc = P->method == EIK_HCM || P->method == EIK_FHCM;
     } else if (P->method == EIK_FMSM) {
-      P->run_cap = 2;
-      b.sms = 2;
-      b.prio = 0.5;
+      P->run_cap = fmsm_ctas;
+      b.sms = fmsm_ctas;
+      b.prio = fmsm_prio;
     } else {
       const double J = (double)P->cells_x * P->cells_y;
       const double w =
@@ -866,6 +874,7 @@ int eik_solve_batch(const eik_problem* const* problems, const eik_cells* const* 
     if (!outs[k].u) return fail(EIK_ERR_DOMAIN, "output needs a u buffer");
   int device = 0;
   CK(cudaGetDevice(&device));
+  const auto t_start = std::chrono::steady_clock::now();
   std::vector<eik_plan*> plans(n, nullptr);
   std::vector<int> codes(n, EIK_OK);
   std::vector<std::string> msgs(n);
@@ -883,10 +892,18 @@ int eik_solve_batch(const eik_problem* const* problems, const eik_cells* const* 
       });
     for (auto& t : th) t.join();
   }
+  const auto t_created = std::chrono::steady_clock::now();
   int rc = EIK_OK;
   for (int k = 0; k < n && !rc; ++k)
     if (codes[k]) rc = fail(codes[k], "batch problem " + std::to_string(k) + ": " + msgs[k]);
   if (!rc) rc = plan_run_batch(plans.data(), n, outs, batch_ms);
+  if (std::getenv("EIK_BATCH_TIMING")) {
+    const auto t_end = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "eik_solve_batch: create %.2f ms, run %.2f ms (device %.2f ms)\n",
+                 std::chrono::duration<double, std::milli>(t_created - t_start).count(),
+                 std::chrono::duration<double, std::milli>(t_end - t_created).count(),
+                 batch_ms ? *batch_ms : -1.0);
+  }
   for (eik_plan* P : plans) plan_free(P);
   return rc;
 }
