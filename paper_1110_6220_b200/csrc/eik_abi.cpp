@@ -527,6 +527,8 @@ int batch_slots(eik_plan* const* plans, int n, int budget, std::vector<BatchSlot
   double fmsm_prio = 0.5;
   if (const char* c = std::getenv("EIK_BATCH_FMSM_CTAS")) fmsm_ctas = std::max(1, std::atoi(c));
   if (const char* c = std::getenv("EIK_BATCH_FMSM_PRIO")) fmsm_prio = std::atof(c);
+  int fixed_per_sm = 0;  // FSM/FMM CTAs counted per SM (0: as many as fit)
+  if (const char* c = std::getenv("EIK_BATCH_FIXED_PER_SM")) fixed_per_sm = std::atoi(c);
   for (int k = 0; k < n; ++k) {
     eik_plan* P = plans[k];
     int dev = 0, fixed = 0;
@@ -537,7 +539,8 @@ int batch_slots(eik_plan* const* plans, int n, int budget, std::vector<BatchSlot
     BatchSlot& b = slot[k];
     P->run_cap = 0;
     if (fixed > 0) {
-      b.sms = (fixed + per_sm - 1) / per_sm;
+      const int pf = fixed_per_sm > 0 ? std::min(fixed_per_sm, per_sm) : per_sm;
+      b.sms = (fixed + pf - 1) / pf;
       b.prio = 1.0;
     } else if (P->ctas_cap > 0) {
       b.sms = (std::min(P->ctas_cap, dev) + per_sm - 1) / per_sm;
