@@ -887,11 +887,16 @@ int eik_solve_batch(const eik_problem* const* problems, const eik_cells* const* 
     for (int k = 0; k < n; ++k)
       th.emplace_back([&, k]() {
         cudaSetDevice(device);
+        const auto t0 = std::chrono::steady_clock::now();
         plans[k] = plan_create(problems[k], cells ? cells[k] : nullptr, methods[k], true);
         if (!plans[k]) {
           codes[k] = g_last_code != EIK_OK ? g_last_code : EIK_ERR_CUDA;
           msgs[k] = g_last_error;
         }
+        if (std::getenv("EIK_BATCH_TIMING"))
+          std::fprintf(stderr, "  create %d (method %d): %.2f ms\n", k, methods[k],
+                       std::chrono::duration<double, std::milli>(
+                           std::chrono::steady_clock::now() - t0).count());
       });
     for (auto& t : th) t.join();
   }
