@@ -199,21 +199,23 @@ struct BucketPQ {
   // remove(w) takes it out, rescan(w) renews the bucket's cached minimum --
   // the committer overlaps both with the loads the popped cell needs
   __device__ int argmin(int lane, int& w_out) const {
-    double kl = mk[lane];
-    int il = mi[lane], wl = lane;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ko = __shfl_xor_sync(kFull, kl, o);
-      const int io = __shfl_xor_sync(kFull, il, o);
-      const int wo = __shfl_xor_sync(kFull, wl, o);
-      if (less(ko, io, kl, il)) {
-        kl = ko;
-        il = io;
-        wl = wo;
-      }
-    }
-    w_out = wl;
-    return (!(kl < kInf) && il == 0x7fffffff) ? -1 : il;  // every bucket empty
+    // Keys are cell values: >= 0 or +inf, so their bit patterns (with -0
+    // folded into +0) order like the values; (key, id) is then a 96-bit
+    // unsigned key and three warp min-reductions find the minimum, ties to
+    // the smaller id as the reference heap pops them.
+    const double kl = mk[lane];
+    const int il = mi[lane];
+    const unsigned long long kb =
+        kl == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(kl);
+    const unsigned hi = (unsigned)(kb >> 32), lo = (unsigned)kb;
+    const unsigned mhi = __reduce_min_sync(kFull, hi);
+    const unsigned mlo = __reduce_min_sync(kFull, hi == mhi ? lo : 0xFFFFFFFFu);
+    const bool kmin = hi == mhi && lo == mlo;
+    const unsigned mid = __reduce_min_sync(kFull, kmin ? (unsigned)il : 0xFFFFFFFFu);
+    const unsigned won = __ballot_sync(kFull, kmin && (unsigned)il == mid);
+    w_out = __ffs(won) - 1;
+    const bool empty = mhi == 0x7FF00000u && mlo == 0u && mid == 0x7fffffffu;
+    return empty ? -1 : (int)mid;  // every bucket empty: -1
   }
   __device__ void remove(int lane, int w, int top) {
     if (lane == 0) {
@@ -239,21 +241,22 @@ struct BucketPQ {
         sb = s;
       }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ko = __shfl_xor_sync(kFull, kb, o);
-      const int io = __shfl_xor_sync(kFull, ib, o);
-      const int so = __shfl_xor_sync(kFull, sb, o);
-      if (less(ko, io, kb, ib)) {
-        kb = ko;
-        ib = io;
-        sb = so;
-      }
-    }
+    // warp minimum of (key, id) by three min-reductions (see argmin)
+    const unsigned long long kbits =
+        kb == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(kb);
+    const unsigned hi = (unsigned)(kbits >> 32), lo = (unsigned)kbits;
+    const unsigned mhi = __reduce_min_sync(kFull, hi);
+    const unsigned mlo = __reduce_min_sync(kFull, hi == mhi ? lo : 0xFFFFFFFFu);
+    const bool kmin = hi == mhi && lo == mlo;
+    const unsigned mid = __reduce_min_sync(kFull, kmin ? (unsigned)ib : 0xFFFFFFFFu);
+    const unsigned won = __ballot_sync(kFull, kmin && (unsigned)ib == mid);
+    const int src = __ffs(won) - 1;
+    const double kw = __shfl_sync(kFull, kb, src);
+    const int sw = __shfl_sync(kFull, sb, src);
     if (lane == 0) {
-      mk[w] = kb;
-      mi[w] = ib;
-      msl[w] = sb;
+      mk[w] = kw;
+      mi[w] = (int)mid;
+      msl[w] = sw;
     }
     __syncwarp();
   }
