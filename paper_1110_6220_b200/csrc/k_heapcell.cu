@@ -671,14 +671,6 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       if (lane == 0) atomicExch(a.status, 3);
       break;
     }
-    if (helper) {
-      if (lane == 0) {
-        mbox[0] = cell;
-        mbox[1] = wpop;
-      }
-      named_bar_arrive(kBarQueuePop, 64);  // orders the mailbox stores (BAR drains STS)
-      pending = true;
-    }
     int cxi, cyi;
     cell_xy(cell, g.cells_x, a.cx_magic, cxi, cyi);
     const int nbs[4] = {cxi > 0 ? cell - 1 : -1, cxi + 1 < g.cells_x ? cell + 1 : -1,
@@ -710,6 +702,16 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     st = ld_relaxed_u64_nb(a.state + cell);  // every lane: one warp-wide load each
     svp0 = ld_relaxed_u32_nb(spec_p + cell);
     svc0 = ld_relaxed_u32_nb(spec_c + cell);
+    // hand the pop to the helper only now: the barrier waits for this warp's
+    // earlier memory operations, and the loads above are then already in flight
+    if (helper) {
+      if (lane == 0) {
+        mbox[0] = cell;
+        mbox[1] = wpop;
+      }
+      named_bar_arrive(kBarQueuePop, 64);  // orders the mailbox stores (BAR drains STS)
+      pending = true;
+    }
     // take the cell out of its bucket and renew that bucket's minimum while
     // those loads are in flight (the neighbours sit in other buckets, so
     // neither moves their prefetched positions)
