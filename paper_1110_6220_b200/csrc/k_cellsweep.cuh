@@ -246,6 +246,7 @@ __device__ __forceinline__ bool cell_sweep_lock(const CellTile& T, int dir, int 
   };
   load(0);
   const int last = (h - 1) + (w - 1);
+#pragma unroll 2
   for (int s = 0; s <= last; ++s) {
     double cur[NS], cc[NS], e[NS], ce[NS], n[NS], cn[NS], cs[NS], hs[NS];
     int lk[NS];
