@@ -246,7 +246,12 @@ __device__ __forceinline__ bool cell_sweep_lock(const CellTile& T, int dir, int 
   };
   load(0);
   const int last = (h - 1) + (w - 1);
-#pragma unroll 2
+  // Not unrolled: unrolling by 2 removes ~16 register moves per step and is
+  // 2-11 % faster per solve alone or on its batch slice, but the 14 concurrent
+  // solves of a batch step ran 5 % slower (438 vs 464 M points/s, 3 runs
+  // each) -- the larger loop bodies of the engine variants compete for the
+  // instruction caches of SMs running different solves.
+#pragma unroll 1
   for (int s = 0; s <= last; ++s) {
     double cur[NS], cc[NS], e[NS], ce[NS], n[NS], cn[NS], cs[NS], hs[NS];
     int lk[NS];
