@@ -390,6 +390,10 @@ def main():
     t0 = time.perf_counter()
     E.solve_batch(jobs, outs=pinned_u)  # the K steps' solves, uploads and downloads
     e2e_s = (time.perf_counter() - t0) / K
+    if world > 1:  # the slowest rank's end-to-end time, like the device timing
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
 
     # the global sweep at BASELINE config 5 (32769^2, 1.07e9 points, u + F ~17 GB):
     # the one configuration of the path where HBM, not the dependency chain
