@@ -219,6 +219,7 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
   track(P->dExitCost);
   if ((rc = dalloc(&P->dStatus, 8))) return rc;
   track(P->dStatus);
+  P->deferred = defer_upload;
   if (defer_upload) {
     P->defer_F = p->speed;
     P->defer_F_dev = p->speed_on_device != 0;
@@ -380,6 +381,12 @@ int plan_run(eik_plan* P, eik_output* out) {
                        P->stream));
     P->defer_F = nullptr;
   }
+  for (int s = 0; s < 4; ++s)
+    if (P->defer_probe[s]) {
+      CK(cudaMemcpyAsync(P->dProbe[s], P->defer_probe[s], sizeof(double) * P->probe_len[s],
+                         cudaMemcpyHostToDevice, P->stream));
+      P->defer_probe[s] = nullptr;
+    }
   int rc;
   switch (P->method) {
     case EIK_FSM:

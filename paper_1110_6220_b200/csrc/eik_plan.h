@@ -33,6 +33,9 @@ struct eik_plan {
   // plans' solves)
   const double* defer_F = nullptr;
   bool defer_F_dev = false;
+  bool deferred = false;                      // created with deferred uploads
+  const double* defer_probe[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t probe_len[4] = {0, 0, 0, 0};
   int64_t pitch = 0;       // padded row pitch of dC / dU (m + 2*kPad)
   // FSM wavefront state
   int nstrips = 0;
@@ -53,7 +56,6 @@ struct eik_plan {
   std::vector<int64_t> exit_nodes;
   std::vector<double> exit_cost, exit_points_xy, exit_point_cost;
   std::vector<double> center_speed;
-  std::vector<double> probe[4];
   eikb200::CellGeom cg{};
   int warps_per_cta = 0;
   int32_t* dOrder = nullptr;

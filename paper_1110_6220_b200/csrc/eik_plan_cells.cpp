@@ -52,9 +52,11 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
   }
   if (c->center_speed) P->center_speed.assign(c->center_speed, c->center_speed + J);
   const int64_t vlen = (int64_t)c->cells_x * P->g.n, hlen = (int64_t)c->cells_y * P->g.m;
+  // border-probe speed tables (HCM/FHCM): uploaded straight from the
+  // caller's arrays -- by the first run when the plan defers its uploads
+  // (eik_solve_batch), else now
   const double* tabs[4] = {c->probe_speed_w, c->probe_speed_e, c->probe_speed_s, c->probe_speed_n};
-  for (int s = 0; s < 4; ++s)
-    if (tabs[s]) P->probe[s].assign(tabs[s], tabs[s] + (s < 2 ? vlen : hlen));
+  for (int s = 0; s < 4; ++s) P->probe_len[s] = tabs[s] ? (s < 2 ? vlen : hlen) : 0;
 
   CellGeom& g = P->cg;
   g.m = P->g.m;
@@ -86,10 +88,14 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     if (smem > 227 * 1024)
       return fail(EIK_ERR_NOT_IMPL, "cell too large for the shared-memory tile (max ~110x110 nodes)");
     for (int s = 0; s < 4; ++s) {
-      if ((rc = dalloc(&P->dProbe[s], P->probe[s].size()))) return rc;
+      if ((rc = dalloc(&P->dProbe[s], (size_t)P->probe_len[s]))) return rc;
       P->allocs.push_back(P->dProbe[s]);
-      CK(cudaMemcpyAsync(P->dProbe[s], P->probe[s].data(), sizeof(double) * P->probe[s].size(),
-                         cudaMemcpyHostToDevice, P->stream));
+      if (P->deferred) {
+        P->defer_probe[s] = tabs[s];
+      } else {
+        CK(cudaMemcpyAsync(P->dProbe[s], tabs[s], sizeof(double) * P->probe_len[s],
+                           cudaMemcpyHostToDevice, P->stream));
+      }
     }
     if ((rc = dalloc(&P->dState, J))) return rc;
     P->allocs.push_back(P->dState);
