@@ -119,13 +119,15 @@ __device__ __forceinline__ unsigned chg_mask(const ChgWin& w) {
 // Clean-step skipping (LSM's idea, classic_solvers.cpp:160-212, applied to
 // the exact sweep): a node whose four neighbours did not change since its
 // last evaluation recomputes exactly its old candidate, which cannot be below
-// its value, so skipping it changes nothing.  A step is skipped by the whole
-// warp when no lane's node is dirty: no neighbour changed in the previous
-// sweep (change bits), and neither the upwind column (the lane's previous
-// step) nor the upwind row (lane t-1's previous step, or the upwind strip's
-// edge value, sent with its sign bit set when it changed) changed in this
-// sweep.  Any lane updating at step s makes step s+1 a compute step, so the
-// in-sweep test is one flag per lane.
+// its value, so skipping it changes nothing.  A node is dirty when a
+// neighbour changed in the previous sweep (change bits), or in this sweep its
+// upwind column (the lane's previous step) or upwind row (lane t-1's previous
+// step, or the upwind strip's edge value, sent with its sign bit set when it
+// changed).  The decision is taken per 8-step block by one vote: a block in
+// which no lane has a dirty node at any step, with no update at the step
+// before it, only forwards its old values; any other block computes all 8
+// steps (a per-step vote would sit on the fp64 chain).  While lane 0 waits
+// for mailbox slots (SLOW), the per-step form with its vote is used.
 template <bool IASC>
 __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t rowp,
                                             const Chan& ch, const unsigned* crd, unsigned* cwr,
