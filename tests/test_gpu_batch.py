@@ -137,3 +137,45 @@ def test_batch_rejects_duplicates_and_empty():
         assert outs == [] and ms == 0.0
     finally:
         pl.close()
+
+
+def test_solve_batch_device_speed_equals_solve():
+    """eik_solve_batch with the speed field already on the device
+    (speed_on_device = 1): each plan's run copies it device to device before
+    its solve (the deferred upload), results bit-identical to solve()."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1110_6220_b200 import _native as N
+    from paper_1110_6220_b200 import solvers as S
+
+    p = configs.config1().problem
+    rows = matrix(p, (16,))
+    Fd = torch.from_numpy(np.ascontiguousarray(p.sampled_speed())).cuda()
+    torch.cuda.synchronize()
+    n = len(rows)
+    keep, pp, cc = [], (C.POINTER(N.eik_problem) * n)(), (C.POINTER(N.eik_cells) * n)()
+    meth = (C.c_int32 * n)()
+    res = (N.eik_output * n)()
+    us = []
+    for k, (m, _, cells) in enumerate(rows):
+        cp, kp = S._c_problem(p, p.sampled_speed())
+        cp.speed = C.cast(C.c_void_p(Fd.data_ptr()), C.POINTER(C.c_double))
+        cp.speed_on_device = 1
+        tables = S.cell_tables(p, cells) if cells is not None else None
+        c, kc = S._c_cells(cells, tables)
+        keep += [cp, kp, c, kc]
+        pp[k] = C.pointer(cp)
+        cc[k] = C.pointer(c) if c is not None else C.POINTER(N.eik_cells)()
+        meth[k] = N.METHOD_NAMES[m]
+        u = np.empty(p.grid.size())
+        us.append(u)
+        res[k].u = N.dptr(u)
+        res[k].u_on_device = 0
+    ms = C.c_double()
+    N.raise_for(N.lib.eik_solve_batch(pp, cc, meth, n, res, C.byref(ms)))
+    for k, (m, cs, cells) in enumerate(rows):
+        so = E.solve(p, m, cells)
+        assert bitwise(us[k], so.values), m
+        assert res[k].sweeps == so.sweeps and res[k].heap_removals == so.heap_removals, m
