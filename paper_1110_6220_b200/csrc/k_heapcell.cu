@@ -539,22 +539,23 @@ __device__ __forceinline__ void process_cell(const HcArgs& a, HTile& T, double* 
   const long long p1b = prof ? clock64() : 0;
   const CellTile ct{T.U, T.Ct, T.lock, T.pu, T.w, T.h, 2};
   long long nsw = 0, upd = 0;
-  if (a.fast) {
-    for (int k = 0; k < 4; ++k) {  // process_flagged_once (heap_cell.cpp:150-160)
-      if (!(my_flags & (1u << kFlagOrder[k]))) continue;
-      cell_sweep<2>(ct, kFlagOrder[k], lane, upd);
-      ++nsw;
-    }
-  } else {  // process_to_convergence (heap_cell.cpp:130-147)
-    int perm[4], at = 0;
+  {
+    // FHCM, process_flagged_once (heap_cell.cpp:150-160): one sweep per raised
+    // flag, NE, NW, SE, SW.  HCM, process_to_convergence (:130-147): the
+    // flagged directions first, then the unflagged ones in rotation order,
+    // then the rotation, until a sweep changes nothing.  One call site, so
+    // the kernel holds one copy of each engine variant.
+    int perm[4], nflag = 0;
     for (int k = 0; k < 4; ++k)
-      if (my_flags & (1u << kFlagOrder[k])) perm[at++] = kFlagOrder[k];
+      if (my_flags & (1u << kFlagOrder[k])) perm[nflag++] = kFlagOrder[k];
+    int at = nflag;
     for (int k = 0; k < 4; ++k)
       if (!(my_flags & (1u << kRotation[k]))) perm[at++] = kRotation[k];
     bool changed = true;
-    while (changed) {
+    for (;;) {
+      if (a.fast ? nsw >= nflag : !changed) break;
       const int dir = nsw < 4 ? perm[nsw] : kRotation[nsw % 4];
-      changed = cell_sweep<2>(ct, dir, lane, upd, /*skip=*/nsw >= a.skip_from);
+      changed = cell_sweep<2>(ct, dir, lane, upd, /*skip=*/!a.fast && nsw >= a.skip_from);
       ++nsw;
     }
   }
