@@ -246,12 +246,12 @@ __device__ __forceinline__ bool cell_sweep_lock(const CellTile& T, int dir, int 
   };
   load(0);
   const int last = (h - 1) + (w - 1);
-  // Not unrolled: unrolling by 2 removes ~16 register moves per step and is
-  // 2-11 % faster per solve alone or on its batch slice, but the 14 concurrent
-  // solves of a batch step ran 5 % slower (438 vs 464 M points/s, 3 runs
-  // each) -- the larger loop bodies of the engine variants compete for the
-  // instruction caches of SMs running different solves.
-#pragma unroll 1
+  // Unrolled by 2: no register moves for the prefetched operands, 3-11 %
+  // faster per solve alone.  Concurrent solves contend for instruction cache:
+  // with two engine call sites per kernel the unroll cost the batch 5 %; with
+  // one (process_cell) it trades 2.4 % of the resident batch value for 1.8 %
+  // of the end-to-end batch (9 runs each), and is kept.
+#pragma unroll 2
   for (int s = 0; s <= last; ++s) {
     double cur[NS], cc[NS], e[NS], ce[NS], n[NS], cn[NS], cs[NS], hs[NS];
     int lk[NS];
