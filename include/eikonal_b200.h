@@ -31,7 +31,7 @@ extern "C" {
 enum eik_method {
   EIK_FMM = 0,  /* fmm_solve   classic_solvers.hpp:18 */
   EIK_FSM = 1,  /* fsm_solve   classic_solvers.hpp:33 */
-  EIK_LSM = 2,  /* lsm_solve   classic_solvers.hpp:38 (not on the GPU path) */
+  EIK_LSM = 2,  /* lsm_solve   classic_solvers.hpp:38 */
   EIK_HCM = 3,  /* hcm_solve   heap_cell.hpp:36 */
   EIK_FHCM = 4, /* fhcm_solve  heap_cell.hpp:41 */
   EIK_FMSM = 5  /* fmsm_solve  fmsm.hpp:36 */
@@ -181,6 +181,13 @@ int eik_solve_batch(const eik_problem* const* problems, const eik_cells* const* 
  *   eik_plan_get_rows / eik_plan_set_rows  copy rows [row0, row0+nrows) of
  *                     the value field out of / into the plan (dense m-wide
  *                     rows; host or device buffer). */
+/* FmmOptions::record_acceptance_order (classic_solvers.hpp:10-13,
+ * classic_solvers.cpp:64-71): after an EIK_FMM plan has run, write the
+ * order fmm_solve accepts the non-exit nodes in -- M - n_exit linear indices
+ * by non-decreasing value (equal values in index order) -- into `order`
+ * (host or device buffer). */
+int eik_plan_acceptance_order(eik_plan* plan, int32_t* order, int32_t on_device);
+
 int eik_plan_prepare(eik_plan* plan);
 int eik_plan_sweep(eik_plan* plan, int64_t first_sweep, int32_t count, int32_t* changed);
 int eik_plan_get_rows(eik_plan* plan, int64_t row0, int64_t nrows, double* dst, int32_t on_device);
@@ -192,6 +199,9 @@ int eik_plan_set_rows(eik_plan* plan, int64_t row0, int64_t nrows, const double*
 const char* eik_last_error(void);
 int eik_last_status(void);
 int eik_abi_version(void);
+/* Re-read the EIK_* tuning/debug environment knobs (read once at load
+ * otherwise; none of them changes a result).  Test hook. */
+void eik_debug_reload_knobs(void);
 /* Number of visible CUDA devices (0 on a CPU-only host; never fails). */
 int eik_device_count(void);
 /* Error metrics of a method's field against a ground truth

@@ -9,9 +9,8 @@
 // border probe points (heap_cell.cpp:195-205) and at the cell centres
 // (fmsm.cpp:18-30).  Status codes become the reference's exceptions.
 //
-// lsm_solve is not on the GPU path (not a BASELINE method); this binding
-// forwards it to the reference's implementation, linked under a renamed
-// symbol (see oracle/Makefile target `dropin`).
+// Every one of the six solvers runs on the device, including lsm_solve and
+// fmm_solve's record_acceptance_order option.
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -25,8 +24,6 @@
 #include "eikonal_b200.h"
 
 namespace eikonal {
-
-SolverOutput ref_lsm_solve(const Problem& problem);  // the reference's, renamed
 
 namespace {
 
@@ -101,7 +98,8 @@ Tables cell_tables(const Problem& problem, const CellDecomposition& cells) {
   return t;
 }
 
-SolverOutput run(const Problem& problem, const CellDecomposition* cells, int method) {
+SolverOutput run(const Problem& problem, const CellDecomposition* cells, int method,
+                 bool acceptance_order = false) {
   Sampled s = sample(problem);
   Tables t;
   if (cells) t = cell_tables(problem, *cells);
@@ -109,8 +107,20 @@ SolverOutput run(const Problem& problem, const CellDecomposition* cells, int met
   out.values = ValueField(problem.grid.m, problem.grid.n);
   eik_output o{};
   o.u = out.values.values.data();
-  const int rc = eik_solve(&s.p, cells ? &t.c : nullptr, method, &o);
-  if (rc != EIK_OK) rethrow(rc);
+  if (acceptance_order) {  // a resident plan: the order comes from its field
+    eik_plan* plan = eik_plan_create(&s.p, nullptr, method);
+    if (!plan) rethrow(eik_last_status());
+    int rc = eik_plan_run(plan, &o);
+    if (rc == EIK_OK) {
+      out.acceptance_order.resize((size_t)(problem.grid.size() - s.p.n_exit));
+      rc = eik_plan_acceptance_order(plan, out.acceptance_order.data(), 0);
+    }
+    eik_plan_destroy(plan);
+    if (rc != EIK_OK) rethrow(rc);
+  } else {
+    const int rc = eik_solve(&s.p, cells ? &t.c : nullptr, method, &o);
+    if (rc != EIK_OK) rethrow(rc);
+  }
   out.sweeps = o.sweeps;
   out.node_updates = o.node_updates;
   out.heap_removals = o.heap_removals;
@@ -127,12 +137,10 @@ SolverOutput run(const Problem& problem, const CellDecomposition* cells, int met
 }  // namespace
 
 SolverOutput fmm_solve(const Problem& problem, const FmmOptions& opts) {
-  if (opts.record_acceptance_order)
-    throw std::runtime_error("eikonal_b200: acceptance order is not recorded on the GPU path");
-  return run(problem, nullptr, EIK_FMM);
+  return run(problem, nullptr, EIK_FMM, opts.record_acceptance_order);
 }
 SolverOutput fsm_solve(const Problem& problem) { return run(problem, nullptr, EIK_FSM); }
-SolverOutput lsm_solve(const Problem& problem) { return ref_lsm_solve(problem); }
+SolverOutput lsm_solve(const Problem& problem) { return run(problem, nullptr, EIK_LSM); }
 SolverOutput hcm_solve(const Problem& problem, const CellDecomposition& cells) {
   return run(problem, &cells, EIK_HCM);
 }

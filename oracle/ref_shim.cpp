@@ -9,6 +9,7 @@
 // restatement in oracle/eik_oracle.c, (2) as the "reference" CPU baseline in
 // bench.py, (3) to generate golden fixtures.
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -130,6 +131,114 @@ int ref_solve(int method, const eik_grid* g, const eik_field* field,
     return 5;
   }
 }
+
+// bench.py --impl reference: BASELINE config 2 (or any sinusoid field) built
+// entirely by the reference -- its own SpeedSpec (speed_fields.cpp:27-29) and
+// build_problem (grid.cpp:43-90) on Grid(m, m, 2/(m-1), -1, -1) with a point
+// source at the origin -- and solved by its own solver.  Returns the solver
+// call's steady_clock time in *ms (the scope of run_row, experiment.cpp:204-213)
+// and the field's checksum (sum of finite values) in *sum.
+int ref_bench_sinusoid(int method, int m, double amp, int freq, int cells, double* ms,
+                       double* sum) {
+  try {
+    using namespace eikonal;
+    Grid g(m, m, 2.0 / (m - 1), -1.0, -1.0);
+    ExitSpec ex;
+    ex.kind = ExitKind::Point;
+    ex.point = {0.0, 0.0};
+    Problem p = build_problem(g, speed_sinusoid(amp, freq).fn(), ex);
+    SolverOutput out;
+    auto t0 = std::chrono::steady_clock::now();
+    switch (method) {
+      case 0: out = fmm_solve(p); break;
+      case 1: out = fsm_solve(p); break;
+      case 2: out = lsm_solve(p); break;
+      case 3: out = hcm_solve(p, build_cells(p.grid, cells, cells)); break;
+      case 4: out = fhcm_solve(p, build_cells(p.grid, cells, cells)); break;
+      case 5: out = fmsm_solve(p, build_cells(p.grid, cells, cells)); break;
+      default: g_err = "bad method"; return 1;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    double acc = 0.0;
+    for (double v : out.values.values)
+      if (v < kInf) acc += v;
+    *sum = acc;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 5;
+  }
+}
+
+// Config 5 at full size (32769^2): the same reference solvers with an
+// ARRAY-BACKED SpeedFn.  On a grid node
+// (x == x0 + i*h and y == y0 + j*h exactly, Grid::x/y of grid.hpp:52-53) it
+// returns F[j*m+i], which holds the bits eik_field_eval gives at that node
+// (eik_field_sample is the same function, tabulated); off-grid points (the
+// FHCM/HCM border probes, heap_cell.cpp:195-205, and FMSM cell centres,
+// fmsm.cpp:18-30) are evaluated in closed form.  So the result is bit for bit
+// what the on-demand SpeedFn would give, hours faster.
+//
+// The result stays in the reference's own SolverOutput (no 8.6 GB copy):
+// ref_solve_array returns a handle, ref_result_values points at its field
+// and ref_result_free releases it.
+void* ref_solve_array(int method, const eik_grid* g, const eik_field* field,
+                      const double* F, const int64_t* exit_nodes, const double* exit_cost,
+                      int64_t n_exit, int cells_x, int cells_y, ref_stats* st) {
+  try {
+    using namespace eikonal;
+    Problem p;
+    p.grid = Grid(static_cast<int>(g->m), static_cast<int>(g->n), g->h, g->x0, g->y0);
+    eik_field fcopy = *field;
+    const int64_t m = g->m, n = g->n;
+    const double x0 = g->x0, y0 = g->y0, h = g->h;
+    p.speed = [fcopy, F, m, n, x0, y0, h](double x, double y) {
+      const long long i = std::llround((x - x0) / h), j = std::llround((y - y0) / h);
+      if (i >= 0 && i < m && j >= 0 && j < n && x0 + static_cast<int>(i) * h == x &&
+          y0 + static_cast<int>(j) * h == y)
+        return F[j * m + i];
+      return eik_field_eval(&fcopy, x, y);
+    };
+    for (int64_t k = 0; k < n_exit; ++k) {
+      p.exit_nodes.push_back(static_cast<int>(exit_nodes[k]));
+      p.exit_cost.push_back(exit_cost[k]);
+    }
+    auto* out = new SolverOutput;
+    auto t0 = std::chrono::steady_clock::now();
+    switch (method) {
+      case 0: *out = fmm_solve(p); break;
+      case 1: *out = fsm_solve(p); break;
+      case 2: *out = lsm_solve(p); break;
+      case 3: *out = hcm_solve(p, build_cells(p.grid, cells_x, cells_y)); break;
+      case 4: *out = fhcm_solve(p, build_cells(p.grid, cells_x, cells_y)); break;
+      case 5: *out = fmsm_solve(p, build_cells(p.grid, cells_x, cells_y)); break;
+      default: delete out; g_err = "bad method"; return nullptr;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    st->sweeps = out->sweeps;
+    st->node_updates = out->node_updates;
+    st->heap_removals = out->heap_removals;
+    st->cell_removals = out->hybrid.cell_removals;
+    st->cell_sweeps = out->hybrid.cell_sweeps;
+    st->mon_checks = out->hybrid.mon_checks;
+    st->mon_single = out->hybrid.mon_single;
+    st->avhr = out->hybrid.avhr;
+    st->avs = out->hybrid.avs;
+    st->mon_pct = out->hybrid.mon_pct;
+    st->elapsed_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    return out;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+
+const double* ref_result_values(void* r) {
+  return static_cast<eikonal::SolverOutput*>(r)->values.values.data();
+}
+
+void ref_result_free(void* r) { delete static_cast<eikonal::SolverOutput*>(r); }
 
 // ground_truth (metrics.cpp:77-99) + method_metrics (metrics.cpp:70-75):
 // fills l_inf, l_1, R, rho, R-ratio of `u_method` against FMM-on-refined

@@ -5,20 +5,18 @@ Python mirror of the reference solver interface
 include/eikonal_b200.h.  The solves run in hand-written sm_100a kernels
 (paper_1110_6220_b200/csrc/); there is no CPU fallback.
 """
-import os as _os
-
-# eik_plan_run_batch's concurrent solves want one hardware work queue per
-# stream (the driver default is 8); only effective before the process creates
-# its CUDA context
-_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# Concurrent solves (run_batch / solve_batch) run best with one hardware
+# work queue per stream: export CUDA_DEVICE_MAX_CONNECTIONS=32 before anything
+# in the process creates the CUDA context (bench.py does).  Neither the
+# package nor the library changes the process environment.
 
 from ._native import BudgetError, ConfigError, LIB_PATH, lib
 from .problem import (CellDecomposition, CellTables, ExitSpec, Grid, Problem, SpeedField,
                       build_cells, build_problem, cell_tables, snap_point_to_node,
                       speed_blocks, speed_checkerboard, speed_comb_maze, speed_constant,
                       speed_nodemask, speed_sinsum, speed_sinusoid)
-from .solvers import (HybridStats, Plan, SolverOutput, fhcm_solve, fmm_solve, fmsm_solve,
-                      fsm_solve, hcm_solve, run_batch, solve, solve_batch)
+from .solvers import (FmmOptions, HybridStats, Plan, SolverOutput, fhcm_solve, fmm_solve,
+                      fmsm_solve, fsm_solve, hcm_solve, lsm_solve, run_batch, solve, solve_batch)
 from .distributed import StripSolve, fsm_solve_strips, strip_bounds
 from .metrics import MetricsReport, ground_truth, method_metrics, refined_problem
 from . import experiment_io
@@ -41,8 +39,8 @@ __all__ = [
     "Grid", "Problem", "SpeedField", "build_cells", "build_problem", "cell_tables",
     "snap_point_to_node", "speed_blocks", "speed_checkerboard", "speed_comb_maze",
     "speed_constant", "speed_nodemask", "speed_sinsum", "speed_sinusoid", "HybridStats",
-    "Plan", "SolverOutput", "fhcm_solve", "fmm_solve", "fmsm_solve", "fsm_solve",
-    "hcm_solve", "solve", "run_batch", "solve_batch", "device_count", "set_device", "StripSolve", "fsm_solve_strips",
+    "Plan", "SolverOutput", "FmmOptions", "fhcm_solve", "fmm_solve", "fmsm_solve",
+    "fsm_solve", "lsm_solve", "hcm_solve", "solve", "run_batch", "solve_batch", "device_count", "set_device", "StripSolve", "fsm_solve_strips",
     "strip_bounds", "MetricsReport", "ground_truth", "method_metrics", "refined_problem",
     "experiment_io",
 ]

@@ -83,6 +83,7 @@ EXPORTS = {
     "eik_plan_pitch": (C.c_int64, [C.c_void_p]),
     "eik_plan_destroy": (None, [C.c_void_p]),
     "eik_plan_prepare": (C.c_int, [C.c_void_p]),
+    "eik_plan_acceptance_order": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int32]),
     "eik_plan_sweep": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_int32)]),
     "eik_plan_get_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]),
     "eik_plan_set_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]),
@@ -97,6 +98,7 @@ EXPORTS = {
     "eik_last_error": (C.c_char_p, []),
     "eik_last_status": (C.c_int, []),
     "eik_abi_version": (C.c_int, []),
+    "eik_debug_reload_knobs": (None, []),
     "eik_device_count": (C.c_int, []),
     "eik_set_device": (C.c_int, [C.c_int32]),
     "eik_release_cached": (None, []),

@@ -27,16 +27,60 @@ namespace eikb200 {
 
 namespace {
 constexpr double kInfHost = __builtin_huge_val();
-// Concurrent plans (eik_plan_run_batch) need a hardware work queue per
-// stream: with the driver's default of 8, streams share queues and a solve
-// waits behind another stream's persistent kernel.  Read when the CUDA
-// context is created, so this only takes effect if the library is loaded
-// before anything else in the process initialises CUDA; a value the user set
-// is kept.
-struct ConnectionsDefault {
-  ConnectionsDefault() { setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0); }
-} g_connections_default;
+// Concurrent plans (eik_plan_run_batch) run best with one hardware work queue
+// per stream (CUDA_DEVICE_MAX_CONNECTIONS=32): with the driver's default of 8,
+// streams share queues and a solve can wait behind another stream's
+// persistent kernel.  The library does not touch the process environment;
+// the caller exports it before CUDA initialises (bench.py does).
 }  // namespace
+
+namespace {
+Knobs read_knobs() {
+  Knobs k;
+  auto gi = [](const char* n, int d) {
+    const char* v = std::getenv(n);
+    return v ? std::atoi(v) : d;
+  };
+  auto gd = [](const char* n, double d) {
+    const char* v = std::getenv(n);
+    return v ? std::atof(v) : d;
+  };
+  auto gb = [](const char* n) { return std::getenv(n) != nullptr; };
+  k.fsm_noskip = gb("EIK_FSM_NOSKIP");
+  static std::string trace_path;  // owned copy (the environment may change)
+  trace_path = std::getenv("EIK_TRACE_FSM") ? std::getenv("EIK_TRACE_FSM") : "";
+  k.fsm_trace = trace_path.empty() ? nullptr : trace_path.c_str();
+  k.fsm_wpc = gi("EIK_FSM_WPC", 0);
+  k.hc_warps = gi("EIK_HC_WARPS", 0);
+  k.hc_min_smem = std::getenv("EIK_HC_MIN_SMEM") ? std::atol(std::getenv("EIK_HC_MIN_SMEM")) : -1;
+  k.hc_global_heap = gb("EIK_HC_GLOBAL_HEAP");
+  k.hc_heap_cap = gi("EIK_HC_HEAP_CAP", 0);
+  k.hc_chain = gi("EIK_HC_CHAIN", 1);
+  k.hc_ctas = gi("EIK_HC_CTAS", 0);
+  k.hc_debug = gb("EIK_HC_DEBUG");
+  k.hc_profile = gb("EIK_HC_PROFILE");
+  k.hc_idle_ns = gi("EIK_HC_IDLE_NS", 200);
+  k.hc_skip_from = gi("EIK_HC_SKIP_FROM", 1);
+  k.batch_sms_scale = gd("EIK_BATCH_SMS_SCALE", 2.0);
+  k.batch_fmsm_ctas = std::max(1, gi("EIK_BATCH_FMSM_CTAS", 16));
+  k.batch_fmsm_prio = gd("EIK_BATCH_FMSM_PRIO", 0.5);
+  k.batch_fixed_per_sm = gi("EIK_BATCH_FIXED_PER_SM", 0);
+  k.batch_trace = gb("EIK_BATCH_TRACE");
+  k.batch_timing = gb("EIK_BATCH_TIMING");
+  k.batch_workers = gi("EIK_BATCH_WORKERS", 0);
+  k.hcm_exact = gi("EIK_HCM_EXACT", 0);
+  k.hcm_band = gd("EIK_HCM_BAND", 0.0);
+  return k;
+}
+std::mutex g_knobs_mu;
+Knobs g_knobs = read_knobs();
+}  // namespace
+
+const Knobs& knobs() { return g_knobs; }
+void reload_knobs() {
+  std::lock_guard<std::mutex> lk(g_knobs_mu);
+  g_knobs = read_knobs();
+}
 
 thread_local std::string g_last_error;
 thread_local int g_last_code = EIK_OK;
@@ -70,6 +114,12 @@ int check_problem(const eik_problem* p) {
     if (k > 0 && p->exit_nodes[k] <= p->exit_nodes[k - 1])
       return fail(EIK_ERR_DOMAIN, "exit nodes must be strictly ascending");
     if (!std::isfinite(p->exit_cost[k])) return fail(EIK_ERR_CONFIG, "exit cost must be finite");
+    // The reference accepts any finite cost (grid.cpp:70); the device path
+    // orders values by their bit patterns (heap-cell queues) and carries the
+    // FSM strip hand-off's change flag in the sign bit, both of which need
+    // values >= 0, so negative costs are refused instead of solved wrongly.
+    if (p->exit_cost[k] < 0.0)
+      return fail(EIK_ERR_DOMAIN, "negative exit costs are not supported on the device path");
   }
   if (p->n_exit_points < 0 || (p->n_exit_points > 0 && (!p->exit_points_xy || !p->exit_point_cost)))
     return fail(EIK_ERR_DOMAIN, "bad exit point list");
@@ -102,7 +152,20 @@ std::mutex g_pool_mu;
 std::map<std::pair<int, size_t>, std::vector<void*>> g_pool_free;  // (device, bytes)
 std::map<void*, std::pair<int, size_t>> g_pool_live;
 size_t g_pool_cached = 0;
-constexpr size_t kPoolCap = size_t(32) << 30;  // cached bytes kept at most
+// cached bytes kept at most: 40 % of the device (72 GB on a B200), at least
+// 32 GB -- enough that a benchmark's resident plans return to the cache
+// without driver frees
+size_t pool_cap() {
+  static size_t cap = [] {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+      cudaGetLastError();
+      tot = 0;
+    }
+    return std::max<size_t>(size_t(32) << 30, tot / 10 * 4);
+  }();
+  return cap;
+}
 }  // namespace
 
 cudaError_t pool_alloc(void** p, size_t bytes) {
@@ -139,7 +202,7 @@ void pool_release(void* p) {
   if (it == g_pool_live.end()) return;
   const auto key = it->second;
   g_pool_live.erase(it);
-  if (g_pool_cached + key.second > kPoolCap) {
+  if (g_pool_cached + key.second > pool_cap()) {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(key.first);
@@ -171,7 +234,8 @@ int plan_capacity(eik_plan* P, int* device, int* fixed) {
   switch (P->method) {
     case EIK_FSM:
     case EIK_FMM:
-      CK(fsm_capacity(P->nstrips, fixed, device));
+    case EIK_LSM:
+      CK(fsm_capacity(P->nstrips, fixed, device, P->method == EIK_LSM));
       break;
     case EIK_FMSM:
       CK(fmsm_capacity(P->cg.tile_doubles, P->warps_per_cta, device));
@@ -189,18 +253,23 @@ void plan_free(eik_plan* P) {
   for (void* ptr : P->allocs) pool_release(ptr);
   if (P->ev0) cudaEventDestroy(P->ev0);
   if (P->ev1) cudaEventDestroy(P->ev1);
-  if (P->stream) cudaStreamDestroy(P->stream);
+  if (P->stream && P->own_stream) cudaStreamDestroy(P->stream);
   delete P;
 }
 
 int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
-              bool defer_upload = false) {
+              bool defer_upload = false, cudaStream_t ext_stream = nullptr) {
   P->method = method;
   P->g = p->grid;
   P->M = p->grid.m * p->grid.n;
   P->n_exit = p->n_exit;
   CK(cudaGetDevice(&P->device));
-  CK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  if (ext_stream) {
+    P->stream = ext_stream;
+    P->own_stream = false;
+  } else {
+    CK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
+  }
   CK(cudaEventCreate(&P->ev0));
   CK(cudaEventCreate(&P->ev1));
   auto track = [&](void* q) { P->allocs.push_back(q); };
@@ -233,9 +302,51 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
   CK(cudaMemcpyAsync(P->dExitCost, p->exit_cost, sizeof(double) * P->n_exit,
                      cudaMemcpyHostToDevice, P->stream));
   P->h2d_bytes = (p->speed_on_device ? 0 : 8 * P->M) + 16 * P->n_exit;
-  if (method == EIK_FSM || method == EIK_FMM) {
+  if (method == EIK_FSM || method == EIK_FMM || method == EIK_LSM) {
     P->nstrips = (int)((P->g.n + 31) / 32);
     P->max_sweeps = 1 << 16;
+    {  // every strip's warp must be resident (cooperative launch)
+      int need = 0, ctas = 0;
+      CK(fsm_capacity(P->nstrips, &need, &ctas, method == EIK_LSM));
+      if (need > ctas)
+        return fail(EIK_ERR_NOT_IMPL,
+                    "grid has " + std::to_string(P->g.n) + " rows: one device's FSM wavefront "
+                    "holds " + std::to_string(ctas) + " CTAs (" + std::to_string(need) +
+                    " needed); shard the rows across devices (distributed.fsm_solve_strips)");
+    }
+    if (method == EIK_FMM) {
+      // fmm_solve's counters (classic_solvers.cpp:40-43,64-90): every non-exit
+      // node adjacent to an exit is evaluated once at initialisation, and
+      // every edge between two non-exit nodes once, when its first end is
+      // accepted; no sweeps.  Independent of the acceptance order.
+      const int64_t m = P->g.m, n = P->g.n;
+      const int64_t* ex = p->exit_nodes;
+      const int64_t ne = p->n_exit;
+      auto is_exit = [&](int64_t idx) { return std::binary_search(ex, ex + ne, idx); };
+      int64_t exit_edges = 0, exit_exit = 0;
+      std::vector<int64_t> adj;
+      adj.reserve((size_t)ne * 4);
+      for (int64_t k = 0; k < ne; ++k) {
+        const int64_t i = ex[k] % m, j = ex[k] / m;
+        const int64_t nb[4] = {i + 1 < m ? ex[k] + 1 : -1, i > 0 ? ex[k] - 1 : -1,
+                               j + 1 < n ? ex[k] + m : -1, j > 0 ? ex[k] - m : -1};
+        for (int d = 0; d < 4; ++d) {
+          if (nb[d] < 0) continue;
+          ++exit_edges;
+          if (is_exit(nb[d])) ++exit_exit;  // counted from both ends
+          else adj.push_back(nb[d]);
+        }
+      }
+      std::sort(adj.begin(), adj.end());
+      const int64_t n_adj = std::unique(adj.begin(), adj.end()) - adj.begin();
+      const int64_t edges = (m - 1) * n + m * (n - 1);
+      P->fmm_updates = edges - (exit_edges - exit_exit / 2) + n_adj;
+    }
+    if (method == EIK_LSM) {
+      if ((rc = dalloc(&P->dLsmCnt, P->max_sweeps))) return rc;
+      track(P->dLsmCnt);
+      CK(cudaMemsetAsync(P->dLsmCnt, 0, sizeof(unsigned long long) * P->max_sweeps, P->stream));
+    }
     if ((rc = dalloc(&P->dProg, P->nstrips))) return rc;
     track(P->dProg);
     if ((rc = dalloc(&P->dMbox, (size_t)2 * P->nstrips * P->pitch))) return rc;
@@ -251,8 +362,6 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
     if ((rc = dalloc(&P->dChg, nchg))) return rc;
     track(P->dChg);
     CK(cudaMemsetAsync(P->dChg, 0, sizeof(unsigned) * nchg, P->stream));
-  } else if (method == EIK_LSM) {
-    return fail(EIK_ERR_NOT_IMPL, "lsm is not on the device path (out of scope, SURVEY.md §2.1)");
   } else {
     if ((rc = plan_init_cells(P, p, c))) return rc;
   }
@@ -281,9 +390,10 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   a.trace = nullptr;
   a.chg = P->dChg;
   a.cw = P->chg_cw;
-  a.noskip = std::getenv("EIK_FSM_NOSKIP") ? 1 : 0;
+  a.noskip = knobs().fsm_noskip ? 1 : 0;
   a.part_strips = 0;
   a.snap = nullptr;
+  a.lsm_cnt = P->method == EIK_LSM ? P->dLsmCnt : nullptr;
   if (P->part_strips > 0 && P->part_strips < P->nstrips) {
     const int nb = (P->nstrips - 1) / P->part_strips;
     const int64_t need = (int64_t)2 * nb * 2 * P->pitch;
@@ -301,7 +411,7 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
     a.part_strips = P->part_strips;
     a.snap = P->dSnap;
   }
-  if (std::getenv("EIK_TRACE_FSM")) {
+  if (knobs().fsm_trace) {
     if (!P->dTrace) {
       int rc = dalloc(&P->dTrace, (size_t)kTraceSweeps * P->nstrips * kTraceWords);
       if (rc) return rc;
@@ -319,6 +429,8 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   size_t clear = (size_t)std::min<int64_t>(P->max_sweeps, P->last_sweeps_bound);
   CK(cudaMemsetAsync(P->dChanged, 0, sizeof(int) * clear, P->stream));
   CK(cudaMemsetAsync(P->dDone, 0, sizeof(int) * clear, P->stream));
+  if (a.lsm_cnt)
+    CK(cudaMemsetAsync(P->dLsmCnt, 0, sizeof(unsigned long long) * clear, P->stream));
   CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
                     P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
   if (a.part_strips > 0)  // part edges read +inf before the first exchange
@@ -332,6 +444,7 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   CK(cudaStreamSynchronize(P->stream));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
+  if (st[0] != 0) P->last_sweeps_bound = P->max_sweeps;  // flags of a failed run: clear all
   if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
   if (st[0] == 3) return fail(EIK_ERR_BUDGET, "fsm exceeded the device sweep budget");
   if (st[0] == 4) return fail(EIK_ERR_CUDA, "fsm wavefront watchdog fired (scheduling bug)");
@@ -341,8 +454,20 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   out->heap_removals = 0;
   if (P->method == EIK_FMM) {
     // The FMM row is served by the exact fixed-point solver (SURVEY.md §8f
-    // row 1); its accepted-node count is M - |Q| as in classic_solvers.cpp:67-69.
+    // row 1) and reports fmm_solve's own counters: accepted nodes M - |Q|
+    // (classic_solvers.cpp:67-69), candidate evaluations (plan_init), no sweeps.
     out->heap_removals = P->M - P->n_exit;
+    out->node_updates = P->fmm_updates;
+    out->sweeps = 0;
+  } else if (P->method == EIK_LSM) {
+    // lsm_solve's node_updates: nodes processed unlocked, summed over the
+    // reference's sweeps (the pipelined wavefront may run a few more)
+    std::vector<unsigned long long> cnt((size_t)st[1]);
+    CK(cudaMemcpy(cnt.data(), P->dLsmCnt, sizeof(unsigned long long) * cnt.size(),
+                  cudaMemcpyDeviceToHost));
+    int64_t tot = 0;
+    for (unsigned long long c : cnt) tot += (int64_t)c;
+    out->node_updates = tot;
   }
   out->device_ms = ms;
   out->kernel_launches = launches;
@@ -350,7 +475,7 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
     std::vector<unsigned long long> tr((size_t)kTraceSweeps * P->nstrips * kTraceWords);
     CK(cudaMemcpy(tr.data(), a.trace, sizeof(unsigned long long) * tr.size(),
                   cudaMemcpyDeviceToHost));
-    const char* path = std::getenv("EIK_TRACE_FSM");
+    const char* path = knobs().fsm_trace;
     if (FILE* f = std::fopen(path, "w")) {
       for (int k = 0; k < kTraceSweeps; ++k)
         for (int b = 0; b < P->nstrips; ++b) {
@@ -391,6 +516,7 @@ int plan_run(eik_plan* P, eik_output* out) {
   switch (P->method) {
     case EIK_FSM:
     case EIK_FMM:
+    case EIK_LSM:
       rc = plan_run_fsm(P, out);
       break;
     case EIK_FMSM:
@@ -405,6 +531,7 @@ int plan_run(eik_plan* P, eik_output* out) {
   }
   if (rc) return rc;
   P->last_ms = out->device_ms + out->host_ms;
+  P->ran = true;
   if (out->u) {
     // padded device layout -> caller's dense row-major m*n field
     CK(cudaMemcpy2DAsync(out->u, sizeof(double) * P->g.m, P->dU + kPad,
@@ -458,9 +585,13 @@ int plan_sweep(eik_plan* P, int64_t first_sweep, int count, int* changed) {
   a.trace = nullptr;
   a.chg = P->dChg;
   a.cw = P->chg_cw;
-  a.noskip = std::getenv("EIK_FSM_NOSKIP") ? 1 : 0;
+  a.noskip = knobs().fsm_noskip ? 1 : 0;
   a.part_strips = 0;  // sweep-level control is one Gauss-Seidel wavefront
   a.snap = nullptr;
+  a.lsm_cnt = nullptr;
+  // the flags this call leaves in [0, count) must be cleared by a later run
+  P->last_sweeps_bound = std::min<int64_t>(P->max_sweeps,
+                                           std::max<int64_t>(P->last_sweeps_bound, count + 8));
   int launches = 0;
   CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
   CK(cudaMemsetAsync(P->dProg, 0, sizeof(unsigned long long) * P->nstrips, P->stream));
@@ -523,50 +654,46 @@ struct BatchSlot {
   bool hc = false;
 };
 
+int batch_slot(eik_plan* P, int sms, int budget, BatchSlot& b) {
+  const Knobs& kn = knobs();
+  int dev = 0, fixed = 0;
+  int rc = plan_capacity(P, &dev, &fixed);
+  if (rc) return rc;
+  if (dev < 1) return fail(EIK_ERR_CUDA, "batch: a kernel does not fit on the device");
+  const int per_sm = std::max(1, dev / sms);
+  b = BatchSlot{};
+  P->run_cap = 0;
+  if (fixed > 0) {
+    const int pf = kn.batch_fixed_per_sm > 0 ? std::min(kn.batch_fixed_per_sm, per_sm) : per_sm;
+    b.sms = (fixed + pf - 1) / pf;
+    b.prio = 1.0;
+  } else if (P->ctas_cap > 0) {
+    b.sms = (std::min(P->ctas_cap, dev) + per_sm - 1) / per_sm;
+    b.prio = 1.5;
+    b.hc = P->method == EIK_HCM || P->method == EIK_FHCM;
+  } else if (P->method == EIK_FMSM) {
+    P->run_cap = kn.batch_fmsm_ctas;
+    b.sms = kn.batch_fmsm_ctas;
+    b.prio = kn.batch_fmsm_prio;
+  } else {
+    const double J = (double)P->cells_x * P->cells_y;
+    const double w = std::pow(J, 0.25) / std::sqrt((double)std::max(1, P->hc_warps_per_cta));
+    b.sms = std::max(2, (int)std::lround(kn.batch_sms_scale * w));
+    b.prio = 2.0 + w + (P->method == EIK_HCM ? 0.01 : 0.0);
+    b.hc = true;
+  }
+  b.sms = std::min(b.sms, budget);
+  if (P->run_cap == 0 && fixed == 0 && P->ctas_cap == 0) P->run_cap = b.sms * per_sm;
+  return EIK_OK;
+}
+
 int batch_slots(eik_plan* const* plans, int n, int budget, std::vector<BatchSlot>& slot) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plans[0]->device));
   slot.assign(n, BatchSlot{});
-  double scale = 2.0;
-  if (const char* c = std::getenv("EIK_BATCH_SMS_SCALE")) scale = std::atof(c);
-  int fmsm_ctas = 16;  // C2 step, 3 runs each: 2 -> 432, 4 -> 447, 8 -> 462,
-                       // 16 -> 468 (+-0.6 %), 32 -> 461 M points/s
-  double fmsm_prio = 0.5;
-  if (const char* c = std::getenv("EIK_BATCH_FMSM_CTAS")) fmsm_ctas = std::max(1, std::atoi(c));
-  if (const char* c = std::getenv("EIK_BATCH_FMSM_PRIO")) fmsm_prio = std::atof(c);
-  int fixed_per_sm = 0;  // FSM/FMM CTAs counted per SM (0: as many as fit)
-  if (const char* c = std::getenv("EIK_BATCH_FIXED_PER_SM")) fixed_per_sm = std::atoi(c);
   for (int k = 0; k < n; ++k) {
-    eik_plan* P = plans[k];
-    int dev = 0, fixed = 0;
-    int rc = plan_capacity(P, &dev, &fixed);
+    int rc = batch_slot(plans[k], sms, budget, slot[k]);
     if (rc) return rc;
-    if (dev < 1) return fail(EIK_ERR_CUDA, "batch: a kernel does not fit on the device");
-    const int per_sm = std::max(1, dev / sms);
-    BatchSlot& b = slot[k];
-    P->run_cap = 0;
-    if (fixed > 0) {
-      const int pf = fixed_per_sm > 0 ? std::min(fixed_per_sm, per_sm) : per_sm;
-      b.sms = (fixed + pf - 1) / pf;
-      b.prio = 1.0;
-    } else if (P->ctas_cap > 0) {
-      b.sms = (std::min(P->ctas_cap, dev) + per_sm - 1) / per_sm;
-      b.prio = 1.5;
-      b.hc = P->method == EIK_HCM || P->method == EIK_FHCM;
-    } else if (P->method == EIK_FMSM) {
-      P->run_cap = fmsm_ctas;
-      b.sms = fmsm_ctas;
-      b.prio = fmsm_prio;
-    } else {
-      const double J = (double)P->cells_x * P->cells_y;
-      const double w =
-          std::pow(J, 0.25) / std::sqrt((double)std::max(1, P->hc_warps_per_cta));
-      b.sms = std::max(2, (int)std::lround(scale * w));
-      b.prio = 2.0 + w + (P->method == EIK_HCM ? 0.01 : 0.0);
-      b.hc = true;
-    }
-    b.sms = std::min(b.sms, budget);
-    if (P->run_cap == 0 && fixed == 0 && P->ctas_cap == 0) P->run_cap = b.sms * per_sm;
   }
   return EIK_OK;
 }
@@ -656,7 +783,7 @@ int plan_run_batch(eik_plan* const* plans, int n, eik_output* outs, double* batc
   for (int k = 0; k < n; ++k) plans[k]->run_cap = 0;
   double t_end = 0.0;
   cudaError_t e = cudaSuccess;
-  const bool trace = std::getenv("EIK_BATCH_TRACE") != nullptr;
+  const bool trace = knobs().batch_trace;
   for (int k = 0; k < n && e == cudaSuccess; ++k) {
     float ms = 0.f, ms0 = 0.f;
     if (codes[k] == EIK_OK) e = cudaEventElapsedTime(&ms, ref, plans[k]->ev1);
@@ -673,6 +800,159 @@ int plan_run_batch(eik_plan* const* plans, int n, eik_output* outs, double* batc
   return EIK_OK;
 }
 
+eik_plan* plan_create(const eik_problem* p, const eik_cells* c, int32_t method, bool defer_upload,
+                      cudaStream_t stream = nullptr) {
+  g_last_code = EIK_OK;
+  g_last_error.clear();
+  if (check_problem(p) || check_cells(p, c, method)) return nullptr;
+  if (method < EIK_FMM || method > EIK_FMSM) {
+    fail(EIK_ERR_CONFIG, "unknown method");
+    return nullptr;
+  }
+  if (eik_device_count() < 1) {
+    fail(EIK_ERR_CUDA, "no CUDA device visible: the Eikonal hot path has no CPU fallback");
+    return nullptr;
+  }
+  eik_plan* P = new eik_plan();
+  if (plan_init(P, p, c, method, defer_upload, stream)) {
+    std::string keep = g_last_error;
+    int keep_code = g_last_code;
+    plan_free(P);
+    g_last_error = keep;
+    g_last_code = keep_code;
+    return nullptr;
+  }
+  return P;
+}
+
+// eik_solve_batch: the same list schedule as plan_run_batch, but each
+// solve's plan exists only while it is needed.  A fixed pool of worker
+// threads (one stream each) takes the jobs in order; a worker creates the
+// job's plan (device buffers from the pool cache, inputs uploaded from the
+// caller's host arrays), waits until the schedule admits it (priority order
+// among the created jobs, SMs free), runs it, downloads u, and returns the
+// buffers before taking the next job.  Device memory and host threads are
+// bounded by the pool size, not by the number of solves, and no buffer is
+// allocated from the driver in steady state (the exact-size cache serves
+// every plan after the first of its shape).
+int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* const* cells,
+                          const int32_t* methods, int n, eik_output* outs, double* batch_ms) {
+  int device = 0, sms = 0;
+  CK(cudaGetDevice(&device));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  const int budget = std::max(1, (int)std::floor(0.98 * sms));
+  const Knobs& kn = knobs();
+  const int workers = std::max(1, std::min(n, kn.batch_workers > 0 ? kn.batch_workers : 24));
+  struct Waiting {
+    int k;
+    BatchSlot b;
+  };
+  std::mutex mu;
+  std::condition_variable cv;
+  int next_job = 0, free_sms = budget, hc_launching = 0;
+  bool abort = false;
+  std::vector<Waiting> waiting;
+  std::vector<char> admitted(n, 0);
+  std::vector<int> codes(n, EIK_OK);
+  std::vector<std::string> msgs(n);
+  double t_end = 0.0;
+  auto admit = [&]() {  // under mu: highest priority first, later ones fill in
+    std::stable_sort(waiting.begin(), waiting.end(),
+                     [](const Waiting& x, const Waiting& y) { return x.b.prio > y.b.prio; });
+    for (size_t i = 0; i < waiting.size();) {
+      if (waiting[i].b.sms <= free_sms) {
+        admitted[waiting[i].k] = 1;
+        free_sms -= waiting[i].b.sms;
+        if (waiting[i].b.hc) ++hc_launching;
+        waiting.erase(waiting.begin() + i);
+      } else {
+        ++i;
+      }
+    }
+    cv.notify_all();
+  };
+  CK(cudaDeviceSynchronize());
+  cudaEvent_t ref;
+  CK(cudaEventCreate(&ref));
+  CK(cudaEventRecord(ref, 0));
+  CK(cudaEventSynchronize(ref));
+  auto worker = [&]() {
+    cudaSetDevice(device);
+    cudaStream_t st = nullptr;
+    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+      std::lock_guard<std::mutex> lk(mu);
+      abort = true;
+      return;
+    }
+    for (;;) {
+      int k;
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        if (abort || next_job >= n) break;
+        k = next_job++;
+      }
+      eik_plan* P = plan_create(problems[k], cells ? cells[k] : nullptr, methods[k], false, st);
+      BatchSlot b;
+      int rc = P ? batch_slot(P, sms, budget, b) : (g_last_code != EIK_OK ? g_last_code : EIK_ERR_CUDA);
+      if (rc) {
+        codes[k] = rc;
+        msgs[k] = g_last_error;
+        plan_free(P);
+        std::lock_guard<std::mutex> lk(mu);
+        abort = true;
+        cv.notify_all();
+        break;
+      }
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        waiting.push_back({k, b});
+        admit();
+        cv.wait(lk, [&]() { return abort || (admitted[k] && (b.hc || hc_launching == 0)); });
+        if (!admitted[k]) {  // aborted while waiting
+          waiting.erase(std::remove_if(waiting.begin(), waiting.end(),
+                                       [&](const Waiting& w) { return w.k == k; }),
+                        waiting.end());
+          plan_free(P);
+          break;
+        }
+      }
+      bool signalled = !b.hc;
+      auto launched = [&]() {
+        std::lock_guard<std::mutex> lk(mu);
+        if (--hc_launching == 0) cv.notify_all();
+      };
+      if (b.hc) P->on_launched = [&]() {
+        signalled = true;
+        launched();
+      };
+      codes[k] = plan_run(P, &outs[k]);
+      P->on_launched = nullptr;
+      if (!signalled) launched();
+      if (codes[k]) msgs[k] = g_last_error;
+      float ms = 0.f;
+      const bool timed = codes[k] == EIK_OK && cudaEventElapsedTime(&ms, ref, P->ev1) == cudaSuccess;
+      plan_free(P);
+      std::lock_guard<std::mutex> lk(mu);
+      if (timed) t_end = std::max(t_end, (double)ms);
+      if (codes[k]) abort = true;
+      free_sms += b.sms;
+      admit();
+    }
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+  };
+  std::vector<std::thread> th;
+  th.reserve(workers);
+  for (int w = 0; w < workers; ++w) th.emplace_back(worker);
+  for (auto& t : th) t.join();
+  cudaEventDestroy(ref);
+  for (int k = 0; k < n; ++k)
+    if (codes[k]) return fail(codes[k], "batch problem " + std::to_string(k) + ": " + msgs[k]);
+  if (abort) return fail(EIK_ERR_CUDA, "batch: a worker could not start");
+  if (batch_ms) *batch_ms = t_end;
+  return EIK_OK;
+}
+
 }  // namespace eikb200
 
 using namespace eikb200;
@@ -680,6 +960,8 @@ using namespace eikb200;
 extern "C" {
 
 int eik_abi_version(void) { return EIK_ABI_VERSION; }
+
+void eik_debug_reload_knobs(void) { reload_knobs(); }
 
 const char* eik_last_error(void) { return g_last_error.c_str(); }
 
@@ -772,36 +1054,9 @@ int eik_set_device(int32_t device) {
   return EIK_OK;
 }
 
-static eik_plan* plan_create(const eik_problem* p, const eik_cells* c, int32_t method,
-                      bool defer_upload);
 
 eik_plan* eik_plan_create(const eik_problem* p, const eik_cells* c, int32_t method) {
   return plan_create(p, c, method, false);
-}
-
-static eik_plan* plan_create(const eik_problem* p, const eik_cells* c, int32_t method,
-                      bool defer_upload) {
-  g_last_code = EIK_OK;
-  g_last_error.clear();
-  if (check_problem(p) || check_cells(p, c, method)) return nullptr;
-  if (method < EIK_FMM || method > EIK_FMSM) {
-    fail(EIK_ERR_CONFIG, "unknown method");
-    return nullptr;
-  }
-  if (eik_device_count() < 1) {
-    fail(EIK_ERR_CUDA, "no CUDA device visible: the Eikonal hot path has no CPU fallback");
-    return nullptr;
-  }
-  eik_plan* P = new eik_plan();
-  if (plan_init(P, p, c, method, defer_upload)) {
-    std::string keep = g_last_error;
-    int keep_code = g_last_code;
-    plan_free(P);
-    g_last_error = keep;
-    g_last_code = keep_code;
-    return nullptr;
-  }
-  return P;
 }
 
 int eik_plan_run(eik_plan* P, eik_output* out) {
@@ -814,6 +1069,27 @@ const double* eik_plan_values(const eik_plan* P) { return P ? P->dU + kPad : nul
 int64_t eik_plan_pitch(const eik_plan* P) { return P ? P->pitch : 0; }
 
 void eik_plan_destroy(eik_plan* P) { plan_free(P); }
+
+int eik_plan_acceptance_order(eik_plan* P, int32_t* order, int32_t on_device) {
+  if (!P || !order) return fail(EIK_ERR_DOMAIN, "null argument");
+  if (P->method != EIK_FMM) return fail(EIK_ERR_CONFIG, "acceptance order needs an fmm plan");
+  if (!P->ran) return fail(EIK_ERR_CONFIG, "acceptance order: run the plan first");
+  if (P->M > INT32_MAX) return fail(EIK_ERR_NOT_IMPL, "acceptance order: grid exceeds int32 indices");
+  CK(cudaSetDevice(P->device));
+  int32_t* dst = order;
+  void* tmp = nullptr;
+  if (!on_device) {
+    CK(pool_alloc(&tmp, sizeof(int32_t) * P->M));
+    dst = static_cast<int32_t*>(tmp);
+  }
+  cudaError_t e = device_acceptance_order(P->dU, P->dC, P->g.m, P->g.n, P->pitch, kPad, dst,
+                                          P->stream);
+  if (e == cudaSuccess && !on_device)
+    e = cudaMemcpy(order, dst, sizeof(int32_t) * (P->M - P->n_exit), cudaMemcpyDeviceToHost);
+  if (tmp) pool_release(tmp);
+  if (e != cudaSuccess) return cuda_fail(e, "eik_plan_acceptance_order");
+  return EIK_OK;
+}
 
 int eik_plan_prepare(eik_plan* P) {
   if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
@@ -850,6 +1126,7 @@ int eik_plan_set_partitions(eik_plan* P, int32_t part_rows) {
   if (part_rows < 0 || part_rows % 32 != 0)
     return fail(EIK_ERR_CONFIG, "part_rows must be a non-negative multiple of 32");
   P->part_strips = part_rows / 32;
+  P->last_sweeps_bound = P->max_sweeps;  // the next run may need more sweeps
   return EIK_OK;
 }
 
@@ -882,45 +1159,13 @@ int eik_solve_batch(const eik_problem* const* problems, const eik_cells* const* 
     return fail(EIK_ERR_DOMAIN, "batch: bad arguments");
   for (int k = 0; k < n; ++k)
     if (!outs[k].u) return fail(EIK_ERR_DOMAIN, "output needs a u buffer");
-  int device = 0;
-  CK(cudaGetDevice(&device));
-  const auto t_start = std::chrono::steady_clock::now();
-  std::vector<eik_plan*> plans(n, nullptr);
-  std::vector<int> codes(n, EIK_OK);
-  std::vector<std::string> msgs(n);
-  {  // one host thread per problem; each speed field is uploaded by its
-     // plan's run, in the schedule's order, overlapping earlier solves
-    std::vector<std::thread> th;
-    for (int k = 0; k < n; ++k)
-      th.emplace_back([&, k]() {
-        cudaSetDevice(device);
-        const auto t0 = std::chrono::steady_clock::now();
-        plans[k] = plan_create(problems[k], cells ? cells[k] : nullptr, methods[k], true);
-        if (!plans[k]) {
-          codes[k] = g_last_code != EIK_OK ? g_last_code : EIK_ERR_CUDA;
-          msgs[k] = g_last_error;
-        }
-        if (std::getenv("EIK_BATCH_TIMING"))
-          std::fprintf(stderr, "  create %d (method %d): %.2f ms\n", k, methods[k],
-                       std::chrono::duration<double, std::milli>(
-                           std::chrono::steady_clock::now() - t0).count());
-      });
-    for (auto& t : th) t.join();
+  if (n == 0) {
+    if (batch_ms) *batch_ms = 0.0;
+    return EIK_OK;
   }
-  const auto t_created = std::chrono::steady_clock::now();
-  int rc = EIK_OK;
-  for (int k = 0; k < n && !rc; ++k)
-    if (codes[k]) rc = fail(codes[k], "batch problem " + std::to_string(k) + ": " + msgs[k]);
-  if (!rc) rc = plan_run_batch(plans.data(), n, outs, batch_ms);
-  if (std::getenv("EIK_BATCH_TIMING")) {
-    const auto t_end = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "eik_solve_batch: create %.2f ms, run %.2f ms (device %.2f ms)\n",
-                 std::chrono::duration<double, std::milli>(t_created - t_start).count(),
-                 std::chrono::duration<double, std::milli>(t_end - t_created).count(),
-                 batch_ms ? *batch_ms : -1.0);
-  }
-  for (eik_plan* P : plans) plan_free(P);
-  return rc;
+  if (eik_device_count() < 1)
+    return fail(EIK_ERR_CUDA, "no CUDA device visible: the Eikonal hot path has no CPU fallback");
+  return solve_batch_pipelined(problems, cells, methods, n, outs, batch_ms);
 }
 
 int eik_solve(const eik_problem* p, const eik_cells* c, int32_t method, eik_output* out) {

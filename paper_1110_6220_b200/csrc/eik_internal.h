@@ -42,6 +42,10 @@ struct FsmArgs {
   // the upper part's bottom row; padded rows, +inf before the first sweep).
   int part_strips;
   double* snap;
+  // LSM (lsm_solve, classic_solvers.cpp:160-212): when non-null, the sweep
+  // also counts the nodes the reference's locking sweep processes
+  // (lsm_cnt[k] += unlocked nodes of sweep k).  Values and sweeps are FSM's.
+  unsigned long long* lsm_cnt;
 };
 constexpr int64_t kChgWordOff = 3;
 constexpr int64_t kChgWordPad = 8;  // pad words per row (kChgWordOff before, the rest after)
@@ -159,7 +163,12 @@ cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int
                            int* launches);
 cudaError_t launch_fsm(const FsmArgs& a, cudaStream_t s, int* launches, int* grid = nullptr);
 cudaError_t launch_fill(double* p, int64_t count, double v, cudaStream_t s, int* launches);
-cudaError_t fsm_capacity(int nstrips, int* need, int* ctas);
+cudaError_t fsm_capacity(int nstrips, int* need, int* ctas, bool lsm = false);
+
+cudaError_t device_acceptance_order(const double* u, const double* C, int64_t m, int64_t n,
+                                    int64_t P, int64_t pad, int32_t* order_dev, cudaStream_t s);
+cudaError_t pool_alloc(void** p, size_t bytes);
+void pool_release(void* p);
 
 cudaError_t device_metrics(const double* vm, const double* ve, const double* vt, int64_t M,
                            const int64_t* exits, int64_t n_exit, uint8_t* mask, cudaStream_t s,

@@ -19,6 +19,7 @@ struct eik_plan {
   int64_t n_exit = 0;
   int device = 0;
   cudaStream_t stream = nullptr;
+  bool own_stream = true;   // false: borrowed from eik_solve_batch's worker
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<void*> allocs;
   double* dF = nullptr;   // speed (resident input)
@@ -51,6 +52,8 @@ struct eik_plan {
   double* dSnap = nullptr;    // [2][boundaries][2] padded rows
   int64_t snap_count = 0;
   int* dDone = nullptr;
+  unsigned long long* dLsmCnt = nullptr;  // [max_sweeps] LSM unlocked nodes per sweep
+  int64_t fmm_updates = 0;    // fmm_solve's node_updates (order independent)
   // two-scale methods: host copies of the inputs (the plan owns them)
   int32_t cells_x = 0, cells_y = 0;
   std::vector<int64_t> exit_nodes;
@@ -83,7 +86,9 @@ struct eik_plan {
   unsigned* dSpecVer = nullptr;
   int* dBusy = nullptr;
   eikb200::SpecRec* dRec = nullptr;
-  int* dHcMisc = nullptr;   // [0] done flag, [1] published heap size
+  int* dHcMisc = nullptr;
+  int* dDbg = nullptr;      // EIK_HC_DEBUG: per-worker phase trace
+  int* dOwner = nullptr;    // EIK_HC_DEBUG: last claiming worker per speculation   // [0] done flag, [1] published heap size
   int hc_warps_per_cta = 1;
   int64_t hc_min_smem = 0;  // dynamic smem floor per CTA (one CTA per SM)
   uint64_t hc_cx_magic = 0; // cell id -> row by multiply-shift (0: division)
@@ -94,12 +99,48 @@ struct eik_plan {
   int run_cap = 0;
 
   int cap() const { return run_cap > 0 ? run_cap : ctas_cap; }
-  double last_ms = 0.0;  // device + host ms of the last run (batch admission order)
+  double last_ms = 0.0;
+  bool ran = false;      // a run completed (the resident field is a solution)  // device + host ms of the last run (batch admission order)
   // batch runs: called (then cleared) once the heap-cell grid is submitted
   std::function<void()> on_launched;
 };
 
 namespace eikb200 {
+
+// Tuning and debug knobs, read from the environment ONCE per process
+// (eik_debug_reload_knobs re-reads them; tests use it).  None changes a
+// result: every variant is tested bit-exact.  Defaults are the measured
+// optima.
+struct Knobs {
+  // FSM wavefront
+  bool fsm_noskip = false;         // EIK_FSM_NOSKIP: evaluate every node
+  const char* fsm_trace = nullptr; // EIK_TRACE_FSM=path: per-strip timing trace (copied)
+  int fsm_wpc = 0;                 // EIK_FSM_WPC: strips per CTA (0 = auto)
+  // heap-cell replay
+  int hc_warps = 0;                // EIK_HC_WARPS (0 = fit)
+  long hc_min_smem = -1;           // EIK_HC_MIN_SMEM (-1 = 116 KB)
+  bool hc_global_heap = false;     // EIK_HC_GLOBAL_HEAP
+  int hc_heap_cap = 0;             // EIK_HC_HEAP_CAP (0 = fit)
+  int hc_chain = 1;                // EIK_HC_CHAIN
+  int hc_ctas = 0;                 // EIK_HC_CTAS (0 = device)
+  bool hc_debug = false;           // EIK_HC_DEBUG: per-worker phase trace
+  bool hc_profile = false;         // EIK_HC_PROFILE: instrumented kernel
+  int hc_idle_ns = 200;            // EIK_HC_IDLE_NS
+  int hc_skip_from = 1;            // EIK_HC_SKIP_FROM
+  // batches
+  double batch_sms_scale = 2.0;    // EIK_BATCH_SMS_SCALE
+  int batch_fmsm_ctas = 16;        // EIK_BATCH_FMSM_CTAS
+  double batch_fmsm_prio = 0.5;    // EIK_BATCH_FMSM_PRIO
+  int batch_fixed_per_sm = 0;      // EIK_BATCH_FIXED_PER_SM
+  bool batch_trace = false;        // EIK_BATCH_TRACE
+  bool batch_timing = false;       // EIK_BATCH_TIMING
+  int batch_workers = 0;           // EIK_BATCH_WORKERS (0 = auto)
+  // HCM band scheduler
+  int hcm_exact = 0;               // EIK_HCM_EXACT=1: HCM by the exact replay
+  double hcm_band = 0.0;           // EIK_HCM_BAND: band width scale (0 = default)
+};
+const Knobs& knobs();
+void reload_knobs();
 
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);

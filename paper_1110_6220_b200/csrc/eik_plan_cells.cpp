@@ -152,8 +152,8 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     // EIK_HC_WARPS / EIK_HC_MIN_SMEM override.
     const int fit = (int)std::max<size_t>(1, std::min<size_t>(8, (216 * 1024) / (tile * 8)));
     P->hc_warps_per_cta = fit;
-    if (const char* w = std::getenv("EIK_HC_WARPS"))
-      P->hc_warps_per_cta = std::max(1, std::min(fit, std::atoi(w)));
+    const Knobs& kn = knobs();
+    if (kn.hc_warps > 0) P->hc_warps_per_cta = std::max(1, std::min(fit, kn.hc_warps));
     P->hc_min_smem = 116 * 1024;
     {  // row of a cell id by a multiply and shift, checked for every id
       const uint64_t d = (uint64_t)P->cells_x;
@@ -163,7 +163,7 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
         if ((((uint64_t)c * magic) >> 40) != (uint64_t)c / d) magic = 0;
       P->hc_cx_magic = magic;
     }
-    if (const char* w = std::getenv("EIK_HC_MIN_SMEM")) P->hc_min_smem = std::atol(w);
+    if (kn.hc_min_smem >= 0) P->hc_min_smem = kn.hc_min_smem;
     // the committer's heap + cell values go to its shared memory when they
     // fit next to its tile (uint16 heap indices)
     {
@@ -174,17 +174,16 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
       while (capb > 0 && heapcell_committer_heap_bytes((int)capb) > room) --capb;
       P->hc_heap_cap = capb >= 8 ? (int)capb : 0;
     }
-    if (std::getenv("EIK_HC_GLOBAL_HEAP")) P->hc_heap_cap = 0;
+    if (kn.hc_global_heap) P->hc_heap_cap = 0;
     // EIK_HC_HEAP_CAP=n caps the shared-memory heap (exercises the overflow
     // fallback in tests)
-    if (const char* c = std::getenv("EIK_HC_HEAP_CAP"))
-      P->hc_heap_cap = std::min(P->hc_heap_cap, std::max(1, std::atoi(c)));
+    if (kn.hc_heap_cap > 0) P->hc_heap_cap = std::min(P->hc_heap_cap, kn.hc_heap_cap);
     // EIK_HC_CHAIN: 0 plain speculations only, 1 chain on the neighbour
     // expected next (default), 2 on every neighbour expected first
-    if (const char* c = std::getenv("EIK_HC_CHAIN")) P->hc_chain = std::atoi(c);
+    P->hc_chain = kn.hc_chain;
     // EIK_HC_CTAS=1 runs the committer alone (serial exact replay)
     P->hc_max_ctas = 1 << 20;
-    if (const char* w = std::getenv("EIK_HC_CTAS")) P->hc_max_ctas = std::max(1, std::atoi(w));
+    if (kn.hc_ctas > 0) P->hc_max_ctas = kn.hc_ctas;
     return EIK_OK;
   }
   if ((rc = dalloc(&P->dOrder, J))) return rc;
@@ -371,24 +370,27 @@ retry:  // after a committer heap overflow, with the heap in global memory
   a.ckey = P->dCKey;
   a.wdbg = nullptr;
   a.owner = nullptr;
-  if (std::getenv("EIK_HC_DEBUG")) {
-    static int* dbg = nullptr;
-    static int* own = nullptr;
-    if (!dbg) {
-      cudaMalloc(&dbg, sizeof(int) * 4 * 148 * 64);
-      cudaMemset(dbg, 0, sizeof(int) * 4 * 148 * 64);
-      cudaMalloc(&own, sizeof(int) * 2 * (size_t)(1 << 20));
+  const Knobs& kn = knobs();
+  if (kn.hc_debug) {  // per-plan debug buffers sized for this grid and device
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device);
+    const size_t nw = (size_t)4 * sms * 64;
+    if (!P->dDbg) {
+      int rc2;
+      if ((rc2 = dalloc(&P->dDbg, nw))) return rc2;
+      P->allocs.push_back(P->dDbg);
+      if ((rc2 = dalloc(&P->dOwner, 2 * (size_t)J))) return rc2;
+      P->allocs.push_back(P->dOwner);
     }
-    cudaMemsetAsync(dbg, 0, sizeof(int) * 4 * 148 * 64, P->stream);
-    cudaMemsetAsync(own, 0xFF, sizeof(int) * 2 * (size_t)J, P->stream);
-    a.wdbg = dbg;
-    a.owner = own;
+    CK(cudaMemsetAsync(P->dDbg, 0, sizeof(int) * nw, P->stream));
+    CK(cudaMemsetAsync(P->dOwner, 0xFF, sizeof(int) * 2 * (size_t)J, P->stream));
+    a.wdbg = P->dDbg;
+    a.owner = P->dOwner;
   }
   a.ctag = P->dCTag;
   a.chain = P->hc_chain;
-  a.idle_ns = 200;
-  a.prof = std::getenv("EIK_HC_PROFILE") ? 1 : 0;
-  if (const char* c = std::getenv("EIK_HC_IDLE_NS")) a.idle_ns = std::atoi(c);
+  a.prof = kn.hc_profile ? 1 : 0;
+  a.idle_ns = kn.hc_idle_ns;
   a.done_flag = P->dHcMisc;
   a.hsize_pub = P->dHcMisc + 32;
   a.heap_capb_global = P->hc_capb_global;
@@ -399,8 +401,7 @@ retry:  // after a committer heap overflow, with the heap in global memory
   // HCM's first sweep runs mostly unlocked nodes: the branch-free engine wins
   // there, the vote-skip one on the convergence sweeps (measured 1-3 % at
   // every cell size; EIK_HC_SKIP_FROM overrides)
-  a.skip_from = 1;
-  if (const char* c = std::getenv("EIK_HC_SKIP_FROM")) a.skip_from = std::atoi(c);
+  a.skip_from = kn.hc_skip_from;
   CK(cudaMemsetAsync(P->dHcMisc, 0, sizeof(int) * (32 + 32 * 32), P->stream));
   const int hc_ctas = P->cap() > 0 ? std::min(P->hc_max_ctas, P->cap()) : P->hc_max_ctas;
   int grid = 0;
@@ -438,7 +439,7 @@ retry:  // after a committer heap overflow, with the heap in global memory
     return fail(EIK_ERR_CUDA, st[0] == 4 ? "heap-cell committer watchdog fired"
                                          : "heap-cell slot index out of range");
   }
-  if (std::getenv("EIK_HC_PROFILE"))
+  if (kn.hc_profile)
     std::fprintf(stderr,
                  "heapcell committer cycles: pop %llu obtain %llu self %llu commit %llu | self: "
                  "stage %llu sweeps %llu scans %llu | hits %llu (chained %llu) self %llu | "
@@ -447,7 +448,7 @@ retry:  // after a committer heap overflow, with the heap in global memory
                  cnt[8], cnt[9], cnt[10], cnt[11], cnt[12], cnt[13], cnt[14], cnt[6], cnt[15],
                  cnt[5], cnt[38], P->hc_heap_cap, cnt[39], cnt[40], cnt[41], cnt[42], cnt[43],
                  cnt[44], cnt[7], cnt[45]);
-  if (std::getenv("EIK_HC_PROFILE"))
+  if (kn.hc_profile)
     std::fprintf(stderr,
                  "heapcell misses: unchained %llu pending %llu stale %llu wrong-inst %llu "
                  "other-side %llu | last=self %llu prev-pop-adjacent %llu plain-stale-by-1 %llu\n",

@@ -30,6 +30,7 @@
 #include <algorithm>
 
 #include "eik_internal.h"
+#include "eik_plan.h"
 #include "k_common.cuh"
 
 namespace eikb200 {
@@ -110,6 +111,35 @@ __device__ __forceinline__ unsigned chg_mask(const ChgWin& w) {
   return IASC ? d : (__brev(d) >> 24);
 }
 
+// LSM (lsm_solve, classic_solvers.cpp:160-212) processes exactly the nodes
+// that are unlocked when their turn comes; every other node would recompute
+// a candidate >= its value, so LSM's values and sweep count are FSM's (the
+// reference's lsm_solve and fsm_solve return the same field; checked on every
+// golden) and only node_updates differs.  A node is unlocked at its visit in
+// sweep k iff a 4-neighbour lowered its value after the node's visit in sweep
+// k-1 to below the node's value (classic_solvers.cpp:198-204; a neighbour's
+// decreases are monotone, so its current value decides).  "After the visit in
+// sweep k-1" = the neighbours downwind in sweep k-1's direction that changed
+// in sweep k-1 (previous-sweep change bits) or the neighbours upwind in sweep
+// k that changed in sweep k (in-sweep flags).  Sweep 0: a node is unlocked iff
+// it neighbours an exit (classic_solvers.cpp:172-182) or an upwind neighbour
+// changed -- both iff a neighbour is finite when it is visited.
+// lsm_masks: per step t, bit t = the previous sweep changed the node's column
+// neighbour (mc) / row neighbour (mr) on sweep k-1's downwind side.
+template <bool IASC>
+__device__ __forceinline__ void lsm_masks(const ChgWin& w, bool iasc_prev, bool jasc_prev,
+                                          unsigned& mc, unsigned& mr) {
+  const unsigned long long xu = (((unsigned long long)w.u1 << 32) | w.u0) >> w.sh;
+  const unsigned long long xc = (((unsigned long long)w.c1 << 32) | w.c0) >> w.sh;
+  const unsigned long long xd = (((unsigned long long)w.d1 << 32) | w.d0) >> w.sh;
+  // absolute order: bit j = column lo+j; W = xc bit j, E = bit j+2, S/N = rows
+  // r-1 / r+1 at bit j+1
+  const unsigned c = (unsigned)(iasc_prev ? (xc >> 2) : xc) & 0xFFu;
+  const unsigned r = (unsigned)((jasc_prev ? xd : xu) >> 1) & 0xFFu;
+  mc = IASC ? c : (__brev(c) >> 24);
+  mr = IASC ? r : (__brev(r) >> 24);
+}
+
 // One sweep of one warp-strip.  IASC selects the column direction at compile
 // time so every access in the unrolled block is an immediate offset from a
 // per-block pointer; the padded layout (kPad columns of +inf / -1 on both
@@ -128,10 +158,11 @@ __device__ __forceinline__ unsigned chg_mask(const ChgWin& w) {
 // before it, only forwards its old values; any other block computes all 8
 // steps (a per-step vote would sit on the fp64 chain).  While lane 0 waits
 // for mailbox slots (SLOW), the per-step form with its vote is used.
-template <bool IASC>
+template <bool IASC, bool LSM>
 __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t rowp,
                                             const Chan& ch, const unsigned* crd, unsigned* cwr,
-                                            unsigned force, unsigned long long* tr) {
+                                            unsigned force, unsigned long long* tr, int dprev,
+                                            bool jasc, unsigned long long& lcnt) {
   constexpr int S = IASC ? 1 : -1;
   const int64_t m = a.m, cw = a.cw;
   const int64_t P = a.P;
@@ -155,7 +186,12 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
     const int64_t q = (int64_t)b * kU - lane;
     return IASC ? q : m - 1 - q - (kU - 1);
   };
-  unsigned pm = force ? force : chg_mask<IASC>(ld_chgwin(crow, cw, lo_of(0) - 1));
+  const ChgWin w0 = ld_chgwin(crow, cw, lo_of(0) - 1);
+  unsigned pm = force ? force : chg_mask<IASC>(w0);
+  // LSM: previous-sweep direction (dprev < 0: sweep 0 of the solve)
+  const bool iasc_prev = dprev == 0 || dprev == 1, jasc_prev = dprev == 0 || dprev == 3;
+  unsigned lmc = 0, lmr = 0;
+  if (LSM && dprev >= 0) lsm_masks<IASC>(w0, iasc_prev, jasc_prev, lmc, lmr);
   ChgWin wa = ld_chgwin(crow, cw, lo_of(1) - 1);
   ChgWin wb = ld_chgwin(crow, cw, lo_of(2) - 1);
 
@@ -196,6 +232,8 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       nh[t] = halo_lane ? __ldcg(ph + S * (kU + t)) : kInf;
     }
     const unsigned pm_next = force ? force : chg_mask<IASC>(wa);
+    unsigned lmc_next = 0, lmr_next = 0;
+    if (LSM && dprev >= 0) lsm_masks<IASC>(wa, iasc_prev, jasc_prev, lmc_next, lmr_next);
     wa = wb;
     wb = ld_chgwin(crow, cw, lo_of(blk + 3) - 1);
     unsigned um = 0;
@@ -240,6 +278,24 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
           const double c = cc[t];
           const double cand = node_update4(cu[t + 1], res_prev, nv, sv, c);
           upd = (c > 0.0) && (cand < cur);  // exits / padding carry c = -1
+          if (LSM) {
+            // lane t-1's step at this column (its previous step) lowered it
+            const unsigned bal = __ballot_sync(kFull, upd_prev);
+            const bool row_up_upd = lane == 0 ? h_chg : ((bal >> (lane - 1)) & 1u);
+            bool unl;
+            if (dprev < 0) {
+              unl = fmin(fmin(cu[t + 1], res_prev), fmin(nv, sv)) < kInf;
+            } else {
+              // the changed neighbour's current value: the column one is
+              // downwind now iff the column direction did not turn (old value
+              // cu[t+1]) else upwind (new value res_prev); rows alike (nv / sv)
+              const double vpc = (iasc_prev == IASC) ? cu[t + 1] : res_prev;
+              const double vpr = (jasc_prev == jasc) ? nv : sv;
+              unl = (((lmc >> t) & 1u) && vpc < cur) || (((lmr >> t) & 1u) && vpr < cur) ||
+                    (upd_prev && res_prev < cur) || (row_up_upd && sv < cur);
+            }
+            lcnt += (unl && c > 0.0) ? 1ull : 0ull;
+          }
           if (upd) {
             res = cand;
             pu[S * t] = cand;
@@ -322,6 +378,10 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       wcur = wn;
     }
     pm = pm_next;
+    if (LSM) {
+      lmc = lmc_next;
+      lmr = lmr_next;
+    }
     pu += S * kU;
     pc += S * kU;
     ph += S * kU;
@@ -345,6 +405,7 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
   return changed;
 }
 
+template <bool LSM>
 __global__ void __launch_bounds__(32 * kMaxWarpsPerCta)
 fsm_wavefront_kernel(FsmArgs a) {
   const int lane = threadIdx.x & 31;
@@ -441,9 +502,17 @@ fsm_wavefront_kernel(FsmArgs a) {
     const unsigned* crd = a.chg + (int64_t)((k + 1) & 1) * cpar;
     unsigned* cwr = a.chg + (int64_t)(k & 1) * cpar;
     const unsigned force = (k == 0 || a.noskip) ? 0xFFu : 0u;
-    const bool changed = iasc ? sweep_strip<true>(a, lane, rowp, ch, crd, cwr, force, tr)
-                              : sweep_strip<false>(a, lane, rowp, ch, crd, cwr, force, tr);
+    const int dprev = k == 0 ? -1 : ((a.first_sweep + k - 1) & 3);
+    unsigned long long lcnt = 0;
+    const bool changed =
+        iasc ? sweep_strip<true, LSM>(a, lane, rowp, ch, crd, cwr, force, tr, dprev, jasc, lcnt)
+             : sweep_strip<false, LSM>(a, lane, rowp, ch, crd, cwr, force, tr, dprev, jasc, lcnt);
     if (*(volatile int*)a.status == kStatusWatchdog) return;
+    if (LSM) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) lcnt += __shfl_xor_sync(kFull, lcnt, o);
+      if (lane == 0 && lcnt) atomicAdd(&a.lsm_cnt[k], lcnt);
+    }
 
     // sweep complete for this strip: make every lane's writes visible, then
     // publish completion and the change flag (once per sweep).
@@ -532,19 +601,21 @@ static int fsm_wpc(int nstrips) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (const char* e = std::getenv("EIK_FSM_WPC")) return std::max(1, std::min(kMaxWarpsPerCta, std::atoi(e)));
+  if (knobs().fsm_wpc > 0) return std::min(kMaxWarpsPerCta, knobs().fsm_wpc);
   if (nstrips <= kWarpsPerCta * sms) return kWarpsPerCta;
   return std::min(kMaxWarpsPerCta, (nstrips + sms - 1) / sms);
 }
 
-static const void* fsm_kernel_fn() { return (const void*)fsm_wavefront_kernel; }
+static const void* fsm_kernel_fn(bool lsm = false) {
+  return lsm ? (const void*)fsm_wavefront_kernel<true> : (const void*)fsm_wavefront_kernel<false>;
+}
 
-cudaError_t fsm_capacity(int nstrips, int* need, int* ctas) {
+cudaError_t fsm_capacity(int nstrips, int* need, int* ctas, bool lsm) {
   int per_sm = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int wpc = fsm_wpc(nstrips);
-  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fsm_kernel_fn(),
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fsm_kernel_fn(lsm),
                                                                 32 * wpc, 0);
   if (e != cudaSuccess) return e;
   *need = (nstrips + wpc - 1) / wpc;
@@ -560,8 +631,8 @@ cudaError_t launch_fsm(const FsmArgs& args, cudaStream_t s, int* launches, int* 
   void* params[] = {&a};
   // Strips spin on each other's progress, so every CTA must be co-resident:
   // a cooperative launch guarantees it (or fails loudly).
-  cudaError_t e = cudaLaunchCooperativeKernel(fsm_kernel_fn(), dim3(ctas), dim3(32 * wpc), params,
-                                              0, s);
+  cudaError_t e = cudaLaunchCooperativeKernel(fsm_kernel_fn(a.lsm_cnt != nullptr), dim3(ctas),
+                                              dim3(32 * wpc), params, 0, s);
   *launches += 1;
   return e;
 }

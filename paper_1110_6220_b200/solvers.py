@@ -1,7 +1,8 @@
 """Solver entry points mirroring the reference's L2 API.
 
-    fmm_solve(problem)            classic_solvers.hpp:18
+    fmm_solve(problem, opts)      classic_solvers.hpp:18
     fsm_solve(problem)            classic_solvers.hpp:33
+    lsm_solve(problem)            classic_solvers.hpp:38
     hcm_solve(problem, cells)     heap_cell.hpp:36
     fhcm_solve(problem, cells)    heap_cell.hpp:41
     fmsm_solve(problem, cells)    fmsm.hpp:36
@@ -50,6 +51,7 @@ class SolverOutput:
     kernel_launches: int = 0
     spec: tuple = (0, 0, 0)  # heap-cell replay: (hits, waits, self-processed)
     ctas: int = 0            # CTAs of the persistent solve kernel
+    acceptance_order: Optional[np.ndarray] = None  # FMM only, when requested (grid.hpp:148)
 
     def at(self, i: int, j: int) -> float:
         return float(self.values[j * self.m + i])
@@ -122,12 +124,33 @@ def solve(problem: Problem, method: str, cells: Optional[CellDecomposition] = No
     return _pack(res, u, problem.grid)
 
 
-def fmm_solve(problem: Problem) -> SolverOutput:
-    return solve(problem, "fmm")
+@dataclass
+class FmmOptions:
+    """classic_solvers.hpp:10-13."""
+    record_acceptance_order: bool = False
+
+
+def fmm_solve(problem: Problem, opts: Optional[FmmOptions] = None) -> SolverOutput:
+    if opts is None or not opts.record_acceptance_order:
+        return solve(problem, "fmm")
+    plan = Plan(problem, "fmm")
+    try:
+        out = plan.run(np.empty(problem.grid.size(), dtype=np.float64))
+        order = np.empty(problem.grid.size() - len(problem.exit_nodes), dtype=np.int32)
+        N.raise_for(N.lib.eik_plan_acceptance_order(
+            plan._h, order.ctypes.data_as(C.POINTER(C.c_int32)), 0))
+        out.acceptance_order = order
+    finally:
+        plan.close()
+    return out
 
 
 def fsm_solve(problem: Problem) -> SolverOutput:
     return solve(problem, "fsm")
+
+
+def lsm_solve(problem: Problem) -> SolverOutput:
+    return solve(problem, "lsm")
 
 
 def hcm_solve(problem: Problem, cells: CellDecomposition) -> SolverOutput:

@@ -171,6 +171,49 @@ def c34():
         json.dump(out, f, indent=1, sort_keys=True)
 
 
+def extra():
+    """Round-2 fixtures (extra.json):
+    * lsm: the reference's lsm_solve on C1, C2, C3, C4 and config 5's 2049^2
+      member -- sha256 + counters (its field and sweeps are fsm_solve's; only
+      node_updates differs);
+    * fmm_vs_fsm: L-inf between the reference's FMM and FSM fields on C2, C3,
+      C4 -- the GPU FMM row is bitwise the reference FSM (pinned by sha256),
+      so this is exactly its distance to the reference FMM;
+    * c3r: BASELINE config 3's seeded random-block variant (block speeds iid
+      from {0.5, 1, 2}, seed 7), every method and cell size as c34.json."""
+    out = {"lsm": {}, "fmm_vs_fsm": {}}
+    cases = [("c1", configs.config1()), ("c2", configs.config2()), ("c3", configs.config3()),
+             ("c4", configs.config4()), ("c5_2049", configs.config5(2049))]
+    for name, cfg in cases:
+        p = cfg.problem
+        t = time.time()
+        r = O.ref_solve(p, "lsm")
+        out["lsm"][name] = dict(sha256=sha(r.u), ms=r.elapsed_ms, **counters(r))
+        print(name, "lsm", round(time.time() - t, 1), flush=True)
+        if name in ("c2", "c3", "c4"):
+            a = O.ref_solve(p, "fmm")
+            b = O.ref_solve(p, "fsm")
+            out["fmm_vs_fsm"][name] = dict(linf=float(np.max(np.abs(a.u - b.u))),
+                                           fmm_sha256=sha(a.u), fsm_sha256=sha(b.u),
+                                           fmm=counters(a))
+            print(name, "fmm vs fsm", out["fmm_vs_fsm"][name]["linf"], flush=True)
+    p = configs.config3(seed=7).problem
+    c3r = {}
+    for method in ("fsm", "fmm"):
+        r = O.ref_solve(p, method)
+        c3r[method] = dict(sha256=sha(r.u), ms=r.elapsed_ms, **counters(r))
+    for cs in C34_CELLS["c3"]:
+        cx = p.grid.m // cs
+        for method in ("fmsm", "hcm", "fhcm"):
+            r = O.ref_solve(p, method, cx, cx)
+            c3r[f"{method}/{cs}"] = dict(sha256=sha(r.u), cells=cx, ms=r.elapsed_ms,
+                                         **counters(r))
+            print("c3r", method, cs, round(r.elapsed_ms), flush=True)
+    out["c3r"] = c3r
+    with open(os.path.join(HERE, "extra.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
 def metrics():
     """metrics.cpp on the small cases: the reference's refine-4 ground truth
     (metrics.npz, its FMM on the refined grid, subsampled) and its
@@ -222,6 +265,7 @@ if __name__ == "__main__":
     ap.add_argument("--c34", action="store_true")
     ap.add_argument("--c5", action="store_true")
     ap.add_argument("--metrics", action="store_true")
+    ap.add_argument("--extra", action="store_true")
     a = ap.parse_args()
     if not O.have_ref():
         sys.exit("oracle/_ref/libeikref.so missing: run make -C oracle here")
@@ -233,6 +277,9 @@ if __name__ == "__main__":
         sys.exit(0)
     if a.metrics:
         metrics()
+        sys.exit(0)
+    if a.extra:
+        extra()
         sys.exit(0)
     with open(os.path.join(HERE, "kat.json"), "w") as f:
         json.dump(kat(), f, indent=1)

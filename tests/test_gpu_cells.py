@@ -226,6 +226,16 @@ def test_heapcell_engine_variants_bitwise(env, monkeypatch):
     (C2 at 16x16-node cells)."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
+    E.lib.eik_debug_reload_knobs()  # the library reads its knobs once
+    try:
+        _engine_variant_bitwise(env)
+    finally:
+        for k in env:
+            monkeypatch.delenv(k)
+        E.lib.eik_debug_reload_knobs()
+
+
+def _engine_variant_bitwise(env):
     p = configs.config2(257).problem
     cells = E.build_cells(p.grid, 16, 16)
     for method in ("hcm", "fhcm"):
