@@ -39,6 +39,14 @@ sys.path.insert(0, ROOT)
 
 CELL_SIZES = [8, 16, 32, 64]
 METHODS = ["fmm", "fsm", "fmsm", "hcm", "fhcm"]
+METRIC = "converged fine-grid points/s"
+# identical in both arms (the driver compares the arms' config objects)
+CONFIG = {"workload": "c2_sinusoid_2049_method_matrix", "grid": 2049,
+          "speed": "1 + 0.5 sin(20 pi x) sin(20 pi y), centre point source",
+          "methods": METHODS, "cell_sizes": CELL_SIZES,
+          "step": "one solve of each of the 14 method-configs (fmm, fsm, fmsm/hcm/fhcm x 8,16,32,64)",
+          "l2": "inputs larger than L2 (resident plans ~0.2 GB each, K steps); one 256 MB flush "
+                "before the timed region"}
 
 
 def matrix(cfg):
@@ -117,55 +125,97 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", "0")))
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _ref_lib():
+    """The unmodified reference (oracle/_ref/libeikref.so, built from
+    /root/reference by oracle/Makefile) through plain ctypes: the reference
+    arm imports nothing from paper_1110_6220_b200 and maps none of its code."""
+    import ctypes as C
+    path = os.path.join(ROOT, "oracle", "_ref", "libeikref.so")
+    if not os.path.exists(path):
+        return None
+    lib = C.CDLL(path)
+    lib.ref_bench_sinusoid.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_int,
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    lib.ref_bench_sinusoid.restype = C.c_int
+    lib.ref_last_error.restype = C.c_char_p
+    return lib
+
+
+_REF_METHOD = {"fmm": 0, "fsm": 1, "lsm": 2, "hcm": 3, "fhcm": 4, "fmsm": 5}
+
+
 def run_reference(args):
-    """Reference arm: the unmodified reference (oracle/_ref, built from
-    /root/reference) on the host cores, one method-config per thread (the
-    reference's own --jobs model, experiment.cpp:284-310)."""
+    """Reference arm: the unmodified reference on the box's host cores.  Every
+    step is the full 14-solve C2 matrix, built by the reference itself (its
+    SpeedSpec and build_problem, oracle/ref_shim.cpp ref_bench_sinusoid).  All
+    W warm-up steps' solves, then all K timed steps' solves, go through ONE
+    work queue on nproc threads (the reference's --jobs model,
+    experiment.cpp:284-310, with no barrier between steps; longest solves
+    first), so every core stays busy; value = 14 M K / wall time."""
+    import ctypes as C
+    from concurrent.futures import ThreadPoolExecutor
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from concurrent.futures import ThreadPoolExecutor
-
-    from oracle import oracle as O
-    from paper_1110_6220_b200 import configs
-    if not O.have_ref():
+    lib = _ref_lib()
+    if lib is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libeikref.so not built"}))
         return
-    cfg = configs.config2()
-    p = cfg.problem
-    M = p.grid.size()
-    rows = matrix(cfg)
+    m = CONFIG["grid"]
+    M = m * m
+    rows = matrix(None)
     cores = os.cpu_count() or 1
 
     def one(row):
         meth, cs = row
-        cx = p.grid.m // cs if cs else 0
-        return O.ref_solve(p, meth, cx, cx).elapsed_ms
+        ms, sm = C.c_double(), C.c_double()
+        rc = lib.ref_bench_sinusoid(_REF_METHOD[meth], m, 0.5, 20, m // cs if cs else 0,
+                                    C.byref(ms), C.byref(sm))
+        if rc:
+            raise RuntimeError(lib.ref_last_error().decode())
+        return row, ms.value
 
-    times = []
+    def run_all(jobs):
+        with ThreadPoolExecutor(max_workers=cores) as ex:
+            return list(ex.map(one, jobs))
+
+    warm = run_all(rows * max(1, args.warmup))
+    est = {}
+    for row, ms in warm:
+        est.setdefault(row, []).append(ms)
+    order = sorted(rows, key=lambda r: -statistics.mean(est[r]))  # longest first
+    t0 = time.perf_counter()
+    res = run_all([r for r in order for _ in range(args.steps)])
+    wall = time.perf_counter() - t0
     per = {}
-    for step in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        with ThreadPoolExecutor(max_workers=min(cores, len(rows))) as ex:
-            ms = list(ex.map(one, rows))
-        dt = time.perf_counter() - t0
-        if step >= args.warmup:
-            times.append(dt)
-            for r, t in zip(rows, ms):
-                per.setdefault(f"{r[0]}" + (f"/{r[1]}" if r[1] else ""), []).append(t)
-    step_s = statistics.mean(times)
+    for (meth, cs), ms in res:
+        per.setdefault(meth + (f"/{cs}" if cs else ""), []).append(ms)
+    step_s = wall / args.steps
     value = len(rows) * M / step_s
+    core_s = sum(ms for _, ms in res) / 1e3
     out = {
-        "impl": "reference", "metric": "converged fine-grid points/s", "value": value,
-        "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config 2)",
-        "config": {"workload": "c2_sinusoid_2049_method_matrix", "grid": 2049,
-                   "methods": METHODS, "cell_sizes": CELL_SIZES},
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": min(cores, len(rows)),
-                         "kind": "reference",
-                         "sample": f"the full {len(rows)}-solve C2 matrix per step, one solve per "
-                                   f"thread (reference solves are single-threaded)"},
+        "config": CONFIG,
+        "cpu_baseline": {"value": value, "unit": "points/s", "cores": cores, "kind": "reference",
+                         "cpu_model": cpu_model(), "nproc": cores,
+                         "sample": f"{args.steps} steps x {len(rows)} solves of the C2 matrix on "
+                                   f"one {cores}-thread work queue (longest first, no per-step "
+                                   f"barrier); {core_s:.1f} core-s in {wall:.1f} s wall "
+                                   f"({core_s / wall / cores:.0%} of the cores busy)"},
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "per_solve_ms": {k: statistics.mean(v) for k, v in per.items()},
@@ -186,40 +236,83 @@ def fsm_roof(methods, M, hbm, peak_kind):
                     "direction turn) bounds it, not HBM"}
 
 
-def measure_fsm_c5(hbm, peak_kind):
-    """FSM on BASELINE config 5 with the field resident: best of 2 device
-    times, algorithmic bytes 24 B per node per sweep; DRAM
-    traffic per launch from the committed ncu capture of the same solve."""
-    import paper_1110_6220_b200 as E
-    from paper_1110_6220_b200 import configs
-    p5 = configs.config5().problem
-    M5 = p5.grid.m * p5.grid.n
-    plan = E.Plan(p5, "fsm")
-    best = None
-    for _ in range(2):
-        o = plan.run()
-        best = o if best is None or o.device_ms < best.device_ms else best
-    plan.close()
-    del p5
-    traffic = None
+def _ncu_dram(path):
+    """dram__bytes_read.sum + dram__bytes_write.sum from a committed ncu csv."""
+    import csv
     try:
-        import csv
-        with open(os.path.join(ROOT, "profiles", "r01_fsm_c5_v4_metrics.csv")) as f:
+        with open(os.path.join(ROOT, "profiles", path)) as f:
             rows = [r for r in csv.reader(x for x in f if not x.startswith("=="))]
         hdr = rows[0]
         vals = {r[hdr.index("Metric Name")]: float(r[hdr.index("Metric Value")]) for r in rows[1:]}
-        traffic = vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+        return vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
     except (OSError, ValueError, KeyError, IndexError):
-        pass
-    ms = best.device_ms
-    nbytes = 24.0 * M5 * best.sweeps
-    ach = nbytes / (ms / 1e3) / 1e9
-    return {"workload": "c5_sinsum_32769_64_sources_fsm", "points": M5, "device_ms": round(ms, 3),
-            "sweeps": best.sweeps, "points_per_s": M5 / (ms / 1e3),
-            "roofline": {"bound": "hbm", "kernel": "fsm_wavefront", "achieved": round(ach, 2),
-                         "peak": hbm, "unit": "GB/s", "frac": ach / hbm, "traffic": traffic,
-                         "algorithmic_bytes": nbytes, "peak_kind": peak_kind},
-            "ref_cpu_estimate": "~1-1.3 h on one core (SURVEY 8(d)); not run"}
+        return None
+
+
+# Per-config lines (BASELINE configs 3, 4, 5): each solve alone on the GPU,
+# best of 2 device times, inputs resident; FMSM's host Part I is included in
+# its time.  The reference's counters and its solve time (one core of the
+# machine that generated the goldens) are listed beside ours.
+CONFIG_ROWS = {
+    "c3": [("fsm", 0), ("fmm", 0), ("lsm", 0), ("fmsm", 16), ("hcm", 16), ("fhcm", 16),
+           ("fmsm", 48), ("hcm", 48), ("fhcm", 48)],
+    "c4": [("fsm", 0), ("fmm", 0), ("lsm", 0), ("fmsm", 16), ("hcm", 16), ("fhcm", 16),
+           ("fmsm", 32), ("hcm", 32), ("fhcm", 32)],
+    "c5": [("fsm", 0), ("fmsm", 32), ("fhcm", 32), ("hcm", 32)],
+}
+
+
+def measure_configs(hbm, peak_kind):
+    import paper_1110_6220_b200 as E
+    from paper_1110_6220_b200 import configs
+    gold = {}
+    for fn, pre in (("c34.json", ""), ("extra.json", None), ("c5_full.json", "")):
+        try:
+            with open(os.path.join(ROOT, "tests", "golden", fn)) as f:
+                d = json.load(f)
+        except OSError:
+            continue
+        if pre is None:
+            for name, v in d.get("lsm", {}).items():
+                gold[f"{name}/lsm"] = v
+        else:
+            for k, v in d.items():
+                gold[k.replace("c5_full/", "c5/")] = v
+    out = {}
+    for name, rows in CONFIG_ROWS.items():
+        cfg = {"c3": configs.config3, "c4": configs.config4, "c5": configs.config5}[name]()
+        p = cfg.problem
+        M = p.grid.size()
+        for meth, cs in rows:
+            key = f"{name}/{meth}" + (f"/{cs}" if cs else "")
+            cells = E.build_cells(p.grid, p.grid.m // cs, p.grid.m // cs) if cs else None
+            plan = E.Plan(p, meth, cells)
+            best = None
+            for _ in range(2):
+                o = plan.run()
+                if best is None or o.device_ms + o.host_ms < best.device_ms + best.host_ms:
+                    best = o
+            plan.close()
+            t = best.device_ms + best.host_ms
+            ref = gold.get(key, {})
+            row = {"ms": round(t, 3), "device_ms": round(best.device_ms, 3),
+                   "host_ms": round(best.host_ms, 3), "points_per_s": M / (t / 1e3),
+                   "sweeps": best.sweeps, "node_updates": best.node_updates,
+                   "heap_removals": best.heap_removals, "ref_sweeps": ref.get("sweeps"),
+                   "ref_node_updates": ref.get("node_updates"),
+                   "ref_heap_removals": ref.get("heap_removals"),
+                   "ref_cpu_ms_golden_host": ref.get("ms")}
+            if meth in ("fsm", "lsm"):
+                nbytes = 24.0 * M * best.sweeps
+                ach = nbytes / (best.device_ms / 1e3) / 1e9
+                row["roofline"] = {"bound": "hbm", "achieved": round(ach, 2), "peak": hbm,
+                                   "unit": "GB/s", "frac": ach / hbm, "algorithmic_bytes": nbytes,
+                                   "peak_kind": peak_kind}
+                if key == "c5/fsm":
+                    row["roofline"]["traffic"] = _ncu_dram("r02_fsm_c5_metrics.csv")
+            out[key] = row
+        del p, cfg
+    return out
 
 
 def cpu_baseline_single_core():
@@ -248,8 +341,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-c5", action="store_true",
-                    help="skip the config-5 FSM measurement (HBM-scale global sweep)")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config lines (configs 3, 4, 5 at full size)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
@@ -395,35 +488,34 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e_s = float(t.item())
 
-    # the global sweep at BASELINE config 5 (32769^2, 1.07e9 points, u + F ~17 GB):
-    # the one configuration of the path where HBM, not the dependency chain
-    # alone, is in reach; measured after the timed region, rank 0 at N = 1
-    fsm_c5 = None
-    if not args.no_c5 and rank == 0 and world == 1:
-        fsm_c5 = measure_fsm_c5(hbm, peak_kind)
+    # per-config lines (configs 3, 4 and 5 at full size), after the timed
+    # region, rank 0 at N = 1
+    per_config = None
+    if not args.no_configs and rank == 0 and world == 1:
+        for plan in all_plans:
+            plan.close()
+        all_plans = []
+        per_config = measure_configs(hbm, peak_kind)
 
     cpu = None if args.no_cpu_baseline or rank != 0 else cpu_baseline_single_core()
     if rank == 0:
         out = {
-            "metric": "converged fine-grid points/s", "value": value, "unit": "points/s",
+            "metric": METRIC, "value": value, "unit": "points/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, BASELINE config 2)",
-            "config": {"workload": "c2_sinusoid_2049_method_matrix", "grid": 2049,
-                       "methods": METHODS, "cell_sizes": CELL_SIZES,
-                       "parallelism": f"replicas x{world}",
-                       "concurrency": f"{len(rows)} solves per step, each on its own SMs "
-                                      "(eik_plan_run_batch list schedule)",
-                       "steps_overlap": f"the {K} timed steps run as one list schedule "
-                                        "(a step's long replays overlap the next step's "
-                                        "solves); single_step_ms is one step alone",
-                       "l2": f"inputs larger than L2 ({K * len(rows)} resident plans, "
-                             "~0.2 GB each); one 256 MB flush before the timed region"},
+            "config": CONFIG,
+            "schedule": {"parallelism": f"replicas x{world}",
+                         "concurrency": f"{len(rows)} solves per step, each on its own SMs "
+                                        "(eik_plan_run_batch list schedule)",
+                         "steps_overlap": f"the {K} timed steps run as one list schedule "
+                                          "(a step's long replays overlap the next step's "
+                                          "solves); single_step_ms is one step alone"},
             "e2e": {"value": world * len(rows) * M / e2e_s, "unit": "points/s",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "single_step_ms": single_step_ms,
             "roofline": roofline, "roofline_fsm_c2": fsm_roof(methods, M, hbm, peak_kind),
-            "fsm_c5": fsm_c5, "cpu_baseline": cpu, "gpu_launches": launches,
+            "configs": per_config, "cpu_baseline": cpu, "gpu_launches": launches,
             "clocks": clk.summary(), "methods": methods,
         }
         print(json.dumps(out))

@@ -4,10 +4,9 @@ sources.
 * At 2049^2, where the unmodified reference runs in this container, FSM and
   HCM/FHCM/FMSM at 16/32-node cells reproduce its field bit for bit with
   identical counters (tests/golden/c5.json, make_golden.py --c5).
-* At the full 32769^2 (1.07e9 points), where the reference would take about an
-  hour per FSM solve: FSM's result is a fixed point (one further sweep changes
-  nothing), sources are 0, and FHCM -- monotone upwind updates from +inf --
-  stays above it up to rounding.
+* At the full 32769^2 (1.07e9 points) against the reference's own run of the
+  same problem (tests/golden/c5_full.json, make_c5_full.py): FSM, HCM, FHCM
+  and FMSM at 16/32-node cells bit for bit with identical counters.
 """
 import hashlib
 import json
@@ -53,27 +52,53 @@ def test_c5_family_bitwise_2049(method, cs):
                                        want["mon_single"])
 
 
+FULL = os.path.join(os.path.dirname(__file__), "golden", "c5_full.json")
+
+
+def _full_keys():
+    if not os.path.exists(FULL):
+        return []
+    with open(FULL) as f:
+        return sorted(json.load(f))
+
+
+_FULL = {}
+
+
+def _c5_full():
+    if "cfg" not in _FULL:
+        _FULL["cfg"] = configs.config5()
+        _FULL["u"] = np.empty(_FULL["cfg"].problem.grid.size())
+    return _FULL["cfg"], _FULL["u"]
+
+
 @pytest.mark.slow
-def test_c5_full_size_fsm_fixed_point_and_fhcm_above_it():
-    cfg = configs.config5()
+@pytest.mark.parametrize("key", _full_keys())
+def test_c5_full_size_bitwise_against_reference(key):
+    """Config 5 at its full 32769^2 (1.07e9 nodes): the unmodified reference
+    solved it on the CPU (array-backed SpeedFn, tests/golden/make_c5_full.py;
+    FSM ~1-2 h, the cell methods minutes) and its field hash, per-1024-row
+    block hashes and counters are in c5_full.json.  The device must reproduce
+    them bit for bit."""
+    with open(FULL) as f:
+        want = json.load(f)[key]
+    cfg, u = _c5_full()
     p = cfg.problem
-    M = p.grid.size()
-    u = np.empty(M)
-    plan = E.Plan(p, "fsm")
-    out = plan.run(u)
-    assert out.sweeps >= 2 and out.node_updates == out.sweeps * (M - len(p.exit_nodes))
-    assert plan.sweep(out.sweeps, 1) == [False]  # a fixed point of the update
-    plan.close()
-    assert np.all(u[p.exit_nodes] == 0.0)
-    assert np.isfinite(u).all() and float(u.min()) == 0.0
-    cells = E.build_cells(p.grid, cfg.cells_for(32), cfg.cells_for(32))
-    v = np.empty(M)
-    fh = E.Plan(p, "fhcm", cells)
-    o2 = fh.run(v)
-    fh.close()
-    assert o2.heap_removals >= cells.cell_count()
-    assert np.isfinite(v).all()
-    # FHCM approaches the fixed point from above (monotone updates from +inf);
-    # different update orders can end on fixed points that differ by rounding
-    d = float(np.min(v - u))
-    assert d >= -1e-12 * float(u.max()), d
+    method = want["method"]
+    cells = E.build_cells(p.grid, want["cells"], want["cells"]) if want["cells"] else None
+    plan = E.Plan(p, method, cells)
+    try:
+        out = plan.run(u)
+    finally:
+        plan.close()
+    got = (out.sweeps, out.node_updates, out.heap_removals, out.hybrid.mon_checks,
+           out.hybrid.mon_single)
+    ref = (want["sweeps"], want["node_updates"], want["heap_removals"], want["mon_checks"],
+           want["mon_single"])
+    m, br = p.grid.m, want["block_rows"]
+    if sha(u) != want["sha256"]:
+        bad = [b for b, h in enumerate(want["block_sha256"])
+               if hashlib.sha256(memoryview(u[b * br * m:min(m, (b + 1) * br) * m])).hexdigest() != h]
+        raise AssertionError(f"{key}: field differs in row blocks {bad[:20]} ({len(bad)} of "
+                             f"{len(want['block_sha256'])}); counters {got} vs {ref}")
+    assert got == ref, key
