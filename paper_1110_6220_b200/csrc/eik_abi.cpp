@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -82,6 +83,12 @@ void reload_knobs() {
   g_knobs = read_knobs();
 }
 
+thread_local SlowCall t_slow;
+double now_ms_host() {
+  return std::chrono::duration<double, std::milli>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 thread_local std::string g_last_error;
 thread_local int g_last_code = EIK_OK;
 
@@ -149,6 +156,7 @@ int check_cells(const eik_problem* p, const eik_cells* c, int method) {
 // ---- device buffer cache ------------------------------------------------
 namespace {
 std::mutex g_pool_mu;
+std::atomic<long long> g_malloc_calls{0}, g_malloc_us{0}, g_free_calls{0};
 std::map<std::pair<int, size_t>, std::vector<void*>> g_pool_free;  // (device, bytes)
 std::map<void*, std::pair<int, size_t>> g_pool_live;
 size_t g_pool_cached = 0;
@@ -166,7 +174,38 @@ size_t pool_cap() {
   }();
   return cap;
 }
+// Cache misses allocate from a per-device stream-ordered memory pool
+// (cudaMallocFromPoolAsync on the allocating plan's stream, release threshold
+// unlimited): cudaMalloc can block until kernels running on OTHER streams end,
+// which stalled eik_solve_batch's plan creation behind the persistent solves
+// of earlier jobs (measured: 438 cudaMalloc calls, 22 s blocked, over a
+// 20-step batch).
+cudaMemPool_t device_pool(int dev) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t> pools;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+    cudaGetLastError();
+    pool = nullptr;
+  } else {
+    unsigned long long thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  pools[dev] = pool;
+  return pool;
+}
+thread_local cudaStream_t t_alloc_stream = nullptr;
 }  // namespace
+
+AllocStream::AllocStream(cudaStream_t s) : prev_(t_alloc_stream) { t_alloc_stream = s; }
+AllocStream::~AllocStream() { t_alloc_stream = prev_; }
 
 cudaError_t pool_alloc(void** p, size_t bytes) {
   int dev = 0;
@@ -183,11 +222,16 @@ cudaError_t pool_alloc(void** p, size_t bytes) {
       return cudaSuccess;
     }
   }
-  e = cudaMalloc(p, bytes);
+  const auto tm0 = std::chrono::steady_clock::now();
+  cudaMemPool_t pool = t_alloc_stream ? device_pool(dev) : nullptr;
+  e = pool ? cudaMallocFromPoolAsync(p, bytes, pool, t_alloc_stream) : cudaMalloc(p, bytes);
+  g_malloc_calls.fetch_add(1);
+  g_malloc_us.fetch_add((long long)std::chrono::duration<double, std::micro>(
+                            std::chrono::steady_clock::now() - tm0).count());
   if (e == cudaErrorMemoryAllocation) {  // give the cache back and retry once
     eik_release_cached();
     cudaGetLastError();
-    e = cudaMalloc(p, bytes);
+    e = pool ? cudaMallocFromPoolAsync(p, bytes, pool, t_alloc_stream) : cudaMalloc(p, bytes);
   }
   if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> lk(g_pool_mu);
@@ -207,6 +251,7 @@ void pool_release(void* p) {
     cudaGetDevice(&cur);
     cudaSetDevice(key.first);
     cudaFree(p);
+    g_free_calls.fetch_add(1);
     cudaSetDevice(cur);
     return;
   }
@@ -251,14 +296,17 @@ void plan_free(eik_plan* P) {
   if (!P) return;
   if (P->stream) cudaStreamSynchronize(P->stream);  // nothing in flight on reused blocks
   for (void* ptr : P->allocs) pool_release(ptr);
-  if (P->ev0) cudaEventDestroy(P->ev0);
-  if (P->ev1) cudaEventDestroy(P->ev1);
+  if (P->own_events) {
+    if (P->ev0) cudaEventDestroy(P->ev0);
+    if (P->ev1) cudaEventDestroy(P->ev1);
+  }
   if (P->stream && P->own_stream) cudaStreamDestroy(P->stream);
   delete P;
 }
 
 int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
-              bool defer_upload = false, cudaStream_t ext_stream = nullptr) {
+              bool defer_upload = false, cudaStream_t ext_stream = nullptr,
+              const cudaEvent_t* ext_events = nullptr) {
   P->method = method;
   P->g = p->grid;
   P->M = p->grid.m * p->grid.n;
@@ -270,8 +318,15 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
   } else {
     CK(cudaStreamCreateWithFlags(&P->stream, cudaStreamNonBlocking));
   }
-  CK(cudaEventCreate(&P->ev0));
-  CK(cudaEventCreate(&P->ev1));
+  AllocStream alloc_on(P->stream);  // cache misses: stream-ordered pool
+  if (ext_events) {  // borrowed: event create/destroy can block behind running kernels
+    P->ev0 = ext_events[0];
+    P->ev1 = ext_events[1];
+    P->own_events = false;
+  } else {
+    CK(cudaEventCreate(&P->ev0));
+    CK(cudaEventCreate(&P->ev1));
+  }
   auto track = [&](void* q) { P->allocs.push_back(q); };
   int rc;
   if ((rc = dalloc(&P->dF, P->M))) return rc;
@@ -365,7 +420,9 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
   } else {
     if ((rc = plan_init_cells(P, p, c))) return rc;
   }
+  const auto ts0 = std::chrono::steady_clock::now();
   CK(cudaStreamSynchronize(P->stream));
+  P->init_sync_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts0).count();
   return EIK_OK;
 }
 
@@ -463,8 +520,9 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
     // lsm_solve's node_updates: nodes processed unlocked, summed over the
     // reference's sweeps (the pipelined wavefront may run a few more)
     std::vector<unsigned long long> cnt((size_t)st[1]);
-    CK(cudaMemcpy(cnt.data(), P->dLsmCnt, sizeof(unsigned long long) * cnt.size(),
-                  cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(cnt.data(), P->dLsmCnt, sizeof(unsigned long long) * cnt.size(),
+                       cudaMemcpyDeviceToHost, P->stream));
+    CK(cudaStreamSynchronize(P->stream));
     int64_t tot = 0;
     for (unsigned long long c : cnt) tot += (int64_t)c;
     out->node_updates = tot;
@@ -801,7 +859,7 @@ int plan_run_batch(eik_plan* const* plans, int n, eik_output* outs, double* batc
 }
 
 eik_plan* plan_create(const eik_problem* p, const eik_cells* c, int32_t method, bool defer_upload,
-                      cudaStream_t stream = nullptr) {
+                      cudaStream_t stream = nullptr, const cudaEvent_t* events = nullptr) {
   g_last_code = EIK_OK;
   g_last_error.clear();
   if (check_problem(p) || check_cells(p, c, method)) return nullptr;
@@ -814,7 +872,7 @@ eik_plan* plan_create(const eik_problem* p, const eik_cells* c, int32_t method, 
     return nullptr;
   }
   eik_plan* P = new eik_plan();
-  if (plan_init(P, p, c, method, defer_upload, stream)) {
+  if (plan_init(P, p, c, method, defer_upload, stream, events)) {
     std::string keep = g_last_error;
     int keep_code = g_last_code;
     plan_free(P);
@@ -835,6 +893,41 @@ eik_plan* plan_create(const eik_problem* p, const eik_cells* c, int32_t method, 
 // bounded by the pool size, not by the number of solves, and no buffer is
 // allocated from the driver in steady state (the exact-size cache serves
 // every plan after the first of its shape).
+// Worker streams and events for eik_solve_batch, created once per process and
+// reused by every call: creating or destroying an event while other kernels
+// run blocks the calling thread until they end (measured: 0.1-1.6 s per
+// cudaEventCreate inside a 20-step batch), so none is created on that path.
+struct WorkerRes {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+};
+std::mutex g_wres_mu;
+std::map<int, std::vector<WorkerRes>> g_wres_free;  // device -> idle resources
+
+int take_worker_res(int device, int count, std::vector<WorkerRes>& out) {
+  std::lock_guard<std::mutex> lk(g_wres_mu);
+  auto& fl = g_wres_free[device];
+  while ((int)out.size() < count) {
+    if (!fl.empty()) {
+      out.push_back(fl.back());
+      fl.pop_back();
+      continue;
+    }
+    WorkerRes r;
+    CK(cudaStreamCreateWithFlags(&r.stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&r.ev[0]));
+    CK(cudaEventCreate(&r.ev[1]));
+    out.push_back(r);
+  }
+  return EIK_OK;
+}
+
+void give_worker_res(int device, std::vector<WorkerRes>& res) {
+  std::lock_guard<std::mutex> lk(g_wres_mu);
+  for (auto& r : res) g_wres_free[device].push_back(r);
+  res.clear();
+}
+
 int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* const* cells,
                           const int32_t* methods, int n, eik_output* outs, double* batch_ms) {
   int device = 0, sms = 0;
@@ -842,7 +935,7 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   const int budget = std::max(1, (int)std::floor(0.98 * sms));
   const Knobs& kn = knobs();
-  const int workers = std::max(1, std::min(n, kn.batch_workers > 0 ? kn.batch_workers : 24));
+  const int workers = std::max(1, std::min(n, kn.batch_workers > 0 ? kn.batch_workers : 32));
   struct Waiting {
     int k;
     BatchSlot b;
@@ -871,19 +964,26 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
     }
     cv.notify_all();
   };
-  CK(cudaDeviceSynchronize());
-  cudaEvent_t ref;
-  CK(cudaEventCreate(&ref));
-  CK(cudaEventRecord(ref, 0));
+  std::vector<WorkerRes> wres;
+  {
+    const int rc = take_worker_res(device, workers + 1, wres);  // +1: the reference event
+    if (rc) {
+      give_worker_res(device, wres);
+      return rc;
+    }
+  }
+  cudaEvent_t ref = wres[workers].ev[0];
+  CK(cudaEventRecord(ref, wres[workers].stream));
   CK(cudaEventSynchronize(ref));
+  std::atomic<int> next_worker{0};
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  auto now_ms = [&]() { return std::chrono::duration<double, std::milli>(clk::now() - t0).count(); };
   auto worker = [&]() {
     cudaSetDevice(device);
-    cudaStream_t st = nullptr;
-    if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
-      std::lock_guard<std::mutex> lk(mu);
-      abort = true;
-      return;
-    }
+    const WorkerRes& wr = wres[next_worker.fetch_add(1)];
+    cudaStream_t st = wr.stream;
+    const cudaEvent_t* evs = wr.ev;
     for (;;) {
       int k;
       {
@@ -891,7 +991,12 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
         if (abort || next_job >= n) break;
         k = next_job++;
       }
-      eik_plan* P = plan_create(problems[k], cells ? cells[k] : nullptr, methods[k], false, st);
+      const double tc0 = now_ms();
+      t_slow = SlowCall{};
+      eik_plan* P = plan_create(problems[k], cells ? cells[k] : nullptr, methods[k], false, st, evs);
+      const double tc1 = now_ms();
+      const SlowCall slow_create = t_slow;
+      t_slow = SlowCall{};
       BatchSlot b;
       int rc = P ? batch_slot(P, sms, budget, b) : (g_last_code != EIK_OK ? g_last_code : EIK_ERR_CUDA);
       if (rc) {
@@ -916,6 +1021,7 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
           break;
         }
       }
+      const double ta = now_ms();
       bool signalled = !b.hc;
       auto launched = [&]() {
         std::lock_guard<std::mutex> lk(mu);
@@ -926,12 +1032,37 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
         launched();
       };
       codes[k] = plan_run(P, &outs[k]);
+      const double tr = now_ms();
+      const double init_sync = P->init_sync_ms;
       P->on_launched = nullptr;
       if (!signalled) launched();
       if (codes[k]) msgs[k] = g_last_error;
       float ms = 0.f;
       const bool timed = codes[k] == EIK_OK && cudaEventElapsedTime(&ms, ref, P->ev1) == cudaSuccess;
-      plan_free(P);
+      const SlowCall slow_run = t_slow;
+      const double tf0 = now_ms();
+      double tsync = 0, tpool = 0, tev = 0, x;
+      {  // plan_free, timed piecewise
+        x = now_ms();
+        cudaStreamSynchronize(P->stream);
+        tsync = now_ms() - x;
+        x = now_ms();
+        for (void* ptr : P->allocs) pool_release(ptr);
+        P->allocs.clear();
+        tpool = now_ms() - x;
+        x = now_ms();
+        plan_free(P);
+        tev = now_ms() - x;
+      }
+      if (kn.batch_trace)
+        std::fprintf(stderr, "solve_batch job %d method %d sms %d: create %.1f-%.1f (sync %.1f; "
+                     "slowest %s %.1f) admit %.1f run+download -%.1f (slowest %s %.1f) free %.1f "
+                     "(sync %.1f pool %.1f rest %.1f) (device end %.1f) mallocs %lld\n", k,
+                     methods[k], b.sms, tc0, tc1, init_sync, slow_create.what ? slow_create.what : "-",
+                     slow_create.ms, ta, tr, slow_run.what ? slow_run.what : "-", slow_run.ms,
+                     now_ms() - tf0, tsync, tpool, tev, ms, g_malloc_calls.load());
+      else
+        (void)tf0;
       std::lock_guard<std::mutex> lk(mu);
       if (timed) t_end = std::max(t_end, (double)ms);
       if (codes[k]) abort = true;
@@ -939,13 +1070,12 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
       admit();
     }
     cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
   };
   std::vector<std::thread> th;
   th.reserve(workers);
   for (int w = 0; w < workers; ++w) th.emplace_back(worker);
   for (auto& t : th) t.join();
-  cudaEventDestroy(ref);
+  give_worker_res(device, wres);
   for (int k = 0; k < n; ++k)
     if (codes[k]) return fail(codes[k], "batch problem " + std::to_string(k) + ": " + msgs[k]);
   if (abort) return fail(EIK_ERR_CUDA, "batch: a worker could not start");
@@ -990,6 +1120,7 @@ int eik_metrics(const double* u_method, const double* u_exact, const double* u_t
   cudaStream_t s;
   CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   std::vector<void*> tmp;
+  AllocStream alloc_on(s);
   auto cleanup = [&]() {
     cudaStreamSynchronize(s);
     for (void* q : tmp) pool_release(q);
@@ -1041,6 +1172,10 @@ void eik_release_cached(void) {
   for (auto& kv : g_pool_free) {
     cudaSetDevice(kv.first.first);
     for (void* q : kv.second) cudaFree(q);
+  }
+  for (auto& kv : g_pool_free) {
+    cudaMemPool_t pool = device_pool(kv.first.first);
+    if (pool) cudaMemPoolTrimTo(pool, 0);
   }
   cudaSetDevice(cur);
   g_pool_free.clear();

@@ -20,6 +20,7 @@ struct eik_plan {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = true;   // false: borrowed from eik_solve_batch's worker
+  bool own_events = true;   // ev0/ev1 likewise
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<void*> allocs;
   double* dF = nullptr;   // speed (resident input)
@@ -100,7 +101,8 @@ struct eik_plan {
 
   int cap() const { return run_cap > 0 ? run_cap : ctas_cap; }
   double last_ms = 0.0;
-  bool ran = false;      // a run completed (the resident field is a solution)  // device + host ms of the last run (batch admission order)
+  bool ran = false;
+  double init_sync_ms = 0.0;  // creation: wait for the uploads (diagnostics)      // a run completed (the resident field is a solution)  // device + host ms of the last run (batch admission order)
   // batch runs: called (then cleared) once the heap-cell grid is submitted
   std::function<void()> on_launched;
 };
@@ -145,10 +147,22 @@ void reload_knobs();
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);
 
-#define CK(expr)                                          \
-  do {                                                    \
-    cudaError_t e_ = (expr);                              \
-    if (e_ != cudaSuccess) return cuda_fail(e_, #expr);   \
+// slowest CUDA call of this thread since the last reset (diagnostics for
+// EIK_BATCH_TRACE): which API call blocks a batch worker
+struct SlowCall {
+  const char* what = nullptr;
+  double ms = 0.0;
+};
+extern thread_local SlowCall t_slow;
+double now_ms_host();
+
+#define CK(expr)                                                  \
+  do {                                                            \
+    const double t0_ = now_ms_host();                             \
+    cudaError_t e_ = (expr);                                      \
+    const double dt_ = now_ms_host() - t0_;                       \
+    if (dt_ > t_slow.ms) t_slow = SlowCall{#expr, dt_};           \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr);           \
   } while (0)
 
 // Device buffers come from a per-device cache of released blocks (exact-size
@@ -158,6 +172,17 @@ int cuda_fail(cudaError_t e, const char* where);
 // (eik_release_cached frees them).
 cudaError_t pool_alloc(void** p, size_t bytes);
 void pool_release(void* p);
+// While alive, cache misses of this thread's pool_alloc are served
+// stream-ordered on `s` (the plan's stream) instead of by cudaMalloc.
+struct AllocStream {
+  explicit AllocStream(cudaStream_t s);
+  ~AllocStream();
+  AllocStream(const AllocStream&) = delete;
+  AllocStream& operator=(const AllocStream&) = delete;
+
+ private:
+  cudaStream_t prev_;
+};
 
 template <class T>
 int dalloc(T** p, size_t count) {
