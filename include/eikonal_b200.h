@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define EIK_ABI_VERSION 2
+#define EIK_ABI_VERSION 3
 
 /* Solver selection; numbering mirrors eikonal::Method (experiment.hpp:11). */
 enum eik_method {
@@ -34,7 +34,10 @@ enum eik_method {
   EIK_LSM = 2,  /* lsm_solve   classic_solvers.hpp:38 */
   EIK_HCM = 3,  /* hcm_solve   heap_cell.hpp:36 */
   EIK_FHCM = 4, /* fhcm_solve  heap_cell.hpp:41 */
-  EIK_FMSM = 5  /* fmsm_solve  fmsm.hpp:36 */
+  EIK_FMSM = 5, /* fmsm_solve  fmsm.hpp:36 */
+  /* hcm_solve by the exact replay of its heap order: bit-identical field and
+   * counters (EIK_HCM's default is the band scheduler, eik_set_hcm_mode) */
+  EIK_HCM_EXACT = 6
 };
 
 enum eik_status {
@@ -104,6 +107,7 @@ typedef struct eik_output {
    * commit, pops that waited on a worker, pops processed by the committer */
   int64_t spec_hits, spec_waits, spec_self;
   int64_t grid_ctas;    /* CTAs of the persistent solve kernel this run launched */
+  int64_t rounds;       /* HCM band scheduler: rounds (heap_removals = its pops) */
 } eik_output;
 
 /* One solve.  `cells` may be NULL for FMM/FSM.  Thread-safe: each call owns
@@ -152,6 +156,18 @@ void eik_plan_destroy(eik_plan* plan);
  *                     and downloads overlap); cells[k] may be NULL for
  *                     FMM/FSM and `cells` itself NULL when no solve needs one. */
 int eik_plan_set_ctas(eik_plan* plan, int32_t max_ctas);
+/* HCM ordering (north_star item 3).  mode 0 (default): the band scheduler --
+ * every round processes all queued cells within the acceptance band
+ * [kmin, kmin + (h+h_c)/(2 F_max)] that are local minima among their in-band
+ * queued neighbours (never two adjacent cells), in one persistent launch;
+ * the field is hcm_solve's fixed point within rounding (<= 1e-10, measured
+ * ~1e-15), pops / sweeps / node updates are this order's.  mode 1: the exact
+ * replay of hcm_solve's heap order -- bit-identical field and counters.
+ * eik_set_hcm_mode sets the default for plans created afterwards
+ * (EIK_HCM_EXACT=1 in the environment sets it to 1); eik_plan_set_hcm_mode
+ * one plan's. */
+int eik_set_hcm_mode(int32_t mode);
+int eik_plan_set_hcm_mode(eik_plan* plan, int32_t mode);
 /* eik_plan_set_partitions  strip-Jacobi on one device for an EIK_FSM/EIK_FMM
  *                     plan: parts of part_rows rows (a multiple of 32; 0 =
  *                     one exact Gauss-Seidel wavefront, the default) sweep

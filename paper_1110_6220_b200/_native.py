@@ -12,9 +12,11 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libeikonal_b200.so")
 
-EIK_FMM, EIK_FSM, EIK_LSM, EIK_HCM, EIK_FHCM, EIK_FMSM = range(6)
+EIK_FMM, EIK_FSM, EIK_LSM, EIK_HCM, EIK_FHCM, EIK_FMSM, EIK_HCM_EXACT = range(7)
+# "hcm" runs the band scheduler (default, eik_set_hcm_mode); "hcm_exact" the
+# exact replay of hcm_solve's heap order (bit-identical field and counters)
 METHOD_NAMES = {"fmm": EIK_FMM, "fsm": EIK_FSM, "lsm": EIK_LSM, "hcm": EIK_HCM,
-                "fhcm": EIK_FHCM, "fmsm": EIK_FMSM}
+                "fhcm": EIK_FHCM, "fmsm": EIK_FMSM, "hcm_exact": EIK_HCM_EXACT}
 
 EIK_OK, EIK_ERR_CONFIG, EIK_ERR_CUDA, EIK_ERR_BUDGET, EIK_ERR_NOT_IMPL, EIK_ERR_DOMAIN = range(6)
 
@@ -52,7 +54,8 @@ class eik_output(C.Structure):
                 ("mon_single", C.c_int64), ("avhr", C.c_double), ("avs", C.c_double),
                 ("mon_pct", C.c_double), ("device_ms", C.c_double), ("host_ms", C.c_double),
                 ("kernel_launches", C.c_int64), ("spec_hits", C.c_int64),
-                ("spec_waits", C.c_int64), ("spec_self", C.c_int64), ("grid_ctas", C.c_int64)]
+                ("spec_waits", C.c_int64), ("spec_self", C.c_int64), ("grid_ctas", C.c_int64),
+                ("rounds", C.c_int64)]
 
 
 class eik_field(C.Structure):
@@ -88,6 +91,8 @@ EXPORTS = {
     "eik_plan_get_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]),
     "eik_plan_set_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]),
     "eik_plan_set_ctas": (C.c_int, [C.c_void_p, C.c_int32]),
+    "eik_set_hcm_mode": (C.c_int, [C.c_int32]),
+    "eik_plan_set_hcm_mode": (C.c_int, [C.c_void_p, C.c_int32]),
     "eik_plan_set_partitions": (C.c_int, [C.c_void_p, C.c_int32]),
     "eik_plan_capacity": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "eik_plan_run_batch": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(eik_output),

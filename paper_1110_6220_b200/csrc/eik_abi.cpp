@@ -78,6 +78,14 @@ Knobs g_knobs = read_knobs();
 }  // namespace
 
 const Knobs& knobs() { return g_knobs; }
+
+namespace {
+std::atomic<int> g_hcm_mode{-1};  // -1: not set by eik_set_hcm_mode, use the knob
+}  // namespace
+int hcm_default_mode() {
+  const int m = g_hcm_mode.load();
+  return m >= 0 ? m : (knobs().hcm_exact ? 1 : 0);
+}
 void reload_knobs() {
   std::lock_guard<std::mutex> lk(g_knobs_mu);
   g_knobs = read_knobs();
@@ -134,7 +142,8 @@ int check_problem(const eik_problem* p) {
 }
 
 int check_cells(const eik_problem* p, const eik_cells* c, int method) {
-  const bool hybrid = method == EIK_HCM || method == EIK_FHCM || method == EIK_FMSM;
+  const bool hybrid = method == EIK_HCM || method == EIK_FHCM || method == EIK_FMSM ||
+                      method == EIK_HCM_EXACT;
   if (!hybrid) return EIK_OK;
   if (!c) return fail(EIK_ERR_CONFIG, "two-scale methods need a cell decomposition");
   // build_cells (cells.cpp:33-36)
@@ -285,6 +294,13 @@ int plan_capacity(eik_plan* P, int* device, int* fixed) {
     case EIK_FMSM:
       CK(fmsm_capacity(P->cg.tile_doubles, P->warps_per_cta, device));
       break;
+    case EIK_HCM:
+      if (P->hcm_band) {
+        CK(hcm_band_capacity(P->cg.tile_doubles, P->hc_warps_per_cta, (size_t)P->hc_min_smem,
+                             device));
+        break;
+      }
+      [[fallthrough]];
     default:
       CK(heapcell_capacity(P->cg.tile_doubles, P->hc_heap_cap, P->hc_warps_per_cta,
                            (size_t)P->hc_min_smem, device));
@@ -307,6 +323,8 @@ void plan_free(eik_plan* P) {
 int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
               bool defer_upload = false, cudaStream_t ext_stream = nullptr,
               const cudaEvent_t* ext_events = nullptr) {
+  P->hcm_exact_req = method == EIK_HCM_EXACT;
+  if (method == EIK_HCM_EXACT) method = EIK_HCM;
   P->method = method;
   P->g = p->grid;
   P->M = p->grid.m * p->grid.n;
@@ -557,6 +575,7 @@ int plan_run(eik_plan* P, eik_output* out) {
   out->host_ms = 0.0;
   out->spec_hits = out->spec_waits = out->spec_self = 0;
   out->grid_ctas = 0;
+  out->rounds = 0;
   CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
   if (P->defer_F) {  // created by eik_solve_batch: the field goes up now
     CK(cudaMemcpyAsync(P->dF, P->defer_F, sizeof(double) * P->M,
@@ -863,7 +882,7 @@ eik_plan* plan_create(const eik_problem* p, const eik_cells* c, int32_t method, 
   g_last_code = EIK_OK;
   g_last_error.clear();
   if (check_problem(p) || check_cells(p, c, method)) return nullptr;
-  if (method < EIK_FMM || method > EIK_FMSM) {
+  if (method < EIK_FMM || method > EIK_HCM_EXACT) {
     fail(EIK_ERR_CONFIG, "unknown method");
     return nullptr;
   }
@@ -1245,6 +1264,20 @@ int eik_plan_set_rows(eik_plan* P, int64_t row0, int64_t nrows, const double* sr
                       int32_t on_device) {
   if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
   return plan_rows(P, row0, nrows, const_cast<double*>(src), on_device, true);
+}
+
+int eik_set_hcm_mode(int32_t mode) {
+  if (mode != 0 && mode != 1) return fail(EIK_ERR_CONFIG, "hcm mode is 0 (band) or 1 (exact)");
+  g_hcm_mode.store(mode);
+  return EIK_OK;
+}
+
+int eik_plan_set_hcm_mode(eik_plan* P, int32_t mode) {
+  if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
+  if (mode != 0 && mode != 1) return fail(EIK_ERR_CONFIG, "hcm mode is 0 (band) or 1 (exact)");
+  if (P->method != EIK_HCM) return fail(EIK_ERR_CONFIG, "hcm mode applies to hcm plans");
+  P->hcm_band = mode == 0;
+  return EIK_OK;
 }
 
 int eik_plan_set_ctas(eik_plan* P, int32_t max_ctas) {

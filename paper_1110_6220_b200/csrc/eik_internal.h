@@ -144,6 +144,16 @@ struct HcArgs {
   int fast;                 // 0 = HCM, 1 = FHCM
   long long budget;         // removal budget 100*J+16 (heap_cell.cpp:270)
   int max_len;              // longest cell side
+  // HCM band scheduler (hcm_band_kernel): rounds of mutually non-adjacent
+  // queued cells within the acceptance band [kmin, kmin + delta]
+  int* b_inq;               // [J] cell is queued
+  unsigned* b_flags;        // [J] raised sweep flags
+  unsigned char* b_fdone;   // [J] first removal done
+  int* b_list;              // [2][J] queued cells (ping-pong by round parity)
+  int* b_work;              // [J] cells selected this round
+  int* b_ctl;               // [0..1] list sizes, [2] selected count, [3] dispenser, [4] rounds
+  unsigned long long* b_kmin;  // [0] round minimum key bits, [1] minimum C bits
+  double band_scale;        // delta = band_scale * (h + min(hc_x, hc_y)) / (2 F_max)
 };
 
 size_t heapcell_smem_bytes(const CellGeom& g, int max_len);
@@ -152,6 +162,10 @@ cudaError_t launch_heapcell(const HcArgs& a, int warps_per_cta, int max_ctas, cu
                             int* launches, int* grid = nullptr);
 cudaError_t heapcell_capacity(int64_t tile_doubles, int heap_cap, int warps_per_cta,
                               size_t min_smem, int* ctas);
+cudaError_t launch_hcm_band(const HcArgs& a, int warps_per_cta, int max_ctas, cudaStream_t s,
+                            int* launches, int* grid = nullptr);
+cudaError_t hcm_band_capacity(int64_t tile_doubles, int warps_per_cta, size_t min_smem,
+                              int* ctas);
 // Raise a kernel's dynamic shared-memory limit to at least `bytes` (never
 // lowers it: concurrent launches of the same kernel from other host threads
 // may need the larger limit).

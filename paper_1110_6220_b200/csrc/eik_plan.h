@@ -88,6 +88,16 @@ struct eik_plan {
   int* dBusy = nullptr;
   eikb200::SpecRec* dRec = nullptr;
   int* dHcMisc = nullptr;
+  // HCM band scheduler (k_heapcell.cu hcm_band_kernel)
+  bool hcm_band = false;    // HCM plan runs the band scheduler (else the exact replay)
+  bool hcm_exact_req = false;  // created as EIK_HCM_EXACT
+  int* dBInq = nullptr;
+  unsigned* dBFlags = nullptr;
+  unsigned char* dBFdone = nullptr;
+  int* dBList = nullptr;
+  int* dBWork = nullptr;
+  int* dBCtl = nullptr;
+  unsigned long long* dBKmin = nullptr;
   int* dDbg = nullptr;      // EIK_HC_DEBUG: per-worker phase trace
   int* dOwner = nullptr;    // EIK_HC_DEBUG: last claiming worker per speculation   // [0] done flag, [1] published heap size
   int hc_warps_per_cta = 1;
@@ -143,6 +153,9 @@ struct Knobs {
 };
 const Knobs& knobs();
 void reload_knobs();
+// HCM ordering for new plans: 0 = band scheduler, 1 = exact replay
+// (eik_set_hcm_mode; EIK_HCM_EXACT=1 sets the default to 1)
+int hcm_default_mode();
 
 int fail(int code, const std::string& msg);
 int cuda_fail(cudaError_t e, const char* where);

@@ -140,6 +140,23 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     // 128-byte line each (all workers poll them)
     if ((rc = dalloc(&P->dHcMisc, 32 + 32 * 32))) return rc;
     P->allocs.push_back(P->dHcMisc);
+    if (P->method == EIK_HCM) {  // band scheduler state (hcm_band_kernel)
+      if ((rc = dalloc(&P->dBInq, J))) return rc;
+      P->allocs.push_back(P->dBInq);
+      if ((rc = dalloc(&P->dBFlags, J))) return rc;
+      P->allocs.push_back(P->dBFlags);
+      if ((rc = dalloc(&P->dBFdone, J))) return rc;
+      P->allocs.push_back(P->dBFdone);
+      if ((rc = dalloc(&P->dBList, 2 * J))) return rc;
+      P->allocs.push_back(P->dBList);
+      if ((rc = dalloc(&P->dBWork, J))) return rc;
+      P->allocs.push_back(P->dBWork);
+      if ((rc = dalloc(&P->dBCtl, 8))) return rc;
+      P->allocs.push_back(P->dBCtl);
+      if ((rc = dalloc(&P->dBKmin, 2))) return rc;
+      P->allocs.push_back(P->dBKmin);
+      P->hcm_band = !P->hcm_exact_req && hcm_default_mode() == 0;
+    }
     // per-warp tile: values + costs with halo, 4 border snapshots, lock bytes
     const size_t tile = ((smem + sizeof(double) - 1) / sizeof(double) + 1) & ~(size_t)1;
     P->cg.tile_doubles = (int64_t)tile;
@@ -289,6 +306,88 @@ int plan_run_fmsm(eik_plan* P, eik_output* out) {
   return EIK_OK;
 }
 
+// HCM by rounds of the acceptance band (k_heapcell.cu hcm_band_kernel).
+int plan_run_hcm_band(eik_plan* P, eik_output* out, const std::vector<int>& icells,
+                      const std::vector<double>& ivals) {
+  const int64_t J = (int64_t)P->cells_x * P->cells_y;
+  const Knobs& kn = knobs();
+  int launches = 0;
+  CK(cudaEventRecord(P->ev0, P->stream));
+  CK(cudaMemcpyAsync(P->dInitCells, icells.data(), sizeof(int) * icells.size(),
+                     cudaMemcpyHostToDevice, P->stream));
+  CK(cudaMemcpyAsync(P->dInitValues, ivals.data(), sizeof(double) * ivals.size(),
+                     cudaMemcpyHostToDevice, P->stream));
+  CK(cudaMemsetAsync(P->dCounters, 0, sizeof(unsigned long long) * 48, P->stream));
+  CK(cudaMemsetAsync(P->dBCtl, 0, sizeof(int) * 8, P->stream));
+  CK(cudaMemsetAsync(P->dBKmin, 0xFF, sizeof(unsigned long long) * 2, P->stream));
+  CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
+                    P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
+  HcArgs a{};
+  a.g = P->cg;
+  a.C = P->dC;
+  a.u = P->dU;
+  for (int s = 0; s < 4; ++s) a.probe[s] = P->dProbe[s];
+  a.h = P->g.h;
+  a.hc_x = (double)(P->g.m / P->cells_x) * P->g.h;  // cells.cpp:44-45
+  a.hc_y = (double)(P->g.n / P->cells_y) * P->g.h;
+  a.cval = P->dCVal;
+  a.init_cells = P->dInitCells;
+  a.init_values = P->dInitValues;
+  a.n_init = (int)icells.size();
+  a.counters = P->dCounters;
+  a.status = P->dStatus;
+  a.J = (int)J;
+  a.fast = 0;
+  a.budget = 100LL * J + 16;
+  a.max_len = P->max_len;
+  a.tile_doubles = P->cg.tile_doubles;
+  a.min_smem = P->hc_min_smem;
+  a.cx_magic = P->hc_cx_magic;
+  a.skip_from = kn.hc_skip_from;
+  a.b_inq = P->dBInq;
+  a.b_flags = P->dBFlags;
+  a.b_fdone = P->dBFdone;
+  a.b_list = P->dBList;
+  a.b_work = P->dBWork;
+  a.b_ctl = P->dBCtl;
+  a.b_kmin = P->dBKmin;
+  a.band_scale = kn.hcm_band > 0.0 ? kn.hcm_band : 1.0;
+  const int hc_ctas = P->cap() > 0 ? std::min(P->hc_max_ctas, P->cap()) : P->hc_max_ctas;
+  int grid = 0;
+  CK(launch_hcm_band(a, P->hc_warps_per_cta, hc_ctas, P->stream, &launches, &grid));
+  out->grid_ctas = grid;
+  if (P->on_launched) {
+    auto f = std::move(P->on_launched);
+    P->on_launched = nullptr;
+    f();
+  }
+  CK(cudaEventRecord(P->ev1, P->stream));
+  int st[8];
+  int ctl[8];
+  unsigned long long cnt[4];
+  CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
+  CK(cudaMemcpyAsync(ctl, P->dBCtl, sizeof(ctl), cudaMemcpyDeviceToHost, P->stream));
+  CK(cudaMemcpyAsync(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost, P->stream));
+  CK(cudaStreamSynchronize(P->stream));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  if (st[0] == 3) return fail(EIK_ERR_BUDGET, "heap-cell removal budget exceeded");
+  out->heap_removals = (int64_t)cnt[0];
+  out->sweeps = (int64_t)cnt[1];
+  out->node_updates = (int64_t)cnt[2];
+  out->mon_checks = out->mon_single = 0;
+  out->cell_removals = out->heap_removals;
+  out->cell_sweeps = out->sweeps;
+  out->avhr = (double)out->heap_removals / (double)J;
+  out->avs = (double)out->sweeps / (double)J;
+  out->mon_pct = 0.0;
+  out->rounds = ctl[4];
+  out->device_ms = ms;
+  out->kernel_launches = launches;
+  return EIK_OK;
+}
+
 int plan_run_heapcell(eik_plan* P, eik_output* out) {
   const int64_t J = (int64_t)P->cells_x * P->cells_y;
   // Cells intersecting the exit set start on the list with value = max exit
@@ -329,6 +428,7 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
     ivals[k] = init[k].second;
   }
   int launches = 0;
+  if (P->method == EIK_HCM && P->hcm_band) return plan_run_hcm_band(P, out, icells, ivals);
 retry:  // after a committer heap overflow, with the heap in global memory
   CK(cudaEventRecord(P->ev0, P->stream));
   CK(cudaMemcpyAsync(P->dInitCells, icells.data(), sizeof(int) * icells.size(),

@@ -32,6 +32,8 @@
 // and counter equals the reference's (tests/test_gpu_cells.py).
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "eik_internal.h"
 #include "k_cellsweep.cuh"
 #include "k_common.cuh"
@@ -1351,6 +1353,270 @@ __global__ void heapcell_gather_kernel(HcArgs a) {
   }
 }
 
+// ---- HCM band scheduler ------------------------------------------------------
+// north_star (3): instead of popping one cell at a time, every round processes
+// all queued cells whose value lies in the acceptance band [kmin, kmin+delta]
+// and that are a (value, id) local minimum among the in-band queued cells
+// next to them -- so no two cells of a round are adjacent: each reads only
+// its own nodes and the cross halo of its four neighbours, none of which
+// changes during the round, and the round equals the same pops made one
+// after another in any order.  Every pop is the reference's HCM processing
+// (heap_cell.cpp:273-312: snapshot, process_to_convergence, the four border
+// scans with cell_value min-update, flag OR and insertion), so the algorithm
+// is HCM with a different pop order: it ends, like the reference, when no
+// cell is queued, i.e. at the discrete fixed point -- within rounding of the
+// reference's field (tests: <= 1e-10; measured ~1e-15).  delta =
+// (h + h_c) / (2 F_max) is the smallest increment a border scan can add to a
+// neighbour's value (cell_value_candidate, cells.hpp:109-112): no cell in the
+// band can receive a smaller key from another in-band cell's processing
+// (SURVEY finding 5: 854 rounds instead of 22k pops on C2 at 16-node cells).
+// Pops, sweeps and node updates are this order's, reported beside the
+// reference's; EIK_HCM_EXACT=1 / eik_plan_set_hcm_mode select the exact
+// replay (bit-identical, the reference's counters).
+namespace cg = cooperative_groups;
+
+__device__ __forceinline__ unsigned long long key_bits(double k) {
+  return k == 0.0 ? 0ull : (unsigned long long)__double_as_longlong(k);  // k >= 0
+}
+__device__ __forceinline__ bool key_less(double ka, int ia, double kb, int ib) {
+  return ka < kb || (ka == kb && ia < ib);
+}
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long w = __shfl_xor_sync(kFull, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+// One pop of HCM, in place in u: stage the cell and its cross halo, sweep to
+// convergence, write the values back, scan the borders and apply the scans to
+// the neighbours (atomics: neighbours of a round's cells may be shared).
+__device__ void band_process(const HcArgs& a, HTile& T, double* before, SpecRec* rec, int cell,
+                             int lane, long long& sweeps, long long& updates, int* nxt,
+                             int* nxt_cnt) {
+  const CellGeom& g = a.g;
+  int64_t ib, ie, jb, je;
+  hc_cell_rect(g, a.cx_magic, cell, ib, ie, jb, je);
+  T.w = (int)(ie - ib);
+  T.h = (int)(je - jb);
+  int cx, cy;
+  cell_xy(cell, g.cells_x, a.cx_magic, cx, cy);
+  const bool has_nb[4] = {cx > 0, cx + 1 < g.cells_x, cy > 0, cy + 1 < g.cells_y};
+  const int nbs[4] = {cell - 1, cell + 1, cell - g.cells_x, cell + g.cells_x};
+  double* pstrip = before + 4 * a.max_len;
+  // values and costs with the cross halo (no corners), row by row; the padded
+  // layout gives +inf / -1 beside the grid, rows -1 and n are filled here
+  const int tw = T.w + 2;
+  for (int y = -1; y <= T.h; ++y) {
+    const int64_t gj = jb + y;
+    const bool rin = gj >= 0 && gj < g.n;
+    const double* ur = a.u + gj * g.P + g.pad + ib;
+    const double* cr = a.C + gj * g.P + g.pad + ib;
+    for (int t = lane; t < tw; t += 32) {
+      const int x = t - 1;
+      const bool corner = (y < 0 || y >= T.h) && (x < 0 || x >= T.w);
+      if (corner) continue;
+      T.u(x, y) = rin ? __ldcg(ur + x) : kInf;
+      T.Ct[T.ci(x, y)] = rin ? __ldg(cr + x) : -1.0;
+    }
+  }
+  for (int t = lane; t < a.max_len; t += 32) {  // F at the border probe points
+    if (t < T.h) {
+      pstrip[0 * a.max_len + t] = has_nb[0] ? __ldg(a.probe[0] + (int64_t)cx * g.n + jb + t) : 1.0;
+      pstrip[1 * a.max_len + t] = has_nb[1] ? __ldg(a.probe[1] + (int64_t)cx * g.n + jb + t) : 1.0;
+    }
+    if (t < T.w) {
+      pstrip[2 * a.max_len + t] = has_nb[2] ? __ldg(a.probe[2] + (int64_t)cy * g.m + ib + t) : 1.0;
+      pstrip[3 * a.max_len + t] = has_nb[3] ? __ldg(a.probe[3] + (int64_t)cy * g.m + ib + t) : 1.0;
+    }
+  }
+  __syncwarp();
+  for (int t = lane; t < T.h; t += 32) {  // border snapshots (heap_cell.cpp:279-282)
+    before[0 * a.max_len + t] = T.u(0, t);
+    before[1 * a.max_len + t] = T.u(T.w - 1, t);
+  }
+  for (int t = lane; t < T.w; t += 32) {
+    before[2 * a.max_len + t] = T.u(t, 0);
+    before[3 * a.max_len + t] = T.u(t, T.h - 1);
+  }
+  // flags and first removal: only this cell's neighbours write them, and
+  // none of them is processed in this round
+  unsigned my_flags = 0;
+  bool first_removal = false;
+  if (lane == 0) {
+    my_flags = __ldcg(a.b_flags + cell);
+    a.b_flags[cell] = 0;
+    first_removal = !__ldcg(a.b_fdone + cell);
+    a.b_fdone[cell] = 1;
+  }
+  my_flags = __shfl_sync(kFull, my_flags, 0);
+  first_removal = __shfl_sync(kFull, first_removal, 0);
+  reset_locks(T, ib > 0, ie < g.m, jb > 0, je < g.n, lane);
+  const CellTile ct{T.U, T.Ct, T.lock, T.pu, T.w, T.h, 2};
+  long long nsw = 0, upd = 0;
+  {  // process_to_convergence (heap_cell.cpp:130-147)
+    int perm[4], nflag = 0;
+    for (int k = 0; k < 4; ++k)
+      if (my_flags & (1u << kFlagOrder[k])) perm[nflag++] = kFlagOrder[k];
+    int at = nflag;
+    for (int k = 0; k < 4; ++k)
+      if (!(my_flags & (1u << kRotation[k]))) perm[at++] = kRotation[k];
+    bool changed = true;
+    while (changed) {
+      const int dir = nsw < 4 ? perm[nsw] : kRotation[nsw % 4];
+      changed = cell_sweep<2>(ct, dir, lane, upd, /*skip=*/nsw >= a.skip_from);
+      ++nsw;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) upd += __shfl_xor_sync(kFull, upd, o);
+  sweeps += nsw;
+  updates += upd;
+  // values back into the field
+  for (int k = lane; k < T.w * T.h; k += 32) {
+    const int y = k / T.w, x = k % T.w;
+    __stcg(a.u + (jb + y) * g.P + g.pad + ib + x, T.u(x, y));
+  }
+  scan_all(a, T, before, pstrip, first_removal,
+           (has_nb[0] ? 1u : 0u) | (has_nb[1] ? 2u : 0u) | (has_nb[2] ? 4u : 0u) |
+               (has_nb[3] ? 8u : 0u),
+           rec, lane);
+  __syncwarp();
+  if (lane < 4 && has_nb[lane]) {  // the scans' effects on the four neighbours
+    const int nb = nbs[lane];
+    const double cand = rec->cand[lane];
+    const unsigned sd = rec->side[lane];
+    if (cand < kInf)  // cell_value[nb] = min(cell_value[nb], cand); keys >= 0
+      atomicMin(reinterpret_cast<unsigned long long*>(a.cval + nb), key_bits(cand));
+    if (sd & 1u) {
+      atomicOr(a.b_flags + nb, (sd >> 8) & 0xFFu);
+      if (atomicExch(a.b_inq + nb, 1) == 0) nxt[atomicAdd(nxt_cnt, 1)] = nb;
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ __align__(16) double smem[];
+  __shared__ SpecRec srec[8];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  const int wpc = blockDim.x >> 5;
+  const CellGeom& g = a.g;
+  HTile T;
+  T.pu = g.pu;
+  T.U = smem + (size_t)wib * a.tile_doubles;
+  T.Ct = T.U + (size_t)(g.max_h + 2) * g.pu;
+  double* before = T.Ct + (size_t)(g.max_h + 2) * g.pu;
+  T.lock = reinterpret_cast<uint8_t*>(before + 8 * a.max_len);
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nthreads = gridDim.x * blockDim.x;
+  const int J = a.J;
+
+  // ---- init: cell state, F_max (the band width), the Q-cells -----------------
+  unsigned long long cmin = ~0ull;
+  for (int c = tid; c < J; c += nthreads) {
+    a.cval[c] = kInf;
+    a.b_inq[c] = 0;
+    a.b_flags[c] = 0;
+    a.b_fdone[c] = 0;
+  }
+  for (int64_t k = tid; k < g.n * g.P; k += nthreads) {  // min C = h / F_max over nodes
+    const double c = a.C[k];
+    if (c > 0.0) cmin = min(cmin, (unsigned long long)__double_as_longlong(c));
+  }
+  cmin = warp_min_u64(cmin);
+  if (lane == 0 && cmin != ~0ull) atomicMin(a.b_kmin + 1, cmin);
+  grid.sync();
+  if (tid == 0) {
+    for (int k = 0; k < a.n_init; ++k) {  // heap_cell.cpp:255-268
+      const int c = a.init_cells[k];
+      a.cval[c] = a.init_values[k];
+      a.b_inq[c] = 1;
+      a.b_list[k] = c;
+    }
+    a.b_ctl[0] = a.n_init;
+    a.b_ctl[1] = 0;
+  }
+  grid.sync();
+  const double cmin_d = __longlong_as_double((long long)a.b_kmin[1]);
+  const double delta = a.band_scale * 0.5 * (a.h + fmin(a.hc_x, a.hc_y)) * (cmin_d / a.h);
+
+  long long removals = 0, sweeps = 0, updates = 0;
+  int round = 0;
+  for (;; ++round) {
+    const int par = round & 1;
+    int* cur = a.b_list + (size_t)par * J;
+    int* nxt = a.b_list + (size_t)(par ^ 1) * J;
+    const int ncur = *(volatile int*)(a.b_ctl + par);
+    if (ncur == 0) break;
+    // phase 1: the band's base, the minimum key of the queued cells
+    unsigned long long mk = ~0ull;
+    for (int i = tid; i < ncur; i += nthreads) mk = min(mk, key_bits(__ldcg(a.cval + __ldcg(cur + i))));
+    mk = warp_min_u64(mk);
+    if (lane == 0 && mk != ~0ull) atomicMin(a.b_kmin, mk);
+    if (tid == 0) {
+      a.b_ctl[par ^ 1] = 0;
+      a.b_ctl[2] = 0;
+      a.b_ctl[3] = 0;
+    }
+    grid.sync();
+    // phase 2: select the in-band local minima; the rest stay queued
+    const double kmin = __longlong_as_double((long long)*(volatile unsigned long long*)a.b_kmin);
+    const double band = kmin + delta;
+    for (int i = tid; i < ncur; i += nthreads) {
+      const int c = __ldcg(cur + i);
+      const double k = __ldcg(a.cval + c);
+      bool sel = k <= band;
+      if (sel) {
+        int cx, cy;
+        cell_xy(c, g.cells_x, a.cx_magic, cx, cy);
+        const int nbs[4] = {cx > 0 ? c - 1 : -1, cx + 1 < g.cells_x ? c + 1 : -1,
+                            cy > 0 ? c - g.cells_x : -1, cy + 1 < g.cells_y ? c + g.cells_x : -1};
+#pragma unroll
+        for (int d = 0; d < 4; ++d) {
+          const int nb = nbs[d];
+          if (nb >= 0 && __ldcg(a.b_inq + nb)) {
+            const double kn = __ldcg(a.cval + nb);
+            if (kn <= band && key_less(kn, nb, k, c)) sel = false;
+          }
+        }
+      }
+      if (sel) a.b_work[atomicAdd(a.b_ctl + 2, 1)] = c;
+      else nxt[atomicAdd(a.b_ctl + (par ^ 1), 1)] = c;
+    }
+    grid.sync();
+    // phase 3: the selected cells, one warp each
+    if (tid == 0) a.b_kmin[0] = ~0ull;
+    const int nwork = *(volatile int*)(a.b_ctl + 2);
+    if (tid == 0) {
+      removals += nwork;
+      if (removals > a.budget) atomicExch(a.status, 3);  // read by all after the sync
+    }
+    for (;;) {
+      int i = 0;
+      if (lane == 0) i = atomicAdd(a.b_ctl + 3, 1);
+      i = __shfl_sync(kFull, i, 0);
+      if (i >= nwork) break;
+      const int c = __ldcg(a.b_work + i);
+      if (lane == 0) a.b_inq[c] = 0;  // popped
+      band_process(a, T, before, &srec[wib], c, lane, sweeps, updates, nxt, a.b_ctl + (par ^ 1));
+    }
+    grid.sync();
+    if (*(volatile int*)a.status == 3) break;  // set before the sync: all threads agree
+  }
+  if (lane == 0) {
+    atomicAdd(a.counters + 1, (unsigned long long)sweeps);
+    atomicAdd(a.counters + 2, (unsigned long long)updates);
+  }
+  if (tid == 0) {
+    atomicAdd(a.counters + 0, (unsigned long long)removals);
+    a.b_ctl[4] = round;
+  }
+}
+
 }  // namespace
 
 size_t heapcell_smem_bytes(const CellGeom& g, int max_len) {
@@ -1419,6 +1685,44 @@ cudaError_t launch_heapcell(const HcArgs& args, int warps_per_cta, int max_ctas,
   heapcell_gather_kernel<<<blocks, 256, 0, s>>>(args);
   *launches += 3;
   return cudaGetLastError();
+}
+
+cudaError_t hcm_band_capacity(int64_t tile_doubles, int warps_per_cta, size_t min_smem,
+                              int* ctas) {
+  const size_t smem = std::max((size_t)warps_per_cta * tile_doubles * sizeof(double), min_smem);
+  const void* kern = (const void*)hcm_band_kernel;
+  cudaError_t e = ensure_dynamic_smem(kern, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps_per_cta, smem);
+  if (e != cudaSuccess) return e;
+  *ctas = per_sm * sms;
+  return cudaSuccess;
+}
+
+cudaError_t launch_hcm_band(const HcArgs& args, int warps_per_cta, int max_ctas, cudaStream_t s,
+                            int* launches, int* grid) {
+  const size_t smem =
+      std::max((size_t)warps_per_cta * args.tile_doubles * sizeof(double), (size_t)args.min_smem);
+  const void* kern = (const void*)hcm_band_kernel;
+  cudaError_t e = ensure_dynamic_smem(kern, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0, dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps_per_cta, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) return cudaErrorInvalidConfiguration;
+  int ctas = std::min(per_sm * sms, max_ctas);
+  if (ctas < 1) ctas = 1;
+  if (grid) *grid = ctas;
+  HcArgs a = args;
+  void* params[] = {&a};
+  e = cudaLaunchCooperativeKernel(kern, dim3(ctas), dim3(32 * warps_per_cta), params, smem, s);
+  *launches += 1;
+  return e;
 }
 
 }  // namespace eikb200

@@ -50,6 +50,7 @@ class SolverOutput:
     host_ms: float = 0.0
     kernel_launches: int = 0
     spec: tuple = (0, 0, 0)  # heap-cell replay: (hits, waits, self-processed)
+    rounds: int = 0          # HCM band scheduler: rounds
     ctas: int = 0            # CTAs of the persistent solve kernel
     acceptance_order: Optional[np.ndarray] = None  # FMM only, when requested (grid.hpp:148)
 
@@ -102,7 +103,7 @@ def _pack(out: N.eik_output, values: np.ndarray, g) -> SolverOutput:
                         device_ms=out.device_ms, host_ms=out.host_ms,
                         kernel_launches=out.kernel_launches,
                         spec=(out.spec_hits, out.spec_waits, out.spec_self),
-                        ctas=out.grid_ctas)
+                        ctas=out.grid_ctas, rounds=out.rounds)
 
 
 def solve(problem: Problem, method: str, cells: Optional[CellDecomposition] = None,
@@ -155,6 +156,12 @@ def lsm_solve(problem: Problem) -> SolverOutput:
 
 def hcm_solve(problem: Problem, cells: CellDecomposition) -> SolverOutput:
     return solve(problem, "hcm", cells)
+
+
+def set_hcm_mode(mode: str) -> None:
+    """Default HCM ordering for later solves/plans: "band" (the band
+    scheduler, default) or "exact" (the exact replay; also method "hcm_exact")."""
+    N.raise_for(N.lib.eik_set_hcm_mode({"band": 0, "exact": 1}[mode]))
 
 
 def fhcm_solve(problem: Problem, cells: CellDecomposition) -> SolverOutput:

@@ -75,8 +75,13 @@ def test_run_row_matches_reference_row(tmp_path):
     p = make()
     exact = E.fmm_solve(p).values
     truth = E.ground_truth(p, 4)
-    for meth in ("fhcm", "hcm", "fmsm"):
-        r = X.run_row(cid, p, meth, cells[0], exact, truth, dump_dir=str(tmp_path))
+    E.set_hcm_mode("exact")  # the reference's counters need its exact heap order
+    try:
+        rows = [(meth, X.run_row(cid, p, meth, cells[0], exact, truth, dump_dir=str(tmp_path)))
+                for meth in ("fhcm", "hcm", "fmsm")]
+    finally:
+        E.set_hcm_mode("band")
+    for meth, r in rows:
         key = f"{cid}/{meth}/{cells[0]}"
         assert (r.sweeps, r.node_updates, r.heap_removals) == (
             counters[key]["sweeps"], counters[key]["node_updates"], counters[key]["heap_removals"])

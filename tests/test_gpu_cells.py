@@ -19,6 +19,9 @@ from oracle import oracle as O
 from tests.golden.make_golden import SMALL_CASES
 
 pytestmark = pytest.mark.gpu
+# bit-exact parity with the reference's HCM needs the exact replay of its heap
+# order ("hcm_exact"); "hcm" itself runs the band scheduler (test_gpu_hcm_band.py)
+EXACT = {"hcm": "hcm_exact"}
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 
@@ -128,7 +131,7 @@ def test_hcm_fhcm_small_golden_fields(cid, make, cells):
     for c in cells:
         for method in ("hcm", "fhcm"):
             key = f"{cid}/{method}/{c}"
-            out = E.solve(p, method, E.build_cells(p.grid, c, c))
+            out = E.solve(p, EXACT.get(method, method), E.build_cells(p.grid, c, c))
             assert bitwise(out.values, arrays[key]), key
             m = meta[key]
             assert (out.sweeps, out.node_updates, out.heap_removals, out.hybrid.mon_checks,
@@ -141,7 +144,7 @@ def test_hcm_fhcm_small_golden_fields(cid, make, cells):
 def test_heapcell_c2_bitwise_full_size(method, cs):
     big = _big()[f"c2/{method}/{cs}"]
     p = configs.config2().problem
-    out = E.solve(p, method, E.build_cells(p.grid, big["cells"], big["cells"]))
+    out = E.solve(p, EXACT.get(method, method), E.build_cells(p.grid, big["cells"], big["cells"]))
     assert sha(out.values) == big["sha256"]
     assert (out.sweeps, out.node_updates, out.heap_removals, out.hybrid.mon_checks,
             out.hybrid.mon_single) == (big["sweeps"], big["node_updates"], big["heap_removals"],
@@ -163,7 +166,7 @@ def test_heapcell_random_against_oracle(seed):
     for cx, cy in [(1, 1), (2, 3), (int(rng.integers(2, 10)), int(rng.integers(2, 10)))]:
         cells = E.build_cells(g, cx, cy)
         for method in ("hcm", "fhcm"):
-            a = E.solve(p, method, cells)
+            a = E.solve(p, EXACT.get(method, method), cells)
             b = O.oracle_solve(p, method, cells)
             assert bitwise(a.values, b.u), (method, cx, cy)
             assert (a.sweeps, a.node_updates, a.heap_removals, a.hybrid.mon_checks,
@@ -239,7 +242,7 @@ def _engine_variant_bitwise(env):
     p = configs.config2(257).problem
     cells = E.build_cells(p.grid, 16, 16)
     for method in ("hcm", "fhcm"):
-        a = E.solve(p, method, cells)
+        a = E.solve(p, EXACT.get(method, method), cells)
         b = O.oracle_solve(p, method, cells)
         assert bitwise(a.values, b.u), (method, env)
         assert (a.sweeps, a.node_updates, a.heap_removals, a.hybrid.mon_checks,
