@@ -351,7 +351,8 @@ int plan_run_hcm_band(eik_plan* P, eik_output* out, const std::vector<int>& icel
   a.b_work = P->dBWork;
   a.b_ctl = P->dBCtl;
   a.b_kmin = P->dBKmin;
-  a.band_scale = kn.hcm_band > 0.0 ? kn.hcm_band : 1.0;
+  a.band_scale = kn.hcm_band > 0.0 ? kn.hcm_band : 4.0;
+  a.prof = kn.hc_profile ? 1 : 0;
   const int hc_ctas = P->cap() > 0 ? std::min(P->hc_max_ctas, P->cap()) : P->hc_max_ctas;
   int grid = 0;
   CK(launch_hcm_band(a, P->hc_warps_per_cta, hc_ctas, P->stream, &launches, &grid));
@@ -364,7 +365,7 @@ int plan_run_hcm_band(eik_plan* P, eik_output* out, const std::vector<int>& icel
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];
   int ctl[8];
-  unsigned long long cnt[4];
+  unsigned long long cnt[12];
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaMemcpyAsync(ctl, P->dBCtl, sizeof(ctl), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaMemcpyAsync(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost, P->stream));
@@ -373,6 +374,11 @@ int plan_run_hcm_band(eik_plan* P, eik_output* out, const std::vector<int>& icel
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
   if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
   if (st[0] == 3) return fail(EIK_ERR_BUDGET, "heap-cell removal budget exceeded");
+  if (kn.hc_profile && grid > 0)
+    std::fprintf(stderr, "hcm band: %d rounds, per CTA per round (cycles): sync %.0f select %.0f "
+                 "work %.0f kmin %.0f\n", ctl[4], (double)cnt[8] / grid / std::max(1, ctl[4]),
+                 (double)cnt[9] / grid / std::max(1, ctl[4]), (double)cnt[10] / grid / std::max(1, ctl[4]),
+                 (double)cnt[11] / grid / std::max(1, ctl[4]));
   out->heap_removals = (int64_t)cnt[0];
   out->sweeps = (int64_t)cnt[1];
   out->node_updates = (int64_t)cnt[2];

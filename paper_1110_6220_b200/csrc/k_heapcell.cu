@@ -1545,6 +1545,16 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
   const double delta = a.band_scale * 0.5 * (a.h + fmin(a.hc_x, a.hc_y)) * (cmin_d / a.h);
 
   long long removals = 0, sweeps = 0, updates = 0;
+  long long cyc_sync = 0, cyc_sel = 0, cyc_work = 0, cyc_kmin = 0;  // EIK_HC_PROFILE
+  const bool prof = a.prof && threadIdx.x == 0;
+  long long tp = prof ? clock64() : 0;
+  auto lap = [&](long long& acc) {
+    if (prof) {
+      const long long t = clock64();
+      acc += t - tp;
+      tp = t;
+    }
+  };
   int round = 0;
   for (;; ++round) {
     const int par = round & 1;
@@ -1562,7 +1572,9 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
       a.b_ctl[2] = 0;
       a.b_ctl[3] = 0;
     }
+    lap(cyc_kmin);
     grid.sync();
+    lap(cyc_sync);
     // phase 2: select the in-band local minima; the rest stay queued
     const double kmin = __longlong_as_double((long long)*(volatile unsigned long long*)a.b_kmin);
     const double band = kmin + delta;
@@ -1587,7 +1599,9 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
       if (sel) a.b_work[atomicAdd(a.b_ctl + 2, 1)] = c;
       else nxt[atomicAdd(a.b_ctl + (par ^ 1), 1)] = c;
     }
+    lap(cyc_sel);
     grid.sync();
+    lap(cyc_sync);
     // phase 3: the selected cells, one warp each
     if (tid == 0) a.b_kmin[0] = ~0ull;
     const int nwork = *(volatile int*)(a.b_ctl + 2);
@@ -1604,7 +1618,9 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
       if (lane == 0) a.b_inq[c] = 0;  // popped
       band_process(a, T, before, &srec[wib], c, lane, sweeps, updates, nxt, a.b_ctl + (par ^ 1));
     }
+    lap(cyc_work);
     grid.sync();
+    lap(cyc_sync);
     if (*(volatile int*)a.status == 3) break;  // set before the sync: all threads agree
   }
   if (lane == 0) {
@@ -1614,6 +1630,12 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
   if (tid == 0) {
     atomicAdd(a.counters + 0, (unsigned long long)removals);
     a.b_ctl[4] = round;
+  }
+  if (prof) {  // per-CTA sums (thread 0): where a round's time goes
+    atomicAdd(a.counters + 8, (unsigned long long)cyc_sync);
+    atomicAdd(a.counters + 9, (unsigned long long)cyc_sel);
+    atomicAdd(a.counters + 10, (unsigned long long)cyc_work);
+    atomicAdd(a.counters + 11, (unsigned long long)cyc_kmin);
   }
 }
 

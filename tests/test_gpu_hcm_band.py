@@ -42,7 +42,7 @@ def test_band_small_cases_against_reference_hcm(cid, make, cells):
 @pytest.mark.parametrize("seed", range(6))
 def test_band_random_grids(seed):
     rng = np.random.default_rng(900 + seed)
-    m, n = int(rng.integers(10, 160)), int(rng.integers(10, 160))
+    m, n = int(rng.integers(10, 120)), int(rng.integers(10, 120))
     g = E.Grid(m, n, float(rng.uniform(0.002, 0.05)), 0.2, -0.4)
     F = rng.uniform(0.05, 3.0, size=(n, m))
     sp = lambda x, y, F=F, g=g: F[np.clip(np.rint((y - g.y0) / g.h).astype(int), 0, g.n - 1),  # noqa: E731
