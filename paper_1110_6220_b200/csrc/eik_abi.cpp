@@ -954,7 +954,7 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   const int budget = std::max(1, (int)std::floor(0.98 * sms));
   const Knobs& kn = knobs();
-  const int workers = std::max(1, std::min(n, kn.batch_workers > 0 ? kn.batch_workers : 32));
+  const int workers = std::max(1, std::min(n, kn.batch_workers > 0 ? kn.batch_workers : 64));
   struct Waiting {
     int k;
     BatchSlot b;
