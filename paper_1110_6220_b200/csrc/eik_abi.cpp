@@ -295,7 +295,14 @@ int plan_capacity(eik_plan* P, int* device, int* fixed) {
       CK(fmsm_capacity(P->cg.tile_doubles, P->warps_per_cta, device));
       break;
     case EIK_HCM:
-      if (P->hcm_band) {
+    case EIK_FHCM:
+      if (P->cells_big) {  // one warp: the serial heap loop
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, P->device));
+        *device = sms;
+        break;
+      }
+      if (P->method == EIK_HCM && P->hcm_band) {
         CK(hcm_band_capacity(P->cg.tile_doubles, P->hc_warps_per_cta, (size_t)P->hc_min_smem,
                              device));
         break;
@@ -350,11 +357,15 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
   if ((rc = dalloc(&P->dF, P->M))) return rc;
   track(P->dF);
   P->pitch = P->g.m + 2 * kPad;
-  const size_t padded = (size_t)(P->g.n + 1) * P->pitch;
-  if ((rc = dalloc(&P->dC, padded))) return rc;
-  track(P->dC);
-  if ((rc = dalloc(&P->dU, padded))) return rc;
-  track(P->dU);
+  // rows -1 .. n (both dummies): dC / dU point at row 0
+  const size_t padded = (size_t)(P->g.n + 2) * P->pitch;
+  double* base = nullptr;
+  if ((rc = dalloc(&base, padded))) return rc;
+  track(base);
+  P->dC = base + P->pitch;
+  if ((rc = dalloc(&base, padded))) return rc;
+  track(base);
+  P->dU = base + P->pitch;
   if ((rc = dalloc(&P->dExit, P->n_exit))) return rc;
   track(P->dExit);
   if ((rc = dalloc(&P->dExitCost, P->n_exit))) return rc;

@@ -8,7 +8,8 @@ namespace eikb200 {
 
 // Device layout of every plan (chosen for the kernels, not the caller):
 // value field u and cost C = h/F are stored with a row pitch P = m + 2*kPad
-// and n+1 rows; grid node (i,j) lives at j*P + kPad + i.  Padding columns and
+// and rows -1..n (the base pointer is row 0); grid node (i,j) lives at
+// j*P + kPad + i.  Padding columns and
 // the dummy row n hold u = +inf, C = -1 (the exit/no-update marker), so the
 // sweep kernels never test bounds.
 constexpr int64_t kPad = 64;
@@ -76,6 +77,7 @@ struct FmsmArgs {
   int* status;
   int J;
   int max_cell_sweeps;
+  int big;                  // cells too large for a shared-memory tile: swept in place
 };
 
 // max_ctas caps the persistent grid (0: the whole device) so that plans can
@@ -154,6 +156,10 @@ struct HcArgs {
   int* b_ctl;               // [0..1] list sizes, [2] selected count, [3] dispenser, [4] rounds
   unsigned long long* b_kmin;  // [0] round minimum key bits, [1] minimum C bits
   double band_scale;        // delta = band_scale * (h + min(hc_x, hc_y)) / (2 F_max)
+  // cells too large for a shared-memory tile (heapcell_serial_kernel): the
+  // exact heap loop, one warp, cells swept in place in u
+  uint8_t* big_lock;        // [max_h * max_w] lock bytes
+  double* big_scratch;      // [8 * max_len] border snapshots + probe strips
 };
 
 size_t heapcell_smem_bytes(const CellGeom& g, int max_len);
@@ -164,6 +170,7 @@ cudaError_t heapcell_capacity(int64_t tile_doubles, int heap_cap, int warps_per_
                               size_t min_smem, int* ctas);
 cudaError_t launch_hcm_band(const HcArgs& a, int warps_per_cta, int max_ctas, cudaStream_t s,
                             int* launches, int* grid = nullptr);
+cudaError_t launch_heapcell_serial(const HcArgs& a, cudaStream_t s, int* launches);
 cudaError_t hcm_band_capacity(int64_t tile_doubles, int warps_per_cta, size_t min_smem,
                               int* ctas);
 // Raise a kernel's dynamic shared-memory limit to at least `bytes` (never

@@ -98,6 +98,9 @@ struct eik_plan {
   int* dBWork = nullptr;
   int* dBCtl = nullptr;
   unsigned long long* dBKmin = nullptr;
+  bool cells_big = false;   // cell tiles exceed shared memory: swept in place in u
+  uint8_t* dBigLock = nullptr;
+  double* dBigScratch = nullptr;
   int* dDbg = nullptr;      // EIK_HC_DEBUG: per-worker phase trace
   int* dOwner = nullptr;    // EIK_HC_DEBUG: last claiming worker per speculation   // [0] done flag, [1] published heap size
   int hc_warps_per_cta = 1;

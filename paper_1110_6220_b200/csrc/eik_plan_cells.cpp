@@ -74,19 +74,64 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
   if (P->method == EIK_HCM || P->method == EIK_FHCM) g.pu = even_up(g.max_w + 3);
   g.pc = even_up(g.max_w);
   g.tile_doubles = 2 * (int64_t)(g.max_h + 2) * g.pu;  // values + costs, both with halo
-  if (g.max_h > 32 * 4)
-    return fail(EIK_ERR_NOT_IMPL, "cells taller than 128 nodes are not supported by the warp engine");
   const size_t tile_bytes = (size_t)g.tile_doubles * sizeof(double);
-  if (tile_bytes > kTileMax)
-    return fail(EIK_ERR_NOT_IMPL, "cell too large for the shared-memory tile (max ~150x150 nodes)");
-  P->warps_per_cta = (int)std::max<size_t>(1, std::min<size_t>(8, kTileBudget / tile_bytes));
+  const bool hc = P->method == EIK_HCM || P->method == EIK_FHCM;
+  P->max_len = std::max(g.max_w, g.max_h);
+  // Cells whose tile does not fit shared memory (or taller than the 4 rows
+  // per lane of the register engine) are swept in place in the padded field
+  // by the band-splitting engine (k_cellsweep.cuh big_cell_sweep): FMSM by
+  // the same dataflow kernel, HCM/FHCM by the exact serial heap loop
+  // (heapcell_serial_kernel) -- any decomposition cells.cpp:32-47 accepts.
+  P->cells_big = tile_bytes > kTileMax || (hc && heapcell_smem_bytes(g, P->max_len) > 227 * 1024);
+  if (P->cells_big) g.tile_doubles = 0;
+  P->warps_per_cta = P->cells_big
+                         ? 8
+                         : (int)std::max<size_t>(1, std::min<size_t>(8, kTileBudget / tile_bytes));
 
   int rc;
-  if (P->method == EIK_HCM || P->method == EIK_FHCM) {
-    P->max_len = std::max(g.max_w, g.max_h);
+  if (hc && P->cells_big) {
+    for (int s = 0; s < 4; ++s) {
+      if ((rc = dalloc(&P->dProbe[s], (size_t)P->probe_len[s]))) return rc;
+      P->allocs.push_back(P->dProbe[s]);
+      if (P->deferred) {
+        P->defer_probe[s] = tabs[s];
+      } else {
+        CK(cudaMemcpyAsync(P->dProbe[s], tabs[s], sizeof(double) * P->probe_len[s],
+                           cudaMemcpyHostToDevice, P->stream));
+      }
+    }
+    if ((rc = dalloc(&P->dCVal, J))) return rc;
+    P->allocs.push_back(P->dCVal);
+    if ((rc = dalloc(&P->dInitCells, J))) return rc;
+    P->allocs.push_back(P->dInitCells);
+    if ((rc = dalloc(&P->dInitValues, J))) return rc;
+    P->allocs.push_back(P->dInitValues);
+    if ((rc = dalloc(&P->dCounters, 48))) return rc;
+    P->allocs.push_back(P->dCounters);
+    if ((rc = dalloc(&P->dBInq, J))) return rc;
+    P->allocs.push_back(P->dBInq);
+    if ((rc = dalloc(&P->dBFlags, J))) return rc;
+    P->allocs.push_back(P->dBFlags);
+    if ((rc = dalloc(&P->dBFdone, J))) return rc;
+    P->allocs.push_back(P->dBFdone);
+    if ((rc = dalloc(&P->dBigLock, (size_t)g.max_w * g.max_h))) return rc;
+    P->allocs.push_back(P->dBigLock);
+    if ((rc = dalloc(&P->dBigScratch, 8 * (size_t)P->max_len))) return rc;
+    P->allocs.push_back(P->dBigScratch);
+    {  // row of a cell id by a multiply and shift, checked for every id
+      const uint64_t d = (uint64_t)P->cells_x;
+      uint64_t magic = ((1ull << 40) + d - 1) / d;
+      for (int64_t c = 0; magic && c < J; ++c)
+        if ((((uint64_t)c * magic) >> 40) != (uint64_t)c / d) magic = 0;
+      P->hc_cx_magic = magic;
+    }
+    P->hc_warps_per_cta = 1;
+    P->hc_min_smem = 0;
+    P->hc_max_ctas = 1;
+    return EIK_OK;
+  }
+  if (hc) {
     const size_t smem = heapcell_smem_bytes(g, P->max_len);
-    if (smem > 227 * 1024)
-      return fail(EIK_ERR_NOT_IMPL, "cell too large for the shared-memory tile (max ~110x110 nodes)");
     for (int s = 0; s < 4; ++s) {
       if ((rc = dalloc(&P->dProbe[s], (size_t)P->probe_len[s]))) return rc;
       P->allocs.push_back(P->dProbe[s]);
@@ -279,6 +324,7 @@ int plan_run_fmsm(eik_plan* P, eik_output* out) {
   a.status = P->dStatus;
   a.J = (int)J;
   a.max_cell_sweeps = 1 << 20;
+  a.big = P->cells_big ? 1 : 0;
   int grid = 0;
   CK(launch_fmsm(a, P->warps_per_cta, P->cap(), P->stream, &launches, &grid));
   out->grid_ctas = grid;
@@ -302,6 +348,75 @@ int plan_run_fmsm(eik_plan* P, eik_output* out) {
   out->avs = (double)out->sweeps / (double)J;
   out->device_ms = ms;
   out->host_ms = host_ms;
+  out->kernel_launches = launches;
+  return EIK_OK;
+}
+
+// Cells too large for a shared-memory tile: the exact serial heap loop.
+int plan_run_heapcell_serial(eik_plan* P, eik_output* out, const std::vector<int>& icells,
+                             const std::vector<double>& ivals) {
+  const int64_t J = (int64_t)P->cells_x * P->cells_y;
+  int launches = 0;
+  CK(cudaEventRecord(P->ev0, P->stream));
+  CK(cudaMemcpyAsync(P->dInitCells, icells.data(), sizeof(int) * icells.size(),
+                     cudaMemcpyHostToDevice, P->stream));
+  CK(cudaMemcpyAsync(P->dInitValues, ivals.data(), sizeof(double) * ivals.size(),
+                     cudaMemcpyHostToDevice, P->stream));
+  CK(cudaMemsetAsync(P->dCounters, 0, sizeof(unsigned long long) * 48, P->stream));
+  CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
+                    P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
+  HcArgs a{};
+  a.g = P->cg;
+  a.C = P->dC;
+  a.u = P->dU;
+  for (int s = 0; s < 4; ++s) a.probe[s] = P->dProbe[s];
+  a.h = P->g.h;
+  a.hc_x = (double)(P->g.m / P->cells_x) * P->g.h;  // cells.cpp:44-45
+  a.hc_y = (double)(P->g.n / P->cells_y) * P->g.h;
+  a.cval = P->dCVal;
+  a.init_cells = P->dInitCells;
+  a.init_values = P->dInitValues;
+  a.n_init = (int)icells.size();
+  a.counters = P->dCounters;
+  a.status = P->dStatus;
+  a.J = (int)J;
+  a.fast = P->method == EIK_FHCM ? 1 : 0;
+  a.budget = 100LL * J + 16;
+  a.max_len = P->max_len;
+  a.cx_magic = P->hc_cx_magic;
+  a.b_inq = P->dBInq;
+  a.b_flags = P->dBFlags;
+  a.b_fdone = P->dBFdone;
+  a.big_lock = P->dBigLock;
+  a.big_scratch = P->dBigScratch;
+  CK(launch_heapcell_serial(a, P->stream, &launches));
+  out->grid_ctas = 1;
+  if (P->on_launched) {
+    auto f = std::move(P->on_launched);
+    P->on_launched = nullptr;
+    f();
+  }
+  CK(cudaEventRecord(P->ev1, P->stream));
+  int st[8];
+  unsigned long long cnt[5];
+  CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
+  CK(cudaMemcpyAsync(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost, P->stream));
+  CK(cudaStreamSynchronize(P->stream));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  if (st[0] == 3) return fail(EIK_ERR_BUDGET, "heap-cell removal budget exceeded");
+  out->heap_removals = (int64_t)cnt[0];
+  out->sweeps = (int64_t)cnt[1];
+  out->node_updates = (int64_t)cnt[2];
+  out->mon_checks = (int64_t)cnt[3];
+  out->mon_single = (int64_t)cnt[4];
+  out->cell_removals = out->heap_removals;
+  out->cell_sweeps = out->sweeps;
+  out->avhr = (double)out->heap_removals / (double)J;
+  out->avs = (double)out->sweeps / (double)J;
+  out->mon_pct = out->mon_checks == 0 ? 0.0 : 100.0 * out->mon_single / (double)out->mon_checks;
+  out->device_ms = ms;
   out->kernel_launches = launches;
   return EIK_OK;
 }
@@ -434,6 +549,7 @@ int plan_run_heapcell(eik_plan* P, eik_output* out) {
     ivals[k] = init[k].second;
   }
   int launches = 0;
+  if (P->cells_big) return plan_run_heapcell_serial(P, out, icells, ivals);
   if (P->method == EIK_HCM && P->hcm_band) return plan_run_hcm_band(P, out, icells, ivals);
 retry:  // after a committer heap overflow, with the heap in global memory
   CK(cudaEventRecord(P->ev0, P->stream));

@@ -103,7 +103,19 @@ __global__ void fmsm_dataflow_kernel(FmsmArgs a) {
       if (nb >= 0 && a.rank[nb] < p) ok = wait_ge_s32(a.done + nb, 1, a.status);
     }
     if (__any_sync(kFull, !ok)) return;
-    const int exits = stage_in(a.g, a.C, a.u, ib, jb, T, lane);
+    int exits = 0;
+    if (a.big) {
+      // a cell too large for the tile: swept in place, its cross halo being
+      // the neighbours' nodes (adjacent cells never run at the same time)
+      T.pu = (int)a.g.P;
+      T.U = a.u + (jb - 1) * a.g.P + a.g.pad + ib - 1;
+      T.Ct = const_cast<double*>(a.C) + (jb - 1) * a.g.P + a.g.pad + ib - 1;
+      for (int k = lane; k < T.w * T.h; k += 32)
+        exits += __ldg(a.C + (jb + k / T.w) * a.g.P + a.g.pad + ib + k % T.w) < 0.0;
+      for (int o = 16; o > 0; o >>= 1) exits += __shfl_xor_sync(kFull, exits, o);
+    } else {
+      exits = stage_in(a.g, a.C, a.u, ib, jb, T, lane);
+    }
     const int flags = a.flags[cell];
     int nsw = 0;
     long long unused = 0;
@@ -111,7 +123,7 @@ __global__ void fmsm_dataflow_kernel(FmsmArgs a) {
       // Q-cell: FSM to convergence with the halo frozen (fmsm.cpp:200-210)
       bool changed = true;
       while (changed) {
-        changed = cell_sweep<0>(T, nsw & 3, lane, unused);
+        changed = big_cell_sweep<0>(T, nsw & 3, lane, unused);
         ++nsw;
         if (nsw > a.max_cell_sweeps) {
           if (lane == 0) atomicExch(a.status, 3);
@@ -124,11 +136,11 @@ __global__ void fmsm_dataflow_kernel(FmsmArgs a) {
 #pragma unroll
       for (int k = 0; k < 4; ++k)
         if (flags & (1 << order[k])) {
-          cell_sweep<1>(T, order[k], lane, unused);
+          big_cell_sweep<1>(T, order[k], lane, unused);
           ++nsw;
         }
     }
-    stage_out(a.g, a.u, ib, jb, T, lane);
+    if (!a.big) stage_out(a.g, a.u, ib, jb, T, lane);
     __threadfence();
     __syncwarp();
     if (lane == 0) st_release_s32(a.done + cell, 1);

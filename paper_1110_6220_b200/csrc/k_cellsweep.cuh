@@ -26,6 +26,10 @@ struct CellTile {
   uint8_t* lock;    // h x w lock bytes (1 = unlocked), locked sweeps only
   int pu, w, h;
   int ox;           // column of node x = 0 in a tile row (the west halo is ox-1)
+  // A band of rows of a taller cell (big_cell_sweep): the halo row below
+  // (y = -1) / above (y = h) is a row of the same cell, so the locking sweep
+  // unlocks it like any in-cell neighbour (heap_cell.cpp:113-122).
+  bool in_lo = false, in_hi = false;
 };
 
 // MODE 0: node_update over all non-exit nodes (FSM inside a cell,
@@ -44,6 +48,8 @@ __device__ bool cell_sweep_ns(const CellTile& T, int dir, int lane, long long& u
   const int dyl = jasc ? T.w : -T.w;      // next row in sweep order (lock pitch)
   const int w = T.w, h = T.h;
   const int x0 = iasc ? 0 : w - 1;        // column of sweep step a = 0
+  const bool up_in = jasc ? T.in_lo : T.in_hi;  // upwind / downwind halo row in the cell
+  const bool dn_in = jasc ? T.in_hi : T.in_lo;
 
   int vbase[NS];             // value offset of (a = 0) for this lane's row
   int lbase[NS];             // lock offset of (a = 0)
@@ -161,8 +167,10 @@ __device__ bool cell_sweep_ns(const CellTile& T, int dir, int lane, long long& u
               uint8_t* lp = T.lock + lbase[r] + dx * a;
               // already-processed W and S neighbours: unlocked for the next sweep
               if (a > 0 && c_prev[r] >= 0.0 && wv > cand) lp[-dx] = 1;
-              if (b > 0 && c_cs[r] >= 0.0 && sv > cand) lp[-dyl] = 1;
+              if ((b > 0 || up_in) && c_cs[r] >= 0.0 && sv > cand) lp[-dyl] = 1;
               un_n = (b + 1 < h) && c_cn[r] >= 0.0 && c_n[r] > cand;
+              // the next band's first row: unlocked in memory for this sweep
+              if (b + 1 == h && dn_in && c_cn[r] >= 0.0 && c_n[r] > cand) lp[dyl] = 1;
             }
           }
           // relock on processing (heap_cell.cpp:110-111)
@@ -203,6 +211,8 @@ __device__ __forceinline__ bool cell_sweep_lock(const CellTile& T, int dir, int 
   const int dyp = jasc ? pu : -pu;
   const int dyl = jasc ? w : -w;
   const int x0 = iasc ? 0 : w - 1;
+  const bool up_in = jasc ? T.in_lo : T.in_hi;  // upwind / downwind halo row in the cell
+  const bool dn_in = jasc ? T.in_hi : T.in_lo;
   double* __restrict__ U = T.U;
   const double* __restrict__ C = T.Ct;
   uint8_t* __restrict__ L = T.lock;
@@ -320,7 +330,9 @@ __device__ __forceinline__ bool cell_sweep_lock(const CellTile& T, int dir, int 
         U[o] = cand[r];
         // already-processed W and S neighbours: unlocked for the next sweep
         if (a > 0 && cw[r] >= 0.0 && wv[r] > cand[r]) L[lo - dx] = 1;
-        if (b > 0 && cs[r] >= 0.0 && sv[r] > cand[r]) L[lo - dyl] = 1;
+        if ((b > 0 || up_in) && cs[r] >= 0.0 && sv[r] > cand[r]) L[lo - dyl] = 1;
+        // the next band's first row: unlocked in memory for this sweep
+        if (b + 1 == h && dn_in && cn[r] >= 0.0 && n[r] > cand[r]) L[lo + dyl] = 1;
       }
       const bool un_n = dec && (b + 1 < h) && cn[r] >= 0.0 && n[r] > cand[r];
       unW[r] = dec && (a + 1 < w) && ce[r] >= 0.0 && e[r] > cand[r];
@@ -358,6 +370,36 @@ __device__ bool cell_sweep(const CellTile& T, int dir, int lane, long long& upda
   if (T.h <= 64) return cell_sweep_ns<MODE, 2>(T, dir, lane, updates);
   if (T.h <= 96) return cell_sweep_ns<MODE, 3>(T, dir, lane, updates);
   return cell_sweep_ns<MODE, 4>(T, dir, lane, updates);
+}
+
+// A cell of any height: bands of at most 128 rows swept one after another in
+// the sweep's row order.  A band's upwind halo row is the previous band's
+// last row (new values) and its downwind halo row the next band's first row
+// (old values), which is exactly the reference's row-loop order, so values
+// and counters are the single sweep's.  Lock bytes of the whole cell are
+// contiguous (row pitch w), so a band unlocks its neighbours' rows in place.
+template <int MODE>
+__device__ bool big_cell_sweep(const CellTile& T, int dir, int lane, long long& updates,
+                               bool skip = false) {
+  if (T.h <= 128) return cell_sweep<MODE>(T, dir, lane, updates, skip);
+  const bool jasc = (dir == kSW || dir == kSE);
+  bool changed = false;
+  const int nb = (T.h + 127) / 128;
+  for (int k = 0; k < nb; ++k) {
+    const int band = jasc ? k : nb - 1 - k;
+    const int y0 = band * 128;
+    const int hb = min(128, T.h - y0);
+    CellTile S = T;
+    S.U = T.U + (size_t)y0 * T.pu;
+    S.Ct = T.Ct + (size_t)y0 * T.pu;
+    if (T.lock) S.lock = T.lock + (size_t)y0 * T.w;
+    S.h = hb;
+    S.in_lo = y0 > 0 || T.in_lo;
+    S.in_hi = y0 + hb < T.h || T.in_hi;
+    changed = cell_sweep<MODE>(S, dir, lane, updates, skip) || changed;
+    __syncwarp();
+  }
+  return changed;
 }
 
 }  // namespace eikb200

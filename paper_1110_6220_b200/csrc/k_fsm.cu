@@ -529,23 +529,23 @@ fsm_wavefront_kernel(FsmArgs a) {
   }
 }
 
-// Padded layout: row r (0..n, row n is a dummy) holds element i at
-// r*P + pad + i; padding columns and the dummy row carry u = +inf, C = -1.
+// Padded layout: row r (-1..n; rows -1 and n are dummies) holds element i at
+// r*P + pad + i; padding columns and the dummy rows carry u = +inf, C = -1.
 __global__ void prepare_padded_kernel(const double* __restrict__ F, double* __restrict__ C,
                                       double* __restrict__ u, int64_t m, int64_t n, int64_t P,
                                       int64_t pad, double h, int* __restrict__ status) {
-  const int64_t total = (n + 1) * P;
+  const int64_t total = (n + 2) * P;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = idx / P, i = idx - r * P - pad;
+    const int64_t r = idx / P - 1, i = idx - (r + 1) * P - pad;
     double c = -1.0;
-    if (r < n && i >= 0 && i < m) {
+    if (r >= 0 && r < n && i >= 0 && i < m) {
       const double f = F[r * m + i];
       if (!(f > 0.0) || !(f < kInf)) atomicExch(&status[0], 1);
       c = h / f;  // same IEEE division as local_update.hpp:33
     }
-    C[idx] = c;
-    u[idx] = kInf;
+    C[idx - P] = c;
+    u[idx - P] = kInf;
   }
 }
 
@@ -583,7 +583,7 @@ cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int
                            const double* cost, int64_t n_exit, int* status, cudaStream_t s,
                            int* launches) {
   const int threads = 256;
-  int64_t blocks = ((n + 1) * P + threads - 1) / threads;
+  int64_t blocks = ((n + 2) * P + threads - 1) / threads;
   if (blocks > 148 * 16) blocks = 148 * 16;
   prepare_padded_kernel<<<(unsigned)blocks, threads, 0, s>>>(F, C, u, m, n, P, pad, h, status);
   int64_t eb = (n_exit + threads - 1) / threads;

@@ -1639,6 +1639,149 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
   }
 }
 
+// ---- cells too large for a shared-memory tile ------------------------------
+// heap_cell_solve (heap_cell.cpp:243-324) exactly as the reference runs it:
+// one warp pops the minimum (value, id) cell (a warp argmin over the J cells;
+// big cells mean small J), processes it in place in u -- the tile aliases the
+// padded global field, so the cross halo is the neighbours' nodes -- with the
+// band-splitting engine (big_cell_sweep), scans its borders and updates the
+// neighbours.  The order is the reference's, so values and every counter are.
+__global__ void __launch_bounds__(32) heapcell_serial_kernel(HcArgs a) {
+  __shared__ SpecRec rec;
+  const int lane = threadIdx.x;
+  const CellGeom& g = a.g;
+  const int J = a.J;
+  for (int c = lane; c < J; c += 32) {
+    a.cval[c] = kInf;
+    a.b_inq[c] = 0;
+    a.b_flags[c] = 0;
+    a.b_fdone[c] = 0;
+  }
+  __syncwarp();
+  if (lane == 0)
+    for (int k = 0; k < a.n_init; ++k) {  // heap_cell.cpp:255-268
+      const int c = a.init_cells[k];
+      a.cval[c] = a.init_values[k];
+      a.b_inq[c] = 1;
+      if (a.fast) a.b_flags[c] = 0xFu;
+    }
+  __syncwarp();
+  double* before = a.big_scratch;
+  double* pstrip = before + 4 * a.max_len;
+  long long removals = 0, sweeps = 0, updates = 0, mon_checks = 0, mon_single = 0;
+  for (;;) {
+    // pop: minimum (value, id) over the queued cells (ties to the smaller id)
+    double kb = kInf;
+    int ib_ = 0x7fffffff;
+    for (int c = lane; c < J; c += 32)
+      if (a.b_inq[c] && key_less(a.cval[c], c, kb, ib_)) {
+        kb = a.cval[c];
+        ib_ = c;
+      }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ok = __shfl_xor_sync(kFull, kb, o);
+      const int oi = __shfl_xor_sync(kFull, ib_, o);
+      if (key_less(ok, oi, kb, ib_)) {
+        kb = ok;
+        ib_ = oi;
+      }
+    }
+    if (ib_ == 0x7fffffff) break;
+    const int cell = ib_;
+    if (++removals > a.budget) {
+      if (lane == 0) atomicExch(a.status, 3);
+      return;
+    }
+    int64_t ib, ie, jb, je;
+    hc_cell_rect(g, a.cx_magic, cell, ib, ie, jb, je);
+    HTile T;
+    T.pu = (int)g.P;
+    T.w = (int)(ie - ib);
+    T.h = (int)(je - jb);
+    T.U = a.u + (jb - 1) * g.P + g.pad + ib - 2;  // node (x, y) at (y+1)*P + x+2
+    T.Ct = const_cast<double*>(a.C) + (jb - 1) * g.P + g.pad + ib - 2;
+    T.lock = a.big_lock;
+    int cx, cy;
+    cell_xy(cell, g.cells_x, a.cx_magic, cx, cy);
+    const bool has_nb[4] = {cx > 0, cx + 1 < g.cells_x, cy > 0, cy + 1 < g.cells_y};
+    const int nbs[4] = {cell - 1, cell + 1, cell - g.cells_x, cell + g.cells_x};
+    for (int t = lane; t < a.max_len; t += 32) {
+      if (t < T.h) {
+        before[0 * a.max_len + t] = T.u(0, t);
+        before[1 * a.max_len + t] = T.u(T.w - 1, t);
+        pstrip[0 * a.max_len + t] = has_nb[0] ? __ldg(a.probe[0] + (int64_t)cx * g.n + jb + t) : 1.0;
+        pstrip[1 * a.max_len + t] = has_nb[1] ? __ldg(a.probe[1] + (int64_t)cx * g.n + jb + t) : 1.0;
+      }
+      if (t < T.w) {
+        before[2 * a.max_len + t] = T.u(t, 0);
+        before[3 * a.max_len + t] = T.u(t, T.h - 1);
+        pstrip[2 * a.max_len + t] = has_nb[2] ? __ldg(a.probe[2] + (int64_t)cy * g.m + ib + t) : 1.0;
+        pstrip[3 * a.max_len + t] = has_nb[3] ? __ldg(a.probe[3] + (int64_t)cy * g.m + ib + t) : 1.0;
+      }
+    }
+    const unsigned my_flags = a.b_flags[cell];
+    const bool first_removal = !a.b_fdone[cell];
+    __syncwarp();
+    if (lane == 0) {
+      a.b_inq[cell] = 0;
+      a.b_flags[cell] = 0;
+      a.b_fdone[cell] = 1;
+    }
+    reset_locks(T, ib > 0, ie < g.m, jb > 0, je < g.n, lane);
+    const CellTile ct{T.U, T.Ct, T.lock, T.pu, T.w, T.h, 2};
+    long long nsw = 0, upd = 0;
+    {  // process_flagged_once / process_to_convergence (heap_cell.cpp:130-160)
+      int perm[4], nflag = 0;
+      for (int k = 0; k < 4; ++k)
+        if (my_flags & (1u << kFlagOrder[k])) perm[nflag++] = kFlagOrder[k];
+      int at = nflag;
+      for (int k = 0; k < 4; ++k)
+        if (!(my_flags & (1u << kRotation[k]))) perm[at++] = kRotation[k];
+      bool changed = true;
+      for (;;) {
+        if (a.fast ? nsw >= nflag : !changed) break;
+        const int dir = nsw < 4 ? perm[nsw] : kRotation[nsw % 4];
+        changed = big_cell_sweep<2>(ct, dir, lane, upd);
+        ++nsw;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) upd += __shfl_xor_sync(kFull, upd, o);
+    sweeps += nsw;
+    updates += upd;
+    __syncwarp();
+    scan_all(a, T, before, pstrip, first_removal,
+             (has_nb[0] ? 1u : 0u) | (has_nb[1] ? 2u : 0u) | (has_nb[2] ? 4u : 0u) |
+                 (has_nb[3] ? 8u : 0u),
+             &rec, lane);
+    __syncwarp();
+    if (lane == 0) {
+      for (int d = 0; d < 4; ++d) {  // W, E, S, N in the reference's order
+        if (!has_nb[d]) continue;
+        const int nb = nbs[d];
+        const unsigned sd = rec.side[d];
+        if (rec.cand[d] < a.cval[nb]) a.cval[nb] = rec.cand[d];
+        if (sd & 1u) {
+          a.b_flags[nb] |= (sd >> 8) & 0xFFu;
+          if (sd & (1u << 16)) {
+            ++mon_checks;
+            if (sd & (1u << 24)) ++mon_single;
+          }
+          a.b_inq[nb] = 1;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    a.counters[0] = (unsigned long long)removals;
+    a.counters[1] = (unsigned long long)sweeps;
+    a.counters[2] = (unsigned long long)updates;
+    a.counters[3] = (unsigned long long)mon_checks;
+    a.counters[4] = (unsigned long long)mon_single;
+  }
+}
+
 }  // namespace
 
 size_t heapcell_smem_bytes(const CellGeom& g, int max_len) {
@@ -1745,6 +1888,12 @@ cudaError_t launch_hcm_band(const HcArgs& args, int warps_per_cta, int max_ctas,
   e = cudaLaunchCooperativeKernel(kern, dim3(ctas), dim3(32 * warps_per_cta), params, smem, s);
   *launches += 1;
   return e;
+}
+
+cudaError_t launch_heapcell_serial(const HcArgs& a, cudaStream_t s, int* launches) {
+  heapcell_serial_kernel<<<1, 32, 0, s>>>(a);
+  *launches += 1;
+  return cudaGetLastError();
 }
 
 }  // namespace eikb200
