@@ -14,6 +14,7 @@ namespace eikb200 {
 
 namespace {
 
+constexpr int kStatusWatchdogHost = 4;  // k_common.cuh kStatusWatchdog
 constexpr size_t kTileBudget = 96 * 1024;  // smem per CTA for warp tiles
 constexpr size_t kTileMax = 200 * 1024;
 
@@ -489,6 +490,8 @@ int plan_run_hcm_band(eik_plan* P, eik_output* out, const std::vector<int>& icel
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
   if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
   if (st[0] == 3) return fail(EIK_ERR_BUDGET, "heap-cell removal budget exceeded");
+  if (st[0] == kStatusWatchdogHost)
+    return fail(EIK_ERR_CUDA, "hcm band scheduler made no progress (scheduling bug)");
   if (kn.hc_profile && grid > 0)
     std::fprintf(stderr, "hcm band: %d rounds, per CTA per round (cycles): sync %.0f select %.0f "
                  "work %.0f kmin %.0f\n", ctl[4], (double)cnt[8] / grid / std::max(1, ctl[4]),

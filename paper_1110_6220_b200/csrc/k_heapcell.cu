@@ -1541,8 +1541,14 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
     a.b_ctl[1] = 0;
   }
   grid.sync();
-  const double cmin_d = __longlong_as_double((long long)a.b_kmin[1]);
-  const double delta = a.band_scale * 0.5 * (a.h + fmin(a.hc_x, a.hc_y)) * (cmin_d / a.h);
+  // no node with C > 0 (every node an exit): width 0 -- the minimum cell is
+  // still selected every round, so every round makes progress
+  const unsigned long long cmin_bits = *(volatile unsigned long long*)(a.b_kmin + 1);
+  double delta = 0.0;
+  if (cmin_bits != ~0ull)
+    delta = a.band_scale * 0.5 * (a.h + fmin(a.hc_x, a.hc_y)) *
+            (__longlong_as_double((long long)cmin_bits) / a.h);
+  if (!(delta >= 0.0 && delta < kInf)) delta = 0.0;
 
   long long removals = 0, sweeps = 0, updates = 0;
   long long cyc_sync = 0, cyc_sel = 0, cyc_work = 0, cyc_kmin = 0;  // EIK_HC_PROFILE
@@ -1608,6 +1614,8 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
     if (tid == 0) {
       removals += nwork;
       if (removals > a.budget) atomicExch(a.status, 3);  // read by all after the sync
+      // every round selects at least the minimum cell; an empty one is a bug
+      if (nwork == 0 || round > a.budget) atomicExch(a.status, kStatusWatchdog);
     }
     for (;;) {
       int i = 0;
@@ -1621,7 +1629,8 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
     lap(cyc_work);
     grid.sync();
     lap(cyc_sync);
-    if (*(volatile int*)a.status == 3) break;  // set before the sync: all threads agree
+    const int stv = *(volatile int*)a.status;  // set before the sync: all threads agree
+    if (stv == 3 || stv == kStatusWatchdog) break;
   }
   if (lane == 0) {
     atomicAdd(a.counters + 1, (unsigned long long)sweeps);
