@@ -19,8 +19,8 @@ namespace {
 
 constexpr double kInf = std::numeric_limits<double>::infinity();
 
-double quadrant(double ua, double ub, double f, double h) {  // local_update.hpp:30-43
-  const double c = h / f;
+// local_update.hpp:30-43 with c = h / f precomputed (the same IEEE division)
+inline double quadrant_c(double ua, double ub, double c) {
   if (std::isfinite(ua) && std::isfinite(ub)) {
     const double diff = ua - ub;
     if (std::abs(diff) <= c) return 0.5 * (ua + ub) + 0.5 * std::sqrt(2.0 * c * c - diff * diff);
@@ -28,71 +28,87 @@ double quadrant(double ua, double ub, double f, double h) {  // local_update.hpp
   return c + std::min(ua, ub);
 }
 
-// Binary min-heap keyed by (value, id) with decrease-key, ties to the
-// smaller id (indexed_min_heap.hpp:66-69).
+// 4-ary min-heap of (value, id) entries with lazy deletion: a decrease-key
+// pushes a new entry and the superseded one is skipped when it surfaces.
+// The live entries are exactly an indexed heap's -- a node's current (value,
+// id) -- and a stale entry of a node carries a larger value than its live
+// one, so pops come out in the reference's order: minimum value, ties to the
+// smaller id (indexed_min_heap.hpp:36-48,66-69).  No position index: every
+// sift touches only the contiguous heap array.
 class Heap {
  public:
-  explicit Heap(int64_t cap) : key_(cap), pos_(cap, -1) { h_.reserve(cap); }
+  Heap() { h_.reserve(1024); }
   bool empty() const { return h_.empty(); }
-  bool contains(int64_t id) const { return pos_[id] >= 0; }
-  void insert(int64_t id, double k) {
-    key_[id] = k;
-    pos_[id] = (int64_t)h_.size();
-    h_.push_back(id);
-    up(pos_[id]);
-  }
-  void decrease(int64_t id, double k) {
-    key_[id] = k;
-    up(pos_[id]);
-  }
-  int64_t pop() {
-    int64_t top = h_[0], last = h_.back();
-    h_.pop_back();
-    pos_[top] = -1;
-    if (!h_.empty()) {
-      h_[0] = last;
-      pos_[last] = 0;
-      down(0);
+  void push(int32_t id, double k) {
+    h_.push_back({k, id});
+    int32_t p = (int32_t)h_.size() - 1;
+    const Ent e = h_[p];
+    while (p > 0) {
+      const int32_t par = (p - 1) >> 2;
+      if (!less(e, h_[par])) break;
+      h_[p] = h_[par];
+      p = par;
     }
-    return top;
+    h_[p] = e;
+  }
+  // the minimum entry (value, id); removes it
+  void pop(double& k, int32_t& id) {
+    k = h_[0].k;
+    id = h_[0].id;
+    const Ent last = h_.back();
+    h_.pop_back();
+    const int32_t n = (int32_t)h_.size();
+    if (n == 0) return;
+    int32_t p = 0;
+    for (;;) {
+      const int32_t c0 = 4 * p + 1;
+      if (c0 >= n) break;
+      int32_t c = c0;
+      const int32_t ce = std::min(c0 + 4, n);
+      for (int32_t q = c0 + 1; q < ce; ++q)
+        if (less(h_[q], h_[c])) c = q;
+      if (!less(h_[c], last)) break;
+      h_[p] = h_[c];
+      p = c;
+    }
+    h_[p] = last;
   }
 
  private:
-  bool less(int64_t a, int64_t b) const {
-    if (key_[a] != key_[b]) return key_[a] < key_[b];
-    return a < b;
-  }
-  void up(int64_t p) {
-    int64_t id = h_[p];
-    while (p > 0) {
-      int64_t par = (p - 1) / 2;
-      if (!less(id, h_[par])) break;
-      h_[p] = h_[par];
-      pos_[h_[p]] = p;
-      p = par;
-    }
-    h_[p] = id;
-    pos_[id] = p;
-  }
-  void down(int64_t p) {
-    int64_t id = h_[p];
-    const int64_t n = (int64_t)h_.size();
-    for (;;) {
-      int64_t c = 2 * p + 1;
-      if (c >= n) break;
-      if (c + 1 < n && less(h_[c + 1], h_[c])) ++c;
-      if (!less(h_[c], id)) break;
-      h_[p] = h_[c];
-      pos_[h_[p]] = p;
-      p = c;
-    }
-    h_[p] = id;
-    pos_[id] = p;
-  }
-  std::vector<double> key_;
-  std::vector<int64_t> pos_;
-  std::vector<int64_t> h_;
+  struct Ent {
+    double k;
+    int32_t id;
+  };
+  static bool less(const Ent& a, const Ent& b) { return a.k < b.k || (a.k == b.k && a.id < b.id); }
+  std::vector<Ent> h_;
 };
+
+// Stable LSD radix sort of 64-bit keys, 11-bit digits (cache-sized count
+// tables), skipping digits that are equal in every key.
+void radix_sort_u64(std::vector<uint64_t>& a) {
+  constexpr int kBits = 11;
+  constexpr uint64_t kMask = (1u << kBits) - 1;
+  std::vector<uint64_t> tmp(a.size());
+  uint64_t all_or = 0, all_and = ~0ull;
+  for (uint64_t v : a) {
+    all_or |= v;
+    all_and &= v;
+  }
+  std::vector<uint32_t> cnt(1u << kBits);
+  for (int shift = 0; shift < 64; shift += kBits) {
+    if ((((all_or ^ all_and) >> shift) & kMask) == 0) continue;  // constant digit
+    std::fill(cnt.begin(), cnt.end(), 0u);
+    for (uint64_t v : a) ++cnt[(v >> shift) & kMask];
+    uint32_t sum = 0;
+    for (auto& c : cnt) {
+      const uint32_t t = c;
+      c = sum;
+      sum += t;
+    }
+    for (uint64_t v : a) tmp[cnt[(v >> shift) & kMask]++] = v;
+    a.swap(tmp);
+  }
+}
 
 }  // namespace
 
@@ -176,15 +192,17 @@ int fmsm_part1(const eik_problem* p, const eik_cells* cells, FmsmOrder* out) {
   // spacing hc_x, speed = F at the actual cell centres
   out->coarse_updates = 0;
   out->coarse_pops = 0;
-  Heap H(J);
+  Heap H;
   const int di[4] = {1, -1, 0, 0}, dj[4] = {0, 0, 1, -1};
+  std::vector<double> cc(J);  // h_c / F per cell, as quadrant_update computes it
+  for (int64_t c = 0; c < J; ++c) cc[c] = hc_x / Fc[c];
   auto update = [&](int64_t a, int64_t b) {
     ++out->coarse_updates;
     const double E = a + 1 < cx ? v[b * cx + a + 1] : kInf;
     const double W = a - 1 >= 0 ? v[b * cx + a - 1] : kInf;
     const double N = b + 1 < cy ? v[(b + 1) * cx + a] : kInf;
     const double S = b - 1 >= 0 ? v[(b - 1) * cx + a] : kInf;
-    return quadrant(std::min(E, W), std::min(N, S), Fc[b * cx + a], hc_x);
+    return quadrant_c(std::min(E, W), std::min(N, S), cc[b * cx + a]);
   };
   for (int64_t c = 0; c < J; ++c) {
     if (!isx[c]) continue;
@@ -197,11 +215,15 @@ int fmsm_part1(const eik_problem* p, const eik_cells* cells, FmsmOrder* out) {
       label[nc] = 1;
       const double cand = update(na, nb);
       if (cand < v[nc]) v[nc] = cand;
-      H.insert(nc, v[nc]);
+      H.push((int32_t)nc, v[nc]);
     }
   }
   while (!H.empty()) {
-    const int64_t c = H.pop();
+    double key;
+    int32_t top;
+    H.pop(key, top);
+    const int64_t c = top;
+    if (label[c] == 2 || key != v[c]) continue;  // superseded entry
     ++out->coarse_pops;
     label[c] = 2;
     const int64_t a = c % cx, b = c / cx;
@@ -214,10 +236,10 @@ int fmsm_part1(const eik_problem* p, const eik_cells* cells, FmsmOrder* out) {
       if (label[nc] == 0) {
         label[nc] = 1;
         if (cand < v[nc]) v[nc] = cand;
-        H.insert(nc, v[nc]);
+        H.push((int32_t)nc, v[nc]);
       } else if (cand < v[nc]) {
         v[nc] = cand;
-        H.decrease(nc, cand);
+        H.push((int32_t)nc, cand);
       }
     }
   }
@@ -227,16 +249,17 @@ int fmsm_part1(const eik_problem* p, const eik_cells* cells, FmsmOrder* out) {
   for (int64_t c = 0; c < J; ++c)
     if (std::isfinite(v[c])) vmax = std::max(vmax, v[c]);
   const double quantum = 1e-9 * vmax;
-  std::vector<long long> key(J);
-  for (int64_t c = 0; c < J; ++c)
-    key[c] = std::isfinite(v[c]) ? (long long)std::floor(v[c] / quantum)
-                                 : std::numeric_limits<long long>::max();
+  // (key, id) packed into one word: keys are floor(v / (1e-9 vmax)) <= 1e9 <
+  // 2^31 (an unreached cell sorts last), ids < 2^31 -- a radix sort of the
+  // words is the reference's stable sort by key then id
+  std::vector<uint64_t> kw(J);
+  for (int64_t c = 0; c < J; ++c) {
+    const uint64_t key = std::isfinite(v[c]) ? (uint64_t)std::floor(v[c] / quantum) : 0xFFFFFFFFull;
+    kw[c] = (key << 32) | (uint64_t)c;
+  }
+  radix_sort_u64(kw);
   out->order.resize(J);
-  for (int64_t c = 0; c < J; ++c) out->order[c] = (int32_t)c;
-  std::sort(out->order.begin(), out->order.end(), [&](int32_t a, int32_t b) {
-    if (key[a] != key[b]) return key[a] < key[b];
-    return a < b;
-  });
+  for (int64_t r = 0; r < J; ++r) out->order[r] = (int32_t)(kw[r] & 0xFFFFFFFFull);
   out->rank.resize(J);
   for (int64_t r = 0; r < J; ++r) out->rank[out->order[r]] = (int32_t)r;
   return 0;
