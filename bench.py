@@ -498,6 +498,26 @@ def main():
         all_plans = []
         per_config = measure_configs(hbm, peak_kind)
 
+    # N > 1: config 5 (32769^2) sharded as row strips over the ranks
+    # (distributed.fsm_solve_strips: NCCL edge-row exchange and change-flag
+    # all-reduce, rounds stream-ordered); each rank samples and holds only its
+    # strip, the field stays sharded; device time = max over ranks
+    c5_sharded = None
+    if world > 1 and not args.no_configs:
+        from paper_1110_6220_b200.distributed import fsm_solve_strips, strip_bounds
+        p5 = configs.config5().problem
+        r5 = fsm_solve_strips(p5, gather="none")
+        M5 = p5.grid.size()
+        a5, b5 = strip_bounds(p5.grid.n, world, rank)
+        c5_sharded = {"workload": "c5_sinsum_32769_fsm_row_strips", "ranks": world,
+                      "rounds": r5.sweeps, "device_ms": round(r5.device_ms, 3),
+                      "points_per_s": M5 / (r5.device_ms / 1e3),
+                      "rows_per_rank": b5 - a5,
+                      "bytes_per_rank_u_C_F": 24 * (b5 - a5 + 2) * p5.grid.m,
+                      "note": "strip-Jacobi (SURVEY 8(e) option A): same fixed point, more "
+                              "rounds than fsm_solve's 28 sweeps"}
+        del p5
+
     cpu = None if args.no_cpu_baseline or rank != 0 else cpu_baseline_single_core()
     if rank == 0:
         out = {
@@ -516,7 +536,8 @@ def main():
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "single_step_ms": single_step_ms,
             "roofline": roofline, "roofline_fsm_c2": fsm_roof(methods, M, hbm, peak_kind),
-            "configs": per_config, "cpu_baseline": cpu, "gpu_launches": launches,
+            "configs": per_config, "c5_sharded": c5_sharded, "cpu_baseline": cpu,
+            "gpu_launches": launches,
             "clocks": clk.summary(), "methods": methods,
         }
         print(json.dumps(out))

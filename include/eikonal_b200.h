@@ -115,6 +115,17 @@ typedef struct eik_output {
 int eik_solve(const eik_problem* p, const eik_cells* cells, int32_t method,
               eik_output* out);
 
+/* Several GPUs of this process (SURVEY.md 8(b) "n_gpus plus device list"):
+ * fsm_solve (EIK_FSM) or the FMM row (EIK_FMM) with the grid's rows split
+ * into n_devices strips, one per device, strip-Jacobi rounds with the strips'
+ * edge rows exchanged by peer copies over NVLink after every sweep (no
+ * communicator: one process drives every device).  The field is the discrete
+ * fixed point fsm_solve converges to (<= 1e-10; bit-identical with
+ * n_devices = 1, which is eik_solve); `sweeps` (= `rounds`) counts the
+ * rounds.  Each device holds only its strip.  Host speed and u buffers. */
+int eik_solve_multi(const eik_problem* p, int32_t method, const int32_t* devices,
+                    int32_t n_devices, eik_output* out);
+
 /* Resident plan: uploads the problem once and keeps device work buffers, so
  * repeated solves (benchmarks) time the device path alone.  The plan copies
  * every input; the caller's arrays may be freed after eik_plan_create. */
@@ -209,6 +220,15 @@ int eik_plan_sweep(eik_plan* plan, int64_t first_sweep, int32_t count, int32_t* 
 int eik_plan_get_rows(eik_plan* plan, int64_t row0, int64_t nrows, double* dst, int32_t on_device);
 int eik_plan_set_rows(eik_plan* plan, int64_t row0, int64_t nrows, const double* src,
                       int32_t on_device);
+/* Stream-ordered variants for a rank that drives its rounds without host
+ * synchronisation (distributed.py): the sweeps and row copies are enqueued on
+ * `stream` (a cudaStream_t of the calling framework; NULL = the plan's own),
+ * the per-sweep change flags land in device memory (changed_dev[count]).
+ * eik_plan_get_rows reports a watchdog failure of an earlier async sweep. */
+int eik_plan_sweep_async(eik_plan* plan, int64_t first_sweep, int32_t count, int32_t* changed_dev,
+                         void* stream);
+int eik_plan_rows_async(eik_plan* plan, int64_t row0, int64_t nrows, double* dev_buf,
+                        int32_t to_plan, void* stream);
 
 /* Thread-local description / status code of the last failure on this
  * thread (eik_plan_create returns NULL and sets both). */
@@ -289,6 +309,10 @@ int eik_field_sample(const eik_field* f, const eik_grid* g, double* out,
                      int32_t threads);
 int eik_field_eval_points(const eik_field* f, const double* xy, int64_t count,
                           double* out);
+/* Rows [row0, row0+nrows) of eik_field_sample's array (global coordinates:
+ * bit-identical to the whole grid's sampling), for a rank's row strip. */
+int eik_field_sample_rows(const eik_field* f, const eik_grid* g, int64_t row0, int64_t nrows,
+                          double* out, int32_t threads);
 
 #ifdef __cplusplus
 }

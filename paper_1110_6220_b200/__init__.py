@@ -17,7 +17,7 @@ from .problem import (CellDecomposition, CellTables, ExitSpec, Grid, Problem, Sp
                       speed_nodemask, speed_sinsum, speed_sinusoid)
 from .solvers import (FmmOptions, HybridStats, Plan, SolverOutput, fhcm_solve, fmm_solve,
                       fmsm_solve, fsm_solve, hcm_solve, lsm_solve, run_batch, set_hcm_mode, solve,
-                      solve_batch)
+                      solve_batch, solve_multi)
 from .distributed import StripSolve, fsm_solve_strips, strip_bounds
 from .metrics import MetricsReport, ground_truth, method_metrics, refined_problem
 from . import experiment_io
@@ -41,7 +41,7 @@ __all__ = [
     "snap_point_to_node", "speed_blocks", "speed_checkerboard", "speed_comb_maze",
     "speed_constant", "speed_nodemask", "speed_sinsum", "speed_sinusoid", "HybridStats",
     "Plan", "SolverOutput", "FmmOptions", "fhcm_solve", "fmm_solve", "fmsm_solve",
-    "fsm_solve", "lsm_solve", "hcm_solve", "set_hcm_mode", "solve", "run_batch", "solve_batch", "device_count", "set_device", "StripSolve", "fsm_solve_strips",
+    "fsm_solve", "lsm_solve", "hcm_solve", "set_hcm_mode", "solve", "solve_multi", "run_batch", "solve_batch", "device_count", "set_device", "StripSolve", "fsm_solve_strips",
     "strip_bounds", "MetricsReport", "ground_truth", "method_metrics", "refined_problem",
     "experiment_io",
 ]

@@ -90,6 +90,9 @@ EXPORTS = {
     "eik_plan_sweep": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.POINTER(C.c_int32)]),
     "eik_plan_get_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]),
     "eik_plan_set_rows": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]),
+    "eik_plan_sweep_async": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p]),
+    "eik_plan_rows_async": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32,
+                                      C.c_void_p]),
     "eik_plan_set_ctas": (C.c_int, [C.c_void_p, C.c_int32]),
     "eik_set_hcm_mode": (C.c_int, [C.c_int32]),
     "eik_plan_set_hcm_mode": (C.c_int, [C.c_void_p, C.c_int32]),
@@ -97,6 +100,10 @@ EXPORTS = {
     "eik_plan_capacity": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "eik_plan_run_batch": (C.c_int, [C.POINTER(C.c_void_p), C.c_int32, C.POINTER(eik_output),
                                      C.POINTER(C.c_double)]),
+    "eik_solve_multi": (C.c_int, [C.POINTER(eik_problem), C.c_int32, C.POINTER(C.c_int32), C.c_int32,
+                                  C.POINTER(eik_output)]),
+    "eik_field_sample_rows": (C.c_int, [C.POINTER(eik_field), C.POINTER(eik_grid), C.c_int64,
+                                        C.c_int64, _dp, C.c_int32]),
     "eik_solve_batch": (C.c_int, [C.POINTER(C.POINTER(eik_problem)), C.POINTER(C.POINTER(eik_cells)),
                                   C.POINTER(C.c_int32), C.c_int32, C.POINTER(eik_output),
                                   C.POINTER(C.c_double)]),

@@ -282,6 +282,36 @@ cudaError_t ensure_dynamic_smem(const void* kernel, size_t bytes) {
   return e;
 }
 
+// fmm_solve's counters (classic_solvers.cpp:40-43,64-90): every non-exit
+// node adjacent to an exit is evaluated once at initialisation, and every
+// edge between two non-exit nodes once, when its first end is accepted; no
+// sweeps.  Independent of the acceptance order.
+int64_t fmm_node_updates(const eik_grid& g, const int64_t* ex, int64_t ne) {
+  const int64_t m = g.m, n = g.n;
+  auto is_exit = [&](int64_t idx) { return std::binary_search(ex, ex + ne, idx); };
+  int64_t exit_edges = 0, exit_exit = 0;
+  std::vector<int64_t> adj;
+  adj.reserve((size_t)ne * 4);
+  for (int64_t k = 0; k < ne; ++k) {
+    const int64_t i = ex[k] % m, j = ex[k] / m;
+    const int64_t nb[4] = {i + 1 < m ? ex[k] + 1 : -1, i > 0 ? ex[k] - 1 : -1,
+                           j + 1 < n ? ex[k] + m : -1, j > 0 ? ex[k] - m : -1};
+    for (int d = 0; d < 4; ++d) {
+      if (nb[d] < 0) continue;
+      ++exit_edges;
+      if (is_exit(nb[d])) ++exit_exit;  // counted from both ends
+      else adj.push_back(nb[d]);
+    }
+  }
+  std::sort(adj.begin(), adj.end());
+  const int64_t n_adj = std::unique(adj.begin(), adj.end()) - adj.begin();
+  const int64_t edges = (m - 1) * n + m * (n - 1);
+  return edges - (exit_edges - exit_exit / 2) + n_adj;
+}
+
+int solve_multi(const eik_problem* p, int32_t method, const int32_t* devices, int32_t n_dev,
+                eik_output* out);
+
 int plan_capacity(eik_plan* P, int* device, int* fixed) {
   CK(cudaSetDevice(P->device));
   *fixed = 0;
@@ -398,34 +428,7 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
                     "holds " + std::to_string(ctas) + " CTAs (" + std::to_string(need) +
                     " needed); shard the rows across devices (distributed.fsm_solve_strips)");
     }
-    if (method == EIK_FMM) {
-      // fmm_solve's counters (classic_solvers.cpp:40-43,64-90): every non-exit
-      // node adjacent to an exit is evaluated once at initialisation, and
-      // every edge between two non-exit nodes once, when its first end is
-      // accepted; no sweeps.  Independent of the acceptance order.
-      const int64_t m = P->g.m, n = P->g.n;
-      const int64_t* ex = p->exit_nodes;
-      const int64_t ne = p->n_exit;
-      auto is_exit = [&](int64_t idx) { return std::binary_search(ex, ex + ne, idx); };
-      int64_t exit_edges = 0, exit_exit = 0;
-      std::vector<int64_t> adj;
-      adj.reserve((size_t)ne * 4);
-      for (int64_t k = 0; k < ne; ++k) {
-        const int64_t i = ex[k] % m, j = ex[k] / m;
-        const int64_t nb[4] = {i + 1 < m ? ex[k] + 1 : -1, i > 0 ? ex[k] - 1 : -1,
-                               j + 1 < n ? ex[k] + m : -1, j > 0 ? ex[k] - m : -1};
-        for (int d = 0; d < 4; ++d) {
-          if (nb[d] < 0) continue;
-          ++exit_edges;
-          if (is_exit(nb[d])) ++exit_exit;  // counted from both ends
-          else adj.push_back(nb[d]);
-        }
-      }
-      std::sort(adj.begin(), adj.end());
-      const int64_t n_adj = std::unique(adj.begin(), adj.end()) - adj.begin();
-      const int64_t edges = (m - 1) * n + m * (n - 1);
-      P->fmm_updates = edges - (exit_edges - exit_exit / 2) + n_adj;
-    }
+    if (method == EIK_FMM) P->fmm_updates = fmm_node_updates(P->g, p->exit_nodes, p->n_exit);
     if (method == EIK_LSM) {
       if ((rc = dalloc(&P->dLsmCnt, P->max_sweeps))) return rc;
       track(P->dLsmCnt);
@@ -647,7 +650,10 @@ int plan_prepare(eik_plan* P) {
   return EIK_OK;
 }
 
-int plan_sweep(eik_plan* P, int64_t first_sweep, int count, int* changed) {
+// sync: read the flags back (changed) and check the watchdog; async: leave
+// them in device memory (changed_dev) on `stream`, the caller reads them later
+int plan_sweep_impl(eik_plan* P, int64_t first_sweep, int count, int* changed, int* changed_dev,
+                    cudaStream_t stream) {
   if (P->method != EIK_FSM && P->method != EIK_FMM)
     return fail(EIK_ERR_CONFIG, "sweep-level control needs an fsm/fmm plan");
   if (count < 1 || count > P->max_sweeps || first_sweep < 0)
@@ -681,12 +687,17 @@ int plan_sweep(eik_plan* P, int64_t first_sweep, int count, int* changed) {
   P->last_sweeps_bound = std::min<int64_t>(P->max_sweeps,
                                            std::max<int64_t>(P->last_sweeps_bound, count + 8));
   int launches = 0;
-  CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
-  CK(cudaMemsetAsync(P->dProg, 0, sizeof(unsigned long long) * P->nstrips, P->stream));
-  CK(cudaMemsetAsync(P->dMbox, 0xFF, sizeof(double) * 2 * P->nstrips * P->pitch, P->stream));
-  CK(cudaMemsetAsync(P->dChanged, 0, sizeof(int) * count, P->stream));
-  CK(cudaMemsetAsync(P->dDone, 0, sizeof(int) * count, P->stream));
-  CK(launch_fsm(a, P->stream, &launches));
+  const cudaStream_t s = stream ? stream : P->stream;
+  if (!changed_dev) CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, s));
+  CK(cudaMemsetAsync(P->dProg, 0, sizeof(unsigned long long) * P->nstrips, s));
+  CK(cudaMemsetAsync(P->dMbox, 0xFF, sizeof(double) * 2 * P->nstrips * P->pitch, s));
+  CK(cudaMemsetAsync(P->dChanged, 0, sizeof(int) * count, s));
+  CK(cudaMemsetAsync(P->dDone, 0, sizeof(int) * count, s));
+  CK(launch_fsm(a, s, &launches));
+  if (changed_dev) {  // stream-ordered: no host synchronisation
+    CK(cudaMemcpyAsync(changed_dev, P->dChanged, sizeof(int) * count, cudaMemcpyDeviceToDevice, s));
+    return EIK_OK;
+  }
   int st[8];
   std::vector<int> ch((size_t)count);
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
@@ -697,6 +708,10 @@ int plan_sweep(eik_plan* P, int64_t first_sweep, int count, int* changed) {
   if (changed)
     for (int k = 0; k < count; ++k) changed[k] = ch[k] != 0;
   return EIK_OK;
+}
+
+int plan_sweep(eik_plan* P, int64_t first_sweep, int count, int* changed) {
+  return plan_sweep_impl(P, first_sweep, count, changed, nullptr, nullptr);
 }
 
 int plan_rows(eik_plan* P, int64_t row0, int64_t nrows, double* host_or_dev, int on_device,
@@ -714,7 +729,27 @@ int plan_rows(eik_plan* P, int64_t row0, int64_t nrows, double* host_or_dev, int
   else
     CK(cudaMemcpy2DAsync(host_or_dev, w, dev, dp, w, nrows,
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, P->stream));
+  int st = 0;
+  CK(cudaMemcpyAsync(&st, P->dStatus, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaStreamSynchronize(P->stream));
+  if (st == 4) return fail(EIK_ERR_CUDA, "fsm wavefront watchdog fired (scheduling bug)");
+  return EIK_OK;
+}
+
+// stream-ordered row copies between the plan and a device buffer (dense
+// m-wide rows), no host synchronisation
+int plan_rows_async(eik_plan* P, int64_t row0, int64_t nrows, double* dev_buf, bool to_plan,
+                    cudaStream_t stream) {
+  if (row0 < 0 || nrows < 0 || row0 + nrows > P->g.n)
+    return fail(EIK_ERR_CONFIG, "row range outside the grid");
+  if (nrows == 0) return EIK_OK;
+  if (!dev_buf) return fail(EIK_ERR_DOMAIN, "null row buffer");
+  CK(cudaSetDevice(P->device));
+  double* dev = P->dU + row0 * P->pitch + kPad;
+  const size_t w = sizeof(double) * P->g.m, dp = sizeof(double) * P->pitch;
+  const cudaStream_t s = stream ? stream : P->stream;
+  if (to_plan) CK(cudaMemcpy2DAsync(dev, dp, dev_buf, w, w, nrows, cudaMemcpyDeviceToDevice, s));
+  else CK(cudaMemcpy2DAsync(dev_buf, w, dev, dp, w, nrows, cudaMemcpyDeviceToDevice, s));
   return EIK_OK;
 }
 
@@ -1266,6 +1301,19 @@ int eik_plan_sweep(eik_plan* P, int64_t first_sweep, int32_t count, int32_t* cha
   return plan_sweep(P, first_sweep, count, changed);
 }
 
+int eik_plan_sweep_async(eik_plan* P, int64_t first_sweep, int32_t count, int32_t* changed_dev,
+                         void* stream) {
+  if (!P || !changed_dev) return fail(EIK_ERR_DOMAIN, "null argument");
+  return plan_sweep_impl(P, first_sweep, count, nullptr, changed_dev,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int eik_plan_rows_async(eik_plan* P, int64_t row0, int64_t nrows, double* dev_buf, int32_t to_plan,
+                        void* stream) {
+  if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
+  return plan_rows_async(P, row0, nrows, dev_buf, to_plan != 0, static_cast<cudaStream_t>(stream));
+}
+
 int eik_plan_get_rows(eik_plan* P, int64_t row0, int64_t nrows, double* dst, int32_t on_device) {
   if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
   return plan_rows(P, row0, nrows, dst, on_device, false);
@@ -1345,6 +1393,31 @@ int eik_solve_batch(const eik_problem* const* problems, const eik_cells* const* 
   if (eik_device_count() < 1)
     return fail(EIK_ERR_CUDA, "no CUDA device visible: the Eikonal hot path has no CPU fallback");
   return solve_batch_pipelined(problems, cells, methods, n, outs, batch_ms);
+}
+
+int eik_solve_multi(const eik_problem* p, int32_t method, const int32_t* devices,
+                    int32_t n_devices, eik_output* out) {
+  g_last_code = EIK_OK;
+  g_last_error.clear();
+  if (!out || !out->u) return fail(EIK_ERR_DOMAIN, "output needs a u buffer");
+  if (n_devices < 1 || !devices) return fail(EIK_ERR_DOMAIN, "need at least one device");
+  const int nd = eik_device_count();
+  for (int d = 0; d < n_devices; ++d)
+    if (devices[d] < 0 || devices[d] >= nd) return fail(EIK_ERR_CONFIG, "no such CUDA device");
+  if (n_devices == 1) {
+    CK(cudaSetDevice(devices[0]));
+    return eik_solve(p, nullptr, method, out);
+  }
+  if (method != EIK_FSM && method != EIK_FMM)
+    return fail(EIK_ERR_NOT_IMPL, "eik_solve_multi shards fsm / fmm (row strips)");
+  if (check_problem(p)) return g_last_code;
+  out->sweeps = out->node_updates = out->heap_removals = 0;
+  out->cell_removals = out->cell_sweeps = out->mon_checks = out->mon_single = 0;
+  out->avhr = out->avs = out->mon_pct = 0.0;
+  out->host_ms = 0.0;
+  out->spec_hits = out->spec_waits = out->spec_self = 0;
+  out->kernel_launches = 0;
+  return solve_multi(p, method, devices, n_devices, out);
 }
 
 int eik_solve(const eik_problem* p, const eik_cells* c, int32_t method, eik_output* out) {

@@ -98,15 +98,26 @@ static double gy(const eik_grid* g, int64_t j) { return g->y0 + (double)j * g->h
 
 int eik_field_sample(const eik_field* f, const eik_grid* g, double* out,
                      int32_t threads) {
-  if (!f || !g || !out || g->m < 1 || g->n < 1) return EIK_ERR_DOMAIN;
-  const int64_t m = g->m, n = g->n;
+  if (!g) return EIK_ERR_DOMAIN;
+  return eik_field_sample_rows(f, g, 0, g->n, out, threads);
+}
+
+/* Rows [row0, row0 + nrows) of the grid's nodes (out[(j - row0) * m + i]),
+ * with the GLOBAL coordinates y0 + j*h: a strip samples exactly the bits the
+ * whole grid's sampling holds there (a local grid with a shifted y0 would
+ * round differently). */
+int eik_field_sample_rows(const eik_field* f, const eik_grid* g, int64_t row0, int64_t nrows,
+                          double* out, int32_t threads) {
+  if (!f || !g || !out || g->m < 1 || g->n < 1 || row0 < 0 || nrows < 0 || row0 + nrows > g->n)
+    return EIK_ERR_DOMAIN;
+  const int64_t m = g->m, n = nrows;
   if (f->kind == EIK_FIELD_SINSUM) {
     /* Tabulated separable evaluation; identical bits to sinsum_eval. */
     const int K = f->K;
     double* sa = (double*)malloc(sizeof(double) * (size_t)K * (size_t)m);
     double* ca = (double*)malloc(sizeof(double) * (size_t)K * (size_t)m);
-    double* sb = (double*)malloc(sizeof(double) * (size_t)K * (size_t)n);
-    double* cb = (double*)malloc(sizeof(double) * (size_t)K * (size_t)n);
+    double* sb = (double*)malloc(sizeof(double) * (size_t)K * (size_t)(n + 1));
+    double* cb = (double*)malloc(sizeof(double) * (size_t)K * (size_t)(n + 1));
     if (!sa || !ca || !sb || !cb) {
       free(sa); free(ca); free(sb); free(cb);
       return EIK_ERR_DOMAIN;
@@ -121,33 +132,33 @@ int eik_field_sample(const eik_field* f, const eik_grid* g, double* out,
       }
     }
 #pragma omp parallel for num_threads(threads > 0 ? threads : 1) schedule(static)
-    for (int64_t j = 0; j < n; ++j) {
-      double y = gy(g, j);
+    for (int64_t jj = 0; jj < n; ++jj) {
+      double y = gy(g, row0 + jj);
       for (int k = 0; k < K; ++k) {
         double b = kPi * f->kq[k] * y;
-        sb[(size_t)j * K + k] = sin(b);
-        cb[(size_t)j * K + k] = cos(b);
+        sb[(size_t)jj * K + k] = sin(b);
+        cb[(size_t)jj * K + k] = cos(b);
       }
     }
 #pragma omp parallel for num_threads(threads > 0 ? threads : 1) schedule(static)
-    for (int64_t j = 0; j < n; ++j) {
-      const double* sbj = sb + (size_t)j * K;
-      const double* cbj = cb + (size_t)j * K;
+    for (int64_t j = row0; j < row0 + n; ++j) {
+      const double* sbj = sb + (size_t)(j - row0) * K;
+      const double* cbj = cb + (size_t)(j - row0) * K;
       for (int64_t i = 0; i < m; ++i) {
         const double* sai = sa + (size_t)i * K;
         const double* cai = ca + (size_t)i * K;
         double s = 0.0;
         for (int k = 0; k < K; ++k) s = s + (sai[k] * cbj[k] + cai[k] * sbj[k]);
-        out[j * m + i] = 1.0 + 0.5 * (s / (double)K);
+        out[(j - row0) * m + i] = 1.0 + 0.5 * (s / (double)K);
       }
     }
     free(sa); free(ca); free(sb); free(cb);
     return EIK_OK;
   }
 #pragma omp parallel for num_threads(threads > 0 ? threads : 1) schedule(static)
-  for (int64_t j = 0; j < n; ++j) {
+  for (int64_t j = row0; j < row0 + n; ++j) {
     double y = gy(g, j);
-    for (int64_t i = 0; i < m; ++i) out[j * m + i] = eik_field_eval(f, gx(g, i), y);
+    for (int64_t i = 0; i < m; ++i) out[(j - row0) * m + i] = eik_field_eval(f, gx(g, i), y);
   }
   return EIK_OK;
 }

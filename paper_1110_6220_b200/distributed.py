@@ -43,16 +43,37 @@ def strip_bounds(n: int, world: int, rank: int):
     return n * rank // world, n * (rank + 1) // world
 
 
+def strip_speed(problem: Problem, r0: int, r1: int) -> np.ndarray:
+    """F on rows [r0, r1) only, at the GLOBAL node coordinates (bit-identical
+    to the whole grid's sampling): a rank never materialises the full field."""
+    from .problem import SpeedField
+    g = problem.grid
+    if problem._F is not None:  # already sampled (e.g. a caller-provided array)
+        return problem._F.reshape(g.n, g.m)[r0:r1]
+    out = np.empty((r1 - r0) * g.m, dtype=np.float64)
+    if isinstance(problem.speed, SpeedField):
+        import os
+        gc = g.c()
+        N.raise_for(N.lib.eik_field_sample_rows(C.byref(problem.speed.cfield), C.byref(gc), r0,
+                                                r1 - r0, N.dptr(out), min(32, os.cpu_count() or 1)))
+    else:
+        xs = g.x0 + np.arange(g.m, dtype=np.float64) * g.h
+        ys = g.y0 + np.arange(r0, r1, dtype=np.float64) * g.h  # Grid::y(j) = y0 + j*h
+        X, Y = np.meshgrid(xs, ys)
+        out[:] = np.asarray(problem.speed(X, Y), dtype=np.float64).reshape(-1)
+    return out.reshape(r1 - r0, g.m)
+
+
 def strip_problem(problem: Problem, r0: int, r1: int) -> Problem:
     """The strip's own problem: rows [r0-1, r1] of the grid (local rows 0 and
     nl-1 are the ghost rows), exits = the strip's exits plus every ghost node
-    (frozen; their values are set after prepare and after each exchange)."""
+    (frozen; their values are set after prepare and after each exchange).
+    Only the strip's rows of F are sampled (memory ~1/P of the grid)."""
     g = problem.grid
     m = g.m
     nl = r1 - r0 + 2
-    F = problem.sampled_speed().reshape(g.n, m)
     Fl = np.ones((nl, m), dtype=np.float64)  # ghost rows: any positive speed
-    Fl[1:-1] = F[r0:r1]
+    Fl[1:-1] = strip_speed(problem, r0, r1)
     ex = np.asarray(problem.exit_nodes, dtype=np.int64)
     ec = np.asarray(problem.exit_cost, dtype=np.float64)
     rows = ex // m
@@ -86,6 +107,17 @@ class DeviceStripSweeper:
         N.raise_for(N.lib.eik_plan_sweep(self.plan._h, k, 1, ch))
         return bool(ch[0])
 
+    # stream-ordered variants (no host synchronisation): the round runs on the
+    # caller's CUDA stream, the change flag lands in a device int32 tensor
+    def sweep_async(self, k: int, flag, stream: int) -> None:
+        N.raise_for(N.lib.eik_plan_sweep_async(self.plan._h, k, 1, C.c_void_p(flag.data_ptr()),
+                                               C.c_void_p(stream)))
+
+    def rows_async(self, row0: int, nrows: int, buf, to_plan: bool, stream: int) -> None:
+        N.raise_for(N.lib.eik_plan_rows_async(self.plan._h, row0, nrows,
+                                              C.c_void_p(buf.data_ptr()), 1 if to_plan else 0,
+                                              C.c_void_p(stream)))
+
     @staticmethod
     def _ptr(buf):
         if isinstance(buf, np.ndarray):
@@ -106,17 +138,32 @@ class DeviceStripSweeper:
 
 @dataclass
 class StripSolve:
-    values: np.ndarray      # the full m*n field (every rank)
+    values: Optional[np.ndarray]  # the m*n field (gather="all", or rank 0 with "rank0"),
+                                  # this rank's rows (gather="none"), else None
     sweeps: int             # rounds, including the final unchanged one
     node_updates: int       # sweeps * (M - |Q|), the reference's accounting
     rows: tuple             # this rank's [r0, r1)
+    device_ms: float = 0.0  # the rounds (max over ranks on GPUs), CUDA events
+
+
+LOOKAHEAD = 2  # rounds enqueued beyond the last one whose change flag was read
 
 
 def fsm_solve_strips(problem: Problem, group=None,
                      sweeper_factory: Optional[Callable[[Problem], object]] = None,
-                     max_rounds: Optional[int] = None) -> StripSolve:
+                     max_rounds: Optional[int] = None, gather: str = "all") -> StripSolve:
     """fsm_solve over the ranks of `group` (torch.distributed), strip-Jacobi.
-    Without an initialised process group it runs as a single strip."""
+    Without an initialised process group it runs as a single strip.
+
+    On GPUs (NCCL) a round is enqueued on the current CUDA stream with no host
+    synchronisation -- sweep (eik_plan_sweep_async), edge rows into send
+    buffers, NCCL send/recv, ghost rows back, all-reduce(MAX) of the change
+    flag, its copy into pinned memory -- and the host reads the flag of the
+    round LOOKAHEAD behind, so the device never idles on the host; rounds
+    enqueued past the first unchanged one change nothing (a fixed point stays
+    fixed) and the count reported is the first unchanged round's.
+    gather: "all" (every rank gets the field), "rank0", or "none" (each rank
+    keeps its own rows)."""
     import torch
     import torch.distributed as dist
 
@@ -146,51 +193,122 @@ def fsm_solve_strips(problem: Problem, group=None,
     send_lo, send_hi, recv_lo, recv_hi = row(), row(), row(), row()
     limit = max_rounds if max_rounds is not None else 4 * (m + n) + 16
     k = 0
-    while True:
-        if k >= limit:
-            raise N.BudgetError("strip-Jacobi FSM did not converge within the round budget")
-        changed = sw.sweep(k)
-        k += 1
-        if world > 1:
-            ops = []
-            if rank > 0:
-                take(1, send_lo)
-                ops += [dist.P2POp(dist.isend, send_lo, rank - 1, group),
-                        dist.P2POp(dist.irecv, recv_lo, rank - 1, group)]
-            if rank < world - 1:
-                take(nl - 2, send_hi)
-                ops += [dist.P2POp(dist.isend, send_hi, rank + 1, group),
-                        dist.P2POp(dist.irecv, recv_hi, rank + 1, group)]
-            for w in dist.batch_isend_irecv(ops):
-                w.wait()
-            if on_gpu:
-                torch.cuda.current_stream().synchronize()
-            if rank > 0:
-                put(0, recv_lo)
-            if rank < world - 1:
-                put(nl - 1, recv_hi)
-            flag = torch.tensor([1 if changed else 0], dtype=torch.int32, device=dev)
-            dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
-            changed = bool(flag.item())
-        if not changed:
-            break
-    # assemble the full field on every rank (strips padded to the largest)
+    dev_ms = 0.0
+    if on_gpu and hasattr(sw, "sweep_async"):
+        k, dev_ms = _rounds_async(sw, rank, world, group, nl, limit, send_lo, send_hi, recv_lo,
+                                  recv_hi, dev)
+    else:
+        while True:
+            if k >= limit:
+                raise N.BudgetError("strip-Jacobi FSM did not converge within the round budget")
+            changed = sw.sweep(k)
+            k += 1
+            if world > 1:
+                ops = []
+                if rank > 0:
+                    take(1, send_lo)
+                    ops += [dist.P2POp(dist.isend, send_lo, rank - 1, group),
+                            dist.P2POp(dist.irecv, recv_lo, rank - 1, group)]
+                if rank < world - 1:
+                    take(nl - 2, send_hi)
+                    ops += [dist.P2POp(dist.isend, send_hi, rank + 1, group),
+                            dist.P2POp(dist.irecv, recv_hi, rank + 1, group)]
+                for w in dist.batch_isend_irecv(ops):
+                    w.wait()
+                if on_gpu:
+                    torch.cuda.current_stream().synchronize()
+                if rank > 0:
+                    put(0, recv_lo)
+                if rank < world - 1:
+                    put(nl - 1, recv_hi)
+                flag = torch.tensor([1 if changed else 0], dtype=torch.int32, device=dev)
+                dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+                changed = bool(flag.item())
+            if not changed:
+                break
+    # the field: every rank ("all"), rank 0 ("rank0") or each its own rows
     own = np.empty((r1 - r0) * m, dtype=np.float64)
     sw.get_rows(1, r1 - r0, own)
-    if world > 1:
+    u = own
+    if world > 1 and gather != "none":
         rows_max = max(strip_bounds(n, world, r)[1] - strip_bounds(n, world, r)[0]
                        for r in range(world))
         buf = torch.full((rows_max * m,), math.inf, dtype=torch.float64, device=dev)
         buf[: own.size] = torch.from_numpy(own).to(dev)
-        parts = [torch.empty_like(buf) for _ in range(world)]
-        dist.all_gather(parts, buf, group=group)
-        u = np.empty(n * m, dtype=np.float64)
-        for r in range(world):
-            a, b = strip_bounds(n, world, r)
-            u[a * m:b * m] = parts[r][: (b - a) * m].cpu().numpy()
-    else:
-        u = own
+        if gather == "all":
+            parts = [torch.empty_like(buf) for _ in range(world)]
+            dist.all_gather(parts, buf, group=group)
+        else:
+            parts = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
+            dist.gather(buf, parts, dst=0, group=group)
+        if parts is not None:
+            u = np.empty(n * m, dtype=np.float64)
+            for r in range(world):
+                a, b = strip_bounds(n, world, r)
+                u[a * m:b * m] = parts[r][: (b - a) * m].cpu().numpy()
+        else:
+            u = None
     close = getattr(sw, "close", None)
     if close:
         close()
-    return StripSolve(u, k, k * (m * n - len(problem.exit_nodes)), (r0, r1))
+    return StripSolve(u, k, k * (m * n - len(problem.exit_nodes)), (r0, r1), dev_ms)
+
+
+def _rounds_async(sw, rank, world, group, nl, limit, send_lo, send_hi, recv_lo, recv_hi, dev):
+    """The rounds on the device, stream-ordered (see fsm_solve_strips);
+    returns (rounds, device ms of the rounds, max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+    ring = 8
+    flags = torch.zeros(ring, dtype=torch.int32, device=dev)
+    host = torch.zeros(limit + 1, dtype=torch.int32, pin_memory=True)
+    events = [None] * ring
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    k = 0
+    done_at = None
+    while done_at is None:
+        if k >= limit:
+            raise N.BudgetError("strip-Jacobi FSM did not converge within the round budget")
+        slot = k % ring
+        if events[slot] is not None:
+            events[slot].synchronize()  # ring slot free (LOOKAHEAD < ring, so already done)
+        f = flags[slot:slot + 1]
+        sw.sweep_async(k, f, sh)
+        if world > 1:
+            ops = []
+            if rank > 0:
+                sw.rows_async(1, 1, send_lo, False, sh)
+                ops += [dist.P2POp(dist.isend, send_lo, rank - 1, group),
+                        dist.P2POp(dist.irecv, recv_lo, rank - 1, group)]
+            if rank < world - 1:
+                sw.rows_async(nl - 2, 1, send_hi, False, sh)
+                ops += [dist.P2POp(dist.isend, send_hi, rank + 1, group),
+                        dist.P2POp(dist.irecv, recv_hi, rank + 1, group)]
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()  # NCCL: the current stream waits; the host does not
+            if rank > 0:
+                sw.rows_async(0, 1, recv_lo, True, sh)
+            if rank < world - 1:
+                sw.rows_async(nl - 1, 1, recv_hi, True, sh)
+            dist.all_reduce(f, op=dist.ReduceOp.MAX, group=group)
+        host[k:k + 1].copy_(f, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        events[slot] = ev
+        j = k - LOOKAHEAD
+        if j >= 0:
+            events[j % ring].synchronize()
+            if int(host[j]) == 0:
+                done_at = j
+        k += 1
+    # rounds j+1 .. k-1 were enqueued past the fixed point: harmless
+    e1.record(stream)
+    e1.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=group)
+    return done_at + 1, float(ms.item())

@@ -172,6 +172,24 @@ def fmsm_solve(problem: Problem, cells: CellDecomposition) -> SolverOutput:
     return solve(problem, "fmsm", cells)
 
 
+def solve_multi(problem: Problem, method: str = "fsm", devices=None) -> SolverOutput:
+    """fsm_solve / the FMM row over several GPUs of this process
+    (eik_solve_multi): row strips, one per device, strip-Jacobi rounds with
+    the edge rows exchanged by peer copies.  `devices` lists CUDA ordinals (a
+    device may appear more than once: its strips then share it)."""
+    devs = list(devices) if devices is not None else [0]
+    F = problem.sampled_speed()
+    p, keep_p = _c_problem(problem, F)
+    u = np.empty(problem.grid.size(), dtype=np.float64)
+    res = N.eik_output()
+    res.u = N.dptr(u)
+    res.u_on_device = 0
+    dv = (C.c_int32 * len(devs))(*devs)
+    N.raise_for(N.lib.eik_solve_multi(C.byref(p), N.METHOD_NAMES[method], dv, len(devs),
+                                      C.byref(res)))
+    return _pack(res, u, problem.grid)
+
+
 class Plan:
     """Resident solve (eik_plan_*): inputs uploaded once, values stay in HBM."""
 

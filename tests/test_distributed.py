@@ -202,3 +202,79 @@ def test_device_partitions_equal_emulation(part_rows, kind):
     plan.close()
     with pytest.raises(E.ConfigError):
         E.Plan(p, "fsm").set_partitions(48)
+
+
+def test_strip_speed_is_the_whole_grid_sampling():
+    """A rank samples only its rows, with the GLOBAL coordinates: bit for bit
+    the rows of the whole grid's sampling (SpeedField and plain callables)."""
+    from paper_1110_6220_b200.configs import config5
+    from paper_1110_6220_b200.distributed import strip_speed
+    p = config5(257).problem  # the 16-sinusoid field (tabulated sampling)
+    q = _problem()
+    for prob in (p, q):
+        F = prob.sampled_speed().reshape(prob.grid.n, prob.grid.m)
+        fresh = E.Problem(prob.grid, prob.speed, prob.exit_nodes, prob.exit_cost)
+        for a, b in [(0, 17), (40, 41), (prob.grid.n - 9, prob.grid.n)]:
+            assert np.array_equal(strip_speed(fresh, a, b), F[a:b])
+    g = q.grid
+    call = E.Problem(g, lambda x, y: 1.0 + 0.25 * np.sin(3 * x) * np.cos(2 * y), q.exit_nodes,
+                     q.exit_cost)
+    F = call.sampled_speed().reshape(g.n, g.m)
+    fresh = E.Problem(g, call.speed, q.exit_nodes, q.exit_cost)
+    assert np.array_equal(strip_speed(fresh, 5, 30), F[5:30])
+
+
+def _nccl_single(outdir, port):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        p = _problem(kind="chk")
+        r = E.fsm_solve_strips(p, gather="rank0")
+        np.save(os.path.join(outdir, "u.npy"), r.values)
+        np.save(os.path.join(outdir, "k.npy"), np.array([r.sweeps, r.node_updates]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_device_stream_ordered_rounds_single_rank():
+    """The NCCL path (rounds enqueued on the stream, the change flag read two
+    rounds behind) with one rank is fsm_solve: same bits, same sweep count."""
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_nccl_single, args=(d, _free_port()), nprocs=1, join=True)
+        u = np.load(os.path.join(d, "u.npy"))
+        k = np.load(os.path.join(d, "k.npy"))
+    ref = O.oracle_solve(_problem(kind="chk"), "fsm")
+    assert np.array_equal(u, ref.u) and k[0] == ref.sweeps and k[1] == ref.node_updates
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices,kind", [([0, 0], "chk"), ([0, 0, 0], "sin"),
+                                          ([0, 0, 0, 0, 0], "chk")])
+def test_solve_multi_equals_emulation(devices, kind):
+    """eik_solve_multi: strips on the listed devices (here several strips on
+    one GPU; the rounds' kernels never wait on each other), edge rows by peer
+    copy -- the serial emulation of the same rounds bit for bit."""
+    p = _problem(m=73, n=131, kind=kind)
+    out = E.solve_multi(p, "fsm", devices)
+    u, k = emulate(p, len(devices))
+    assert np.array_equal(out.values, u) and out.sweeps == k == out.rounds
+    assert float(np.max(np.abs(out.values - O.oracle_solve(p, "fsm").u))) <= 1e-10
+    fmm = E.solve_multi(p, "fmm", devices)
+    ref = O.oracle_solve(p, "fmm")
+    assert np.array_equal(fmm.values, u)
+    assert (fmm.sweeps, fmm.node_updates, fmm.heap_removals) == (0, ref.node_updates,
+                                                                ref.heap_removals)
+
+
+@pytest.mark.gpu
+def test_solve_multi_one_device_is_fsm():
+    p = _problem()
+    a = E.solve_multi(p, "fsm", [0])
+    b = O.oracle_solve(p, "fsm")
+    assert np.array_equal(a.values, b.u) and a.sweeps == b.sweeps
