@@ -224,7 +224,7 @@ def test_strip_speed_is_the_whole_grid_sampling():
     assert np.array_equal(strip_speed(fresh, 5, 30), F[5:30])
 
 
-def _nccl_single(outdir, port):
+def _nccl_single(_index, outdir, port):
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
