@@ -260,7 +260,22 @@ def _rounds_async(sw, rank, world, group, nl, limit, send_lo, send_hi, recv_lo, 
     import torch
     import torch.distributed as dist
 
-    stream = torch.cuda.current_stream(dev)
+    # a stream of our own: the default stream's handle is 0, which the ABI
+    # reads as "the plan's stream" (not ordered with torch's work)
+    stream = torch.cuda.Stream(dev)
+    stream.wait_stream(torch.cuda.current_stream(dev))
+    with torch.cuda.stream(stream):
+        out = _rounds_on(stream, sw, rank, world, group, nl, limit, send_lo, send_hi, recv_lo,
+                         recv_hi, dev)
+    torch.cuda.current_stream(dev).wait_stream(stream)
+    return out
+
+
+def _rounds_on(stream, sw, rank, world, group, nl, limit, send_lo, send_hi, recv_lo, recv_hi,
+               dev):
+    import torch
+    import torch.distributed as dist
+
     sh = stream.cuda_stream
     ring = 8
     flags = torch.zeros(ring, dtype=torch.int32, device=dev)
