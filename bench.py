@@ -309,7 +309,8 @@ def measure_configs(hbm, peak_kind):
                                    "unit": "GB/s", "frac": ach / hbm, "algorithmic_bytes": nbytes,
                                    "peak_kind": peak_kind}
                 if key == "c5/fsm":
-                    row["roofline"]["traffic"] = _ncu_dram("r02_fsm_c5_metrics.csv")
+                    row["roofline"]["traffic"] = (_ncu_dram("r02_fsm_c5_metrics.csv") or
+                                                  _ncu_dram("r01_fsm_c5_v4_metrics.csv"))
             out[key] = row
         del p, cfg
     return out
@@ -449,18 +450,29 @@ def main():
     dom_k, dom_t, dom_bytes, dom_ach = best
     # DRAM bytes of the dominant launch from a committed `ncu --set full`
     # capture (profiles/r01_traffic.json), when it profiled this same solve
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as f:
-            traffic = json.load(f).get(dom_k, {}).get("dram_bytes_per_launch")
-    except (OSError, ValueError):
-        pass
+    traffic, prof = None, {}
+    for fn in ("r02_traffic.json", "r01_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", fn)) as f:
+                prof = json.load(f).get(dom_k, {})
+        except (OSError, ValueError):
+            prof = {}
+        if prof:
+            traffic = prof.get("dram_bytes_per_launch")
+            break
     roofline = {"bound": "hbm", "kernel": dom_k, "achieved": round(dom_ach, 2), "peak": hbm,
                 "unit": "GB/s", "frac": dom_ach / hbm, "traffic": traffic,
                 "algorithmic_bytes": dom_bytes, "peak_kind": peak_kind,
+                # the in-cell regime's own bounds, from the committed
+                # `ncu --set full` capture of this solve alone
+                "fp64_pipe_frac": prof.get("fp64_pipe_pct_of_peak", 0) / 100 if prof else None,
+                "issue_active_frac": prof.get("issue_active_pct", 0) / 100 if prof else None,
+                "smem_wavefront_frac": (prof.get("smem_wavefronts_pct_of_peak", 0) / 100
+                                        if prof else None),
                 "note": "the longest solve of the concurrent step (its kernel's duration inside "
-                        "the step); latency-bound fp64 dependency chains; algorithmic bytes per "
-                        "SURVEY §8(d)"}
+                        "the step); latency-bound fp64 dependency chains (one warp per cell, "
+                        "a serial committer), so HBM, fp64 pipe and shared memory are all far "
+                        "from their peaks; algorithmic bytes per SURVEY §8(d)"}
 
     # e2e: public API (eik_solve_batch), pinned host buffers, H2D + solves +
     # D2H of every solve of the step inside the timed region
