@@ -62,7 +62,7 @@ Knobs read_knobs() {
   k.hc_profile = gb("EIK_HC_PROFILE");
   k.hc_idle_ns = gi("EIK_HC_IDLE_NS", 200);
   k.hc_skip_from = gi("EIK_HC_SKIP_FROM", 1);
-  k.batch_sms_scale = gd("EIK_BATCH_SMS_SCALE", 2.0);
+  k.batch_sms_scale = gd("EIK_BATCH_SMS_SCALE", 0.0);
   k.batch_fmsm_ctas = std::max(1, gi("EIK_BATCH_FMSM_CTAS", 16));
   k.batch_fmsm_prio = gd("EIK_BATCH_FMSM_PRIO", 0.5);
   k.batch_fixed_per_sm = gi("EIK_BATCH_FIXED_PER_SM", 0);
@@ -777,7 +777,7 @@ struct BatchSlot {
   bool hc = false;
 };
 
-int batch_slot(eik_plan* P, int sms, int budget, BatchSlot& b) {
+int batch_slot(eik_plan* P, int sms, int budget, BatchSlot& b, double scale = 2.0) {
   const Knobs& kn = knobs();
   int dev = 0, fixed = 0;
   int rc = plan_capacity(P, &dev, &fixed);
@@ -801,7 +801,7 @@ int batch_slot(eik_plan* P, int sms, int budget, BatchSlot& b) {
   } else {
     const double J = (double)P->cells_x * P->cells_y;
     const double w = std::pow(J, 0.25) / std::sqrt((double)std::max(1, P->hc_warps_per_cta));
-    b.sms = std::max(2, (int)std::lround(kn.batch_sms_scale * w));
+    b.sms = std::max(2, (int)std::lround(scale * w));
     b.prio = 2.0 + w + (P->method == EIK_HCM ? 0.01 : 0.0);
     b.hc = true;
   }
@@ -810,15 +810,62 @@ int batch_slot(eik_plan* P, int sms, int budget, BatchSlot& b) {
   return EIK_OK;
 }
 
+// Heap-cell slice scale for a batch: 2 J^(1/4)/sqrt(w) SMs per replay keeps
+// the schedule's tail short when the batch is about one wave of the device;
+// a batch of many waves is bound by total SM-time instead, which is lower on
+// smaller slices (C2 matrix, 20 steps = 280 solves: scale 2 -> 891, 1 -> 1022
+// M points/s; 3 steps: 2 -> 550, 1 -> 440).  `waves` = the batch's slices at
+// scale 2 over the SM budget.  EIK_BATCH_SMS_SCALE > 0 overrides.
+double batch_scale_for(double waves) {
+  const double k = knobs().batch_sms_scale;
+  if (k > 0.0) return k;
+  return waves >= 8.0 ? 1.0 : 2.0;
+}
+
 int batch_slots(eik_plan* const* plans, int n, int budget, std::vector<BatchSlot>& slot) {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, plans[0]->device));
   slot.assign(n, BatchSlot{});
+  double total = 0.0;
   for (int k = 0; k < n; ++k) {
     int rc = batch_slot(plans[k], sms, budget, slot[k]);
     if (rc) return rc;
+    total += slot[k].sms;
   }
+  const double scale = batch_scale_for(total / budget);
+  if (scale != 2.0)
+    for (int k = 0; k < n; ++k) {
+      int rc = batch_slot(plans[k], sms, budget, slot[k], scale);
+      if (rc) return rc;
+    }
   return EIK_OK;
+}
+
+// The same waves estimate before any plan exists (eik_solve_batch): slices
+// from the problem shapes alone, heap-cell warps per CTA as plan_init_cells
+// sizes them (k_heapcell.cu heapcell_smem_bytes).
+double batch_waves_estimate(const eik_problem* const* problems, const eik_cells* const* cells,
+                            const int32_t* methods, int n, int budget) {
+  const Knobs& kn = knobs();
+  double total = 0.0;
+  for (int k = 0; k < n; ++k) {
+    const int32_t m = methods[k];
+    const eik_grid& g = problems[k]->grid;
+    if (m == EIK_FMSM) {
+      total += kn.batch_fmsm_ctas;
+    } else if ((m == EIK_HCM || m == EIK_FHCM || m == EIK_HCM_EXACT) && cells && cells[k]) {
+      const int64_t cx = cells[k]->cells_x, cy = cells[k]->cells_y;
+      const int64_t bw = g.m / cx, bh = g.n / cy;
+      const int64_t mw = g.m - (cx - 1) * bw, mh = g.n - (cy - 1) * bh;
+      const int64_t pu = (mw + 4) & ~(int64_t)1, ml = std::max(mw, mh);
+      const double bytes = 8.0 * (2.0 * (mh + 2) * pu + 8.0 * ml) + (double)mw * mh + 128.0;
+      const double w = std::max(1.0, std::min(8.0, std::floor(216.0 * 1024 / bytes)));
+      total += std::max(2.0, std::round(2.0 * std::pow((double)cx * cy, 0.25) / std::sqrt(w)));
+    } else {
+      total += std::max<int64_t>(1, (g.n + 32 * 12 - 1) / (32 * 12));  // FSM strips, 12 per SM
+    }
+  }
+  return total / std::max(1, budget);
 }
 
 // Runs the plans as a list schedule: in order of priority, each plan starts
@@ -879,6 +926,9 @@ int plan_run_batch(eik_plan* const* plans, int n, eik_output* outs, double* batc
       th.emplace_back([&, k, P]() {
         cudaSetDevice(device);
         const bool hc = slot[k].hc;
+        // FMSM Part I runs before the plan waits for its SMs (a failure is
+        // reported by plan_run, which calls it again)
+        if (plan_prepare_host(P)) P->fmsm_ready = false;
         {
           std::unique_lock<std::mutex> lk(mu);
           cv.wait(lk, [&]() { return admitted[k] && (hc || hc_launching == 0); });
@@ -1001,6 +1051,7 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
   const int budget = std::max(1, (int)std::floor(0.98 * sms));
   const Knobs& kn = knobs();
   const int workers = std::max(1, std::min(n, kn.batch_workers > 0 ? kn.batch_workers : 64));
+  const double scale = batch_scale_for(batch_waves_estimate(problems, cells, methods, n, budget));
   struct Waiting {
     int k;
     BatchSlot b;
@@ -1063,7 +1114,9 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
       const SlowCall slow_create = t_slow;
       t_slow = SlowCall{};
       BatchSlot b;
-      int rc = P ? batch_slot(P, sms, budget, b) : (g_last_code != EIK_OK ? g_last_code : EIK_ERR_CUDA);
+      int rc = P ? batch_slot(P, sms, budget, b, scale)
+                 : (g_last_code != EIK_OK ? g_last_code : EIK_ERR_CUDA);
+      if (!rc) rc = plan_prepare_host(P);  // FMSM Part I before the SMs are held
       if (rc) {
         codes[k] = rc;
         msgs[k] = g_last_error;

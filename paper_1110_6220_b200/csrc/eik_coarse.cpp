@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <limits>
 #include <vector>
 
@@ -33,19 +34,34 @@ inline double quadrant_c(double ua, double ub, double c) {
 // The live entries are exactly an indexed heap's -- a node's current (value,
 // id) -- and a stale entry of a node carries a larger value than its live
 // one, so pops come out in the reference's order: minimum value, ties to the
-// smaller id (indexed_min_heap.hpp:36-48,66-69).  No position index: every
-// sift touches only the contiguous heap array.
+// smaller id (indexed_min_heap.hpp:36-48,66-69).  Values are >= 0 (exit
+// costs are refused when negative, candidates only add to them), so an
+// entry packs into one 128-bit word -- value bits above the id -- whose
+// unsigned order is the (value, id) order; -0.0 is folded into +0.0.
 class Heap {
  public:
+  using Ent = unsigned __int128;
   Heap() { h_.reserve(1024); }
   bool empty() const { return h_.empty(); }
+  static Ent pack(int32_t id, double k) {
+    uint64_t b;
+    std::memcpy(&b, &k, 8);
+    if (k == 0.0) b = 0;
+    return ((Ent)b << 32) | (uint32_t)id;
+  }
+  static double key_of(Ent e) {
+    const uint64_t b = (uint64_t)(e >> 32);
+    double k;
+    std::memcpy(&k, &b, 8);
+    return k;
+  }
   void push(int32_t id, double k) {
-    h_.push_back({k, id});
+    const Ent e = pack(id, k);
+    h_.push_back(e);
     int32_t p = (int32_t)h_.size() - 1;
-    const Ent e = h_[p];
     while (p > 0) {
       const int32_t par = (p - 1) >> 2;
-      if (!less(e, h_[par])) break;
+      if (!(e < h_[par])) break;
       h_[p] = h_[par];
       p = par;
     }
@@ -53,33 +69,43 @@ class Heap {
   }
   // the minimum entry (value, id); removes it
   void pop(double& k, int32_t& id) {
-    k = h_[0].k;
-    id = h_[0].id;
+    const Ent top = h_[0];
+    k = key_of(top);
+    id = (int32_t)(uint32_t)top;
     const Ent last = h_.back();
     h_.pop_back();
     const int32_t n = (int32_t)h_.size();
     if (n == 0) return;
     int32_t p = 0;
+    Ent* h = h_.data();
     for (;;) {
       const int32_t c0 = 4 * p + 1;
       if (c0 >= n) break;
       int32_t c = c0;
-      const int32_t ce = std::min(c0 + 4, n);
-      for (int32_t q = c0 + 1; q < ce; ++q)
-        if (less(h_[q], h_[c])) c = q;
-      if (!less(h_[c], last)) break;
-      h_[p] = h_[c];
+      Ent mc = h[c0];
+      if (c0 + 3 < n) {  // branch-free minimum of four children
+        const Ent a1 = h[c0 + 1], a2 = h[c0 + 2], a3 = h[c0 + 3];
+        const int32_t i01 = a1 < mc ? c0 + 1 : c0;
+        const Ent m01 = a1 < mc ? a1 : mc;
+        const int32_t i23 = a3 < a2 ? c0 + 3 : c0 + 2;
+        const Ent m23 = a3 < a2 ? a3 : a2;
+        c = m23 < m01 ? i23 : i01;
+        mc = m23 < m01 ? m23 : m01;
+      } else {
+        for (int32_t q = c0 + 1; q < n; ++q)
+          if (h[q] < mc) {
+            mc = h[q];
+            c = q;
+          }
+      }
+      if (!(mc < last)) break;
+      h[p] = mc;
       p = c;
     }
-    h_[p] = last;
+    h[p] = last;
   }
 
  private:
-  struct Ent {
-    double k;
-    int32_t id;
-  };
-  static bool less(const Ent& a, const Ent& b) { return a.k < b.k || (a.k == b.k && a.id < b.id); }
   std::vector<Ent> h_;
 };
 
@@ -135,26 +161,47 @@ int fmsm_part1(const eik_problem* p, const eik_cells* cells, FmsmOrder* out) {
   const double hc_x = (double)(g.m / cx) * g.h;  // cells.cpp:44
   auto gx = [&](int64_t i) { return g.x0 + (double)i * g.h; };
   auto gy = [&](int64_t j) { return g.y0 + (double)j * g.h; };
-  // cell centres (cells.hpp:44-48)
-  std::vector<double> ccx(J), ccy(J);
-  for (int64_t c = 0; c < J; ++c) {
-    const int64_t a = c % cx, b = c / cx;
-    ccx[c] = 0.5 * (gx(ib[a]) + gx(ie[a] - 1));
-    ccy[c] = 0.5 * (gy(jb[b]) + gy(je[b] - 1));
-  }
+  // cell centres (cells.hpp:44-48), one per column and per row
+  std::vector<double> ccx(cx), ccy(cy);
+  for (int32_t a = 0; a < cx; ++a) ccx[a] = 0.5 * (gx(ib[a]) + gx(ie[a] - 1));
+  for (int32_t b = 0; b < cy; ++b) ccy[b] = 0.5 * (gy(jb[b]) + gy(je[b] - 1));
   const double* Fc = cells->center_speed;
 
   // coarse exits (fmsm.cpp:37-81)
   std::vector<double> best(J, kInf);
   if (p->n_exit_points > 0) {
     const bool single = p->n_exit_points == 1;
+    std::vector<int64_t> cand;
     for (int64_t k = 0; k < p->n_exit_points; ++k) {
       const double qx = p->exit_points_xy[2 * k], qy = p->exit_points_xy[2 * k + 1];
+      // The reference takes dmin = min hypot over every cell, then every cell
+      // with hypot <= dmin + 1e-12 (h + dmin).  Squared distances prune first:
+      // a cell with dx^2 + dy^2 > R^2, R = sqrt(smin)(1 + 1e-6) + 1e-9 h, has
+      // hypot > dmin + tie by a margin far above rounding, so hypot is
+      // evaluated only on the few cells that can be nearest or tie.
+      double smin = kInf;
+      for (int32_t b = 0; b < cy; ++b) {
+        const double dy = qy - ccy[b], dy2 = dy * dy;
+        for (int32_t a = 0; a < cx; ++a) {
+          const double dx = qx - ccx[a];
+          smin = std::min(smin, dx * dx + dy2);
+        }
+      }
+      const double R = std::sqrt(smin) * (1.0 + 1e-6) + 1e-9 * g.h, R2 = R * R;
+      cand.clear();
+      for (int32_t b = 0; b < cy; ++b) {
+        const double dy = qy - ccy[b], dy2 = dy * dy;
+        if (dy2 > R2) continue;
+        for (int32_t a = 0; a < cx; ++a) {
+          const double dx = qx - ccx[a];
+          if (dx * dx + dy2 <= R2) cand.push_back((int64_t)b * cx + a);
+        }
+      }
       double dmin = kInf;
-      for (int64_t c = 0; c < J; ++c) dmin = std::min(dmin, std::hypot(qx - ccx[c], qy - ccy[c]));
+      for (int64_t c : cand) dmin = std::min(dmin, std::hypot(qx - ccx[c % cx], qy - ccy[c / cx]));
       const double tie = 1e-12 * (g.h + dmin);
-      for (int64_t c = 0; c < J; ++c) {
-        const double dist = std::hypot(qx - ccx[c], qy - ccy[c]);
+      for (int64_t c : cand) {
+        const double dist = std::hypot(qx - ccx[c % cx], qy - ccy[c / cx]);
         if (dist > dmin + tie) continue;
         const double cost = single ? p->exit_point_cost[k] : p->exit_point_cost[k] + dist / Fc[c];
         best[c] = std::min(best[c], cost);
@@ -164,100 +211,130 @@ int fmsm_part1(const eik_problem* p, const eik_cells* cells, FmsmOrder* out) {
     const bool single = p->n_exit == 1;
     for (int64_t k = 0; k < p->n_exit; ++k) {
       const int64_t idx = p->exit_nodes[k], i = idx % g.m, j = idx / g.m;
-      int64_t a = 0, b = 0;  // cell_of_node (cells.cpp:23-30)
-      while (ie[a] <= i) ++a;
-      while (je[b] <= j) ++b;
+      // cell_of_node (cells.cpp:23-30): the last cell with begin <= node
+      const int64_t a = std::upper_bound(ib.begin(), ib.end(), i) - ib.begin() - 1;
+      const int64_t b = std::upper_bound(jb.begin(), jb.end(), j) - jb.begin() - 1;
       const int64_t c = b * cx + a;
-      const double dist = std::hypot(gx(i) - ccx[c], gy(j) - ccy[c]);
+      const double dist = std::hypot(gx(i) - ccx[a], gy(j) - ccy[b]);
       const double cost = single ? p->exit_cost[k] : p->exit_cost[k] + dist / Fc[c];
       best[c] = std::min(best[c], cost);
     }
   }
-  out->is_q.assign(J, 0);
-  std::vector<double> v(J, kInf);
-  std::vector<uint8_t> label(J, 0);  // 0 far, 1 considered, 2 accepted
-  std::vector<uint8_t> isx(J, 0);
-  int64_t nq = 0;
-  for (int64_t c = 0; c < J; ++c)
-    if (std::isfinite(best[c])) {
-      out->is_q[c] = 1;
-      isx[c] = 1;
-      v[c] = best[c];
-      label[c] = 2;
-      ++nq;
-    }
-  if (nq == 0) return 1;
 
   // coarse Fast March (classic_solvers.cpp:28-92) on the cx x cy lattice,
-  // spacing hc_x, speed = F at the actual cell centres
-  out->coarse_updates = 0;
-  out->coarse_pops = 0;
+  // spacing hc_x, speed = F at the actual cell centres.  The lattice is
+  // padded by one ring (value +inf, label accepted), so a neighbour outside
+  // the lattice reads +inf and is never updated: no bounds checks, no
+  // divisions.  Padded index p = (b + 1) * W + a + 1 orders like the cell id.
+  const int64_t W = (int64_t)cx + 2;
+  const int64_t NP = W * ((int64_t)cy + 2);
+  std::vector<double> v(NP, kInf), cc(NP, 0.0);
+  std::vector<uint8_t> label(NP, 2);  // 0 far, 1 considered, 2 accepted / exit / pad
+  out->is_q.assign(J, 0);
+  std::vector<int32_t> seq;  // acceptance sequence (cell ids): exits, then pops
+  seq.reserve(J);
+  for (int32_t b = 0; b < cy; ++b)
+    for (int32_t a = 0; a < cx; ++a) {
+      const int64_t c = (int64_t)b * cx + a, q = (b + 1) * W + a + 1;
+      cc[q] = hc_x / Fc[c];  // h_c / F, as quadrant_update computes it
+      if (std::isfinite(best[c])) {
+        out->is_q[c] = 1;
+        v[q] = best[c];
+        seq.push_back((int32_t)c);
+      } else {
+        label[q] = 0;
+      }
+    }
+  const int64_t nq = (int64_t)seq.size();
+  if (nq == 0) return 1;
+
+  int64_t updates = 0, pops = 0;
   Heap H;
-  const int di[4] = {1, -1, 0, 0}, dj[4] = {0, 0, 1, -1};
-  std::vector<double> cc(J);  // h_c / F per cell, as quadrant_update computes it
-  for (int64_t c = 0; c < J; ++c) cc[c] = hc_x / Fc[c];
-  auto update = [&](int64_t a, int64_t b) {
-    ++out->coarse_updates;
-    const double E = a + 1 < cx ? v[b * cx + a + 1] : kInf;
-    const double W = a - 1 >= 0 ? v[b * cx + a - 1] : kInf;
-    const double N = b + 1 < cy ? v[(b + 1) * cx + a] : kInf;
-    const double S = b - 1 >= 0 ? v[(b - 1) * cx + a] : kInf;
-    return quadrant_c(std::min(E, W), std::min(N, S), cc[b * cx + a]);
+  const int64_t off[4] = {1, -1, W, -W};  // E, W, N, S (di/dj of classic_solvers.cpp:38-39)
+  auto update = [&](int64_t q) {
+    ++updates;
+    return quadrant_c(std::min(v[q + 1], v[q - 1]), std::min(v[q + W], v[q - W]), cc[q]);
   };
-  for (int64_t c = 0; c < J; ++c) {
-    if (!isx[c]) continue;
-    const int64_t a = c % cx, b = c / cx;
+  for (int64_t k = 0; k < nq; ++k) {
+    const int64_t c = seq[k], q = (c / cx + 1) * W + c % cx + 1;
     for (int d = 0; d < 4; ++d) {
-      const int64_t na = a + di[d], nb = b + dj[d];
-      if (na < 0 || na >= cx || nb < 0 || nb >= cy) continue;
-      const int64_t nc = nb * cx + na;
-      if (label[nc] != 0) continue;
-      label[nc] = 1;
-      const double cand = update(na, nb);
-      if (cand < v[nc]) v[nc] = cand;
-      H.push((int32_t)nc, v[nc]);
+      const int64_t nqd = q + off[d];
+      if (label[nqd] != 0) continue;
+      label[nqd] = 1;
+      const double cand = update(nqd);
+      if (cand < v[nqd]) v[nqd] = cand;
+      H.push((int32_t)nqd, v[nqd]);
     }
   }
   while (!H.empty()) {
     double key;
     int32_t top;
     H.pop(key, top);
-    const int64_t c = top;
-    if (label[c] == 2 || key != v[c]) continue;  // superseded entry
-    ++out->coarse_pops;
-    label[c] = 2;
-    const int64_t a = c % cx, b = c / cx;
+    const int64_t q = top;
+    if (label[q] == 2 || key != v[q]) continue;  // superseded entry
+    ++pops;
+    label[q] = 2;
+    seq.push_back((int32_t)(q - W - 1 - 2 * (q / W - 1)));
     for (int d = 0; d < 4; ++d) {
-      const int64_t na = a + di[d], nb = b + dj[d];
-      if (na < 0 || na >= cx || nb < 0 || nb >= cy) continue;
-      const int64_t nc = nb * cx + na;
-      if (label[nc] == 2 || isx[nc]) continue;
-      const double cand = update(na, nb);
-      if (label[nc] == 0) {
-        label[nc] = 1;
-        if (cand < v[nc]) v[nc] = cand;
-        H.push((int32_t)nc, v[nc]);
-      } else if (cand < v[nc]) {
-        v[nc] = cand;
-        H.push((int32_t)nc, cand);
+      const int64_t nqd = q + off[d];
+      if (label[nqd] == 2) continue;
+      const double cand = update(nqd);
+      if (label[nqd] == 0) {
+        label[nqd] = 1;
+        if (cand < v[nqd]) v[nqd] = cand;
+        H.push((int32_t)nqd, v[nqd]);
+      } else if (cand < v[nqd]) {
+        v[nqd] = cand;
+        H.push((int32_t)nqd, cand);
       }
     }
   }
+  out->coarse_updates = updates;
+  out->coarse_pops = pops;
+  const int64_t nreached = (int64_t)seq.size();
+  for (int64_t c = 0; c < J && nreached < J; ++c)  // never reached: +inf, by id
+    if (label[(c / cx + 1) * W + c % cx + 1] == 0) seq.push_back((int32_t)c);
 
-  // quantised acceptance order (fmsm.cpp:138-160)
+  // quantised acceptance order (fmsm.cpp:138-160): sort by (floor(v /
+  // 1e-9 vmax), id).  (key, id) packed into one word: keys are <= 1e9 < 2^31
+  // (an unreached cell sorts last), ids < 2^31.  The acceptance sequence is
+  // already sorted up to near-ties and the exits' place, so an insertion
+  // sort with a move budget finishes it in O(J); past the budget, a radix
+  // sort.  Either way the result is the reference's stable sort.
+  std::vector<double> vc(J);  // values by cell id
   double vmax = hc_x;
-  for (int64_t c = 0; c < J; ++c)
-    if (std::isfinite(v[c])) vmax = std::max(vmax, v[c]);
+  for (int32_t b = 0; b < cy; ++b)
+    for (int32_t a = 0; a < cx; ++a) {
+      const double x = v[(b + 1) * W + a + 1];
+      vc[(int64_t)b * cx + a] = x;
+      if (std::isfinite(x)) vmax = std::max(vmax, x);
+    }
   const double quantum = 1e-9 * vmax;
-  // (key, id) packed into one word: keys are floor(v / (1e-9 vmax)) <= 1e9 <
-  // 2^31 (an unreached cell sorts last), ids < 2^31 -- a radix sort of the
-  // words is the reference's stable sort by key then id
   std::vector<uint64_t> kw(J);
-  for (int64_t c = 0; c < J; ++c) {
-    const uint64_t key = std::isfinite(v[c]) ? (uint64_t)std::floor(v[c] / quantum) : 0xFFFFFFFFull;
-    kw[c] = (key << 32) | (uint64_t)c;
+  for (int64_t r = 0; r < J; ++r) {
+    const int64_t c = seq[r];
+    const double x = vc[c];
+    const uint64_t key = std::isfinite(x) ? (uint64_t)std::floor(x / quantum) : 0xFFFFFFFFull;
+    kw[r] = (key << 32) | (uint64_t)c;
   }
-  radix_sort_u64(kw);
+  {
+    int64_t budget = 8 * J + 64;
+    bool ok = true;
+    for (int64_t r = 1; r < J && ok; ++r) {
+      const uint64_t x = kw[r];
+      int64_t s = r;
+      while (s > 0 && kw[s - 1] > x) {
+        kw[s] = kw[s - 1];
+        --s;
+        if (--budget < 0) {
+          ok = false;
+          break;
+        }
+      }
+      kw[s] = x;
+    }
+    if (!ok) radix_sort_u64(kw);
+  }
   out->order.resize(J);
   for (int64_t r = 0; r < J; ++r) out->order[r] = (int32_t)(kw[r] & 0xFFFFFFFFull);
   out->rank.resize(J);

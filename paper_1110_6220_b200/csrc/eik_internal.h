@@ -87,20 +87,32 @@ cudaError_t launch_fmsm(const FmsmArgs& a, int warps_per_cta, int max_ctas, cuda
                         int* launches, int* grid = nullptr);
 cudaError_t fmsm_capacity(int64_t tile_doubles, int warps_per_cta, int* ctas);
 
-// Result of processing one cell (sweeps + the four border scans), produced by
-// a worker speculatively and applied by the committer.
-// Laid out for the committer's loads: per side one double and one word, the
-// counters and instance number in one 16-byte vector.
+// Result of processing one cell (sweeps + the four border scans): the
+// per-warp staging copy in shared memory that process_cell fills.
 struct alignas(16) SpecRec {
   double cand[4];
   int sweeps, updates;
-  unsigned inst;            // instance number (written last)
+  unsigned inst;            // instance number
   unsigned tag;             // version of the cell the result is valid at
   unsigned side[4];         // per side: bit 0 add, bits 8-15 sweep flags, bit 16
                             // monotonicity checked, bit 24 single-direction
   unsigned dmask;           // chained: sides whose pending results it assumes
   unsigned dinst[4];        // ... and their instance numbers
-  unsigned nseq;            // instances written so far (busy holder only)
+  unsigned nseq;            // unused in the staging copy
+};
+
+// The published speculation record in global memory: eight 16-byte words,
+// each written and read as ONE single-copy-atomic 128-bit access (PTX
+// ld/st .b128).  Every word carries the instance number of the write it
+// belongs to, so a reader that loads the words it needs in one batch -- no
+// ordering between the loads -- knows they come from one complete write iff
+// their instance numbers agree.
+//   word d (0-3): cand[d] (f64 bits) | side[d] | inst
+//   word 4:       sweeps | updates | tag | inst
+//   word 5:       dmask | dinst[0] | dinst[1] | inst
+//   word 6:       dinst[2] | dinst[3] | nseq (writes so far) | inst
+struct alignas(128) PRec {
+  uint4 w[8];
 };
 
 struct HcArgs {
@@ -111,7 +123,7 @@ struct HcArgs {
   unsigned long long* state;  // [J] packed state word (k_heapcell.cu)
   unsigned* spec_ver;       // [2][J] tag of the plain / chained speculation
   int* busy;                // [2][J] a warp is computing that speculation
-  SpecRec* rec;             // [2][J]
+  PRec* rec;                // [2][J] published speculation records
   double* ckey;             // [J] heap key published for the workers (inf = not queued)
   unsigned* ctag;           // [J] instance number of the last committed result
   int chain;                // make chained speculations

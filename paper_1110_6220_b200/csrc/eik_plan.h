@@ -86,7 +86,7 @@ struct eik_plan {
   double* dSlots = nullptr;
   unsigned* dSpecVer = nullptr;
   int* dBusy = nullptr;
-  eikb200::SpecRec* dRec = nullptr;
+  eikb200::PRec* dRec = nullptr;
   int* dHcMisc = nullptr;
   // HCM band scheduler (k_heapcell.cu hcm_band_kernel)
   bool hcm_band = false;    // HCM plan runs the band scheduler (else the exact replay)
@@ -118,6 +118,13 @@ struct eik_plan {
   double init_sync_ms = 0.0;  // creation: wait for the uploads (diagnostics)      // a run completed (the resident field is a solution)  // device + host ms of the last run (batch admission order)
   // batch runs: called (then cleared) once the heap-cell grid is submitted
   std::function<void()> on_launched;
+  // FMSM Part I computed ahead of the run (plan_prepare_host, called by the
+  // batch paths before a plan waits for its SMs); consumed by the next run
+  bool fmsm_ready = false;
+  std::vector<int32_t> fmsm_order, fmsm_rank;
+  std::vector<uint8_t> fmsm_flags;
+  int64_t fmsm_coarse_pops = 0, fmsm_coarse_updates = 0;
+  double fmsm_host_ms = 0.0;
 };
 
 namespace eikb200 {
@@ -143,7 +150,7 @@ struct Knobs {
   int hc_idle_ns = 200;            // EIK_HC_IDLE_NS
   int hc_skip_from = 1;            // EIK_HC_SKIP_FROM
   // batches
-  double batch_sms_scale = 2.0;    // EIK_BATCH_SMS_SCALE
+  double batch_sms_scale = 0.0;    // EIK_BATCH_SMS_SCALE (0 = by the batch size)
   int batch_fmsm_ctas = 16;        // EIK_BATCH_FMSM_CTAS
   double batch_fmsm_prio = 0.5;    // EIK_BATCH_FMSM_PRIO
   int batch_fixed_per_sm = 0;      // EIK_BATCH_FIXED_PER_SM
@@ -215,5 +222,9 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c);
 int plan_capacity(eik_plan* P, int* device, int* fixed);
 int plan_run_fmsm(eik_plan* P, eik_output* out);
 int plan_run_heapcell(eik_plan* P, eik_output* out);
+// Host-side work of the next run that needs no device (FMSM Part I): the
+// batch paths call it before a plan waits for SMs, so no SM is held idle
+// while the host computes.  A no-op for the other methods.
+int plan_prepare_host(eik_plan* P);
 
 }  // namespace eikb200

@@ -264,7 +264,8 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
   return EIK_OK;
 }
 
-int plan_run_fmsm(eik_plan* P, eik_output* out) {
+int plan_prepare_host(eik_plan* P) {
+  if (P->method != EIK_FMSM || P->fmsm_ready) return EIK_OK;
   using clk = std::chrono::steady_clock;
   const int64_t J = (int64_t)P->cells_x * P->cells_y;
   // ---- Part I on the host (the reference's own split, fmsm.cpp:130-162) --
@@ -283,30 +284,46 @@ int plan_run_fmsm(eik_plan* P, eik_output* out) {
   hc.center_speed = P->center_speed.data();
   FmsmOrder ord;
   if (fmsm_part1(&hp, &hc, &ord)) return fail(EIK_ERR_CONFIG, "fmsm: empty coarse exit set");
-  std::vector<uint8_t> flags(J);
-  for (int64_t cell = 0; cell < J; ++cell) {
-    if (ord.is_q[cell]) {
-      flags[cell] = 16;
-      continue;
+  std::vector<uint8_t>& flags = P->fmsm_flags;
+  flags.resize(J);
+  const int32_t* rank = ord.rank.data();
+  for (int64_t cy = 0, cell = 0; cy < P->cells_y; ++cy)
+    for (int64_t cx = 0; cx < P->cells_x; ++cx, ++cell) {
+      if (ord.is_q[cell]) {
+        flags[cell] = 16;
+        continue;
+      }
+      const int32_t r = rank[cell];
+      const bool w = cx > 0 && rank[cell - 1] < r;
+      const bool e = cx + 1 < P->cells_x && rank[cell + 1] < r;
+      const bool s = cy > 0 && rank[cell - P->cells_x] < r;
+      const bool n = cy + 1 < P->cells_y && rank[cell + P->cells_x] < r;
+      flags[cell] = fmsm_dir_mask(w, e, s, n);
     }
-    const int64_t cx = cell % P->cells_x, cy = cell / P->cells_x;
-    const int32_t r = ord.rank[cell];
-    const bool w = cx > 0 && ord.rank[cell - 1] < r;
-    const bool e = cx + 1 < P->cells_x && ord.rank[cell + 1] < r;
-    const bool s = cy > 0 && ord.rank[cell - P->cells_x] < r;
-    const bool n = cy + 1 < P->cells_y && ord.rank[cell + P->cells_x] < r;
-    flags[cell] = fmsm_dir_mask(w, e, s, n);
-  }
-  const double host_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+  P->fmsm_order = std::move(ord.order);
+  P->fmsm_rank = std::move(ord.rank);
+  P->fmsm_coarse_pops = ord.coarse_pops;
+  P->fmsm_coarse_updates = ord.coarse_updates;
+  P->fmsm_host_ms = std::chrono::duration<double, std::milli>(clk::now() - t0).count();
+  P->fmsm_ready = true;
+  return EIK_OK;
+}
+
+int plan_run_fmsm(eik_plan* P, eik_output* out) {
+  const int64_t J = (int64_t)P->cells_x * P->cells_y;
+  int rc0 = plan_prepare_host(P);
+  if (rc0) return rc0;
+  P->fmsm_ready = false;  // every run computes its own Part I
+  const double host_ms = P->fmsm_host_ms;
 
   // ---- Part II on the device -------------------------------------------
   int launches = 0;
   CK(cudaEventRecord(P->ev0, P->stream));
-  CK(cudaMemcpyAsync(P->dOrder, ord.order.data(), sizeof(int32_t) * J, cudaMemcpyHostToDevice,
+  CK(cudaMemcpyAsync(P->dOrder, P->fmsm_order.data(), sizeof(int32_t) * J,
+                     cudaMemcpyHostToDevice, P->stream));
+  CK(cudaMemcpyAsync(P->dRank, P->fmsm_rank.data(), sizeof(int32_t) * J, cudaMemcpyHostToDevice,
                      P->stream));
-  CK(cudaMemcpyAsync(P->dRank, ord.rank.data(), sizeof(int32_t) * J, cudaMemcpyHostToDevice,
-                     P->stream));
-  CK(cudaMemcpyAsync(P->dFlags, flags.data(), J, cudaMemcpyHostToDevice, P->stream));
+  CK(cudaMemcpyAsync(P->dFlags, P->fmsm_flags.data(), J, cudaMemcpyHostToDevice, P->stream));
   CK(cudaMemsetAsync(P->dCellDone, 0, sizeof(int) * J, P->stream));
   CK(cudaMemsetAsync(P->dNext, 0, sizeof(int) * 4, P->stream));
   CK(cudaMemsetAsync(P->dCounters, 0, sizeof(unsigned long long) * 8, P->stream));
@@ -343,8 +360,8 @@ int plan_run_fmsm(eik_plan* P, eik_output* out) {
   // counters: sweeps are fine-pass cell sweeps; removals/updates include the
   // coarse Fast March's (fmsm.cpp:173-174)
   out->sweeps = (int64_t)cnt[0];
-  out->node_updates = ord.coarse_updates + (int64_t)cnt[1];
-  out->heap_removals = ord.coarse_pops;
+  out->node_updates = P->fmsm_coarse_updates + (int64_t)cnt[1];
+  out->heap_removals = P->fmsm_coarse_pops;
   out->cell_sweeps = out->sweeps;
   out->avs = (double)out->sweeps / (double)J;
   out->device_ms = ms;

@@ -118,6 +118,44 @@ __device__ __forceinline__ int ld_relaxed_s32(const int* p) {
 __device__ __forceinline__ bool tag_is(unsigned sv, unsigned v) {
   return sv != kSpecNone && (sv & kTagMask) == v;
 }
+// Instance numbers: workers' writes (nseq << 1 | kind) below bit 23, the
+// committer's own processings kSelfInst | removal count -- unique per cell,
+// so a chained speculation built on a worker's result never matches a
+// processing the committer did itself.
+constexpr unsigned kInstMask = 0x7FFFFFu;
+constexpr unsigned kSelfInst = 0x800000u;
+// 128-bit single-copy-atomic accesses to the record words (PRec)
+__device__ __forceinline__ uint4 mk4(unsigned long long a, unsigned long long b) {
+  return make_uint4((unsigned)a, (unsigned)(a >> 32), (unsigned)b, (unsigned)(b >> 32));
+}
+__device__ __forceinline__ uint4 ld_w128(const uint4* p) {
+  unsigned long long a, b;
+  asm volatile("{ .reg .b128 t; ld.relaxed.gpu.global.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
+               : "=l"(a), "=l"(b) : "l"(p) : "memory");
+  return mk4(a, b);
+}
+// without the compiler memory barrier: independent loads issue together
+__device__ __forceinline__ uint4 ld_w128_nb(const uint4* p) {
+  unsigned long long a, b;
+  asm volatile("{ .reg .b128 t; ld.relaxed.gpu.global.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
+               : "=l"(a), "=l"(b) : "l"(p));
+  return mk4(a, b);
+}
+__device__ __forceinline__ uint4 ld_acquire_w128(const uint4* p) {
+  unsigned long long a, b;
+  asm volatile("{ .reg .b128 t; ld.acquire.gpu.global.b128 t, [%2]; mov.b128 {%0, %1}, t; }"
+               : "=l"(a), "=l"(b) : "l"(p) : "memory");
+  return mk4(a, b);
+}
+__device__ __forceinline__ void st_w128(uint4* p, uint4 v) {
+  const unsigned long long a = ((unsigned long long)v.y << 32) | v.x;
+  const unsigned long long b = ((unsigned long long)v.w << 32) | v.z;
+  asm volatile("{ .reg .b128 t; mov.b128 t, {%1, %2}; st.relaxed.gpu.global.b128 [%0], t; }"
+               ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ double w_cand(uint4 w) {
+  return __hiloint2double((int)w.y, (int)w.x);
+}
 // named barriers between the committer (warp 0) and its queue helper (warp 1)
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
@@ -424,7 +462,7 @@ __device__ __forceinline__ void hc_cell_rect(const CellGeom& g, u64 magic, int c
 __device__ __forceinline__ double* slot_ptr(const HcArgs& a, int s, int cell) {
   return a.slots + ((size_t)s * a.J + cell) * a.cellsz;
 }
-__device__ __forceinline__ SpecRec* rec_ptr(const HcArgs& a, int kind, int cell) {
+__device__ __forceinline__ PRec* rec_ptr(const HcArgs& a, int kind, int cell) {
   return a.rec + (size_t)kind * a.J + cell;
 }
 
@@ -434,9 +472,9 @@ __device__ __forceinline__ SpecRec* rec_ptr(const HcArgs& a, int kind, int cell)
 // come from slot oslot[side] (the pending results a chained speculation
 // builds on, whose scans add `cflags` to the cell's flags) -- then sweep,
 // scan and write the record (all fields but the instance number and tags).
-__device__ __forceinline__ void process_cell(const HcArgs& a, HTile& T, double* before, int cell, int kind, u64 st,
-                             unsigned omask, const int oslot[4], unsigned cflags, int lane,
-                             long long* prof = nullptr) {
+__device__ __forceinline__ void process_cell(const HcArgs& a, HTile& T, double* before, SpecRec* stg,
+                             int cell, int kind, u64 st, unsigned omask, const int oslot[4],
+                             unsigned cflags, int lane, long long* prof = nullptr) {
   const long long p0 = prof ? clock64() : 0;
   const CellGeom& g = a.g;
   int64_t ib, ie, jb, je;
@@ -569,14 +607,13 @@ __device__ __forceinline__ void process_cell(const HcArgs& a, HTile& T, double* 
     const int y = k / T.w, x = k % T.w;
     spare[y * mw + x] = T.u(x, y);
   }
-  SpecRec* rec = rec_ptr(a, kind, cell);
   scan_all(a, T, before, pstrip, first_removal,
            (has_nb[0] ? 1u : 0u) | (has_nb[1] ? 2u : 0u) | (has_nb[2] ? 4u : 0u) |
                (has_nb[3] ? 8u : 0u),
-           rec, lane);
+           stg, lane);
   if (lane == 0) {
-    rec->sweeps = (int)nsw;
-    rec->updates = (int)upd;
+    stg->sweeps = (int)nsw;
+    stg->updates = (int)upd;
   }
   if (prof) {
     prof[4] += p1b - p1;                        // reset_locks
@@ -589,26 +626,26 @@ __device__ __forceinline__ void process_cell(const HcArgs& a, HTile& T, double* 
 }
 
 // Publish the result process_cell just wrote (all lanes call; lane 0 writes):
-// tag, assumed instances and instance number, then the speculation word, then
-// free the cell.  A chained result assuming |A| commits is valid at version
-// (read version + |A|).
+// the record words from the staging copy, each stamped with a fresh instance
+// number, then the speculation tag, then free the cell.  A chained result
+// assuming |A| commits is valid at version (read version + |A|).
 __device__ void publish(const HcArgs& a, int cell, int kind, u64 st, unsigned dmask,
-                        const unsigned dinst[4], int lane) {
-  SpecRec* rec = rec_ptr(a, kind, cell);
+                        const unsigned dinst[4], const SpecRec* stg, int lane) {
+  PRec* rec = rec_ptr(a, kind, cell);
   const unsigned tag = (st_ver(st) + (unsigned)__popc(dmask)) & kTagMask;
-  unsigned inst = 0;
-  if (lane == 0) {
-    const unsigned n = __ldcg(&rec->nseq) + 1u;  // only the busy holder writes it
-    rec->nseq = n;
-    inst = ((n << 1) | (unsigned)kind) & kTagMask;
-    rec->tag = tag;
-    rec->dmask = dmask;
-    for (int d = 0; d < 4; ++d) rec->dinst[d] = dinst[d];
-  }
-  __threadfence();  // values, record, tag before the instance number
+  __threadfence();  // the slot values (every lane's stores) before the record
   __syncwarp();
   if (lane == 0) {
-    st_relaxed_u32(&rec->inst, inst);
+    const unsigned n = ld_w128(&rec->w[6]).z + 1u;  // writes so far (busy holder only)
+    const unsigned inst = ((n << 1) | (unsigned)kind) & kInstMask;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      const unsigned long long cb = (unsigned long long)__double_as_longlong(stg->cand[d]);
+      st_w128(&rec->w[d], make_uint4((unsigned)cb, (unsigned)(cb >> 32), stg->side[d], inst));
+    }
+    st_w128(&rec->w[4], make_uint4((unsigned)stg->sweeps, (unsigned)stg->updates, tag, inst));
+    st_w128(&rec->w[5], make_uint4(dmask, dinst[0], dinst[1], inst));
+    st_w128(&rec->w[6], make_uint4(dinst[2], dinst[3], n, inst));
     st_release_u32(a.spec_ver + (size_t)kind * a.J + cell, tag);
     if (a.wdbg) a.owner[(size_t)kind * a.J + cell] = 0x60000 | kind;
     st_release_s32(a.busy + (size_t)kind * a.J + cell, 0);
@@ -620,7 +657,8 @@ __device__ void publish(const HcArgs& a, int cell, int kind, u64 st, unsigned dm
 // of the production instantiation, where those ~25 live counters would cost
 // registers the hot path needs.
 template <bool PROF>
-__device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before, int lane) {
+__device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before, SpecRec* stg,
+                          int lane) {
   const CellGeom& g = a.g;
   bool ovf = false;  // a bucket filled up (per lane; voted once per pop)
   if (lane == 0) {
@@ -681,20 +719,20 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     // obtain a valid result: the plain speculation if its tag is the current
     // version, else the chained one if its tag is the current version and
     // every neighbour it assumed last committed the instance it read, else
-    // process the cell here.  Polls are relaxed (an acquire would flush
-    // this SM's L1); the record is then read through an address that depends
-    // on the observed tag, so it cannot be read early.
-    int mode = 0, kind = 0, dep = 0;  // mode 0: valid speculation, 1: process here
+    // process the cell here.  The records are read word by word (128-bit
+    // single-copy-atomic loads, one batch): lanes 0-4 the plain record's
+    // words 0-4, lanes 8-14 the chained one's words 0-6; a record is whole
+    // iff its words carry one instance number, so the tags, the scans and
+    // the counters arrive in ONE round trip.  Polls are relaxed (an acquire
+    // would flush this SM's L1).
+    int mode = 0, kind = 0;  // mode 0: valid speculation, 1: process here
     u64 st = 0;
-    // the commit's loads that do not depend on the speculation (only this
-    // warp writes these words) go out with the first poll
     // lanes 0-3 load side `lane`: the neighbour's state, cell value, queue
     // position and committed instance (only this warp writes those words)
     u64 my_nst = 0ull;
     double my_cv = kInf;
     int my_pos = -1;
     unsigned my_ctag = kSpecNone;
-    unsigned svp0 = 0, svc0 = 0;
     if (lane < 4 && nbs[lane < 4 ? lane : 0] >= 0) {
       const int nb = nbs[lane];
       my_nst = ld_relaxed_u64_nb(a.state + nb);
@@ -703,8 +741,11 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       my_ctag = __ldcg(a.ctag + nb);
     }
     st = ld_relaxed_u64_nb(a.state + cell);  // every lane: one warp-wide load each
-    svp0 = ld_relaxed_u32_nb(spec_p + cell);
-    svc0 = ld_relaxed_u32_nb(spec_c + cell);
+    const int wkind = lane >> 3, wi = lane & 7;  // record word this lane reads
+    const bool wlane = (wkind == 0 && wi < 5) || (wkind == 1 && wi < 7);
+    const uint4* wptr = &rec_ptr(a, wkind & 1, cell)->w[wi < 7 ? wi : 0];
+    uint4 rw = make_uint4(0u, 0u, 0u, kSpecNone);
+    if (wlane) rw = ld_w128_nb(wptr);
     // hand the pop to the helper only now: the barrier waits for this warp's
     // earlier memory operations, and the loads above are then already in flight
     if (helper) {
@@ -725,44 +766,37 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     }
     const long long t1a = PROF ? clock64() : 0;
     if (PROF) cyc_rescan += t1a - t1;
-    // every lane validates (the same words, each read by one warp-wide load,
-    // so the lanes agree without a broadcast); lane 0 alone claims
+    // every lane validates from the shuffled words; lane 0 alone claims
     {
       const unsigned v = st_ver(st);
       long long spins = 0;
       bool waited = false;
-      bool first = true;
-      const unsigned vchk = v;  // first use of the loaded state word
       long long tw0 = 0;
       if (PROF) {
         tw0 = clock64();
-        cyc_rt1 += (vchk == 0xFFFFFFFFu ? 1 : 0) + tw0 - t1a;
+        cyc_rt1 += (v == 0xFFFFFFFFu ? 1 : 0) + tw0 - t1a;
       }
+      // the chained record's assumed instances against the neighbours'
+      // committed ones (lanes 0-3 hold those)
+      const unsigned ctg0 = __shfl_sync(kFull, my_ctag, 0), ctg1 = __shfl_sync(kFull, my_ctag, 1);
+      const unsigned ctg2 = __shfl_sync(kFull, my_ctag, 2), ctg3 = __shfl_sync(kFull, my_ctag, 3);
       for (;;) {
-        const unsigned svp = first ? svp0 : ld_relaxed_u32_nb(spec_p + cell);
-        const unsigned svc = first ? svc0 : ld_relaxed_u32_nb(spec_c + cell);
-        first = false;
-        if (tag_is(svp, v)) {
-          unsigned d;
-          asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(svp));
-          dep = (int)((d & kTagMask) - v);  // == 0, but the compiler cannot know
+        // plain: words 0-4 on lanes 0-4; chained: words 0-6 on lanes 8-14
+        const unsigned ip = __shfl_sync(kFull, rw.w, 4), tp = __shfl_sync(kFull, rw.z, 4);
+        const unsigned ic = __shfl_sync(kFull, rw.w, 12), tc = __shfl_sync(kFull, rw.z, 12);
+        const bool whole_lane = !wlane || rw.w == (wkind == 0 ? ip : ic);
+        const unsigned bad = __ballot_sync(kFull, !whole_lane);
+        if ((bad & 0xFFu) == 0u && ip != kSpecNone && tag_is(tp, v)) {
           kind = 0;
           break;
         }
-        if (tag_is(svc, v)) {
-          unsigned d;
-          asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(svc));
-          const int dd = (int)((d & kTagMask) - v);
-          const SpecRec* r1 = rec_ptr(a, 1, cell + dd);
-          const unsigned dm = __ldcg(&r1->dmask);
-          bool ok = true;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const unsigned ctk = __shfl_sync(kFull, my_ctag, k);
-            if ((dm >> k) & 1u) ok = ok && __ldcg(&r1->dinst[k]) == ctk;
-          }
+        if ((bad & 0xFF00u) == 0u && ic != kSpecNone && tag_is(tc, v)) {
+          const unsigned dm = __shfl_sync(kFull, rw.x, 13);
+          const unsigned d0 = __shfl_sync(kFull, rw.y, 13), d1 = __shfl_sync(kFull, rw.z, 13);
+          const unsigned d2 = __shfl_sync(kFull, rw.x, 14), d3 = __shfl_sync(kFull, rw.y, 14);
+          const bool ok = (!(dm & 1u) || d0 == ctg0) && (!(dm & 2u) || d1 == ctg1) &&
+                          (!(dm & 4u) || d2 == ctg2) && (!(dm & 8u) || d3 == ctg3);
           if (ok) {
-            dep = dd;
             kind = 1;
             ++chain_hits;
             break;
@@ -772,17 +806,18 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
         if (lane == 0) got = atomicCAS(a.busy + cell, 0, 1) == 0 ? 1 : 0;
         if (__shfl_sync(kFull, got, 0)) {
           if (lane == 0 && a.wdbg) a.owner[cell] = 0x30000;
-          unsigned sv2 = 0;
-          if (lane == 0) sv2 = ld_relaxed_u32(spec_p + cell);
-          sv2 = __shfl_sync(kFull, sv2, 0);
-          if (tag_is(sv2, v)) {
+          // a worker may have published since the loads above: re-read the
+          // plain record under the busy flag (no writer can start now)
+          uint4 pw = make_uint4(0u, 0u, 0u, kSpecNone);
+          if (lane < 5) pw = ld_w128(&rec_ptr(a, 0, cell)->w[lane]);
+          const unsigned ip2 = __shfl_sync(kFull, pw.w, 4), tp2 = __shfl_sync(kFull, pw.z, 4);
+          const bool whole2 = (__ballot_sync(kFull, lane < 5 && pw.w != ip2) == 0u);
+          if (whole2 && ip2 != kSpecNone && tag_is(tp2, v)) {
             if (lane == 0) {
               if (a.wdbg) a.owner[cell] = 0x40000;
               st_release_s32(a.busy + cell, 0);
             }
-            unsigned d;
-            asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(sv2));
-            dep = (int)((d & kTagMask) - v);
+            if (lane < 8) rw = pw;
             kind = 0;
           } else {
             mode = 1;
@@ -838,6 +873,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
           mode = 2;
           break;
         }
+        if (wlane) rw = ld_w128(wptr);  // poll both records again
       }
       if (mode == 0) ++fast_hits;
       if (waited) ++waits;
@@ -846,48 +882,70 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     long long t2 = PROF ? clock64() : 0;
     if (PROF) cyc_obtain += t2 - t1;
     if (mode == 2) break;
+    // the result to commit: side d's scan on lane d, counters on lane 0
+    double rcand = kInf;
+    unsigned rside = 0u, rinst = 0u;
+    int rsweeps = 0, rupdates = 0;
     if (mode == 1) {
+      // processed here: the scans stay in the staging record (shared
+      // memory), the values go to the plain slot, made visible before the
+      // commit's state words; no record is published and the instance is
+      // the committer's own (kSelfInst | removal count)
       const int none[4] = {0, 0, 0, 0};
-      const unsigned noinst[4] = {0, 0, 0, 0};
-      process_cell(a, T, before, cell, 0, st, 0u, none, 0u, lane, PROF ? prof : nullptr);
-      publish(a, cell, 0, st, 0u, noinst, lane);
+      process_cell(a, T, before, stg, cell, 0, st, 0u, none, 0u, lane, PROF ? prof : nullptr);
+      __threadfence();
+      __syncwarp();
+      if (lane < 4) {
+        rcand = stg->cand[lane];
+        rside = stg->side[lane];
+      }
+      rsweeps = stg->sweeps;
+      rupdates = stg->updates;
+      rinst = kSelfInst | ((unsigned)removals & kInstMask);
+      if (lane == 0) {
+        if (a.wdbg) a.owner[cell] = 0x60000;
+        st_release_s32(a.busy + cell, 0);
+      }
       kind = 0;
       ++self_processed;
+    } else {
+      const int src = kind ? lane + 8 : lane;  // word `lane` of the chosen record
+      const unsigned x = __shfl_sync(kFull, rw.x, src & 31), y = __shfl_sync(kFull, rw.y, src & 31);
+      const unsigned z = __shfl_sync(kFull, rw.z, src & 31);
+      const int s4 = kind ? 12 : 4;
+      rsweeps = (int)__shfl_sync(kFull, rw.x, s4);
+      rupdates = (int)__shfl_sync(kFull, rw.y, s4);
+      rinst = __shfl_sync(kFull, rw.w, s4);
+      if (lane < 4) {
+        rcand = __hiloint2double((int)y, (int)x);
+        rside = z;
+      }
     }
     long long t3 = PROF ? clock64() : 0;
     if (PROF) cyc_self += t3 - t2;
     // commit: the popped cell on lane 0, its four neighbours on lanes 0-3 at
     // once (their queue buckets differ); every load before the first update
     {
-      const SpecRec* rec = rec_ptr(a, kind, cell + dep);
       const int cur = st_cur(st), ps = st_pslot(st), qs = 3 - cur - ps;
       const int ncur = kind ? qs : ps, nps = kind ? ps : cur;
       int ins = 0;
       if (lane < 4) {
         const int d = lane, nb = nbs[d];
-        const double cand = __ldcg(&rec->cand[d]);
-        const unsigned sw = __ldcg(&rec->side[d]);
-        int rsweeps = 0, rupdates = 0;
-        unsigned inst = 0;
-        if (d == 0) {
-          const int4 ctr = __ldcg(reinterpret_cast<const int4*>(&rec->sweeps));
-          rsweeps = ctr.x;
-          rupdates = ctr.y;
-          inst = (unsigned)ctr.z;
-        }
+        const double cand = rcand;
+        const unsigned sw = rside;
         const unsigned add = sw & 1u, fl = (sw >> 8) & 0xFFu;
         const unsigned mc = (sw >> 16) & 1u, ms = sw >> 24;
         if (d == 0) {
           sweeps += rsweeps;
           updates += rupdates;
-          if (PROF) cyc_rec += clock64() - t3;  // the record has arrived
+          if (PROF) cyc_rec += clock64() - t3;
           // popped cell: flags cleared, first removal done, the committed
           // kind's slot becomes current and the old current slot takes its
           // role, +1 version
           const unsigned lo =
               (((unsigned)st & ~(15u | (3u << 5))) | 16u | ((unsigned)ncur << 5)) + kVerOne;
           st_relaxed_u64(a.state + cell, (u64)lo | (st & (0xFFull << 34)) | ((u64)nps << 32));
-          a.ctag[cell] = inst;
+          a.ctag[cell] = rinst;
         }
         if (nb >= 0) {  // heap_cell.cpp:288-311
           bool moved = false;
@@ -1018,15 +1076,18 @@ __device__ __forceinline__ void cell_nbs(const HcArgs& a, int cell, int nbs[4]) 
 // holds x's chained busy flag (the record is then stable).
 __device__ bool chain_dead(const HcArgs& a, int x, unsigned svc, u64 st, const int nbx[4]) {
   if (svc == kSpecNone) return true;
-  const SpecRec* r = rec_ptr(a, 1, x);
-  const unsigned dm = __ldcg(&r->dmask);
+  const PRec* r = rec_ptr(a, 1, x);
+  const uint4 w5 = ld_w128(&r->w[5]), w6 = ld_w128(&r->w[6]);
+  if (w5.w != w6.w) return false;  // being rewritten (only without x's busy flag)
+  const unsigned dm = w5.x;
+  const unsigned di[4] = {w5.y, w5.z, w6.x, w6.y};
   const unsigned n = (unsigned)__popc(dm);
   const unsigned k = (st_ver(st) - (((svc & kTagMask) - n) & kTagMask)) & kTagMask;
   if (k > n) return true;
   unsigned c = 0;
 #pragma unroll
   for (int d = 0; d < 4; ++d)
-    if ((dm >> d) & 1u) c += __ldcg(a.ctag + nbx[d]) == __ldcg(&r->dinst[d]) ? 1u : 0u;
+    if ((dm >> d) & 1u) c += __ldcg(a.ctag + nbx[d]) == di[d] ? 1u : 0u;
   return k > c;
 }
 
@@ -1072,16 +1133,18 @@ __device__ bool claim_chain(const HcArgs& a, int x, const int nbx[4], unsigned a
       ok = false;
       break;
     }
-    const SpecRec* ry = rec_ptr(a, yk, y);
-    const unsigned inst = ld_acquire_u32(&ry->inst);
+    const PRec* ry = rec_ptr(a, yk, y);
+    const uint4 w4 = ld_acquire_w128(&ry->w[4]);  // instance and tag of one write
+    const unsigned inst = w4.w;
     const u64 sty = ld_relaxed_u64(a.state + y);
-    const unsigned ahead = (__ldcg(&ry->tag) - st_ver(sty)) & kTagMask;
-    if (inst == kSpecNone || ahead > 4) {
+    const unsigned ahead = (w4.z - st_ver(sty)) & kTagMask;
+    const int xside_of_y = d ^ 1;
+    const uint4 wsd = ld_w128(&ry->w[xside_of_y]);
+    if (inst == kSpecNone || ahead > 4 || wsd.w != inst) {
       ok = false;
       break;
     }
-    const int xside_of_y = d ^ 1;
-    const unsigned sw = __ldcg(&ry->side[xside_of_y]);
+    const unsigned sw = wsd.z;
     if (sw & 1u) j.cflags |= (sw >> 8) & 0xFFu;
     j.oslot[d] = kind_slot(sty, yk);
     j.dinst[d] = inst;
@@ -1168,12 +1231,13 @@ __device__ bool pick_job(const HcArgs& a, int pidx, Job& j, int wid) {
   // 2. neighbours that the commit of this cell's result queues or moves up
   const int ck = pick_kind(a, cell, st);
   if (ck < 0) return false;
-  const SpecRec* rc = rec_ptr(a, ck, cell);
+  const PRec* rc = rec_ptr(a, ck, cell);
   for (int d = 0; d < 4; ++d) {
     const int x = nbs[d];
     if (x < 0) continue;
-    const double cand = __ldcg(&rc->cand[d]);
-    if (!(__ldcg(&rc->side[d]) & 1u) && !(cand < knb[d])) continue;
+    const uint4 wd = ld_w128(&rc->w[d]);
+    const double cand = w_cand(wd);
+    if (!(wd.z & 1u) && !(cand < knb[d])) continue;
     const double kx = cand < knb[d] ? cand : knb[d];  // x's key after this commit
     int nbx[4];
     cell_nbs(a, x, nbx);
@@ -1206,7 +1270,9 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
   T.U = smem + (size_t)wib * a.tile_doubles;
   T.Ct = T.U + (size_t)(g.max_h + 2) * g.pu;
   double* before = T.Ct + (size_t)(g.max_h + 2) * g.pu;  // [4][max_len]
-  T.lock = reinterpret_cast<uint8_t*>(before + 8 * a.max_len);  // [4] snapshots + [4] probes
+  // [4] snapshots + [4] probes, then the staging record (128 bytes), then locks
+  SpecRec* stg = reinterpret_cast<SpecRec*>(before + 8 * a.max_len);
+  T.lock = reinterpret_cast<uint8_t*>(before + 8 * a.max_len + 16);
 
   // The committer runs alone in CTA 0: every gpu-scope acquire issued on an
   // SM invalidates that SM's L1 (CCTL.IVALL).  Workers poll with relaxed
@@ -1246,7 +1312,7 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
     H.cnt[lane] = 0;
     H.pubcnt[32 * lane] = 0;
     __syncwarp();
-    committer<PROF>(a, H, T, before, lane);
+    committer<PROF>(a, H, T, before, stg, lane);
     return;
   }
 
@@ -1296,9 +1362,9 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
         j.dinst[d] = __shfl_sync(kFull, j.dinst[d], 0);
       }
       if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 13;
-      process_cell(a, T, before, j.cell, j.kind, j.st, j.omask, j.oslot, j.cflags, lane);
+      process_cell(a, T, before, stg, j.cell, j.kind, j.st, j.omask, j.oslot, j.cflags, lane);
       if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 2;
-      publish(a, j.cell, j.kind, j.st, j.omask, j.dinst, lane);
+      publish(a, j.cell, j.kind, j.st, j.omask, j.dinst, stg, lane);
       if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 3;
       worked = true;
       break;
@@ -1325,11 +1391,10 @@ __global__ void heapcell_init_kernel(HcArgs a) {
       for (int kind = 0; kind < 2; ++kind) {
         a.spec_ver[(size_t)kind * a.J + cell] = kSpecNone;
         a.busy[(size_t)kind * a.J + cell] = 0;
-        SpecRec* rec = rec_ptr(a, kind, cell);
-        rec->inst = kSpecNone;
-        rec->nseq = 0;
-        rec->tag = kSpecNone;
-        rec->dmask = 0;
+        PRec* rec = rec_ptr(a, kind, cell);
+        const uint4 none = make_uint4(0u, 0u, 0u, kSpecNone);
+        for (int w = 0; w < 8; ++w) rec->w[w] = none;
+        rec->w[4].z = kSpecNone;  // tag
       }
       a.ckey[cell] = kInf;
       a.ctag[cell] = kSpecNone;
@@ -1794,7 +1859,7 @@ __global__ void __launch_bounds__(32) heapcell_serial_kernel(HcArgs a) {
 }  // namespace
 
 size_t heapcell_smem_bytes(const CellGeom& g, int max_len) {
-  return sizeof(double) * (2 * (size_t)(g.max_h + 2) * g.pu + 8 * (size_t)max_len) +
+  return sizeof(double) * (2 * (size_t)(g.max_h + 2) * g.pu + 8 * (size_t)max_len + 16) +
          (((size_t)g.max_w * g.max_h + 7) & ~(size_t)7);
 }
 

@@ -1,0 +1,4 @@
+for cs in 8 16 32; do
+  timeout 120 python scripts/one_solve.py c2 fhcm $cs 3
+  EIK_HC_PROFILE=1 timeout 120 python scripts/one_solve.py c2 fhcm $cs 1
+done
