@@ -482,7 +482,14 @@ def main():
                       _F=pinned_F)
     pinned_u = [torch.empty(M, dtype=torch.float64, pin_memory=True).numpy()
                 for _ in range(K * len(rows))]
-    jobs = [(p_pin, meth, cells_of.get(cs), tables.get(cs)) for meth, cs in rows] * K
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True).numpy()
+        t[...] = a
+        return t
+    tables_pin = {cs: E.CellTables(*[pinned(x) for x in (tb.probe_w, tb.probe_e, tb.probe_s,
+                                                         tb.probe_n, tb.center)])
+                  for cs, tb in tables.items()}
+    jobs = [(p_pin, meth, cells_of.get(cs), tables_pin.get(cs)) for meth, cs in rows] * K
     h2d = d2h = 0
     for meth, cs in rows:
         h2d += 8 * M + 16 * len(p.exit_nodes)

@@ -97,6 +97,15 @@ double now_ms_host() {
              std::chrono::steady_clock::now().time_since_epoch()).count();
 }
 
+cudaError_t stream_wait(cudaStream_t s) {
+  for (int i = 0;; ++i) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e != cudaErrorNotReady) return e;
+    if (i < 32) std::this_thread::yield();
+    else std::this_thread::sleep_for(std::chrono::microseconds(i < 256 ? 5 : 20));
+  }
+}
+
 thread_local std::string g_last_error;
 thread_local int g_last_code = EIK_OK;
 
@@ -386,7 +395,8 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
   int rc;
   if ((rc = dalloc(&P->dF, P->M))) return rc;
   track(P->dF);
-  P->pitch = P->g.m + 2 * kPad;
+  // even pitch: 16-byte row strides (the FMSM tile loads' tensor maps need it)
+  P->pitch = P->g.m + 2 * kPad + (P->g.m & 1);
   // rows -1 .. n (both dummies): dC / dU point at row 0
   const size_t padded = (size_t)(P->g.n + 2) * P->pitch;
   double* base = nullptr;
@@ -453,7 +463,7 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
     if ((rc = plan_init_cells(P, p, c))) return rc;
   }
   const auto ts0 = std::chrono::steady_clock::now();
-  CK(cudaStreamSynchronize(P->stream));
+  CK(stream_wait(P->stream));
   P->init_sync_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ts0).count();
   return EIK_OK;
 }
@@ -529,8 +539,9 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   out->grid_ctas = grid;
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];
+  CK(stream_wait(P->stream));  // no spinning core while the solve runs
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
-  CK(cudaStreamSynchronize(P->stream));
+  CK(stream_wait(P->stream));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
   if (st[0] != 0) P->last_sweeps_bound = P->max_sweeps;  // flags of a failed run: clear all
@@ -554,7 +565,7 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
     std::vector<unsigned long long> cnt((size_t)st[1]);
     CK(cudaMemcpyAsync(cnt.data(), P->dLsmCnt, sizeof(unsigned long long) * cnt.size(),
                        cudaMemcpyDeviceToHost, P->stream));
-    CK(cudaStreamSynchronize(P->stream));
+    CK(stream_wait(P->stream));
     int64_t tot = 0;
     for (unsigned long long c : cnt) tot += (int64_t)c;
     out->node_updates = tot;
@@ -629,7 +640,7 @@ int plan_run(eik_plan* P, eik_output* out) {
                          sizeof(double) * P->pitch, sizeof(double) * P->g.m, P->g.n,
                          out->u_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost,
                          P->stream));
-    CK(cudaStreamSynchronize(P->stream));
+    CK(stream_wait(P->stream));
   }
   return EIK_OK;
 }
@@ -644,8 +655,9 @@ int plan_prepare(eik_plan* P) {
   CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
                     P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
   int st[8];
+  CK(stream_wait(P->stream));  // no spinning core while the solve runs
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
-  CK(cudaStreamSynchronize(P->stream));
+  CK(stream_wait(P->stream));
   if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
   return EIK_OK;
 }
@@ -700,10 +712,11 @@ int plan_sweep_impl(eik_plan* P, int64_t first_sweep, int count, int* changed, i
   }
   int st[8];
   std::vector<int> ch((size_t)count);
+  CK(stream_wait(P->stream));  // no spinning core while the solve runs
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaMemcpyAsync(ch.data(), P->dChanged, sizeof(int) * count, cudaMemcpyDeviceToHost,
                      P->stream));
-  CK(cudaStreamSynchronize(P->stream));
+  CK(stream_wait(P->stream));
   if (st[0] == 4) return fail(EIK_ERR_CUDA, "fsm wavefront watchdog fired (scheduling bug)");
   if (changed)
     for (int k = 0; k < count; ++k) changed[k] = ch[k] != 0;
@@ -730,8 +743,9 @@ int plan_rows(eik_plan* P, int64_t row0, int64_t nrows, double* host_or_dev, int
     CK(cudaMemcpy2DAsync(host_or_dev, w, dev, dp, w, nrows,
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, P->stream));
   int st = 0;
+  CK(stream_wait(P->stream));
   CK(cudaMemcpyAsync(&st, P->dStatus, sizeof(int), cudaMemcpyDeviceToHost, P->stream));
-  CK(cudaStreamSynchronize(P->stream));
+  CK(stream_wait(P->stream));
   if (st == 4) return fail(EIK_ERR_CUDA, "fsm wavefront watchdog fired (scheduling bug)");
   return EIK_OK;
 }
@@ -1059,6 +1073,33 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
   std::mutex mu;
   std::condition_variable cv;
   int next_job = 0, free_sms = budget, hc_launching = 0;
+  // Plan creation (the uploads) in job order, kCreateWindow at a time: the
+  // first jobs' inputs reach the device first instead of sharing the link with 64
+  // workers' uploads (measured: the first heap-cell replays of a 20-step
+  // batch admitted only after 50-170 ms).  create_prefix = jobs [0, prefix)
+  // are created.
+  constexpr int kCreateWindow = 8;
+  int create_prefix = 0;
+  std::vector<char> created(n, 0);  // by position in `order`
+  // Jobs are taken in the schedule's admission order (batch_slot's
+  // priorities, estimated from the shapes: heap-cell replays by weight, then
+  // the fixed grids, then FMSM), so the long replays of every step upload and
+  // start first, as in plan_run_batch where all plans exist up front.
+  std::vector<int> order(n);
+  {
+    std::vector<double> prio(n, 1.0);
+    for (int k = 0; k < n; ++k) {
+      const int32_t m = methods[k];
+      if (m == EIK_FMSM) {
+        prio[k] = kn.batch_fmsm_prio;
+      } else if ((m == EIK_HCM || m == EIK_FHCM || m == EIK_HCM_EXACT) && cells && cells[k]) {
+        const double J = (double)cells[k]->cells_x * cells[k]->cells_y;
+        prio[k] = 2.0 + std::pow(J, 0.25) + (m == EIK_FHCM ? 0.0 : 0.01);
+      }
+    }
+    for (int k = 0; k < n; ++k) order[k] = k;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return prio[x] > prio[y]; });
+  }
   bool abort = false;
   std::vector<Waiting> waiting;
   std::vector<char> admitted(n, 0);
@@ -1101,16 +1142,28 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
     cudaStream_t st = wr.stream;
     const cudaEvent_t* evs = wr.ev;
     for (;;) {
-      int k;
+      int k, pos;
       {
         std::lock_guard<std::mutex> lk(mu);
         if (abort || next_job >= n) break;
-        k = next_job++;
+        pos = next_job++;
+        k = order[pos];
+      }
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&]() { return abort || create_prefix >= pos - kCreateWindow + 1; });
+        if (abort) break;
       }
       const double tc0 = now_ms();
       t_slow = SlowCall{};
       eik_plan* P = plan_create(problems[k], cells ? cells[k] : nullptr, methods[k], false, st, evs);
       const double tc1 = now_ms();
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        created[pos] = 1;
+        while (create_prefix < n && created[create_prefix]) ++create_prefix;
+        cv.notify_all();
+      }
       const SlowCall slow_create = t_slow;
       t_slow = SlowCall{};
       BatchSlot b;
@@ -1162,7 +1215,7 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
       double tsync = 0, tpool = 0, tev = 0, x;
       {  // plan_free, timed piecewise
         x = now_ms();
-        cudaStreamSynchronize(P->stream);
+        stream_wait(P->stream);
         tsync = now_ms() - x;
         x = now_ms();
         for (void* ptr : P->allocs) pool_release(ptr);
@@ -1187,7 +1240,7 @@ int solve_batch_pipelined(const eik_problem* const* problems, const eik_cells* c
       free_sms += b.sms;
       admit();
     }
-    cudaStreamSynchronize(st);
+    stream_wait(st);
   };
   std::vector<std::thread> th;
   th.reserve(workers);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>  // CUtensorMap (the FMSM tile loads)
 #include <cuda_runtime.h>
 
 namespace eikb200 {
@@ -78,6 +79,11 @@ struct FmsmArgs {
   int J;
   int max_cell_sweeps;
   int big;                  // cells too large for a shared-memory tile: swept in place
+  // Tile staging by TMA: 2-D tensor maps over the padded u / C from row -1
+  // (pitch P), box pu x (max_h + 2) = one tile with its halo; the cost tile
+  // sits tile_doubles / 2 after the value tile (both 128-byte aligned)
+  int use_tma;
+  const CUtensorMap* tmaps;  // device memory: [0] u, [1] C
 };
 
 // max_ctas caps the persistent grid (0: the whole device) so that plans can

@@ -120,6 +120,7 @@ struct eik_plan {
   std::function<void()> on_launched;
   // FMSM Part I computed ahead of the run (plan_prepare_host, called by the
   // batch paths before a plan waits for its SMs); consumed by the next run
+  void* dTmaps = nullptr;   // FMSM tile-load tensor maps (device copy, 2 x 128 B)
   bool fmsm_ready = false;
   std::vector<int32_t> fmsm_order, fmsm_rank;
   std::vector<uint8_t> fmsm_flags;
@@ -178,6 +179,11 @@ struct SlowCall {
 };
 extern thread_local SlowCall t_slow;
 double now_ms_host();
+// Waits for the stream's work without spinning a core: the batch paths run
+// dozens of host threads that each wait on a solve, and the runtime's default
+// schedule (one context) spins in every blocking call -- starving the threads
+// that create the next plans and run FMSM Part I.  Polls, then sleeps.
+cudaError_t stream_wait(cudaStream_t s);
 
 #define CK(expr)                                                  \
   do {                                                            \

@@ -73,8 +73,12 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
   g.pu = even_up(g.max_w + 2);
   // heap-cell tiles put node x at column x+2 (16-byte aligned value pairs)
   if (P->method == EIK_HCM || P->method == EIK_FHCM) g.pu = even_up(g.max_w + 3);
+  // FMSM tiles by TMA: boxes start on an even padded column, so node 0 sits
+  // at tile column 1 or 2 -- two more columns than the halo needs
+  if (P->method == EIK_FMSM) g.pu = even_up(g.max_w + 2) + 2;
   g.pc = even_up(g.max_w);
-  g.tile_doubles = 2 * (int64_t)(g.max_h + 2) * g.pu;  // values + costs, both with halo
+  // values + costs, both with halo; each half 128-byte aligned (TMA destinations)
+  g.tile_doubles = 2 * (((int64_t)(g.max_h + 2) * g.pu + 15) & ~(int64_t)15);
   const size_t tile_bytes = (size_t)g.tile_doubles * sizeof(double);
   const bool hc = P->method == EIK_HCM || P->method == EIK_FHCM;
   P->max_len = std::max(g.max_w, g.max_h);
@@ -264,6 +268,59 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
   return EIK_OK;
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// libcuda link dependency); null when the driver does not provide it
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// Tensor maps of the FMSM tile loads: the padded u and C from row -1, box =
+// one tile (pu x (max_h + 2)).  False when a box dimension or the row
+// stride is outside what the TMA unit takes (the warps then stage by loads).
+bool fmsm_tensor_maps(eik_plan* P, FmsmArgs* a) {
+  const EncodeTiledFn enc = encode_tiled();
+  const CellGeom& g = P->cg;
+  if (!enc || g.pu > 256 || g.max_h + 2 > 256 || (P->pitch * 8) % 16 != 0) return false;
+  if (const char* e = std::getenv("EIK_FMSM_TMA"))
+    if (e[0] == '0') return false;
+  alignas(64) CUtensorMap maps[2];
+  const cuuint64_t dims[2] = {(cuuint64_t)P->pitch, (cuuint64_t)(P->g.n + 2)};
+  const cuuint64_t strides[1] = {(cuuint64_t)P->pitch * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)g.pu, (cuuint32_t)(g.max_h + 2)};
+  const cuuint32_t estr[2] = {1, 1};
+  for (int t = 0; t < 2; ++t) {
+    double* base = (t == 0 ? P->dU : P->dC) - P->pitch;  // row -1
+    CUresult r = enc(&maps[t], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+  }
+  // the maps live in device memory (64-byte aligned), copied before the launch
+  if (!P->dTmaps) {
+    if (pool_alloc(&P->dTmaps, sizeof(maps)) != cudaSuccess) return false;
+    P->allocs.push_back(P->dTmaps);
+  }
+  if (cudaMemcpyAsync(P->dTmaps, maps, sizeof(maps), cudaMemcpyHostToDevice, P->stream) !=
+      cudaSuccess)
+    return false;
+  a->tmaps = static_cast<const CUtensorMap*>(P->dTmaps);
+  return true;
+}
+
 int plan_prepare_host(eik_plan* P) {
   if (P->method != EIK_FMSM || P->fmsm_ready) return EIK_OK;
   using clk = std::chrono::steady_clock;
@@ -343,15 +400,17 @@ int plan_run_fmsm(eik_plan* P, eik_output* out) {
   a.J = (int)J;
   a.max_cell_sweeps = 1 << 20;
   a.big = P->cells_big ? 1 : 0;
+  a.use_tma = (!P->cells_big && fmsm_tensor_maps(P, &a)) ? 1 : 0;
   int grid = 0;
   CK(launch_fmsm(a, P->warps_per_cta, P->cap(), P->stream, &launches, &grid));
   out->grid_ctas = grid;
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];
   unsigned long long cnt[2];
+  CK(stream_wait(P->stream));  // no spinning core while the solve runs
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaMemcpyAsync(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost, P->stream));
-  CK(cudaStreamSynchronize(P->stream));
+  CK(stream_wait(P->stream));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
   if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
@@ -417,9 +476,10 @@ int plan_run_heapcell_serial(eik_plan* P, eik_output* out, const std::vector<int
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];
   unsigned long long cnt[5];
+  CK(stream_wait(P->stream));  // no spinning core while the solve runs
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaMemcpyAsync(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost, P->stream));
-  CK(cudaStreamSynchronize(P->stream));
+  CK(stream_wait(P->stream));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
   if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
@@ -499,10 +559,11 @@ int plan_run_hcm_band(eik_plan* P, eik_output* out, const std::vector<int>& icel
   int st[8];
   int ctl[8];
   unsigned long long cnt[12];
+  CK(stream_wait(P->stream));  // no spinning core while the solve runs
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaMemcpyAsync(ctl, P->dBCtl, sizeof(ctl), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaMemcpyAsync(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost, P->stream));
-  CK(cudaStreamSynchronize(P->stream));
+  CK(stream_wait(P->stream));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
   if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
@@ -657,9 +718,10 @@ retry:  // after a committer heap overflow, with the heap in global memory
   CK(cudaEventRecord(P->ev1, P->stream));
   int st[8];
   unsigned long long cnt[48];
+  CK(stream_wait(P->stream));  // no spinning core while the solve runs
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
   CK(cudaMemcpyAsync(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost, P->stream));
-  CK(cudaStreamSynchronize(P->stream));
+  CK(stream_wait(P->stream));
   if (st[0] == 6 && P->hc_heap_cap == 0)
     return fail(EIK_ERR_CUDA, "heap-cell queue bucket overflow in global memory (sizing bug)");
   if (st[0] == 6 && P->hc_heap_cap > 0) {

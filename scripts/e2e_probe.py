@@ -28,6 +28,14 @@ pinned_F[:] = p.sampled_speed()
 p_pin = E.Problem(g, p.speed, p.exit_nodes, p.exit_cost, p.exit_points, p.exit_point_cost,
                   _F=pinned_F)
 outs = [torch.empty(M, dtype=torch.float64, pin_memory=True).numpy() for _ in range(K * len(rows))]
+def pinned(a):
+    t = torch.empty(a.shape, dtype=torch.float64, pin_memory=True).numpy()
+    t[...] = a
+    return t
+
+
+tables = {cs: E.CellTables(*[pinned(x) for x in (tb.probe_w, tb.probe_e, tb.probe_s, tb.probe_n,
+                                                 tb.center)]) for cs, tb in tables.items()}
 jobs = [(p_pin, meth, cells_of.get(cs), tables.get(cs)) for meth, cs in rows] * K
 for rep in range(3):
     t0 = time.perf_counter()
