@@ -174,6 +174,7 @@ struct HcArgs {
   int* b_ctl;               // [0..1] list sizes, [2] selected count, [3] dispenser, [4] rounds
   unsigned long long* b_kmin;  // [0] round minimum key bits, [1] minimum C bits
   double band_scale;        // delta = band_scale * (h + min(hc_x, hc_y)) / (2 F_max)
+  int band_adapt;           // widen / narrow the band by the cells a round selects
   // cells too large for a shared-memory tile (heapcell_serial_kernel): the
   // exact heap loop, one warp, cells swept in place in u
   uint8_t* big_lock;        // [max_h * max_w] lock bytes

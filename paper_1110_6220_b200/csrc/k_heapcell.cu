@@ -1626,6 +1626,14 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
       tp = t;
     }
   };
+  // Adaptive width: a front a few cells wide (the maze, C4) leaves the
+  // device idle at the base width, and there a wider band costs no extra
+  // pops (C4 HCM/16: x4 2.44 s, 303 k pops; x64 0.48 s, 282 k pops), while a
+  // wide front re-queues cells under a wide band (C2 HCM/16 x16: 2.1x the
+  // pops).  The multiplier doubles after a round of fewer than 32 cells and
+  // halves after one of more than 128 (x1..x16 of the base): a function of
+  // the values alone, so a solve stays bit-reproducible on any grid size.
+  double mult = 1.0;
   int round = 0;
   for (;; ++round) {
     const int par = round & 1;
@@ -1648,7 +1656,7 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
     lap(cyc_sync);
     // phase 2: select the in-band local minima; the rest stay queued
     const double kmin = __longlong_as_double((long long)*(volatile unsigned long long*)a.b_kmin);
-    const double band = kmin + delta;
+    const double band = kmin + delta * mult;
     for (int i = tid; i < ncur; i += nthreads) {
       const int c = __ldcg(cur + i);
       const double k = __ldcg(a.cval + c);
@@ -1676,6 +1684,10 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
     // phase 3: the selected cells, one warp each
     if (tid == 0) a.b_kmin[0] = ~0ull;
     const int nwork = *(volatile int*)(a.b_ctl + 2);
+    if (a.band_adapt) {
+      if (nwork < 32 && mult < 16.0) mult *= 2.0;
+      else if (nwork > 128 && mult > 1.0) mult *= 0.5;
+    }
     if (tid == 0) {
       removals += nwork;
       if (removals > a.budget) atomicExch(a.status, 3);  // read by all after the sync

@@ -1,0 +1,5 @@
+# adaptive band vs fixed widths (C2 all cell sizes, C4 16/32)
+for cs in 8 16 32 64; do timeout 100 python scripts/one_solve.py c2 hcm $cs 3; done
+timeout 300 python scripts/one_solve.py c4 hcm 16 2
+timeout 300 python scripts/one_solve.py c4 hcm 32 2
+timeout 300 python scripts/one_solve.py c3 hcm 16 2
