@@ -535,6 +535,20 @@ def main():
                       "bytes_per_rank_u_C_F": 24 * (b5 - a5 + 2) * p5.grid.m,
                       "note": "strip-Jacobi (SURVEY 8(e) option A): same fixed point, more "
                               "rounds than fsm_solve's 28 sweeps"}
+        # FMSM/32 sharded by row strips of cells, by levels of the cell DAG
+        # (distributed.fmsm_solve_strips: bit-exact fmsm_solve)
+        from paper_1110_6220_b200.distributed import fmsm_solve_strips
+        cfg5 = configs.config5()
+        cs5 = cfg5.cells_for(32)
+        cells5 = E.build_cells(p5.grid, cs5, cs5)
+        f5 = fmsm_solve_strips(p5, cells5, gather="none")
+        c5_sharded["fmsm32"] = {"levels": f5.levels, "device_ms": round(f5.device_ms, 3),
+                                "points_per_s": M5 / (f5.device_ms / 1e3),
+                                "sweeps": f5.sweeps, "node_updates": f5.node_updates,
+                                "edge_rows_sent_by_rank0": f5.exchanges,
+                                "note": "Part II by DAG levels over row strips of cells, edge "
+                                        "rows exchanged after the levels that changed them; "
+                                        "Part I on every rank's host, not in device_ms"}
         del p5
 
     cpu = None if args.no_cpu_baseline or rank != 0 else cpu_baseline_single_core()

@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define EIK_ABI_VERSION 3
+#define EIK_ABI_VERSION 4
 
 /* Solver selection; numbering mirrors eikonal::Method (experiment.hpp:11). */
 enum eik_method {
@@ -229,6 +229,37 @@ int eik_plan_sweep_async(eik_plan* plan, int64_t first_sweep, int32_t count, int
                          void* stream);
 int eik_plan_rows_async(eik_plan* plan, int64_t row0, int64_t nrows, double* dev_buf,
                         int32_t to_plan, void* stream);
+
+/* ---- FMSM sharded by row strips of cells ------------------
+ * fmsm_solve (fmsm.cpp:126-226) over several GPUs, driven by
+ * paper_1110_6220_b200/distributed.py fmsm_solve_strips.  Part I is computed
+ * by every rank identically; Part II runs by LEVELS of the cell DAG (a cell's
+ * earlier-ranked neighbours lie in earlier levels, so the cells of one level
+ * are pairwise non-adjacent and independent), with the strips' edge rows
+ * exchanged after the levels that changed them.  Exact: every cell reads the
+ * same inputs as in the reference's rank-order pass.
+ *
+ * eik_fmsm_schedule: order/rank (fmsm.cpp:138-160), per-cell sweep flags (bit
+ *   d = SweepDir d, 16 = Q-cell; fmsm.cpp:83-120,196-222), per-cell level;
+ *   counters2 = coarse heap removals, coarse node updates.  Any output may be
+ *   NULL.  Host only.
+ * eik_plan_create_fmsm_strip: a plan over one strip's own problem (its rows
+ *   plus a ghost row on each interior side, ghost nodes as exits) holding
+ *   cells_y rows of cells_x cells, rows of height base_y from local node row
+ *   row0, the last ending at row_end (exclusive).
+ * eik_plan_fmsm_levels: the strip's cells grouped by level (local ids, level L
+ *   = cells[level_off[L] .. level_off[L+1])), their flags; prepares u and C.
+ * eik_plan_fmsm_level_async: sweep the cells of one level, enqueued on
+ *   `stream` (NULL: the plan's stream).
+ * eik_plan_fmsm_counters: sweeps and node updates so far (synchronises). */
+int eik_fmsm_schedule(const eik_problem* p, const eik_cells* c, int32_t* order, int32_t* rank,
+                      uint8_t* flags, int32_t* level, int64_t* counters2);
+eik_plan* eik_plan_create_fmsm_strip(const eik_problem* local, int32_t cells_x, int32_t cells_y,
+                                     int64_t base_y, int64_t row0, int64_t row_end);
+int eik_plan_fmsm_levels(eik_plan* plan, const int32_t* cells, const int32_t* level_off,
+                         int32_t nlevels, const uint8_t* flags);
+int eik_plan_fmsm_level_async(eik_plan* plan, int32_t level, void* stream);
+int eik_plan_fmsm_counters(eik_plan* plan, int64_t* out2);
 
 /* Thread-local description / status code of the last failure on this
  * thread (eik_plan_create returns NULL and sets both). */

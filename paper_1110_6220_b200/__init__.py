@@ -18,7 +18,8 @@ from .problem import (CellDecomposition, CellTables, ExitSpec, Grid, Problem, Sp
 from .solvers import (FmmOptions, HybridStats, Plan, SolverOutput, fhcm_solve, fmm_solve,
                       fmsm_solve, fsm_solve, hcm_solve, lsm_solve, run_batch, set_hcm_mode, solve,
                       solve_batch, solve_multi)
-from .distributed import StripSolve, fsm_solve_strips, strip_bounds
+from .distributed import (FmsmStripSolve, StripSolve, fmsm_schedule, fmsm_solve_strips,
+                          fsm_solve_strips, strip_bounds)
 from .metrics import MetricsReport, ground_truth, method_metrics, refined_problem
 from . import experiment_io
 
@@ -41,7 +42,7 @@ __all__ = [
     "snap_point_to_node", "speed_blocks", "speed_checkerboard", "speed_comb_maze",
     "speed_constant", "speed_nodemask", "speed_sinsum", "speed_sinusoid", "HybridStats",
     "Plan", "SolverOutput", "FmmOptions", "fhcm_solve", "fmm_solve", "fmsm_solve",
-    "fsm_solve", "lsm_solve", "hcm_solve", "set_hcm_mode", "solve", "solve_multi", "run_batch", "solve_batch", "device_count", "set_device", "StripSolve", "fsm_solve_strips",
+    "fsm_solve", "lsm_solve", "hcm_solve", "set_hcm_mode", "solve", "solve_multi", "run_batch", "solve_batch", "device_count", "set_device", "StripSolve", "fsm_solve_strips", "FmsmStripSolve", "fmsm_solve_strips", "fmsm_schedule",
     "strip_bounds", "MetricsReport", "ground_truth", "method_metrics", "refined_problem",
     "experiment_io",
 ]

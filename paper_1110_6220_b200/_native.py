@@ -94,6 +94,13 @@ EXPORTS = {
     "eik_plan_rows_async": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32,
                                       C.c_void_p]),
     "eik_plan_set_ctas": (C.c_int, [C.c_void_p, C.c_int32]),
+    "eik_fmsm_schedule": (C.c_int, [C.POINTER(eik_problem), C.POINTER(eik_cells), C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "eik_plan_create_fmsm_strip": (C.c_void_p, [C.POINTER(eik_problem), C.c_int32, C.c_int32,
+                                                C.c_int64, C.c_int64, C.c_int64]),
+    "eik_plan_fmsm_levels": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p]),
+    "eik_plan_fmsm_level_async": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    "eik_plan_fmsm_counters": (C.c_int, [C.c_void_p, C.c_void_p]),
     "eik_set_hcm_mode": (C.c_int, [C.c_int32]),
     "eik_plan_set_hcm_mode": (C.c_int, [C.c_void_p, C.c_int32]),
     "eik_plan_set_partitions": (C.c_int, [C.c_void_p, C.c_int32]),

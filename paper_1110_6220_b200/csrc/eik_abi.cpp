@@ -1397,6 +1397,64 @@ int eik_plan_acceptance_order(eik_plan* P, int32_t* order, int32_t on_device) {
   return EIK_OK;
 }
 
+eik_plan* eik_plan_create_fmsm_strip(const eik_problem* local, int32_t cells_x, int32_t cells_y,
+                                     int64_t base_y, int64_t row0, int64_t row_end) {
+  g_last_code = EIK_OK;
+  g_last_error.clear();
+  if (check_problem(local)) return nullptr;
+  const eik_grid& g = local->grid;
+  if (cells_x < 1 || cells_y < 1 || cells_x > g.m || base_y < 1 || row0 < 0 ||
+      row0 + (int64_t)(cells_y - 1) * base_y >= row_end || row_end > g.n) {
+    fail(EIK_ERR_CONFIG, "fmsm strip: cell rows outside the strip's grid");
+    return nullptr;
+  }
+  if (eik_device_count() < 1) {
+    fail(EIK_ERR_CUDA, "no CUDA device visible: the Eikonal hot path has no CPU fallback");
+    return nullptr;
+  }
+  eik_cells c{};
+  c.cells_x = cells_x;
+  c.cells_y = cells_y;
+  const StripGeom sg{base_y, row0, row_end};
+  t_strip_geom = &sg;
+  eik_plan* P = new eik_plan();
+  const int rc = plan_init(P, local, &c, EIK_FMSM);
+  t_strip_geom = nullptr;
+  if (rc) {
+    std::string keep = g_last_error;
+    int keep_code = g_last_code;
+    plan_free(P);
+    g_last_error = keep;
+    g_last_code = keep_code;
+    return nullptr;
+  }
+  return P;
+}
+
+int eik_plan_fmsm_levels(eik_plan* P, const int32_t* cells, const int32_t* level_off,
+                         int32_t nlevels, const uint8_t* flags) {
+  if (!P || !flags) return fail(EIK_ERR_DOMAIN, "null argument");
+  return plan_fmsm_levels(P, cells, level_off, nlevels, flags);
+}
+
+int eik_plan_fmsm_level_async(eik_plan* P, int32_t level, void* stream) {
+  if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
+  return plan_fmsm_level_async(P, level, static_cast<cudaStream_t>(stream));
+}
+
+int eik_plan_fmsm_counters(eik_plan* P, int64_t* out2) {
+  if (!P || !out2) return fail(EIK_ERR_DOMAIN, "null argument");
+  return plan_fmsm_counters(P, out2);
+}
+
+int eik_fmsm_schedule(const eik_problem* p, const eik_cells* c, int32_t* order, int32_t* rank,
+                      uint8_t* flags, int32_t* level, int64_t* counters2) {
+  g_last_code = EIK_OK;
+  g_last_error.clear();
+  if (check_problem(p)) return g_last_code;
+  return fmsm_schedule(p, c, order, rank, flags, level, counters2);
+}
+
 int eik_plan_prepare(eik_plan* P) {
   if (!P) return fail(EIK_ERR_DOMAIN, "null plan");
   return plan_prepare(P);

@@ -62,6 +62,8 @@ struct CellGeom {
   int64_t base_x, base_y;
   int max_w, max_h;         // largest cell (the last row/column of cells)
   int pu, pc;               // even smem pitches of the u tile (w+2) and C tile (w)
+  int64_t row0, row_end;    // node rows of cell row 0 / end of the last cell row
+                            // (0 and n, except on a sharded FMSM's strip)
   int64_t tile_doubles;     // per-warp smem: (max_h+2)*pu + max_h*pc
 };
 
@@ -84,6 +86,8 @@ struct FmsmArgs {
   // sits tile_doubles / 2 after the value tile (both 128-byte aligned)
   int use_tma;
   const CUtensorMap* tmaps;  // device memory: [0] u, [1] C
+  int nowait;               // a level of a sharded solve: the listed cells are
+                            // pairwise non-adjacent and their inputs final
 };
 
 // max_ctas caps the persistent grid (0: the whole device) so that plans can

@@ -121,6 +121,10 @@ struct eik_plan {
   // FMSM Part I computed ahead of the run (plan_prepare_host, called by the
   // batch paths before a plan waits for its SMs); consumed by the next run
   void* dTmaps = nullptr;   // FMSM tile-load tensor maps (device copy, 2 x 128 B)
+  bool tma_tried = false, tma_ok = false;  // a strip plan's maps (levels)
+  int* dLevelNext = nullptr;               // a sharded FMSM's strip: claim counter per level
+  int64_t level_cap = 0;
+  std::vector<int32_t> level_off;
   bool fmsm_ready = false;
   std::vector<int32_t> fmsm_order, fmsm_rank;
   std::vector<uint8_t> fmsm_flags;
@@ -232,5 +236,17 @@ int plan_run_heapcell(eik_plan* P, eik_output* out);
 // batch paths call it before a plan waits for SMs, so no SM is held idle
 // while the host computes.  A no-op for the other methods.
 int plan_prepare_host(eik_plan* P);
+// A sharded FMSM's strip (distributed.fmsm_solve_strips): cell rows of height
+// base_y from local node row row0, the last ending at row_end.
+struct StripGeom {
+  int64_t base_y, row0, row_end;
+};
+extern thread_local const StripGeom* t_strip_geom;  // read by plan_init_cells
+int plan_fmsm_levels(eik_plan* P, const int32_t* cells, const int32_t* off, int32_t nlevels,
+                     const uint8_t* flags);
+int plan_fmsm_level_async(eik_plan* P, int32_t L, cudaStream_t stream);
+int plan_fmsm_counters(eik_plan* P, int64_t out[2]);
+int fmsm_schedule(const eik_problem* p, const eik_cells* c, int32_t* order, int32_t* rank,
+                  uint8_t* flags, int32_t* level, int64_t* counters);
 
 }  // namespace eikb200

@@ -41,6 +41,8 @@ uint8_t fmsm_dir_mask(bool w, bool e, bool s, bool n) {
 
 }  // namespace
 
+thread_local const StripGeom* t_strip_geom = nullptr;
+
 int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
   P->cells_x = c->cells_x;
   P->cells_y = c->cells_y;
@@ -68,8 +70,15 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
   g.cells_y = c->cells_y;
   g.base_x = P->g.m / c->cells_x;
   g.base_y = P->g.n / c->cells_y;
+  g.row0 = 0;
+  g.row_end = P->g.n;
+  if (const StripGeom* sg = t_strip_geom) {  // a sharded FMSM's strip
+    g.base_y = sg->base_y;
+    g.row0 = sg->row0;
+    g.row_end = sg->row_end;
+  }
   g.max_w = (int)(P->g.m - (c->cells_x - 1) * g.base_x);
-  g.max_h = (int)(P->g.n - (c->cells_y - 1) * g.base_y);
+  g.max_h = (int)std::max<int64_t>(g.base_y, g.row_end - (g.row0 + (c->cells_y - 1) * g.base_y));
   g.pu = even_up(g.max_w + 2);
   // heap-cell tiles put node x at column x+2 (16-byte aligned value pairs)
   if (P->method == EIK_HCM || P->method == EIK_FHCM) g.pu = even_up(g.max_w + 3);
@@ -400,6 +409,7 @@ int plan_run_fmsm(eik_plan* P, eik_output* out) {
   a.J = (int)J;
   a.max_cell_sweeps = 1 << 20;
   a.big = P->cells_big ? 1 : 0;
+  a.nowait = 0;
   a.use_tma = (!P->cells_big && fmsm_tensor_maps(P, &a)) ? 1 : 0;
   int grid = 0;
   CK(launch_fmsm(a, P->warps_per_cta, P->cap(), P->stream, &launches, &grid));
@@ -774,6 +784,144 @@ retry:  // after a committer heap overflow, with the heap in global memory
   out->mon_pct = out->mon_checks == 0 ? 0.0 : 100.0 * out->mon_single / (double)out->mon_checks;
   out->device_ms = ms;
   out->kernel_launches = launches;
+  return EIK_OK;
+}
+
+// ---- a sharded FMSM's strip: levels of the cell DAG ----------------------
+// (distributed.fmsm_solve_strips).  The cells of one level are pairwise
+// non-adjacent and every earlier-ranked neighbour of each sits in an earlier
+// level, so a level runs with no waiting: its inputs are final once the
+// earlier levels and the ghost rows they changed are in place.
+int plan_fmsm_levels(eik_plan* P, const int32_t* cells, const int32_t* off, int32_t nlevels,
+                     const uint8_t* flags) {
+  if (P->method != EIK_FMSM) return fail(EIK_ERR_CONFIG, "fmsm levels need an fmsm plan");
+  if (nlevels < 0 || (nlevels > 0 && (!cells || !off))) return fail(EIK_ERR_DOMAIN, "bad levels");
+  const int64_t J = (int64_t)P->cells_x * P->cells_y;
+  const int64_t total = nlevels > 0 ? off[nlevels] : 0;
+  if (total != J) return fail(EIK_ERR_DOMAIN, "the levels must list every cell of the strip once");
+  for (int32_t L = 0; L < nlevels; ++L)
+    if (off[L] > off[L + 1]) return fail(EIK_ERR_DOMAIN, "level offsets must not decrease");
+  for (int64_t k = 0; k < total; ++k)
+    if (cells[k] < 0 || cells[k] >= J) return fail(EIK_ERR_DOMAIN, "level cell id out of range");
+  CK(cudaSetDevice(P->device));
+  AllocStream alloc_on(P->stream);
+  if (P->level_cap < std::max<int64_t>(1, nlevels)) {
+    int rc;
+    if ((rc = dalloc(&P->dLevelNext, std::max<int64_t>(1, nlevels)))) return rc;
+    P->allocs.push_back(P->dLevelNext);
+    P->level_cap = std::max<int64_t>(1, nlevels);
+  }
+  P->level_off.assign(off, off + nlevels + 1);
+  CK(cudaMemcpyAsync(P->dOrder, cells, sizeof(int32_t) * J, cudaMemcpyHostToDevice, P->stream));
+  CK(cudaMemcpyAsync(P->dFlags, flags, J, cudaMemcpyHostToDevice, P->stream));
+  CK(cudaMemsetAsync(P->dLevelNext, 0, sizeof(int) * P->level_cap, P->stream));
+  CK(cudaMemsetAsync(P->dCellDone, 0, sizeof(int) * J, P->stream));
+  CK(cudaMemsetAsync(P->dCounters, 0, sizeof(unsigned long long) * 8, P->stream));
+  CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
+  int launches = 0;
+  CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
+                    P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
+  CK(stream_wait(P->stream));
+  return EIK_OK;
+}
+
+int plan_fmsm_level_async(eik_plan* P, int32_t L, cudaStream_t stream) {
+  if (P->method != EIK_FMSM || L < 0 || L + 1 >= (int32_t)P->level_off.size())
+    return fail(EIK_ERR_CONFIG, "no such fmsm level (eik_plan_fmsm_levels first)");
+  const int32_t n = P->level_off[L + 1] - P->level_off[L];
+  if (n == 0) return EIK_OK;
+  CK(cudaSetDevice(P->device));
+  const cudaStream_t s = stream ? stream : P->stream;
+  FmsmArgs a;
+  a.g = P->cg;
+  a.C = P->dC;
+  a.u = P->dU;
+  a.order = P->dOrder + P->level_off[L];
+  a.rank = P->dRank;
+  a.flags = P->dFlags;
+  a.done = P->dCellDone;
+  a.next = P->dLevelNext + L;
+  a.counters = P->dCounters;
+  a.status = P->dStatus;
+  a.J = n;
+  a.max_cell_sweeps = 1 << 20;
+  a.big = P->cells_big ? 1 : 0;
+  a.nowait = 1;
+  a.use_tma = 0;
+  a.tmaps = nullptr;
+  if (!P->cells_big) {
+    // the tensor maps were copied on the plan's stream: order it before `s`
+    if (!P->tma_tried) {
+      P->tma_ok = fmsm_tensor_maps(P, &a);
+      P->tma_tried = true;
+      CK(stream_wait(P->stream));
+    }
+    if (P->tma_ok) {
+      a.use_tma = 1;
+      a.tmaps = static_cast<const CUtensorMap*>(P->dTmaps);
+    }
+  }
+  int launches = 0;
+  CK(launch_fmsm(a, P->warps_per_cta, P->cap(), s, &launches, nullptr));
+  return EIK_OK;
+}
+
+int plan_fmsm_counters(eik_plan* P, int64_t out[2]) {
+  CK(cudaSetDevice(P->device));
+  CK(stream_wait(P->stream));
+  CK(cudaDeviceSynchronize());
+  int st[8];
+  unsigned long long cnt[2];
+  CK(cudaMemcpy(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost));
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  if (st[0] == 3) return fail(EIK_ERR_BUDGET, "fmsm: in-cell sweep budget exceeded");
+  out[0] = (int64_t)cnt[0];
+  out[1] = (int64_t)cnt[1];
+  return EIK_OK;
+}
+
+// The schedule every rank of a sharded FMSM computes identically: Part I's
+// order and rank, each cell's sweep flags, and its DAG level.
+int fmsm_schedule(const eik_problem* p, const eik_cells* c, int32_t* order, int32_t* rank,
+                  uint8_t* flags, int32_t* level, int64_t* counters) {
+  if (!p || !c || !c->center_speed) return fail(EIK_ERR_DOMAIN, "fmsm schedule: null argument");
+  if (c->cells_x < 2 || c->cells_y < 2) return fail(EIK_ERR_CONFIG, "fmsm needs at least 2x2 cells");
+  const int32_t cx = c->cells_x, cy = c->cells_y;
+  const int64_t J = (int64_t)cx * cy;
+  FmsmOrder ord;
+  if (fmsm_part1(p, c, &ord)) return fail(EIK_ERR_CONFIG, "fmsm: empty coarse exit set");
+  const int32_t* rk = ord.rank.data();
+  for (int64_t y = 0, cell = 0; y < cy; ++y)
+    for (int64_t x = 0; x < cx; ++x, ++cell) {
+      uint8_t f = 16;
+      if (!ord.is_q[cell]) {
+        const int32_t r = rk[cell];
+        f = fmsm_dir_mask(x > 0 && rk[cell - 1] < r, x + 1 < cx && rk[cell + 1] < r,
+                          y > 0 && rk[cell - cx] < r, y + 1 < cy && rk[cell + cx] < r);
+      }
+      if (flags) flags[cell] = f;
+    }
+  if (level) {
+    std::vector<int32_t> lv(J, 0);
+    for (int64_t p2 = 0; p2 < J; ++p2) {  // rank order: predecessors first
+      const int64_t cell = ord.order[p2], x = cell % cx, y = cell / cx;
+      int32_t L = 0;
+      const int32_t r = rk[cell];
+      if (x > 0 && rk[cell - 1] < r) L = std::max(L, lv[cell - 1] + 1);
+      if (x + 1 < cx && rk[cell + 1] < r) L = std::max(L, lv[cell + 1] + 1);
+      if (y > 0 && rk[cell - cx] < r) L = std::max(L, lv[cell - cx] + 1);
+      if (y + 1 < cy && rk[cell + cx] < r) L = std::max(L, lv[cell + cx] + 1);
+      lv[cell] = L;
+    }
+    std::memcpy(level, lv.data(), sizeof(int32_t) * J);
+  }
+  if (order) std::memcpy(order, ord.order.data(), sizeof(int32_t) * J);
+  if (rank) std::memcpy(rank, ord.rank.data(), sizeof(int32_t) * J);
+  if (counters) {
+    counters[0] = ord.coarse_pops;
+    counters[1] = ord.coarse_updates;
+  }
   return EIK_OK;
 }
 

@@ -25,8 +25,8 @@ __device__ __forceinline__ void cell_rect(const CellGeom& g, int cell, int64_t& 
   const int cx = cell % g.cells_x, cy = cell / g.cells_x;
   ib = (int64_t)cx * g.base_x;
   ie = (cx == g.cells_x - 1) ? g.m : ib + g.base_x;  // remainder to the last cell
-  jb = (int64_t)cy * g.base_y;
-  je = (cy == g.cells_y - 1) ? g.n : jb + g.base_y;
+  jb = g.row0 + (int64_t)cy * g.base_y;
+  je = (cy == g.cells_y - 1) ? g.row_end : jb + g.base_y;
 }
 
 __device__ __forceinline__ int cell_neighbor(const CellGeom& g, int cell, int side) {
@@ -168,7 +168,7 @@ __global__ void fmsm_dataflow_kernel(FmsmArgs a) {
     T.h = (int)(je - jb);
     // wait for the earlier-ranked neighbour cells (one lane per side)
     int ok = 1;
-    if (lane < 4) {
+    if (lane < 4 && !a.nowait) {
       const int nb = cell_neighbor(a.g, cell, lane);
       if (nb >= 0 && a.rank[nb] < p) ok = wait_ge_s32(a.done + nb, 1, a.status);
     }

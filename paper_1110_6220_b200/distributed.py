@@ -327,3 +327,271 @@ def _rounds_on(stream, sw, rank, world, group, nl, limit, send_lo, send_hi, recv
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=group)
     return done_at + 1, float(ms.item())
+
+
+# ---- FMSM sharded by row strips of cells --------------------
+#
+# fmsm_solve (fmsm.cpp:126-226): Part I (the coarse Fast March and its
+# quantised order) is computed by every rank identically on the host; Part II
+# -- one pass over the cells in rank order, a cell reading only its nodes and
+# its cross halo -- runs by LEVELS of the cell DAG: level(c) = 0 without an
+# earlier-ranked neighbour, else 1 + the largest level among them
+# (eik_fmsm_schedule).  A cell's earlier-ranked neighbours lie in earlier
+# levels and its later-ranked ones in later levels, so when level L runs, each
+# of its cells sees exactly the inputs it sees in the reference's pass; the
+# cells of one level are pairwise non-adjacent and run at once.  Rank r owns
+# the cell rows [cy0, cy1) (their node rows plus a ghost row on each side);
+# after a level that processed cells of its first / last cell row, it sends
+# that edge row to the neighbour, which knows from the same schedule when to
+# receive it.  The field, sweeps and node updates are fmsm_solve's bit for bit.
+
+
+@dataclass
+class FmsmSchedule:
+    order: np.ndarray   # cells in coarse order
+    rank: np.ndarray    # inverse of order
+    flags: np.ndarray   # per cell: bit d = SweepDir d chosen, 16 = Q-cell
+    level: np.ndarray   # per cell: DAG level
+    coarse_pops: int
+    coarse_updates: int
+
+
+def fmsm_schedule(problem: Problem, cells, tables=None) -> FmsmSchedule:
+    """Part I on the host through the C-ABI (eik_fmsm_schedule)."""
+    from .problem import _eval_speed
+    from .solvers import _c_problem
+    # Part I reads neither F nor the border probes: only F at the cell
+    # centres (fmsm.cpp:18-30), sampled here for the J centres alone
+    F = problem._F if problem._F is not None else np.ones(1)
+    p, keep_p = _c_problem(problem, F)
+    J = cells.cells_x * cells.cells_y
+    if tables is not None:
+        centre = np.ascontiguousarray(tables.center, dtype=np.float64)
+    else:
+        g = problem.grid.c()
+        cxy = np.empty((J, 2), dtype=np.float64)
+        N.lib.eik_cell_centers(C.byref(g), cells.cells_x, cells.cells_y, N.dptr(cxy))
+        centre = np.ascontiguousarray(_eval_speed(problem.speed, cxy), dtype=np.float64)
+    c = N.eik_cells()
+    c.cells_x, c.cells_y = cells.cells_x, cells.cells_y
+    c.center_speed = N.dptr(centre)
+    order = np.empty(J, dtype=np.int32)
+    rank = np.empty(J, dtype=np.int32)
+    flags = np.empty(J, dtype=np.uint8)
+    level = np.empty(J, dtype=np.int32)
+    cnt = np.zeros(2, dtype=np.int64)
+    N.raise_for(N.lib.eik_fmsm_schedule(C.byref(p), C.byref(c), order.ctypes.data,
+                                        rank.ctypes.data, flags.ctypes.data, level.ctypes.data,
+                                        cnt.ctypes.data))
+    return FmsmSchedule(order, rank, flags, level, int(cnt[0]), int(cnt[1]))
+
+
+class DeviceFmsmStrip:
+    """A strip of a sharded FMSM on the device (eik_plan_create_fmsm_strip):
+    the strip's cells run level by level (eik_plan_fmsm_level_async)."""
+
+    def __init__(self, local: Problem, cells_x: int, cells_y: int, base_y: int, row0: int,
+                 row_end: int):
+        from .solvers import _c_problem
+        try:
+            import torch
+            if torch.cuda.is_available() and torch.cuda.is_initialized():
+                N.raise_for(N.lib.eik_set_device(torch.cuda.current_device()))
+        except ImportError:
+            pass
+        self._F = local.sampled_speed()
+        p, self._keep = _c_problem(local, self._F)
+        self._h = N.lib.eik_plan_create_fmsm_strip(C.byref(p), cells_x, cells_y, base_y, row0,
+                                                   row_end)
+        if not self._h:
+            N.raise_for(N.lib.eik_last_status() or N.EIK_ERR_CUDA)
+
+    def levels(self, cells_by_level: np.ndarray, level_off: np.ndarray, flags: np.ndarray):
+        self._lv = (np.ascontiguousarray(cells_by_level, dtype=np.int32),
+                    np.ascontiguousarray(level_off, dtype=np.int32),
+                    np.ascontiguousarray(flags, dtype=np.uint8))
+        N.raise_for(N.lib.eik_plan_fmsm_levels(self._h, self._lv[0].ctypes.data,
+                                               self._lv[1].ctypes.data, len(level_off) - 1,
+                                               self._lv[2].ctypes.data))
+
+    def run_level(self, L: int, stream: int = 0) -> None:
+        N.raise_for(N.lib.eik_plan_fmsm_level_async(self._h, int(L), C.c_void_p(stream)))
+
+    def rows_async(self, row0: int, nrows: int, buf, to_plan: bool, stream: int) -> None:
+        N.raise_for(N.lib.eik_plan_rows_async(self._h, row0, nrows, C.c_void_p(buf.data_ptr()),
+                                              1 if to_plan else 0, C.c_void_p(stream)))
+
+    def get_rows(self, row0: int, nrows: int, out) -> None:
+        p, dev = DeviceStripSweeper._ptr(out)
+        N.raise_for(N.lib.eik_plan_get_rows(self._h, row0, nrows, C.c_void_p(p), dev))
+
+    def set_rows(self, row0: int, nrows: int, src) -> None:
+        p, dev = DeviceStripSweeper._ptr(src)
+        N.raise_for(N.lib.eik_plan_set_rows(self._h, row0, nrows, C.c_void_p(p), dev))
+
+    def counters(self):
+        out = np.zeros(2, dtype=np.int64)
+        N.raise_for(N.lib.eik_plan_fmsm_counters(self._h, out.ctypes.data))
+        return int(out[0]), int(out[1])
+
+    def close(self):
+        if self._h:
+            N.lib.eik_plan_destroy(self._h)
+            self._h = None
+
+
+@dataclass
+class FmsmStripSolve:
+    values: Optional[np.ndarray]  # as StripSolve.values
+    sweeps: int                   # fine-pass cell sweeps (fmsm.cpp:208,222)
+    node_updates: int             # coarse + fine node updates (fmsm.cpp:173-174,183)
+    heap_removals: int            # coarse Fast March removals (fmsm.cpp:173)
+    levels: int                   # DAG levels of the fine pass
+    exchanges: int                # edge rows this rank sent
+    rows: tuple                   # this rank's node rows [r0, r1)
+    device_ms: float = 0.0
+
+
+def fmsm_solve_strips(problem: Problem, cells, tables=None, group=None,
+                      strip_factory: Optional[Callable] = None,
+                      gather: str = "all") -> FmsmStripSolve:
+    """fmsm_solve over the ranks of `group`, row strips of cells, by levels of
+    the cell DAG (see above).  Without a process group: one strip.  On GPUs
+    (NCCL) the levels, edge-row copies and sends are enqueued on one CUDA
+    stream with no host synchronisation."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        on_gpu = dist.get_backend(group) == "nccl"
+    else:
+        rank, world, on_gpu = 0, 1, False
+    g = problem.grid
+    m, n = g.m, g.n
+    cx, cy = cells.cells_x, cells.cells_y
+    sch = fmsm_schedule(problem, cells, tables)
+    cy0, cy1 = strip_bounds(cy, world, rank)
+    base_y = n // cy
+    jb = lambda c: c * base_y  # noqa: E731  (cells.cpp:7-19: remainder to the last)
+    je = lambda c: n if c == cy - 1 else (c + 1) * base_y  # noqa: E731
+    r0, r1 = jb(cy0), je(cy1 - 1)
+    local = strip_problem(problem, r0, r1)
+    nl = local.grid.n
+    sp = (strip_factory or DeviceFmsmStrip)(local, cx, cy1 - cy0, base_y, 1, 1 + r1 - r0)
+    # the strip's cells grouped by level, by rank within a level
+    lv = sch.level.reshape(cy, cx)
+    mine = np.arange(cy0 * cx, cy1 * cx, dtype=np.int64)
+    nlev = int(sch.level.max()) + 1
+    key = sch.level[mine].astype(np.int64) * (cx * cy) + sch.rank[mine]
+    srt = mine[np.argsort(key, kind="stable")]
+    counts = np.bincount(sch.level[mine], minlength=nlev)
+    off = np.zeros(nlev + 1, dtype=np.int32)
+    off[1:] = np.cumsum(counts)
+    sp.levels((srt - cy0 * cx).astype(np.int32), off, sch.flags[mine])
+    # when an edge row changes: the levels of the cells in my first / last cell
+    # row (sent) and in the neighbours' adjacent rows (received)
+    send_lo = set(lv[cy0].tolist()) if rank > 0 else set()
+    send_hi = set(lv[cy1 - 1].tolist()) if rank < world - 1 else set()
+    recv_lo = set(lv[cy0 - 1].tolist()) if rank > 0 else set()
+    recv_hi = set(lv[cy1].tolist()) if rank < world - 1 else set()
+    dev = torch.device("cuda", torch.cuda.current_device()) if on_gpu else torch.device("cpu")
+    bufs = [torch.empty(m, dtype=torch.float64, device=dev) for _ in range(4)]
+    inf_row = torch.full((m,), math.inf, dtype=torch.float64, device=dev)
+
+    def swap(do_send_lo, do_send_hi, do_recv_lo, do_recv_hi, stream):
+        ops = []
+        if do_send_lo:
+            take(1, bufs[0], stream)
+            ops.append(dist.P2POp(dist.isend, bufs[0], rank - 1, group))
+        if do_recv_lo:
+            ops.append(dist.P2POp(dist.irecv, bufs[1], rank - 1, group))
+        if do_send_hi:
+            take(nl - 2, bufs[2], stream)
+            ops.append(dist.P2POp(dist.isend, bufs[2], rank + 1, group))
+        if do_recv_hi:
+            ops.append(dist.P2POp(dist.irecv, bufs[3], rank + 1, group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        if do_recv_lo:
+            put(0, bufs[1], stream)
+        if do_recv_hi:
+            put(nl - 1, bufs[3], stream)
+        return int(do_send_lo) + int(do_send_hi)
+
+    def take(r, t, stream):
+        if on_gpu:
+            sp.rows_async(r, 1, t, False, stream)
+        else:
+            sp.get_rows(r, 1, t.numpy())
+
+    def put(r, t, stream):
+        if on_gpu:
+            sp.rows_async(r, 1, t, True, stream)
+        else:
+            sp.set_rows(r, 1, t.numpy())
+
+    sent = 0
+    dev_ms = 0.0
+
+    def levels_loop(stream):
+        nonlocal sent
+        sh = stream.cuda_stream if stream is not None else 0
+        # ghost rows: +inf past the grid, else the neighbour's prepared edge row
+        put(0, inf_row, sh)
+        put(nl - 1, inf_row, sh)
+        sent += swap(rank > 0, rank < world - 1, rank > 0, rank < world - 1, sh)
+        for L in range(nlev):
+            if off[L + 1] > off[L]:
+                sp.run_level(L, sh)
+            if world > 1:
+                sent += swap(L in send_lo, L in send_hi, L in recv_lo, L in recv_hi, sh)
+
+    if on_gpu:
+        stream = torch.cuda.Stream(dev)
+        stream.wait_stream(torch.cuda.current_stream(dev))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            levels_loop(stream)
+            e1.record(stream)
+        e1.synchronize()
+        torch.cuda.current_stream(dev).wait_stream(stream)
+        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=group)
+        dev_ms = float(ms.item())
+    else:
+        levels_loop(None)
+    sweeps, updates = sp.counters()
+    if world > 1:
+        t = torch.tensor([sweeps, updates], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        sweeps, updates = int(t[0]), int(t[1])
+    own = np.empty((r1 - r0) * m, dtype=np.float64)
+    sp.get_rows(1, r1 - r0, own)
+    u = own
+    if world > 1 and gather != "none":
+        bounds = [(jb(strip_bounds(cy, world, r)[0]), je(strip_bounds(cy, world, r)[1] - 1))
+                  for r in range(world)]
+        rows_max = max(b - a for a, b in bounds)
+        buf = torch.full((rows_max * m,), math.inf, dtype=torch.float64, device=dev)
+        buf[: own.size] = torch.from_numpy(own).to(dev)
+        if gather == "all":
+            parts = [torch.empty_like(buf) for _ in range(world)]
+            dist.all_gather(parts, buf, group=group)
+        else:
+            parts = [torch.empty_like(buf) for _ in range(world)] if rank == 0 else None
+            dist.gather(buf, parts, dst=0, group=group)
+        if parts is not None:
+            u = np.empty(n * m, dtype=np.float64)
+            for r, (a, b) in enumerate(bounds):
+                u[a * m:b * m] = parts[r][: (b - a) * m].cpu().numpy()
+        else:
+            u = None
+    close = getattr(sp, "close", None)
+    if close:
+        close()
+    return FmsmStripSolve(u, sweeps, sch.coarse_updates + updates, sch.coarse_pops, nlev, sent,
+                          (r0, r1), dev_ms)

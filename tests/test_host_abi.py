@@ -42,7 +42,7 @@ def test_library_is_sm100a():
 
 
 def test_abi_version():
-    assert N.lib.eik_abi_version() == 3
+    assert N.lib.eik_abi_version() == 4
 
 
 def _c_problem(p):
