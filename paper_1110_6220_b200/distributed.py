@@ -435,9 +435,13 @@ class DeviceFmsmStrip:
         return int(out[0]), int(out[1])
 
     def close(self):
-        if self._h:
-            N.lib.eik_plan_destroy(self._h)
+        lib = getattr(N, "lib", None)
+        if self._h and lib is not None:
+            lib.eik_plan_destroy(self._h)
             self._h = None
+
+    def __del__(self):
+        self.close()
 
 
 @dataclass

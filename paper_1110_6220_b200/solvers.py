@@ -248,8 +248,9 @@ class Plan:
         return [bool(x) for x in ch]
 
     def close(self):
-        if getattr(self, "_h", None):
-            N.lib.eik_plan_destroy(self._h)
+        lib = getattr(N, "lib", None)  # None during interpreter shutdown
+        if getattr(self, "_h", None) and lib is not None:
+            lib.eik_plan_destroy(self._h)
             self._h = None
 
     def __del__(self):
