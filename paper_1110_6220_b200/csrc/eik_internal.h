@@ -134,6 +134,9 @@ struct HcArgs {
   unsigned* spec_ver;       // [2][J] tag of the plain / chained speculation
   int* busy;                // [2][J] a warp is computing that speculation
   PRec* rec;                // [2][J] published speculation records
+  int use_tma;              // tiles by TMA: the replay's cost tiles (tmc: the padded
+  const CUtensorMap* tmc;   // C from row -1), the band rounds' value and cost
+  const CUtensorMap* tm_band;  // tiles (tm_band: [u, C])
   double* ckey;             // [J] heap key published for the workers (inf = not queued)
   unsigned* ctag;           // [J] instance number of the last committed result
   int chain;                // make chained speculations

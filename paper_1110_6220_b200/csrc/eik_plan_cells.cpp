@@ -296,22 +296,22 @@ static EncodeTiledFn encode_tiled() {
   return fn;
 }
 
-// Tensor maps of the FMSM tile loads: the padded u and C from row -1, box =
-// one tile (pu x (max_h + 2)).  False when a box dimension or the row
-// stride is outside what the TMA unit takes (the warps then stage by loads).
-bool fmsm_tensor_maps(eik_plan* P, FmsmArgs* a) {
+// Tensor maps of the tile loads: the padded u and C from row -1, box = one
+// tile (pu x (max_h + 2)).  False when a box dimension or the row stride is
+// outside what the TMA unit takes (the warps then stage by loads), or
+// EIK_TILE_TMA=0.  nmaps = 2: u then C (FMSM); 1: C alone (heap cells).
+static bool tile_tensor_maps(eik_plan* P, int nmaps) {
   const EncodeTiledFn enc = encode_tiled();
   const CellGeom& g = P->cg;
   if (!enc || g.pu > 256 || g.max_h + 2 > 256 || (P->pitch * 8) % 16 != 0) return false;
-  if (const char* e = std::getenv("EIK_FMSM_TMA"))
-    if (e[0] == '0') return false;
+  if (knobs().tile_tma == 0) return false;
   alignas(64) CUtensorMap maps[2];
   const cuuint64_t dims[2] = {(cuuint64_t)P->pitch, (cuuint64_t)(P->g.n + 2)};
   const cuuint64_t strides[1] = {(cuuint64_t)P->pitch * sizeof(double)};
   const cuuint32_t box[2] = {(cuuint32_t)g.pu, (cuuint32_t)(g.max_h + 2)};
   const cuuint32_t estr[2] = {1, 1};
-  for (int t = 0; t < 2; ++t) {
-    double* base = (t == 0 ? P->dU : P->dC) - P->pitch;  // row -1
+  for (int t = 0; t < nmaps; ++t) {
+    double* base = (nmaps == 2 && t == 0 ? P->dU : P->dC) - P->pitch;  // row -1
     CUresult r = enc(&maps[t], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims,
                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -326,6 +326,11 @@ bool fmsm_tensor_maps(eik_plan* P, FmsmArgs* a) {
   if (cudaMemcpyAsync(P->dTmaps, maps, sizeof(maps), cudaMemcpyHostToDevice, P->stream) !=
       cudaSuccess)
     return false;
+  return true;
+}
+
+bool fmsm_tensor_maps(eik_plan* P, FmsmArgs* a) {
+  if (!tile_tensor_maps(P, 2)) return false;
   a->tmaps = static_cast<const CUtensorMap*>(P->dTmaps);
   return true;
 }
@@ -544,6 +549,12 @@ int plan_run_hcm_band(eik_plan* P, eik_output* out, const std::vector<int>& icel
   a.budget = 100LL * J + 16;
   a.max_len = P->max_len;
   a.tile_doubles = P->cg.tile_doubles;
+  // value and cost tiles by TMA when every cell's box starts on a 16-byte
+  // column (even cell width)
+  if (!P->cells_big && P->cg.base_x % 2 == 0 && tile_tensor_maps(P, 2)) {
+    a.use_tma = 1;
+    a.tm_band = static_cast<const CUtensorMap*>(P->dTmaps);
+  }
   a.min_smem = P->hc_min_smem;
   a.cx_magic = P->hc_cx_magic;
   a.skip_from = kn.hc_skip_from;
@@ -708,6 +719,15 @@ retry:  // after a committer heap overflow, with the heap in global memory
   a.done_flag = P->dHcMisc;
   a.hsize_pub = P->dHcMisc + 32;
   a.heap_capb_global = P->hc_capb_global;
+  // cost tiles by TMA when every cell's box starts on a 16-byte column
+  // (even cell width: node ib - 2 of an even ib); the maps travel with the
+  // plan's stream ahead of the launch
+  a.use_tma = 0;
+  a.tmc = nullptr;
+  if (!P->cells_big && P->cg.base_x % 2 == 0 && tile_tensor_maps(P, 1)) {
+    a.use_tma = 1;
+    a.tmc = static_cast<const CUtensorMap*>(P->dTmaps);
+  }
   a.pub_capb = P->hc_heap_cap > 0 ? P->hc_heap_cap : P->hc_capb_global;
   a.tile_doubles = P->cg.tile_doubles;
   a.min_smem = P->hc_min_smem;

@@ -305,10 +305,17 @@ struct BucketPQ {
 // Node (x, y) of the cell sits at row y+1, column x+2 of the tile, so even
 // columns of the interior are 16-byte aligned (async 16-byte copies of value
 // pairs); the west halo is column 1.
+// value / cost halves of a warp's tile: (max_h + 2) rows of pu doubles,
+// each rounded to 128 bytes (the cost tile is a TMA destination)
+__host__ __device__ __forceinline__ int64_t hc_half(const CellGeom& g) {
+  return ((int64_t)(g.max_h + 2) * g.pu + 15) & ~(int64_t)15;
+}
+
 struct HTile {
   double* U;      // (h+2) x pu values with cross halo
   double* Ct;     // (h+2) x pu costs with halo (-1 = exit / off-grid)
   uint8_t* lock;  // h x w, 1 = unlocked
+  uint64_t* bar;  // the warp's mbarrier (TMA cost-tile loads)
   int pu, w, h;
   __device__ int ci(int x, int y) const { return (y + 1) * pu + (x + 2); }
   __device__ double& u(int x, int y) const { return U[ci(x, y)]; }
@@ -324,6 +331,60 @@ __device__ __forceinline__ void cp_async8_ca(void* sdst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// The cost tile by TMA (one lane): the box of pu x (max_h + 2) costs whose
+// top-left is node (ib - 2, jb - 1) of the padded C -- 16-byte aligned when
+// the cell's first column is even -- completing on the warp's mbarrier;
+// returns the arrival's state token for the wait.
+__device__ __forceinline__ unsigned long long tma_cost_tile(const HcArgs& a, const HTile& T,
+                                                            int64_t ib, int64_t jb) {
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(T.bar);
+  const unsigned dst = (unsigned)__cvta_generic_to_shared(T.Ct);
+  const unsigned bytes = (unsigned)a.g.pu * (unsigned)(a.g.max_h + 2) * 8u;
+  unsigned long long tok;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+               : "=l"(tok) : "r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];"
+      ::"r"(dst), "l"(a.tmc), "r"((int)(a.g.pad + ib - 2)), "r"((int)jb), "r"(bar) : "memory");
+  return tok;
+}
+// Band rounds (cells swept in place in u): the value and cost tiles of the
+// same box from the padded u and C, after the neighbours' values stored
+// before the last grid barrier (generic proxy) are ordered before the
+// async-proxy reads.
+__device__ __forceinline__ unsigned long long tma_band_tiles(const HcArgs& a, const HTile& T,
+                                                             int64_t ib, int64_t jb) {
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(T.bar);
+  const unsigned bytes = 2u * (unsigned)a.g.pu * (unsigned)(a.g.max_h + 2) * 8u;
+  const int x = (int)(a.g.pad + ib - 2), y = (int)jb;
+  unsigned long long tok;
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 %0, [%1], %2;"
+               : "=l"(tok) : "r"(bar), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];"
+      ::"r"((unsigned)__cvta_generic_to_shared(T.U)), "l"(a.tm_band), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];"
+      ::"r"((unsigned)__cvta_generic_to_shared(T.Ct)), "l"(a.tm_band + 1), "r"(x), "r"(y),
+        "r"(bar)
+      : "memory");
+  return tok;
+}
+__device__ __forceinline__ void tma_wait(const HTile& T, unsigned long long tok) {
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(T.bar);
+  unsigned ok = 0;
+  while (!ok)
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok) : "r"(bar), "l"(tok) : "memory");
+}
 
 // reset_locks (heap_cell.cpp:65-94).  Lanes take (row offset, column) pairs
 // with one division per call, and every node's five cost loads are issued
@@ -493,6 +554,7 @@ __device__ __forceinline__ void process_cell(const HcArgs& a, HTile& T, double* 
   // halo and the probe strips through registers.
   const double* own = slot_ptr(a, st_cur(st), cell);
   double* pstrip = before + 4 * a.max_len;
+  unsigned long long tma_tok = 0;
   {
     const int pr = (T.w + 1) >> 1;  // value pairs per row (an odd width copies
                                     // one pad value into the east halo column,
@@ -506,16 +568,20 @@ __device__ __forceinline__ void process_cell(const HcArgs& a, HTile& T, double* 
       for (int p2 = lane; p2 < pr; p2 += 32)
         for (int y = 0; y < T.h; ++y) cp_async16_cg(&T.U[T.ci(2 * p2, y)], own + y * mw + 2 * p2);
     }
-    for (int xb = 0; xb < T.w + 2; xb += 32) {
-      const int x = xb + lane - 1;  // tile column -1 .. w
-      if (x > T.w) continue;
-      const bool xin = x >= 0 && x < T.w;
-      const double* cb = a.C + (jb - 1) * g.P + g.pad + ib + x;  // row y = -1
-      for (int y = xin ? -1 : 0; y <= (xin ? T.h : T.h - 1); ++y) {
-        const int64_t gj = jb + y;
-        double* dst = &T.Ct[T.ci(x, y)];
-        if (gj >= 0 && gj < g.n) cp_async8_ca(dst, cb + (int64_t)(y + 1) * g.P);
-        else *dst = -1.0;
+    if (a.use_tma) {
+      if (lane == 0) tma_tok = tma_cost_tile(a, T, ib, jb);
+    } else {
+      for (int xb = 0; xb < T.w + 2; xb += 32) {
+        const int x = xb + lane - 1;  // tile column -1 .. w
+        if (x > T.w) continue;
+        const bool xin = x >= 0 && x < T.w;
+        const double* cb = a.C + (jb - 1) * g.P + g.pad + ib + x;  // row y = -1
+        for (int y = xin ? -1 : 0; y <= (xin ? T.h : T.h - 1); ++y) {
+          const int64_t gj = jb + y;
+          double* dst = &T.Ct[T.ci(x, y)];
+          if (gj >= 0 && gj < g.n) cp_async8_ca(dst, cb + (int64_t)(y + 1) * g.P);
+          else *dst = -1.0;
+        }
       }
     }
   }
@@ -560,6 +626,7 @@ __device__ __forceinline__ void process_cell(const HcArgs& a, HTile& T, double* 
       }
     }
     if (first) cp_async_wait_all();
+    if (a.use_tma) tma_wait(T, __shfl_sync(kFull, tma_tok, 0));
     if (prof) prof[3] += clock64() - p0;
   }
   __syncwarp();
@@ -1261,18 +1328,27 @@ __device__ bool pick_job(const HcArgs& a, int pidx, Job& j, int wid) {
 
 template <bool PROF>
 __global__ void heapcell_spec_kernel(HcArgs a) {
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
   const CellGeom& g = a.g;
   HTile T;
   T.pu = g.pu;
   T.U = smem + (size_t)wib * a.tile_doubles;
-  T.Ct = T.U + (size_t)(g.max_h + 2) * g.pu;
-  double* before = T.Ct + (size_t)(g.max_h + 2) * g.pu;  // [4][max_len]
+  T.Ct = T.U + hc_half(g);
+  double* before = T.Ct + hc_half(g);  // [4][max_len]
   // [4] snapshots + [4] probes, then the staging record (128 bytes), then locks
   SpecRec* stg = reinterpret_cast<SpecRec*>(before + 8 * a.max_len);
   T.lock = reinterpret_cast<uint8_t*>(before + 8 * a.max_len + 16);
+  T.bar = reinterpret_cast<uint64_t*>(T.lock + (((size_t)g.max_w * g.max_h + 7) & ~(size_t)7));
+  // (only the warps that process cells own a tile: in CTA 0 the committer's
+  // queue lies past warp 0's tile)
+  if (a.use_tma && lane == 0 && (blockIdx.x != 0 || wib == 0)) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;"
+                 ::"r"((unsigned)__cvta_generic_to_shared(T.bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
 
   // The committer runs alone in CTA 0: every gpu-scope acquire issued on an
   // SM invalidates that SM's L1 (CCTL.IVALL).  Workers poll with relaxed
@@ -1471,10 +1547,14 @@ __device__ void band_process(const HcArgs& a, HTile& T, double* before, SpecRec*
   const bool has_nb[4] = {cx > 0, cx + 1 < g.cells_x, cy > 0, cy + 1 < g.cells_y};
   const int nbs[4] = {cell - 1, cell + 1, cell - g.cells_x, cell + g.cells_x};
   double* pstrip = before + 4 * a.max_len;
-  // values and costs with the cross halo (no corners), row by row; the padded
-  // layout gives +inf / -1 beside the grid, rows -1 and n are filled here
-  const int tw = T.w + 2;
-  for (int y = -1; y <= T.h; ++y) {
+  // values and costs with the cross halo: by TMA (the box of the padded u
+  // and C, +inf / -1 beside the grid and on the dummy rows), or row by row
+  unsigned long long tma_tok = 0;
+  if (a.use_tma) {
+    if (lane == 0) tma_tok = tma_band_tiles(a, T, ib, jb);
+  }
+  const int tw = a.use_tma ? 0 : T.w + 2;
+  for (int y = -1; y <= T.h && !a.use_tma; ++y) {
     const int64_t gj = jb + y;
     const bool rin = gj >= 0 && gj < g.n;
     const double* ur = a.u + gj * g.P + g.pad + ib;
@@ -1497,6 +1577,7 @@ __device__ void band_process(const HcArgs& a, HTile& T, double* before, SpecRec*
       pstrip[3 * a.max_len + t] = has_nb[3] ? __ldg(a.probe[3] + (int64_t)cy * g.m + ib + t) : 1.0;
     }
   }
+  if (a.use_tma) tma_wait(T, __shfl_sync(kFull, tma_tok, 0));
   __syncwarp();
   for (int t = lane; t < T.h; t += 32) {  // border snapshots (heap_cell.cpp:279-282)
     before[0 * a.max_len + t] = T.u(0, t);
@@ -1564,7 +1645,7 @@ __device__ void band_process(const HcArgs& a, HTile& T, double* before, SpecRec*
 
 __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
   cg::grid_group grid = cg::this_grid();
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   __shared__ SpecRec srec[8];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -1573,9 +1654,16 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
   HTile T;
   T.pu = g.pu;
   T.U = smem + (size_t)wib * a.tile_doubles;
-  T.Ct = T.U + (size_t)(g.max_h + 2) * g.pu;
-  double* before = T.Ct + (size_t)(g.max_h + 2) * g.pu;
+  T.Ct = T.U + hc_half(g);
+  double* before = T.Ct + hc_half(g);
   T.lock = reinterpret_cast<uint8_t*>(before + 8 * a.max_len);
+  T.bar = reinterpret_cast<uint64_t*>(T.lock + (((size_t)g.max_w * g.max_h + 7) & ~(size_t)7));
+  if (a.use_tma && (threadIdx.x & 31) == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;"
+                 ::"r"((unsigned)__cvta_generic_to_shared(T.bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
   const int tid = blockIdx.x * blockDim.x + threadIdx.x;
   const int nthreads = gridDim.x * blockDim.x;
   const int J = a.J;
@@ -1871,8 +1959,11 @@ __global__ void __launch_bounds__(32) heapcell_serial_kernel(HcArgs a) {
 }  // namespace
 
 size_t heapcell_smem_bytes(const CellGeom& g, int max_len) {
-  return sizeof(double) * (2 * (size_t)(g.max_h + 2) * g.pu + 8 * (size_t)max_len + 16) +
-         (((size_t)g.max_w * g.max_h + 7) & ~(size_t)7);
+  // values, costs, 4 snapshots + 4 probe strips, the staging record, the lock
+  // bytes, the warp's mbarrier; a multiple of 128 bytes (aligned tiles)
+  const size_t b = sizeof(double) * (2 * (size_t)hc_half(g) + 8 * (size_t)max_len + 16) +
+                   (((size_t)g.max_w * g.max_h + 7) & ~(size_t)7) + 8;
+  return (b + 127) & ~(size_t)127;
 }
 
 size_t heapcell_committer_heap_bytes(int capb) {
