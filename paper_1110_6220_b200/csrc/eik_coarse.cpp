@@ -55,7 +55,7 @@ class Heap {
     std::memcpy(&k, &b, 8);
     return k;
   }
-  void push(int32_t id, double k) {
+  bool push(int32_t id, double k) {
     const Ent e = pack(id, k);
     h_.push_back(e);
     int32_t p = (int32_t)h_.size() - 1;
@@ -66,6 +66,7 @@ class Heap {
       p = par;
     }
     h_[p] = e;
+    return true;
   }
   // the minimum entry (value, id); removes it
   void pop(double& k, int32_t& id) {
@@ -107,6 +108,65 @@ class Heap {
 
  private:
   std::vector<Ent> h_;
+};
+
+// Exact (value, id) priority queue for the coarse Fast March, bucketed by
+// value: bucket b holds the entries with floor((value - base) / delta) == b,
+// kept in a ring of nb buckets past the current one.  A Fast March's keys
+// only move forward by at most max(h_c / F) per acceptance (a candidate is at
+// most the accepted value plus its own h_c / F, local_update.hpp:30-43), so
+// every live entry lies within the ring; the current bucket is sorted once
+// when it becomes current and popped from its end, and an entry landing at
+// or below the current bucket (ulp-level non-monotone candidates) is
+// inserted into it in order.  Buckets partition the value axis monotonically,
+// so pops come out in exactly the (value, id) order of Heap (and of the
+// reference's indexed heap).  push() returns false when an entry would fall
+// past the ring (the caller then restarts with Heap).
+class BucketQueue {
+ public:
+  using Ent = Heap::Ent;
+  BucketQueue(double base, double delta, int nb) : base_(base), inv_(1.0 / delta), mask_(nb - 1),
+                                                    ring_(nb) {}
+  bool empty() const { return count_ == 0; }
+  bool push(int32_t id, double k) {
+    const Ent e = Heap::pack(id, k);
+    const double f = std::floor((k - base_) * inv_);
+    if (!(f < 9.0e15)) return false;  // inf / NaN / beyond any ring
+    const int64_t b = (int64_t)f;
+    if (b <= cur_) {  // into the current (sorted, descending) bucket
+      auto it = std::upper_bound(curv_.begin(), curv_.end(), e, [](const Ent& x, const Ent& y) {
+        return x > y;
+      });
+      curv_.insert(it, e);
+    } else {
+      if (b - cur_ > mask_) return false;
+      ring_[b & mask_].push_back(e);
+    }
+    ++count_;
+    return true;
+  }
+  void pop(double& k, int32_t& id) {
+    while (curv_.empty()) {  // the next non-empty bucket becomes current
+      ++cur_;
+      std::vector<Ent>& r = ring_[cur_ & mask_];
+      if (r.empty()) continue;
+      curv_.swap(r);
+      std::sort(curv_.begin(), curv_.end(), [](const Ent& x, const Ent& y) { return x > y; });
+    }
+    const Ent e = curv_.back();
+    curv_.pop_back();
+    --count_;
+    k = Heap::key_of(e);
+    id = (int32_t)(uint32_t)e;
+  }
+
+ private:
+  double base_, inv_;
+  int64_t mask_;
+  int64_t cur_ = -1;
+  int64_t count_ = 0;
+  std::vector<std::vector<Ent>> ring_;
+  std::vector<Ent> curv_;
 };
 
 // Stable LSD radix sort of 64-bit keys, 11-bit digits (cache-sized count
@@ -249,45 +309,85 @@ int fmsm_part1(const eik_problem* p, const eik_cells* cells, FmsmOrder* out) {
   if (nq == 0) return 1;
 
   int64_t updates = 0, pops = 0;
-  Heap H;
   const int64_t off[4] = {1, -1, W, -W};  // E, W, N, S (di/dj of classic_solvers.cpp:38-39)
   auto update = [&](int64_t q) {
     ++updates;
     return quadrant_c(std::min(v[q + 1], v[q - 1]), std::min(v[q + W], v[q - W]), cc[q]);
   };
-  for (int64_t k = 0; k < nq; ++k) {
-    const int64_t c = seq[k], q = (c / cx + 1) * W + c % cx + 1;
-    for (int d = 0; d < 4; ++d) {
-      const int64_t nqd = q + off[d];
-      if (label[nqd] != 0) continue;
-      label[nqd] = 1;
-      const double cand = update(nqd);
-      if (cand < v[nqd]) v[nqd] = cand;
-      H.push((int32_t)nqd, v[nqd]);
-    }
-  }
-  while (!H.empty()) {
-    double key;
-    int32_t top;
-    H.pop(key, top);
-    const int64_t q = top;
-    if (label[q] == 2 || key != v[q]) continue;  // superseded entry
-    ++pops;
-    label[q] = 2;
-    seq.push_back((int32_t)(q - W - 1 - 2 * (q / W - 1)));
-    for (int d = 0; d < 4; ++d) {
-      const int64_t nqd = q + off[d];
-      if (label[nqd] == 2) continue;
-      const double cand = update(nqd);
-      if (label[nqd] == 0) {
+  // Returns false when the bucketed queue overflows its ring (the run then
+  // restarts from the initial state with the heap).
+  auto march = [&](auto& H) -> bool {
+    for (int64_t k = 0; k < nq; ++k) {
+      const int64_t c = seq[k], q = (c / cx + 1) * W + c % cx + 1;
+      for (int d = 0; d < 4; ++d) {
+        const int64_t nqd = q + off[d];
+        if (label[nqd] != 0) continue;
         label[nqd] = 1;
+        const double cand = update(nqd);
         if (cand < v[nqd]) v[nqd] = cand;
-        H.push((int32_t)nqd, v[nqd]);
-      } else if (cand < v[nqd]) {
-        v[nqd] = cand;
-        H.push((int32_t)nqd, cand);
+        if (!H.push((int32_t)nqd, v[nqd])) return false;
       }
     }
+    while (!H.empty()) {
+      double key;
+      int32_t top;
+      H.pop(key, top);
+      const int64_t q = top;
+      if (label[q] == 2 || key != v[q]) continue;  // superseded entry
+      ++pops;
+      label[q] = 2;
+      seq.push_back((int32_t)(q - W - 1 - 2 * (q / W - 1)));
+      for (int d = 0; d < 4; ++d) {
+        const int64_t nqd = q + off[d];
+        if (label[nqd] == 2) continue;
+        const double cand = update(nqd);
+        if (label[nqd] == 0) {
+          label[nqd] = 1;
+          if (cand < v[nqd]) v[nqd] = cand;
+          if (!H.push((int32_t)nqd, v[nqd])) return false;
+        } else if (cand < v[nqd]) {
+          v[nqd] = cand;
+          if (!H.push((int32_t)nqd, cand)) return false;
+        }
+      }
+    }
+    return true;
+  };
+  // bucket width: an eighth of the smallest h_c / F; ring: the largest h_c / F
+  // (the reach of one acceptance) plus the spread of the exits' costs
+  double cmin = kInf, cmax = 0.0, qmin = kInf, qmax = -kInf;
+  for (int64_t q = 0; q < NP; ++q)
+    if (cc[q] > 0.0) {
+      cmin = std::min(cmin, cc[q]);
+      cmax = std::max(cmax, cc[q]);
+    }
+  for (int64_t k = 0; k < nq; ++k) {
+    const int64_t c = seq[k];
+    qmin = std::min(qmin, best[c]);
+    qmax = std::max(qmax, best[c]);
+  }
+  bool done = false;
+  const double delta = cmin / 8.0;
+  const double span = (qmax - qmin) + 2.0 * cmax;
+  if (delta > 0.0 && std::isfinite(span) && span / delta < (double)(1 << 20)) {
+    int nb = 64;
+    while ((double)nb < span / delta + 4.0) nb <<= 1;
+    BucketQueue B(qmin, delta, nb);
+    done = march(B);
+    if (!done) {  // a key past the ring: start over with the heap
+      for (int32_t b = 0; b < cy; ++b)
+        for (int32_t a = 0; a < cx; ++a) {
+          const int64_t c = (int64_t)b * cx + a, q = (b + 1) * W + a + 1;
+          v[q] = std::isfinite(best[c]) ? best[c] : kInf;
+          label[q] = std::isfinite(best[c]) ? 2 : 0;
+        }
+      seq.resize(nq);
+      updates = pops = 0;
+    }
+  }
+  if (!done) {
+    Heap H;
+    march(H);
   }
   out->coarse_updates = updates;
   out->coarse_pops = pops;
