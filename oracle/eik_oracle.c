@@ -692,6 +692,13 @@ static int keyed_cmp(const void* a, const void* b) {
 }
 
 int orc_fmsm(const orc_problem* p, const orc_cells* c, double* v, orc_stats* st) {
+  return orc_fmsm_ex(p, c, v, st, NULL);
+}
+
+/* orc_fmsm with the quantised cell order (fmsm.cpp:138-160) copied to
+ * order_out (J entries) when non-NULL; v == NULL stops after Part I. */
+int orc_fmsm_ex(const orc_problem* p, const orc_cells* c, double* v, orc_stats* st,
+                int64_t* order_out) {
   memset(st, 0, sizeof *st);
   if (c->cells_x < 2 || c->cells_y < 2) return 1; /* fmsm.cpp:124-125 */
   cellgeo G;
@@ -769,6 +776,12 @@ int orc_fmsm(const orc_problem* p, const orc_cells* c, double* v, orc_stats* st)
     }
     qsort(order, (size_t)J, sizeof(keyed), keyed_cmp);
     for (int64_t k = 0; k < J; ++k) rank[order[k].id] = k;
+    if (order_out)
+      for (int64_t k = 0; k < J; ++k) order_out[k] = order[k].id;
+    st->heap_removals = cst.heap_removals;
+    st->node_updates = cst.node_updates;
+  }
+  if (rc == 0 && v) {
 
     char* is_exit = (char*)malloc((size_t)(m * n));
     init_values(p, v, is_exit);

@@ -63,6 +63,10 @@ int orc_lsm(const orc_problem* p, double* u, orc_stats* st);
 int orc_hcm(const orc_problem* p, const orc_cells* c, double* u, orc_stats* st);
 int orc_fhcm(const orc_problem* p, const orc_cells* c, double* u, orc_stats* st);
 int orc_fmsm(const orc_problem* p, const orc_cells* c, double* u, orc_stats* st);
+/* orc_fmsm plus the quantised cell order (order_out: J ids, may be NULL);
+ * u == NULL runs Part I only (stats: the coarse Fast March's counters). */
+int orc_fmsm_ex(const orc_problem* p, const orc_cells* c, double* u, orc_stats* st,
+                int64_t* order_out);
 
 #ifdef __cplusplus
 }

@@ -69,6 +69,9 @@ def _load_oracle():
         getattr(lib, nm).argtypes = [C.POINTER(orc_problem), C.POINTER(orc_cells), _dp,
                                      C.POINTER(orc_stats)]
         getattr(lib, nm).restype = C.c_int
+    lib.orc_fmsm_ex.argtypes = [C.POINTER(orc_problem), C.POINTER(orc_cells), _dp,
+                                C.POINTER(orc_stats), C.c_void_p]
+    lib.orc_fmsm_ex.restype = C.c_int
     lib.orc_quadrant_update.argtypes = [C.c_double] * 4
     lib.orc_quadrant_update.restype = C.c_double
     lib.orc_node_update.argtypes = [_dp, C.c_double, C.c_double]
@@ -156,6 +159,24 @@ def oracle_solve(p: Problem, method: str, cells: CellDecomposition = None,
     if rc == 3:
         raise N.BudgetError("heap-cell removal budget exceeded")
     return Result(u, st.sweeps, st.node_updates, st.heap_removals, st.mon_checks, st.mon_single)
+
+
+def oracle_fmsm_order(p: Problem, cells: CellDecomposition, tables: CellTables = None):
+    """FMSM Part I only (fmsm.cpp:126-162): the quantised cell order and the
+    coarse Fast March's heap removals and node updates."""
+    from paper_1110_6220_b200.problem import cell_tables
+    op, keep = _orc_problem(p)
+    if tables is None:
+        tables = cell_tables(p, cells)
+    arrs = [np.ascontiguousarray(a, dtype=np.float64) for a in
+            (tables.probe_w, tables.probe_e, tables.probe_s, tables.probe_n, tables.center)]
+    oc = orc_cells(cells.cells_x, cells.cells_y, *[a.ctypes.data_as(_dp) for a in arrs])
+    order = np.empty(cells.cells_x * cells.cells_y, dtype=np.int64)
+    st = orc_stats()
+    rc = olib.orc_fmsm_ex(C.byref(op), C.byref(oc), None, C.byref(st), order.ctypes.data)
+    if rc == 1:
+        raise N.ConfigError("oracle: bad configuration")
+    return order, st.heap_removals, st.node_updates
 
 
 def oracle_fsm_sweep(m: int, n: int, h: float, F: np.ndarray, frozen: np.ndarray, u: np.ndarray,

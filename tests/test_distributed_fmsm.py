@@ -256,3 +256,46 @@ def test_device_stream_ordered_levels_single_rank():
     p, cells = _case("chk")
     ref = O.oracle_solve(p, "fmsm", cells)
     assert np.array_equal(u, ref.u) and k[0] == ref.sweeps and k[1] == ref.node_updates
+
+
+def _random_problem(rng, k):
+    m = int(rng.integers(9, 70))
+    n = int(rng.integers(9, 70))
+    g = E.Grid(m, n, 1.0 / (m - 1), -0.3, 0.2)
+    kind = k % 5
+    if kind == 4:  # speed ratio 1e6: past the bucket ring, the heap path
+        sp = E.speed_checkerboard(3, 1e-6, 1.0)
+    elif kind == 0:
+        sp = E.speed_sinusoid(0.5, int(rng.integers(1, 6)))
+    elif kind == 1:
+        sp = E.speed_checkerboard(int(rng.integers(0, 4)) * 2 + 1, 1.0, float(rng.uniform(1.5, 80)))
+    elif kind == 2:
+        sp = E.speed_constant()
+    else:
+        sp = E.speed_checkerboard(3, 0.01, 1.0)
+    if k % 3 == 0:
+        ex = E.ExitSpec.point_source((g.x0 + float(rng.uniform(0, m - 1)) * g.h,
+                                      g.y0 + float(rng.uniform(0, n - 1)) * g.h))
+    else:
+        cnt = int(rng.integers(1, 6))
+        nodes = sorted({(int(rng.integers(0, m)), int(rng.integers(0, n))) for _ in range(cnt)})
+        costs = [float(rng.uniform(0, 50.0 if k % 5 == 0 else 0.05)) for _ in nodes]
+        ex = E.ExitSpec.node_set(nodes, costs)
+    p = E.build_problem(g, sp, ex)
+    cx = int(rng.integers(2, max(3, m // 2)))
+    cy = int(rng.integers(2, max(3, n // 2)))
+    return p, E.build_cells(g, cx, cy)
+
+
+def test_schedule_order_equals_the_oracle_on_random_problems():
+    """eik_fmsm_schedule (the product's Part I: bucketed exact queue, heap
+    fallback for extreme speed ratios / cost spreads, insertion-sorted
+    quantised order) equals the oracle's Part I -- order, coarse removals and
+    coarse updates -- on random problems (CPU, no device)."""
+    rng = np.random.default_rng(11)
+    for k in range(120):
+        p, cells = _random_problem(rng, k)
+        s = fmsm_schedule(p, cells)
+        order, pops, upd = O.oracle_fmsm_order(p, cells)
+        assert np.array_equal(s.order, order), k
+        assert (s.coarse_pops, s.coarse_updates) == (pops, upd), k
