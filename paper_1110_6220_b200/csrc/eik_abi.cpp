@@ -72,6 +72,7 @@ Knobs read_knobs() {
   k.batch_workers = gi("EIK_BATCH_WORKERS", 0);
   k.hcm_exact = gi("EIK_HCM_EXACT", 0);
   k.hcm_band = gd("EIK_HCM_BAND", 0.0);
+  k.hcm_band_shrink = gi("EIK_HCM_BAND_SHRINK", 128);
   return k;
 }
 std::mutex g_knobs_mu;

@@ -182,6 +182,7 @@ struct HcArgs {
   unsigned long long* b_kmin;  // [0] round minimum key bits, [1] minimum C bits
   double band_scale;        // delta = band_scale * (h + min(hc_x, hc_y)) / (2 F_max)
   int band_adapt;           // widen / narrow the band by the cells a round selects
+  int band_shrink;          // ... narrowing after a round of more cells than this
   // cells too large for a shared-memory tile (heapcell_serial_kernel): the
   // exact heap loop, one warp, cells swept in place in u
   uint8_t* big_lock;        // [max_h * max_w] lock bytes

@@ -166,6 +166,7 @@ struct Knobs {
   // HCM band scheduler
   int hcm_exact = 0;               // EIK_HCM_EXACT=1: HCM by the exact replay
   double hcm_band = 0.0;           // EIK_HCM_BAND: band width scale (0 = default)
+  int hcm_band_shrink = 128;       // EIK_HCM_BAND_SHRINK: narrow after rounds of more cells
 };
 const Knobs& knobs();
 void reload_knobs();

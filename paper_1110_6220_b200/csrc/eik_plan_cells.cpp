@@ -567,6 +567,7 @@ int plan_run_hcm_band(eik_plan* P, eik_output* out, const std::vector<int>& icel
   a.b_kmin = P->dBKmin;
   a.band_scale = kn.hcm_band > 0.0 ? kn.hcm_band : 4.0;
   a.band_adapt = kn.hcm_band > 0.0 ? 0 : 1;  // an explicit EIK_HCM_BAND fixes the width
+  a.band_shrink = kn.hcm_band_shrink;
   a.prof = kn.hc_profile ? 1 : 0;
   const int hc_ctas = P->cap() > 0 ? std::min(P->hc_max_ctas, P->cap()) : P->hc_max_ctas;
   int grid = 0;

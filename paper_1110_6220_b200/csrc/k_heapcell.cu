@@ -1716,11 +1716,15 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
   };
   // Adaptive width: a front a few cells wide (the maze, C4) leaves the
   // device idle at the base width, and there a wider band costs no extra
-  // pops (C4 HCM/16: x4 2.44 s, 303 k pops; x64 0.48 s, 282 k pops), while a
+  // pops -- the walls' h/F is 100x the base's (C4 HCM/16: x4 2.44 s, 303 k
+  // pops; x64 0.40 s, 282 k; x128 41 ms, 255 k; x256 31 ms, 233 k) -- while a
   // wide front re-queues cells under a wide band (C2 HCM/16 x16: 2.1x the
   // pops).  The multiplier doubles after a round of fewer than 32 cells and
-  // halves after one of more than 128 (x1..x16 of the base): a function of
-  // the values alone, so a solve stays bit-reproducible on any grid size.
+  // halves after one of more than band_shrink (128; x1..x64 of the base): a
+  // function of the values alone, so a solve stays bit-reproducible on any
+  // grid size.  (Narrowing later -- 256, 512, 1024 -- buys C4 HCM/16 90, 38,
+  // 33 ms but costs the C2 matrix 5-10 % in re-queued pops: 1169 -> 1111,
+  // 1083, 1053 M points/s at 20 steps.)
   double mult = 1.0;
   int round = 0;
   for (;; ++round) {
@@ -1773,8 +1777,8 @@ __global__ void __launch_bounds__(256, 1) hcm_band_kernel(HcArgs a) {
     if (tid == 0) a.b_kmin[0] = ~0ull;
     const int nwork = *(volatile int*)(a.b_ctl + 2);
     if (a.band_adapt) {
-      if (nwork < 32 && mult < 16.0) mult *= 2.0;
-      else if (nwork > 128 && mult > 1.0) mult *= 0.5;
+      if (nwork < 32 && mult < 64.0) mult *= 2.0;
+      else if (nwork > a.band_shrink && mult > 1.0) mult *= 0.5;
     }
     if (tid == 0) {
       removals += nwork;
