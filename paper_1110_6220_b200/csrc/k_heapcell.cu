@@ -873,20 +873,13 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
         if (lane == 0) got = atomicCAS(a.busy + cell, 0, 1) == 0 ? 1 : 0;
         if (__shfl_sync(kFull, got, 0)) {
           if (lane == 0 && a.wdbg) a.owner[cell] = 0x30000;
-          // a worker may have published since the loads above: re-read the
-          // plain record under the busy flag (no writer can start now)
-          uint4 pw = make_uint4(0u, 0u, 0u, kSpecNone);
-          if (lane < 5) pw = ld_w128(&rec_ptr(a, 0, cell)->w[lane]);
-          const unsigned ip2 = __shfl_sync(kFull, pw.w, 4), tp2 = __shfl_sync(kFull, pw.z, 4);
-          const bool whole2 = (__ballot_sync(kFull, lane < 5 && pw.w != ip2) == 0u);
-          if (whole2 && ip2 != kSpecNone && tag_is(tp2, v)) {
-            if (lane == 0) {
-              if (a.wdbg) a.owner[cell] = 0x40000;
-              st_release_s32(a.busy + cell, 0);
-            }
-            if (lane < 8) rw = pw;
-            kind = 0;
-          } else {
+          // The cell is ours to process.  A worker may have published a
+          // valid result between the loads above and the claim; processing
+          // it here anyway is exact (the plain slot is ours now, and the
+          // commit's new version and committer instance invalidate that
+          // result and every speculation built on it) and saves the round
+          // trip of a re-read on every miss.
+          {
             mode = 1;
             if (lane == 0 && a.wdbg) a.owner[cell] = 0x50000;
             // classify the miss (profiling counters 16..23)
@@ -969,9 +962,9 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       rsweeps = stg->sweeps;
       rupdates = stg->updates;
       rinst = kSelfInst | ((unsigned)removals & kInstMask);
-      if (lane == 0) {
+      if (lane == 0) {  // every lane's fence above ordered its slot stores first
         if (a.wdbg) a.owner[cell] = 0x60000;
-        st_release_s32(a.busy + cell, 0);
+        st_relaxed_u32(reinterpret_cast<unsigned*>(a.busy + cell), 0u);
       }
       kind = 0;
       ++self_processed;
