@@ -225,6 +225,30 @@ struct BucketPQ {
     }
     return true;
   }
+  // The commit's variants: the bucket's count and cached minimum were loaded
+  // ahead of the commit's stores (only this lane touches the bucket now), and
+  // the entry's id is the caller's
+  __device__ bool insert_pre(int id, double k, int l, int s, double mkl, int mil) {
+    if (s >= capb) return false;
+    set(l, s, k, id);
+    cnt[l] = s + 1;
+    pubcnt[32 * l] = s + 1;
+    if (less(k, id, mkl, mil)) {
+      mk[l] = k;
+      mi[l] = id;
+      msl[l] = s;
+    }
+    return true;
+  }
+  __device__ void decrease_pre(int enc, double k, int id, double mkl, int mil) {
+    const int l = enc >> 24, s = enc & 0xFFFFFF;
+    bk[l * capb + s] = k;
+    if (less(k, id, mkl, mil)) {
+      mk[l] = k;
+      mi[l] = id;
+      msl[l] = s;
+    }
+  }
   __device__ void decrease(int enc, double k) {  // one lane per bucket; keys only decrease
     const int l = enc >> 24, s = enc & 0xFFFFFF;
     const int id = bi[l * capb + s];
@@ -1008,13 +1032,21 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
           a.ctag[cell] = rinst;
         }
         if (nb >= 0) {  // heap_cell.cpp:288-311
+          // the neighbour's bucket: its queue entry's, or the one it would be
+          // inserted into (side d of bucket wpop: -1, +1, -2, +2); its count
+          // and cached minimum are loaded ahead of the stores below
+          const int lq = my_pos >= 0 ? (my_pos >> 24)
+                                     : ((wpop + (d < 2 ? 2 * d - 1 : 2 * (2 * d - 5))) & 31);
+          const int cnt_l = H.cnt[lq];
+          const double mk_l = H.mk[lq];
+          const int mi_l = H.mi[lq];
           bool moved = false;
           double cvd = my_cv;
           if (cand < cvd) {
             cvd = cand;
             a.cval[nb] = cand;
             if (my_pos >= 0) {
-              H.decrease(my_pos, cand);
+              H.decrease_pre(my_pos, cand, nb, mk_l, mi_l);
               moved = true;
             }
           }
@@ -1026,9 +1058,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
               if (ms) ++mon_single;
             }
             if (my_pos < 0) {
-              // the neighbour on side d sits in bucket wpop -1, +1, -2, +2
-              const int l = (wpop + (d < 2 ? 2 * d - 1 : 2 * (2 * d - 5))) & 31;
-              if (H.insert(nb, cvd, l)) ++ins;
+              if (H.insert_pre(nb, cvd, lq, cnt_l, mk_l, mi_l)) ++ins;
               else ovf = true;
               moved = true;
             }
