@@ -220,12 +220,14 @@ def test_device_strip_larger_grid_bitwise():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("kind", ["sin", "chk"])
-def test_device_strips_two_ranks_bitwise(kind):
+@pytest.mark.parametrize("world,kind", [(2, "sin"), (2, "chk"), (3, "chk")])
+def test_device_strips_ranks_bitwise(world, kind):
+    """Two / three ranks on one GPU over gloo (the levels are host-synchronised:
+    no kernel waits on another rank's)."""
     p, cells = _case(kind)
-    us, ks = _run_world(2, True, kind)
+    us, ks = _run_world(world, True, kind)
     ref = O.oracle_solve(p, "fmsm", cells)
-    for r in range(2):
+    for r in range(world):
         assert np.array_equal(us[r], ref.u)
         assert tuple(ks[r][:3]) == (ref.sweeps, ref.node_updates, ref.heap_removals)
 

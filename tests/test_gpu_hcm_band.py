@@ -113,3 +113,36 @@ def test_default_mode_switch():
     assert ex.rounds == 0
     band = E.solve(p, "hcm", cells)
     assert band.rounds > 0
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_band_walls_widen_the_band(seed):
+    """A maze-like field (walls of F = 1e-3, 1000x the base h/F): the adaptive
+    width grows to its cap on narrow fronts; the field still lands on the
+    reference HCM's fixed point, and the solve is reproducible."""
+    rng = np.random.default_rng(1700 + seed)
+    m = n = int(rng.integers(60, 160))
+    g = E.Grid(m, n, 1.0 / (m - 1), 0.0, 0.0)
+    F = np.ones((n, m))
+    for _ in range(int(rng.integers(3, 9))):  # walls with a gap
+        if rng.integers(0, 2):
+            j = int(rng.integers(2, n - 2))
+            F[j:j + 2, :] = 1e-3
+            a = int(rng.integers(0, m - 6))
+            F[j:j + 2, a:a + 5] = 1.0
+        else:
+            i = int(rng.integers(2, m - 2))
+            F[:, i:i + 2] = 1e-3
+            a = int(rng.integers(0, n - 6))
+            F[a:a + 5, i:i + 2] = 1.0
+    sp = lambda x, y, F=F, g=g: F[np.clip(np.rint((y - g.y0) / g.h).astype(int), 0, g.n - 1),  # noqa: E731
+                                  np.clip(np.rint((x - g.x0) / g.h).astype(int), 0, g.m - 1)]
+    p = E.build_problem(g, sp, E.ExitSpec.node_set([(0, 0)], [0.0]))
+    for c in (4, 8, 16):
+        cells = E.build_cells(g, max(1, m // c), max(1, n // c))
+        a = E.solve(p, "hcm", cells)
+        b = O.oracle_solve(p, "hcm", cells)
+        scale = max(1.0, float(np.max(b.u)))
+        assert float(np.max(np.abs(a.values - b.u))) <= TOL * scale, c
+        again = E.solve(p, "hcm", cells)
+        assert bitwise(again.values, a.values) and again.rounds == a.rounds
