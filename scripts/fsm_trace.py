@@ -22,8 +22,10 @@ for name, p in cases:
     plan.run()
     path = os.path.join(out_dir, f"trace_{name}.txt")
     os.environ["EIK_TRACE_FSM"] = path
+    E.lib.eik_debug_reload_knobs()  # knobs are read once per process
     o = plan.run()
     del os.environ["EIK_TRACE_FSM"]
+    E.lib.eik_debug_reload_knobs()
     rows = [tuple(int(x) for x in line.split()) for line in open(path)]
     t0 = min(r[2] for r in rows)
     print(f"== {name}: sweeps={o.sweeps} dev_ms={o.device_ms:.3f}")
