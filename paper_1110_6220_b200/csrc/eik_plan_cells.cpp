@@ -780,10 +780,11 @@ retry:  // after a committer heap overflow, with the heap in global memory
                  "heapcell committer cycles: pop %llu obtain %llu self %llu commit %llu | self: "
                  "stage %llu sweeps %llu scans %llu | hits %llu (chained %llu) self %llu | "
                  "heap max %llu cap %d | stage: %llu reset_locks %llu steps %llu | commit: record %llu | "
-                 "obtain: rescan %llu first-rt %llu waits %llu (%llu cycles)\n",
+                 "obtain: rescan %llu first-rt %llu waits %llu (%llu cycles) | commit to end of "
+                 "the neighbour block %llu\n",
                  cnt[8], cnt[9], cnt[10], cnt[11], cnt[12], cnt[13], cnt[14], cnt[6], cnt[15],
                  cnt[5], cnt[38], P->hc_heap_cap, cnt[39], cnt[40], cnt[41], cnt[42], cnt[43],
-                 cnt[44], cnt[7], cnt[45]);
+                 cnt[44], cnt[7], cnt[45], cnt[46]);
   if (kn.hc_profile)
     std::fprintf(stderr,
                  "heapcell misses: unchained %llu pending %llu stale %llu wrong-inst %llu "

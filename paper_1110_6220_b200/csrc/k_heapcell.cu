@@ -115,6 +115,22 @@ __device__ __forceinline__ int ld_relaxed_s32(const int* p) {
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// predicated stores (generic addresses: the queue lives in shared or global
+// memory), so lanes taking different cases stay in one instruction stream
+__device__ __forceinline__ void st_pred_f64(double* p, double v, bool c) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.f64 [%0], %1; }"
+               ::"l"(p), "d"(v), "r"((unsigned)c) : "memory");
+}
+__device__ __forceinline__ void st_pred_s32(int* p, int v, bool c) {
+  asm volatile("{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.s32 [%0], %1; }"
+               ::"l"(p), "r"(v), "r"((unsigned)c) : "memory");
+}
+__device__ __forceinline__ void st_pred_relaxed_u64(unsigned long long* p, unsigned long long v,
+                                                    bool c) {
+  asm volatile(
+      "{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.relaxed.gpu.global.u64 [%0], %1; }"
+      ::"l"(p), "l"(v), "r"((unsigned)c) : "memory");
+}
 __device__ __forceinline__ bool tag_is(unsigned sv, unsigned v) {
   return sv != kSpecNone && (sv & kTagMask) == v;
 }
@@ -768,7 +784,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
   long long removals = 0, sweeps = 0, updates = 0, mon_checks = 0, mon_single = 0;
   long long self_processed = 0, fast_hits = 0, waits = 0, chain_hits = 0;
   long long cyc_pop = 0, cyc_obtain = 0, cyc_self = 0, cyc_commit = 0, cyc_rec = 0;
-  long long cyc_rescan = 0, cyc_rt1 = 0, cyc_wait = 0;
+  long long cyc_rescan = 0, cyc_rt1 = 0, cyc_wait = 0, cyc_nbb = 0;
   long long prof[6] = {0, 0, 0, 0, 0, 0};
   long long miss_cls[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   int max_size = H.size;
@@ -1031,47 +1047,57 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
           st_relaxed_u64(a.state + cell, (u64)lo | (st & (0xFFull << 34)) | ((u64)nps << 32));
           a.ctag[cell] = rinst;
         }
-        if (nb >= 0) {  // heap_cell.cpp:288-311
-          // the neighbour's bucket: its queue entry's, or the one it would be
-          // inserted into (side d of bucket wpop: -1, +1, -2, +2); its count
-          // and cached minimum are loaded ahead of the stores below
-          const int lq = my_pos >= 0 ? (my_pos >> 24)
-                                     : ((wpop + (d < 2 ? 2 * d - 1 : 2 * (2 * d - 5))) & 31);
-          const int cnt_l = H.cnt[lq];
-          const double mk_l = H.mk[lq];
-          const int mi_l = H.mi[lq];
-          bool moved = false;
-          double cvd = my_cv;
-          if (cand < cvd) {
-            cvd = cand;
-            a.cval[nb] = cand;
-            if (my_pos >= 0) {
-              H.decrease_pre(my_pos, cand, nb, mk_l, mi_l);
-              moved = true;
-            }
-          }
-          unsigned lo = (unsigned)my_nst + kVerOne;
-          if (add) {
-            lo |= fl;
-            if (mc) {
-              ++mon_checks;
-              if (ms) ++mon_single;
-            }
-            if (my_pos < 0) {
-              if (H.insert_pre(nb, cvd, lq, cnt_l, mk_l, mi_l)) ++ins;
-              else ovf = true;
-              moved = true;
-            }
-          }
-          if (moved) a.ckey[nb] = cvd;
-          // the popped cell sits on side (d ^ 1) of its neighbour, which
-          // learns its new slot
-          const int sh = 34 + 2 * (d ^ 1);
-          st_relaxed_u64(a.state + nb, (u64)lo | (my_nst & ~((3ull << sh) | 0xFFFFFFFFull)) |
-                                           ((u64)ncur << sh));
+        // heap_cell.cpp:288-311, branch-free: the four lanes run one
+        // instruction stream (their cases -- lower the key, queue the cell,
+        // neither -- differ), every store predicated on its case
+        const bool has = nb >= 0;
+        const int nbq = has ? nb : cell;  // an in-range id for the addresses
+        // the neighbour's bucket: its queue entry's, or the one it would be
+        // inserted into (side d of bucket wpop: -1, +1, -2, +2); its count and
+        // cached minimum are loaded ahead of the stores
+        const int lq = my_pos >= 0 ? (my_pos >> 24)
+                                   : ((wpop + (d < 2 ? 2 * d - 1 : 2 * (2 * d - 5))) & 31);
+        const int cnt_l = H.cnt[lq];
+        const double mk_l = H.mk[lq];
+        const int mi_l = H.mi[lq];
+        const bool lower = has && cand < my_cv;
+        const double cvd = lower ? cand : my_cv;
+        const bool addq = has && add != 0u;
+        const bool dec = lower && my_pos >= 0;
+        const bool try_ins = addq && my_pos < 0;
+        const bool do_ins = try_ins && cnt_l < H.capb;
+        ovf = ovf || (try_ins && !do_ins);
+        const int sl = dec ? (my_pos & 0xFFFFFF) : cnt_l;
+        const int ix = lq * H.capb + sl;
+        const bool newmin = (dec || do_ins) && BucketPQ::less(cvd, nbq, mk_l, mi_l);
+        st_pred_f64(H.bk + ix, cvd, dec || do_ins);
+        st_pred_s32(H.bi + ix, nbq, do_ins);
+        st_pred_s32(H.pos + nbq, (lq << 24) | sl, do_ins);
+        if (H.pub) st_pred_s32(H.pub + ix, nbq, do_ins);
+        st_pred_s32(H.cnt + lq, sl + 1, do_ins);
+        st_pred_s32(H.pubcnt + 32 * lq, sl + 1, do_ins);
+        st_pred_f64(H.mk + lq, cvd, newmin);
+        st_pred_s32(H.mi + lq, nbq, newmin);
+        st_pred_s32(H.msl + lq, sl, newmin);
+        st_pred_f64(a.cval + nbq, cand, lower);
+        st_pred_f64(a.ckey + nbq, cvd, dec || try_ins);
+        ins += do_ins ? 1 : 0;
+        if (addq && mc) {
+          ++mon_checks;
+          if (ms) ++mon_single;
         }
+        const unsigned lo = ((unsigned)my_nst + kVerOne) | (addq ? fl : 0u);
+        // the popped cell sits on side (d ^ 1) of its neighbour, which
+        // learns its new slot
+        const int sh = 34 + 2 * (d ^ 1);
+        st_pred_relaxed_u64(a.state + nbq,
+                            (u64)lo | (my_nst & ~((3ull << sh) | 0xFFFFFFFFull)) |
+                                ((u64)ncur << sh),
+                            has);
       }
       if (PROF) {
+        __syncwarp();
+        if (lane == 0) cyc_nbb += clock64() - t3;
         ins += __shfl_xor_sync(kFull, ins, 1);
         ins += __shfl_xor_sync(kFull, ins, 2);
         if (lane == 0) {
@@ -1121,6 +1147,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
     a.counters[43] = cyc_rescan;
     a.counters[44] = cyc_rt1;
     a.counters[45] = cyc_wait;
+    a.counters[46] = cyc_nbb;
     for (int k = 0; k < 8; ++k) a.counters[16 + k] = miss_cls[k];
     a.counters[38] = (unsigned long long)max_size;
   }
