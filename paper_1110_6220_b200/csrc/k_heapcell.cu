@@ -479,27 +479,28 @@ __device__ void scan_all(const HcArgs& a, const HTile& T, const double* before,
   int arg = 0x7fffffff;
   bool add = false, inc_viol = false, dec_viol = false;
   if (has) {
+    // the strip's node t and the node across the border, as offsets from the
+    // strip's first node (one instruction stream for the four 8-lane groups:
+    // their sides differ only in these constants)
+    const int x0 = side == EAST ? T.w - 1 : 0, y0 = side == NORTH ? T.h - 1 : 0;
+    const int step = vertical ? T.pu : 1;           // along the strip
+    const int across = side == WEST ? -1 : side == EAST ? 1 : side == SOUTH ? -T.pu : T.pu;
+    const int o0 = T.ci(x0, y0);
     for (int t = q; t < len; t += 8) {
-      int x, y, ax, ay;
-      switch (side) {
-        case WEST: x = 0; y = t; ax = -1; ay = t; break;
-        case EAST: x = T.w - 1; y = t; ax = T.w; ay = t; break;
-        case SOUTH: x = t; y = 0; ax = t; ay = -1; break;
-        default: x = t; y = T.h - 1; ax = t; ay = T.h; break;
-      }
-      const double vi = T.u(x, y);
+      const int o = o0 + t * step;
+      const double vi = T.U[o];
       if (vi > vmax) {  // first strict maximum along the strip
         vmax = vi;
         arg = t;
       }
-      const bool across_exit = T.c(ax, ay) < 0.0;
+      const bool across_exit = T.Ct[o + across] < 0.0;
       const bool changed = vi < bf[t];
-      if (!across_exit && vi < T.u(ax, ay) && (changed || (first_removal && T.c(x, y) < 0.0)))
-        add = true;
+      add = add || (!across_exit && vi < T.U[o + across] &&
+                    (changed || (first_removal && T.Ct[o] < 0.0)));
       if (t > 0) {
-        const double prev = vertical ? T.u(x, y - 1) : T.u(x - 1, y);
-        if (vi < prev) inc_viol = true;
-        if (vi > prev) dec_viol = true;
+        const double prev = T.U[o - step];
+        inc_viol = inc_viol || vi < prev;
+        dec_viol = dec_viol || vi > prev;
       }
     }
   }
@@ -883,27 +884,28 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
         tw0 = clock64();
         cyc_rt1 += (v == 0xFFFFFFFFu ? 1 : 0) + tw0 - t1a;
       }
-      // the chained record's assumed instances against the neighbours'
-      // committed ones (lanes 0-3 hold those)
-      const unsigned ctg0 = __shfl_sync(kFull, my_ctag, 0), ctg1 = __shfl_sync(kFull, my_ctag, 1);
-      const unsigned ctg2 = __shfl_sync(kFull, my_ctag, 2), ctg3 = __shfl_sync(kFull, my_ctag, 3);
       for (;;) {
-        // plain: words 0-4 on lanes 0-4; chained: words 0-6 on lanes 8-14
+        // plain: words 0-4 on lanes 0-4 (the common hit: checked first, alone)
         const unsigned ip = __shfl_sync(kFull, rw.w, 4), tp = __shfl_sync(kFull, rw.z, 4);
-        const unsigned ic = __shfl_sync(kFull, rw.w, 12), tc = __shfl_sync(kFull, rw.z, 12);
-        const bool whole_lane = !wlane || rw.w == (wkind == 0 ? ip : ic);
-        const unsigned bad = __ballot_sync(kFull, !whole_lane);
-        if ((bad & 0xFFu) == 0u && ip != kSpecNone && tag_is(tp, v)) {
+        if (__ballot_sync(kFull, lane < 5 && rw.w != ip) == 0u && ip != kSpecNone &&
+            tag_is(tp, v)) {
           kind = 0;
           break;
         }
-        if ((bad & 0xFF00u) == 0u && ic != kSpecNone && tag_is(tc, v)) {
+        // chained: words 0-6 on lanes 8-14; lane d (0-3) checks the instance
+        // the record assumed for side d against the neighbour's committed one
+        const unsigned ic = __shfl_sync(kFull, rw.w, 12), tc = __shfl_sync(kFull, rw.z, 12);
+        if (__ballot_sync(kFull, wkind == 1 && wlane && rw.w != ic) == 0u && ic != kSpecNone &&
+            tag_is(tc, v)) {
+          // dinst[0], [3] sit in .y of lanes 13 / 14, dinst[1], [2] in .z of
+          // 13 / .x of 14; the mask in .x of 13
+          const unsigned r2 = lane == 13 ? rw.z : rw.x;
           const unsigned dm = __shfl_sync(kFull, rw.x, 13);
-          const unsigned d0 = __shfl_sync(kFull, rw.y, 13), d1 = __shfl_sync(kFull, rw.z, 13);
-          const unsigned d2 = __shfl_sync(kFull, rw.x, 14), d3 = __shfl_sync(kFull, rw.y, 14);
-          const bool ok = (!(dm & 1u) || d0 == ctg0) && (!(dm & 2u) || d1 == ctg1) &&
-                          (!(dm & 4u) || d2 == ctg2) && (!(dm & 8u) || d3 == ctg3);
-          if (ok) {
+          const int src = lane < 2 ? 13 : 14;
+          const unsigned s1 = __shfl_sync(kFull, rw.y, src), s2 = __shfl_sync(kFull, r2, src);
+          const unsigned mine = (lane == 0 || lane == 3) ? s1 : s2;
+          const bool bad_side = lane < 4 && ((dm >> lane) & 1u) && mine != my_ctag;
+          if (__ballot_sync(kFull, bad_side) == 0u) {
             kind = 1;
             ++chain_hits;
             break;
