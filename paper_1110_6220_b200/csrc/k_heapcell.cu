@@ -131,6 +131,10 @@ __device__ __forceinline__ void st_pred_relaxed_u64(unsigned long long* p, unsig
       "{ .reg .pred q; setp.ne.u32 q, %2, 0; @q st.relaxed.gpu.global.u64 [%0], %1; }"
       ::"l"(p), "l"(v), "r"((unsigned)c) : "memory");
 }
+// release fence at gpu scope (a fence.acq_rel followed by a relaxed store
+// is a release pattern); lighter than __threadfence's sequentially
+// consistent MEMBAR.SC
+__device__ __forceinline__ void fence_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ bool tag_is(unsigned sv, unsigned v) {
   return sv != kSpecNone && (sv & kTagMask) == v;
 }
@@ -741,7 +745,7 @@ __device__ void publish(const HcArgs& a, int cell, int kind, u64 st, unsigned dm
                         const unsigned dinst[4], const SpecRec* stg, int lane) {
   PRec* rec = rec_ptr(a, kind, cell);
   const unsigned tag = (st_ver(st) + (unsigned)__popc(dmask)) & kTagMask;
-  __threadfence();  // the slot values (every lane's stores) before the record
+  fence_rel_gpu();  // the slot values (every lane's stores) before the record
   __syncwarp();
   if (lane == 0) {
     const unsigned n = ld_w128(&rec->w[6]).z + 1u;  // writes so far (busy holder only)
@@ -995,7 +999,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
       // the committer's own (kSelfInst | removal count)
       const int none[4] = {0, 0, 0, 0};
       process_cell(a, T, before, stg, cell, 0, st, 0u, none, 0u, lane, PROF ? prof : nullptr);
-      __threadfence();
+      fence_rel_gpu();
       __syncwarp();
       if (lane < 4) {
         rcand = stg->cand[lane];
