@@ -62,6 +62,8 @@ Knobs read_knobs() {
   k.hc_debug = gb("EIK_HC_DEBUG");
   k.hc_profile = gb("EIK_HC_PROFILE");
   k.hc_idle_ns = gi("EIK_HC_IDLE_NS", 200);
+  k.hc_first_min = gi("EIK_HC_FIRST_MIN", 2);
+  k.hc_first_min_pool = gi("EIK_HC_FIRST_MIN_POOL", 256);
   k.hc_skip_from = gi("EIK_HC_SKIP_FROM", 1);
   k.batch_sms_scale = gd("EIK_BATCH_SMS_SCALE", 0.0);
   k.batch_fmsm_ctas = std::max(1, gi("EIK_BATCH_FMSM_CTAS", 16));

@@ -146,6 +146,9 @@ struct HcArgs {
   int* owner;               // optional debug: [2][J] last claiming worker
   int* done_flag;
   int* hsize_pub;           // per-bucket queue counts for the workers, bucket b at [32 b]
+  int* pubmin;              // per-bucket minimum id for the workers (-1 empty), [32 b]
+  int first_min;            // workers wid < 32 * first_min try their bucket's minimum first ...
+  int first_min_pool;       // ... in pools of at most this many workers
   int64_t tile_doubles;     // per-warp smem
   int64_t min_smem;         // launch at least this much dynamic smem per CTA (SM-exclusive CTAs)
   unsigned long long cx_magic;

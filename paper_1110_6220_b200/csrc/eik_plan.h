@@ -154,6 +154,8 @@ struct Knobs {
   bool hc_debug = false;           // EIK_HC_DEBUG: per-worker phase trace
   bool hc_profile = false;         // EIK_HC_PROFILE: instrumented kernel
   int hc_idle_ns = 200;            // EIK_HC_IDLE_NS
+  int hc_first_min = 2;            // EIK_HC_FIRST_MIN: worker rows of 32 that chase bucket minima
+  int hc_first_min_pool = 256;     // EIK_HC_FIRST_MIN_POOL: ... in pools up to this size
   int hc_skip_from = 1;            // EIK_HC_SKIP_FROM
   // batches
   double batch_sms_scale = 0.0;    // EIK_BATCH_SMS_SCALE (0 = by the batch size)

@@ -197,7 +197,7 @@ int plan_init_cells(eik_plan* P, const eik_problem* p, const eik_cells* c) {
     P->allocs.push_back(P->dRec);
     // [0] done flag (its own line), then the 32 published bucket counts, one
     // 128-byte line each (all workers poll them)
-    if ((rc = dalloc(&P->dHcMisc, 32 + 32 * 32))) return rc;
+    if ((rc = dalloc(&P->dHcMisc, 32 + 2 * 32 * 32))) return rc;
     P->allocs.push_back(P->dHcMisc);
     if (P->method == EIK_HCM) {  // band scheduler state (hcm_band_kernel)
       if ((rc = dalloc(&P->dBInq, J))) return rc;
@@ -719,6 +719,9 @@ retry:  // after a committer heap overflow, with the heap in global memory
   a.idle_ns = kn.hc_idle_ns;
   a.done_flag = P->dHcMisc;
   a.hsize_pub = P->dHcMisc + 32;
+  a.pubmin = P->dHcMisc + 32 + 32 * 32;
+  a.first_min = kn.hc_first_min;
+  a.first_min_pool = kn.hc_first_min_pool;
   a.heap_capb_global = P->hc_capb_global;
   // cost tiles by TMA when every cell's box starts on a 16-byte column
   // (even cell width: node ib - 2 of an even ib); the maps travel with the
@@ -738,6 +741,7 @@ retry:  // after a committer heap overflow, with the heap in global memory
   // every cell size; EIK_HC_SKIP_FROM overrides)
   a.skip_from = kn.hc_skip_from;
   CK(cudaMemsetAsync(P->dHcMisc, 0, sizeof(int) * (32 + 32 * 32), P->stream));
+  CK(cudaMemsetAsync(a.pubmin, 0xFF, sizeof(int) * 32 * 32, P->stream));
   const int hc_ctas = P->cap() > 0 ? std::min(P->hc_max_ctas, P->cap()) : P->hc_max_ctas;
   int grid = 0;
   CK(launch_heapcell(a, P->hc_warps_per_cta, hc_ctas, P->stream, &launches, &grid));

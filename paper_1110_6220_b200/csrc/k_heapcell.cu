@@ -219,6 +219,7 @@ struct BucketPQ {
   int* pos;       // global [J]: bucket << 24 | slot, -1 = not queued
   int* pub;       // global [32][capb] id mirror (null: bi is global already)
   int* pubcnt;    // global count mirror, bucket l at pubcnt[32 * l] (one line each)
+  int* pubmin;    // global mirror of each bucket's minimum id (-1: empty), [32 * l]
   int size;       // entries (instrumented build only)
   __device__ static bool less(double ka, int ia, double kb, int ib) {
     return ka < kb || (ka == kb && ia < ib);
@@ -242,32 +243,9 @@ struct BucketPQ {
       mk[l] = k;
       mi[l] = id;
       msl[l] = s;
+      pubmin[32 * l] = id;
     }
     return true;
-  }
-  // The commit's variants: the bucket's count and cached minimum were loaded
-  // ahead of the commit's stores (only this lane touches the bucket now), and
-  // the entry's id is the caller's
-  __device__ bool insert_pre(int id, double k, int l, int s, double mkl, int mil) {
-    if (s >= capb) return false;
-    set(l, s, k, id);
-    cnt[l] = s + 1;
-    pubcnt[32 * l] = s + 1;
-    if (less(k, id, mkl, mil)) {
-      mk[l] = k;
-      mi[l] = id;
-      msl[l] = s;
-    }
-    return true;
-  }
-  __device__ void decrease_pre(int enc, double k, int id, double mkl, int mil) {
-    const int l = enc >> 24, s = enc & 0xFFFFFF;
-    bk[l * capb + s] = k;
-    if (less(k, id, mkl, mil)) {
-      mk[l] = k;
-      mi[l] = id;
-      msl[l] = s;
-    }
   }
   __device__ void decrease(int enc, double k) {  // one lane per bucket; keys only decrease
     const int l = enc >> 24, s = enc & 0xFFFFFF;
@@ -277,6 +255,7 @@ struct BucketPQ {
       mk[l] = k;
       mi[l] = id;
       msl[l] = s;
+      pubmin[32 * l] = id;
     }
   }
   // all lanes: the minimum's id (or -1 when empty) and its bucket in w_out;
@@ -341,6 +320,7 @@ struct BucketPQ {
       mk[w] = kw;
       mi[w] = (int)mid;
       msl[w] = sw;
+      pubmin[32 * w] = n > 0 ? (int)mid : -1;
     }
     __syncwarp();
   }
@@ -1085,6 +1065,7 @@ __device__ void committer(const HcArgs& a, BucketPQ& H, HTile& T, double* before
         st_pred_f64(H.mk + lq, cvd, newmin);
         st_pred_s32(H.mi + lq, nbq, newmin);
         st_pred_s32(H.msl + lq, sl, newmin);
+        st_pred_s32(H.pubmin + 32 * lq, nbq, newmin);
         st_pred_f64(a.cval + nbq, cand, lower);
         st_pred_f64(a.ckey + nbq, cvd, dec || try_ins);
         ins += do_ins ? 1 : 0;
@@ -1295,9 +1276,13 @@ __device__ __forceinline__ bool key_before(double ka, int a_id, double kb, int b
 //   2. chained speculations of c's neighbours that c's commit will queue or
 //      move up (the front's next cells), on c and on their other neighbours
 //      queued above them.
+__device__ bool pick_job_cell(const HcArgs& a, int cell, Job& j, int wid);
 __device__ bool pick_job(const HcArgs& a, int pidx, Job& j, int wid) {
   const int cell = ld_relaxed_s32(a.harr + pidx);
   if (cell < 0 || cell >= a.J) return false;
+  return pick_job_cell(a, cell, j, wid);
+}
+__device__ bool pick_job_cell(const HcArgs& a, int cell, Job& j, int wid) {
   int nbs[4];
   cell_nbs(a, cell, nbs);
   u64 st = ld_relaxed_u64_nb(a.state + cell);
@@ -1433,6 +1418,7 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
     H.cnt = H.msl + 32;
     H.pos = a.hpos;
     H.pubcnt = a.hsize_pub;  // bucket counts, one 128-byte line each
+    H.pubmin = a.pubmin;
     H.size = 0;
     if (wib == 1) {
       queue_helper(a, H, lane);
@@ -1452,57 +1438,66 @@ __global__ void heapcell_spec_kernel(HcArgs a) {
   const int wpc = blockDim.x >> 5;
   const int wid = (blockIdx.x - 1) * wpc + wib;
   const int nworkers = (gridDim.x - 1) * wpc;
+  // small pools (the batch's slices) leave the cells about to be popped
+  // unspeculated while the workers walk the buckets: some of them chase the
+  // buckets' minima (FHCM/8 on 6 CTAs 345 -> 233 ms); in the full-device pool
+  // every queued cell is covered anyway and chasing only re-speculates
+  // (148 CTAs: 169 -> 174 ms)
+  const bool first_min = nworkers <= a.first_min_pool && (wid >> 5) < a.first_min;
   unsigned polls = 0;
   for (;;) {
-    // lane 0 reads the shared words and broadcasts them: lanes reading them
-    // independently could see different values, run different trip counts
-    // and meet at mismatched warp collectives (a deadlock)
     int done = 0;
     if (lane == 0 && (++polls & 7) == 0) done = ld_relaxed_s32(a.done_flag);  // 1 poll in 8
     if (__shfl_sync(kFull, done, 0)) return;
-    // queued cells: bucket b's entries [b*pub_capb, b*pub_capb + count_b) of
-    // the mirror; workers spread over the buckets, then over their slots
-    bool worked = false;
-    const bool wide = nworkers >= 32;
-    for (int bkt = wide ? (wid & 31) : wid; bkt < 32 && !worked; bkt += wide ? 32 : nworkers) {
-      int nb = 0;
-      if (lane == 0) nb = ld_relaxed_s32(a.hsize_pub + 32 * bkt);
-      nb = __shfl_sync(kFull, nb, 0);
-      const int sstep = wide ? (nworkers >> 5) : 1;
-    for (int sl = wide ? (wid >> 5) : 0; sl < nb; sl += sstep) {
-      const int pidx = bkt * a.pub_capb + sl;
-      Job j;
-      int got = 0;
-      if (lane == 0) got = pick_job(a, pidx, j, wid) ? 1 : 0;
-      if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 2] = 100 + got;
-      if (!__shfl_sync(kFull, got, 0)) continue;
-      if (lane == 0 && a.wdbg) {
-        a.wdbg[4 * wid + 0] = 1;
-        a.wdbg[4 * wid + 1] = j.cell;
-        a.wdbg[4 * wid + 2] = j.kind;
-        a.wdbg[4 * wid + 3] = (int)(clock64() >> 10);
-        a.owner[(size_t)j.kind * a.J + j.cell] = 0x70000 | wid;
+    // Lane 0 alone chooses the job and broadcasts it (lanes reading the
+    // shared words independently could see different values, run different
+    // trip counts and meet at mismatched warp collectives: a deadlock).  A small pool of workers first tries
+    // its bucket's current minimum -- a cell about to be popped -- then, as
+    // every pool does, the queued cells: bucket b's entries [b*pub_capb,
+    // b*pub_capb + count_b) of the mirror, workers spread over the buckets,
+    // then over their slots.
+    Job j;
+    int got = 0;
+    if (lane == 0) {
+      const bool wide = nworkers >= 32;
+      if (first_min) {
+        const int c = ld_relaxed_s32(a.pubmin + 32 * (wid & 31));
+        if (c >= 0 && c < a.J) got = pick_job_cell(a, c, j, wid) ? 1 : 0;
       }
-      j.cell = __shfl_sync(kFull, j.cell, 0);
-      j.kind = __shfl_sync(kFull, j.kind, 0);
-      j.st = __shfl_sync(kFull, j.st, 0);
-      j.omask = __shfl_sync(kFull, j.omask, 0);
-      j.cflags = __shfl_sync(kFull, j.cflags, 0);
+      for (int bkt = wide ? (wid & 31) : wid; bkt < 32 && !got; bkt += wide ? 32 : nworkers) {
+        const int nb = ld_relaxed_s32(a.hsize_pub + 32 * bkt);
+        const int sstep = wide ? (nworkers >> 5) : 1;
+        for (int sl = wide ? (wid >> 5) : 0; sl < nb && !got; sl += sstep)
+          got = pick_job(a, bkt * a.pub_capb + sl, j, wid) ? 1 : 0;
+      }
+    }
+    if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 2] = 100 + got;
+    if (!__shfl_sync(kFull, got, 0)) {
+      __nanosleep(a.idle_ns);
+      continue;
+    }
+    if (lane == 0 && a.wdbg) {
+      a.wdbg[4 * wid + 0] = 1;
+      a.wdbg[4 * wid + 1] = j.cell;
+      a.wdbg[4 * wid + 2] = j.kind;
+      a.wdbg[4 * wid + 3] = (int)(clock64() >> 10);
+      a.owner[(size_t)j.kind * a.J + j.cell] = 0x70000 | wid;
+    }
+    j.cell = __shfl_sync(kFull, j.cell, 0);
+    j.kind = __shfl_sync(kFull, j.kind, 0);
+    j.st = __shfl_sync(kFull, j.st, 0);
+    j.omask = __shfl_sync(kFull, j.omask, 0);
+    j.cflags = __shfl_sync(kFull, j.cflags, 0);
 #pragma unroll
-      for (int d = 0; d < 4; ++d) {
-        j.oslot[d] = __shfl_sync(kFull, j.oslot[d], 0);
-        j.dinst[d] = __shfl_sync(kFull, j.dinst[d], 0);
-      }
-      if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 13;
-      process_cell(a, T, before, stg, j.cell, j.kind, j.st, j.omask, j.oslot, j.cflags, lane);
-      if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 2;
-      publish(a, j.cell, j.kind, j.st, j.omask, j.dinst, stg, lane);
-      if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 3;
-      worked = true;
-      break;
+    for (int d = 0; d < 4; ++d) {
+      j.oslot[d] = __shfl_sync(kFull, j.oslot[d], 0);
+      j.dinst[d] = __shfl_sync(kFull, j.dinst[d], 0);
     }
-    }
-    if (!worked) __nanosleep(a.idle_ns);
+    if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 13;
+    process_cell(a, T, before, stg, j.cell, j.kind, j.st, j.omask, j.oslot, j.cflags, lane);
+    if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 2;
+    publish(a, j.cell, j.kind, j.st, j.omask, j.dinst, stg, lane);
+    if (lane == 0 && a.wdbg) a.wdbg[4 * wid + 0] = 3;
   }
 }
 
