@@ -52,6 +52,7 @@ Knobs read_knobs() {
   trace_path = std::getenv("EIK_TRACE_FSM") ? std::getenv("EIK_TRACE_FSM") : "";
   k.fsm_trace = trace_path.empty() ? nullptr : trace_path.c_str();
   k.fsm_wpc = gi("EIK_FSM_WPC", 0);
+  k.fsm_sb = gi("EIK_FSM_SB", 1);
   k.hc_warps = gi("EIK_HC_WARPS", 0);
   k.hc_min_smem = std::getenv("EIK_HC_MIN_SMEM") ? std::atol(std::getenv("EIK_HC_MIN_SMEM")) : -1;
   k.hc_global_heap = gb("EIK_HC_GLOBAL_HEAP");
@@ -463,6 +464,9 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
     if ((rc = dalloc(&P->dChg, nchg))) return rc;
     track(P->dChg);
     CK(cudaMemsetAsync(P->dChg, 0, sizeof(unsigned) * nchg, P->stream));
+    P->nsb = fsm_nsb(P->g.m);
+    if ((rc = dalloc(&P->dSb, (size_t)4 * P->nstrips * P->nsb))) return rc;
+    track(P->dSb);
   } else {
     if ((rc = plan_init_cells(P, p, c))) return rc;
   }
@@ -497,6 +501,8 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   a.part_strips = 0;
   a.snap = nullptr;
   a.lsm_cnt = P->method == EIK_LSM ? P->dLsmCnt : nullptr;
+  a.sb = knobs().fsm_sb ? P->dSb : nullptr;
+  a.nsb = P->nsb;
   if (P->part_strips > 0 && P->part_strips < P->nstrips) {
     const int nb = (P->nstrips - 1) / P->part_strips;
     const int64_t need = (int64_t)2 * nb * 2 * P->pitch;
@@ -513,6 +519,7 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
     }
     a.part_strips = P->part_strips;
     a.snap = P->dSnap;
+    a.sb = nullptr;  // part edges exchange snapshot rows every block
   }
   if (knobs().fsm_trace) {
     if (!P->dTrace) {
@@ -528,6 +535,7 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   CK(cudaEventRecord(P->ev0, P->stream));
   CK(cudaMemsetAsync(P->dProg, 0, sizeof(unsigned long long) * P->nstrips, P->stream));
   CK(cudaMemsetAsync(P->dMbox, 0xFF, sizeof(double) * 2 * P->nstrips * P->pitch, P->stream));
+  if (a.sb) CK(cudaMemsetAsync(P->dSb, 0, sizeof(unsigned) * 4 * P->nstrips * P->nsb, P->stream));
   // only the sweeps that can run need clearing; bound by the previous run
   size_t clear = (size_t)std::min<int64_t>(P->max_sweeps, P->last_sweeps_bound);
   CK(cudaMemsetAsync(P->dChanged, 0, sizeof(int) * clear, P->stream));
@@ -586,8 +594,8 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
         for (int b = 0; b < P->nstrips; ++b) {
           const unsigned long long* t = &tr[((size_t)k * P->nstrips + b) * kTraceWords];
           if (t[0])
-            std::fprintf(f, "%d %d %llu %llu %llu %llu %llu\n", k, b, t[0], t[1], t[2], t[3],
-                         t[4]);
+            std::fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu\n", k, b, t[0], t[1], t[2], t[3],
+                         t[4], t[5]);
         }
       std::fclose(f);
     }
@@ -699,6 +707,8 @@ int plan_sweep_impl(eik_plan* P, int64_t first_sweep, int count, int* changed, i
   a.part_strips = 0;  // sweep-level control is one Gauss-Seidel wavefront
   a.snap = nullptr;
   a.lsm_cnt = nullptr;
+  a.sb = knobs().fsm_sb ? P->dSb : nullptr;
+  a.nsb = P->nsb;
   // the flags this call leaves in [0, count) must be cleared by a later run
   P->last_sweeps_bound = std::min<int64_t>(P->max_sweeps,
                                            std::max<int64_t>(P->last_sweeps_bound, count + 8));
@@ -707,6 +717,7 @@ int plan_sweep_impl(eik_plan* P, int64_t first_sweep, int count, int* changed, i
   if (!changed_dev) CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, s));
   CK(cudaMemsetAsync(P->dProg, 0, sizeof(unsigned long long) * P->nstrips, s));
   CK(cudaMemsetAsync(P->dMbox, 0xFF, sizeof(double) * 2 * P->nstrips * P->pitch, s));
+  if (a.sb) CK(cudaMemsetAsync(P->dSb, 0, sizeof(unsigned) * 4 * P->nstrips * P->nsb, s));
   CK(cudaMemsetAsync(P->dChanged, 0, sizeof(int) * count, s));
   CK(cudaMemsetAsync(P->dDone, 0, sizeof(int) * count, s));
   CK(launch_fsm(a, s, &launches));

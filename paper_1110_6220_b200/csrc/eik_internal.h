@@ -48,11 +48,23 @@ struct FsmArgs {
   // also counts the nodes the reference's locking sweep processes
   // (lsm_cnt[k] += unlocked nodes of sweep k).  Values and sweeps are FSM's.
   unsigned long long* lsm_cnt;
+  // Super-block skipping (k_fsm.cu): a strip's sweep is cut into super-blocks
+  // of kFsmSbBlocks blocks; sb holds [2][nstrips][nsb] per-sweep-parity update
+  // summaries (bit 0 any row, bit 1 the strip's lowest row, bit 2 its highest)
+  // followed by [2][nstrips][nsb] edge tokens per row direction (sweep stamp
+  // << 2 | state; zeroed before every launch).  Null: no super-block skipping.
+  unsigned* sb;
+  int nsb;
 };
+constexpr int kFsmSbBlocks = 4;    // blocks of 8 steps per super-block (32 steps)
+inline int fsm_nsb(int64_t m) {
+  const int64_t nblocks = (m + 31 + 7) / 8;
+  return (int)((nblocks + kFsmSbBlocks - 1) / kFsmSbBlocks);
+}
 constexpr int64_t kChgWordOff = 3;
 constexpr int64_t kChgWordPad = 8;  // pad words per row (kChgWordOff before, the rest after)
 constexpr int kTraceSweeps = 16;
-constexpr int kTraceWords = 5;  // start, body start, end, polls, compute steps
+constexpr int kTraceWords = 6;  // start, body start, end, polls, compute steps, skipped super-blocks
 
 // Cell decomposition as seen by the device (build_cells, cells.cpp:32-47):
 // cell (cx,cy) spans columns [cx*base_x, cx==cells_x-1 ? m : (cx+1)*base_x).

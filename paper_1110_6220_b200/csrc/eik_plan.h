@@ -49,6 +49,8 @@ struct eik_plan {
   int* dChanged = nullptr;
   unsigned* dChg = nullptr;   // [2][n+3][chg_cw] change bits (k_fsm.cu)
   int64_t chg_cw = 0;
+  unsigned* dSb = nullptr;    // [4][nstrips][nsb] super-block summaries + edge tokens (k_fsm.cu)
+  int nsb = 0;
   int part_strips = 0;        // strip-Jacobi parts (eik_plan_set_partitions), 0 = exact GS
   double* dSnap = nullptr;    // [2][boundaries][2] padded rows
   int64_t snap_count = 0;
@@ -143,6 +145,7 @@ struct Knobs {
   bool fsm_noskip = false;         // EIK_FSM_NOSKIP: evaluate every node
   const char* fsm_trace = nullptr; // EIK_TRACE_FSM=path: per-strip timing trace (copied)
   int fsm_wpc = 0;                 // EIK_FSM_WPC: strips per CTA (0 = auto)
+  int fsm_sb = 1;                  // EIK_FSM_SB=0: no super-block skipping
   // heap-cell replay
   int hc_warps = 0;                // EIK_HC_WARPS (0 = fit)
   long hc_min_smem = -1;           // EIK_HC_MIN_SMEM (-1 = 116 KB)

@@ -66,6 +66,54 @@ __device__ __forceinline__ double poll_slot(const double* p, int* status) {
   return __longlong_as_double((long long)v);
 }
 
+__device__ __forceinline__ unsigned ld_relaxed_u32(const void* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Super-block skipping.  A strip's sweep is cut into super-blocks of kSB
+// blocks (kSbCols steps).  In sparse late sweeps most of them are clean: no
+// node of the strip's rows (or of the two adjoining edge rows) changed in the
+// previous sweep around their columns, no update is in flight inside the
+// strip, and the upwind strip's edge row does not change over them in this
+// sweep.  Every one of their 8-step blocks would then only forward old values
+// (the block-level rule below), so the strip passes over the whole
+// super-block without streaming u, C or the change bits: it copies its own
+// edge row into the downwind mailbox, re-arms the upwind slots, zeroes its
+// change bits and publishes
+//   * a summary word per (sweep parity, strip, super-block): bit 0 = some node
+//     updated, bit 1 / 2 = the strip's lowest / highest row updated -- read by
+//     the next sweep's decision of this strip and its two neighbours;
+//   * an edge token per (row direction, strip, super-block) = sweep stamp << 2
+//     | state (2: edge row unchanged over the super-block, 3: changed), written
+//     after the mailbox values it covers -- read by the downwind strip.
+// Lane 0 of the downwind strip visits column q one step after... 31 steps
+// before the upwind strip's lane 31 finishes the super-block holding q, so a
+// strip needs the upwind tokens g and g+1 to skip its super-block g.  The
+// decision only selects between two schedules with the same result.
+constexpr int kSB = kFsmSbBlocks;
+constexpr int kSbCols = kSB * kU;
+constexpr int kSbShift = kSbCols == 32 ? 5 : (kSbCols == 64 ? 6 : (kSbCols == 128 ? 7 : 8));
+static_assert((1 << kSbShift) == kSbCols && kSbCols >= 32, "super-block: 32..256 steps, power of two");
+
+struct SbCtx {
+  bool pub;                // summaries and tokens are kept (a.sb != null)
+  bool skip;               // this sweep may skip (not a forced sweep)
+  bool block;              // wait for the upwind tokens (sparse regime) or only look
+  bool has_lo, has_hi;     // strips b-1 / b+1 exist
+  bool prev_iasc;          // column direction of the previous sweep
+  bool lo_is_lane0;        // lane 0 owns the strip's lowest row (jasc)
+  int k, flow, b;          // sweep, row direction (mailbox / token set), strip
+};
+// [2][nstrips][nsb] summaries by sweep parity, then [2][nstrips][nsb] tokens by row direction
+__device__ __forceinline__ unsigned* sb_sum(const FsmArgs& a, int par, int b) {
+  return a.sb + ((int64_t)par * a.nstrips + b) * a.nsb;
+}
+__device__ __forceinline__ unsigned* sb_tok(const FsmArgs& a, int flow, int b) {
+  return a.sb + ((int64_t)(2 + flow) * a.nstrips + b) * a.nsb;
+}
+
 struct Chan {
   double* gin;            // global mailbox row of the upwind strip (or the dummy row)
   double* gout;           // global mailbox row to the downwind strip (or dummy)
@@ -162,7 +210,8 @@ template <bool IASC, bool LSM>
 __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t rowp,
                                             const Chan& ch, const unsigned* crd, unsigned* cwr,
                                             unsigned force, unsigned long long* tr, int dprev,
-                                            bool jasc, unsigned long long& lcnt) {
+                                            bool jasc, unsigned long long& lcnt, const SbCtx& sb,
+                                            unsigned& ncomp_out) {
   constexpr int S = IASC ? 1 : -1;
   const int64_t m = a.m, cw = a.cw;
   const int64_t P = a.P;
@@ -186,24 +235,12 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
     const int64_t q = (int64_t)b * kU - lane;
     return IASC ? q : m - 1 - q - (kU - 1);
   };
-  const ChgWin w0 = ld_chgwin(crow, cw, lo_of(0) - 1);
-  unsigned pm = force ? force : chg_mask<IASC>(w0);
   // LSM: previous-sweep direction (dprev < 0: sweep 0 of the solve)
   const bool iasc_prev = dprev == 0 || dprev == 1, jasc_prev = dprev == 0 || dprev == 3;
-  unsigned lmc = 0, lmr = 0;
-  if (LSM && dprev >= 0) lsm_masks<IASC>(w0, iasc_prev, jasc_prev, lmc, lmr);
-  ChgWin wa = ld_chgwin(crow, cw, lo_of(1) - 1);
-  ChgWin wb = ld_chgwin(crow, cw, lo_of(2) - 1);
-
+  unsigned pm = 0, lmc = 0, lmr = 0;
+  ChgWin wa, wb;
   double cu[kU + 1], cc[kU], hv[kU];
   double nu[kU + 1], nc[kU], nh[kU];
-#pragma unroll
-  for (int t = 0; t <= kU; ++t) cu[t] = pu[S * t];
-#pragma unroll
-  for (int t = 0; t < kU; ++t) {
-    cc[t] = __ldg(pc + S * t);
-    hv[t] = halo_lane ? __ldcg(ph + S * t) : kInf;
-  }
   double res_prev = kInf;
   bool upd_prev = false, changed = false;
   int q0 = -lane;
@@ -211,9 +248,165 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
   // change bits of the word holding the next column to visit
   int64_t wcur = (IASC ? (int64_t)-lane : m - 1 + lane) >> 5;
   unsigned acc = 0;
-  unsigned npoll = 0, ncomp = 0;
+  unsigned npoll = 0, ncomp = 0, nskip = 0;
 
-  for (int blk = 0; blk < nblocks; ++blk) {
+  // (re)start the register pipeline at block blk: at the sweep's start and
+  // after skipped super-blocks (the lane's previous column is old there)
+  auto prime = [&](int blk) {
+    const ChgWin w0 = ld_chgwin(crow, cw, lo_of(blk) - 1);
+    pm = force ? force : chg_mask<IASC>(w0);
+    if (LSM && dprev >= 0) lsm_masks<IASC>(w0, iasc_prev, jasc_prev, lmc, lmr);
+    wa = ld_chgwin(crow, cw, lo_of(blk + 1) - 1);
+    wb = ld_chgwin(crow, cw, lo_of(blk + 2) - 1);
+#pragma unroll
+    for (int t = 0; t <= kU; ++t) cu[t] = pu[S * t];
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {
+      cc[t] = __ldg(pc + S * t);
+      hv[t] = halo_lane ? __ldcg(ph + S * t) : kInf;
+    }
+    res_prev = pu[-S];  // padding (+inf) ahead of the row's first column
+    upd_prev = false;
+  };
+
+  // this block's change bits into the row's words (absolute columns lo..lo+7)
+  auto put_bits = [&](int blk, unsigned um) {
+    const int64_t lo = lo_of(blk);
+    const unsigned ub = IASC ? um : (__brev(um) >> 24);
+    const int64_t wl = lo >> 5;
+    const unsigned long long x = (unsigned long long)ub << (lo & 31);
+    const unsigned lowp = (unsigned)x, highp = (unsigned)(x >> 32);
+    const int64_t wn = (IASC ? lo + kU : lo - 1) >> 5;  // word of the next column
+    if (IASC) {
+      acc |= lowp;
+      if (wn != wl) {
+        __stcg(wrow + wl, acc);
+        acc = highp;
+      }
+    } else if (wcur != wl) {  // straddles: word wl+1 first, then wl
+      __stcg(wrow + wcur, acc | highp);
+      acc = lowp;
+    } else {
+      acc |= lowp;
+      if (wn != wl) {
+        __stcg(wrow + wl, acc);
+        acc = 0;
+      }
+    }
+    wcur = wn;
+  };
+
+  // ---- super-block skipping (see SbCtx) ----------------------------------
+  const unsigned stamp = (unsigned)(sb.k + 1) << 2;
+  // did the previous sweep update anything around super-block g (the strip's
+  // rows and the adjoining edge rows, one column wider on each side)?
+  auto sum_dirty = [&](int g) -> bool {
+    int64_t lo = (int64_t)g * kSbCols - 32, hi = (int64_t)g * kSbCols + kSbCols;
+    if (sb.prev_iasc != IASC) {
+      const int64_t t = m - 1 - hi;
+      hi = m - 1 - lo;
+      lo = t;
+    }
+    // the previous sweep's super-block g' holds its sweep-order columns
+    // [kSbCols g' - 31, kSbCols g' + kSbCols - 1]
+    int64_t g0 = lo >> kSbShift, g1 = (hi + 31) >> kSbShift;
+    if (g0 < 0) g0 = 0;
+    if (g1 > a.nsb - 1) g1 = a.nsb - 1;
+    unsigned v = 0;
+    // at most 4 of them: (kSbCols + 32 + 31) / kSbCols < 3 for kSbCols >= 32
+    if (lane < 12) {
+      const int ds = lane / 4 - 1;
+      const int64_t gi = g0 + lane % 4;
+      const bool valid = gi <= g1 && (ds == 0 || (ds < 0 ? sb.has_lo : sb.has_hi));
+      const unsigned mask = ds == 0 ? 1u : (ds < 0 ? 4u : 2u);  // b-1: its highest row; b+1: its lowest
+      if (valid) v = __ldcg(sb_sum(a, (sb.k + 1) & 1, sb.b + ds) + gi) & mask;
+    }
+    return __any_sync(kFull, v != 0u);
+  };
+  // Pass over the super-block starting at block blk if the upwind edge row
+  // does not change over it (its local conditions hold already).  On success
+  // the per-lane pointers stand at the next super-block.
+  auto try_skip = [&](int blk) -> bool {
+    const int g = blk / kSB;
+    const int nb = nblocks - blk < kSB ? nblocks - blk : kSB;
+    // element q of lane 31's row / of the mailboxes, from the lanes' own pointers
+    const int64_t q0_31 = (int64_t)q0 + lane - 31, q0_0 = (int64_t)q0 + lane;
+    const double* edge_q0 = (const double*)__shfl_sync(kFull, (unsigned long long)pu, 31);
+    double* gout_q0 = (double*)__shfl_sync(kFull, (unsigned long long)po, 31);
+    double* gin_q0 = (double*)__shfl_sync(kFull, (unsigned long long)ph, 0);
+    const int64_t qe0 = (int64_t)g * kSbCols - 31 + lane;  // lane 31's columns, spread over the warp
+    double ev[kSbCols / 32];
+    if (ch.out_glob) {
+#pragma unroll
+      for (int j = 0; j < kSbCols / 32; ++j) {
+        const int64_t q = qe0 + 32 * j;
+        ev[j] = (q >= 0 && q < m) ? __ldcg(edge_q0 + S * (q - q0_31)) : 0.0;
+      }
+    }
+    if (ch.in_glob) {
+      unsigned tk = stamp | 2u;
+      const int gi = g + lane;
+      if (lane < 2 && gi < a.nsb) {
+        const unsigned* tp = sb_tok(a, sb.flow, sb.flow ? sb.b + 1 : sb.b - 1) + gi;
+        tk = ld_relaxed_u32(tp);
+        if (sb.block) {
+          long long spins = 0;
+          while ((tk >> 2) != (stamp >> 2)) {
+            if (++spins > kSpinCap) {
+              atomicExch(a.status, kStatusWatchdog);
+              break;
+            }
+            if ((spins & 1023) == 0 && *(volatile int*)a.status == kStatusWatchdog) break;
+            tk = ld_relaxed_u32(tp);
+          }
+        }
+      }
+      if (__any_sync(kFull, tk != (stamp | 2u))) return false;
+      // re-arm the upwind slots of lane 0's columns (their values have landed:
+      // the tokens are written after them)
+#pragma unroll
+      for (int j = 0; j < kSbCols / 32; ++j) {
+        const int64_t q = (int64_t)g * kSbCols + lane + 32 * j;
+        if (q < m) __stcg(gin_q0 + S * (q - q0_0), sent);
+      }
+    }
+    if (ch.out_glob) {
+#pragma unroll
+      for (int j = 0; j < kSbCols / 32; ++j) {
+        const int64_t q = qe0 + 32 * j;
+        if (q >= 0 && q < m) __stcg(gout_q0 + S * (q - q0_31), ev[j]);
+      }
+      __threadfence();  // the values before the token
+      __syncwarp();
+      if (lane == 0) __stcg(sb_tok(a, sb.flow, sb.b) + g, stamp | 2u);
+    }
+    if (lane == 0) __stcg(sb_sum(a, sb.k & 1, sb.b) + g, 0u);
+    for (int j = 0; j < nb; ++j) put_bits(blk + j, 0u);
+    pu += S * kU * nb;
+    pc += S * kU * nb;
+    ph += S * kU * nb;
+    po += S * kU * nb;
+    q0 += kU * nb;
+    ++nskip;
+    return true;
+  };
+
+  unsigned sb_um = 0;
+  int blk = 0;
+  // Outer loop: a run of skipped super-blocks, then a run of computed blocks
+  // with the register pipeline primed once (the pipeline is dead across the
+  // skip phase, so the skip code shares its registers).
+  bool local_clean = sb.skip && !sum_dirty(0);
+  for (;;) {
+    if (local_clean) {
+      while (try_skip(blk)) {
+        blk += kSB;
+        if (blk >= nblocks || sum_dirty(blk / kSB)) break;
+      }
+      if (blk >= nblocks) break;
+    }
+    prime(blk);
+    for (;;) {
     {
       // land the previous prefetch before issuing the next one: the steps
       // below then never wait on a scoreboard shared with fresh loads
@@ -351,31 +544,24 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
         upd_prev = false;
       }
     }
-    // this block's change bits into the row's words (absolute columns lo..lo+7)
-    {
-      const int64_t lo = lo_of(blk);
-      const unsigned ub = IASC ? um : (__brev(um) >> 24);
-      const int64_t wl = lo >> 5;
-      const unsigned long long x = (unsigned long long)ub << (lo & 31);
-      const unsigned lowp = (unsigned)x, highp = (unsigned)(x >> 32);
-      const int64_t wn = (IASC ? lo + kU : lo - 1) >> 5;  // word of the next column
-      if (IASC) {
-        acc |= lowp;
-        if (wn != wl) {
-          __stcg(wrow + wl, acc);
-          acc = highp;
+    put_bits(blk, um);
+    if (sb.pub) {
+      // end of a super-block: its summary for the next sweep's decisions and
+      // the edge token for the downwind strip
+      sb_um |= um;
+      if (((blk + 1) & (kSB - 1)) == 0 || blk + 1 == nblocks) {
+        const unsigned bal = __ballot_sync(kFull, sb_um != 0u);
+        const bool e0 = bal & 1u, e31 = (bal >> 31) & 1u;
+        const int g = blk / kSB;
+        if (lane == 0)
+          __stcg(sb_sum(a, sb.k & 1, sb.b) + g, (bal ? 1u : 0u) | ((sb.lo_is_lane0 ? e0 : e31) ? 2u : 0u) |
+                                   ((sb.lo_is_lane0 ? e31 : e0) ? 4u : 0u));
+        if (out_g) {  // lane 31 wrote the mailbox values itself
+          if (!e31) __threadfence();
+          __stcg(sb_tok(a, sb.flow, sb.b) + g, stamp | (e31 ? 3u : 2u));
         }
-      } else if (wcur != wl) {  // straddles: word wl+1 first, then wl
-        __stcg(wrow + wcur, acc | highp);
-        acc = lowp;
-      } else {
-        acc |= lowp;
-        if (wn != wl) {
-          __stcg(wrow + wl, acc);
-          acc = 0;
-        }
+        sb_um = 0;
       }
-      wcur = wn;
     }
     pm = pm_next;
     if (LSM) {
@@ -396,12 +582,25 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       cc[t] = nc[t];
       hv[t] = nh[t];
     }
+    ++blk;
+    if (blk >= nblocks) break;
+    // at a super-block boundary with no update in flight and nothing changed
+    // around the next super-block: leave the pipeline for the skip phase
+    if (sb.skip && (blk & (kSB - 1)) == 0 && !__any_sync(kFull, upd_prev) &&
+        !sum_dirty(blk / kSB)) {
+      local_clean = true;
+      break;
+    }
+    }
+    if (blk >= nblocks) break;
   }
   __stcg(wrow + wcur, acc);
   if (tr && lane == 0) {
     tr[3] = npoll;
     tr[4] = ncomp;
+    tr[5] = nskip;
   }
+  ncomp_out = ncomp;
   return changed;
 }
 
@@ -413,6 +612,7 @@ fsm_wavefront_kernel(FsmArgs a) {
   const int b = blockIdx.x * (blockDim.x >> 5) + w;
   if (b >= a.nstrips) return;  // warps past the last grid row do not exist
   const int64_t n = a.n, P = a.P;
+  unsigned prev_comp = ~0u;  // steps this strip computed in its previous sweep
 
   for (int k = 0;; ++k) {
     // ---- stop decision: identical in every strip --------------------------
@@ -504,9 +704,33 @@ fsm_wavefront_kernel(FsmArgs a) {
     const unsigned force = (k == 0 || a.noskip) ? 0xFFu : 0u;
     const int dprev = k == 0 ? -1 : ((a.first_sweep + k - 1) & 3);
     unsigned long long lcnt = 0;
+    SbCtx sb;
+    sb.pub = a.sb != nullptr;
+#ifdef SB_NOSKIP
+    sb.skip = false;
+#else
+    sb.skip = sb.pub && !force;
+#endif
+#ifdef SB_NOPUB
+    sb.pub = false;
+#endif
+    // sparse regime (under a quarter of the strip's steps computed last
+    // sweep): wait for the upwind tokens; otherwise only use them if present
+    sb.block = prev_comp < (unsigned)((a.m + 31) / 4);
+    sb.prev_iasc = dprev == 0 || dprev == 1;
+    sb.lo_is_lane0 = jasc;
+    sb.has_lo = b > 0;
+    sb.has_hi = b + 1 < a.nstrips;
+    sb.k = k;
+    sb.flow = flow;
+    sb.b = b;
+    unsigned ncomp = 0;
     const bool changed =
-        iasc ? sweep_strip<true, LSM>(a, lane, rowp, ch, crd, cwr, force, tr, dprev, jasc, lcnt)
-             : sweep_strip<false, LSM>(a, lane, rowp, ch, crd, cwr, force, tr, dprev, jasc, lcnt);
+        iasc ? sweep_strip<true, LSM>(a, lane, rowp, ch, crd, cwr, force, tr, dprev, jasc, lcnt, sb,
+                                      ncomp)
+             : sweep_strip<false, LSM>(a, lane, rowp, ch, crd, cwr, force, tr, dprev, jasc, lcnt, sb,
+                                       ncomp);
+    prev_comp = __shfl_sync(kFull, ncomp, 0);
     if (*(volatile int*)a.status == kStatusWatchdog) return;
     if (LSM) {
 #pragma unroll
