@@ -188,6 +188,60 @@ __device__ __forceinline__ void lsm_masks(const ChgWin& w, bool iasc_prev, bool 
   mr = IASC ? r : (__brev(r) >> 24);
 }
 
+// Dirty map of a strip's super-blocks for one sweep, built once at the
+// sweep's start (after both neighbouring strips finished the previous sweep)
+// into the warp's shared-memory words: bit g = something changed in the
+// previous sweep around super-block g (the strip's rows and the adjoining edge
+// rows, one column wider on each side), i.e. the super-block is not locally
+// clean.  prevw: scratch for the previous sweep's bits in its own order.
+constexpr int kMapWords = 64;  // super-blocks per row <= 2048 (host: larger grids keep sb off)
+template <bool IASC>
+__device__ __forceinline__ void sb_build_map(const FsmArgs& a, const SbCtx& sb, int lane,
+                                             unsigned* prevw, unsigned* curw) {
+  const int nsb = a.nsb, nw = (nsb + 31) >> 5;
+  const unsigned* s0 = sb_sum(a, (sb.k + 1) & 1, sb.b);
+  const unsigned* slo = s0 - nsb;  // strip b-1: its highest row (bit 2)
+  const unsigned* shi = s0 + nsb;  // strip b+1: its lowest row (bit 1)
+  for (int j = 0; j < nw; ++j) {
+    const int g = 32 * j + lane;
+    unsigned v = 0;
+    if (g < nsb) {
+      v = __ldcg(s0 + g) & 1u;
+      if (sb.has_lo) v |= __ldcg(slo + g) & 4u;
+      if (sb.has_hi) v |= __ldcg(shi + g) & 2u;
+    }
+    const unsigned w = __ballot_sync(kFull, v != 0u);
+    if (lane == 0) prevw[j] = w;
+  }
+  if (lane == 0) prevw[nw] = 0u;
+  __syncwarp();
+  const int64_t m = a.m;
+  for (int j = 0; j < nw; ++j) {
+    const int g = 32 * j + lane;
+    int64_t lo = (int64_t)g * kSbCols - 32, hi = (int64_t)g * kSbCols + kSbCols;
+    if (sb.prev_iasc != IASC) {
+      const int64_t t = m - 1 - hi;
+      hi = m - 1 - lo;
+      lo = t;
+    }
+    // the previous sweep's super-block g' holds its sweep-order columns
+    // [kSbCols g' - 31, kSbCols g' + kSbCols - 1]: at most 4 of them overlap
+    int64_t g0 = lo >> kSbShift, g1 = (hi + 31) >> kSbShift;
+    if (g0 < 0) g0 = 0;
+    if (g1 > nsb - 1) g1 = nsb - 1;
+    bool d = false;
+    if (g < nsb && g1 >= g0) {
+      const int wi = (int)(g0 >> 5);
+      const unsigned long long x =
+          ((((unsigned long long)prevw[wi + 1]) << 32) | prevw[wi]) >> (g0 & 31);
+      d = (x & ((1ull << (g1 - g0 + 1)) - 1ull)) != 0ull;
+    }
+    const unsigned w = __ballot_sync(kFull, d);
+    if (lane == 0) curw[j] = w;
+  }
+  __syncwarp();
+}
+
 // One sweep of one warp-strip.  IASC selects the column direction at compile
 // time so every access in the unrolled block is an immediate offset from a
 // per-block pointer; the padded layout (kPad columns of +inf / -1 on both
@@ -211,7 +265,7 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
                                             const Chan& ch, const unsigned* crd, unsigned* cwr,
                                             unsigned force, unsigned long long* tr, int dprev,
                                             bool jasc, unsigned long long& lcnt, const SbCtx& sb,
-                                            unsigned& ncomp_out) {
+                                            const unsigned* sbmap, unsigned& ncomp_out) {
   constexpr int S = IASC ? 1 : -1;
   const int64_t m = a.m, cw = a.cw;
   const int64_t P = a.P;
@@ -298,97 +352,106 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
 
   // ---- super-block skipping (see SbCtx) ----------------------------------
   const unsigned stamp = (unsigned)(sb.k + 1) << 2;
-  // did the previous sweep update anything around super-block g (the strip's
-  // rows and the adjoining edge rows, one column wider on each side)?
-  auto sum_dirty = [&](int g) -> bool {
-    int64_t lo = (int64_t)g * kSbCols - 32, hi = (int64_t)g * kSbCols + kSbCols;
-    if (sb.prev_iasc != IASC) {
-      const int64_t t = m - 1 - hi;
-      hi = m - 1 - lo;
-      lo = t;
-    }
-    // the previous sweep's super-block g' holds its sweep-order columns
-    // [kSbCols g' - 31, kSbCols g' + kSbCols - 1]
-    int64_t g0 = lo >> kSbShift, g1 = (hi + 31) >> kSbShift;
-    if (g0 < 0) g0 = 0;
-    if (g1 > a.nsb - 1) g1 = a.nsb - 1;
-    unsigned v = 0;
-    // at most 4 of them: (kSbCols + 32 + 31) / kSbCols < 3 for kSbCols >= 32
-    if (lane < 12) {
-      const int ds = lane / 4 - 1;
-      const int64_t gi = g0 + lane % 4;
-      const bool valid = gi <= g1 && (ds == 0 || (ds < 0 ? sb.has_lo : sb.has_hi));
-      const unsigned mask = ds == 0 ? 1u : (ds < 0 ? 4u : 2u);  // b-1: its highest row; b+1: its lowest
-      if (valid) v = __ldcg(sb_sum(a, (sb.k + 1) & 1, sb.b + ds) + gi) & mask;
-    }
-    return __any_sync(kFull, v != 0u);
-  };
-  // Pass over the super-block starting at block blk if the upwind edge row
-  // does not change over it (its local conditions hold already).  On success
-  // the per-lane pointers stand at the next super-block.
-  auto try_skip = [&](int blk) -> bool {
-    const int g = blk / kSB;
-    const int nb = nblocks - blk < kSB ? nblocks - blk : kSB;
-    // element q of lane 31's row / of the mailboxes, from the lanes' own pointers
-    const int64_t q0_31 = (int64_t)q0 + lane - 31, q0_0 = (int64_t)q0 + lane;
-    const double* edge_q0 = (const double*)__shfl_sync(kFull, (unsigned long long)pu, 31);
-    double* gout_q0 = (double*)__shfl_sync(kFull, (unsigned long long)po, 31);
-    double* gin_q0 = (double*)__shfl_sync(kFull, (unsigned long long)ph, 0);
-    const int64_t qe0 = (int64_t)g * kSbCols - 31 + lane;  // lane 31's columns, spread over the warp
-    double ev[kSbCols / 32];
-    if (ch.out_glob) {
+  const int nsb = a.nsb;
+  auto dirty_at = [&](int g) -> bool { return (sbmap[g >> 5] >> (g & 31)) & 1u; };
+  // first locally dirty super-block >= g (nsb if none): lane L looks at word L
+  // and L + 32
+  auto next_dirty = [&](int g) -> int {
+    int best = nsb;
+    const int nw = (nsb + 31) >> 5;
 #pragma unroll
-      for (int j = 0; j < kSbCols / 32; ++j) {
-        const int64_t q = qe0 + 32 * j;
-        ev[j] = (q >= 0 && q < m) ? __ldcg(edge_q0 + S * (q - q0_31)) : 0.0;
+    for (int h = 0; h < kMapWords / 32; ++h) {
+      const int wi = 32 * h + lane;
+      unsigned w = wi < nw ? sbmap[wi] : 0u;
+      if (wi == (g >> 5)) w &= ~0u << (g & 31);
+      if (wi < (g >> 5)) w = 0u;
+      const unsigned bal = __ballot_sync(kFull, w != 0u);
+      if (bal && best == nsb) {
+        const int src = __ffs(bal) - 1;
+        const unsigned ww = __shfl_sync(kFull, w, src);
+        best = 32 * (32 * h + src) + __ffs(ww) - 1;
       }
     }
+    return best < nsb ? best : nsb;
+  };
+  // Pass over a run of locally clean super-blocks starting at block blk, as
+  // far as the upwind tokens already allow (at most 30 at a time); returns the
+  // number of super-blocks passed (0: the upwind edge row changes, or its
+  // tokens are not there yet and the strip does not wait for them).
+  auto try_skip = [&](int blk) -> int {
+    const int g = blk / kSB;
+    int rmax = next_dirty(g) - g;
+    if (rmax > 30) rmax = 30;
+    int r = rmax;
     if (ch.in_glob) {
-      unsigned tk = stamp | 2u;
-      const int gi = g + lane;
-      if (lane < 2 && gi < a.nsb) {
-        const unsigned* tp = sb_tok(a, sb.flow, sb.flow ? sb.b + 1 : sb.b - 1) + gi;
-        tk = ld_relaxed_u32(tp);
-        if (sb.block) {
-          long long spins = 0;
-          while ((tk >> 2) != (stamp >> 2)) {
-            if (++spins > kSpinCap) {
-              atomicExch(a.status, kStatusWatchdog);
-              break;
-            }
-            if ((spins & 1023) == 0 && *(volatile int*)a.status == kStatusWatchdog) break;
-            tk = ld_relaxed_u32(tp);
+      const unsigned* tp = sb_tok(a, sb.flow, sb.flow ? sb.b + 1 : sb.b - 1) + g + lane;
+      const bool mine = lane <= rmax && g + lane < nsb;
+      unsigned tk = mine ? ld_relaxed_u32(tp) : (stamp | 2u);
+      if (sb.block && lane < 2 && mine) {
+        long long spins = 0;
+        while ((tk >> 2) != (stamp >> 2)) {
+          if (++spins > kSpinCap) {
+            atomicExch(a.status, kStatusWatchdog);
+            break;
           }
+          if ((spins & 1023) == 0 && *(volatile int*)a.status == kStatusWatchdog) break;
+          tk = ld_relaxed_u32(tp);
         }
       }
-      if (__any_sync(kFull, tk != (stamp | 2u))) return false;
+      // tokens g .. g+r let the strip pass r super-blocks
+      const unsigned bad = __ballot_sync(kFull, tk != (stamp | 2u));
+      const int lead = bad ? __ffs(bad) - 1 : 32;
+      if (lead - 1 < r) r = lead - 1;
+      if (r <= 0) return 0;
+    }
+    int nb = kSB * r;
+    if (nb > nblocks - blk) nb = nblocks - blk;
+    if (ch.in_glob) {
       // re-arm the upwind slots of lane 0's columns (their values have landed:
       // the tokens are written after them)
-#pragma unroll
-      for (int j = 0; j < kSbCols / 32; ++j) {
+      double* gin_q0 = (double*)__shfl_sync(kFull, (unsigned long long)ph, 0);
+      const int64_t q0_0 = (int64_t)q0 + lane;
+      for (int j = 0; j < r; ++j) {
         const int64_t q = (int64_t)g * kSbCols + lane + 32 * j;
         if (q < m) __stcg(gin_q0 + S * (q - q0_0), sent);
       }
     }
     if (ch.out_glob) {
+      // the strip's edge row (lane 31's) over the run into the downwind mailbox
+      const int64_t q0_31 = (int64_t)q0 + lane - 31;
+      const double* edge_q0 = (const double*)__shfl_sync(kFull, (unsigned long long)pu, 31);
+      double* gout_q0 = (double*)__shfl_sync(kFull, (unsigned long long)po, 31);
+      const int64_t qe0 = (int64_t)g * kSbCols - 31 + lane;
+      for (int j0 = 0; j0 < r; j0 += 8) {
+        double ev[8];
 #pragma unroll
-      for (int j = 0; j < kSbCols / 32; ++j) {
-        const int64_t q = qe0 + 32 * j;
-        if (q >= 0 && q < m) __stcg(gout_q0 + S * (q - q0_31), ev[j]);
+        for (int j = 0; j < 8; ++j) {
+          const int64_t q = qe0 + 32 * (j0 + j);
+          ev[j] = (j0 + j < r && q >= 0 && q < m) ? __ldcg(edge_q0 + S * (q - q0_31)) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int64_t q = qe0 + 32 * (j0 + j);
+          if (j0 + j < r && q >= 0 && q < m) __stcg(gout_q0 + S * (q - q0_31), ev[j]);
+        }
       }
-      __threadfence();  // the values before the token
+      __threadfence();  // the values before the tokens
       __syncwarp();
-      if (lane == 0) __stcg(sb_tok(a, sb.flow, sb.b) + g, stamp | 2u);
+      if (lane < r) __stcg(sb_tok(a, sb.flow, sb.b) + g + lane, stamp | 2u);
     }
-    if (lane == 0) __stcg(sb_sum(a, sb.k & 1, sb.b) + g, 0u);
-    for (int j = 0; j < nb; ++j) put_bits(blk + j, 0u);
+    if (lane < r) __stcg(sb_sum(a, sb.k & 1, sb.b) + g + lane, 0u);
+    // zero change bits over the lane's 32 r columns: the open word (acc), then
+    // whole words; the next column to visit opens an empty word
+    for (int i = 0; i < r; ++i) __stcg(wrow + (IASC ? wcur + i : wcur - i), i == 0 ? acc : 0u);
+    acc = 0u;
+    wcur += IASC ? r : -r;
     pu += S * kU * nb;
     pc += S * kU * nb;
     ph += S * kU * nb;
     po += S * kU * nb;
     q0 += kU * nb;
-    ++nskip;
-    return true;
+    nskip += (unsigned)r;
+    return r;
   };
 
   unsigned sb_um = 0;
@@ -396,12 +459,13 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
   // Outer loop: a run of skipped super-blocks, then a run of computed blocks
   // with the register pipeline primed once (the pipeline is dead across the
   // skip phase, so the skip code shares its registers).
-  bool local_clean = sb.skip && !sum_dirty(0);
+  bool local_clean = sb.skip && !dirty_at(0);
   for (;;) {
     if (local_clean) {
-      while (try_skip(blk)) {
-        blk += kSB;
-        if (blk >= nblocks || sum_dirty(blk / kSB)) break;
+      for (;;) {
+        const int r = try_skip(blk);
+        blk += kSB * r;
+        if (r == 0 || blk >= nblocks || dirty_at(blk / kSB)) break;
       }
       if (blk >= nblocks) break;
     }
@@ -586,8 +650,8 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
     if (blk >= nblocks) break;
     // at a super-block boundary with no update in flight and nothing changed
     // around the next super-block: leave the pipeline for the skip phase
-    if (sb.skip && (blk & (kSB - 1)) == 0 && !__any_sync(kFull, upd_prev) &&
-        !sum_dirty(blk / kSB)) {
+    if (sb.skip && (blk & (kSB - 1)) == 0 && !dirty_at(blk / kSB) &&
+        !__any_sync(kFull, upd_prev)) {
       local_clean = true;
       break;
     }
@@ -612,6 +676,9 @@ fsm_wavefront_kernel(FsmArgs a) {
   const int b = blockIdx.x * (blockDim.x >> 5) + w;
   if (b >= a.nstrips) return;  // warps past the last grid row do not exist
   const int64_t n = a.n, P = a.P;
+  __shared__ unsigned s_sbmap[kMaxWarpsPerCta][2][kMapWords + 2];
+  unsigned* const sbprev = s_sbmap[w][0];
+  unsigned* const sbmap = s_sbmap[w][1];
   unsigned prev_comp = ~0u;  // steps this strip computed in its previous sweep
 
   for (int k = 0;; ++k) {
@@ -714,9 +781,9 @@ fsm_wavefront_kernel(FsmArgs a) {
 #ifdef SB_NOPUB
     sb.pub = false;
 #endif
-    // sparse regime (under a quarter of the strip's steps computed last
+    // sparse regime (fewer than (m + 31) / sb_wait_div steps computed last
     // sweep): wait for the upwind tokens; otherwise only use them if present
-    sb.block = prev_comp < (unsigned)((a.m + 31) / 4);
+    sb.block = a.sb_wait_div > 0 && prev_comp < (unsigned)((a.m + 31) / a.sb_wait_div);
     sb.prev_iasc = dprev == 0 || dprev == 1;
     sb.lo_is_lane0 = jasc;
     sb.has_lo = b > 0;
@@ -724,12 +791,16 @@ fsm_wavefront_kernel(FsmArgs a) {
     sb.k = k;
     sb.flow = flow;
     sb.b = b;
+    if (sb.skip) {
+      if (iasc) sb_build_map<true>(a, sb, lane, sbprev, sbmap);
+      else sb_build_map<false>(a, sb, lane, sbprev, sbmap);
+    }
     unsigned ncomp = 0;
     const bool changed =
         iasc ? sweep_strip<true, LSM>(a, lane, rowp, ch, crd, cwr, force, tr, dprev, jasc, lcnt, sb,
-                                      ncomp)
+                                      sbmap, ncomp)
              : sweep_strip<false, LSM>(a, lane, rowp, ch, crd, cwr, force, tr, dprev, jasc, lcnt, sb,
-                                       ncomp);
+                                       sbmap, ncomp);
     prev_comp = __shfl_sync(kFull, ncomp, 0);
     if (*(volatile int*)a.status == kStatusWatchdog) return;
     if (LSM) {
