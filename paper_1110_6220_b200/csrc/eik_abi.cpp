@@ -596,8 +596,8 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
         for (int b = 0; b < P->nstrips; ++b) {
           const unsigned long long* t = &tr[((size_t)k * P->nstrips + b) * kTraceWords];
           if (t[0])
-            std::fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu\n", k, b, t[0], t[1], t[2], t[3],
-                         t[4], t[5]);
+            std::fprintf(f, "%d %d %llu %llu %llu %llu %llu %llu %llu %llu\n", k, b, t[0], t[1], t[2],
+                         t[3], t[4], t[5], t[6], t[7]);
         }
       std::fclose(f);
     }

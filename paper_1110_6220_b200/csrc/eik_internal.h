@@ -67,7 +67,8 @@ inline int fsm_nsb(int64_t m) {
 constexpr int64_t kChgWordOff = 3;
 constexpr int64_t kChgWordPad = 8;  // pad words per row (kChgWordOff before, the rest after)
 constexpr int kTraceSweeps = 16;
-constexpr int kTraceWords = 6;  // start, body start, end, polls, compute steps, skipped super-blocks
+constexpr int kTraceWords = 8;  // start, body start, end, polls, compute steps, skipped super-blocks,
+                                // ns and blocks in computed runs
 
 // Cell decomposition as seen by the device (build_cells, cells.cpp:32-47):
 // cell (cx,cy) spans columns [cx*base_x, cx==cells_x-1 ? m : (cx+1)*base_x).

@@ -456,6 +456,8 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
 
   unsigned sb_um = 0;
   int blk = 0;
+  unsigned long long t_norm = 0;  // trace: time and blocks in the computed runs
+  unsigned n_norm = 0;
   // Outer loop: a run of skipped super-blocks, then a run of computed blocks
   // with the register pipeline primed once (the pipeline is dead across the
   // skip phase, so the skip code shares its registers).
@@ -469,6 +471,8 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       }
       if (blk >= nblocks) break;
     }
+    const unsigned long long tn0 = tr ? globaltimer() : 0ull;
+    const int blk_n0 = blk;
     prime(blk);
     for (;;) {
     {
@@ -656,6 +660,10 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       break;
     }
     }
+    if (tr) {
+      t_norm += globaltimer() - tn0;
+      n_norm += (unsigned)(blk - blk_n0);
+    }
     if (blk >= nblocks) break;
   }
   __stcg(wrow + wcur, acc);
@@ -663,6 +671,8 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
     tr[3] = npoll;
     tr[4] = ncomp;
     tr[5] = nskip;
+    tr[6] = t_norm;
+    tr[7] = n_norm;
   }
   ncomp_out = ncomp;
   return changed;
