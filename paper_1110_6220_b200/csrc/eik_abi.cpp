@@ -54,6 +54,7 @@ Knobs read_knobs() {
   k.fsm_wpc = gi("EIK_FSM_WPC", 0);
   k.fsm_sb = gi("EIK_FSM_SB", 1);
   k.fsm_sb_wait_div = gi("EIK_FSM_SB_WAIT_DIV", 1);
+  k.fsm_start_ahead = std::max(0, gi("EIK_FSM_START_AHEAD", 12));
   k.hc_warps = gi("EIK_HC_WARPS", 0);
   k.hc_min_smem = std::getenv("EIK_HC_MIN_SMEM") ? std::atol(std::getenv("EIK_HC_MIN_SMEM")) : -1;
   k.hc_global_heap = gb("EIK_HC_GLOBAL_HEAP");
@@ -505,6 +506,7 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   a.sb = (knobs().fsm_sb && P->nsb <= kFsmSbMaxPerRow) ? P->dSb : nullptr;
   a.nsb = P->nsb;
   a.sb_wait_div = knobs().fsm_sb_wait_div;
+  a.start_ahead = knobs().fsm_start_ahead;
   if (P->part_strips > 0 && P->part_strips < P->nstrips) {
     const int nb = (P->nstrips - 1) / P->part_strips;
     const int64_t need = (int64_t)2 * nb * 2 * P->pitch;
@@ -712,6 +714,7 @@ int plan_sweep_impl(eik_plan* P, int64_t first_sweep, int count, int* changed, i
   a.sb = (knobs().fsm_sb && P->nsb <= kFsmSbMaxPerRow) ? P->dSb : nullptr;
   a.nsb = P->nsb;
   a.sb_wait_div = knobs().fsm_sb_wait_div;
+  a.start_ahead = knobs().fsm_start_ahead;
   // the flags this call leaves in [0, count) must be cleared by a later run
   P->last_sweeps_bound = std::min<int64_t>(P->max_sweeps,
                                            std::max<int64_t>(P->last_sweeps_bound, count + 8));

@@ -55,6 +55,7 @@ struct FsmArgs {
   // << 2 | state; zeroed before every launch).  Null: no super-block skipping.
   unsigned* sb;
   int nsb;
+  int start_ahead;          // a computed run starts once the upwind strip is this many columns ahead
   int sb_wait_div;          // a strip waits for upwind tokens when it computed fewer than
                             // (m + 31) / sb_wait_div steps in its previous sweep (0: never)
 };

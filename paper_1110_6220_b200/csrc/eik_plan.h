@@ -146,6 +146,7 @@ struct Knobs {
   const char* fsm_trace = nullptr; // EIK_TRACE_FSM=path: per-strip timing trace (copied)
   int fsm_wpc = 0;                 // EIK_FSM_WPC: strips per CTA (0 = auto)
   int fsm_sb = 1;                  // EIK_FSM_SB=0: no super-block skipping
+  int fsm_start_ahead = 12;        // EIK_FSM_START_AHEAD (FsmArgs::start_ahead)
   int fsm_sb_wait_div = 1;         // EIK_FSM_SB_WAIT_DIV: token-wait threshold (FsmArgs::sb_wait_div)
   // heap-cell replay
   int hc_warps = 0;                // EIK_HC_WARPS (0 = fit)

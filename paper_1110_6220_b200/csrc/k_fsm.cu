@@ -473,6 +473,15 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
     }
     const unsigned long long tn0 = tr ? globaltimer() : 0ull;
     const int blk_n0 = blk;
+    if (a.start_ahead > 0 && in_g) {
+      // start a computed run only once the upwind strip is start_ahead
+      // columns ahead: the block prefetches then find their slots filled and
+      // the run never drops to the per-step polling path
+      int64_t q = (int64_t)q0 + a.start_ahead;
+      if (q > m - 1) q = m - 1;
+      if (q >= 0) (void)poll_slot(ph + S * (q - q0), a.status);
+    }
+    __syncwarp();
     prime(blk);
     for (;;) {
     {
