@@ -53,6 +53,7 @@ Knobs read_knobs() {
   k.fsm_trace = trace_path.empty() ? nullptr : trace_path.c_str();
   k.fsm_wpc = gi("EIK_FSM_WPC", 0);
   k.fsm_sb = gi("EIK_FSM_SB", 1);
+  k.fsm_cont = gi("EIK_FSM_CONT", 1);
   k.fsm_sb_wait_div = gi("EIK_FSM_SB_WAIT_DIV", 1);
   k.fsm_start_ahead = std::max(0, gi("EIK_FSM_START_AHEAD", 12));
   k.hc_warps = gi("EIK_HC_WARPS", 0);
@@ -467,7 +468,7 @@ int plan_init(eik_plan* P, const eik_problem* p, const eik_cells* c, int method,
     track(P->dChg);
     CK(cudaMemsetAsync(P->dChg, 0, sizeof(unsigned) * nchg, P->stream));
     P->nsb = fsm_nsb(P->g.m);
-    if ((rc = dalloc(&P->dSb, (size_t)4 * P->nstrips * P->nsb))) return rc;
+    if ((rc = dalloc(&P->dSb, (size_t)4 * P->nstrips * P->nsb + P->nstrips))) return rc;
     track(P->dSb);
   } else {
     if ((rc = plan_init_cells(P, p, c))) return rc;
@@ -507,6 +508,9 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   a.nsb = P->nsb;
   a.sb_wait_div = knobs().fsm_sb_wait_div;
   a.start_ahead = knobs().fsm_start_ahead;
+  a.cont = 0;
+  a.par0 = 0;
+  P->chg_valid = false;  // a later sweep-level launch starts from scratch
   if (P->part_strips > 0 && P->part_strips < P->nstrips) {
     const int nb = (P->nstrips - 1) / P->part_strips;
     const int64_t need = (int64_t)2 * nb * 2 * P->pitch;
@@ -667,6 +671,7 @@ int plan_prepare(eik_plan* P) {
     return fail(EIK_ERR_CONFIG, "sweep-level control needs an fsm/fmm plan");
   CK(cudaSetDevice(P->device));
   CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, P->stream));
+  P->chg_valid = false;  // fresh values: the next sweep launch evaluates every node
   int launches = 0;
   CK(launch_prepare(P->dF, P->dC, P->dU, P->g.m, P->g.n, P->pitch, kPad, P->g.h, P->dExit,
                     P->dExitCost, P->n_exit, P->dStatus, P->stream, &launches));
@@ -715,6 +720,13 @@ int plan_sweep_impl(eik_plan* P, int64_t first_sweep, int count, int* changed, i
   a.nsb = P->nsb;
   a.sb_wait_div = knobs().fsm_sb_wait_div;
   a.start_ahead = knobs().fsm_start_ahead;
+  // A launch that follows another sweep launch on the same values continues
+  // from its change bits (rows written in between were marked, plan_rows):
+  // only the first launch after eik_plan_prepare evaluates every node.
+  a.cont = (P->chg_valid && knobs().fsm_cont) ? 1 : 0;
+  a.par0 = a.cont ? ((P->chg_last_par + 1) & 1) : 0;
+  P->chg_last_par = (count - 1 + a.par0) & 1;
+  P->chg_valid = true;
   // the flags this call leaves in [0, count) must be cleared by a later run
   P->last_sweeps_bound = std::min<int64_t>(P->max_sweeps,
                                            std::max<int64_t>(P->last_sweeps_bound, count + 8));
@@ -723,7 +735,11 @@ int plan_sweep_impl(eik_plan* P, int64_t first_sweep, int count, int* changed, i
   if (!changed_dev) CK(cudaMemsetAsync(P->dStatus, 0, sizeof(int) * 8, s));
   CK(cudaMemsetAsync(P->dProg, 0, sizeof(unsigned long long) * P->nstrips, s));
   CK(cudaMemsetAsync(P->dMbox, 0xFF, sizeof(double) * 2 * P->nstrips * P->pitch, s));
-  if (a.sb) CK(cudaMemsetAsync(P->dSb, 0, sizeof(unsigned) * 4 * P->nstrips * P->nsb, s));
+  if (a.sb) {  // edge tokens always; the summaries only when nothing carries over
+    const size_t half = (size_t)2 * P->nstrips * P->nsb;
+    if (a.cont) CK(cudaMemsetAsync(P->dSb + half, 0, sizeof(unsigned) * half, s));
+    else CK(cudaMemsetAsync(P->dSb, 0, sizeof(unsigned) * (2 * half + P->nstrips), s));
+  }
   CK(cudaMemsetAsync(P->dChanged, 0, sizeof(int) * count, s));
   CK(cudaMemsetAsync(P->dDone, 0, sizeof(int) * count, s));
   CK(launch_fsm(a, s, &launches));
@@ -757,7 +773,25 @@ int plan_rows(eik_plan* P, int64_t row0, int64_t nrows, double* host_or_dev, int
   CK(cudaSetDevice(P->device));
   double* dev = P->dU + row0 * P->pitch + kPad;
   const size_t w = sizeof(double) * P->g.m, dp = sizeof(double) * P->pitch;
-  if (to_plan)
+  if (to_plan && P->chg_valid && P->dChg) {
+    // between sweep launches: mark what the new rows change (k_fsm.cu)
+    double* stage = nullptr;
+    const double* src = host_or_dev;
+    if (!on_device) {
+      CK(pool_alloc((void**)&stage, w * nrows));
+      CK(cudaMemcpyAsync(stage, host_or_dev, w * nrows, cudaMemcpyHostToDevice, P->stream));
+      src = stage;
+    }
+    CK(launch_set_rows_marked(P->dU, src, row0, nrows, P->g.m, P->pitch, kPad,
+                              P->dChg + (int64_t)P->chg_last_par * (P->g.n + 3) * P->chg_cw,
+                              P->chg_cw,
+                              P->dSb + (int64_t)P->chg_last_par * P->nstrips * P->nsb, P->nsb,
+                              P->stream));
+    if (stage) {
+      CK(stream_wait(P->stream));
+      pool_release(stage);
+    }
+  } else if (to_plan)
     CK(cudaMemcpy2DAsync(dev, dp, host_or_dev, w, w, nrows,
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P->stream));
   else
@@ -783,7 +817,12 @@ int plan_rows_async(eik_plan* P, int64_t row0, int64_t nrows, double* dev_buf, b
   double* dev = P->dU + row0 * P->pitch + kPad;
   const size_t w = sizeof(double) * P->g.m, dp = sizeof(double) * P->pitch;
   const cudaStream_t s = stream ? stream : P->stream;
-  if (to_plan) CK(cudaMemcpy2DAsync(dev, dp, dev_buf, w, w, nrows, cudaMemcpyDeviceToDevice, s));
+  if (to_plan && P->chg_valid && P->dChg)
+    CK(launch_set_rows_marked(P->dU, dev_buf, row0, nrows, P->g.m, P->pitch, kPad,
+                              P->dChg + (int64_t)P->chg_last_par * (P->g.n + 3) * P->chg_cw,
+                              P->chg_cw,
+                              P->dSb + (int64_t)P->chg_last_par * P->nstrips * P->nsb, P->nsb, s));
+  else if (to_plan) CK(cudaMemcpy2DAsync(dev, dp, dev_buf, w, w, nrows, cudaMemcpyDeviceToDevice, s));
   else CK(cudaMemcpy2DAsync(dev_buf, w, dev, dp, w, nrows, cudaMemcpyDeviceToDevice, s));
   return EIK_OK;
 }

@@ -53,8 +53,10 @@ struct FsmArgs {
   // summaries (bit 0 any row, bit 1 the strip's lowest row, bit 2 its highest)
   // followed by [2][nstrips][nsb] edge tokens per row direction (sweep stamp
   // << 2 | state; zeroed before every launch).  Null: no super-block skipping.
-  unsigned* sb;
+  unsigned* sb;             // ... then [nstrips] steps each strip computed in its last sweep
   int nsb;
+  int cont;                 // continuing launch: sweep 0 uses the change bits its predecessor left
+  int par0;                 // parity offset: sweep k writes parity (k + par0) & 1
   int start_ahead;          // a computed run starts once the upwind strip is this many columns ahead
   int sb_wait_div;          // a strip waits for upwind tokens when it computed fewer than
                             // (m + 31) / sb_wait_div steps in its previous sweep (0: never)
@@ -230,6 +232,9 @@ cudaError_t launch_prepare(const double* F, double* C, double* u, int64_t m, int
                            const double* cost, int64_t n_exit, int* status, cudaStream_t s,
                            int* launches);
 cudaError_t launch_fsm(const FsmArgs& a, cudaStream_t s, int* launches, int* grid = nullptr);
+cudaError_t launch_set_rows_marked(double* u, const double* src, int64_t row0, int64_t nrows,
+                                   int64_t m, int64_t P, int64_t pad, unsigned* chg_par, int64_t cw,
+                                   unsigned* sum_par, int nsb, cudaStream_t s);
 cudaError_t launch_fill(double* p, int64_t count, double v, cudaStream_t s, int* launches);
 cudaError_t fsm_capacity(int nstrips, int* need, int* ctas, bool lsm = false);
 

@@ -35,6 +35,8 @@ eik_plan* plan_create(const eik_problem* p, const eik_cells* c, int32_t method, 
                       cudaStream_t stream, const cudaEvent_t* events);
 int plan_prepare(eik_plan* P);
 int plan_sweep(eik_plan* P, int64_t first_sweep, int count, int* changed);
+int plan_rows_async(eik_plan* P, int64_t row0, int64_t nrows, double* dev_buf, bool to_plan,
+                    cudaStream_t stream);
 void plan_free(eik_plan* P);
 int64_t fmm_node_updates(const eik_grid& g, const int64_t* exits, int64_t n_exit);
 
@@ -71,6 +73,9 @@ struct Strip {
   std::vector<double> cost;
   eik_plan* plan = nullptr;
   cudaStream_t stream = nullptr;
+  double* recv = nullptr;           // [2][m] on the strip's device: the neighbours' edge rows land
+                                    // here, then go into the ghost rows through plan_rows_async,
+                                    // which marks what they change for the next sweep launch
   int changed[2] = {0, 0};  // by round parity: a fast thread writes round k+1's
                             // flag while a slow one still reads round k's
   int rc = EIK_OK;
@@ -144,6 +149,10 @@ int solve_multi(const eik_problem* p, int32_t method, const int32_t* devices, in
       else {  // off-grid beyond the domain edges: +inf ghost rows until exchanged
         cudaMemcpy(s.row(0), inf_row.data(), sizeof(double) * m, cudaMemcpyHostToDevice);
         cudaMemcpy(s.row(s.nl - 1), inf_row.data(), sizeof(double) * m, cudaMemcpyHostToDevice);
+        if (cudaMalloc(&s.recv, sizeof(double) * 2 * m) != cudaSuccess) {
+          s.rc = EIK_ERR_CUDA;
+          s.msg = "cannot allocate the ghost-row receive buffer";
+        }
       }
       s.F.clear();
       s.F.shrink_to_fit();
@@ -163,15 +172,26 @@ int solve_multi(const eik_problem* p, int32_t method, const int32_t* devices, in
       s.changed[k & 1] = ch;
       bar.wait();  // every strip swept round k
       // edge rows into the neighbours' ghost rows (device to device)
-      if (s.rc == EIK_OK && d > 0 && S[d - 1].plan)
-        cudaMemcpyPeerAsync(S[d - 1].row(S[d - 1].nl - 1), S[d - 1].device, s.row(1), s.device,
+      // (into their receive buffers: slot 0 = their lower ghost row's new
+      // values, slot 1 = their upper one's)
+      if (s.rc == EIK_OK && d > 0 && S[d - 1].recv)
+        cudaMemcpyPeerAsync(S[d - 1].recv + m, S[d - 1].device, s.row(1), s.device,
                             sizeof(double) * m, s.stream);
-      if (s.rc == EIK_OK && d + 1 < n_dev && S[d + 1].plan)
-        cudaMemcpyPeerAsync(S[d + 1].row(0), S[d + 1].device, s.row(s.nl - 2), s.device,
+      if (s.rc == EIK_OK && d + 1 < n_dev && S[d + 1].recv)
+        cudaMemcpyPeerAsync(S[d + 1].recv, S[d + 1].device, s.row(s.nl - 2), s.device,
                             sizeof(double) * m, s.stream);
       if (s.rc == EIK_OK && cudaStreamSynchronize(s.stream) != cudaSuccess) {
         s.rc = EIK_ERR_CUDA;
         s.msg = "peer copy of strip edge rows failed";
+      }
+      bar.wait();  // every receive buffer holds round k's edges
+      if (s.rc == EIK_OK && d > 0 && S[d - 1].rc == EIK_OK)
+        if (int rc = plan_rows_async(s.plan, 0, 1, s.recv, true, s.stream)) fail_here(rc);
+      if (s.rc == EIK_OK && d + 1 < n_dev && S[d + 1].rc == EIK_OK)
+        if (int rc = plan_rows_async(s.plan, s.nl - 1, 1, s.recv + m, true, s.stream)) fail_here(rc);
+      if (s.rc == EIK_OK && cudaStreamSynchronize(s.stream) != cudaSuccess) {
+        s.rc = EIK_ERR_CUDA;
+        s.msg = "ghost row update failed";
       }
       bar.wait();  // ghost rows hold round k's edges
       bool any = false;
@@ -209,6 +229,7 @@ int solve_multi(const eik_problem* p, int32_t method, const int32_t* devices, in
   for (Strip& s : S) {
     if (s.plan) {
       cudaSetDevice(s.device);
+      if (s.recv) cudaFree(s.recv);
       plan_free(s.plan);
     }
     if (s.stream) cudaStreamDestroy(s.stream);

@@ -51,6 +51,8 @@ struct eik_plan {
   int64_t chg_cw = 0;
   unsigned* dSb = nullptr;    // [4][nstrips][nsb] super-block summaries + edge tokens (k_fsm.cu)
   int nsb = 0;
+  bool chg_valid = false;     // the change bits describe every change since the last sweep launch
+  int chg_last_par = 0;       // parity the last sweep of that launch wrote
   int part_strips = 0;        // strip-Jacobi parts (eik_plan_set_partitions), 0 = exact GS
   double* dSnap = nullptr;    // [2][boundaries][2] padded rows
   int64_t snap_count = 0;
@@ -146,6 +148,7 @@ struct Knobs {
   const char* fsm_trace = nullptr; // EIK_TRACE_FSM=path: per-strip timing trace (copied)
   int fsm_wpc = 0;                 // EIK_FSM_WPC: strips per CTA (0 = auto)
   int fsm_sb = 1;                  // EIK_FSM_SB=0: no super-block skipping
+  int fsm_cont = 1;                // EIK_FSM_CONT=0: every sweep-level launch evaluates every node
   int fsm_start_ahead = 12;        // EIK_FSM_START_AHEAD (FsmArgs::start_ahead)
   int fsm_sb_wait_div = 1;         // EIK_FSM_SB_WAIT_DIV: token-wait threshold (FsmArgs::sb_wait_div)
   // heap-cell replay

@@ -105,6 +105,7 @@ struct SbCtx {
   bool prev_iasc;          // column direction of the previous sweep
   bool lo_is_lane0;        // lane 0 owns the strip's lowest row (jasc)
   int k, flow, b;          // sweep, row direction (mailbox / token set), strip
+  int par;                 // parity this sweep writes (change bits and summaries)
 };
 // [2][nstrips][nsb] summaries by sweep parity, then [2][nstrips][nsb] tokens by row direction
 __device__ __forceinline__ unsigned* sb_sum(const FsmArgs& a, int par, int b) {
@@ -199,7 +200,7 @@ template <bool IASC>
 __device__ __forceinline__ void sb_build_map(const FsmArgs& a, const SbCtx& sb, int lane,
                                              unsigned* prevw, unsigned* curw) {
   const int nsb = a.nsb, nw = (nsb + 31) >> 5;
-  const unsigned* s0 = sb_sum(a, (sb.k + 1) & 1, sb.b);
+  const unsigned* s0 = sb_sum(a, sb.par ^ 1, sb.b);
   const unsigned* slo = s0 - nsb;  // strip b-1: its highest row (bit 2)
   const unsigned* shi = s0 + nsb;  // strip b+1: its lowest row (bit 1)
   for (int j = 0; j < nw; ++j) {
@@ -439,7 +440,7 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       __syncwarp();
       if (lane < r) __stcg(sb_tok(a, sb.flow, sb.b) + g + lane, stamp | 2u);
     }
-    if (lane < r) __stcg(sb_sum(a, sb.k & 1, sb.b) + g + lane, 0u);
+    if (lane < r) __stcg(sb_sum(a, sb.par, sb.b) + g + lane, 0u);
     // zero change bits over the lane's 32 r columns: the open word (acc), then
     // whole words; the next column to visit opens an empty word
     for (int i = 0; i < r; ++i) __stcg(wrow + (IASC ? wcur + i : wcur - i), i == 0 ? acc : 0u);
@@ -477,9 +478,10 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       // start a computed run only once the upwind strip is start_ahead
       // columns ahead: the block prefetches then find their slots filled and
       // the run never drops to the per-step polling path
+      // (lane 0 past the row's end has consumed and re-armed every slot)
       int64_t q = (int64_t)q0 + a.start_ahead;
       if (q > m - 1) q = m - 1;
-      if (q >= 0) (void)poll_slot(ph + S * (q - q0), a.status);
+      if (q0 < m) (void)poll_slot(ph + S * (q - q0), a.status);
     }
     __syncwarp();
     prime(blk);
@@ -631,7 +633,7 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
         const bool e0 = bal & 1u, e31 = (bal >> 31) & 1u;
         const int g = blk / kSB;
         if (lane == 0)
-          __stcg(sb_sum(a, sb.k & 1, sb.b) + g, (bal ? 1u : 0u) | ((sb.lo_is_lane0 ? e0 : e31) ? 2u : 0u) |
+          __stcg(sb_sum(a, sb.par, sb.b) + g, (bal ? 1u : 0u) | ((sb.lo_is_lane0 ? e0 : e31) ? 2u : 0u) |
                                    ((sb.lo_is_lane0 ? e31 : e0) ? 4u : 0u));
         if (out_g) {  // lane 31 wrote the mailbox values itself
           if (!e31) __threadfence();
@@ -698,7 +700,9 @@ fsm_wavefront_kernel(FsmArgs a) {
   __shared__ unsigned s_sbmap[kMaxWarpsPerCta][2][kMapWords + 2];
   unsigned* const sbprev = s_sbmap[w][0];
   unsigned* const sbmap = s_sbmap[w][1];
-  unsigned prev_comp = ~0u;  // steps this strip computed in its previous sweep
+  // steps this strip computed in its previous sweep (a continuing launch
+  // reads what its predecessor left)
+  unsigned prev_comp = (a.cont && a.sb) ? a.sb[(int64_t)4 * a.nstrips * a.nsb + b] : ~0u;
 
   for (int k = 0;; ++k) {
     // ---- stop decision: identical in every strip --------------------------
@@ -785,10 +789,15 @@ fsm_wavefront_kernel(FsmArgs a) {
     // of a launch evaluates every node (the bits of an earlier launch do not
     // describe changes made since, e.g. ghost rows set by the host)
     const int64_t cpar = (n + 3) * a.cw;
-    const unsigned* crd = a.chg + (int64_t)((k + 1) & 1) * cpar;
-    unsigned* cwr = a.chg + (int64_t)(k & 1) * cpar;
-    const unsigned force = (k == 0 || a.noskip) ? 0xFFu : 0u;
-    const int dprev = k == 0 ? -1 : ((a.first_sweep + k - 1) & 3);
+    // a continuing launch (a.cont: sweep-level control, one launch after
+    // another on the same values) starts from the bits its predecessor left:
+    // par0 lines the parities up, and rows written in between were marked by
+    // mark_rows_kernel
+    const int par = (k + a.par0) & 1;
+    const unsigned* crd = a.chg + (int64_t)(par ^ 1) * cpar;
+    unsigned* cwr = a.chg + (int64_t)par * cpar;
+    const unsigned force = ((k == 0 && !a.cont) || a.noskip) ? 0xFFu : 0u;
+    const int dprev = (k == 0 && !a.cont) ? -1 : ((a.first_sweep + k + 3) & 3);
     unsigned long long lcnt = 0;
     SbCtx sb;
     sb.pub = a.sb != nullptr;
@@ -808,6 +817,7 @@ fsm_wavefront_kernel(FsmArgs a) {
     sb.has_lo = b > 0;
     sb.has_hi = b + 1 < a.nstrips;
     sb.k = k;
+    sb.par = par;
     sb.flow = flow;
     sb.b = b;
     if (sb.skip) {
@@ -821,6 +831,7 @@ fsm_wavefront_kernel(FsmArgs a) {
              : sweep_strip<false, LSM>(a, lane, rowp, ch, crd, cwr, force, tr, dprev, jasc, lcnt, sb,
                                        sbmap, ncomp);
     prev_comp = __shfl_sync(kFull, ncomp, 0);
+    if (a.sb && lane == 0) a.sb[(int64_t)4 * a.nstrips * a.nsb + b] = prev_comp;
     if (*(volatile int*)a.status == kStatusWatchdog) return;
     if (LSM) {
 #pragma unroll
@@ -881,6 +892,41 @@ __global__ void fill_kernel(double* __restrict__ p, int64_t count, double v) {
     p[i] = v;
 }
 
+
+// Rows written between two launches of a sweep-by-sweep solve (ghost rows of
+// a sharded run, eik_plan_set_rows): copy them in and mark what changed as
+// "changed in the previous sweep" -- change bits of the parity the next
+// launch reads, and the summary words of the row's strip (every super-block:
+// the skewed indexing of the sweep to come is not known here) -- so that a
+// continuing launch need not evaluate every node.
+__global__ void set_rows_marked_kernel(double* __restrict__ u, const double* __restrict__ src,
+                                       int64_t row0, int64_t nrows, int64_t m, int64_t P,
+                                       int64_t pad, unsigned* __restrict__ chg_par, int64_t cw,
+                                       unsigned* __restrict__ sum_par, int nsb) {
+  const int lane = threadIdx.x & 31;
+  const int64_t words = (m + 31) / 32;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t it = warp; it < nrows * words; it += nwarps) {
+    const int64_t r = it / words, w = it - r * words, row = row0 + r, i = 32 * w + lane;
+    bool ch = false;
+    if (i < m) {
+      const double v = src[r * m + i];
+      double* p = u + row * P + pad + i;
+      ch = __double_as_longlong(v) != __double_as_longlong(*p);
+      *p = v;
+    }
+    const unsigned mask = __ballot_sync(kFull, ch);
+    if (mask && lane == 0) {
+      atomicOr(chg_par + (row + 1) * cw + kChgWordOff + w, mask);
+      const unsigned bits = 1u | ((row & 31) == 0 ? 2u : 0u) | ((row & 31) == 31 ? 4u : 0u);
+      unsigned* sp = sum_par + (row >> 5) * (int64_t)nsb;
+      if ((atomicOr(sp, bits) & bits) != bits)  // first marker of this strip fills the rest
+        for (int g = 1; g < nsb; ++g) atomicOr(sp + g, bits);
+    }
+  }
+}
+
 }  // namespace
 
 cudaError_t launch_fill(double* p, int64_t count, double v, cudaStream_t s, int* launches) {
@@ -889,6 +935,18 @@ cudaError_t launch_fill(double* p, int64_t count, double v, cudaStream_t s, int*
   if (blocks < 1) blocks = 1;
   fill_kernel<<<(unsigned)blocks, 256, 0, s>>>(p, count, v);
   *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_rows_marked(double* u, const double* src, int64_t row0, int64_t nrows,
+                                   int64_t m, int64_t P, int64_t pad, unsigned* chg_par, int64_t cw,
+                                   unsigned* sum_par, int nsb, cudaStream_t s) {
+  int64_t warps = nrows * ((m + 31) / 32);
+  int64_t blocks = (warps + 7) / 8;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  set_rows_marked_kernel<<<(unsigned)blocks, 256, 0, s>>>(u, src, row0, nrows, m, P, pad, chg_par,
+                                                         cw, sum_par, nsb);
   return cudaGetLastError();
 }
 

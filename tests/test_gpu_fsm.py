@@ -152,3 +152,94 @@ def test_set_device_selects_and_rejects():
     assert E.fsm_solve(p).sweeps >= 2
     with pytest.raises(E.ConfigError):
         E.set_device(E.device_count() + 7)
+
+
+def _knob(name, value):
+    if value is None:
+        os.environ.pop(name, None)
+    else:
+        os.environ[name] = value
+    E.lib.eik_debug_reload_knobs()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_super_block_skipping_equals_plain_wavefront_every_sweep(seed):
+    """EIK_FSM_SB=0 (no super-block skipping) and the default agree sweep by
+    sweep: the change flag of every sweep and the field after K sweeps."""
+    rng = np.random.default_rng(100 + seed)
+    m, n = int(rng.integers(40, 700)), int(rng.integers(40, 300))
+    g = E.Grid(m, n, 0.01, 0.0, 0.0)
+    F = rng.uniform(0.2, 3.0, size=(n, m))
+    F[rng.random((n, m)) < 0.08] = 0.02
+    sp = lambda x, y, F=F, g=g: F[np.rint((y - g.y0) / g.h).astype(int),  # noqa: E731
+                                  np.rint((x - g.x0) / g.h).astype(int)]
+    nodes = [(int(rng.integers(0, m)), int(rng.integers(0, n))) for _ in range(3)]
+    p = E.build_problem(g, sp, E.ExitSpec.node_set(nodes))
+    from paper_1110_6220_b200.distributed import DeviceStripSweeper
+
+    def run(sb, K):
+        _knob("EIK_FSM_SB", sb)
+        try:
+            s = DeviceStripSweeper(p)
+            flags = s.plan.sweep(0, K)
+            out = np.zeros((n, m))
+            s.get_rows(0, n, out)
+            s.close()
+        finally:
+            _knob("EIK_FSM_SB", None)
+        return flags, out
+
+    for K in (40, 7, 13):
+        f1, u1 = run(None, K)
+        f0, u0 = run("0", K)
+        assert f1 == f0
+        assert bitwise(u1, u0)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_sweep_by_sweep_launches_carry_change_bits(seed):
+    """One launch per sweep with rows rewritten in between (the sharded path's
+    rounds): carrying the change bits across launches (default) equals
+    evaluating every node in every launch (EIK_FSM_CONT=0), flag by flag."""
+    rng = np.random.default_rng(200 + seed)
+    m, n = int(rng.integers(60, 500)), int(rng.integers(70, 260))
+    g = E.Grid(m, n, 0.01, 0.0, 0.0)
+    F = rng.uniform(0.3, 2.0, size=(n, m))
+    sp = lambda x, y, F=F, g=g: F[np.rint((y - g.y0) / g.h).astype(int),  # noqa: E731
+                                  np.rint((x - g.x0) / g.h).astype(int)]
+    # frozen first and last rows (a strip's ghost rows) plus one source
+    nodes = [(i, 0) for i in range(m)] + [(i, n - 1) for i in range(m)] + [(m // 3, n // 2)]
+    costs = [math.inf] * (2 * m) + [0.0]
+    from paper_1110_6220_b200.distributed import DeviceStripSweeper
+    p = E.build_problem(g, sp, E.ExitSpec.node_set(nodes, [5.0] * (2 * m) + [0.0]))
+    del costs
+    lo = rng.uniform(0.5, 3.0, size=m)
+    hi = rng.uniform(0.5, 3.0, size=m)
+
+    def run(cont):
+        _knob("EIK_FSM_CONT", cont)
+        try:
+            s = DeviceStripSweeper(p)
+            flags = []
+            for k in range(80):
+                flags.append(s.sweep(k))
+                if k == 3:   # the neighbours' edge rows arrive
+                    s.set_rows(0, 1, lo)
+                if k == 6:
+                    s.set_rows(n - 1, 1, hi)
+                if k == 9:   # ... and improve in a few columns only
+                    lo2 = lo.copy()
+                    lo2[m // 2: m // 2 + 5] *= 0.5
+                    s.set_rows(0, 1, lo2)
+            out = np.zeros((n, m))
+            s.get_rows(0, n, out)
+            s.close()
+        finally:
+            _knob("EIK_FSM_CONT", None)
+        return flags, out
+
+    f1, u1 = run(None)
+    f0, u0 = run("0")
+    assert f1 == f0
+    assert bitwise(u1, u0)
+    assert not f1[-1]  # converged: the comparison covers the whole solve
