@@ -233,7 +233,8 @@ def fsm_roof(methods, M, hbm, peak_kind):
             "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
             "algorithmic_bytes": 24.0 * M * f["sweeps"], "peak_kind": peak_kind,
             "note": "u + C (67 MB) stay in L2; the fp64 wavefront chain (m + n steps per "
-                    "direction turn) bounds it, not HBM"}
+                    "direction turn) bounds it, not HBM; clean super-blocks are passed "
+                    "over unstreamed (DESIGN 4(1))"}
 
 
 def _ncu_dram(path):
@@ -311,6 +312,10 @@ def measure_configs(hbm, peak_kind):
                 if key == "c5/fsm":
                     row["roofline"]["traffic"] = (_ncu_dram("r02_fsm_c5_metrics.csv") or
                                                   _ncu_dram("r01_fsm_c5_v4_metrics.csv"))
+                    row["roofline"]["note"] = (
+                        "algorithmic = 24 B per node per sweep (SURVEY 8(d)); the measured DRAM "
+                        "traffic is below it because super-blocks that cannot change are passed "
+                        "over unstreamed (DESIGN 4(1)); the bound is the sweep's dependency chain")
             out[key] = row
         del p, cfg
     return out
@@ -569,6 +574,8 @@ def main():
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "single_step_ms": single_step_ms,
             "roofline": roofline, "roofline_fsm_c2": fsm_roof(methods, M, hbm, peak_kind),
+            # the HBM-bound global sweep at its full size (config 5, 1.07e9 nodes)
+            "roofline_fsm_c5": ((per_config or {}).get("c5/fsm") or {}).get("roofline"),
             "configs": per_config, "c5_sharded": c5_sharded, "cpu_baseline": cpu,
             "gpu_launches": launches,
             "clocks": clk.summary(), "methods": methods,
