@@ -61,8 +61,8 @@ struct FsmArgs {
   int sb_wait_div;          // a strip waits for upwind tokens when it computed fewer than
                             // (m + 31) / sb_wait_div steps in its previous sweep (0: never)
 };
-constexpr int kFsmSbBlocks = 4;    // blocks of 8 steps per super-block (32 steps)
-constexpr int kFsmSbMaxPerRow = 2048;  // the kernel's shared-memory dirty map (k_fsm.cu kMapWords)
+constexpr int kFsmSbBlocks = 4;    // blocks of 8 steps per super-block (32 steps; 16 and 128 measured slower)
+constexpr int kFsmSbMaxPerRow = 4096;  // the kernel's shared-memory dirty map (k_fsm.cu kMapWords)
 inline int fsm_nsb(int64_t m) {
   const int64_t nblocks = (m + 31 + 7) / 8;
   return (int)((nblocks + kFsmSbBlocks - 1) / kFsmSbBlocks);

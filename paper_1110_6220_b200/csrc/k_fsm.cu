@@ -94,8 +94,10 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const void* p) {
 // decision only selects between two schedules with the same result.
 constexpr int kSB = kFsmSbBlocks;
 constexpr int kSbCols = kSB * kU;
-constexpr int kSbShift = kSbCols == 32 ? 5 : (kSbCols == 64 ? 6 : (kSbCols == 128 ? 7 : 8));
-static_assert((1 << kSbShift) == kSbCols && kSbCols >= 32, "super-block: 32..256 steps, power of two");
+constexpr int kSbShift = kSbCols == 16 ? 4 : (kSbCols == 32 ? 5 : (kSbCols == 64 ? 6 : (kSbCols == 128 ? 7 : 8)));
+static_assert((1 << kSbShift) == kSbCols && kSbCols >= 16, "super-block: 16..256 steps, power of two");
+// the upwind super-block whose lane 31 visits the column lane 0 visits first in super-block g is g + kTokOff
+constexpr int kTokOff = 31 >> kSbShift;
 
 struct SbCtx {
   bool pub;                // summaries and tokens are kept (a.sb != null)
@@ -195,7 +197,7 @@ __device__ __forceinline__ void lsm_masks(const ChgWin& w, bool iasc_prev, bool 
 // previous sweep around super-block g (the strip's rows and the adjoining edge
 // rows, one column wider on each side), i.e. the super-block is not locally
 // clean.  prevw: scratch for the previous sweep's bits in its own order.
-constexpr int kMapWords = 64;  // super-blocks per row <= 2048 (host: larger grids keep sb off)
+constexpr int kMapWords = kFsmSbMaxPerRow / 32;  // (host: longer rows keep sb off)
 template <bool IASC>
 __device__ __forceinline__ void sb_build_map(const FsmArgs& a, const SbCtx& sb, int lane,
                                              unsigned* prevw, unsigned* curw) {
@@ -385,8 +387,10 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
     if (rmax > 30) rmax = 30;
     int r = rmax;
     if (ch.in_glob) {
-      const unsigned* tp = sb_tok(a, sb.flow, sb.flow ? sb.b + 1 : sb.b - 1) + g + lane;
-      const bool mine = lane <= rmax && g + lane < nsb;
+      // lane 0's columns of super-blocks g .. g+r-1 are visited by the upwind
+      // lane 31 in its super-blocks g + kTokOff .. g + kTokOff + r
+      const unsigned* tp = sb_tok(a, sb.flow, sb.flow ? sb.b + 1 : sb.b - 1) + g + kTokOff + lane;
+      const bool mine = lane <= rmax && g + kTokOff + lane < nsb;
       unsigned tk = mine ? ld_relaxed_u32(tp) : (stamp | 2u);
       if (sb.block && lane < 2 && mine) {
         long long spins = 0;
@@ -399,7 +403,6 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
           tk = ld_relaxed_u32(tp);
         }
       }
-      // tokens g .. g+r let the strip pass r super-blocks
       const unsigned bad = __ballot_sync(kFull, tk != (stamp | 2u));
       const int lead = bad ? __ffs(bad) - 1 : 32;
       if (lead - 1 < r) r = lead - 1;
@@ -407,13 +410,14 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
     }
     int nb = kSB * r;
     if (nb > nblocks - blk) nb = nblocks - blk;
+    const int ncol = kSbCols * r;  // steps (columns per lane) of the run
     if (ch.in_glob) {
       // re-arm the upwind slots of lane 0's columns (their values have landed:
       // the tokens are written after them)
       double* gin_q0 = (double*)__shfl_sync(kFull, (unsigned long long)ph, 0);
       const int64_t q0_0 = (int64_t)q0 + lane;
-      for (int j = 0; j < r; ++j) {
-        const int64_t q = (int64_t)g * kSbCols + lane + 32 * j;
+      for (int j = lane; j < ncol; j += 32) {
+        const int64_t q = (int64_t)g * kSbCols + j;
         if (q < m) __stcg(gin_q0 + S * (q - q0_0), sent);
       }
     }
@@ -422,18 +426,20 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       const int64_t q0_31 = (int64_t)q0 + lane - 31;
       const double* edge_q0 = (const double*)__shfl_sync(kFull, (unsigned long long)pu, 31);
       double* gout_q0 = (double*)__shfl_sync(kFull, (unsigned long long)po, 31);
-      const int64_t qe0 = (int64_t)g * kSbCols - 31 + lane;
-      for (int j0 = 0; j0 < r; j0 += 8) {
+      const int64_t qe0 = (int64_t)g * kSbCols - 31;
+      for (int j0 = lane; j0 < ncol; j0 += 8 * 32) {
         double ev[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int64_t q = qe0 + 32 * (j0 + j);
-          ev[j] = (j0 + j < r && q >= 0 && q < m) ? __ldcg(edge_q0 + S * (q - q0_31)) : 0.0;
+          const int jj = j0 + 32 * j;
+          const int64_t q = qe0 + jj;
+          ev[j] = (jj < ncol && q >= 0 && q < m) ? __ldcg(edge_q0 + S * (q - q0_31)) : 0.0;
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int64_t q = qe0 + 32 * (j0 + j);
-          if (j0 + j < r && q >= 0 && q < m) __stcg(gout_q0 + S * (q - q0_31), ev[j]);
+          const int jj = j0 + 32 * j;
+          const int64_t q = qe0 + jj;
+          if (jj < ncol && q >= 0 && q < m) __stcg(gout_q0 + S * (q - q0_31), ev[j]);
         }
       }
       __threadfence();  // the values before the tokens
@@ -441,11 +447,20 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
       if (lane < r) __stcg(sb_tok(a, sb.flow, sb.b) + g + lane, stamp | 2u);
     }
     if (lane < r) __stcg(sb_sum(a, sb.par, sb.b) + g + lane, 0u);
-    // zero change bits over the lane's 32 r columns: the open word (acc), then
-    // whole words; the next column to visit opens an empty word
-    for (int i = 0; i < r; ++i) __stcg(wrow + (IASC ? wcur + i : wcur - i), i == 0 ? acc : 0u);
-    acc = 0u;
-    wcur += IASC ? r : -r;
+    // zero change bits over the lane's ncol columns: the open word (acc) and
+    // the whole words the run passes; the word of the next column to visit
+    // stays open
+    {
+      const int64_t lo = lo_of(blk);
+      const int64_t wn = (IASC ? lo + ncol : lo + kU - 1 - ncol) >> 5;
+      if (wn != wcur) {
+        __stcg(wrow + wcur, acc);
+        acc = 0u;
+        if (IASC) for (int64_t w = wcur + 1; w < wn; ++w) __stcg(wrow + w, 0u);
+        else for (int64_t w = wcur - 1; w > wn; --w) __stcg(wrow + w, 0u);
+        wcur = wn;
+      }
+    }
     pu += S * kU * nb;
     pc += S * kU * nb;
     ph += S * kU * nb;
