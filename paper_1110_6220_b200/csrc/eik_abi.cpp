@@ -565,7 +565,7 @@ int plan_run_fsm(eik_plan* P, eik_output* out) {
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
   if (st[0] != 0) P->last_sweeps_bound = P->max_sweeps;  // flags of a failed run: clear all
-  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite, and h / F within [2^-480, 2^500], at every node");
   if (st[0] == 3) return fail(EIK_ERR_BUDGET, "fsm exceeded the device sweep budget");
   if (st[0] == 4) return fail(EIK_ERR_CUDA, "fsm wavefront watchdog fired (scheduling bug)");
   P->last_sweeps_bound = std::min<int64_t>(P->max_sweeps, (int64_t)st[1] + 8);
@@ -679,7 +679,7 @@ int plan_prepare(eik_plan* P) {
   CK(stream_wait(P->stream));  // no spinning core while the solve runs
   CK(cudaMemcpyAsync(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost, P->stream));
   CK(stream_wait(P->stream));
-  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite, and h / F within [2^-480, 2^500], at every node");
   return EIK_OK;
 }
 

@@ -428,7 +428,7 @@ int plan_run_fmsm(eik_plan* P, eik_output* out) {
   CK(stream_wait(P->stream));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
-  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite, and h / F within [2^-480, 2^500], at every node");
   if (st[0] == 3) return fail(EIK_ERR_BUDGET, "fmsm: in-cell sweep budget exceeded");
   if (st[0] == 4) return fail(EIK_ERR_CUDA, "fmsm dataflow watchdog fired (scheduling bug)");
   // counters: sweeps are fine-pass cell sweeps; removals/updates include the
@@ -497,7 +497,7 @@ int plan_run_heapcell_serial(eik_plan* P, eik_output* out, const std::vector<int
   CK(stream_wait(P->stream));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
-  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite, and h / F within [2^-480, 2^500], at every node");
   if (st[0] == 3) return fail(EIK_ERR_BUDGET, "heap-cell removal budget exceeded");
   out->heap_removals = (int64_t)cnt[0];
   out->sweeps = (int64_t)cnt[1];
@@ -589,7 +589,7 @@ int plan_run_hcm_band(eik_plan* P, eik_output* out, const std::vector<int>& icel
   CK(stream_wait(P->stream));
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
-  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite, and h / F within [2^-480, 2^500], at every node");
   if (st[0] == 3) return fail(EIK_ERR_BUDGET, "heap-cell removal budget exceeded");
   if (st[0] == kStatusWatchdogHost)
     return fail(EIK_ERR_CUDA, "hcm band scheduler made no progress (scheduling bug)");
@@ -767,7 +767,7 @@ retry:  // after a committer heap overflow, with the heap in global memory
   }
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
-  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite, and h / F within [2^-480, 2^500], at every node");
   if (st[0] == 3) return fail(EIK_ERR_BUDGET, "heap-cell removal budget exceeded");
   if (st[0] == 4 || st[0] == 5) {
     std::fprintf(stderr,
@@ -900,7 +900,7 @@ int plan_fmsm_counters(eik_plan* P, int64_t out[2]) {
   unsigned long long cnt[2];
   CK(cudaMemcpy(st, P->dStatus, sizeof(st), cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(cnt, P->dCounters, sizeof(cnt), cudaMemcpyDeviceToHost));
-  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite at every node");
+  if (st[0] == 1) return fail(EIK_ERR_DOMAIN, "speed must be positive and finite, and h / F within [2^-480, 2^500], at every node");
   if (st[0] == 3) return fail(EIK_ERR_BUDGET, "fmsm: in-cell sweep budget exceeded");
   out[0] = (int64_t)cnt[0];
   out[1] = (int64_t)cnt[1];

@@ -563,7 +563,7 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
           if (lane == 0) sv = hval;
           if (lane == 31) nv = hval;
           const double c = cc[t];
-          const double cand = node_update4(cu[t + 1], res_prev, nv, sv, c);
+          const double cand = node_update4_fast(cu[t + 1], res_prev, nv, sv, c);
           upd = (c > 0.0) && (cand < cur);  // exits / padding carry c = -1
           if (LSM) {
             // lane t-1's step at this column (its previous step) lowered it
@@ -883,6 +883,9 @@ __global__ void prepare_padded_kernel(const double* __restrict__ F, double* __re
       const double f = F[r * m + i];
       if (!(f > 0.0) || !(f < kInf)) atomicExch(&status[0], 1);
       c = h / f;  // same IEEE division as local_update.hpp:33
+      // the update's square root runs without sqrt()'s out-of-range path
+      // (k_common.cuh sqrt_rn_normal): 2 c^2 must stay in [2^-970, 2^1024)
+      if (!(c >= 0x1p-480) || !(c <= 0x1p500)) atomicExch(&status[0], 1);
     }
     C[idx - P] = c;
     u[idx - P] = kInf;

@@ -144,6 +144,22 @@ def test_bad_speed_is_rejected():
         E.fsm_solve(p)
 
 
+def test_cost_outside_the_square_roots_domain_is_rejected():
+    """h / F beyond [2^-480, 2^500] is refused loudly (the wavefront's
+    straight-line square root has no out-of-range path), not solved wrongly."""
+    g = E.Grid.unit_square(9)
+    for f in (1e150, 1e-152):
+        p = E.build_problem(g, lambda x, y, f=f: np.full_like(x, f), E.ExitSpec.point_source((0.5, 0.5)))
+        with pytest.raises(ValueError):
+            E.fsm_solve(p)
+    # well inside the domain, far from 1: still the reference's bits
+    for f in (1e100, 1e-100):
+        p = E.build_problem(g, lambda x, y, f=f: np.full_like(x, f), E.ExitSpec.point_source((0.5, 0.5)))
+        a = E.fsm_solve(p)
+        b = O.oracle_solve(p, "fsm")
+        assert bitwise(a.values, b.u)
+
+
 def test_set_device_selects_and_rejects():
     """eik_set_device: the library's own CUDA runtime follows the caller's
     device choice (one process per GPU); an absent device is a ConfigError."""
