@@ -177,6 +177,8 @@ __global__ void floor_kernel(int steps, int reps, long long* out, double* sink) 
       double cand;
       if (VAR == 0) {
         cand = node_update4(e, wv, n, sv, c);
+      } else if (VAR == 3) {  // the FSM wavefront's update (straight-line sqrt)
+        cand = node_update4_fast(e, wv, n, sv, c);
       } else if (VAR == 1) {
         const double ua = dmin(e, wv), ub = dmin(n, sv);
         const double diff = ua - ub;
@@ -255,8 +257,12 @@ int main(int argc, char** argv) {
   cudaMemcpy(&c[1], d, 8, cudaMemcpyDeviceToHost);
   floor_kernel<2><<<1, 32>>>(steps, reps, d, s);
   cudaMemcpy(&c[2], d, 8, cudaMemcpyDeviceToHost);
-  printf("floor cycles/step: shfl+update+select %.0f, without sqrt %.0f, shfl+select %.0f\n",
-         c[0] / (double)(steps * reps), c[1] / (double)(steps * reps),
+  long long c3 = 0;
+  floor_kernel<3><<<1, 32>>>(steps, reps, d, s);
+  cudaMemcpy(&c3, d, 8, cudaMemcpyDeviceToHost);
+  printf("floor cycles/step: shfl+update+select %.0f (straight-line sqrt: %.0f), without sqrt %.0f, "
+         "shfl+select %.0f\n",
+         c[0] / (double)(steps * reps), c3 / (double)(steps * reps), c[1] / (double)(steps * reps),
          c[2] / (double)(steps * reps));
   for (int w : {8, 16, 32}) {
     const int h = w, pu = (w + 3) & ~1;
