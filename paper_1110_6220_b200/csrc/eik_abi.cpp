@@ -61,6 +61,7 @@ Knobs read_knobs() {
   k.hc_global_heap = gb("EIK_HC_GLOBAL_HEAP");
   k.hc_heap_cap = gi("EIK_HC_HEAP_CAP", 0);
   k.hc_chain = gi("EIK_HC_CHAIN", 1);
+  k.hc_bands = gi("EIK_HC_BANDS", 1);
   k.tile_tma = gi("EIK_TILE_TMA", gi("EIK_FMSM_TMA", 1));
   k.hc_ctas = gi("EIK_HC_CTAS", 0);
   k.hc_debug = gb("EIK_HC_DEBUG");

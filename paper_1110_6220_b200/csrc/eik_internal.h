@@ -159,6 +159,7 @@ struct HcArgs {
   double* ckey;             // [J] heap key published for the workers (inf = not queued)
   unsigned* ctag;           // [J] instance number of the last committed result
   int chain;                // make chained speculations
+  int bands;                // cells of 33-128 rows swept as 32-row bands (k_cellsweep.cuh)
   int idle_ns;              // worker back-off when it found nothing to do
   int prof;                 // run the instrumented kernel (EIK_HC_PROFILE)
   int* wdbg;                // optional debug: [workers][4] phase, cell, kind, time

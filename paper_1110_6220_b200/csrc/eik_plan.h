@@ -157,6 +157,7 @@ struct Knobs {
   bool hc_global_heap = false;     // EIK_HC_GLOBAL_HEAP
   int hc_heap_cap = 0;             // EIK_HC_HEAP_CAP (0 = fit)
   int hc_chain = 1;                // EIK_HC_CHAIN
+  int hc_bands = 1;                // EIK_HC_BANDS=0: tall cells with several rows per lane
   int tile_tma = 1;                // EIK_TILE_TMA=0: stage cell tiles by loads, not TMA
   int hc_ctas = 0;                 // EIK_HC_CTAS (0 = device)
   bool hc_debug = false;           // EIK_HC_DEBUG: per-worker phase trace

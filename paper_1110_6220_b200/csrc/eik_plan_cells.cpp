@@ -715,6 +715,7 @@ retry:  // after a committer heap overflow, with the heap in global memory
   }
   a.ctag = P->dCTag;
   a.chain = P->hc_chain;
+  a.bands = knobs().hc_bands;
   a.prof = kn.hc_profile ? 1 : 0;
   a.idle_ns = kn.hc_idle_ns;
   a.done_flag = P->dHcMisc;

@@ -687,7 +687,13 @@ __device__ __forceinline__ void process_cell(const HcArgs& a, HTile& T, double* 
     for (;;) {
       if (a.fast ? nsw >= nflag : !changed) break;
       const int dir = nsw < 4 ? perm[nsw] : kRotation[nsw % 4];
-      changed = cell_sweep<2>(ct, dir, lane, upd, /*skip=*/!a.fast && nsw >= a.skip_from);
+      // cells taller than 32 rows as 32-row bands (a.bands, EIK_HC_BANDS=0:
+      // several rows per lane).  The multi-slot variants stay compiled in on
+      // purpose: without them ptxas allocates 139 registers instead of 255
+      // and the 8-32-node cells get 6-9 % slower (FHCM/8 165 -> 176 ms).
+      const bool skip = !a.fast && nsw >= a.skip_from;
+      changed = (ct.h <= 32 || !a.bands) ? cell_sweep<2>(ct, dir, lane, upd, skip)
+                                         : cell_sweep_lock_bands(ct, dir, lane, upd, skip);
       ++nsw;
     }
   }
@@ -1663,7 +1669,7 @@ __device__ void band_process(const HcArgs& a, HTile& T, double* before, SpecRec*
     bool changed = true;
     while (changed) {
       const int dir = nsw < 4 ? perm[nsw] : kRotation[nsw % 4];
-      changed = cell_sweep<2>(ct, dir, lane, upd, /*skip=*/nsw >= a.skip_from);
+      changed = cell_sweep_lock_bands(ct, dir, lane, upd, /*skip=*/nsw >= a.skip_from);
       ++nsw;
     }
   }
