@@ -778,20 +778,24 @@ int plan_rows(eik_plan* P, int64_t row0, int64_t nrows, double* host_or_dev, int
     // between sweep launches: mark what the new rows change (k_fsm.cu)
     double* stage = nullptr;
     const double* src = host_or_dev;
+    cudaError_t e = cudaSuccess;
     if (!on_device) {
       CK(pool_alloc((void**)&stage, w * nrows));
-      CK(cudaMemcpyAsync(stage, host_or_dev, w * nrows, cudaMemcpyHostToDevice, P->stream));
+      e = cudaMemcpyAsync(stage, host_or_dev, w * nrows, cudaMemcpyHostToDevice, P->stream);
       src = stage;
     }
-    CK(launch_set_rows_marked(P->dU, src, row0, nrows, P->g.m, P->pitch, kPad,
-                              P->dChg + (int64_t)P->chg_last_par * (P->g.n + 3) * P->chg_cw,
-                              P->chg_cw,
-                              P->dSb + (int64_t)P->chg_last_par * P->nstrips * P->nsb, P->nsb,
-                              P->stream));
-    if (stage) {
-      CK(stream_wait(P->stream));
+    if (e == cudaSuccess)
+      e = launch_set_rows_marked(P->dU, src, row0, nrows, P->g.m, P->pitch, kPad,
+                                 P->dChg + (int64_t)P->chg_last_par * (P->g.n + 3) * P->chg_cw,
+                                 P->chg_cw,
+                                 P->dSb + (int64_t)P->chg_last_par * P->nstrips * P->nsb, P->nsb,
+                                 P->stream);
+    if (stage) {  // the staging buffer goes back whatever happened
+      const cudaError_t es = cudaStreamSynchronize(P->stream);
       pool_release(stage);
+      if (e == cudaSuccess) e = es;
     }
+    CK(e);
   } else if (to_plan)
     CK(cudaMemcpy2DAsync(dev, dp, host_or_dev, w, w, nrows,
                          on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, P->stream));
