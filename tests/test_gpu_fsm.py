@@ -259,3 +259,28 @@ def test_sweep_by_sweep_launches_carry_change_bits(seed):
     assert f1 == f0
     assert bitwise(u1, u0)
     assert not f1[-1]  # converged: the comparison covers the whole solve
+
+
+def test_rows_longer_than_the_dirty_map_keep_the_plain_wavefront():
+    """Rows beyond 131 k columns do not fit the kernel's shared-memory dirty
+    map: super-block skipping is off and the result is still the reference's."""
+    m, n = 140001, 37
+    g = E.Grid(m, n, 1e-3, 0.0, 0.0)
+    p = E.build_problem(g, lambda x, y: 1.0 + 0.5 * np.sin(40 * x) * np.cos(3 * y),
+                        E.ExitSpec.node_set([(70000, 18), (5, 3)], [0.0, 0.25]))
+    a = E.fsm_solve(p)
+    b = O.oracle_solve(p, "fsm")
+    assert bitwise(a.values, b.u)
+    assert (a.sweeps, a.node_updates) == (b.sweeps, b.node_updates)
+
+
+def test_wide_grid_with_skipping_is_bitwise():
+    """A long thin grid (many super-blocks per strip, two strips)."""
+    m, n = 20011, 50
+    g = E.Grid(m, n, 1e-3, 0.0, 0.0)
+    p = E.build_problem(g, lambda x, y: 1.0 + 0.7 * np.sin(25 * x) * np.sin(31 * y),
+                        E.ExitSpec.node_set([(10, 10), (15000, 40)]))
+    a = E.fsm_solve(p)
+    b = O.oracle_solve(p, "fsm")
+    assert bitwise(a.values, b.u)
+    assert (a.sweeps, a.node_updates) == (b.sweeps, b.node_updates)
