@@ -400,6 +400,7 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
             break;
           }
           if ((spins & 1023) == 0 && *(volatile int*)a.status == kStatusWatchdog) break;
+          __nanosleep(40);
           tk = ld_relaxed_u32(tp);
         }
       }
