@@ -73,3 +73,27 @@ def test_c2_128_node_cells(method):
     column, too large for a shared-memory tile."""
     p = configs.config2().problem
     _check(p, method, E.build_cells(p.grid, 16, 16))
+
+
+@pytest.mark.parametrize("h", [33, 40, 47, 63, 64, 65, 95, 96, 97, 127, 128])
+def test_cells_of_33_to_128_rows_as_bands(h):
+    """Cells of 33-128 rows go through the locked engine band by band (32 rows
+    each, k_cellsweep.cuh cell_sweep_lock_bands) in the replay and the HCM band
+    kernel: every height class, with a shorter last band and a remainder cell
+    row, against the C restatement -- values and every counter (exact replay),
+    and <= 1e-10 for the band scheduler."""
+    rng = np.random.default_rng(1000 + h)
+    m, n = 3 * 37 + 5, 3 * h + 7  # cells_y = 3: two cells of h rows, the last h + 7
+    g = E.Grid(m, n, 0.003, -0.1, 0.2)
+    F = rng.uniform(0.3, 2.5, size=(n, m))
+    F[rng.random((n, m)) < 0.05] = 0.05
+    sp = lambda x, y, F=F, g=g: F[np.clip(np.rint((y - g.y0) / g.h).astype(int), 0, g.n - 1),  # noqa: E731
+                                  np.clip(np.rint((x - g.x0) / g.h).astype(int), 0, g.m - 1)]
+    ex = E.ExitSpec.node_set([(int(rng.integers(0, m)), int(rng.integers(0, n))) for _ in range(3)],
+                             list(rng.uniform(0, 0.05, size=3)))
+    p = E.build_problem(g, sp, ex)
+    cells = E.build_cells(g, 3, 3)
+    for method in ("hcm", "fhcm"):
+        _check(p, method, cells)
+    band = E.solve(p, "hcm", cells)
+    assert float(np.max(np.abs(band.values - O.oracle_solve(p, "hcm", cells).u))) <= 1e-10
