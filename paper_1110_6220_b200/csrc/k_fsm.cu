@@ -570,18 +570,18 @@ __device__ __forceinline__ bool sweep_strip(const FsmArgs& a, int lane, int64_t 
             // lane t-1's step at this column (its previous step) lowered it
             const unsigned bal = __ballot_sync(kFull, upd_prev);
             const bool row_up_upd = lane == 0 ? h_chg : ((bal >> (lane - 1)) & 1u);
-            bool unl;
-            if (dprev < 0) {
-              unl = fmin(fmin(cu[t + 1], res_prev), fmin(nv, sv)) < kInf;
-            } else {
-              // the changed neighbour's current value: the column one is
-              // downwind now iff the column direction did not turn (old value
-              // cu[t+1]) else upwind (new value res_prev); rows alike (nv / sv)
-              const double vpc = (iasc_prev == IASC) ? cu[t + 1] : res_prev;
-              const double vpr = (jasc_prev == jasc) ? nv : sv;
-              unl = (((lmc >> t) & 1u) && vpc < cur) || (((lmr >> t) & 1u) && vpr < cur) ||
-                    (upd_prev && res_prev < cur) || (row_up_upd && sv < cur);
-            }
+            // (both rules evaluated and selected: a branch here would split
+            // the block's eight steps into separate scheduling regions)
+            const bool unl0 = (cu[t + 1] < kInf) | (res_prev < kInf) | (nv < kInf) | (sv < kInf);
+            // the changed neighbour's current value: the column one is
+            // downwind now iff the column direction did not turn (old value
+            // cu[t+1]) else upwind (new value res_prev); rows alike (nv / sv)
+            const double vpc = (iasc_prev == IASC) ? cu[t + 1] : res_prev;
+            const double vpr = (jasc_prev == jasc) ? nv : sv;
+            const bool unl1 = ((((lmc >> t) & 1u) != 0u) & (vpc < cur)) |
+                              ((((lmr >> t) & 1u) != 0u) & (vpr < cur)) |
+                              (upd_prev & (res_prev < cur)) | (row_up_upd & (sv < cur));
+            const bool unl = dprev < 0 ? unl0 : unl1;
             lcnt += (unl && c > 0.0) ? 1ull : 0ull;
           }
           if (upd) {
